@@ -1,0 +1,200 @@
+/*
+ * meshlayers_b200.h -- C ABI of libmeshlayers_b200.so, the B200 (sm_100a) kernel backend that
+ * fills the reference's compiled-backend slot `meshlayers._native`
+ * (reference: pkg/setup.py:5-13 declares it; pkg/src/meshlayers/_kernels_numpy.py:3-5 makes the
+ * numpy module its semantic twin).  Citations "KN:n" = _kernels_numpy.py line n, "SPEC:n" =
+ * SPEC.md line n.
+ *
+ * Conventions
+ *   - Every pointer named *_dev / plane / tri_* is a DEVICE pointer unless the function name ends
+ *     in _host.  No ownership is transferred; planes are mutated in place (KN:96-99, 128-130,
+ *     200-202).  Planes are row-major [row = y][col = x], y-up, texel centre = index + 0.5
+ *     (KN:15, 60, 63).
+ *   - `stream` is a cudaStream_t passed as void*; all work is stream-ordered, nothing synchronises
+ *     the host.  Counts are written to device memory (uint64_t*), never returned by value, so a
+ *     caller can batch strokes without a round trip; the *_host wrappers synchronise and return
+ *     host values like the reference functions do.
+ *   - Row slabs: functions taking (row0, rows) operate on rows [row0, row0+rows) of a
+ *     `height`-row atlas and address planes SLAB-LOCALLY (texel (x, y) at (y-row0)*width + x).
+ *     This is the multi-GPU row sharding (SPEC:150 licenses row-parallel rasterisation).
+ *   - Return value: ML_OK or an ML_ERR_* code; ml_last_error() gives the message
+ *     (thread-local).  The reference kernels raise nothing (KN: no validation); argument errors
+ *     here correspond to TargetMismatch one layer up (errors.py:32).
+ *   - tri_dtype: triangle inputs may be float32 or float64; they are widened to float64 per
+ *     triangle exactly like KN:88, 113-114, 151-152.
+ */
+#ifndef MESHLAYERS_B200_H
+#define MESHLAYERS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ML_OK = 0, ML_ERR_ARG = 1, ML_ERR_CUDA = 2, ML_ERR_NO_DEVICE = 3 };
+enum { ML_F32 = 0, ML_F64 = 1 };
+/* plane element kinds */
+enum { ML_U8 = 0, ML_I8 = 1, ML_I16 = 2, ML_I32 = 3, ML_U32 = 4, ML_F16 = 5, ML_FLOAT32 = 6 };
+/* layer algebra operators (no reference code; frozen in oracle/kn_port.c ext_layer_op) */
+enum { ML_OP_UNION = 0, ML_OP_INTERSECTION = 1, ML_OP_DIFFERENCE = 2, ML_OP_MASKING = 3 };
+
+int ml_version(void);
+const char* ml_last_error(void);
+/* number of SMs of the current device (148 on B200); <= 0 when no device is usable */
+int ml_sm_count(void);
+
+/* Scratch needed by every ml_raster_* / ml_coverage_fill call with `ntri` triangles. */
+size_t ml_raster_workspace_bytes(int64_t ntri);
+
+/* ---- KN:84-100  coverage_fill(tri_xy, width, height, out) -> written -------------------------
+ * tri_xy [ntri][3][2] grid units.  out: uint8/bool slab.  *written (device, must be zeroed by
+ * the caller) += number of texels that went 0 -> 1. */
+int ml_coverage_fill(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
+                     int64_t row0, int64_t rows, uint8_t* out, uint64_t* written,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- KN:103-132  raster_depth(tri_xy, tri_zn, depth) -----------------------------------------
+ * tri_xy window pixels, tri_zn [ntri][3] NDC z, depth float32 [height][width] updated in place
+ * to min(depth, float32(d)) == the reference's serial result for any triangle order.  The
+ * reference's returned update count depends on triangle order and is not reproduced. */
+int ml_raster_depth(const void* tri_xy, const void* tri_zn, int tri_dtype, int64_t ntri,
+                    float* depth, int64_t width, int64_t height,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- KN:135-203  raster_tea(...) -> (edited, fragments) --------------------------------------
+ * Scalar stroke parameters of KN:135-136.  eps_f32 != 0 reproduces numpy's float32 sum
+ * depth[py,px] + eps when eps is a Python float (KN:185 under NEP-50); 0 = float64 sum. */
+typedef struct ml_tea_params {
+    double ww, wh;                 /* window size, KN:179-181 */
+    double eps;                    /* depth bias */
+    double sfx, sfy, bx, by;       /* tool map s = sfx*xn + bx, t = sfy*yn + by, KN:187-188 */
+    const float* depth;            /* device, [depth_h][depth_w] */
+    const uint8_t* shape;          /* device, [shape_h][shape_w], non-zero = inside tool */
+    int64_t depth_w, depth_h, shape_w, shape_h;
+    int32_t eps_f32;
+    int32_t reserved;
+} ml_tea_params;
+
+/* Direct per-triangle TEA: exact for ANY uv layout (overlapping islands included).
+ * data: slab of `esize`-byte elements (1, 2, 4); value_bits: the value already cast to the plane
+ * kind, little-endian in the low bytes.  counters (device, zeroed by caller): [0] += texels whose
+ * edited flag went 0 -> 1, [1] += fragments offered (KN:203). */
+int ml_raster_tea(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
+                  int64_t width, int64_t height, int64_t row0, int64_t rows,
+                  const ml_tea_params* params, void* data, int esize, uint32_t value_bits,
+                  uint8_t* mask, uint8_t* edited, uint64_t* counters,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- surface map (north star (1); definition: oracle/kn_port.c ext_surface_map) ---------------
+ * Pass 1: tri_id[y][x] = largest index of a triangle covering the texel centre, -1 if none.
+ * counters (device, zeroed): [0] += fragments, [1] += overlap events (= fragments - covered). */
+int ml_raster_tri_id(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
+                     int64_t row0, int64_t rows, int32_t* tri_id, uint64_t* counters,
+                     void* workspace, size_t workspace_bytes, void* stream);
+/* Pass 2: per texel, interpolate the owner triangle's attributes.  pos / nrm are three float32
+ * planes each (plane stride = rows*width elements), area one float32 plane.  Uncovered texels:
+ * pos = NaN, nrm = 0, area = 0.  tri_pos / tri_nrm [ntri][3][3].  *covered (device, zeroed)
+ * += covered texels. */
+int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_nrm, int tri_dtype,
+                       int64_t ntri, int64_t width, int64_t row0, int64_t rows,
+                       const int32_t* tri_id, float* pos, float* nrm, float* area,
+                       uint64_t* covered, void* stream);
+
+/* ---- TEA over the cached triangle-id map (SURVEY.md 8 note N1) ---------------------------------
+ * Bit-identical to ml_raster_tea when no two triangles overlap in uv space (overlap events == 0):
+ * each covered texel re-evaluates KN:72-74 and KN:166-193 for its owner triangle.
+ * counters: [0] += newly edited texels, [1] += covered texels (== fragments). */
+int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
+                  int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
+                  const ml_tea_params* params, void* data, int esize, uint32_t value_bits,
+                  uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream);
+
+/* ---- selection brushes (north star (2); definitions: ext_select_sphere / ext_select_threshold) -
+ * Sphere brush over n texels of a position map (three float32 planes, stride pos_stride):
+ * hit = ((px-cx)^2 + (py-cy)^2) + (pz-cz)^2 <= r*r in float64; hits get data = value, mask = 1,
+ * edited = 1.  *count (device, zeroed) += texels whose edited flag went 0 -> 1. */
+int ml_select_sphere(const float* pos, int64_t pos_stride, int64_t n,
+                     double cx, double cy, double cz, double radius,
+                     void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
+                     uint64_t* count, void* stream);
+
+/* K strokes in one pass over the position map.  Stroke k = (cx, cy, cz, r) writes value_bits[k]
+ * into layer layer_of[k]; strokes are applied in index order (a later stroke overwrites an earlier
+ * one on the same layer).  All arrays below are DEVICE arrays: strokes [K][4] f64, layer_of [K]
+ * i32, value_bits [K] u32, data/mask/edited [L] plane pointers, counts [L] u64 (zeroed). */
+int ml_select_sphere_batch(const float* pos, int64_t pos_stride, int64_t n,
+                           const double* strokes, const int32_t* layer_of,
+                           const uint32_t* value_bits, int64_t K,
+                           void* const* data, uint8_t* const* mask, uint8_t* const* edited,
+                           int64_t L, int esize, uint64_t* counts, void* stream);
+
+/* Attribute threshold: hit = (valid == NULL || valid[i] != 0) && lo <= attr[i] <= hi (closed,
+ * float64 compare of the widened attribute; attr_kind is an ML_* plane kind). */
+int ml_select_threshold(const void* attr, int attr_kind, const uint8_t* valid, int64_t n,
+                        double lo, double hi, void* data, int esize, uint32_t value_bits,
+                        uint8_t* mask, uint8_t* edited, uint64_t* count, void* stream);
+
+/* ---- layer algebra (north star (3); definition: ext_layer_op) ---------------------------------
+ * (dc, mc) = (da, ma) op (db, mb) over n texels; mask bytes are true iff non-zero, output mask
+ * bytes are exactly 0/1.  Data planes may all be NULL (esize 0, mask-only algebra: 3 B/texel).
+ * Outputs may alias the A operand. */
+int ml_layer_op(int op, const void* da, const uint8_t* ma, const void* db, const uint8_t* mb,
+                void* dc, uint8_t* mc, int esize, int64_t n, void* stream);
+
+/* Fused left-to-right chain  ((L0 op1 L1) op2 L2) ... op_{N-1} L_{N-1}  in one pass:
+ * reads N layers, writes 1.  HOST arrays of N device pointers / N ops (ops[0] ignored), N <= 16. */
+int ml_layer_chain(int64_t nlayers, const void* const* data, const uint8_t* const* mask,
+                   const int32_t* ops, void* dc, uint8_t* mc, int esize, int64_t n, void* stream);
+
+/* ---- per-layer area / statistics (north star (4); definitions: ext_layer_area ...) ------------
+ * sums[l] (device f64, zeroed) += sum of area[i] over texels with masks[l][i] != 0, accumulated in
+ * float64; counts[l] (device u64, zeroed, may be NULL) += number of such texels.  `masks` is a
+ * HOST array of L device pointers (L <= 64): one pass reads area once and the L masks. */
+int ml_layer_area(const float* area, const uint8_t* const* masks, int64_t L, int64_t n,
+                  double* sums, uint64_t* counts, void* stream);
+/* uint8 label plane: sums[v] += area over texels with mask != 0 and data == v (v < 256). */
+int ml_label_area(const float* area, const uint8_t* data, const uint8_t* mask, int64_t n,
+                  double* sums /* [256] */, uint64_t* counts /* [256] */, void* stream);
+/* out (device, 4 doubles): count, sum, min, max of the widened attribute over mask != 0.
+ * out must be initialised to {0, 0, +inf, -inf}. */
+int ml_layer_stats(const void* attr, int attr_kind, const uint8_t* mask, int64_t n,
+                   double* out, void* stream);
+
+/* ---- TPA: outline mask and padding ----------------------------------------------
+ * Row-sharded stencils: the INPUT plane (cov resp. edited) is a full-width slab of global rows
+ * [in_row0, in_row0+in_rows) which must contain the halo rows the rank can see; rows outside it
+ * count as empty (no coverage / nothing edited).  OUTPUT planes (outline, data, mask) are slabs
+ * of rows [out_row0, out_row0+out_rows), a sub-range of the input rows.
+ * outline[y][x] = 1 iff cov[y][x] == 0 and some cov != 0 within Chebyshev distance <= thickness,
+ * else 0. */
+int ml_outline_mask(const uint8_t* cov, int64_t width, int64_t in_row0, int64_t in_rows,
+                    int64_t out_row0, int64_t out_rows, int64_t thickness, uint8_t* outline,
+                    void* stream);
+/* padding: texels with outline != 0 within Chebyshev distance <= radius of a texel
+ * with edited != 0 get data = value, mask = 1.  *count (device, zeroed) += padded texels. */
+int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t width,
+                     int64_t in_row0, int64_t in_rows, int64_t out_row0, int64_t out_rows,
+                     int64_t radius, void* data, int esize, uint32_t value_bits, uint8_t* mask,
+                     uint64_t* count, void* stream);
+
+/* ---- host-buffer entry points: exact drop-ins for the reference's numpy signatures ------------
+ * All pointers are HOST pointers; the call copies inputs to the device, runs the kernels above,
+ * copies the planes back and synchronises.  tri arrays are float64 (the reference widens to
+ * float64 anyway).  Returns ML_OK / error; counts through out-params. */
+int ml_coverage_fill_host(const double* tri_xy, int64_t ntri, int64_t width, int64_t height,
+                          uint8_t* out, int64_t* written);
+int ml_raster_depth_host(const double* tri_xy, const double* tri_zn, int64_t ntri,
+                         float* depth, int64_t width, int64_t height, int64_t* updated);
+int ml_raster_tea_host(const double* tri_xy, const double* tri_clip, int64_t ntri,
+                       double ww, double wh, const float* depth, int64_t depth_w, int64_t depth_h,
+                       double eps, int eps_f32, double sfx, double sfy, double bx, double by,
+                       const uint8_t* shape, int64_t shape_w, int64_t shape_h,
+                       void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
+                       int64_t width, int64_t height, int64_t* edited_count, int64_t* fragments);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MESHLAYERS_B200_H */

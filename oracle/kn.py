@@ -1,0 +1,270 @@
+"""ctypes front-end of ``oracle/kn_port.c`` -- TEST INFRASTRUCTURE, NOT PRODUCT CODE.
+
+The three pinned functions keep the reference's positional signatures
+(``_kernels_numpy.py``: ``coverage_fill`` KN:84, ``raster_depth`` KN:103, ``raster_tea``
+KN:135-136): numpy arrays in, planes mutated in place, plain ints out.  Parity status of each
+function is stated in the header of ``kn_port.c``.
+"""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "kn_port.c")
+_LIB = os.path.join(_HERE, "_build", "libkn_port.so")
+
+KINDS = {"uint8": 0, "int8": 1, "int16": 2, "int32": 3, "uint32": 4, "float16": 5, "float32": 6,
+         "bool": 0}
+
+
+def build(force=False):
+    """gcc the C restatement (same -ffp-contract=off as the reference's pkg/setup.py:13)."""
+    if (not force and os.path.exists(_LIB)
+            and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC)):
+        return _LIB
+    os.makedirs(os.path.dirname(_LIB), exist_ok=True)
+    cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC",
+           "-o", _LIB, _SRC, "-lm"]
+    subprocess.run(cmd, check=True)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        i64, dbl, vp, i32 = C.c_int64, C.c_double, C.c_void_p, C.c_int
+        _lib.kn_coverage_fill.restype = i64
+        _lib.kn_coverage_fill.argtypes = [vp, i64, i64, i64, vp]
+        _lib.kn_coverage_fill_mt.restype = i64
+        _lib.kn_coverage_fill_mt.argtypes = [vp, i64, i64, i64, vp, i32]
+        _lib.kn_raster_depth.restype = i64
+        _lib.kn_raster_depth.argtypes = [vp, vp, i64, vp, i64, i64]
+        _lib.kn_raster_depth_mt.restype = i64
+        _lib.kn_raster_depth_mt.argtypes = [vp, vp, i64, vp, i64, i64, i32]
+        tea = [vp, vp, i64, dbl, dbl, vp, i64, i64, dbl, i32, dbl, dbl, dbl, dbl,
+               vp, i64, i64, vp, i64, vp, vp, vp, i64, i64, vp, vp]
+        _lib.kn_raster_tea.restype = None
+        _lib.kn_raster_tea.argtypes = tea
+        _lib.kn_raster_tea_mt.restype = None
+        _lib.kn_raster_tea_mt.argtypes = tea + [i32]
+        _lib.kn_max_threads.restype = i32
+        _lib.ext_surface_map.restype = i64
+        _lib.ext_surface_map.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp]
+        _lib.ext_select_sphere.restype = i64
+        _lib.ext_select_sphere.argtypes = [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i64, vp, vp, vp, i32]
+        _lib.ext_select_threshold.restype = i64
+        _lib.ext_select_threshold.argtypes = [vp, i32, vp, i64, dbl, dbl, vp, i64, vp, vp, vp, i32]
+        _lib.ext_layer_op.restype = None
+        _lib.ext_layer_op.argtypes = [i32, vp, vp, vp, vp, vp, vp, i64, i64, i32]
+        _lib.ext_layer_area.restype = dbl
+        _lib.ext_layer_area.argtypes = [vp, vp, i64, vp, i32]
+        _lib.ext_label_area.restype = None
+        _lib.ext_label_area.argtypes = [vp, vp, vp, i64, vp, vp]
+        _lib.ext_layer_stats.restype = None
+        _lib.ext_layer_stats.argtypes = [vp, i32, vp, i64, vp, vp, vp, vp]
+        _lib.ext_outline.restype = None
+        _lib.ext_outline.argtypes = [vp, i64, i64, i64, vp, i32]
+        _lib.ext_padding.restype = i64
+        _lib.ext_padding.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, vp, i32]
+        _lib.ext_mesh_surface_area.restype = dbl
+        _lib.ext_mesh_surface_area.argtypes = [vp, i64]
+    return _lib
+
+
+def max_threads():
+    return int(lib().kn_max_threads())
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f64(a, shape_tail):
+    """KN widens every triangle to float64 before use (KN:88, 113-114, 151-152); f32->f64 is exact."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    assert a.shape[1:] == shape_tail, (a.shape, shape_tail)
+    return a
+
+
+def _plane(a):
+    assert isinstance(a, np.ndarray) and a.flags.c_contiguous and a.flags.writeable
+    return a
+
+
+def _bytes1(a):
+    assert a.dtype.itemsize == 1, a.dtype
+    return a
+
+
+def eps_is_f32(eps):
+    """numpy adds a Python float (weak scalar) to the float32 depth samples IN FLOAT32
+    (KN:185, checked on numpy 2.3.5); a np.float64 scalar forces a float64 sum."""
+    if isinstance(eps, np.floating):
+        return eps.dtype.itemsize <= 4
+    return True
+
+
+def _value_bytes(value, dtype):
+    return np.array(value, dtype=dtype).reshape(1).copy()
+
+
+# ------------------------------------------------------------------ pinned (KN) functions
+
+def coverage_fill(tri_xy, width, height, out, threads=0):
+    tri = _f64(tri_xy, (3, 2))
+    _bytes1(_plane(out))
+    assert out.shape == (height, width)
+    if threads:
+        return int(lib().kn_coverage_fill_mt(_p(tri), tri.shape[0], width, height, _p(out), threads))
+    return int(lib().kn_coverage_fill(_p(tri), tri.shape[0], width, height, _p(out)))
+
+
+def raster_depth(tri_xy, tri_zn, depth, threads=0):
+    tri = _f64(tri_xy, (3, 2))
+    zn = _f64(tri_zn, (3,))
+    assert depth.dtype == np.float32
+    _plane(depth)
+    h, w = depth.shape
+    if threads:
+        return int(lib().kn_raster_depth_mt(_p(tri), _p(zn), tri.shape[0], _p(depth), w, h, threads))
+    return int(lib().kn_raster_depth(_p(tri), _p(zn), tri.shape[0], _p(depth), w, h))
+
+
+def raster_tea(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
+               shape, data, mask, edited, value, threads=0):
+    tri = _f64(tri_xy, (3, 2))
+    clip = _f64(tri_clip, (3, 4))
+    depth = np.ascontiguousarray(depth)
+    assert depth.dtype == np.float32
+    shape = np.ascontiguousarray(shape)
+    _bytes1(shape)
+    _bytes1(_plane(mask))
+    _bytes1(_plane(edited))
+    _plane(data)
+    h, w = mask.shape
+    assert data.shape == (h, w) and edited.shape == (h, w)
+    th, tw = shape.shape
+    dh, dw = depth.shape
+    assert dh >= np.ceil(wh) and dw >= np.ceil(ww), "depth plane smaller than the window"
+    val = _value_bytes(value, data.dtype)
+    ec = C.c_int64(0)
+    fr = C.c_int64(0)
+    args = [_p(tri), _p(clip), tri.shape[0], float(ww), float(wh), _p(depth), dw, dh,
+            float(eps), int(eps_is_f32(eps)), float(sfx), float(sfy), float(bx), float(by),
+            _p(shape), tw, th, _p(data), data.dtype.itemsize, _p(val), _p(mask), _p(edited),
+            w, h, C.addressof(ec), C.addressof(fr)]
+    if threads:
+        lib().kn_raster_tea_mt(*args, threads)
+    else:
+        lib().kn_raster_tea(*args)
+    return int(ec.value), int(fr.value)
+
+
+# ------------------------------------------------------------------ extension definitions
+
+def surface_map(tri_xy, tri_pos, tri_nrm, width, height, rows=None):
+    """Returns dict(tri_id, pos[3,h,w], nrm[3,h,w], area, covered, overlap) for rows [r0,r1)."""
+    tri = _f64(tri_xy, (3, 2))
+    P = _f64(tri_pos, (3, 3))
+    N = _f64(tri_nrm, (3, 3))
+    r0, r1 = rows if rows is not None else (0, height)
+    n = r1 - r0
+    tri_id = np.empty((n, width), np.int32)
+    pos = np.empty((3, n, width), np.float32)
+    nrm = np.empty((3, n, width), np.float32)
+    area = np.empty((n, width), np.float32)
+    ov = C.c_int64(0)
+    cov = lib().ext_surface_map(_p(tri), _p(P), _p(N), tri.shape[0], width, height, r0, r1,
+                                _p(tri_id), _p(pos), _p(nrm), _p(area), C.addressof(ov))
+    return dict(tri_id=tri_id, pos=pos, nrm=nrm, area=area, covered=int(cov), overlap=int(ov.value))
+
+
+def select_sphere(pos, center, radius, data, mask, edited, value, threads=1):
+    assert pos.dtype == np.float32 and pos.flags.c_contiguous and pos.shape[0] == 3
+    n = mask.size
+    assert pos[0].size == n
+    val = _value_bytes(value, data.dtype)
+    return int(lib().ext_select_sphere(_p(pos), n, n, float(center[0]), float(center[1]),
+                                       float(center[2]), float(radius), _p(_plane(data)),
+                                       data.dtype.itemsize, _p(val), _p(_bytes1(_plane(mask))),
+                                       _p(_bytes1(_plane(edited))), threads))
+
+
+def select_threshold(attr, valid, lo, hi, data, mask, edited, value, threads=1):
+    attr = np.ascontiguousarray(attr)
+    kind = KINDS[attr.dtype.name]
+    n = mask.size
+    assert attr.size == n
+    if valid is not None:
+        valid = np.ascontiguousarray(valid)
+        _bytes1(valid)
+    val = _value_bytes(value, data.dtype)
+    return int(lib().ext_select_threshold(_p(attr), kind, _p(valid), n, float(lo), float(hi),
+                                          _p(_plane(data)), data.dtype.itemsize, _p(val),
+                                          _p(_bytes1(_plane(mask))), _p(_bytes1(_plane(edited))),
+                                          threads))
+
+
+OPS = {"union": 0, "intersection": 1, "difference": 2, "masking": 3}
+
+
+def layer_op(op, da, ma, db, mb, dc, mc, threads=1):
+    """(dc, mc) = (da, ma) <op> (db, mb); data planes may all be None (mask-only algebra)."""
+    n = ma.size
+    es = 0 if da is None else da.dtype.itemsize
+    lib().ext_layer_op(OPS[op], _p(da), _p(_bytes1(ma)), _p(db), _p(_bytes1(mb)), _p(dc),
+                       _p(_bytes1(_plane(mc))), es, n, threads)
+
+
+def layer_area(area, mask, threads=1):
+    assert area.dtype == np.float32
+    cnt = C.c_int64(0)
+    a = lib().ext_layer_area(_p(np.ascontiguousarray(area)), _p(_bytes1(np.ascontiguousarray(mask))),
+                             mask.size, C.addressof(cnt), threads)
+    return float(a), int(cnt.value)
+
+
+def label_area(area, data, mask):
+    assert area.dtype == np.float32 and data.dtype.itemsize == 1
+    out = np.zeros(256, np.float64)
+    cnt = np.zeros(256, np.int64)
+    lib().ext_label_area(_p(np.ascontiguousarray(area)), _p(np.ascontiguousarray(data)),
+                         _p(np.ascontiguousarray(mask)), mask.size, _p(out), _p(cnt))
+    return out, cnt
+
+
+def layer_stats(attr, mask):
+    attr = np.ascontiguousarray(attr)
+    cnt = C.c_int64(0)
+    s, mn, mx = C.c_double(0), C.c_double(0), C.c_double(0)
+    lib().ext_layer_stats(_p(attr), KINDS[attr.dtype.name], _p(np.ascontiguousarray(mask)), mask.size,
+                          C.addressof(cnt), C.addressof(s), C.addressof(mn), C.addressof(mx))
+    return int(cnt.value), float(s.value), float(mn.value), float(mx.value)
+
+
+def outline(cov, thickness, threads=1):
+    cov = np.ascontiguousarray(cov)
+    out = np.zeros(cov.shape, np.uint8)
+    h, w = cov.shape
+    lib().ext_outline(_p(_bytes1(cov)), w, h, int(thickness), _p(out), threads)
+    return out
+
+
+def padding(outline_mask, edited, radius, data, mask, value, threads=1):
+    h, w = mask.shape
+    val = _value_bytes(value, data.dtype)
+    return int(lib().ext_padding(_p(_bytes1(np.ascontiguousarray(outline_mask))),
+                                 _p(_bytes1(np.ascontiguousarray(edited))), w, h, int(radius),
+                                 _p(_plane(data)), data.dtype.itemsize, _p(val),
+                                 _p(_bytes1(_plane(mask))), threads))
+
+
+def mesh_surface_area(tri_pos):
+    P = _f64(tri_pos, (3, 3))
+    return float(lib().ext_mesh_surface_area(_p(P), P.shape[0]))

@@ -1,0 +1,675 @@
+"""``_native`` -- the compiled kernel backend, B200 edition.
+
+This module fills the slot the reference declares as ``meshlayers._native`` (reference
+``pkg/setup.py:5-13``): the function-for-function twin of ``meshlayers._kernels_numpy`` (KN).
+The three hot functions keep KN's names, positional signatures, in-place plane mutation and
+return conventions:
+
+    coverage_fill(tri_xy, width, height, out) -> int                       KN:84
+    raster_depth(tri_xy, tri_zn, depth) -> int                             KN:103
+    raster_tea(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
+               shape, data, mask, edited, value) -> (int, int)             KN:135-136
+
+They accept either numpy arrays (HOST buffers, exactly like the reference: the call uploads,
+runs the CUDA kernels, downloads the planes in place) or torch CUDA tensors (device resident:
+nothing is copied).  Everything below them is an extension for the north-star operations
+(surface map, sphere / threshold selection, layer algebra, areas, outline / padding) and works
+on torch CUDA tensors only.
+
+All compute happens in ``libmeshlayers_b200.so`` (hand-written sm_100a CUDA behind the C ABI of
+``include/meshlayers_b200.h``), loaded with ctypes.  There is NO CPU fallback: if the library
+or a CUDA device is missing every call raises ``BackendUnavailable``.
+"""
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+from .errors import BackendUnavailable, MeshLayersError, TargetMismatch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmeshlayers_b200.so")
+
+ML_F32, ML_F64 = 0, 1
+KIND_CODES = {"uint8": 0, "bool": 0, "int8": 1, "int16": 2, "int32": 3, "uint32": 4,
+              "float16": 5, "float32": 6}
+OPS = {"union": 0, "intersection": 1, "difference": 2, "masking": 3}
+
+_lib = None
+
+
+class _TeaParams(C.Structure):
+    _fields_ = [("ww", C.c_double), ("wh", C.c_double), ("eps", C.c_double),
+                ("sfx", C.c_double), ("sfy", C.c_double), ("bx", C.c_double), ("by", C.c_double),
+                ("depth", C.c_void_p), ("shape", C.c_void_p),
+                ("depth_w", C.c_int64), ("depth_h", C.c_int64),
+                ("shape_w", C.c_int64), ("shape_h", C.c_int64),
+                ("eps_f32", C.c_int32), ("reserved", C.c_int32)]
+
+
+def lib():
+    """Load the C-ABI library (once).  Raises BackendUnavailable when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise BackendUnavailable(
+            "libmeshlayers_b200.so is not built; run `python -m paper_2501_14807_b200.build` "
+            "(there is no CPU fallback)")
+    try:
+        L = C.CDLL(LIB_PATH)
+    except OSError as exc:                                   # pragma: no cover
+        raise BackendUnavailable("cannot load %s: %s" % (LIB_PATH, exc))
+    i64, i32, dbl, vp, u32, sz = C.c_int64, C.c_int, C.c_double, C.c_void_p, C.c_uint32, C.c_size_t
+    sig = {
+        "ml_version": (i32, []),
+        "ml_last_error": (C.c_char_p, []),
+        "ml_sm_count": (i32, []),
+        "ml_raster_workspace_bytes": (sz, [i64]),
+        "ml_coverage_fill": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
+        "ml_raster_depth": (i32, [vp, vp, i32, i64, vp, i64, i64, vp, sz, vp]),
+        "ml_raster_tea": (i32, [vp, vp, i32, i64, i64, i64, i64, i64, C.POINTER(_TeaParams), vp, i32,
+                                u32, vp, vp, vp, vp, sz, vp]),
+        "ml_raster_tri_id": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
+        "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
+        "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, C.POINTER(_TeaParams), vp, i32,
+                                u32, vp, vp, vp, vp]),
+        "ml_select_sphere": (i32, [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
+        "ml_select_sphere_batch": (i32, [vp, i64, i64, vp, vp, vp, i64, vp, vp, vp, i64, i32, vp, vp]),
+        "ml_select_threshold": (i32, [vp, i32, vp, i64, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
+        "ml_layer_op": (i32, [i32, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
+        "ml_layer_chain": (i32, [i64, vp, vp, vp, vp, vp, i32, i64, vp]),
+        "ml_layer_area": (i32, [vp, vp, i64, i64, vp, vp, vp]),
+        "ml_label_area": (i32, [vp, vp, vp, i64, vp, vp, vp]),
+        "ml_layer_stats": (i32, [vp, i32, vp, i64, vp, vp]),
+        "ml_outline_mask": (i32, [vp, i64, i64, i64, i64, i64, i64, vp, vp]),
+        "ml_apply_padding": (i32, [vp, vp, i64, i64, i64, i64, i64, i64, vp, i32, u32, vp, vp, vp]),
+        "ml_coverage_fill_host": (i32, [vp, i64, i64, i64, vp, vp]),
+        "ml_raster_depth_host": (i32, [vp, vp, i64, vp, i64, i64, vp]),
+        "ml_raster_tea_host": (i32, [vp, vp, i64, dbl, dbl, vp, i64, i64, dbl, i32, dbl, dbl, dbl, dbl,
+                                     vp, i64, i64, vp, i32, u32, vp, vp, i64, i64, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = (
+    "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
+    "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve", "ml_tea_texels",
+    "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
+    "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
+    "ml_apply_padding", "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
+
+
+def _check(rc):
+    if rc == 0:
+        return
+    msg = lib().ml_last_error().decode("utf-8", "replace")
+    if rc == 1:
+        raise TargetMismatch(msg)
+    if rc == 3:
+        raise BackendUnavailable(msg)
+    raise MeshLayersError("libmeshlayers_b200: " + msg)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def require_cuda():
+    """Fail loudly when the CUDA path cannot run (no fallback exists)."""
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise BackendUnavailable("no CUDA device visible; paper_2501_14807_b200 has no CPU fallback")
+    lib()
+    return torch
+
+
+def _is_cuda_tensor(a):
+    return type(a).__module__.startswith("torch") and hasattr(a, "is_cuda") and a.is_cuda
+
+
+def _stream():
+    return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _tri_dev(a, tail, device):
+    """Triangle attribute array -> contiguous CUDA tensor of float32/float64 (widened on device
+    per triangle like KN:88).  numpy inputs are uploaded."""
+    torch = _torch()
+    if not _is_cuda_tensor(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        a = torch.from_numpy(a).to(device)
+    if a.dtype not in (torch.float32, torch.float64):
+        a = a.to(torch.float64)
+    a = a.contiguous()
+    if tuple(a.shape[1:]) != tail:
+        raise TargetMismatch("expected triangle array of shape (T,%s), got %s" % (tail, tuple(a.shape)))
+    return a, (ML_F32 if a.dtype == torch.float32 else ML_F64)
+
+
+def _same_dtype(*arrs):
+    torch = _torch()
+    if len({a.dtype for a in arrs}) > 1:
+        return [a.to(torch.float64) for a in arrs]
+    return list(arrs)
+
+
+def _np_dtype_of(t):
+    """numpy dtype with the same element layout as a torch tensor / numpy array."""
+    if isinstance(t, np.ndarray):
+        return t.dtype
+    name = str(t.dtype).replace("torch.", "")
+    return np.dtype("bool" if name == "bool" else name)
+
+
+def value_bits(value, plane):
+    """Cast ``value`` the way numpy casts a scalar stored into the plane (KN:200) and return the
+    element's bytes as an unsigned integer."""
+    dt = _np_dtype_of(plane)
+    if dt.itemsize not in (1, 2, 4):
+        raise TargetMismatch("data plane element size %d not supported" % dt.itemsize)
+    v = np.array(value, dtype=dt).reshape(1)
+    return int(v.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[dt.itemsize])[0]), dt.itemsize
+
+
+def _byte_plane(t, what):
+    if _np_dtype_of(t).itemsize != 1:
+        raise TargetMismatch("%s plane must have 1-byte elements (bool / uint8)" % what)
+    if not t.is_contiguous():
+        raise TargetMismatch("%s plane must be contiguous" % what)
+    return t
+
+
+def eps_is_f32(eps):
+    """KN:185 adds ``eps`` to float32 depth samples: numpy keeps the sum in float32 for a Python
+    float (weak scalar) or np.float32, and promotes to float64 for np.float64."""
+    if isinstance(eps, np.floating):
+        return eps.dtype.itemsize <= 4
+    return True
+
+
+def _workspace(ntri, device):
+    torch = _torch()
+    nbytes = int(lib().ml_raster_workspace_bytes(int(ntri)))
+    return torch.empty(nbytes, dtype=torch.uint8, device=device), nbytes
+
+
+def _counters(n, device):
+    torch = _torch()
+    return torch.zeros(n, dtype=torch.int64, device=device)
+
+
+# =============================================================================================
+# KN twins
+# =============================================================================================
+
+def coverage_fill(tri_xy, width, height, out, *, row0=0, counts=None):
+    """KN:84-100.  ``out``: (rows, width) uint8/bool plane, numpy (host) or torch CUDA (device).
+    Returns the number of texels that went 0 -> 1 (or None when ``counts`` is supplied)."""
+    L = lib()
+    if isinstance(out, np.ndarray):
+        if out.shape != (height, width) or out.dtype.itemsize != 1 or not out.flags.c_contiguous:
+            raise TargetMismatch("out must be a contiguous (height, width) uint8 plane")
+        tri = np.ascontiguousarray(tri_xy, dtype=np.float64)
+        if tri.shape[1:] != (3, 2):
+            raise TargetMismatch("tri_xy must be (T,3,2)")
+        written = C.c_int64(0)
+        _check(L.ml_coverage_fill_host(tri.ctypes.data, tri.shape[0], width, height,
+                                       out.ctypes.data, C.addressof(written)))
+        return int(written.value)
+    require_cuda()
+    _byte_plane(out, "out")
+    rows = out.shape[0]
+    if out.shape[1] != width or row0 < 0 or row0 + rows > height:
+        raise TargetMismatch("out slab does not fit a %dx%d plane" % (height, width))
+    tri, dt = _tri_dev(tri_xy, (3, 2), out.device)
+    ws, nb = _workspace(tri.shape[0], out.device)
+    ctr = counts if counts is not None else _counters(2, out.device)
+    _check(L.ml_coverage_fill(_ptr(tri), dt, tri.shape[0], width, height, row0, rows, _ptr(out),
+                              _ptr(ctr), _ptr(ws), nb, _stream()))
+    return None if counts is not None else int(ctr[0].item())
+
+
+def raster_depth(tri_xy, tri_zn, depth):
+    """KN:103-132.  ``depth``: (Wh, Ww) float32 plane updated in place.  The reference's return
+    value depends on triangle order; this returns the number of texels whose
+    depth changed instead."""
+    L = lib()
+    if isinstance(depth, np.ndarray):
+        if depth.dtype != np.float32 or depth.ndim != 2 or not depth.flags.c_contiguous:
+            raise TargetMismatch("depth must be a contiguous 2-D float32 plane")
+        tri = np.ascontiguousarray(tri_xy, dtype=np.float64)
+        zn = np.ascontiguousarray(tri_zn, dtype=np.float64)
+        if tri.shape[1:] != (3, 2) or zn.shape != (tri.shape[0], 3):
+            raise TargetMismatch("tri_xy must be (T,3,2) and tri_zn (T,3)")
+        upd = C.c_int64(0)
+        h, w = depth.shape
+        _check(L.ml_raster_depth_host(tri.ctypes.data, zn.ctypes.data, tri.shape[0],
+                                      depth.ctypes.data, w, h, C.addressof(upd)))
+        return int(upd.value)
+    torch = require_cuda()
+    if depth.dtype != torch.float32 or depth.dim() != 2 or not depth.is_contiguous():
+        raise TargetMismatch("depth must be a contiguous 2-D float32 plane")
+    tri, _ = _tri_dev(tri_xy, (3, 2), depth.device)
+    zn, _ = _tri_dev(tri_zn, (3,), depth.device)
+    tri, zn = _same_dtype(tri, zn)
+    dt = ML_F32 if tri.dtype == torch.float32 else ML_F64
+    if zn.shape[0] != tri.shape[0]:
+        raise TargetMismatch("tri_xy / tri_zn triangle counts differ")
+    before = depth.clone()
+    ws, nb = _workspace(tri.shape[0], depth.device)
+    h, w = depth.shape
+    _check(L.ml_raster_depth(_ptr(tri), _ptr(zn), dt, tri.shape[0], _ptr(depth), w, h,
+                             _ptr(ws), nb, _stream()))
+    return int((before.view(torch.int32) != depth.view(torch.int32)).sum().item())
+
+
+def _tea_params(ww, wh, depth, eps, sfx, sfy, bx, by, shape):
+    p = _TeaParams()
+    p.ww, p.wh, p.eps = float(ww), float(wh), float(eps)
+    p.sfx, p.sfy, p.bx, p.by = float(sfx), float(sfy), float(bx), float(by)
+    p.depth, p.shape = depth.data_ptr(), shape.data_ptr()
+    p.depth_h, p.depth_w = depth.shape
+    p.shape_h, p.shape_w = shape.shape
+    p.eps_f32 = int(eps_is_f32(eps))
+    return p
+
+
+def _check_window(ww, wh, depth_shape, shape_shape):
+    if not (depth_shape[0] >= math.ceil(wh) and depth_shape[1] >= math.ceil(ww)):
+        raise TargetMismatch("depth plane %s smaller than the %sx%s window" % (tuple(depth_shape), ww, wh))
+    if shape_shape[0] < 1 or shape_shape[1] < 1:
+        raise TargetMismatch("tool shape plane is empty")
+
+
+def raster_tea(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
+               shape, data, mask, edited, value, *, height=None, row0=0, counts=None):
+    """KN:135-203, direct per-triangle kernel.  Returns (edited_texels, fragments_offered)."""
+    L = lib()
+    if isinstance(mask, np.ndarray):
+        h, w = mask.shape
+        if data.shape != (h, w) or edited.shape != (h, w):
+            raise TargetMismatch("data / mask / edited planes disagree in shape")
+        for a, nm in ((data, "data"), (mask, "mask"), (edited, "edited")):
+            if not a.flags.c_contiguous:
+                raise TargetMismatch(nm + " plane must be C-contiguous")
+        if mask.dtype.itemsize != 1 or edited.dtype.itemsize != 1:
+            raise TargetMismatch("mask / edited planes must be bool or uint8")
+        tri = np.ascontiguousarray(tri_xy, dtype=np.float64)
+        clip = np.ascontiguousarray(tri_clip, dtype=np.float64)
+        if tri.shape[1:] != (3, 2) or clip.shape != (tri.shape[0], 3, 4):
+            raise TargetMismatch("tri_xy must be (T,3,2) and tri_clip (T,3,4)")
+        dep = np.ascontiguousarray(depth, dtype=np.float32)
+        shp = np.ascontiguousarray(shape)
+        if shp.dtype.itemsize != 1:
+            shp = (shp != 0).astype(np.uint8)
+        _check_window(ww, wh, dep.shape, shp.shape)
+        bits, esize = value_bits(value, data)
+        ec, fr = C.c_int64(0), C.c_int64(0)
+        _check(L.ml_raster_tea_host(tri.ctypes.data, clip.ctypes.data, tri.shape[0], float(ww), float(wh),
+                                    dep.ctypes.data, dep.shape[1], dep.shape[0], float(eps),
+                                    int(eps_is_f32(eps)), float(sfx), float(sfy), float(bx), float(by),
+                                    shp.ctypes.data, shp.shape[1], shp.shape[0], data.ctypes.data, esize,
+                                    bits, mask.ctypes.data, edited.ctypes.data, w, h,
+                                    C.addressof(ec), C.addressof(fr)))
+        return int(ec.value), int(fr.value)
+    torch = require_cuda()
+    rows, w = mask.shape
+    height = rows if height is None else height
+    if tuple(data.shape) != (rows, w) or tuple(edited.shape) != (rows, w):
+        raise TargetMismatch("data / mask / edited planes disagree in shape")
+    _byte_plane(mask, "mask")
+    _byte_plane(edited, "edited")
+    if not data.is_contiguous():
+        raise TargetMismatch("data plane must be contiguous")
+    dev = mask.device
+    tri, _ = _tri_dev(tri_xy, (3, 2), dev)
+    clip, _ = _tri_dev(tri_clip, (3, 4), dev)
+    tri, clip = _same_dtype(tri, clip)
+    dt = ML_F32 if tri.dtype == torch.float32 else ML_F64
+    depth = _as_dev(depth, torch.float32, dev)
+    shape = _as_dev_bytes(shape, dev)
+    _check_window(ww, wh, depth.shape, shape.shape)
+    p = _tea_params(ww, wh, depth, eps, sfx, sfy, bx, by, shape)
+    bits, esize = value_bits(value, data)
+    ws, nb = _workspace(tri.shape[0], dev)
+    ctr = counts if counts is not None else _counters(2, dev)
+    _check(L.ml_raster_tea(_ptr(tri), _ptr(clip), dt, tri.shape[0], w, height, row0, rows, C.byref(p),
+                           _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr), _ptr(ws), nb,
+                           _stream()))
+    if counts is not None:
+        return None
+    c = ctr.tolist()
+    return int(c[0]), int(c[1])
+
+
+def _as_dev(a, dtype, device):
+    torch = _torch()
+    if not _is_cuda_tensor(a):
+        a = torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    if a.dtype != dtype:
+        a = a.to(dtype)
+    return a.contiguous()
+
+
+def _as_dev_bytes(a, device):
+    torch = _torch()
+    if not _is_cuda_tensor(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype.itemsize != 1:
+            a = (a != 0).astype(np.uint8)
+        a = torch.from_numpy(a.view(np.uint8)).to(device)
+    elif _np_dtype_of(a).itemsize != 1:
+        a = (a != 0).to(torch.uint8)
+    return a.contiguous()
+
+
+# =============================================================================================
+# Extensions (torch CUDA tensors only)
+# =============================================================================================
+
+def surface_map(tri_xy, tri_pos, tri_nrm, width, height, *, row0=0, rows=None, device=None):
+    """Texture-space rasterisation of the mesh into the per-texel surface map (north star (1);
+    definition oracle/kn_port.c ext_surface_map).  Returns a dict of CUDA tensors:
+    tri_id int32 (rows,width); pos, nrm float32 (3,rows,width); area float32 (rows,width); and
+    ints covered, fragments, overlap (= fragments - covered; 0 iff no uv overlap)."""
+    torch = require_cuda()
+    L = lib()
+    device = torch.device(device or "cuda")
+    rows = height - row0 if rows is None else rows
+    tri, _ = _tri_dev(tri_xy, (3, 2), device)
+    P, _ = _tri_dev(tri_pos, (3, 3), device)
+    N, _ = _tri_dev(tri_nrm, (3, 3), device)
+    tri, P, N = _same_dtype(tri, P, N)
+    dt = ML_F32 if tri.dtype == torch.float32 else ML_F64
+    T = tri.shape[0]
+    if P.shape[0] != T or N.shape[0] != T:
+        raise TargetMismatch("triangle attribute arrays disagree in length")
+    tri_id = torch.empty((rows, width), dtype=torch.int32, device=device)
+    pos = torch.empty((3, rows, width), dtype=torch.float32, device=device)
+    nrm = torch.empty((3, rows, width), dtype=torch.float32, device=device)
+    area = torch.empty((rows, width), dtype=torch.float32, device=device)
+    ctr = _counters(3, device)
+    ws, nb = _workspace(T, device)
+    _check(L.ml_raster_tri_id(_ptr(tri), dt, T, width, height, row0, rows, _ptr(tri_id), _ptr(ctr),
+                              _ptr(ws), nb, _stream()))
+    _check(L.ml_surface_resolve(_ptr(tri), _ptr(P), _ptr(N), dt, T, width, row0, rows, _ptr(tri_id),
+                                _ptr(pos), _ptr(nrm), _ptr(area), C.c_void_p(ctr.data_ptr() + 16),
+                                _stream()))
+    c = ctr.tolist()
+    return dict(tri_id=tri_id, pos=pos, nrm=nrm, area=area, fragments=int(c[0]), overlap=int(c[1]),
+                covered=int(c[2]))
+
+
+def raster_tri_id(tri_xy, width, height, *, row0=0, rows=None, device=None):
+    """Pass 1 of the surface map only.  Returns (tri_id, fragments, overlap)."""
+    torch = require_cuda()
+    device = torch.device(device or "cuda")
+    rows = height - row0 if rows is None else rows
+    tri, dt = _tri_dev(tri_xy, (3, 2), device)
+    tri_id = torch.empty((rows, width), dtype=torch.int32, device=device)
+    ctr = _counters(2, device)
+    ws, nb = _workspace(tri.shape[0], device)
+    _check(lib().ml_raster_tri_id(_ptr(tri), dt, tri.shape[0], width, height, row0, rows, _ptr(tri_id),
+                                  _ptr(ctr), _ptr(ws), nb, _stream()))
+    c = ctr.tolist()
+    return tri_id, int(c[0]), int(c[1])
+
+
+def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
+               shape, data, mask, edited, value, *, row0=0, counts=None):
+    """TEA over the cached triangle-id map (SURVEY.md 8 note N1): same planes and counts as
+    ``raster_tea`` when the uv layout has no overlaps.  Returns (edited_texels, fragments)."""
+    torch = require_cuda()
+    rows, w = mask.shape
+    dev = mask.device
+    if tuple(tri_id.shape) != (rows, w) or tuple(data.shape) != (rows, w) or tuple(edited.shape) != (rows, w):
+        raise TargetMismatch("tri_id / data / mask / edited planes disagree in shape")
+    _byte_plane(mask, "mask")
+    _byte_plane(edited, "edited")
+    tri, _ = _tri_dev(tri_xy, (3, 2), dev)
+    clip, _ = _tri_dev(tri_clip, (3, 4), dev)
+    tri, clip = _same_dtype(tri, clip)
+    dt = ML_F32 if tri.dtype == torch.float32 else ML_F64
+    depth = _as_dev(depth, torch.float32, dev)
+    shape = _as_dev_bytes(shape, dev)
+    _check_window(ww, wh, depth.shape, shape.shape)
+    p = _tea_params(ww, wh, depth, eps, sfx, sfy, bx, by, shape)
+    bits, esize = value_bits(value, data)
+    ctr = counts if counts is not None else _counters(2, dev)
+    _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
+                               C.byref(p), _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr),
+                               _stream()))
+    if counts is not None:
+        return None
+    c = ctr.tolist()
+    return int(c[0]), int(c[1])
+
+
+def _check_layer_planes(n, data, mask, edited):
+    if mask.numel() != n or data.numel() != n or (edited is not None and edited.numel() != n):
+        raise TargetMismatch("layer planes do not match the %d-texel map" % n)
+    _byte_plane(mask, "mask")
+    if edited is not None:
+        _byte_plane(edited, "edited")
+    if not data.is_contiguous():
+        raise TargetMismatch("data plane must be contiguous")
+
+
+def select_sphere(pos, center, radius, data, mask, edited, value, *, counts=None):
+    """Sphere brush over a (3, rows, width) float32 position map.  Returns newly edited texels."""
+    torch = require_cuda()
+    if pos.dtype != torch.float32 or pos.dim() != 3 or pos.shape[0] != 3 or not pos.is_contiguous():
+        raise TargetMismatch("pos must be a contiguous (3, rows, width) float32 tensor")
+    n = pos.shape[1] * pos.shape[2]
+    _check_layer_planes(n, data, mask, edited)
+    bits, esize = value_bits(value, data)
+    ctr = counts if counts is not None else _counters(1, pos.device)
+    _check(lib().ml_select_sphere(_ptr(pos), n, n, float(center[0]), float(center[1]), float(center[2]),
+                                  float(radius), _ptr(data), esize, bits, _ptr(mask), _ptr(edited),
+                                  _ptr(ctr), _stream()))
+    return None if counts is not None else int(ctr[0].item())
+
+
+class StrokeBatch:
+    """Device-resident description of K sphere strokes over L layers (pointer tables included),
+    reusable across calls: the only per-step host->device traffic is the stroke record upload."""
+
+    def __init__(self, layers_data, layers_mask, layers_edited, device):
+        torch = _torch()
+        self.L = len(layers_data)
+        self.data, self.mask, self.edited = list(layers_data), list(layers_mask), list(layers_edited)
+        esizes = {_np_dtype_of(d).itemsize for d in self.data}
+        if len(esizes) != 1:
+            raise TargetMismatch("all layers of a batch must share one element size")
+        self.esize = esizes.pop()
+        mk = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=device)
+        self.d_data, self.d_mask, self.d_edited = mk(self.data), mk(self.mask), mk(self.edited)
+        self.counts = torch.zeros(self.L, dtype=torch.int64, device=device)
+        self.device = device
+
+    def upload(self, strokes, layer_of, values):
+        """strokes (K,4) float64 [cx,cy,cz,r]; layer_of (K,) int; values (K,) in plane dtype."""
+        torch = _torch()
+        strokes = np.ascontiguousarray(strokes, dtype=np.float64)
+        K = strokes.shape[0]
+        dt = _np_dtype_of(self.data[0])
+        vals = np.zeros(K, dtype=np.uint32)
+        v = np.asarray(values).astype(dt).reshape(K)
+        vals[:] = v.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[dt.itemsize])
+        self.K = K
+        self.d_strokes = torch.from_numpy(strokes).to(self.device, non_blocking=True)
+        self.d_layer_of = torch.from_numpy(np.ascontiguousarray(layer_of, dtype=np.int32)).to(self.device, non_blocking=True)
+        self.d_values = torch.from_numpy(vals.view(np.int32)).to(self.device, non_blocking=True)
+        return self
+
+
+def select_sphere_batch(pos, batch):
+    """Apply ``batch`` (a StrokeBatch after ``upload``) in ONE pass over the position map.
+    Per-layer newly-edited counts accumulate into ``batch.counts`` (device)."""
+    torch = require_cuda()
+    n = pos.shape[1] * pos.shape[2]
+    for d, m, e in zip(batch.data, batch.mask, batch.edited):
+        _check_layer_planes(n, d, m, e)
+    _check(lib().ml_select_sphere_batch(_ptr(pos), n, n, _ptr(batch.d_strokes), _ptr(batch.d_layer_of),
+                                        _ptr(batch.d_values), batch.K, _ptr(batch.d_data),
+                                        _ptr(batch.d_mask), _ptr(batch.d_edited), batch.L, batch.esize,
+                                        _ptr(batch.counts), _stream()))
+
+
+def select_threshold(attr, valid, lo, hi, data, mask, edited, value, *, counts=None):
+    """Attribute-threshold selection: lo <= attr <= hi (closed) where ``valid`` (byte plane or
+    None) is non-zero.  Returns newly edited texels."""
+    require_cuda()
+    n = attr.numel()
+    name = _np_dtype_of(attr).name
+    if name not in KIND_CODES or not attr.is_contiguous():
+        raise TargetMismatch("unsupported attribute plane (%s)" % name)
+    _check_layer_planes(n, data, mask, edited)
+    if valid is not None:
+        _byte_plane(valid, "valid")
+        if valid.numel() != n:
+            raise TargetMismatch("valid plane does not match the attribute plane")
+    bits, esize = value_bits(value, data)
+    ctr = counts if counts is not None else _counters(1, attr.device)
+    _check(lib().ml_select_threshold(_ptr(attr), KIND_CODES[name], _ptr(valid), n, float(lo), float(hi),
+                                     _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr),
+                                     _stream()))
+    return None if counts is not None else int(ctr[0].item())
+
+
+def layer_op(op, da, ma, db, mb, dc, mc):
+    """(dc, mc) = (da, ma) <op> (db, mb).  Data planes may all be None (mask-only algebra)."""
+    require_cuda()
+    n = ma.numel()
+    if mb.numel() != n or mc.numel() != n:
+        raise TargetMismatch("mask planes disagree in size")
+    for m in (ma, mb, mc):
+        _byte_plane(m, "mask")
+    esize = 0
+    if dc is not None:
+        esize = _np_dtype_of(dc).itemsize
+        for d in (da, db):
+            if d is not None and (_np_dtype_of(d).itemsize != esize or d.numel() != n or not d.is_contiguous()):
+                raise TargetMismatch("data planes disagree in kind or size")
+        if da is None or dc.numel() != n or not dc.is_contiguous():
+            raise TargetMismatch("data planes disagree in kind or size")
+    _check(lib().ml_layer_op(OPS[op] if isinstance(op, str) else int(op), _ptr(da), _ptr(ma), _ptr(db),
+                             _ptr(mb), _ptr(dc), _ptr(mc), esize, n, _stream()))
+
+
+def layer_chain(datas, masks, ops, dc, mc):
+    """Fused left-to-right chain ((L0 ops[1] L1) ops[2] L2) ... in one pass.  ``ops[0]`` ignored."""
+    require_cuda()
+    N = len(masks)
+    n = mc.numel()
+    esize = 0 if dc is None else _np_dtype_of(dc).itemsize
+    for m in list(masks) + [mc]:
+        _byte_plane(m, "mask")
+        if m.numel() != n:
+            raise TargetMismatch("mask planes disagree in size")
+    if esize:
+        for d in list(datas) + [dc]:
+            if _np_dtype_of(d).itemsize != esize or d.numel() != n or not d.is_contiguous():
+                raise TargetMismatch("data planes disagree in kind or size")
+    dptr = (C.c_void_p * N)(*[(d.data_ptr() if esize else None) for d in (datas if esize else [None] * N)])
+    mptr = (C.c_void_p * N)(*[m.data_ptr() for m in masks])
+    codes = (C.c_int32 * N)(*[0] + [OPS[o] if isinstance(o, str) else int(o) for o in list(ops)[1:]])
+    _check(lib().ml_layer_chain(N, dptr, mptr, codes, _ptr(dc), _ptr(mc), esize, n, _stream()))
+
+
+def layer_area(area, masks, *, sums=None, counts=None):
+    """Per-layer area: for every mask plane, sum of area over texels with mask != 0 (float64).
+    Returns (sums, counts) as numpy arrays, or None when device accumulators are supplied."""
+    torch = require_cuda()
+    masks = list(masks)
+    n = area.numel()
+    if area.dtype != torch.float32 or not area.is_contiguous():
+        raise TargetMismatch("area must be a contiguous float32 plane")
+    for m in masks:
+        _byte_plane(m, "mask")
+        if m.numel() != n:
+            raise TargetMismatch("mask plane does not match the area plane")
+    Lc = len(masks)
+    own = sums is None
+    if own:
+        sums = torch.zeros(Lc, dtype=torch.float64, device=area.device)
+        counts = torch.zeros(Lc, dtype=torch.int64, device=area.device)
+    for l0 in range(0, Lc, 64):
+        chunk = masks[l0:l0 + 64]
+        mptr = (C.c_void_p * len(chunk))(*[m.data_ptr() for m in chunk])
+        _check(lib().ml_layer_area(_ptr(area), mptr, len(chunk), n,
+                                   C.c_void_p(sums.data_ptr() + 8 * l0),
+                                   None if counts is None else C.c_void_p(counts.data_ptr() + 8 * l0),
+                                   _stream()))
+    if own:
+        return sums.cpu().numpy(), counts.cpu().numpy()
+    return None
+
+
+def label_area(area, data, mask):
+    """Area and texel count per label value of a uint8 data plane -> (sums[256], counts[256])."""
+    torch = require_cuda()
+    n = area.numel()
+    if _np_dtype_of(data).itemsize != 1 or data.numel() != n or mask.numel() != n:
+        raise TargetMismatch("label_area needs 1-byte data / mask planes matching the area plane")
+    sums = torch.zeros(256, dtype=torch.float64, device=area.device)
+    counts = torch.zeros(256, dtype=torch.int64, device=area.device)
+    _check(lib().ml_label_area(_ptr(area), _ptr(data), _ptr(mask), n, _ptr(sums), _ptr(counts), _stream()))
+    return sums.cpu().numpy(), counts.cpu().numpy()
+
+
+def layer_stats(attr, mask):
+    """(count, sum, min, max) of the attribute over mask != 0, float64."""
+    torch = require_cuda()
+    name = _np_dtype_of(attr).name
+    if name not in KIND_CODES or attr.numel() != mask.numel():
+        raise TargetMismatch("attribute / mask planes disagree")
+    out = torch.tensor([0.0, 0.0, math.inf, -math.inf], dtype=torch.float64, device=attr.device)
+    _check(lib().ml_layer_stats(_ptr(attr.contiguous()), KIND_CODES[name], _ptr(_byte_plane(mask, "mask")),
+                                attr.numel(), _ptr(out), _stream()))
+    c, s, mn, mx = out.tolist()
+    return int(c), s, mn, mx
+
+
+def outline_mask(cov, thickness, *, in_row0=0, out_row0=None, out_rows=None, out=None):
+    """SPEC.md:286-289 second pass over a coverage slab (rows [in_row0, in_row0+cov.shape[0]))."""
+    torch = require_cuda()
+    _byte_plane(cov, "coverage")
+    in_rows, w = cov.shape
+    out_row0 = in_row0 if out_row0 is None else out_row0
+    out_rows = in_rows - (out_row0 - in_row0) if out_rows is None else out_rows
+    if out is None:
+        out = torch.empty((out_rows, w), dtype=torch.uint8, device=cov.device)
+    _check(lib().ml_outline_mask(_ptr(cov), w, in_row0, in_rows, out_row0, out_rows, int(thickness),
+                                 _ptr(out), _stream()))
+    return out
+
+
+def apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_row0=None, counts=None):
+    """SPEC.md:295-298.  ``edited`` is the input slab (with halo rows), the others output slabs."""
+    require_cuda()
+    in_rows, w = edited.shape
+    out_rows = outline.shape[0]
+    out_row0 = in_row0 if out_row0 is None else out_row0
+    _byte_plane(outline, "outline")
+    _byte_plane(edited, "edited")
+    _check_layer_planes(out_rows * w, data, mask, None)
+    bits, esize = value_bits(value, data)
+    ctr = counts if counts is not None else _counters(1, edited.device)
+    _check(lib().ml_apply_padding(_ptr(outline), _ptr(edited), w, in_row0, in_rows, out_row0, out_rows,
+                                  int(radius), _ptr(data), esize, bits, _ptr(mask), _ptr(ctr), _stream()))
+    return None if counts is not None else int(ctr[0].item())

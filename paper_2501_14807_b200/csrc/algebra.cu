@@ -1,0 +1,246 @@
+// Layer algebra (north star (3)): union / intersection / difference / masking over (data, mask)
+// layers.  The reference leaves inter-layer algebra out of scope; the frozen
+// definition is oracle/kn_port.c ext_layer_op.
+//
+// Pure HBM streams.  One thread step covers 16 texels: a 128-bit load of each mask plane and
+// ESIZE 128-bit loads of each data plane, all issued before the first use, then SIMD-in-register
+// byte logic and 128-bit stores.  Algorithmic traffic per texel: mask-only 3 B (2 reads + 1
+// write), full layers 3*(1+ESIZE) B, N-layer fused chain (N+1)*(1+ESIZE) B.
+#include "common.cuh"
+#include "meshlayers_b200.h"
+#include "internal.h"
+
+namespace {
+
+constexpr int BLOCK = 256;
+constexpr int MAX_CHAIN = 16;
+
+// 0xff in every byte lane of m that is non-zero
+ML_DEV uint32_t nz_bytes(uint32_t m) { return __vcmpne4(m, 0u); }
+
+// expand the 4 byte-lane flags of `ff` (each 0x00 / 0xff) to element lanes of ESIZE bytes:
+// word j (0 <= j < ESIZE) of the 4-element group
+template <int ESIZE> ML_DEV uint32_t expand(uint32_t ff, int j);
+template <> ML_DEV uint32_t expand<1>(uint32_t ff, int) { return ff; }
+template <> ML_DEV uint32_t expand<2>(uint32_t ff, int j) { return __byte_perm(ff, 0u, j == 0 ? 0x1100 : 0x3322); }
+template <> ML_DEV uint32_t expand<4>(uint32_t ff, int j) {
+    return __byte_perm(ff, 0u, j == 0 ? 0x0000 : j == 1 ? 0x1111 : j == 2 ? 0x2222 : 0x3333);
+}
+
+// One 4-texel group: masks as byte flags (ff), data words d[ESIZE].
+template <int ESIZE>
+struct Group {
+    uint32_t ff;                 // 0xff per valid texel
+    uint32_t d[ESIZE > 0 ? ESIZE : 1];
+};
+
+template <int ESIZE>
+ML_DEV void combine(int op, Group<ESIZE>& acc, const Group<ESIZE>& b) {
+    uint32_t keep_a, take_b, out_ff;
+    switch (op) {
+    case ML_OP_UNION:        out_ff = acc.ff | b.ff;  keep_a = acc.ff;  take_b = b.ff & ~acc.ff; break;
+    case ML_OP_DIFFERENCE:   out_ff = acc.ff & ~b.ff; keep_a = out_ff;  take_b = 0u; break;
+    default:                 out_ff = acc.ff & b.ff;  keep_a = out_ff;  take_b = 0u; break;   // intersection / masking
+    }
+    if (ESIZE > 0) {
+#pragma unroll
+        for (int j = 0; j < (ESIZE > 0 ? ESIZE : 1); ++j)
+            acc.d[j] = (acc.d[j] & expand<(ESIZE > 0 ? ESIZE : 1)>(keep_a, j)) |
+                       (b.d[j] & expand<(ESIZE > 0 ? ESIZE : 1)>(take_b, j));
+    }
+    acc.ff = out_ff;
+}
+
+struct ChainArgs {
+    const void* data[MAX_CHAIN];
+    const uint8_t* mask[MAX_CHAIN];
+    int ops[MAX_CHAIN];
+    int nlayers;
+};
+
+// 16 texels per thread step.  Layers are fetched in groups of GL (all GL*(1+ESIZE) 128-bit
+// requests of a group are issued before the first use), then folded into the accumulator left
+// to right.  GL is chosen so a group fits the register file: 8 / 8 / 4 / 2 for ESIZE 0/1/2/4.
+template <int ESIZE> struct GroupLen { static constexpr int value = ESIZE <= 1 ? 8 : (ESIZE == 2 ? 4 : 2); };
+
+template <int ESIZE>
+__global__ void __launch_bounds__(BLOCK)
+chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
+    constexpr int ES = ESIZE > 0 ? ESIZE : 1;
+    constexpr int GL = GroupLen<ESIZE>::value;
+    const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    const long long nv = n >> 4;
+    for (long long v = tid; v < nv; v += nthreads) {
+        Group<ESIZE> acc[4];                      // four 4-texel groups of the 16-texel vector
+        for (int l0 = 0; l0 < a.nlayers; l0 += GL) {
+            uint4 m[GL];
+            uint4 d[GL][ES];
+#pragma unroll
+            for (int k = 0; k < GL; ++k) {
+                if (l0 + k < a.nlayers) {
+                    m[k] = ld_stream_rw((const uint4*)a.mask[l0 + k] + v);
+                    if (ESIZE > 0) {
+#pragma unroll
+                        for (int j = 0; j < ES; ++j) d[k][j] = ld_stream_rw((const uint4*)a.data[l0 + k] + v * ES + j);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < GL; ++k) {
+                if (l0 + k < a.nlayers) {
+                    const int op = a.ops[l0 + k];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        Group<ESIZE> b;
+                        b.ff = nz_bytes(((const uint32_t*)&m[k])[g]);
+                        if (ESIZE > 0) {
+#pragma unroll
+                            for (int j = 0; j < ES; ++j) b.d[j] = ((const uint32_t*)&d[k][0])[g * ES + j];
+                        }
+                        if (l0 + k == 0) {        // first operand initialises the accumulator
+                            acc[g].ff = b.ff;
+                            if (ESIZE > 0) {
+#pragma unroll
+                                for (int j = 0; j < ES; ++j) acc[g].d[j] = b.d[j] & expand<ES>(b.ff, j);
+                            }
+                        } else {
+                            combine<ESIZE>(op, acc[g], b);
+                        }
+                    }
+                }
+            }
+        }
+        uint4 om;
+        uint4 od[ES];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            ((uint32_t*)&om)[g] = acc[g].ff & 0x01010101u;
+            if (ESIZE > 0) {
+#pragma unroll
+                for (int j = 0; j < ES; ++j) ((uint32_t*)&od[0])[g * ES + j] = acc[g].d[j];
+            }
+        }
+        st_stream((uint4*)mc + v, om);
+        if (ESIZE > 0) {
+#pragma unroll
+            for (int j = 0; j < ES; ++j) st_stream((uint4*)dc + v * ES + j, od[j]);
+        }
+    }
+    // tail (< 16 texels) and nothing else: scalar
+    for (long long i = (nv << 4) + tid; i < n; i += nthreads) {
+        bool am = a.mask[0][i] != 0;
+        uint32_t ad = 0;
+        if (ESIZE == 1) ad = ((const uint8_t*)a.data[0])[i];
+        if (ESIZE == 2) ad = ((const uint16_t*)a.data[0])[i];
+        if (ESIZE == 4) ad = ((const uint32_t*)a.data[0])[i];
+        if (!am) ad = 0;
+        for (int l = 1; l < a.nlayers; ++l) {
+            const bool bm = a.mask[l][i] != 0;
+            uint32_t bd = 0;
+            if (ESIZE == 1) bd = ((const uint8_t*)a.data[l])[i];
+            if (ESIZE == 2) bd = ((const uint16_t*)a.data[l])[i];
+            if (ESIZE == 4) bd = ((const uint32_t*)a.data[l])[i];
+            switch (a.ops[l]) {
+            case ML_OP_UNION:      if (!am && bm) ad = bd; am = am || bm; break;
+            case ML_OP_DIFFERENCE: am = am && !bm; if (!am) ad = 0; break;
+            default:               am = am && bm;  if (!am) ad = 0; break;
+            }
+        }
+        mc[i] = am ? 1 : 0;
+        if (ESIZE == 1) ((uint8_t*)dc)[i] = (uint8_t)ad;
+        if (ESIZE == 2) ((uint16_t*)dc)[i] = (uint16_t)ad;
+        if (ESIZE == 4) ((uint32_t*)dc)[i] = ad;
+    }
+}
+
+// fully scalar kernel for planes that are not 16-byte aligned
+template <int ESIZE>
+__global__ void __launch_bounds__(BLOCK)
+chain_scalar_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    for (long long i = (long long)blockIdx.x * BLOCK + threadIdx.x; i < n; i += nthreads) {
+        bool am = a.mask[0][i] != 0;
+        uint32_t ad = 0;
+        if (ESIZE == 1) ad = ((const uint8_t*)a.data[0])[i];
+        if (ESIZE == 2) ad = ((const uint16_t*)a.data[0])[i];
+        if (ESIZE == 4) ad = ((const uint32_t*)a.data[0])[i];
+        if (!am) ad = 0;
+        for (int l = 1; l < a.nlayers; ++l) {
+            const bool bm = a.mask[l][i] != 0;
+            uint32_t bd = 0;
+            if (ESIZE == 1) bd = ((const uint8_t*)a.data[l])[i];
+            if (ESIZE == 2) bd = ((const uint16_t*)a.data[l])[i];
+            if (ESIZE == 4) bd = ((const uint32_t*)a.data[l])[i];
+            switch (a.ops[l]) {
+            case ML_OP_UNION:      if (!am && bm) ad = bd; am = am || bm; break;
+            case ML_OP_DIFFERENCE: am = am && !bm; if (!am) ad = 0; break;
+            default:               am = am && bm;  if (!am) ad = 0; break;
+            }
+        }
+        mc[i] = am ? 1 : 0;
+        if (ESIZE == 1) ((uint8_t*)dc)[i] = (uint8_t)ad;
+        if (ESIZE == 2) ((uint16_t*)dc)[i] = (uint16_t)ad;
+        if (ESIZE == 4) ((uint32_t*)dc)[i] = ad;
+    }
+}
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+template <int ESIZE>
+int launch_chain(const ChainArgs& a, void* dc, uint8_t* mc, long long n, cudaStream_t st) {
+    bool vec = aligned16(mc) && (ESIZE == 0 || aligned16(dc));
+    for (int l = 0; l < a.nlayers; ++l) vec = vec && aligned16(a.mask[l]) && (ESIZE == 0 || aligned16(a.data[l]));
+    const long long items = vec ? ((n + 15) >> 4) : n;
+    long long blocks = (items + BLOCK - 1) / BLOCK;
+    const long long cap = (long long)ml_sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    if (vec) chain_kernel<ESIZE><<<(unsigned)blocks, BLOCK, 0, st>>>(a, dc, mc, n);
+    else chain_scalar_kernel<ESIZE><<<(unsigned)blocks, BLOCK, 0, st>>>(a, dc, mc, n);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int dispatch_chain(const ChainArgs& a, void* dc, uint8_t* mc, int esize, long long n, cudaStream_t st) {
+    if (n <= 0) return ML_OK;
+    switch (esize) {
+    case 0: return launch_chain<0>(a, dc, mc, n, st);
+    case 1: return launch_chain<1>(a, dc, mc, n, st);
+    case 2: return launch_chain<2>(a, dc, mc, n, st);
+    case 4: return launch_chain<4>(a, dc, mc, n, st);
+    }
+    return ml_fail(ML_ERR_ARG, "esize must be 0 (mask only), 1, 2 or 4");
+}
+
+}  // namespace
+
+extern "C" {
+
+int ml_layer_op(int op, const void* da, const uint8_t* ma, const void* db, const uint8_t* mb,
+                void* dc, uint8_t* mc, int esize, int64_t n, void* stream) {
+    if (op < ML_OP_UNION || op > ML_OP_MASKING) return ml_fail(ML_ERR_ARG, "unknown layer operator");
+    ChainArgs a;
+    a.nlayers = 2;
+    a.data[0] = da; a.mask[0] = ma; a.ops[0] = 0;
+    a.data[1] = (op == ML_OP_MASKING || db == nullptr) ? da : db;   // B's data is never read for masking
+    a.mask[1] = mb; a.ops[1] = op;
+    if (op == ML_OP_UNION && esize > 0 && db == nullptr) return ml_fail(ML_ERR_ARG, "union needs B's data plane");
+    return dispatch_chain(a, dc, mc, esize, n, (cudaStream_t)stream);
+}
+
+int ml_layer_chain(int64_t nlayers, const void* const* data, const uint8_t* const* mask,
+                   const int32_t* ops, void* dc, uint8_t* mc, int esize, int64_t n, void* stream) {
+    if (nlayers < 1 || nlayers > MAX_CHAIN) return ml_fail(ML_ERR_ARG, "chain length must be 1..16");
+    ChainArgs a;
+    a.nlayers = (int)nlayers;
+    for (int l = 0; l < a.nlayers; ++l) {
+        a.data[l] = esize > 0 ? data[l] : nullptr;
+        a.mask[l] = mask[l];
+        a.ops[l] = l == 0 ? 0 : ops[l];
+        if (l > 0 && (ops[l] < ML_OP_UNION || ops[l] > ML_OP_MASKING)) return ml_fail(ML_ERR_ARG, "unknown layer operator");
+    }
+    return dispatch_chain(a, dc, mc, esize, n, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,226 @@
+// Shared device helpers for libmeshlayers_b200 (sm_100a only).
+//
+// Arithmetic contract (reference: pkg/src/meshlayers/_kernels_numpy.py:1-25, cited KN:line):
+// every decision is taken in IEEE float64 with the reference's exact association order and NO
+// fused multiply-add.  The helpers below use the round-to-nearest intrinsics, which ptxas never
+// contracts; the library is additionally compiled with -fmad=false.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#define ML_DEV __device__ __forceinline__
+
+ML_DEV double xadd(double a, double b) { return __dadd_rn(a, b); }
+ML_DEV double xsub(double a, double b) { return __dsub_rn(a, b); }
+ML_DEV double xmul(double a, double b) { return __dmul_rn(a, b); }
+ML_DEV double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---------------------------------------------------------------------------------------------
+// streaming memory access: 128-bit, read-only path, no L1 allocation (each byte is touched once)
+ML_DEV uint4 ld_stream(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+// same without .nc: legal when the kernel's output may alias this input (in-place layer ops)
+ML_DEV uint4 ld_stream_rw(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+    return r;
+}
+ML_DEV float4 ld_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+ML_DEV uint32_t ld_stream(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+ML_DEV void st_stream(uint4* p, uint4 v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+ML_DEV void st_stream(uint32_t* p, uint32_t v) {
+    asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// warp / block reductions
+ML_DEV long long warp_sum(long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+ML_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = xadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+// Block-wide integer sum followed by ONE atomic per block.  Must be reached by all threads.
+ML_DEV void block_count_add(long long v, unsigned long long* counter) {
+    __shared__ long long s_part[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    if (lane == 0) s_part[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        long long t = lane < nw ? s_part[lane] : 0;
+        t = warp_sum(t);
+        if (lane == 0 && t != 0) atomicAdd(counter, (unsigned long long)t);
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Byte planes (mask / edited / coverage, bool or uint8): set one byte to exactly 1 through a
+// 32-bit atomic on the enclosing word and report whether it was 0 before.  This reproduces
+// KN:97-99 / KN:198-202 ("count texels that go 0 -> 1, then store 1") under any interleaving
+// of writers that target the same texel.
+ML_DEV bool byte_set1_was0(uint8_t* plane, long long i) {
+    uint8_t* p = plane + i;
+    uint8_t cur = *(volatile uint8_t*)p;
+    if (cur == 1) return false;
+    uintptr_t a = (uintptr_t)p;
+    unsigned* w = (unsigned*)(a & ~(uintptr_t)3);
+    const unsigned sh = (unsigned)(a & 3) * 8u;
+    if (cur == 0) {
+        unsigned old = atomicOr(w, 1u << sh);
+        unsigned ob = (old >> sh) & 0xffu;
+        if (ob == 0) return true;
+        if (ob == 1) return false;
+    }
+    // the byte held some other non-zero value: force it to exactly 1
+    unsigned old = *(volatile unsigned*)w, assumed;
+    do {
+        assumed = old;
+        old = atomicCAS(w, assumed, (assumed & ~(0xffu << sh)) | (1u << sh));
+    } while (old != assumed);
+    return false;
+}
+
+// store `esize` (1, 2 or 4) bytes of `bits` at element i of a data plane
+ML_DEV void store_value(void* data, int esize, long long i, uint32_t bits) {
+    if (esize == 1) ((uint8_t*)data)[i] = (uint8_t)bits;
+    else if (esize == 2) ((uint16_t*)data)[i] = (uint16_t)bits;
+    else ((uint32_t*)data)[i] = bits;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Triangle setup: KN:32-41 (_ccw), KN:44-47 (tie rule), KN:50-59 (bbox, tightened).
+struct TriSetup {
+    double x0, y0, x1, y1, x2, y2;   // CCW-normalised vertices, grid units
+    double ax, ay, bx, by, cx, cy;   // edge deltas: a = v2-v1, b = v0-v2, c = v1-v0
+    int ix0, ix1, iy0, iy1;          // inclusive texel bbox, clipped to the plane / row slab
+    bool t0, t1, t2;                 // edge i accepts e == 0
+    bool swapped;                    // vertices 1 and 2 were exchanged
+};
+
+template <typename T>
+ML_DEV bool tri_load_ccw(const T* __restrict__ xy, TriSetup& s) {
+    double x0 = (double)xy[0], y0 = (double)xy[1], x1 = (double)xy[2], y1 = (double)xy[3],
+           x2 = (double)xy[4], y2 = (double)xy[5];
+    // non-finite coordinates: the reference raises inside _bands (KN:54); we skip the triangle.
+    if (!(isfinite(x0) && isfinite(y0) && isfinite(x1) && isfinite(y1) && isfinite(x2) && isfinite(y2)))
+        return false;
+    double area2 = xsub(xmul(xsub(x1, x0), xsub(y2, y0)), xmul(xsub(y1, y0), xsub(x2, x0)));  // KN:35
+    if (area2 == 0.0) return false;                                                          // KN:36
+    s.swapped = area2 < 0.0;                                                                 // KN:38
+    if (s.swapped) { double tx = x1, ty = y1; x1 = x2; y1 = y2; x2 = tx; y2 = ty; }
+    s.x0 = x0; s.y0 = y0; s.x1 = x1; s.y1 = y1; s.x2 = x2; s.y2 = y2;
+    s.ax = xsub(x2, x1); s.ay = xsub(y2, y1);
+    s.bx = xsub(x0, x2); s.by = xsub(y0, y2);
+    s.cx = xsub(x1, x0); s.cy = xsub(y1, y0);
+    s.t0 = s.ay < 0.0 || (s.ay == 0.0 && s.ax < 0.0);                                         // KN:75
+    s.t1 = s.by < 0.0 || (s.by == 0.0 && s.bx < 0.0);                                         // KN:76
+    s.t2 = s.cy < 0.0 || (s.cy == 0.0 && s.cx < 0.0);                                         // KN:77
+    return true;
+}
+
+// Inclusive bbox of candidate texels.  Exact geometry needs only centres i+0.5 in [min, max],
+// i.e. ceil(min-0.5) <= i <= floor(max-0.5).  The reference scans the wider box
+// floor(min-0.5) .. ceil(max) (KN:54-57) and accepts whatever passes the ROUNDED edge tests, so a
+// centre a few ulps outside the exact box could in principle still be accepted there.  A sign
+// flip of a rounded edge function needs |e| <= ~4u*(|P|+|Q|), which bounds the distance of such
+// a centre from the exact box by ~u * (triangle extent); the box below keeps
+// a margin tol >= 2^-20 + 2^-30*max|coord| (ten orders of magnitude above that bound), clamped
+// into the reference's box -- a subset of the reference's candidates that contains every texel
+// the reference can accept.  Banding / bbox choice never changes a texel value (KN:23-24).
+ML_DEV bool tri_bbox(TriSetup& s, long long width, long long height, long long row0, long long rows) {
+    double xmin = fmin(fmin(s.x0, s.x1), s.x2), xmax = fmax(fmax(s.x0, s.x1), s.x2);
+    double ymin = fmin(fmin(s.y0, s.y1), s.y2), ymax = fmax(fmax(s.y0, s.y1), s.y2);
+    const double mabs = fmax(fmax(fabs(xmin), fabs(xmax)), fmax(fabs(ymin), fabs(ymax)));
+    const double tol = 9.5367431640625e-07 + 9.313225746154785e-10 * mabs;
+    double fx0 = fmax(ceil(xmin - 0.5 - tol), floor(xmin - 0.5));
+    double fx1 = fmin(floor(xmax - 0.5 + tol), ceil(xmax));
+    double fy0 = fmax(ceil(ymin - 0.5 - tol), floor(ymin - 0.5));
+    double fy1 = fmin(floor(ymax - 0.5 + tol), ceil(ymax));
+    double lox = 0.0, hix = (double)(width - 1);
+    double loy = (double)row0, hiy = (double)(row0 + rows - 1);
+    if (hiy > (double)(height - 1)) hiy = (double)(height - 1);
+    if (fx0 < lox) fx0 = lox;
+    if (fy0 < loy) fy0 = loy;
+    if (fx1 > hix) fx1 = hix;
+    if (fy1 > hiy) fy1 = hiy;
+    if (fx1 < fx0 || fy1 < fy0) return false;
+    s.ix0 = (int)fx0; s.ix1 = (int)fx1; s.iy0 = (int)fy0; s.iy1 = (int)fy1;
+    return true;
+}
+
+// KN:68-81 at texel (x, y): edge functions at the centre (x+0.5, y+0.5) and the coverage test.
+ML_DEV bool tri_inside(const TriSetup& s, int x, int y, double& e0, double& e1, double& e2) {
+    const double cx = xadd((double)x, 0.5), cy = xadd((double)y, 0.5);       // KN:60, 63
+    e0 = xsub(xmul(s.ax, xsub(cy, s.y1)), xmul(s.ay, xsub(cx, s.x1)));       // KN:72
+    e1 = xsub(xmul(s.bx, xsub(cy, s.y2)), xmul(s.by, xsub(cx, s.x2)));       // KN:73
+    e2 = xsub(xmul(s.cx, xsub(cy, s.y0)), xmul(s.cy, xsub(cx, s.x0)));       // KN:74
+    const bool ok0 = (e0 > 0.0) || ((e0 == 0.0) && s.t0);                    // KN:78
+    const bool ok1 = (e1 > 0.0) || ((e1 == 0.0) && s.t1);                    // KN:79
+    const bool ok2 = (e2 > 0.0) || ((e2 == 0.0) && s.t2);                    // KN:80
+    return ok0 && ok1 && ok2;
+}
+
+// ---------------------------------------------------------------------------------------------
+// TEA fragment filters, KN:166-193, for one covered texel.
+struct TeaParams {
+    double ww, wh;          // window size (KN:179-181)
+    double eps;             // depth bias
+    double sfx, sfy, bx, by;
+    const float* depth;     // [dh][dw] window depth plane, y-up rows
+    const uint8_t* shape;   // [th][tw] tool shape plane
+    long long dw, dh, tw, th;
+    int eps_f32;            // 1: depth+eps rounded to float32 (numpy weak-scalar rule), 0: float64
+};
+
+ML_DEV bool tea_fragment(const TeaParams& p, double e0, double e1, double e2,
+                         const double* __restrict__ c0, const double* __restrict__ c1,
+                         const double* __restrict__ c2) {
+    const double esum = xadd(xadd(e0, e1), e2);                                   // KN:166
+    const double l0 = xdiv(e0, esum), l1 = xdiv(e1, esum), l2 = xdiv(e2, esum);   // KN:167-169
+    const double wc = xadd(xadd(xmul(l0, c0[3]), xmul(l1, c1[3])), xmul(l2, c2[3]));  // KN:173
+    if (!(wc > 0.0)) return false;                                                // KN:174
+    const double xc = xadd(xadd(xmul(l0, c0[0]), xmul(l1, c1[0])), xmul(l2, c2[0]));  // KN:170
+    const double yc = xadd(xadd(xmul(l0, c0[1]), xmul(l1, c1[1])), xmul(l2, c2[1]));  // KN:171
+    const double xn = xdiv(xc, wc), yn = xdiv(yc, wc);                            // KN:176-177
+    const double xw = xmul(xmul(xadd(xn, 1.0), 0.5), p.ww);                       // KN:179
+    const double yw = xmul(xmul(xadd(yn, 1.0), 0.5), p.wh);                       // KN:180
+    if (!((xw >= 0.0) && (xw < p.ww) && (yw >= 0.0) && (yw < p.wh))) return false;    // KN:181
+    const double zc = xadd(xadd(xmul(l0, c0[2]), xmul(l1, c1[2])), xmul(l2, c2[2]));  // KN:172
+    const double zn = xdiv(zc, wc);                                               // KN:178
+    const long long px = (long long)xw, py = (long long)yw;                       // KN:182-183
+    const double df = xmul(xadd(zn, 1.0), 0.5);                                   // KN:184
+    const float dv = __ldg(p.depth + py * p.dw + px);
+    const double lim = p.eps_f32 ? (double)__fadd_rn(dv, (float)p.eps) : xadd((double)dv, p.eps);
+    if (!(df <= lim)) return false;                                               // KN:185
+    const double s = xadd(xmul(p.sfx, xn), p.bx);                                 // KN:187
+    const double t = xadd(xmul(p.sfy, yn), p.by);                                 // KN:188
+    if (!((s >= 0.0) && (s <= 1.0) && (t >= 0.0) && (t <= 1.0))) return false;    // KN:189
+    long long si = (long long)xmul(s, (double)p.tw), ti = (long long)xmul(t, (double)p.th);
+    if (si > p.tw - 1) si = p.tw - 1;                                             // KN:191
+    if (ti > p.th - 1) ti = p.th - 1;                                             // KN:192
+    return __ldg(p.shape + ti * p.tw + si) != 0;                                  // KN:193
+}

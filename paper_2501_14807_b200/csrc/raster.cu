@@ -1,0 +1,314 @@
+// Texture-space rasteriser for sm_100a: coverage_fill, raster_depth, raster_tea (direct,
+// per-triangle) and the triangle-id pass of the surface map.
+//
+// Reference semantics: pkg/src/meshlayers/_kernels_numpy.py (KN) 84-100, 103-132, 135-203.
+// The reference walks triangles serially and each triangle's bbox with numpy array ops; here
+// every (triangle, texel) pair is an independent work item, which is legal because
+//   * coverage / TEA planes and counts do not depend on triangle order,
+//   * the depth plane equals min(initial, min_t float32(d_t)) for any order.
+//
+// Work distribution (B200: 148 SMs, thousands of resident warps):
+//   pass A  one WARP per triangle; lanes stride over the bbox in row-major order.  Triangles
+//           whose bbox exceeds SMALL_MAX texels are not rasterised here but appended to a
+//           "large" list together with their number of CHUNK-texel chunks.
+//   pass B  single-block exclusive scan of the chunk counts.
+//   pass C  one BLOCK per (large triangle, chunk): a fixed grid strides over the scanned
+//           work-item range, finds its triangle by binary search, and covers CHUNK
+//           consecutive bbox texels.  No host synchronisation anywhere.
+#include "common.cuh"
+#include "meshlayers_b200.h"
+#include "internal.h"
+
+namespace {
+
+constexpr int SMALL_MAX = 1024;       // bbox texels handled by one warp
+constexpr int CHUNK = 2048;           // bbox texels per block work item (large triangles)
+constexpr int BLOCK = 256;
+
+struct LargeList {
+    int* tri;                         // [ntri] triangle indices
+    unsigned long long* off;          // [ntri+1] chunk counts, then exclusive offsets
+    unsigned long long* count;        // number of large triangles
+    unsigned long long* total;        // total chunks (written by the scan)
+};
+
+// ------------------------------------------------------------------ fragment functors
+// Each functor provides:
+//   struct Tri;  Tri setup(long long t, const TriSetup&)       per-triangle attribute fetch
+//   void fragment(const Tri&, long long t, int x, int y, e0,e1,e2, long long& c0, long long& c1)
+// Planes are slab-local: texel (x, y) lives at (y - row0) * width + x.
+
+struct CoverageFn {
+    uint8_t* out; long long width, row0;
+    struct Tri {};
+    ML_DEV Tri setup(long long, const TriSetup&) const { return Tri(); }
+    ML_DEV void fragment(const Tri&, long long, int x, int y, double, double, double,
+                         long long& c0, long long&) const {
+        if (byte_set1_was0(out, (y - row0) * width + x)) ++c0;           // KN:97-99
+    }
+};
+
+struct TriIdFn {
+    int* tri_id; long long width, row0;
+    struct Tri {};
+    ML_DEV Tri setup(long long, const TriSetup&) const { return Tri(); }
+    ML_DEV void fragment(const Tri&, long long t, int x, int y, double, double, double,
+                         long long& c0, long long& c1) const {
+        // last triangle in submission order owns the texel
+        int old = atomicMax(tri_id + (y - row0) * width + x, (int)t);
+        ++c0;                               // fragments
+        if (old >= 0) ++c1;                 // overlap events = fragments - covered texels
+    }
+};
+
+template <typename T>
+struct DepthFn {
+    const T* tri_zn; float* depth; long long width;
+    struct Tri { double z0, z1, z2; };
+    ML_DEV Tri setup(long long t, const TriSetup& s) const {
+        Tri r;
+        r.z0 = (double)tri_zn[3 * t];
+        r.z1 = (double)tri_zn[3 * t + (s.swapped ? 2 : 1)];              // KN:40 swap attrs too
+        r.z2 = (double)tri_zn[3 * t + (s.swapped ? 1 : 2)];
+        return r;
+    }
+    ML_DEV void fragment(const Tri& a, long long, int x, int y, double e0, double e1, double e2,
+                         long long&, long long&) const {
+        const double esum = xadd(xadd(e0, e1), e2);                                   // KN:122
+        const double l0 = xdiv(e0, esum), l1 = xdiv(e1, esum), l2 = xdiv(e2, esum);   // KN:123-125
+        const double znf = xadd(xadd(xmul(l0, a.z0), xmul(l1, a.z1)), xmul(l2, a.z2));  // KN:126
+        const double d = xmul(xadd(znf, 1.0), 0.5);                                   // KN:127
+        // sequential rule "if d < s: s = f32(d)" (KN:129-130) == running minimum in float32
+        // (monotone rounding): CAS loop keeps exact IEEE compare semantics.
+        float* p = depth + (long long)y * width + x;
+        const float fd = (float)d;
+        float cur = *(volatile float*)p;
+        while (d < (double)cur) {
+            const int assumed = __float_as_int(cur);
+            const int old = atomicCAS((int*)p, assumed, __float_as_int(fd));
+            if (old == assumed) break;
+            cur = __int_as_float(old);
+        }
+    }
+};
+
+template <typename T>
+struct TeaFn {
+    const T* tri_clip; TeaParams p;
+    void* data; uint8_t* mask; uint8_t* edited;
+    long long width, row0; uint32_t value; int esize;
+    struct Tri { double c0[4], c1[4], c2[4]; };
+    ML_DEV Tri setup(long long t, const TriSetup& s) const {
+        Tri r;
+        const T* c = tri_clip + 12 * t;
+        const int i1 = s.swapped ? 8 : 4, i2 = s.swapped ? 4 : 8;        // KN:40 swap attrs too
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            r.c0[k] = (double)c[k]; r.c1[k] = (double)c[i1 + k]; r.c2[k] = (double)c[i2 + k];
+        }
+        return r;
+    }
+    ML_DEV void fragment(const Tri& a, long long, int x, int y, double e0, double e1, double e2,
+                         long long& c0, long long& c1) const {
+        ++c1;                                                            // fragments, KN:158-161
+        if (!tea_fragment(p, e0, e1, e2, a.c0, a.c1, a.c2)) return;
+        const long long i = (y - row0) * width + x;
+        if (byte_set1_was0(edited, i)) ++c0;                             // KN:198-199, 202
+        store_value(data, esize, i, value);                              // KN:200
+        mask[i] = 1;                                                     // KN:201
+    }
+};
+
+// ------------------------------------------------------------------ pass A
+template <typename T, typename F>
+__global__ void __launch_bounds__(BLOCK)
+raster_warp_kernel(const T* __restrict__ tri_xy, long long ntri, long long width, long long height,
+                   long long row0, long long rows, F f, LargeList ll,
+                   unsigned long long* counters) {
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    long long c0 = 0, c1 = 0;
+    for (long long t = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); t < ntri; t += nwarps) {
+        TriSetup s;
+        if (!tri_load_ccw(tri_xy + 6 * t, s)) continue;
+        if (!tri_bbox(s, width, height, row0, rows)) continue;
+        const int bw = s.ix1 - s.ix0 + 1, bh = s.iy1 - s.iy0 + 1;
+        const long long n = (long long)bw * bh;
+        if (n > SMALL_MAX) {
+            if (lane == 0) {
+                unsigned long long k = atomicAdd(ll.count, 1ull);
+                ll.tri[k] = (int)t;
+                ll.off[k] = (unsigned long long)((n + CHUNK - 1) / CHUNK);
+            }
+            continue;
+        }
+        const typename F::Tri a = f.setup(t, s);
+        for (int j = lane; j < (int)n; j += 32) {
+            const int yy = j / bw, x = s.ix0 + (j - yy * bw), y = s.iy0 + yy;
+            double e0, e1, e2;
+            if (tri_inside(s, x, y, e0, e1, e2)) f.fragment(a, t, x, y, e0, e1, e2, c0, c1);
+        }
+    }
+    block_count_add(c0, counters);
+    block_count_add(c1, counters + 1);
+}
+
+// ------------------------------------------------------------------ pass B
+// In-place exclusive scan of off[0..count) by one block; writes off[count] = total as well.
+__global__ void __launch_bounds__(1024) scan_kernel(LargeList ll) {
+    __shared__ unsigned long long s_sum[1024];
+    const unsigned long long n = *ll.count;
+    const unsigned long long per = (n + 1023) / 1024;
+    const unsigned long long b = threadIdx.x * per, e = (b + per < n) ? b + per : n;
+    unsigned long long acc = 0;
+    for (unsigned long long i = b; i < e; ++i) acc += ll.off[i];
+    s_sum[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {                 // Hillis-Steele inclusive scan
+        unsigned long long v = (threadIdx.x >= o) ? s_sum[threadIdx.x - o] : 0;
+        __syncthreads();
+        s_sum[threadIdx.x] += v;
+        __syncthreads();
+    }
+    unsigned long long run = s_sum[threadIdx.x] - acc;   // exclusive prefix of this thread
+    for (unsigned long long i = b; i < e; ++i) { unsigned long long c = ll.off[i]; ll.off[i] = run; run += c; }
+    if (threadIdx.x == 1023) { ll.off[n] = s_sum[1023]; *ll.total = s_sum[1023]; }
+}
+
+// ------------------------------------------------------------------ pass C
+template <typename T, typename F>
+__global__ void __launch_bounds__(BLOCK)
+raster_chunk_kernel(const T* __restrict__ tri_xy, long long width, long long height,
+                    long long row0, long long rows, F f, LargeList ll,
+                    unsigned long long* counters) {
+    __shared__ long long s_k;
+    const unsigned long long total = *ll.total, nl = *ll.count;
+    long long c0 = 0, c1 = 0;
+    for (unsigned long long w = blockIdx.x; w < total; w += gridDim.x) {
+        if (threadIdx.x == 0) {                          // largest k with off[k] <= w
+            unsigned long long lo = 0, hi = nl;
+            while (hi - lo > 1) { unsigned long long mid = (lo + hi) >> 1; if (ll.off[mid] <= w) lo = mid; else hi = mid; }
+            s_k = (long long)lo;
+        }
+        __syncthreads();
+        const long long k = s_k;
+        __syncthreads();
+        const long long t = ll.tri[k];
+        TriSetup s;
+        tri_load_ccw(tri_xy + 6 * t, s);
+        tri_bbox(s, width, height, row0, rows);
+        const long long bw = s.ix1 - s.ix0 + 1, bh = s.iy1 - s.iy0 + 1, n = bw * bh;
+        const long long j0 = (long long)(w - ll.off[k]) * CHUNK;
+        const long long j1 = (j0 + CHUNK < n) ? j0 + CHUNK : n;
+        const typename F::Tri a = f.setup(t, s);
+        for (long long j = j0 + threadIdx.x; j < j1; j += BLOCK) {
+            const long long yy = j / bw;
+            const int x = s.ix0 + (int)(j - yy * bw), y = s.iy0 + (int)yy;
+            double e0, e1, e2;
+            if (tri_inside(s, x, y, e0, e1, e2)) f.fragment(a, t, x, y, e0, e1, e2, c0, c1);
+        }
+    }
+    block_count_add(c0, counters);
+    block_count_add(c1, counters + 1);
+}
+
+template <typename T, typename F>
+int raster_launch(const T* tri_xy, long long ntri, long long width, long long height,
+                  long long row0, long long rows, const F& f, void* workspace, size_t ws_bytes,
+                  unsigned long long* counters, cudaStream_t st) {
+    if (ntri <= 0 || rows <= 0 || width <= 0) return ML_OK;
+    if (ntri > 0x7fffffffLL) return ml_fail(ML_ERR_ARG, "more than 2^31-1 triangles");
+    if (ws_bytes < ml_raster_workspace_bytes(ntri)) return ml_fail(ML_ERR_ARG, "raster workspace too small");
+    // workspace layout: [count, total, c0, c1] u64 | off[ntri+1] u64 | tri[ntri] i32
+    unsigned long long* head = (unsigned long long*)workspace;
+    LargeList ll;
+    ll.count = head; ll.total = head + 1;
+    ll.off = head + 4;
+    ll.tri = (int*)(ll.off + ntri + 1);
+    unsigned long long* ctr = counters ? counters : head + 2;
+    ML_CUDA(cudaMemsetAsync(head, 0, 4 * sizeof(unsigned long long), st));
+    const long long warps_per_block = BLOCK / 32;
+    long long blocks = (ntri + warps_per_block - 1) / warps_per_block;
+    const long long cap = (long long)ml_sm_count() * 64;
+    if (blocks > cap) blocks = cap;
+    raster_warp_kernel<T, F><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr);
+    scan_kernel<<<1, 1024, 0, st>>>(ll);
+    raster_chunk_kernel<T, F><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, width, height, row0, rows, f, ll, ctr);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ml_raster_workspace_bytes(int64_t ntri) {
+    if (ntri < 0) ntri = 0;
+    return 4 * sizeof(unsigned long long) + (size_t)(ntri + 1) * sizeof(unsigned long long) +
+           (size_t)ntri * sizeof(int) + 64;
+}
+
+int ml_coverage_fill(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
+                     int64_t row0, int64_t rows, uint8_t* out, uint64_t* written,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    CoverageFn f{out, width, row0};
+    unsigned long long* ctr = (unsigned long long*)written;
+    if (tri_dtype == ML_F32)
+        return raster_launch((const float*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
+    if (tri_dtype == ML_F64)
+        return raster_launch((const double*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
+    return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+}
+
+int ml_raster_tri_id(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
+                     int64_t row0, int64_t rows, int32_t* tri_id, uint64_t* counters,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (rows > 0 && width > 0)
+        ML_CUDA(cudaMemsetAsync(tri_id, 0xff, (size_t)rows * width * sizeof(int32_t), st));   // -1
+    TriIdFn f{tri_id, width, row0};
+    unsigned long long* ctr = (unsigned long long*)counters;
+    if (tri_dtype == ML_F32)
+        return raster_launch((const float*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
+    if (tri_dtype == ML_F64)
+        return raster_launch((const double*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
+    return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+}
+
+int ml_raster_depth(const void* tri_xy, const void* tri_zn, int tri_dtype, int64_t ntri,
+                    float* depth, int64_t width, int64_t height,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (tri_dtype == ML_F32) {
+        DepthFn<float> f{(const float*)tri_zn, depth, width};
+        return raster_launch((const float*)tri_xy, ntri, width, height, 0, height, f, workspace, workspace_bytes, nullptr, st);
+    }
+    if (tri_dtype == ML_F64) {
+        DepthFn<double> f{(const double*)tri_zn, depth, width};
+        return raster_launch((const double*)tri_xy, ntri, width, height, 0, height, f, workspace, workspace_bytes, nullptr, st);
+    }
+    return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+}
+
+int ml_raster_tea(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
+                  int64_t width, int64_t height, int64_t row0, int64_t rows,
+                  const ml_tea_params* tp, void* data, int esize, uint32_t value_bits,
+                  uint8_t* mask, uint8_t* edited, uint64_t* counters,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
+    TeaParams p = ml_make_tea_params(tp);
+    unsigned long long* ctr = (unsigned long long*)counters;
+    if (tri_dtype == ML_F32) {
+        TeaFn<float> f{(const float*)tri_clip, p, data, mask, edited, width, row0, value_bits, esize};
+        return raster_launch((const float*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
+    }
+    if (tri_dtype == ML_F64) {
+        TeaFn<double> f{(const double*)tri_clip, p, data, mask, edited, width, row0, value_bits, esize};
+        return raster_launch((const double*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
+    }
+    return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+}
+
+}  // extern "C"

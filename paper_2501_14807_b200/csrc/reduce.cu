@@ -1,0 +1,277 @@
+// Per-layer area / statistics reductions (north star (4)).  No reference code beyond
+// mesh_surface_area and the precision metric; the frozen
+// definitions are oracle/kn_port.c ext_layer_area / ext_label_area / ext_layer_stats.
+//
+// ml_layer_area: one pass reads the float32 area plane once plus G <= 8 mask planes per launch
+// group (4 + G B/texel), accumulates in float64 registers, reduces with warp shuffles and issues
+// ONE float64 atomic per block per layer.
+#include "common.cuh"
+#include "meshlayers_b200.h"
+#include "internal.h"
+
+namespace {
+
+constexpr int BLOCK = 256;
+constexpr int MAX_G = 8;
+
+struct AreaArgs {
+    const uint8_t* mask[MAX_G];
+    double* sums;              // [G] slice of the caller's array
+    unsigned long long* counts;
+};
+
+ML_DEV void block_sum_atomic(double v, double* out) {
+    __shared__ double s_part[BLOCK / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) s_part[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = lane < BLOCK / 32 ? s_part[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0 && t != 0.0) atomicAdd(out, t);
+    }
+    __syncthreads();
+}
+
+// 16 texels per thread step: four 128-bit area loads + one 128-bit load per mask plane.
+template <int G, bool VECTOR>
+__global__ void __launch_bounds__(BLOCK)
+area_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
+    double acc[G];
+    long long cnt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) { acc[g] = 0.0; cnt[g] = 0; }
+    const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    long long done = 0;
+    if (VECTOR) {
+        const long long nv = n >> 4;
+        for (long long v = tid; v < nv; v += nthreads) {
+            float4 ar[4];
+            uint4 m[G];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ar[j] = ld_stream((const float4*)area + v * 4 + j);
+#pragma unroll
+            for (int g = 0; g < G; ++g) m[g] = ld_stream((const uint4*)a.mask[g] + v);
+            double d[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                d[4 * j] = (double)ar[j].x; d[4 * j + 1] = (double)ar[j].y;
+                d[4 * j + 2] = (double)ar[j].z; d[4 * j + 3] = (double)ar[j].w;
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const uint32_t w[4] = {m[g].x, m[g].y, m[g].z, m[g].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t ff = __vcmpne4(w[j], 0u);
+                    cnt[g] += __popc(ff) >> 3;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (ff & (0xffu << (8 * e))) acc[g] = xadd(acc[g], d[4 * j + e]);
+                }
+            }
+        }
+        done = nv << 4;
+    }
+    for (long long i = done + tid; i < n; i += nthreads) {
+        const double d = (double)area[i];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+            if (a.mask[g][i] != 0) { acc[g] = xadd(acc[g], d); ++cnt[g]; }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        block_sum_atomic(acc[g], a.sums + g);
+        if (a.counts) block_count_add(cnt[g], a.counts + g);
+    }
+}
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+template <int G>
+int launch_area(const float* area, const AreaArgs& a, long long n, cudaStream_t st) {
+    bool vec = aligned16(area);
+    for (int g = 0; g < G; ++g) vec = vec && aligned16(a.mask[g]);
+    const long long items = vec ? ((n + 15) >> 4) : n;
+    long long blocks = (items + BLOCK - 1) / BLOCK;
+    const long long cap = (long long)ml_sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    if (vec) area_kernel<G, true><<<(unsigned)blocks, BLOCK, 0, st>>>(area, a, n);
+    else area_kernel<G, false><<<(unsigned)blocks, BLOCK, 0, st>>>(area, a, n);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// area per label of a uint8 plane: per-block shared-memory bins, run-length aggregation per
+// thread (labels are spatially coherent), one global atomic per non-empty bin per block.
+__global__ void __launch_bounds__(BLOCK)
+label_area_kernel(const float* __restrict__ area, const uint8_t* __restrict__ data,
+                  const uint8_t* __restrict__ mask, long long n, double* sums, unsigned long long* counts) {
+    __shared__ double s_sum[256];
+    __shared__ unsigned long long s_cnt[256];
+    for (int v = threadIdx.x; v < 256; v += BLOCK) { s_sum[v] = 0.0; s_cnt[v] = 0; }
+    __syncthreads();
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    const long long per = 16;
+    const long long nchunks = (n + per - 1) / per;
+    for (long long c = (long long)blockIdx.x * BLOCK + threadIdx.x; c < nchunks; c += nthreads) {
+        const long long b = c * per, e = (b + per < n) ? b + per : n;
+        int run = -1; double rs = 0.0; unsigned long long rc = 0;
+        for (long long i = b; i < e; ++i) {
+            if (mask[i] == 0) continue;
+            const int v = data[i];
+            if (v != run) {
+                if (rc) { atomicAdd(&s_sum[run], rs); atomicAdd(&s_cnt[run], rc); }
+                run = v; rs = 0.0; rc = 0;
+            }
+            rs = xadd(rs, (double)area[i]); ++rc;
+        }
+        if (rc) { atomicAdd(&s_sum[run], rs); atomicAdd(&s_cnt[run], rc); }
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < 256; v += BLOCK)
+        if (s_cnt[v]) { atomicAdd(sums + v, s_sum[v]); atomicAdd(counts + v, s_cnt[v]); }
+}
+
+// ---------------------------------------------------------------------------------------------
+template <typename T> ML_DEV double widen(T v) { return (double)v; }
+struct HalfBits { uint16_t b; };
+template <> ML_DEV double widen<HalfBits>(HalfBits v) {
+    // IEEE binary16 -> float64 without <cuda_fp16.h> conversions (exact)
+    const uint32_t sign = (uint32_t)(v.b >> 15) << 31, ex = (v.b >> 10) & 31u, man = v.b & 1023u;
+    uint32_t bits;
+    if (ex == 0) {
+        if (man == 0) bits = sign;
+        else {
+            int sh = 0; uint32_t m = man;
+            while (!(m & 1024u)) { m <<= 1; ++sh; }
+            bits = sign | ((uint32_t)(113 - sh) << 23) | ((m & 1023u) << 13);
+        }
+    } else if (ex == 31) bits = sign | 0x7f800000u | (man << 13);
+    else bits = sign | ((ex + 112u) << 23) | (man << 13);
+    return (double)__uint_as_float(bits);
+}
+
+ML_DEV void atomic_min_double(double* p, double v) {
+    unsigned long long* a = (unsigned long long*)p;
+    unsigned long long old = *a;
+    while (v < __longlong_as_double((long long)old)) {
+        const unsigned long long assumed = old;
+        old = atomicCAS(a, assumed, (unsigned long long)__double_as_longlong(v));
+        if (old == assumed) break;
+    }
+}
+ML_DEV void atomic_max_double(double* p, double v) {
+    unsigned long long* a = (unsigned long long*)p;
+    unsigned long long old = *a;
+    while (v > __longlong_as_double((long long)old)) {
+        const unsigned long long assumed = old;
+        old = atomicCAS(a, assumed, (unsigned long long)__double_as_longlong(v));
+        if (old == assumed) break;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(BLOCK)
+stats_kernel(const T* __restrict__ attr, const uint8_t* __restrict__ mask, long long n, double* out) {
+    __shared__ double s_mn[BLOCK / 32], s_mx[BLOCK / 32];
+    double sum = 0.0, mn = INFINITY, mx = -INFINITY;
+    long long cnt = 0;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    for (long long i = (long long)blockIdx.x * BLOCK + threadIdx.x; i < n; i += nthreads) {
+        if (mask[i] == 0) continue;
+        const double v = widen(attr[i]);
+        sum = xadd(sum, v); ++cnt;
+        if (v < mn) mn = v;
+        if (v > mx) mx = v;
+    }
+    // count is accumulated as a double: exact below 2^53 texels
+    block_sum_atomic((double)cnt, out);
+    block_sum_atomic(sum, out + 1);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) { s_mn[wid] = mn; s_mx[wid] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < BLOCK / 32; ++w) { mn = fmin(mn, s_mn[w]); mx = fmax(mx, s_mx[w]); }
+        atomic_min_double(out + 2, mn);
+        atomic_max_double(out + 3, mx);
+    }
+}
+
+template <typename T>
+int launch_stats(const void* attr, const uint8_t* mask, long long n, double* out, cudaStream_t st) {
+    long long blocks = (n + BLOCK - 1) / BLOCK;
+    const long long cap = (long long)ml_sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    stats_kernel<T><<<(unsigned)blocks, BLOCK, 0, st>>>((const T*)attr, mask, n, out);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ml_layer_area(const float* area, const uint8_t* const* masks, int64_t L, int64_t n,
+                  double* sums, uint64_t* counts, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (L < 0 || L > 64) return ml_fail(ML_ERR_ARG, "layer count must be 0..64");
+    if (n <= 0) return ML_OK;
+    for (int64_t l0 = 0; l0 < L; ) {
+        const int64_t left = L - l0;
+        const int g = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
+        AreaArgs a;
+        for (int k = 0; k < MAX_G; ++k) a.mask[k] = k < g ? masks[l0 + k] : nullptr;
+        a.sums = sums + l0;
+        a.counts = counts ? (unsigned long long*)counts + l0 : nullptr;
+        int rc;
+        switch (g) {
+        case 8: rc = launch_area<8>(area, a, n, st); break;
+        case 4: rc = launch_area<4>(area, a, n, st); break;
+        case 2: rc = launch_area<2>(area, a, n, st); break;
+        default: rc = launch_area<1>(area, a, n, st); break;
+        }
+        if (rc != ML_OK) return rc;
+        l0 += g;
+    }
+    return ML_OK;
+}
+
+int ml_label_area(const float* area, const uint8_t* data, const uint8_t* mask, int64_t n,
+                  double* sums, uint64_t* counts, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) return ML_OK;
+    long long blocks = ((n + 15) / 16 + BLOCK - 1) / BLOCK;
+    const long long cap = (long long)ml_sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    label_area_kernel<<<(unsigned)blocks, BLOCK, 0, st>>>(area, data, mask, n, sums, (unsigned long long*)counts);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_layer_stats(const void* attr, int attr_kind, const uint8_t* mask, int64_t n,
+                   double* out, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) return ML_OK;
+    switch (attr_kind) {
+    case ML_U8:  return launch_stats<uint8_t>(attr, mask, n, out, st);
+    case ML_I8:  return launch_stats<int8_t>(attr, mask, n, out, st);
+    case ML_I16: return launch_stats<int16_t>(attr, mask, n, out, st);
+    case ML_I32: return launch_stats<int32_t>(attr, mask, n, out, st);
+    case ML_U32: return launch_stats<uint32_t>(attr, mask, n, out, st);
+    case ML_F16: return launch_stats<HalfBits>(attr, mask, n, out, st);
+    case ML_FLOAT32: return launch_stats<float>(attr, mask, n, out, st);
+    }
+    return ml_fail(ML_ERR_ARG, "unknown attribute kind");
+}
+
+}  // extern "C"

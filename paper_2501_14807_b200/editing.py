@@ -1,0 +1,204 @@
+"""editing -- the stroke pipeline: TEA (``apply_stroke``), TPA
+(``build_outline_mask`` / ``apply_padding``), the projection formulas, and the north-star
+selection brushes (``select_sphere``, ``select_sphere_batch``, ``select_threshold``).
+
+Per stroke the host sends only scalars (the reference's "64 bytes"); planes, the
+surface map and the depth map stay resident in HBM.
+"""
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .errors import DegenerateCamera, LayerMeshMismatch, StaleDepth, TargetMismatch
+
+TRANSFER_BYTES_PER_STROKE = 64
+DEFAULT_DEPTH_BIAS = 1e-4
+
+
+@dataclass
+class EditingTool:
+    """SPEC.md:237-240."""
+    px: float
+    py: float
+    shape: object                      # (T_h, T_w) bool/uint8 plane, numpy or CUDA tensor
+    value: object = 1
+    padding_radius: int = 1
+
+    def __post_init__(self):
+        if self.shape.ndim != 2 or self.shape.shape[0] < 1 or self.shape.shape[1] < 1:
+            raise TargetMismatch("tool shape plane must be a non-empty 2-D plane")
+        if self.padding_radius < 0:
+            raise TargetMismatch("padding radius must be >= 0")
+
+    @property
+    def size(self):
+        return int(self.shape.shape[1]), int(self.shape.shape[0])       # (T_w, T_h)
+
+
+@dataclass
+class EditProjection:
+    """S_f, T_f and the kernel's tool map s = sfx*xn + bx, t = sfy*yn + by."""
+    scale: tuple
+    translate: tuple
+
+    @property
+    def kernel_factors(self):
+        # window x = (xn+1)/2*W ; s = (x - (T_px - T_w/2))/T_w = S_f.x*xn + (0.5 - T_f.x)
+        return self.scale[0], self.scale[1], 0.5 - self.translate[0], 0.5 - self.translate[1]
+
+
+def compute_tool_projection(camera, tool):
+    """SPEC.md:259-267 / PAPER.md:160-171:
+    S_f = (W_w/(2 T_w), W_h/(2 T_h)),  T_f = ((T_px - 0.5 W_w)/T_w, (T_py - 0.5 W_h)/T_h)."""
+    tw, th = tool.size
+    ww, wh = float(camera.width), float(camera.height)
+    if ww < 1 or wh < 1 or tw < 1 or th < 1:
+        raise DegenerateCamera("window and tool sizes must be >= 1")
+    return EditProjection(scale=(ww / (2.0 * tw), wh / (2.0 * th)),
+                          translate=((tool.px - 0.5 * ww) / tw, (tool.py - 0.5 * wh) / th))
+
+
+def project_fragment(s, t, w):
+    """reject w <= 0, divide, reject outside the closed [0,1]^2 (KN:174, 189)."""
+    if not w > 0.0:
+        return None
+    u, v = s / w, t / w
+    if not (0.0 <= u <= 1.0 and 0.0 <= v <= 1.0):
+        return None
+    return u, v
+
+
+@dataclass
+class EditResult:
+    """SPEC.md:245-247.  Counts stay on the device until read (no sync on the stroke path)."""
+    edited_mask: object
+    _counts: object = None
+    padded: int = 0
+    duration_ms: float = 0.0
+    transfer_bytes: int = TRANSFER_BYTES_PER_STROKE
+    _cache: dict = field(default_factory=dict)
+
+    def _read(self):
+        if "c" not in self._cache:
+            self._cache["c"] = [int(v) for v in self._counts.tolist()]
+        return self._cache["c"]
+
+    @property
+    def edited_count(self):
+        return self._read()[0]
+
+    @property
+    def fragments(self):
+        c = self._read()
+        return c[1] if len(c) > 1 else None
+
+    def edited_indices(self):
+        return self.edited_mask.view(_native._torch().uint8).flatten().nonzero().flatten()
+
+
+class StrokeContext:
+    """Everything TEA needs that changes only with the camera or the mesh: device triangle uv
+    (grid units), clip coordinates MVP*vertex per triangle, the depth map, the surface map and a
+    per-stroke ``edited`` plane (SPEC.md:253-255 EditedAreaMask, reset before each stroke)."""
+
+    def __init__(self, mesh, camera, depth, surface, device="cuda"):
+        torch = _native.require_cuda()
+        self.mesh, self.camera, self.depth, self.surface = mesh, camera, depth, surface
+        clip = camera.clip_coords(mesh.vertices)[mesh.triangles]            # (T,3,4) float64
+        self.tri_clip = torch.from_numpy(np.ascontiguousarray(clip)).to(device)
+        self.tri_xy = surface.tri_xy
+        self.edited = torch.zeros((surface.rows, surface.width), dtype=torch.uint8, device=device)
+        self.device = device
+
+
+def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False):
+    """SPEC.md:277-285 TEA.  Uses the per-texel kernel over the cached triangle-id map when the uv
+    layout has no overlaps (bit-identical), else the direct per-triangle kernel."""
+    torch = _native._torch()
+    if ctx.depth.generation != ctx.camera.generation:
+        raise StaleDepth("depth map was rendered for camera generation %d, camera is at %d"
+                         % (ctx.depth.generation, ctx.camera.generation))
+    s = ctx.surface
+    if layer.shape != (s.rows, s.width):
+        raise TargetMismatch("layer is %s, surface map slab is %s" % (layer.shape, (s.rows, s.width)))
+    if s.covered == 0 and s.row0 == 0 and s.rows == s.height:
+        raise LayerMeshMismatch("no uv coverage at layer resolution")
+    sfx, sfy, bx, by = compute_tool_projection(ctx.camera, tool).kernel_factors
+    ctx.edited.zero_()
+    counts = torch.zeros(2, dtype=torch.int64, device=ctx.device)
+    shape = tool.shape if _native._is_cuda_tensor(tool.shape) else _native._as_dev_bytes(tool.shape, ctx.device)
+    args = (float(ctx.camera.width), float(ctx.camera.height), ctx.depth.plane, eps, sfx, sfy, bx, by,
+            shape, layer.data, layer.mask, ctx.edited, tool.value)
+    if s.overlap == 0 and not force_direct:
+        _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts)
+    else:
+        _native.raster_tea(ctx.tri_xy, ctx.tri_clip, *args, height=s.height, row0=s.row0, counts=counts)
+    return EditResult(edited_mask=ctx.edited, _counts=counts)
+
+
+# --------------------------------------------------------------------------------------------
+# north-star selection brushes
+
+def select_sphere(surface, layer, center, radius, value, edited=None):
+    """Sphere brush: every covered texel whose surface point lies within ``radius`` of ``center``
+    gets data = value, mask = true (definition: oracle ext_select_sphere)."""
+    torch = _native._torch()
+    if layer.shape != (surface.rows, surface.width):
+        raise TargetMismatch("layer does not match the surface map")
+    if edited is None:
+        edited = torch.zeros(layer.shape, dtype=torch.uint8, device=surface.pos.device)
+    counts = torch.zeros(1, dtype=torch.int64, device=surface.pos.device)
+    _native.select_sphere(surface.pos, center, radius, layer.data, layer.mask, edited, value, counts=counts)
+    return EditResult(edited_mask=edited, _counts=counts, transfer_bytes=40)
+
+
+def select_sphere_batch(surface, batch):
+    """K strokes over L layers in one pass (``batch`` = _native.StrokeBatch after upload)."""
+    _native.select_sphere_batch(surface.pos, batch)
+    return batch.counts
+
+
+def select_threshold(attr, valid, lo, hi, layer, value, edited=None):
+    """Attribute-threshold selection into ``layer`` (definition: oracle ext_select_threshold)."""
+    torch = _native._torch()
+    if tuple(attr.shape) != layer.shape:
+        raise TargetMismatch("attribute plane does not match the layer")
+    if edited is None:
+        edited = torch.zeros(layer.shape, dtype=torch.uint8, device=attr.device)
+    counts = torch.zeros(1, dtype=torch.int64, device=attr.device)
+    _native.select_threshold(attr, valid, lo, hi, layer.data, layer.mask, edited, value, counts=counts)
+    return EditResult(edited_mask=edited, _counts=counts, transfer_bytes=24)
+
+
+# --------------------------------------------------------------------------------------------
+# TPA
+
+def build_outline_mask(mesh_or_coverage, resolution=None, thickness=1, device="cuda"):
+    """(1) uv_coverage, (2) uncovered texels within Chebyshev distance
+    ``thickness`` of a covered one."""
+    torch = _native._torch()
+    if thickness < 1:
+        raise TargetMismatch("outline thickness must be >= 1")
+    if _native._is_cuda_tensor(mesh_or_coverage):
+        cov = mesh_or_coverage
+    else:
+        from .mesh_core import uv_coverage
+        cov = uv_coverage(mesh_or_coverage, resolution, device=device)
+    return _native.outline_mask(cov.view(torch.uint8) if cov.dtype == torch.bool else cov, thickness).view(torch.bool)
+
+
+def apply_padding(layer, outline, edited, tool_or_value, radius=None):
+    """outline texels within ``radius`` (Chebyshev) of an edited texel receive
+    the stroke value.  Returns the padded texel count."""
+    torch = _native._torch()
+    value = tool_or_value.value if isinstance(tool_or_value, EditingTool) else tool_or_value
+    if radius is None:
+        radius = tool_or_value.padding_radius if isinstance(tool_or_value, EditingTool) else 1
+    if tuple(outline.shape) != layer.shape or tuple(edited.shape) != layer.shape:
+        raise TargetMismatch("grids must share the layer resolution")
+    if radius <= 0:
+        return 0
+    as_u8 = lambda t: t.view(torch.uint8) if t.dtype == torch.bool else t
+    return _native.apply_padding(as_u8(outline), as_u8(edited), radius, layer.data, layer.mask, value)

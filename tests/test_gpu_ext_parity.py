@@ -1,0 +1,318 @@
+"""GPU parity of the north-star operations (surface map, sphere / threshold selection, layer
+algebra, areas, outline / padding) against their frozen definitions in oracle/kn_port.c.
+Integer / byte planes bit-exact; float32 maps bit-exact (tighter than the 1e-5 the north star
+asks); areas within 1e-10 relative (north star: 1e-6)."""
+import numpy as np
+import pytest
+
+import helpers
+from oracle import kn
+from paper_2501_14807_b200 import _native as nat
+from paper_2501_14807_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    import torch
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        return torch.from_numpy(a.view(np.int32)).cuda().view(torch.uint32)
+    return torch.from_numpy(a).cuda()
+
+
+def _host(t):
+    import torch
+    if t.dtype == torch.uint32:
+        return t.view(torch.int32).cpu().numpy().view(np.uint32)
+    return t.cpu().numpy()
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def _mesh_arrays(mesh, w, h):
+    return mesh.tri_uv_texels(w, h), mesh.tri_pos(), mesh.tri_nrm()
+
+
+@pytest.fixture(scope="module")
+def sphere_map():
+    """Icosphere level 3 (1,280 triangles) in a 256^2 chart-grid atlas: oracle + GPU surface maps."""
+    mesh = synth.icosphere_mesh(3)
+    w = h = 256
+    xy, P, N = _mesh_arrays(mesh, w, h)
+    ref = kn.surface_map(xy, P, N, w, h)
+    got = nat.surface_map(xy, P, N, w, h)
+    return mesh, ref, got
+
+
+def test_surface_map_bit_exact(sphere_map):
+    _, ref, got = sphere_map
+    assert got["covered"] == ref["covered"] and got["overlap"] == ref["overlap"] == 0
+    assert np.array_equal(got["tri_id"].cpu().numpy(), ref["tri_id"])
+    for k in ("pos", "nrm", "area"):
+        assert np.array_equal(_bits(got[k].cpu().numpy()), _bits(ref[k])), k
+    # uncovered texels: NaN position, zero normal / area
+    unc = ref["tri_id"] < 0
+    assert np.isnan(got["pos"].cpu().numpy()[:, unc]).all()
+
+
+def test_surface_map_overlap_soup_and_f32_inputs():
+    rng = np.random.default_rng(9)
+    w, h = 150, 90
+    xy = synth.random_soup(rng, 300, float(w)).astype(np.float32)
+    P = rng.normal(size=(300, 3, 3)).astype(np.float32)
+    N = rng.normal(size=(300, 3, 3)).astype(np.float32)
+    ref = kn.surface_map(xy, P, N, w, h)
+    got = nat.surface_map(xy, P, N, w, h)
+    assert got["overlap"] == ref["overlap"] > 0 and got["covered"] == ref["covered"]
+    assert np.array_equal(got["tri_id"].cpu().numpy(), ref["tri_id"])
+    for k in ("pos", "nrm", "area"):
+        assert np.array_equal(_bits(got[k].cpu().numpy()), _bits(ref[k])), k
+
+
+def test_surface_map_area_anchors():
+    """a 1 m^2 flat square fully covering a 64^2 atlas -> every texel carries
+    1/64^2 m^2, the layer area of a full mask is the mesh area, precision = area / texels."""
+    import torch
+    from paper_2501_14807_b200 import TriangleMesh, mesh_surface_area
+    mesh = TriangleMesh(vertices=np.array([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], float),
+                        normals=np.array([[0, 0, 1]] * 4, float),
+                        uvs=np.array([[0, 0], [1, 0], [1, 1], [0, 1]], float),
+                        triangles=np.array([[0, 1, 2], [0, 2, 3]]))
+    assert mesh_surface_area(mesh) == 1.0
+    got = nat.surface_map(*_mesh_arrays(mesh, 64, 64), 64, 64)
+    assert got["covered"] == 4096
+    full = torch.ones((64, 64), dtype=torch.uint8, device="cuda")
+    sums, counts = nat.layer_area(got["area"], [full])
+    assert counts[0] == 4096 and abs(sums[0] - 1.0) < 1e-9
+    assert abs(sums[0] / counts[0] * 1e4 - 1e4 / 64 ** 2) < 1e-9        # cm^2 per texel
+
+
+def test_surface_map_row_slabs(sphere_map):
+    mesh, ref, _ = sphere_map
+    xy, P, N = _mesh_arrays(mesh, 256, 256)
+    parts = [nat.surface_map(xy, P, N, 256, 256, row0=r0, rows=r1 - r0) for r0, r1 in ((0, 100), (100, 101), (101, 256))]
+    assert sum(p["covered"] for p in parts) == ref["covered"]
+    assert np.array_equal(np.concatenate([p["tri_id"].cpu().numpy() for p in parts]), ref["tri_id"])
+    pos = np.concatenate([p["pos"].cpu().numpy() for p in parts], axis=1)
+    assert np.array_equal(_bits(pos), _bits(ref["pos"]))
+
+
+@pytest.mark.parametrize("kind,value", [(np.uint8, 9), (np.int16, -5), (np.uint32, 77777), (np.float32, 0.5)])
+def test_select_sphere_bit_exact(sphere_map, kind, value):
+    _, ref, got = sphere_map
+    rng = np.random.default_rng(3)
+    for center, radius in (((0.0, 0.0, 1.0), 0.25), ((0.6, -0.5, 0.3), 0.6), ((5.0, 5.0, 5.0), 0.1), ((0, 0, 0), 2.0)):
+        data0 = rng.integers(0, 4, size=(256, 256)).astype(kind)
+        mask0 = rng.random((256, 256)) < 0.2
+        ed0 = (rng.random((256, 256)) < 0.1).astype(np.uint8)
+        rd, rm, re = data0.copy(), mask0.copy(), ed0.copy()
+        want = kn.select_sphere(ref["pos"], center, radius, rd, rm, re, value)
+        d, m, e = _dev(data0), _dev(mask0), _dev(ed0)
+        assert nat.select_sphere(got["pos"], center, radius, d, m, e, value) == want
+        assert np.array_equal(_bits(_host(d)), _bits(rd))
+        assert np.array_equal(m.cpu().numpy(), rm) and np.array_equal(e.cpu().numpy(), re)
+
+
+def test_select_sphere_unaligned_and_tail():
+    """n not a multiple of 4 and planes at odd offsets take the scalar path."""
+    import torch
+    rng = np.random.default_rng(4)
+    n_rows, w = 7, 37
+    pos = rng.normal(size=(3, n_rows, w)).astype(np.float32)
+    pos[:, rng.random((n_rows, w)) < 0.2] = np.nan
+    rd = np.zeros((n_rows, w), np.uint8); rm = np.zeros((n_rows, w), bool); re = np.zeros((n_rows, w), np.uint8)
+    want = kn.select_sphere(pos, (0.1, 0.2, -0.1), 0.9, rd, rm, re, 3)
+    d = torch.zeros((n_rows, w), dtype=torch.uint8, device="cuda")
+    m = torch.zeros((n_rows, w), dtype=torch.bool, device="cuda")
+    e = torch.zeros((n_rows, w), dtype=torch.uint8, device="cuda")
+    assert nat.select_sphere(_dev(pos), (0.1, 0.2, -0.1), 0.9, d, m, e, 3) == want
+    assert np.array_equal(d.cpu().numpy(), rd) and np.array_equal(m.cpu().numpy(), rm)
+
+
+@pytest.mark.parametrize("nlayers,K", [(1, 40), (5, 64), (70, 150)])
+def test_select_sphere_batch_equals_sequential(sphere_map, nlayers, K):
+    """K strokes in one pass == K successive single strokes (later strokes overwrite)."""
+    import torch
+    mesh, ref, got = sphere_map
+    strokes, labels = synth.sphere_strokes(mesh, K, seed=11 + K, rmin_frac=0.02, rmax_frac=0.2)
+    layer_of = (np.arange(K) * 7) % nlayers
+    datas = [np.zeros((256, 256), np.uint8) for _ in range(nlayers)]
+    masks = [np.zeros((256, 256), bool) for _ in range(nlayers)]
+    eds = [np.zeros((256, 256), np.uint8) for _ in range(nlayers)]
+    want = np.zeros(nlayers, np.int64)
+    for k in range(K):
+        L = layer_of[k]
+        want[L] += kn.select_sphere(ref["pos"], strokes[k, :3], strokes[k, 3], datas[L], masks[L], eds[L], labels[k])
+    mk = lambda dt: [torch.zeros((256, 256), dtype=dt, device="cuda") for _ in range(nlayers)]
+    gd, gm, ge = mk(torch.uint8), mk(torch.bool), mk(torch.uint8)
+    batch = nat.StrokeBatch(gd, gm, ge, "cuda").upload(strokes, layer_of, labels)
+    nat.select_sphere_batch(got["pos"], batch)
+    assert np.array_equal(batch.counts.cpu().numpy(), want)
+    for L in range(nlayers):
+        assert np.array_equal(gd[L].cpu().numpy(), datas[L]), L
+        assert np.array_equal(gm[L].cpu().numpy(), masks[L]) and np.array_equal(ge[L].cpu().numpy(), eds[L])
+
+
+@pytest.mark.parametrize("akind", [np.float32, np.float16, np.uint8, np.int8, np.int16, np.int32, np.uint32])
+def test_select_threshold_bit_exact(akind):
+    rng = np.random.default_rng(6)
+    h, w = 61, 83                                             # odd sizes: vector body + scalar tail
+    if np.issubdtype(akind, np.floating):
+        attr = rng.normal(size=(h, w)).astype(akind)
+        attr[rng.random((h, w)) < 0.05] = np.nan
+        lo, hi = -0.3, 0.7
+    else:
+        info = np.iinfo(akind)
+        attr = rng.integers(max(info.min, -1000), min(info.max, 1000) + 1, size=(h, w)).astype(akind)
+        lo, hi = 3.0, 90.0
+    for valid in (None, (rng.random((h, w)) < 0.7).astype(np.uint8)):
+        rd = np.zeros((h, w), np.int16); rm = np.zeros((h, w), bool); re = np.zeros((h, w), np.uint8)
+        want = kn.select_threshold(attr, valid, lo, hi, rd, rm, re, -2)
+        d, m, e = _dev(rd * 0), _dev(rm & False), _dev(re * 0)
+        got = nat.select_threshold(_dev(attr), None if valid is None else _dev(valid), lo, hi, d, m, e, -2)
+        assert got == want
+        assert np.array_equal(d.cpu().numpy(), rd) and np.array_equal(m.cpu().numpy(), rm)
+        assert np.array_equal(e.cpu().numpy(), re)
+
+
+@pytest.mark.parametrize("kind", [None, np.uint8, np.int16, np.float32, np.uint32])
+@pytest.mark.parametrize("op", ["union", "intersection", "difference", "masking"])
+def test_layer_op_bit_exact(kind, op):
+    rng = np.random.default_rng(8)
+    n = 16 * 1000 + 13                                        # vector body + tail
+    ma = (rng.random(n) < 0.4).astype(np.uint8) * rng.integers(1, 255, n).astype(np.uint8)   # any non-zero = true
+    mb = (rng.random(n) < 0.5).astype(np.uint8)
+    da = db = None
+    if kind is not None:
+        da = rng.integers(0, 100, n).astype(kind)
+        db = rng.integers(0, 100, n).astype(kind)
+    rc = None if kind is None else np.empty(n, kind)
+    rmc = np.empty(n, np.uint8)
+    kn.layer_op(op, da, ma, db, mb, rc, rmc)
+    gd = None if kind is None else _dev(np.zeros(n, kind))
+    gm = _dev(np.zeros(n, np.uint8))
+    nat.layer_op(op, None if kind is None else _dev(da), _dev(ma),
+                 None if (kind is None or op == "masking") else _dev(db), _dev(mb), gd, gm)
+    assert np.array_equal(gm.cpu().numpy(), rmc)
+    if kind is not None:
+        assert np.array_equal(_bits(_host(gd)), _bits(rc))
+    # in place: output aliases A
+    if kind is not None:
+        a_d, a_m = _dev(da), _dev(ma)
+        nat.layer_op(op, a_d, a_m, _dev(db), _dev(mb), a_d, a_m)
+        assert np.array_equal(_bits(_host(a_d)), _bits(rc)) and np.array_equal(a_m.cpu().numpy(), rmc)
+
+
+@pytest.mark.parametrize("kind", [None, np.uint8, np.uint32])
+def test_layer_chain_equals_sequential_ops(kind):
+    """C3 chain ((L0 u L1) n L2) \\ L3 ... over 8 layers, fused vs step-by-step oracle."""
+    rng = np.random.default_rng(10)
+    n = 16 * 700 + 5
+    N = 8
+    ops = ["union", "intersection", "difference", "union", "masking", "difference", "union"]
+    masks = [(rng.random(n) < 0.45).astype(np.uint8) for _ in range(N)]
+    datas = [None] * N if kind is None else [rng.integers(1, 200, n).astype(kind) for _ in range(N)]
+    cd = None if kind is None else datas[0].copy()
+    cm = masks[0].copy()
+    if kind is not None:
+        cd[cm == 0] = 0
+        cm = (cm != 0).astype(np.uint8)
+    for j in range(1, N):
+        nd = None if kind is None else np.empty(n, kind)
+        nm = np.empty(n, np.uint8)
+        kn.layer_op(ops[j - 1], cd, cm, datas[j], masks[j], nd, nm)
+        cd, cm = nd, nm
+    gd = None if kind is None else _dev(np.zeros(n, kind))
+    gm = _dev(np.zeros(n, np.uint8))
+    nat.layer_chain(None if kind is None else [_dev(d) for d in datas], [_dev(m) for m in masks], [None] + ops, gd, gm)
+    assert np.array_equal(gm.cpu().numpy(), cm)
+    if kind is not None:
+        assert np.array_equal(_bits(_host(gd)), _bits(cd))
+
+
+@pytest.mark.parametrize("L", [1, 3, 8, 13, 64])
+def test_layer_area_matches_oracle(sphere_map, L):
+    _, ref, got = sphere_map
+    rng = np.random.default_rng(12 + L)
+    masks = [(rng.random((256, 256)) < rng.uniform(0.05, 0.9)).astype(np.uint8) for _ in range(L)]
+    sums, counts = nat.layer_area(got["area"], [_dev(m) for m in masks])
+    for l in range(L):
+        a, c = kn.layer_area(ref["area"], masks[l])
+        assert counts[l] == c
+        assert abs(sums[l] - a) <= 1e-10 * max(abs(a), 1e-300)
+
+
+def test_sphere_area_close_to_analytic(sphere_map):
+    """Whole-atlas area of the unit icosphere ~= mesh area (texel sampling error only)."""
+    mesh, ref, got = sphere_map
+    from paper_2501_14807_b200 import mesh_surface_area
+    full = (ref["tri_id"] >= 0).astype(np.uint8)
+    sums, _ = nat.layer_area(got["area"], [_dev(full)])
+    assert abs(sums[0] - mesh_surface_area(mesh)) / mesh_surface_area(mesh) < 0.05
+    assert abs(kn.mesh_surface_area(mesh.tri_pos()) - mesh_surface_area(mesh)) < 1e-12
+
+
+def test_label_area_and_stats(sphere_map):
+    _, ref, got = sphere_map
+    rng = np.random.default_rng(14)
+    data = np.repeat(np.repeat(rng.integers(0, 256, size=(32, 32)), 8, 0), 8, 1).astype(np.uint8)
+    mask = (rng.random((256, 256)) < 0.8).astype(np.uint8)
+    want_s, want_c = kn.label_area(ref["area"], data, mask)
+    s, c = nat.label_area(got["area"], _dev(data), _dev(mask))
+    assert np.array_equal(c, want_c)
+    assert np.allclose(s, want_s, rtol=1e-10, atol=0)
+    for akind in (np.float32, np.int16, np.uint8, np.float16):
+        attr = (rng.normal(size=(256, 256)) * 50).astype(akind)
+        wc, ws, wmn, wmx = kn.layer_stats(attr, mask)
+        gc, gs, gmn, gmx = nat.layer_stats(_dev(attr), _dev(mask))
+        assert (gc, gmn, gmx) == (wc, wmn, wmx) and abs(gs - ws) <= 1e-9 * max(1.0, abs(ws))
+
+
+def test_outline_and_padding_known_answers():
+    """10x10 island in 64x64, thickness 1 -> 44 outline texels."""
+    import torch
+    cov = np.zeros((64, 64), np.uint8)
+    cov[20:30, 30:40] = 1
+    out = nat.outline_mask(_dev(cov), 1)
+    assert int(out.sum().item()) == 44 and np.array_equal(out.cpu().numpy(), kn.outline(cov, 1))
+    assert int(nat.outline_mask(_dev(np.ones((64, 64), np.uint8)), 1).sum().item()) == 0
+    assert int(nat.outline_mask(_dev(np.zeros((64, 64), np.uint8)), 1).sum().item()) == 0
+    edited = np.zeros((64, 64), np.uint8)
+    edited[29, 35] = 1                                       # adjacent to the island border
+    data = torch.zeros((64, 64), dtype=torch.int16, device="cuda")
+    mask = torch.zeros((64, 64), dtype=torch.bool, device="cuda")
+    n = nat.apply_padding(out, _dev(edited), 1, data, mask, 42)
+    rd = np.zeros((64, 64), np.int16); rm = np.zeros((64, 64), bool)
+    assert n == kn.padding(kn.outline(cov, 1), edited, 1, rd, rm, 42) == 3
+    assert np.array_equal(data.cpu().numpy(), rd) and np.array_equal(mask.cpu().numpy(), rm)
+    assert nat.apply_padding(out, _dev(edited), 0, data, mask, 42) == 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("r", [1, 2, 5])
+def test_outline_and_padding_random(seed, r):
+    """randomized island layouts, padded set == outline within Chebyshev r of edited."""
+    import torch
+    rng = np.random.default_rng(100 + seed)
+    h, w = 64 + seed, 70 + 3 * seed
+    cov = (rng.random((h, w)) < 0.03).astype(np.uint8)
+    cov = (kn.outline(cov, 2) | cov).astype(np.uint8)        # blobby islands
+    ref_out = kn.outline(cov, r)
+    got_out = nat.outline_mask(_dev(cov), r)
+    assert np.array_equal(got_out.cpu().numpy(), ref_out)
+    assert not (ref_out & cov).any()
+    edited = ((rng.random((h, w)) < 0.05) & (cov != 0)).astype(np.uint8)
+    rd = np.zeros((h, w), np.uint8); rm = np.zeros((h, w), bool)
+    want = kn.padding(ref_out, edited, r, rd, rm, 9)
+    d = torch.zeros((h, w), dtype=torch.uint8, device="cuda"); m = torch.zeros((h, w), dtype=torch.bool, device="cuda")
+    assert nat.apply_padding(got_out, _dev(edited), r, d, m, 9) == want
+    assert np.array_equal(d.cpu().numpy(), rd) and np.array_equal(m.cpu().numpy(), rm)
+    # row slabs with halo == full
+    parts = []
+    for r0, r1 in ((0, 20), (20, h)):
+        i0, i1 = max(0, r0 - r), min(h, r1 + r)
+        parts.append(nat.outline_mask(_dev(cov[i0:i1]), r, in_row0=i0, out_row0=r0, out_rows=r1 - r0).cpu().numpy())
+    assert np.array_equal(np.concatenate(parts), ref_out)

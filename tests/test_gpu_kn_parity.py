@@ -1,0 +1,234 @@
+"""GPU parity of the three reference kernels (coverage_fill / raster_depth / raster_tea) called
+through the C ABI: against the reference's own outputs (golden fixtures) and against the oracle
+on random scenes.  Bit-exact for every plane; counts exact where the reference's are order-free."""
+import numpy as np
+import pytest
+
+import helpers
+from oracle import kn
+from paper_2501_14807_b200 import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _plane_dev(a):
+    import torch
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        return torch.from_numpy(a.view(np.int32)).cuda().view(torch.uint32)
+    return torch.from_numpy(a).cuda()
+
+
+def _host(t):
+    import torch
+    if t.dtype == torch.uint32:
+        return t.view(torch.int32).cpu().numpy().view(np.uint32)
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------ golden fixtures
+
+@pytest.mark.parametrize("name", helpers.golden_names("coverage_"))
+@pytest.mark.parametrize("path", ["host", "device"])
+def test_coverage_golden(name, path):
+    g = helpers.golden(name)
+    w, h = int(g["width"]), int(g["height"])
+    if path == "host":
+        out = g["out0"].copy()
+        written = nat.coverage_fill(g["tri_xy"], w, h, out)
+    else:
+        d = _dev(g["out0"])
+        written = nat.coverage_fill(_dev(g["tri_xy"]), w, h, d)
+        out = d.cpu().numpy()
+    assert np.array_equal(out, g["out"])
+    assert written == int(g["written"])
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("depth_"))
+@pytest.mark.parametrize("path", ["host", "device"])
+def test_depth_golden(name, path):
+    g = helpers.golden(name)
+    if path == "host":
+        depth = g["depth0"].copy()
+        nat.raster_depth(g["tri_xy"], g["tri_zn"], depth)
+    else:
+        d = _dev(g["depth0"])
+        nat.raster_depth(_dev(g["tri_xy"]), _dev(g["tri_zn"]), d)
+        depth = d.cpu().numpy()
+    assert np.array_equal(depth.view(np.uint32), g["depth"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("tea_rand_"))
+@pytest.mark.parametrize("path", ["host", "device"])
+def test_tea_random_golden(name, path):
+    g = helpers.golden(name)
+    args = (float(g["ww"]), float(g["wh"]), g["depth"], helpers.eps_of(g), float(g["sfx"]), float(g["sfy"]),
+            float(g["bx"]), float(g["by"]), g["shape"])
+    if path == "host":
+        data, mask, edited = g["data0"].copy(), g["mask0"].copy(), g["edited0"].copy()
+        ec, fr = nat.raster_tea(g["tri_xy"], g["tri_clip"], *args, data, mask, edited, g["value"][()])
+    else:
+        d, m, e = _plane_dev(g["data0"]), _dev(g["mask0"]), _dev(g["edited0"])
+        ec, fr = nat.raster_tea(_dev(g["tri_xy"]), _dev(g["tri_clip"]), *args, d, m, e, g["value"][()])
+        data, mask, edited = _host(d), m.cpu().numpy(), e.cpu().numpy()
+    assert (ec, fr) == (int(g["edited_count"]), int(g["fragments"]))
+    assert np.array_equal(data.view(np.uint8), g["data"].view(np.uint8))
+    assert np.array_equal(mask, g["mask"])
+    assert np.array_equal(edited, g["edited"])
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("tea_scene_"))
+def test_tea_scene_golden_direct_and_cached(name):
+    """Reference outputs reproduced by BOTH TEA kernels (direct per-triangle, and per-texel over
+    the cached triangle-id map) on a real camera / mesh / atlas scene."""
+    import torch
+    g = helpers.golden(name)
+    s = helpers.tea_scene_inputs(g["level"], g["atlas"], g["window"], g["tool_r"], g["tool_xy"])
+    A, W = int(g["atlas"]), int(g["window"])
+    depth = torch.ones((W, W), dtype=torch.float32, device="cuda")
+    nat.raster_depth(_dev(s["win_xy"]), _dev(s["win_zn"]), depth)
+    assert np.array_equal(depth.cpu().numpy().view(np.uint32), g["depth"].view(np.uint32))
+    tri_xy, tri_clip = _dev(s["tri_xy"]), _dev(s["tri_clip"])
+    tri_id, frags, overlap = nat.raster_tri_id(tri_xy, A, A)
+    assert overlap == 0 and frags == int(g["cov_count"])
+    for cached in (False, True):
+        data = torch.zeros((A, A), dtype=torch.uint8, device="cuda")
+        mask = torch.zeros((A, A), dtype=torch.bool, device="cuda")
+        edited = torch.zeros((A, A), dtype=torch.bool, device="cuda")
+        args = (float(W), float(W), depth, helpers.eps_of(g), s["sfx"], s["sfy"], s["bx"], s["by"], s["shape"],
+                data, mask, edited, 7)
+        ec, fr = nat.tea_texels(tri_xy, tri_clip, tri_id, *args) if cached else nat.raster_tea(tri_xy, tri_clip, *args)
+        assert (ec, fr) == (int(g["edited_count"]), int(g["fragments"]))
+        assert np.array_equal(np.packbits(mask.cpu().numpy()), g["mask"])
+        assert np.array_equal(np.packbits(edited.cpu().numpy()), g["edited"])
+        d = data.cpu().numpy()
+        assert np.array_equal(np.packbits(d != 0), g["data"]) and set(np.unique(d)) <= {0, 7}
+
+
+def test_eps_promotion_mode_golden():
+    g = helpers.golden("epsmode")
+    got = []
+    for e in (float(g["eps"]), np.float64(g["eps"])):
+        data, mask, edited = np.zeros((4, 4), np.uint8), np.zeros((4, 4), bool), np.zeros((4, 4), bool)
+        depth = np.full((4, 4), g["depth_value"], np.float32)
+        got.append(nat.raster_tea(g["tri_xy"], g["tri_clip"], 4.0, 4.0, depth, e, 0.5, 0.5, 0.5, 0.5,
+                                  np.ones((1, 1), np.uint8), data, mask, edited, 1)[0])
+    assert got == [int(g["edited_weak"]), int(g["edited_f64"])]
+
+
+# ------------------------------------------------------------------ random scenes vs the oracle
+
+@pytest.mark.parametrize("seed", range(8))
+def test_coverage_random_vs_oracle(seed):
+    from paper_2501_14807_b200 import synth
+    rng = np.random.default_rng(1000 + seed)
+    w, h = int(rng.integers(20, 200)), int(rng.integers(20, 200))
+    tri = synth.random_soup(rng, 400, float(max(w, h)), dtype=np.float32 if seed % 2 else np.float64)
+    ref = np.zeros((h, w), np.uint8)
+    want = kn.coverage_fill(tri, w, h, ref)
+    out = _dev(np.zeros((h, w), np.uint8))
+    got = nat.coverage_fill(_dev(tri), w, h, out)
+    assert got == want and np.array_equal(out.cpu().numpy(), ref)
+    # permutation invariance on the GPU path
+    out2 = _dev(np.zeros((h, w), np.uint8))
+    assert nat.coverage_fill(_dev(tri[rng.permutation(len(tri))]), w, h, out2) == want
+    assert np.array_equal(out2.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_depth_random_vs_oracle(seed):
+    from paper_2501_14807_b200 import synth
+    rng = np.random.default_rng(2000 + seed)
+    w, h = int(rng.integers(20, 150)), int(rng.integers(20, 150))
+    tri = synth.random_soup(rng, 500, float(max(w, h)))
+    zn = rng.uniform(-1.5, 1.2, size=(500, 3))
+    ref = np.ones((h, w), np.float32)
+    kn.raster_depth(tri, zn, ref)
+    d = _dev(np.ones((h, w), np.float32))
+    changed = nat.raster_depth(_dev(tri), _dev(zn), d)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    assert changed == int((ref != 1.0).sum())
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_tea_random_vs_oracle(seed):
+    """SPEC.md:605 acceptance #1 scale: >= 20 random scenes, all plane kinds."""
+    kinds = [(np.uint8, 200), (np.int8, -7), (np.int16, 3000), (np.int32, -123456), (np.uint32, 3123456789),
+             (np.float16, 1.5), (np.float32, -0.25)]
+    dt, val = kinds[seed % len(kinds)]
+    c = helpers.random_tea_case(3000 + seed, ntri=300 + 30 * seed, w=96, h=128, plane_dtype=dt, value=val,
+                                tri_dtype=np.float32 if seed % 3 == 0 else np.float64,
+                                eps=np.float64(1e-4) if seed % 4 == 1 else 1e-4)
+    rd, rm, re = c["data"].copy(), c["mask"].copy(), c["edited"].copy()
+    want = kn.raster_tea(*helpers.tea_args(c), rd, rm, re, val)
+    d, m, e = _plane_dev(c["data"]), _dev(c["mask"]), _dev(c["edited"])
+    got = nat.raster_tea(_dev(c["tri_xy"]), _dev(c["tri_clip"]), *helpers.tea_args(c)[2:], d, m, e, val)
+    assert got == want
+    assert np.array_equal(_host(d).view(np.uint8), rd.view(np.uint8))
+    assert np.array_equal(m.cpu().numpy(), rm) and np.array_equal(e.cpu().numpy(), re)
+
+
+def test_tea_idempotent():
+    c = helpers.random_tea_case(77, ntri=200, w=64, h=64)
+    d, m, e = _plane_dev(c["data"]), _dev(c["mask"]), _dev(np.zeros((64, 64), np.uint8))
+    a = (_dev(c["tri_xy"]), _dev(c["tri_clip"])) + helpers.tea_args(c)[2:]
+    first = nat.raster_tea(*a, d, m, e, 9)
+    snap = (d.clone(), m.clone(), e.clone())
+    second = nat.raster_tea(*a, d, m, e, 9)
+    assert second == (0, first[1])
+    assert all(bool((x == y).all()) for x, y in zip(snap, (d, m, e)))
+
+
+def test_large_and_small_triangles_mix():
+    """Exercises all three raster passes: warp-per-triangle, the scan, and block chunks for
+    triangles far larger than SMALL_MAX texels (incl. two that tile the whole plane)."""
+    rng = np.random.default_rng(5)
+    w = h = 700
+    big = np.array([[[0, 0], [w, 0], [w, h]], [[0, 0], [w, h], [0, h]]], dtype=np.float64)
+    mid = rng.uniform(0, w, size=(40, 3, 2))
+    small = rng.uniform(0, w, size=(3000, 1, 2)) + rng.normal(size=(3000, 3, 2)) * 2.0
+    tri = np.concatenate([small[:1500], mid, big, small[1500:]])
+    ref = np.zeros((h, w), np.uint8)
+    want = kn.coverage_fill(tri, w, h, ref, threads=4)
+    out = _dev(np.zeros((h, w), np.uint8))
+    assert nat.coverage_fill(_dev(tri), w, h, out) == want == w * h
+    assert np.array_equal(out.cpu().numpy(), ref)
+    zn = rng.uniform(-1, 1, size=(len(tri), 3))
+    dref = np.ones((h, w), np.float32)
+    kn.raster_depth(tri, zn, dref, threads=4)
+    d = _dev(np.ones((h, w), np.float32))
+    nat.raster_depth(_dev(tri), _dev(zn), d)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), dref.view(np.uint32))
+
+
+def test_row_slabs_concatenate_to_full_plane():
+    """Row sharding (SURVEY.md 4 'distributed testing without a cluster'): logical slabs on one
+    GPU concatenate to the unsharded result bit-for-bit; counts add up."""
+    c = helpers.random_tea_case(91, ntri=400, w=80, h=120)
+    rd, rm, re = c["data"].copy(), c["mask"].copy(), c["edited"].copy()
+    want = kn.raster_tea(*helpers.tea_args(c), rd, rm, re, 5)
+    tri, clip = _dev(c["tri_xy"]), _dev(c["tri_clip"])
+    ec = fr = 0
+    parts = []
+    for r0, r1 in ((0, 37), (37, 38), (38, 120)):
+        d, m, e = _plane_dev(c["data"][r0:r1]), _dev(c["mask"][r0:r1]), _dev(c["edited"][r0:r1])
+        a, b = nat.raster_tea(tri, clip, *helpers.tea_args(c)[2:], d, m, e, 5, height=120, row0=r0)
+        ec, fr = ec + a, fr + b
+        parts.append((d.cpu().numpy(), m.cpu().numpy(), e.cpu().numpy()))
+    assert (ec, fr) == want
+    for k, ref in enumerate((rd, rm, re)):
+        assert np.array_equal(np.concatenate([p[k] for p in parts]), ref)
+
+
+def test_empty_and_degenerate_inputs():
+    import torch
+    out = torch.zeros((8, 8), dtype=torch.uint8, device="cuda")
+    assert nat.coverage_fill(_dev(np.zeros((0, 3, 2))), 8, 8, out) == 0
+    deg = np.array([[[1.0, 1.0], [5.0, 5.0], [3.0, 3.0]], [[np.nan, 0, ], [1, 1], [2, 0]]])
+    assert nat.coverage_fill(_dev(deg), 8, 8, out) == 0 and not bool(out.any())
+    assert nat.coverage_fill(np.zeros((0, 3, 2)), 8, 8, np.zeros((8, 8), np.uint8)) == 0

@@ -1,0 +1,151 @@
+"""Pin the oracle (oracle/kn_port.c) against the reference's own outputs (tests/golden/*.npz,
+made by tests/golden/make_golden.py from /root/reference) and the SPEC known-answer tests.
+CPU only."""
+import numpy as np
+import pytest
+
+import helpers
+from oracle import kn
+
+
+# ------------------------------------------------------------------ golden vectors (reference outputs)
+
+@pytest.mark.parametrize("name", helpers.golden_names("coverage_"))
+@pytest.mark.parametrize("threads", [0, 3])
+def test_coverage_matches_reference(name, threads):
+    g = helpers.golden(name)
+    out = g["out0"].copy()
+    written = kn.coverage_fill(g["tri_xy"], int(g["width"]), int(g["height"]), out, threads=threads)
+    assert np.array_equal(out, g["out"])
+    assert written == int(g["written"])
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("depth_"))
+@pytest.mark.parametrize("threads", [0, 3])
+def test_depth_matches_reference(name, threads):
+    g = helpers.golden(name)
+    depth = g["depth0"].copy()
+    kn.raster_depth(g["tri_xy"], g["tri_zn"], depth, threads=threads)
+    assert np.array_equal(depth.view(np.uint32), g["depth"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("tea_rand_"))
+@pytest.mark.parametrize("threads", [0, 3])
+def test_tea_random_matches_reference(name, threads):
+    g = helpers.golden(name)
+    data, mask, edited = g["data0"].copy(), g["mask0"].copy(), g["edited0"].copy()
+    ec, fr = kn.raster_tea(g["tri_xy"], g["tri_clip"], float(g["ww"]), float(g["wh"]), g["depth"],
+                           helpers.eps_of(g), float(g["sfx"]), float(g["sfy"]), float(g["bx"]), float(g["by"]),
+                           g["shape"], data, mask, edited, g["value"][()], threads=threads)
+    assert (ec, fr) == (int(g["edited_count"]), int(g["fragments"]))
+    assert np.array_equal(data.view(np.uint8), g["data"].view(np.uint8))
+    assert np.array_equal(mask, g["mask"])
+    assert np.array_equal(edited, g["edited"])
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("tea_scene_"))
+def test_tea_scene_matches_reference(name):
+    g = helpers.golden(name)
+    s = helpers.tea_scene_inputs(g["level"], g["atlas"], g["window"], g["tool_r"], g["tool_xy"])
+    A, W = int(g["atlas"]), int(g["window"])
+    depth = np.ones((W, W), np.float32)
+    kn.raster_depth(s["win_xy"], s["win_zn"], depth)
+    assert np.array_equal(depth.view(np.uint32), g["depth"].view(np.uint32))
+    data = np.zeros((A, A), np.uint8)
+    mask = np.zeros((A, A), bool)
+    edited = np.zeros((A, A), bool)
+    ec, fr = kn.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, helpers.eps_of(g),
+                           s["sfx"], s["sfy"], s["bx"], s["by"], s["shape"], data, mask, edited, 7)
+    assert (ec, fr) == (int(g["edited_count"]), int(g["fragments"]))
+    assert np.array_equal(np.packbits(mask), g["mask"])
+    assert np.array_equal(np.packbits(edited), g["edited"])
+    assert np.array_equal(np.packbits(data != 0), g["data"])
+    assert set(np.unique(data)) <= {0, 7}
+    cov = np.zeros((A, A), np.uint8)
+    assert kn.coverage_fill(s["tri_xy"], A, A, cov) == int(g["cov_count"])
+
+
+def _epsmode_counts(fn):
+    g = helpers.golden("epsmode")
+    res = []
+    for e in (float(g["eps"]), np.float64(g["eps"])):
+        data, mask, edited = np.zeros((4, 4), np.uint8), np.zeros((4, 4), bool), np.zeros((4, 4), bool)
+        depth = np.full((4, 4), g["depth_value"], np.float32)
+        res.append(fn(g["tri_xy"], g["tri_clip"], 4.0, 4.0, depth, e, 0.5, 0.5, 0.5, 0.5,
+                      np.ones((1, 1), np.uint8), data, mask, edited, 1)[0])
+    return res, [int(g["edited_weak"]), int(g["edited_f64"])]
+
+
+def test_eps_promotion_mode_matches_reference():
+    """KN:185: float32(depth)+eps is rounded to float32 for a Python-float eps but stays float64
+    for a np.float64 eps; the fixture holds what the reference returned in both modes."""
+    got, want = _epsmode_counts(kn.raster_tea)
+    assert got == want == [0, 16]
+
+
+# ------------------------------------------------------------------ SPEC known answers
+
+def _square(x0, y0, s):
+    return np.array([[[x0, y0], [x0 + s, y0], [x0 + s, y0 + s]],
+                     [[x0, y0], [x0 + s, y0 + s], [x0, y0 + s]]], dtype=np.float64)
+
+
+def test_spec_10x10_square_covers_100_cells():
+    out = np.zeros((64, 64), np.uint8)
+    assert kn.coverage_fill(_square(20.0, 30.0, 10.0), 64, 64, out) == 100
+    assert out[30:40, 20:30].all() and out.sum() == 100
+
+
+def test_spec_coverage_winding_and_permutation_invariant():
+    tri = _square(20.0, 30.0, 10.0)
+    ref = np.zeros((64, 64), np.uint8)
+    kn.coverage_fill(tri, 64, 64, ref)
+    for perm in ([0, 2, 1], [1, 2, 0], [2, 1, 0]):
+        out = np.zeros((64, 64), np.uint8)
+        assert kn.coverage_fill(tri[::-1, perm], 64, 64, out) == 100
+        assert np.array_equal(out, ref)
+
+
+def test_spec_two_triangles_tile_unit_square():
+    out = np.zeros((64, 64), np.uint8)
+    assert kn.coverage_fill(_square(0.0, 0.0, 64.0), 64, 64, out) == 4096
+
+
+def test_spec_triangle_covering_three_centres():
+    tri = np.array([[[1.2, 1.2], [3.4, 1.2], [1.2, 3.4]]])
+    out = np.zeros((6, 6), np.uint8)
+    kn.coverage_fill(tri, 6, 6, out)
+    ys, xs = np.nonzero(out)
+    assert sorted(zip(xs.tolist(), ys.tolist())) == [(1, 1), (1, 2), (2, 1)]
+
+
+def test_spec_watertight_quad_split():                     # SPEC.md:141; KN:13-15
+    quad = _square(2.5, 2.5, 8.0)                          # diagonal passes through texel centres
+    a = np.zeros((16, 16), np.uint8)
+    b = np.zeros((16, 16), np.uint8)
+    na = kn.coverage_fill(quad[:1], 16, 16, a)
+    nb = kn.coverage_fill(quad[1:], 16, 16, b)
+    assert not (a & b).any()                               # no texel owned twice
+    both = np.zeros((16, 16), np.uint8)
+    assert kn.coverage_fill(quad, 16, 16, both) == na + nb == 64   # no gap along the diagonal
+
+
+def test_spec_zero_area_triangle_skipped():                # KN:11-12, 36-37
+    tri = np.array([[[1.0, 1.0], [5.0, 5.0], [3.0, 3.0]]])
+    out = np.zeros((8, 8), np.uint8)
+    assert kn.coverage_fill(tri, 8, 8, out) == 0 and not out.any()
+
+
+def test_spec_full_viewport_triangle_depth_half():
+    tri = np.array([[[-100.0, -100.0], [300.0, -100.0], [-100.0, 300.0]]])
+    depth = np.ones((32, 48), np.float32)
+    kn.raster_depth(tri, np.zeros((1, 3)), depth)
+    assert np.unique(depth).tolist() == [0.5]
+
+
+def test_empty_inputs():                                   # KN: loops simply do not execute
+    out = np.zeros((4, 4), np.uint8)
+    assert kn.coverage_fill(np.zeros((0, 3, 2)), 4, 4, out) == 0
+    depth = np.ones((4, 4), np.float32)
+    assert kn.raster_depth(np.zeros((0, 3, 2)), np.zeros((0, 3)), depth) == 0
+    assert (depth == 1.0).all()
