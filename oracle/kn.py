@@ -166,6 +166,29 @@ def raster_tea(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
     return int(ec.value), int(fr.value)
 
 
+def raster_tea_slab(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
+                    shape, data, mask, edited, value, height, row0, threads):
+    """raster_tea restricted to rows [row0, row0+rows) of a `height`-row atlas; the planes are
+    slab-local (rows, width).  For CPU-baseline timing on a bounded sample of a big atlas."""
+    tri = _f64(tri_xy, (3, 2))
+    clip = _f64(tri_clip, (3, 4))
+    depth = np.ascontiguousarray(depth, dtype=np.float32)
+    shape = np.ascontiguousarray(shape)
+    rows, w = mask.shape
+    th, tw = shape.shape
+    dh, dw = depth.shape
+    val = _value_bytes(value, data.dtype)
+    ec, fr = C.c_int64(0), C.c_int64(0)
+    f = lib().kn_raster_tea_slab
+    f.restype = None
+    f.argtypes = lib().kn_raster_tea.argtypes[:-2] + [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]
+    f(_p(tri), _p(clip), tri.shape[0], float(ww), float(wh), _p(depth), dw, dh, float(eps),
+      int(eps_is_f32(eps)), float(sfx), float(sfy), float(bx), float(by), _p(shape), tw, th,
+      _p(_plane(data)), data.dtype.itemsize, _p(val), _p(_plane(mask)), _p(_plane(edited)), w, height,
+      row0, row0 + rows, C.addressof(ec), C.addressof(fr), threads)
+    return int(ec.value), int(fr.value)
+
+
 # ------------------------------------------------------------------ extension definitions
 
 def surface_map(tri_xy, tri_pos, tri_nrm, width, height, rows=None):

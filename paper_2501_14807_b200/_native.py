@@ -511,9 +511,27 @@ class StrokeBatch:
         v = np.asarray(values).astype(dt).reshape(K)
         vals[:] = v.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[dt.itemsize])
         self.K = K
-        self.d_strokes = torch.from_numpy(strokes).to(self.device, non_blocking=True)
-        self.d_layer_of = torch.from_numpy(np.ascontiguousarray(layer_of, dtype=np.int32)).to(self.device, non_blocking=True)
-        self.d_values = torch.from_numpy(vals.view(np.int32)).to(self.device, non_blocking=True)
+        # stage through pinned host memory (one buffer per record array, grown on demand) so the
+        # host->device copies are asynchronous DMA transfers
+        cap = getattr(self, "_cap", 0)
+        if K > cap:
+            self._cap = max(K, 2 * cap)
+            self._pin = (torch.empty((self._cap, 4), dtype=torch.float64).pin_memory(),
+                         torch.empty(self._cap, dtype=torch.int32).pin_memory(),
+                         torch.empty(self._cap, dtype=torch.int32).pin_memory())
+            self._dev = tuple(torch.empty_like(p, device=self.device) for p in self._pin)
+        if getattr(self, "_ev", None) is not None:
+            self._ev.synchronize()            # the previous upload must have left the pinned buffers
+        ps, pl, pv = self._pin
+        ps[:K].copy_(torch.from_numpy(strokes))
+        pl[:K].copy_(torch.from_numpy(np.ascontiguousarray(layer_of, dtype=np.int32)))
+        pv[:K].copy_(torch.from_numpy(vals.view(np.int32)))
+        for p, d in zip(self._pin, self._dev):
+            d[:K].copy_(p[:K], non_blocking=True)
+        self._ev = torch.cuda.Event()
+        self._ev.record()
+        self.d_strokes, self.d_layer_of, self.d_values = (d[:K] for d in self._dev)
+        self.upload_bytes = K * (32 + 4 + 4)
         return self
 
 

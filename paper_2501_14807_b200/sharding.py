@@ -1,0 +1,131 @@
+"""Row sharding of the atlas across the GPUs of one node.
+
+Every hot kernel is independent per texel, so rank r owns the row slab [row0, row0+rows) of every
+plane (surface map and all layers) and no data-path collective exists.  The only exchanges are
+  * ``broadcast_strokes``: rank 0's stroke records (a few dozen bytes each; the paper's "64 bytes
+    per stroke") -> all ranks, one broadcast per batch, and
+  * ``allreduce_areas`` : per-layer partial area sums (float64) and texel counts (int64), one
+    all-reduce for all layers.
+Both are latency-bound scalars over NCCL/NVLink; with world_size == 1 they are no-ops.  The
+stencil ops (outline / padding) need ``radius`` halo rows from the neighbouring slabs:
+``exchange_halo`` does that with two point-to-point copies.
+
+One process per GPU (torchrun); the same code runs on CPU tensors with the gloo backend, which
+is how the host logic is tested without GPUs.
+"""
+import numpy as np
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def world():
+    """(rank, world_size) of the default process group, (0, 1) when not initialised."""
+    dist = _dist()
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def shard_rows(height, world_size, rank):
+    """Contiguous, balanced row slab of rank ``rank``: returns (row0, rows).  Slabs tile
+    [0, height) exactly; the first ``height % world_size`` ranks get one extra row."""
+    if world_size < 1 or not 0 <= rank < world_size:
+        raise ValueError("bad rank / world size")
+    base, extra = divmod(int(height), int(world_size))
+    row0 = rank * base + min(rank, extra)
+    return row0, base + (1 if rank < extra else 0)
+
+
+def all_slabs(height, world_size):
+    return [shard_rows(height, world_size, r) for r in range(world_size)]
+
+
+def broadcast_strokes(strokes, layer_of, values, device, src=0):
+    """Rank ``src`` supplies numpy arrays (strokes (K,4) f64, layer_of (K,) i32, values (K,) u32
+    bit patterns); every rank returns the same three numpy arrays.  One broadcast of a packed
+    (K,6) float64 tensor; K is broadcast first so receivers can size the buffer."""
+    import torch
+    dist = _dist()
+    rank, ws = world()
+    if ws == 1:
+        return strokes, layer_of, values
+    k = torch.zeros(1, dtype=torch.int64, device=device)
+    if rank == src:
+        k[0] = len(strokes)
+    dist.broadcast(k, src=src)
+    K = int(k.item())
+    buf = torch.zeros((K, 6), dtype=torch.float64, device=device)
+    if rank == src:
+        packed = np.zeros((K, 6), dtype=np.float64)
+        packed[:, :4] = strokes
+        packed[:, 4] = layer_of
+        packed[:, 5] = values            # uint32 bit patterns are exact in float64
+        buf.copy_(torch.from_numpy(packed))
+    dist.broadcast(buf, src=src)
+    out = buf.cpu().numpy()
+    return (np.ascontiguousarray(out[:, :4]), out[:, 4].astype(np.int32), out[:, 5].astype(np.uint32))
+
+
+def allreduce_areas(sums, counts=None):
+    """Sum per-layer partial areas (float64 tensor) and counts (int64 tensor) over all ranks, in
+    place.  One collective: counts ride along as exact float64 (< 2^53 texels)."""
+    import torch
+    dist = _dist()
+    _, ws = world()
+    if ws == 1:
+        return sums, counts
+    if counts is None:
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+        return sums, None
+    packed = torch.cat([sums, counts.to(torch.float64)])
+    dist.all_reduce(packed, op=dist.ReduceOp.SUM)
+    n = sums.numel()
+    sums.copy_(packed[:n])
+    counts.copy_(packed[n:].round().to(torch.int64))
+    return sums, counts
+
+
+def allreduce_counts(counts):
+    """Sum int64 edit counters over ranks, in place."""
+    dist = _dist()
+    _, ws = world()
+    if ws > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    return counts
+
+
+def halo_bounds(row0, rows, height, radius):
+    """Rows a rank needs for a radius-``radius`` stencil: (in_row0, in_rows) clipped to the atlas."""
+    lo = max(0, row0 - radius)
+    hi = min(height, row0 + rows + radius)
+    return lo, hi - lo
+
+
+def exchange_halo(plane, row0, height, radius):
+    """Return the rank's slab of a byte plane extended by up to ``radius`` rows from each
+    neighbour, plus the global row index of its first row.  Neighbour rows travel point-to-point
+    (isend/irecv); interior-only when world_size == 1."""
+    import torch
+    dist = _dist()
+    rank, ws = world()
+    rows = plane.shape[0]
+    if ws == 1 or radius <= 0:
+        return plane, row0
+    up_n = min(radius, row0)                                   # rows needed from rank-1 (above = lower rows)
+    dn_n = min(radius, height - (row0 + rows))
+    reqs, up, dn = [], None, None
+    if rank > 0:
+        up = torch.empty((up_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=plane.device)
+        reqs.append(dist.irecv(up, src=rank - 1))
+        reqs.append(dist.isend(plane[:min(radius, rows)].contiguous(), dst=rank - 1))
+    if rank < ws - 1:
+        dn = torch.empty((dn_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=plane.device)
+        reqs.append(dist.irecv(dn, src=rank + 1))
+        reqs.append(dist.isend(plane[max(0, rows - radius):].contiguous(), dst=rank + 1))
+    for r in reqs:
+        r.wait()
+    parts = [p for p in (up, plane, dn) if p is not None]
+    return torch.cat(parts, dim=0), row0 - (up.shape[0] if up is not None else 0)
