@@ -73,8 +73,9 @@ def lib():
                                 u32, vp, vp, vp, vp, sz, vp]),
         "ml_raster_tri_id": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
         "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
-        "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, C.POINTER(_TeaParams), vp, i32,
+        "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, i32,
                                 u32, vp, vp, vp, vp]),
+        "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp]),
         "ml_select_sphere": (i32, [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
         "ml_select_sphere_batch": (i32, [vp, i64, i64, vp, vp, vp, i64, vp, vp, vp, i64, i32, vp, vp]),
         "ml_select_threshold": (i32, [vp, i32, vp, i64, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
@@ -101,7 +102,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve", "ml_tea_texels",
-    "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
+    "ml_tea_classify", "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
 
@@ -430,9 +431,12 @@ def raster_tri_id(tri_xy, width, height, *, row0=0, rows=None, device=None):
 
 
 def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
-               shape, data, mask, edited, value, *, row0=0, counts=None):
+               shape, data, mask, edited, value, *, row0=0, counts=None, classify=True):
     """TEA over the cached triangle-id map (SURVEY.md 8 note N1): same planes and counts as
-    ``raster_tea`` when the uv layout has no overlaps.  Returns (edited_texels, fragments)."""
+    ``raster_tea`` when the uv layout has no overlaps.  Returns (edited_texels, fragments).
+    ``classify`` runs the per-stroke triangle pre-pass (ml_tea_classify) so that texels of
+    triangles outside the tool footprint skip the float64 evaluation; results are identical
+    either way."""
     torch = require_cuda()
     rows, w = mask.shape
     dev = mask.device
@@ -450,9 +454,13 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
     p = _tea_params(ww, wh, depth, eps, sfx, sfy, bx, by, shape)
     bits, esize = value_bits(value, data)
     ctr = counts if counts is not None else _counters(2, dev)
+    flags = None
+    if classify:
+        flags = torch.empty(tri.shape[0], dtype=torch.uint8, device=dev)
+        _check(lib().ml_tea_classify(_ptr(clip), dt, tri.shape[0], C.byref(p), _ptr(flags), _stream()))
     _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
-                               C.byref(p), _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr),
-                               _stream()))
+                               _ptr(flags), C.byref(p), _ptr(data), esize, bits, _ptr(mask), _ptr(edited),
+                               _ptr(ctr), _stream()))
     if counts is not None:
         return None
     c = ctr.tolist()
@@ -496,6 +504,8 @@ class StrokeBatch:
         if len(esizes) != 1:
             raise TargetMismatch("all layers of a batch must share one element size")
         self.esize = esizes.pop()
+        if any(t.data_ptr() % 16 or not t.is_contiguous() for t in self.data + self.mask + self.edited):
+            raise TargetMismatch("batched strokes need contiguous, 16-byte aligned layer planes")
         mk = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=device)
         self.d_data, self.d_mask, self.d_edited = mk(self.data), mk(self.mask), mk(self.edited)
         self.counts = torch.zeros(self.L, dtype=torch.int64, device=device)

@@ -112,6 +112,52 @@ ML_DEV void store_value(void* data, int esize, long long i, uint32_t bits) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Quad write: the KN:198-202 write rule for 4 horizontally adjacent texels owned by ONE thread
+// (texel index i is a multiple of 4, planes are 4-byte aligned).  `hits` has bit e set when texel
+// i+e is hit.  Byte planes are updated with one 32-bit read-modify-write instead of four byte
+// stores (partial-sector byte stores are what makes hit-heavy strokes slow); returns through cnt
+// the number of hit texels whose edited flag was 0.
+ML_DEV uint32_t spread4(unsigned hits) {            // 4 bits -> 4 byte lanes of 0xff
+    return ((hits * 0x00204081u) & 0x01010101u) * 0xffu;
+}
+ML_DEV uint32_t zero_bytes_msb(uint32_t w) {        // bit 7 of each byte lane set iff that byte == 0
+    return ~((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w)) & 0x80808080u;
+}
+template <int ES>
+ML_DEV void quad_write(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i,
+                       unsigned hits, long long& cnt) {
+    const uint32_t hm = spread4(hits);
+    uint32_t* pe = (uint32_t*)(edited + i);
+    const uint32_t ew = *pe;
+    cnt += __popc(zero_bytes_msb(ew) & hm);
+    const uint32_t en = (ew & ~hm) | (0x01010101u & hm);
+    if (en != ew) *pe = en;
+    uint32_t* pm = (uint32_t*)(mask + i);
+    if (hits == 0xfu) *pm = 0x01010101u;
+    else { const uint32_t mw = *pm, mn = (mw & ~hm) | (0x01010101u & hm); if (mn != mw) *pm = mn; }
+    if (ES == 1) {
+        uint32_t* pd = (uint32_t*)((uint8_t*)data + i);
+        const uint32_t vr = (value & 0xffu) * 0x01010101u;
+        if (hits == 0xfu) *pd = vr;
+        else { const uint32_t dw = *pd; *pd = (dw & ~hm) | (vr & hm); }
+    } else if (ES == 2) {
+        uint16_t* pd = (uint16_t*)data + i;
+        if (hits == 0xfu) { const uint32_t vr = (value & 0xffffu) * 0x00010001u; *(uint2*)pd = make_uint2(vr, vr); }
+        else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) if (hits & (1u << e)) pd[e] = (uint16_t)value;
+        }
+    } else {
+        uint32_t* pd = (uint32_t*)data + i;
+        if (hits == 0xfu) *(uint4*)pd = make_uint4(value, value, value, value);
+        else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) if (hits & (1u << e)) pd[e] = value;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Triangle setup: KN:32-41 (_ccw), KN:44-47 (tie rule), KN:50-59 (bbox, tightened).
 struct TriSetup {
     double x0, y0, x1, y1, x2, y2;   // CCW-normalised vertices, grid units

@@ -36,10 +36,10 @@ ML_DEV void block_sum_atomic(double v, double* out) {
 
 // 16 texels per thread step: four 128-bit area loads + one 128-bit load per mask plane.
 template <int G, bool VECTOR>
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, 2)
 area_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
     double acc[G];
-    long long cnt[G];
+    unsigned cnt[G];                      // per-thread texel counts (< 2^32 texels per thread)
 #pragma unroll
     for (int g = 0; g < G; ++g) { acc[g] = 0.0; cnt[g] = 0; }
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
@@ -54,22 +54,37 @@ area_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
             for (int j = 0; j < 4; ++j) ar[j] = ld_stream((const float4*)area + v * 4 + j);
 #pragma unroll
             for (int g = 0; g < G; ++g) m[g] = ld_stream((const uint4*)a.mask[g] + v);
+            // Layer masks are spatially coherent and the mask bytes this library writes are exactly
+            // 0 / 1, so most 16-texel vectors lie entirely outside (skip) or entirely inside (add the
+            // shared 16-texel sum) a layer; only vectors on a mask boundary, or masks using other
+            // non-zero byte values, take the per-texel path.  Summation order is free (1e-6 rel).
+            uint32_t anyset = 0;
+#pragma unroll
+            for (int g = 0; g < G; ++g) anyset |= m[g].x | m[g].y | m[g].z | m[g].w;
+            if (anyset == 0) continue;
             double d[16];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 d[4 * j] = (double)ar[j].x; d[4 * j + 1] = (double)ar[j].y;
                 d[4 * j + 2] = (double)ar[j].z; d[4 * j + 3] = (double)ar[j].w;
             }
+            double s4[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s4[j] = xadd(xadd(d[4 * j], d[4 * j + 1]), xadd(d[4 * j + 2], d[4 * j + 3]));
+            const double s16 = xadd(xadd(s4[0], s4[1]), xadd(s4[2], s4[3]));
 #pragma unroll
             for (int g = 0; g < G; ++g) {
+                const uint32_t o = m[g].x | m[g].y | m[g].z | m[g].w;
+                if (o == 0) continue;
+                if ((m[g].x & m[g].y & m[g].z & m[g].w) == 0x01010101u) { acc[g] = xadd(acc[g], s16); cnt[g] += 16; continue; }
                 const uint32_t w[4] = {m[g].x, m[g].y, m[g].z, m[g].w};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const uint32_t ff = __vcmpne4(w[j], 0u);
-                    cnt[g] += __popc(ff) >> 3;
+                    if (w[j] == 0) continue;
+                    if (w[j] == 0x01010101u) { acc[g] = xadd(acc[g], s4[j]); cnt[g] += 4; continue; }
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
-                        if (ff & (0xffu << (8 * e))) acc[g] = xadd(acc[g], d[4 * j + e]);
+                        if (w[j] & (0xffu << (8 * e))) { acc[g] = xadd(acc[g], d[4 * j + e]); ++cnt[g]; }
                 }
             }
         }
@@ -84,7 +99,7 @@ area_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         block_sum_atomic(acc[g], a.sums + g);
-        if (a.counts) block_count_add(cnt[g], a.counts + g);
+        if (a.counts) block_count_add((long long)cnt[g], a.counts + g);
     }
 }
 

@@ -4,9 +4,10 @@
 // write rule is the reference's (KN:198-202: count 0 -> 1 edits, data = value, mask = 1,
 // edited = 1).
 //
-// Both are pure streams: 12 B/texel (three float32 position planes) resp. attr + valid bytes,
-// read once with 128-bit no-allocate loads; writes happen only for hits.  Every thread keeps
-// UNROLL independent 16-byte loads per plane in flight.
+// Both are pure HBM streams: 12 B/texel (three float32 position planes) resp. attr + valid bytes,
+// read once with 128-bit no-allocate loads, UNROLL independent loads per plane in flight per
+// thread.  Hits are written per 4-texel quad with 32-bit read-modify-writes (common.cuh
+// quad_write), so hit-dense strokes do not degenerate into partial-sector byte stores.
 #include <cuda_fp16.h>
 #include "common.cuh"
 #include "meshlayers_b200.h"
@@ -25,20 +26,24 @@ ML_DEV void hit_write(void* data, int esize, uint32_t value, uint8_t* mask, uint
     edited[i] = 1;
 }
 
-ML_DEV bool sphere_hit(float px, float py, float pz, double cx, double cy, double cz, double r2) {
-    const double dx = xsub((double)px, cx), dy = xsub((double)py, cy), dz = xsub((double)pz, cz);
-    const double d2 = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
-    return d2 <= r2;
-}
-
-ML_DEV bool sphere_hit_d(double px, double py, double pz, double cx, double cy, double cz, double r2) {
+ML_DEV bool sphere_hit(double px, double py, double pz, double cx, double cy, double cz, double r2) {
     const double dx = xsub(px, cx), dy = xsub(py, cy), dz = xsub(pz, cz);
     const double d2 = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
     return d2 <= r2;
 }
 
-// VEC = 4: 128-bit loads (planes 16-byte aligned); VEC = 1: scalar fallback for odd alignments.
-template <int VEC>
+ML_DEV unsigned sphere_hits4(const float4& x, const float4& y, const float4& z,
+                             double cx, double cy, double cz, double r2) {
+    unsigned h = 0;
+    if (sphere_hit((double)x.x, (double)y.x, (double)z.x, cx, cy, cz, r2)) h |= 1u;
+    if (sphere_hit((double)x.y, (double)y.y, (double)z.y, cx, cy, cz, r2)) h |= 2u;
+    if (sphere_hit((double)x.z, (double)y.z, (double)z.z, cx, cy, cz, r2)) h |= 4u;
+    if (sphere_hit((double)x.w, (double)y.w, (double)z.w, cx, cy, cz, r2)) h |= 8u;
+    return h;
+}
+
+// ES > 0: aligned quad path (planes 16-byte aligned); ES == 0: scalar fallback for any layout.
+template <int ES>
 __global__ void __launch_bounds__(BLOCK)
 sphere_kernel(const float* __restrict__ px, const float* __restrict__ py, const float* __restrict__ pz,
               long long n, double cx, double cy, double cz, double r2,
@@ -47,7 +52,8 @@ sphere_kernel(const float* __restrict__ px, const float* __restrict__ py, const 
     long long cnt = 0;
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
-    if (VEC == 4) {
+    long long done = 0;
+    if (ES > 0) {
         const long long nq = n >> 2;
         const float4* qx = (const float4*)px; const float4* qy = (const float4*)py; const float4* qz = (const float4*)pz;
         for (long long q0 = tid; q0 < nq; q0 += nthreads * UNROLL) {
@@ -61,163 +67,123 @@ sphere_kernel(const float* __restrict__ px, const float* __restrict__ py, const 
             for (int u = 0; u < UNROLL; ++u) {
                 const long long q = q0 + u * nthreads;
                 if (q >= nq) break;
-                const long long i = q << 2;
-                if (sphere_hit(vx[u].x, vy[u].x, vz[u].x, cx, cy, cz, r2)) hit_write(data, esize, value, mask, edited, i, cnt);
-                if (sphere_hit(vx[u].y, vy[u].y, vz[u].y, cx, cy, cz, r2)) hit_write(data, esize, value, mask, edited, i + 1, cnt);
-                if (sphere_hit(vx[u].z, vy[u].z, vz[u].z, cx, cy, cz, r2)) hit_write(data, esize, value, mask, edited, i + 2, cnt);
-                if (sphere_hit(vx[u].w, vy[u].w, vz[u].w, cx, cy, cz, r2)) hit_write(data, esize, value, mask, edited, i + 3, cnt);
+                const unsigned hits = sphere_hits4(vx[u], vy[u], vz[u], cx, cy, cz, r2);
+                if (hits) quad_write<(ES > 0 ? ES : 1)>(data, value, mask, edited, q << 2, hits, cnt);
             }
         }
-        for (long long i = (nq << 2) + tid; i < n; i += nthreads)
-            if (sphere_hit(px[i], py[i], pz[i], cx, cy, cz, r2)) hit_write(data, esize, value, mask, edited, i, cnt);
-    } else {
-        for (long long i = tid; i < n; i += nthreads)
-            if (sphere_hit(px[i], py[i], pz[i], cx, cy, cz, r2)) hit_write(data, esize, value, mask, edited, i, cnt);
+        done = nq << 2;
     }
+    for (long long i = done + tid; i < n; i += nthreads)
+        if (sphere_hit((double)px[i], (double)py[i], (double)pz[i], cx, cy, cz, r2))
+            hit_write(data, esize, value, mask, edited, i, cnt);
     block_count_add(cnt, counter);
 }
 
 // ---------------------------------------------------------------------------------------------
-// K strokes in one pass.  Each block owns TILE consecutive texels per iteration:
-//   1. streams the tile's positions into registers and reduces their bounding box,
-//   2. culls the stroke list against the box (conservative float64 sphere/box test) into an
-//      ORDER-PRESERVING list in shared memory,
-//   3. every texel tests only the surviving strokes, in stroke order, so the result equals K
-//      successive single-stroke passes (later strokes overwrite earlier ones).
-constexpr int TILE_Q = BLOCK;             // quads per tile -> TILE = 1024 texels
-constexpr int MAX_LIST = 1024;            // surviving strokes kept per tile pass
-
+// K strokes in one pass.  Work unit = one WARP x 512 consecutive texels (each lane holds 4 quads,
+// every load instruction covers 512 contiguous bytes):
+//   1. the warp streams its texels into registers and reduces their bounding box with shuffles;
+//   2. strokes are culled 32 at a time (lane k tests stroke k0+k against the box, conservative
+//      float64 sphere/box distance) into a ballot mask -- ascending bit order is stroke order;
+//   3. every texel tests only the surviving strokes, in order, so the result equals K successive
+//      single-stroke passes (a later stroke overwrites an earlier one on the same layer).
+// No shared-memory lists and no block barriers in the loop; per-layer edit counts go to shared
+// counters (L <= 64) and are flushed once per block.
 struct BatchArgs {
     const float *px, *py, *pz;
     long long n;
     const double* strokes; const int* layer_of; const uint32_t* value_bits; long long K;
     void* const* data; uint8_t* const* mask; uint8_t* const* edited; long long L;
-    int esize; unsigned long long* counts;
+    unsigned long long* counts;
 };
 
-ML_DEV float warp_min(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-ML_DEV float warp_max(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
+template <int ES>
 __global__ void __launch_bounds__(BLOCK)
 sphere_batch_kernel(BatchArgs a) {
-    __shared__ float s_lo[3][BLOCK / 32], s_hi[3][BLOCK / 32];
-    __shared__ double s_box[6];
-    __shared__ int s_list[MAX_LIST];
-    __shared__ double s_sph[MAX_LIST][4];
-    __shared__ int s_wcount[BLOCK / 32];
-    __shared__ int s_nlist;
     __shared__ unsigned long long s_counts[64];
     const bool smem_counts = a.L <= 64;
     if (threadIdx.x < 64) s_counts[threadIdx.x] = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const long long nq = a.n >> 2;                       // host guarantees n % 4 == 0 handled by tail call
-    const long long ntiles = (nq + TILE_Q - 1) / TILE_Q;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long q = tile * TILE_Q + threadIdx.x;
-        const bool live = q < nq;
-        float4 vx, vy, vz;
-        const float inf = __int_as_float(0x7f800000);
+    const int lane = threadIdx.x & 31;
+    const long long nq = a.n >> 2;                        // host guarantees n % 4 == 0
+    const long long nunits = (nq + 127) >> 7;             // 128 quads = 512 texels per warp unit
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    const float inf = __int_as_float(0x7f800000);
+    for (long long unit = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); unit < nunits; unit += nwarps) {
+        float4 vx[4], vy[4], vz[4];
         float lo[3] = {inf, inf, inf}, hi[3] = {-inf, -inf, -inf};
-        if (live) {
-            vx = ld_stream((const float4*)a.px + q);
-            vy = ld_stream((const float4*)a.py + q);
-            vz = ld_stream((const float4*)a.pz + q);
-            // fminf / fmaxf ignore NaN (uncovered texels)
-            lo[0] = fminf(fminf(vx.x, vx.y), fminf(vx.z, vx.w)); hi[0] = fmaxf(fmaxf(vx.x, vx.y), fmaxf(vx.z, vx.w));
-            lo[1] = fminf(fminf(vy.x, vy.y), fminf(vy.z, vy.w)); hi[1] = fmaxf(fmaxf(vy.x, vy.y), fmaxf(vy.z, vy.w));
-            lo[2] = fminf(fminf(vz.x, vz.y), fminf(vz.z, vz.w)); hi[2] = fmaxf(fmaxf(vz.x, vz.y), fmaxf(vz.z, vz.w));
-            // a NaN-only component leaves lo = NaN? no: fminf(NaN, NaN) = NaN -> normalise
 #pragma unroll
-            for (int c = 0; c < 3; ++c) { if (!(lo[c] == lo[c])) lo[c] = inf; if (!(hi[c] == hi[c])) hi[c] = -inf; }
+        for (int u = 0; u < 4; ++u) {
+            const long long q = (unit << 7) + u * 32 + lane;
+            if (q < nq) {
+                vx[u] = ld_stream((const float4*)a.px + q);
+                vy[u] = ld_stream((const float4*)a.py + q);
+                vz[u] = ld_stream((const float4*)a.pz + q);
+            } else {
+                const float qn = __int_as_float(0x7fc00000);
+                vx[u] = vy[u] = vz[u] = make_float4(qn, qn, qn, qn);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {                    // fminf / fmaxf drop NaNs (uncovered texels)
+            lo[0] = fminf(lo[0], fminf(fminf(vx[u].x, vx[u].y), fminf(vx[u].z, vx[u].w)));
+            hi[0] = fmaxf(hi[0], fmaxf(fmaxf(vx[u].x, vx[u].y), fmaxf(vx[u].z, vx[u].w)));
+            lo[1] = fminf(lo[1], fminf(fminf(vy[u].x, vy[u].y), fminf(vy[u].z, vy[u].w)));
+            hi[1] = fmaxf(hi[1], fmaxf(fmaxf(vy[u].x, vy[u].y), fmaxf(vy[u].z, vy[u].w)));
+            lo[2] = fminf(lo[2], fminf(fminf(vz[u].x, vz[u].y), fminf(vz[u].z, vz[u].w)));
+            hi[2] = fmaxf(hi[2], fmaxf(fmaxf(vz[u].x, vz[u].y), fmaxf(vz[u].z, vz[u].w)));
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float l = warp_min(lo[c]), h = warp_max(hi[c]);
-            if (lane == 0) { s_lo[c][wid] = l; s_hi[c][wid] = h; }
-        }
-        __syncthreads();
-        if (threadIdx.x < 3) {
-            float l = s_lo[threadIdx.x][0], h = s_hi[threadIdx.x][0];
-            for (int w = 1; w < BLOCK / 32; ++w) { l = fminf(l, s_lo[threadIdx.x][w]); h = fmaxf(h, s_hi[threadIdx.x][w]); }
-            s_box[threadIdx.x] = (double)l; s_box[3 + threadIdx.x] = (double)h;
-        }
-        __syncthreads();
-        const double bl0 = s_box[0], bl1 = s_box[1], bl2 = s_box[2], bh0 = s_box[3], bh1 = s_box[4], bh2 = s_box[5];
-        const bool empty_box = !(bl0 <= bh0);             // tile holds no covered texel
-        // stroke passes: cull MAX_LIST-sized, order-preserving batches
-        for (long long k0 = 0; k0 < a.K && !empty_box; ) {
-            if (threadIdx.x == 0) s_nlist = 0;
-            __syncthreads();
-            long long k = k0;
-            // rounds of BLOCK strokes until the list is (nearly) full or strokes are exhausted
-            while (k < a.K) {
-                const long long kk = k + threadIdx.x;
-                bool keep = false;
-                double sx = 0, sy = 0, sz = 0, sr = 0;
-                if (kk < a.K) {
-                    sx = a.strokes[4 * kk]; sy = a.strokes[4 * kk + 1]; sz = a.strokes[4 * kk + 2]; sr = a.strokes[4 * kk + 3];
-                    // distance from the centre to the box, per axis max(lo-c, 0, c-hi)
-                    const double ddx = fmax(fmax(xsub(bl0, sx), xsub(sx, bh0)), 0.0);
-                    const double ddy = fmax(fmax(xsub(bl1, sy), xsub(sy, bh1)), 0.0);
-                    const double ddz = fmax(fmax(xsub(bl2, sz), xsub(sz, bh2)), 0.0);
-                    const double dmin2 = xadd(xadd(xmul(ddx, ddx), xmul(ddy, ddy)), xmul(ddz, ddz));
-                    // every texel p of the tile has fl(d2(p)) >= dmin2*(1-8u); keep unless the box
-                    // is provably outside: dmin2 > r2*(1+1e-12)
-                    keep = !(dmin2 > xmul(xmul(sr, sr), 1.000000000001));
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (lane == 0) s_wcount[wid] = __popc(bal);
-                __syncthreads();
-                int base = s_nlist, before = 0, total = 0;
-                for (int w = 0; w < BLOCK / 32; ++w) { if (w < wid) before += s_wcount[w]; total += s_wcount[w]; }
-                const bool fits = base + total <= MAX_LIST;
-                if (fits && keep) {
-                    const int slot = base + before + __popc(bal & ((1u << lane) - 1u));
-                    s_list[slot] = (int)kk;
-                    s_sph[slot][0] = sx; s_sph[slot][1] = sy; s_sph[slot][2] = sz; s_sph[slot][3] = xmul(sr, sr);
-                }
-                __syncthreads();
-                if (!fits) break;                         // process what we have, resume at k
-                if (threadIdx.x == 0) s_nlist = base + total;
-                k += BLOCK;
-                __syncthreads();
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+                hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
             }
-            k0 = (k < a.K) ? k : a.K;
-            const int nl = s_nlist;
-            if (live && nl > 0) {
-                const double fx[4] = {(double)vx.x, (double)vx.y, (double)vx.z, (double)vx.w};
-                const double fy[4] = {(double)vy.x, (double)vy.y, (double)vy.z, (double)vy.w};
-                const double fz[4] = {(double)vz.x, (double)vz.y, (double)vz.z, (double)vz.w};
-                for (int j = 0; j < nl; ++j) {
-                    const double sx = s_sph[j][0], sy = s_sph[j][1], sz = s_sph[j][2], r2 = s_sph[j][3];
-                    unsigned hits = 0;
+        }
+        if (!(lo[0] <= hi[0])) continue;                  // no covered texel in this unit (warp-uniform)
+        const double bl0 = lo[0], bl1 = lo[1], bl2 = lo[2], bh0 = hi[0], bh1 = hi[1], bh2 = hi[2];
+        for (long long k0 = 0; k0 < a.K; k0 += 32) {
+            const long long kk = k0 + lane;
+            bool keep = false;
+            if (kk < a.K) {
+                const double sx = a.strokes[4 * kk], sy = a.strokes[4 * kk + 1], sz = a.strokes[4 * kk + 2],
+                             sr = a.strokes[4 * kk + 3];
+                // per-axis distance from the centre to the box: max(lo - c, c - hi, 0)
+                const double ddx = fmax(fmax(xsub(bl0, sx), xsub(sx, bh0)), 0.0);
+                const double ddy = fmax(fmax(xsub(bl1, sy), xsub(sy, bh1)), 0.0);
+                const double ddz = fmax(fmax(xsub(bl2, sz), xsub(sz, bh2)), 0.0);
+                const double dmin2 = xadd(xadd(xmul(ddx, ddx), xmul(ddy, ddy)), xmul(ddz, ddz));
+                // every texel p of the unit has fl(d2(p)) >= dmin2*(1 - 8u): the box is provably
+                // missed only when dmin2 > r*r*(1 + 1e-12); otherwise keep the stroke.
+                keep = !(dmin2 > xmul(xmul(sr, sr), 1.000000000001));
+            }
+            unsigned live = __ballot_sync(0xffffffffu, keep);
+            while (live) {
+                const int b = __ffs(live) - 1;
+                live &= live - 1;
+                const long long k = k0 + b;
+                const double sx = __ldg(a.strokes + 4 * k), sy = __ldg(a.strokes + 4 * k + 1),
+                             sz = __ldg(a.strokes + 4 * k + 2), sr = __ldg(a.strokes + 4 * k + 3);
+                const double r2 = xmul(sr, sr);
+                unsigned hits[4];
+                unsigned any = 0;
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) if (sphere_hit_d(fx[e], fy[e], fz[e], sx, sy, sz, r2)) hits |= 1u << e;
-                    if (hits) {
-                        const int kk = s_list[j];
-                        const int layer = a.layer_of[kk];
-                        const uint32_t value = a.value_bits[kk];
-                        void* d = a.data[layer]; uint8_t* m = a.mask[layer]; uint8_t* ed = a.edited[layer];
-                        long long c = 0;
+                for (int u = 0; u < 4; ++u) { hits[u] = sphere_hits4(vx[u], vy[u], vz[u], sx, sy, sz, r2); any |= hits[u]; }
+                if (any) {
+                    const int layer = __ldg(a.layer_of + k);
+                    const uint32_t value = __ldg(a.value_bits + k);
+                    void* d = a.data[layer]; uint8_t* m = a.mask[layer]; uint8_t* ed = a.edited[layer];
+                    long long c = 0;
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) if (hits & (1u << e)) hit_write(d, a.esize, value, m, ed, (q << 2) + e, c);
-                        if (c) atomicAdd(smem_counts ? &s_counts[layer] : a.counts + layer, (unsigned long long)c);
-                    }
+                    for (int u = 0; u < 4; ++u)
+                        if (hits[u]) quad_write<ES>(d, value, m, ed, ((unit << 7) + u * 32 + lane) << 2, hits[u], c);
+                    if (c) atomicAdd(smem_counts ? &s_counts[layer] : a.counts + layer, (unsigned long long)c);
                 }
             }
-            __syncthreads();
         }
-        __syncthreads();
     }
+    __syncthreads();
     if (smem_counts && threadIdx.x < a.L && s_counts[threadIdx.x]) atomicAdd(a.counts + threadIdx.x, s_counts[threadIdx.x]);
 }
 
@@ -232,7 +198,7 @@ template <> struct AttrT<ML_F16> { typedef uint16_t T; static ML_DEV double get(
 template <> struct AttrT<ML_FLOAT32> { typedef float T; static ML_DEV double get(T v) { return (double)v; } };
 
 // 4 texels per step: one (4*sizeof(T))-byte attribute load + one 4-byte valid load.
-template <int KIND, bool VECTOR>
+template <int KIND, int ES>
 __global__ void __launch_bounds__(BLOCK)
 threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ valid, long long n,
                  double lo, double hi, void* __restrict__ data, int esize, uint32_t value,
@@ -243,7 +209,7 @@ threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ val
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
     long long done = 0;
-    if (VECTOR) {
+    if (ES > 0) {
         struct __align__(sizeof(T) * 4) Quad { T v[4]; };
         const long long nq = n >> 2;
         for (long long q0 = tid; q0 < nq; q0 += nthreads * UNROLL) {
@@ -260,12 +226,13 @@ threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ val
             for (int u = 0; u < UNROLL; ++u) {
                 const long long q = q0 + u * nthreads;
                 if (q >= nq) break;
+                unsigned hits = 0;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    if (((vm[u] >> (8 * e)) & 0xffu) == 0) continue;
                     const double v = AttrT<KIND>::get(a[u].v[e]);
-                    if (lo <= v && v <= hi) hit_write(data, esize, value, mask, edited, (q << 2) + e, cnt);
+                    if ((((vm[u] >> (8 * e)) & 0xffu) != 0) && lo <= v && v <= hi) hits |= 1u << e;
                 }
+                if (hits) quad_write<(ES > 0 ? ES : 1)>(data, value, mask, edited, q << 2, hits, cnt);
             }
         }
         done = nq << 2;
@@ -287,16 +254,21 @@ inline unsigned stream_grid(long long items_per_thread_iter, long long n_items) 
 }
 
 inline bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+inline bool planes_aligned(const void* d, const void* m, const void* e) { return aligned(d, 16) && aligned(m, 16) && aligned(e, 16); }
 
 template <int KIND>
 int launch_threshold(const void* attr, const uint8_t* valid, long long n, double lo, double hi,
                      void* data, int esize, uint32_t value, uint8_t* mask, uint8_t* edited,
                      unsigned long long* counter, cudaStream_t st) {
     typedef typename AttrT<KIND>::T T;
-    const bool vec = aligned(attr, sizeof(T) * 4) && (!valid || aligned(valid, 4));
+    const bool vec = aligned(attr, sizeof(T) * 4) && (!valid || aligned(valid, 4)) && planes_aligned(data, mask, edited);
     const unsigned grid = stream_grid(4 * UNROLL, n);
-    if (vec) threshold_kernel<KIND, true><<<grid, BLOCK, 0, st>>>(attr, valid, n, lo, hi, data, esize, value, mask, edited, counter);
-    else threshold_kernel<KIND, false><<<grid, BLOCK, 0, st>>>(attr, valid, n, lo, hi, data, esize, value, mask, edited, counter);
+#define ML_LAUNCH_THR(ES) threshold_kernel<KIND, ES><<<grid, BLOCK, 0, st>>>(attr, valid, n, lo, hi, data, esize, value, mask, edited, counter)
+    if (!vec) ML_LAUNCH_THR(0);
+    else if (esize == 1) ML_LAUNCH_THR(1);
+    else if (esize == 2) ML_LAUNCH_THR(2);
+    else ML_LAUNCH_THR(4);
+#undef ML_LAUNCH_THR
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }
@@ -314,10 +286,15 @@ int ml_select_sphere(const float* pos, int64_t pos_stride, int64_t n,
     if (n <= 0) return ML_OK;
     const float *px = pos, *py = pos + pos_stride, *pz = pos + 2 * pos_stride;
     const double r2 = radius * radius;      // host IEEE multiply == the oracle's r*r
-    const bool vec = aligned(px, 16) && aligned(py, 16) && aligned(pz, 16);
+    const bool vec = aligned(px, 16) && aligned(py, 16) && aligned(pz, 16) && planes_aligned(data, mask, edited);
     const unsigned grid = stream_grid(4 * UNROLL, n);
-    if (vec) sphere_kernel<4><<<grid, BLOCK, 0, st>>>(px, py, pz, n, cx, cy, cz, r2, data, esize, value_bits, mask, edited, (unsigned long long*)count);
-    else sphere_kernel<1><<<grid, BLOCK, 0, st>>>(px, py, pz, n, cx, cy, cz, r2, data, esize, value_bits, mask, edited, (unsigned long long*)count);
+    unsigned long long* c = (unsigned long long*)count;
+#define ML_LAUNCH_SPH(ES) sphere_kernel<ES><<<grid, BLOCK, 0, st>>>(px, py, pz, n, cx, cy, cz, r2, data, esize, value_bits, mask, edited, c)
+    if (!vec) ML_LAUNCH_SPH(0);
+    else if (esize == 1) ML_LAUNCH_SPH(1);
+    else if (esize == 2) ML_LAUNCH_SPH(2);
+    else ML_LAUNCH_SPH(4);
+#undef ML_LAUNCH_SPH
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }
@@ -333,13 +310,15 @@ int ml_select_sphere_batch(const float* pos, int64_t pos_stride, int64_t n,
     const float *px = pos, *py = pos + pos_stride, *pz = pos + 2 * pos_stride;
     if (!(aligned(px, 16) && aligned(py, 16) && aligned(pz, 16)) || (n & 3))
         return ml_fail(ML_ERR_ARG, "batched sphere brush needs 16-byte aligned planes and n % 4 == 0");
-    BatchArgs a{px, py, pz, n, strokes, layer_of, value_bits, K, data, mask, edited, L, esize,
+    BatchArgs a{px, py, pz, n, strokes, layer_of, value_bits, K, data, mask, edited, L,
                 (unsigned long long*)counts};
-    const long long ntiles = ((n >> 2) + TILE_Q - 1) / TILE_Q;
-    long long blocks = ntiles;
-    const long long cap = (long long)ml_sm_count() * 8;
+    const long long nunits = ((n >> 2) + 127) >> 7;
+    long long blocks = (nunits + BLOCK / 32 - 1) / (BLOCK / 32);
+    const long long cap = (long long)ml_sm_count() * 16;
     if (blocks > cap) blocks = cap;
-    sphere_batch_kernel<<<(unsigned)blocks, BLOCK, 0, st>>>(a);
+    if (esize == 1) sphere_batch_kernel<1><<<(unsigned)blocks, BLOCK, 0, st>>>(a);
+    else if (esize == 2) sphere_batch_kernel<2><<<(unsigned)blocks, BLOCK, 0, st>>>(a);
+    else sphere_batch_kernel<4><<<(unsigned)blocks, BLOCK, 0, st>>>(a);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

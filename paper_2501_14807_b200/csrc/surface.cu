@@ -67,36 +67,132 @@ resolve_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, cons
     block_count_add(cnt, covered);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Per-stroke triangle classification.  flags[t] = 0 only when NO texel of triangle t can pass the
+// TEA filters, decided from the three vertices alone:
+//   * all w_i <= 0: every fragment has wc = (l0*w0 + l1*w1) + l2*w2 <= 0 (l_i >= 0 for covered
+//     texels, products and sums of non-positive terms stay non-positive under rounding) -> KN:174;
+//   * all w_i > 0: xn = xc/wc is a convex combination of the vertex ratios x_i/w_i (weights
+//     l_i*w_i >= 0) up to a rounding error bounded by ~8u*(1 + max|x_i| / min w_i).  If the tool
+//     coordinate s = sfx*xn + bx (KN:187) of all three vertices lies on one side of [0,1] by more
+//     than delta = 1e-9*(|sfx|*(1 + max|x_i|/min w_i) + |bx| + 1)  (>= 10^6 x the rounding bound)
+//     the closed test KN:189 fails for every fragment; likewise for t and for the window test
+//     KN:181 (xn outside [-1,1]).
+// Anything else (mixed signs of w, NaNs) keeps flag 1.  The texel kernel skips flag-0 triangles,
+// which removes the float64 work for everything outside the tool footprint without changing a bit.
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
+tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p, uint8_t* __restrict__ flags) {
+    const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    if (t >= ntri) return;
+    const T* c = tri_clip + 12 * t;
+    double x[3], y[3], w[3];
+#pragma unroll
+    for (int v = 0; v < 3; ++v) { x[v] = (double)c[4 * v]; y[v] = (double)c[4 * v + 1]; w[v] = (double)c[4 * v + 3]; }
+    const int npos = (w[0] > 0.0) + (w[1] > 0.0) + (w[2] > 0.0);
+    const int nnonpos = (w[0] <= 0.0) + (w[1] <= 0.0) + (w[2] <= 0.0);
+    uint8_t keep = 1;
+    if (nnonpos == 3) keep = 0;
+    else if (npos == 3) {
+        const double wmin = fmin(fmin(w[0], w[1]), w[2]);
+        const double ax = fmax(fmax(fabs(x[0]), fabs(x[1])), fabs(x[2])) / wmin;
+        const double ay = fmax(fmax(fabs(y[0]), fabs(y[1])), fabs(y[2])) / wmin;
+        const double xn0 = x[0] / w[0], xn1 = x[1] / w[1], xn2 = x[2] / w[2];
+        const double yn0 = y[0] / w[0], yn1 = y[1] / w[1], yn2 = y[2] / w[2];
+        const double xlo = fmin(fmin(xn0, xn1), xn2), xhi = fmax(fmax(xn0, xn1), xn2);
+        const double ylo = fmin(fmin(yn0, yn1), yn2), yhi = fmax(fmax(yn0, yn1), yn2);
+        const double dxn = 1e-9 * (1.0 + ax), dyn = 1e-9 * (1.0 + ay);
+        // tool test: s = sfx*xn + bx over [xlo, xhi] (sfx may be negative)
+        const double s0 = p.sfx * xlo + p.bx, s1 = p.sfx * xhi + p.bx;
+        const double t0 = p.sfy * ylo + p.by, t1 = p.sfy * yhi + p.by;
+        const double ds = fabs(p.sfx) * dxn + 1e-9 * (fabs(p.bx) + 1.0);
+        const double dt = fabs(p.sfy) * dyn + 1e-9 * (fabs(p.by) + 1.0);
+        const bool out_s = (fmax(s0, s1) + ds < 0.0) || (fmin(s0, s1) - ds > 1.0);
+        const bool out_t = (fmax(t0, t1) + dt < 0.0) || (fmin(t0, t1) - dt > 1.0);
+        const bool out_w = (xhi + dxn < -1.0) || (xlo - dxn > 1.0) || (yhi + dyn < -1.0) || (ylo - dyn > 1.0);
+        if (out_s || out_t || out_w) keep = 0;
+    }
+    flags[t] = keep;
+}
+
+// Full KN:166-193 evaluation of one covered texel for its owner triangle.  Kept out of line so
+// the streaming loop around it stays small.
+template <typename T>
+__device__ __noinline__ bool tea_texel_eval(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
+                                            int t, int x, int y, const TeaParams& p) {
+    TriSetup s;
+    tri_load_ccw(tri_xy + 6ll * t, s);
+    double e0, e1, e2;
+    tri_inside(s, x, y, e0, e1, e2);
+    const T* c = tri_clip + 12ll * t;
+    const int i1 = s.swapped ? 8 : 4, i2 = s.swapped ? 4 : 8;
+    double c0[4], c1[4], c2[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { c0[k] = (double)c[k]; c1[k] = (double)c[i1 + k]; c2[k] = (double)c[i2 + k]; }
+    return tea_fragment(p, e0, e1, e2, c0, c1, c2);
+}
+
+// One thread per 4 consecutive texels: a 128-bit streaming load of the owner ids (4 B/texel is
+// the whole algorithmic traffic), a cached 1-byte flag gather per distinct owner, and the heavy
+// float64 path only for texels of flagged triangles.
+template <typename T, int ES>
+__global__ void __launch_bounds__(BLOCK)
 tea_texel_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
-                 long long row0, long long n, const int* __restrict__ tri_id, TeaParams p,
+                 long long row0, long long n, const int* __restrict__ tri_id,
+                 const uint8_t* __restrict__ flags, TeaParams p,
                  void* __restrict__ data, int esize, uint32_t value,
                  uint8_t* __restrict__ mask, uint8_t* __restrict__ edited,
                  unsigned long long* counters) {
     long long newly = 0, frags = 0;
-    const long long stride = (long long)gridDim.x * BLOCK;
-    for (long long i = (long long)blockIdx.x * BLOCK + threadIdx.x; i < n; i += stride) {
+    const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    long long done = 0;
+    if (ES > 0) {
+        const long long nq = n >> 2;
+        constexpr int U = 4;
+        for (long long q0 = tid; q0 < nq; q0 += nthreads * U) {
+            uint4 ids[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long q = q0 + u * nthreads;
+                if (q < nq) ids[u] = ld_stream((const uint4*)tri_id + q);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long q = q0 + u * nthreads;
+                if (q >= nq) break;
+                const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
+                int last = -1; bool last_keep = false;
+                unsigned hits = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int t = t4[e];
+                    if (t < 0) continue;
+                    ++frags;
+                    if (t != last) { last = t; last_keep = flags ? (__ldg(flags + t) != 0) : true; }
+                    if (!last_keep) continue;
+                    const long long i = (q << 2) + e;
+                    const long long yy = i / width;
+                    if (tea_texel_eval(tri_xy, tri_clip, t, (int)(i - yy * width), (int)(row0 + yy), p)) hits |= 1u << e;
+                }
+                // exactly one thread owns these 4 texels in this kernel: the read-modify-write of
+                // KN:198-202 inside quad_write is race-free
+                if (hits) quad_write<(ES > 0 ? ES : 1)>(data, value, mask, edited, q << 2, hits, newly);
+            }
+        }
+        done = nq << 2;
+    }
+    for (long long i = done + tid; i < n; i += nthreads) {
         const int t = tri_id[i];
         if (t < 0) continue;
         ++frags;
+        if (flags && !flags[t]) continue;
         const long long yy = i / width;
-        const int x = (int)(i - yy * width), y = (int)(row0 + yy);
-        TriSetup s;
-        tri_load_ccw(tri_xy + 6ll * t, s);
-        double e0, e1, e2;
-        tri_inside(s, x, y, e0, e1, e2);
-        const T* c = tri_clip + 12ll * t;
-        const int i1 = s.swapped ? 8 : 4, i2 = s.swapped ? 4 : 8;
-        double c0[4], c1[4], c2[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) { c0[k] = (double)c[k]; c1[k] = (double)c[i1 + k]; c2[k] = (double)c[i2 + k]; }
-        if (!tea_fragment(p, e0, e1, e2, c0, c1, c2)) continue;
-        // exactly one thread owns texel i in this kernel: plain read-modify-write is race-free
-        if (edited[i] == 0) ++newly;                                     // KN:198-199
-        store_value(data, esize, i, value);                              // KN:200
-        mask[i] = 1;                                                     // KN:201
-        edited[i] = 1;                                                   // KN:202
+        if (!tea_texel_eval(tri_xy, tri_clip, t, (int)(i - yy * width), (int)(row0 + yy), p)) continue;
+        if (edited[i] == 0) ++newly;
+        store_value(data, esize, i, value);
+        mask[i] = 1;
+        edited[i] = 1;
     }
     block_count_add(newly, counters);
     block_count_add(frags, counters + 1);
@@ -108,6 +204,25 @@ inline unsigned grid_for(long long n) {
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     return (unsigned)blocks;
+}
+
+template <typename T>
+int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
+                             const int* tri_id, const uint8_t* flags, const TeaParams& p, void* data, int esize,
+                             uint32_t value, uint8_t* mask, uint8_t* edited, unsigned long long* ctr, cudaStream_t st) {
+    const bool vec = ((((uintptr_t)tri_id) | ((uintptr_t)data) | ((uintptr_t)mask) | ((uintptr_t)edited)) & 15) == 0;
+    long long blocks = ((vec ? (n + 15) / 16 : n) + BLOCK - 1) / BLOCK;
+    const long long cap = (long long)ml_sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+#define ML_LAUNCH_TEA(ES) tea_texel_kernel<T, ES><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, n, tri_id, flags, p, data, esize, value, mask, edited, ctr)
+    if (!vec) ML_LAUNCH_TEA(0);
+    else if (esize == 1) ML_LAUNCH_TEA(1);
+    else if (esize == 2) ML_LAUNCH_TEA(2);
+    else ML_LAUNCH_TEA(4);
+#undef ML_LAUNCH_TEA
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
 }
 
 }  // namespace
@@ -135,10 +250,23 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
     return ML_OK;
 }
 
+int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_tea_params* tp,
+                    uint8_t* flags, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ntri <= 0) return ML_OK;
+    TeaParams p = ml_make_tea_params(tp);
+    const unsigned grid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
+    if (tri_dtype == ML_F32) tea_classify_kernel<float><<<grid, BLOCK, 0, st>>>((const float*)tri_clip, ntri, p, flags);
+    else if (tri_dtype == ML_F64) tea_classify_kernel<double><<<grid, BLOCK, 0, st>>>((const double*)tri_clip, ntri, p, flags);
+    else return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
 int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
-                  const ml_tea_params* tp, void* data, int esize, uint32_t value_bits,
-                  uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream) {
+                  const uint8_t* tri_flags, const ml_tea_params* tp, void* data, int esize,
+                  uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream) {
     (void)ntri;
     cudaStream_t st = (cudaStream_t)stream;
     if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
@@ -147,15 +275,12 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
     TeaParams p = ml_make_tea_params(tp);
     unsigned long long* ctr = (unsigned long long*)counters;
     if (tri_dtype == ML_F32)
-        tea_texel_kernel<float><<<grid_for(n), BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_clip,
-            width, row0, n, tri_id, p, data, esize, value_bits, mask, edited, ctr);
-    else if (tri_dtype == ML_F64)
-        tea_texel_kernel<double><<<grid_for(n), BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_clip,
-            width, row0, n, tri_id, p, data, esize, value_bits, mask, edited, ctr);
-    else
-        return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
-    ML_CUDA(cudaGetLastError());
-    return ML_OK;
+        return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, width, row0, n, tri_id, tri_flags, p,
+                                 data, esize, value_bits, mask, edited, ctr, st);
+    if (tri_dtype == ML_F64)
+        return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, width, row0, n, tri_id, tri_flags, p,
+                                 data, esize, value_bits, mask, edited, ctr, st);
+    return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
 }
 
 }  // extern "C"
