@@ -310,7 +310,7 @@ def run_ours(args):
     area_counts = torch.zeros(L, dtype=torch.int64, device=dev)
     counts2 = torch.zeros(2, dtype=torch.int64, device=dev)
     counts1 = torch.zeros(1, dtype=torch.int64, device=dev)
-    launches = {"tea": 1, "sphere": 1, "batch": 1, "chain": 1, "mask_op": 1, "threshold": 1, "area": -(-L // 8)}
+    launches = {"tea": 3, "sphere": 1, "batch": 1, "chain": 1, "mask_op": 1, "threshold": 1, "area": -(-L // 8)}
 
     def stage_call(st, inp, tool, e2e):
         """Run one stage.  e2e=True goes through the public API from host inputs and returns host
@@ -323,7 +323,7 @@ def run_ours(args):
             ctx.edited.zero_()
             nat.tea_texels(ctx.tri_xy, ctx.tri_clip, surf.tri_id, float(wl.cam.width), float(wl.cam.height),
                            depth.plane, wl.eps, sfx, sfy, bx, by, tool.shape, layers[0].data, layers[0].mask,
-                           ctx.edited, tool.value, row0=row0, counts=counts2)
+                           ctx.edited, tool.value, row0=row0, counts=counts2, scratch=ctx.scratch)
         elif st == "sphere":
             s = inp["sphere"]
             if e2e:

@@ -73,8 +73,8 @@ def lib():
                                 u32, vp, vp, vp, vp, sz, vp]),
         "ml_raster_tri_id": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
         "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
-        "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, i32,
-                                u32, vp, vp, vp, vp]),
+        "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
+                                vp, i32, u32, vp, vp, vp, vp]),
         "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp]),
         "ml_select_sphere": (i32, [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
         "ml_select_sphere_batch": (i32, [vp, i64, i64, vp, vp, vp, i64, vp, vp, vp, i64, i32, vp, vp]),
@@ -431,7 +431,7 @@ def raster_tri_id(tri_xy, width, height, *, row0=0, rows=None, device=None):
 
 
 def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
-               shape, data, mask, edited, value, *, row0=0, counts=None, classify=True):
+               shape, data, mask, edited, value, *, row0=0, counts=None, classify=True, scratch=None):
     """TEA over the cached triangle-id map (SURVEY.md 8 note N1): same planes and counts as
     ``raster_tea`` when the uv layout has no overlaps.  Returns (edited_texels, fragments).
     ``classify`` runs the per-stroke triangle pre-pass (ml_tea_classify) so that texels of
@@ -454,17 +454,28 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
     p = _tea_params(ww, wh, depth, eps, sfx, sfy, bx, by, shape)
     bits, esize = value_bits(value, data)
     ctr = counts if counts is not None else _counters(2, dev)
-    flags = None
+    flags = work = None
     if classify:
-        flags = torch.empty(tri.shape[0], dtype=torch.uint8, device=dev)
+        # scratch = (flags[T] uint8, worklist int64[...]) may be supplied to avoid per-stroke allocation
+        if scratch is None:
+            scratch = tea_scratch(tri.shape[0], rows * w, dev)
+        flags, work = scratch
         _check(lib().ml_tea_classify(_ptr(clip), dt, tri.shape[0], C.byref(p), _ptr(flags), _stream()))
     _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
-                               _ptr(flags), C.byref(p), _ptr(data), esize, bits, _ptr(mask), _ptr(edited),
-                               _ptr(ctr), _stream()))
+                               _ptr(flags), C.byref(p), _ptr(work), 0 if work is None else work.numel() * 8,
+                               _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr), _stream()))
     if counts is not None:
         return None
     c = ctr.tolist()
     return int(c[0]), int(c[1])
+
+
+def tea_scratch(ntri, ntexels, device, max_quads=1 << 22):
+    """Per-stroke scratch of ``tea_texels``: triangle flags and the quad work list (device)."""
+    torch = _torch()
+    cap = max(8, min((ntexels + 3) // 4, max_quads))
+    return (torch.empty(max(1, ntri), dtype=torch.uint8, device=device),
+            torch.empty(2 + cap, dtype=torch.int64, device=device))
 
 
 def _check_layer_planes(n, data, mask, edited):

@@ -123,15 +123,15 @@ ML_DEV uint32_t spread4(unsigned hits) {            // 4 bits -> 4 byte lanes of
 ML_DEV uint32_t zero_bytes_msb(uint32_t w) {        // bit 7 of each byte lane set iff that byte == 0
     return ~((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w)) & 0x80808080u;
 }
+// `ew` is the already-loaded 32-bit word edited[i..i+3] (callers load the words of several quads
+// up front so the loads overlap instead of serialising behind the stores).
 template <int ES>
-ML_DEV void quad_write(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i,
-                       unsigned hits, long long& cnt) {
+ML_DEV void quad_write_pre(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i,
+                           unsigned hits, uint32_t ew, long long& cnt) {
     const uint32_t hm = spread4(hits);
-    uint32_t* pe = (uint32_t*)(edited + i);
-    const uint32_t ew = *pe;
     cnt += __popc(zero_bytes_msb(ew) & hm);
     const uint32_t en = (ew & ~hm) | (0x01010101u & hm);
-    if (en != ew) *pe = en;
+    if (en != ew) *(uint32_t*)(edited + i) = en;
     uint32_t* pm = (uint32_t*)(mask + i);
     if (hits == 0xfu) *pm = 0x01010101u;
     else { const uint32_t mw = *pm, mn = (mw & ~hm) | (0x01010101u & hm); if (mn != mw) *pm = mn; }
@@ -155,6 +155,11 @@ ML_DEV void quad_write(void* data, uint32_t value, uint8_t* mask, uint8_t* edite
             for (int e = 0; e < 4; ++e) if (hits & (1u << e)) pd[e] = value;
         }
     }
+}
+template <int ES>
+ML_DEV void quad_write(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i,
+                       unsigned hits, long long& cnt) {
+    quad_write_pre<ES>(data, value, mask, edited, i, hits, *(const uint32_t*)(edited + i), cnt);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -98,7 +98,7 @@ struct BatchArgs {
 };
 
 template <int ES>
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, 2)
 sphere_batch_kernel(BatchArgs a) {
     __shared__ unsigned long long s_counts[64];
     const bool smem_counts = a.L <= 64;
@@ -222,18 +222,25 @@ threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ val
                     vm[u] = valid ? ld_stream((const uint32_t*)valid + q) : 0x01010101u;
                 }
             }
+            unsigned hits[UNROLL];
+            uint32_t ew[UNROLL];
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
+                hits[u] = 0;
                 const long long q = q0 + u * nthreads;
-                if (q >= nq) break;
-                unsigned hits = 0;
+                if (q >= nq) continue;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const double v = AttrT<KIND>::get(a[u].v[e]);
-                    if ((((vm[u] >> (8 * e)) & 0xffu) != 0) && lo <= v && v <= hi) hits |= 1u << e;
+                    if ((((vm[u] >> (8 * e)) & 0xffu) != 0) && lo <= v && v <= hi) hits[u] |= 1u << e;
                 }
-                if (hits) quad_write<(ES > 0 ? ES : 1)>(data, value, mask, edited, q << 2, hits, cnt);
             }
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)      // edited words of all hit quads first: loads overlap
+                ew[u] = hits[u] ? *(const uint32_t*)(edited + ((q0 + u * nthreads) << 2)) : 0u;
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)
+                if (hits[u]) quad_write_pre<(ES > 0 ? ES : 1)>(data, value, mask, edited, (q0 + u * nthreads) << 2, hits[u], ew[u], cnt);
         }
         done = nq << 2;
     }

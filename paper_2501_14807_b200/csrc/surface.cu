@@ -132,48 +132,99 @@ __device__ __noinline__ bool tea_texel_eval(const T* __restrict__ tri_xy, const 
     return tea_fragment(p, e0, e1, e2, c0, c1, c2);
 }
 
-// One thread per 4 consecutive texels: a 128-bit streaming load of the owner ids (4 B/texel is
-// the whole algorithmic traffic), a cached 1-byte flag gather per distinct owner, and the heavy
-// float64 path only for texels of flagged triangles.
+// Texel (x, y) of flat slab index i; 32-bit division when the slab is small enough.
+ML_DEV void texel_xy(long long i, long long width, long long row0, bool small, int& x, int& y) {
+    if (small) {
+        const unsigned yy = (unsigned)i / (unsigned)width;
+        x = (int)((unsigned)i - yy * (unsigned)width); y = (int)(row0 + yy);
+    } else {
+        const long long yy = i / width;
+        x = (int)(i - yy * width); y = (int)(row0 + yy);
+    }
+}
+
+// Work list of quads that need the float64 evaluation: entry = (quad index << 4) | keep bits.
+struct TeaWork {
+    unsigned long long* entries;     // NULL: evaluate inline in the stream kernel
+    unsigned long long* count;       // device counter (zeroed before the stream kernel)
+    unsigned long long cap;
+};
+
+// STREAM kernel.  One thread per 4 consecutive texels: a 128-bit streaming load of the owner ids
+// (4 B/texel is the whole algorithmic traffic) and a cached 1-byte flag gather per owner.  Quads
+// with at least one texel of a flagged triangle are appended (warp-aggregated atomic) to the work
+// list for the EVAL kernel; if the list is absent or full they are evaluated right here.
 template <typename T, int ES>
 __global__ void __launch_bounds__(BLOCK)
-tea_texel_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
-                 long long row0, long long n, const int* __restrict__ tri_id,
-                 const uint8_t* __restrict__ flags, TeaParams p,
-                 void* __restrict__ data, int esize, uint32_t value,
-                 uint8_t* __restrict__ mask, uint8_t* __restrict__ edited,
-                 unsigned long long* counters) {
+tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
+                  long long row0, long long n, const int* __restrict__ tri_id,
+                  const uint8_t* __restrict__ flags, TeaParams p, TeaWork wk,
+                  void* __restrict__ data, int esize, uint32_t value,
+                  uint8_t* __restrict__ mask, uint8_t* __restrict__ edited,
+                  unsigned long long* counters) {
     long long newly = 0, frags = 0;
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
+    const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
+    const int lane = threadIdx.x & 31;
     long long done = 0;
     if (ES > 0) {
         const long long nq = n >> 2;
         constexpr int U = 4;
-        for (long long q0 = tid; q0 < nq; q0 += nthreads * U) {
+        // block-uniform trip count so that the warp-collective append below is convergent
+        for (long long base = (long long)blockIdx.x * BLOCK; base < nq; base += nthreads * U) {
             uint4 ids[U];
+            long long qs[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const long long q = q0 + u * nthreads;
-                if (q < nq) ids[u] = ld_stream((const uint4*)tri_id + q);
+                qs[u] = base + u * nthreads + threadIdx.x;
+                if (qs[u] < nq) ids[u] = ld_stream((const uint4*)tri_id + qs[u]);
+            }
+            // all flag gathers of the 16 owners are issued before any is used (independent loads in
+            // flight; neighbouring texels share owners, so they coalesce and hit L1)
+            unsigned keep[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                keep[u] = 0;
+                if (qs[u] >= nq) continue;
+                const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
+                uint8_t f[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) f[e] = (t4[e] >= 0) ? (flags ? __ldg(flags + t4[e]) : (uint8_t)1) : (uint8_t)0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) { frags += t4[e] >= 0; keep[u] |= (f[e] != 0 ? 1u : 0u) << e; }
+            }
+            if (wk.entries) {
+                // one atomic per warp per iteration reserves slots for all its kept quads
+                unsigned bal[U];
+                int total = 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) { bal[u] = __ballot_sync(0xffffffffu, keep[u] != 0); total += __popc(bal[u]); }
+                if (total == 0) continue;
+                unsigned long long slot = 0;
+                if (lane == 0) slot = atomicAdd(wk.count, (unsigned long long)total);
+                slot = __shfl_sync(0xffffffffu, slot, 0);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (keep[u]) {
+                        const unsigned long long at = slot + __popc(bal[u] & ((1u << lane) - 1u));
+                        if (at < wk.cap) { wk.entries[at] = ((unsigned long long)qs[u] << 4) | keep[u]; keep[u] = 0; }
+                    }
+                    slot += __popc(bal[u]);
+                }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const long long q = q0 + u * nthreads;
-                if (q >= nq) break;
+            for (int u = 0; u < U; ++u) {          // inline evaluation: no list, or list overflow
+                if (!keep[u]) continue;
+                const long long q = qs[u];
                 const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
-                int last = -1; bool last_keep = false;
                 unsigned hits = 0;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const int t = t4[e];
-                    if (t < 0) continue;
-                    ++frags;
-                    if (t != last) { last = t; last_keep = flags ? (__ldg(flags + t) != 0) : true; }
-                    if (!last_keep) continue;
-                    const long long i = (q << 2) + e;
-                    const long long yy = i / width;
-                    if (tea_texel_eval(tri_xy, tri_clip, t, (int)(i - yy * width), (int)(row0 + yy), p)) hits |= 1u << e;
+                    if (!(keep[u] & (1u << e))) continue;
+                    int x, y;
+                    texel_xy((q << 2) + e, width, row0, small, x, y);
+                    if (tea_texel_eval(tri_xy, tri_clip, t4[e], x, y, p)) hits |= 1u << e;
                 }
                 // exactly one thread owns these 4 texels in this kernel: the read-modify-write of
                 // KN:198-202 inside quad_write is race-free
@@ -187,8 +238,9 @@ tea_texel_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, l
         if (t < 0) continue;
         ++frags;
         if (flags && !flags[t]) continue;
-        const long long yy = i / width;
-        if (!tea_texel_eval(tri_xy, tri_clip, t, (int)(i - yy * width), (int)(row0 + yy), p)) continue;
+        int x, y;
+        texel_xy(i, width, row0, small, x, y);
+        if (!tea_texel_eval(tri_xy, tri_clip, t, x, y, p)) continue;
         if (edited[i] == 0) ++newly;
         store_value(data, esize, i, value);
         mask[i] = 1;
@@ -196,6 +248,43 @@ tea_texel_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, l
     }
     block_count_add(newly, counters);
     block_count_add(frags, counters + 1);
+}
+
+// EVAL kernel.  Four adjacent lanes share one work-list quad, one lane per texel, so the float64
+// evaluation runs with full, evenly spread parallelism no matter how compact the tool footprint is
+// in atlas space.  The 4 hit bits are gathered with a ballot and lane 0 of the group writes.
+template <typename T, int ES>
+__global__ void __launch_bounds__(BLOCK)
+tea_eval_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
+                long long row0, long long n, const int* __restrict__ tri_id, TeaParams p, TeaWork wk,
+                void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                uint8_t* __restrict__ edited, unsigned long long* counters) {
+    long long newly = 0;
+    const unsigned long long have = *wk.count;
+    const long long count = (long long)(have < wk.cap ? have : wk.cap);
+    const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
+    const int lane = threadIdx.x & 31, e = lane & 3;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    // block-uniform trip count: every lane reaches the ballot
+    for (long long base = (long long)blockIdx.x * BLOCK; base < count * 4; base += nthreads) {
+        const long long idx = base + threadIdx.x, ent = idx >> 2;
+        bool hit = false;
+        long long q = 0;
+        if (ent < count) {
+            const unsigned long long w = wk.entries[ent];
+            q = (long long)(w >> 4);
+            if (w & (1ull << e)) {
+                const long long i = (q << 2) + e;
+                int x, y;
+                texel_xy(i, width, row0, small, x, y);
+                hit = tea_texel_eval(tri_xy, tri_clip, __ldg(tri_id + i), x, y, p);
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        const unsigned hits = (bal >> (lane & ~3)) & 0xfu;
+        if (e == 0 && hits) quad_write<ES>(data, value, mask, edited, q << 2, hits, newly);
+    }
+    block_count_add(newly, counters);
 }
 
 inline unsigned grid_for(long long n) {
@@ -208,19 +297,29 @@ inline unsigned grid_for(long long n) {
 
 template <typename T>
 int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
-                             const int* tri_id, const uint8_t* flags, const TeaParams& p, void* data, int esize,
-                             uint32_t value, uint8_t* mask, uint8_t* edited, unsigned long long* ctr, cudaStream_t st) {
+                      const int* tri_id, const uint8_t* flags, const TeaParams& p, void* worklist,
+                      size_t worklist_bytes, void* data, int esize, uint32_t value, uint8_t* mask,
+                      uint8_t* edited, unsigned long long* ctr, cudaStream_t st) {
     const bool vec = ((((uintptr_t)tri_id) | ((uintptr_t)data) | ((uintptr_t)mask) | ((uintptr_t)edited)) & 15) == 0;
     long long blocks = ((vec ? (n + 15) / 16 : n) + BLOCK - 1) / BLOCK;
     const long long cap = (long long)ml_sm_count() * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-#define ML_LAUNCH_TEA(ES) tea_texel_kernel<T, ES><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, n, tri_id, flags, p, data, esize, value, mask, edited, ctr)
+    TeaWork wk{nullptr, nullptr, 0};
+    if (vec && worklist && worklist_bytes >= 64 && (((uintptr_t)worklist) & 7) == 0) {
+        wk.count = (unsigned long long*)worklist;
+        wk.entries = wk.count + 2;
+        wk.cap = (worklist_bytes - 16) / 8;
+        ML_CUDA(cudaMemsetAsync(wk.count, 0, 8, st));
+    }
+#define ML_LAUNCH_TEA(ES) tea_stream_kernel<T, ES><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, n, tri_id, flags, p, wk, data, esize, value, mask, edited, ctr)
+#define ML_LAUNCH_EVAL(ES) tea_eval_kernel<T, ES><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, n, tri_id, p, wk, data, value, mask, edited, ctr)
     if (!vec) ML_LAUNCH_TEA(0);
-    else if (esize == 1) ML_LAUNCH_TEA(1);
-    else if (esize == 2) ML_LAUNCH_TEA(2);
-    else ML_LAUNCH_TEA(4);
+    else if (esize == 1) { ML_LAUNCH_TEA(1); if (wk.entries) ML_LAUNCH_EVAL(1); }
+    else if (esize == 2) { ML_LAUNCH_TEA(2); if (wk.entries) ML_LAUNCH_EVAL(2); }
+    else { ML_LAUNCH_TEA(4); if (wk.entries) ML_LAUNCH_EVAL(4); }
 #undef ML_LAUNCH_TEA
+#undef ML_LAUNCH_EVAL
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }
@@ -265,7 +364,8 @@ int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_
 
 int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
-                  const uint8_t* tri_flags, const ml_tea_params* tp, void* data, int esize,
+                  const uint8_t* tri_flags, const ml_tea_params* tp, void* worklist,
+                  size_t worklist_bytes, void* data, int esize,
                   uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream) {
     (void)ntri;
     cudaStream_t st = (cudaStream_t)stream;
@@ -276,10 +376,10 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
     unsigned long long* ctr = (unsigned long long*)counters;
     if (tri_dtype == ML_F32)
         return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, width, row0, n, tri_id, tri_flags, p,
-                                 data, esize, value_bits, mask, edited, ctr, st);
+                                 worklist, worklist_bytes, data, esize, value_bits, mask, edited, ctr, st);
     if (tri_dtype == ML_F64)
         return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, width, row0, n, tri_id, tri_flags, p,
-                                 data, esize, value_bits, mask, edited, ctr, st);
+                                 worklist, worklist_bytes, data, esize, value_bits, mask, edited, ctr, st);
     return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
 }
 

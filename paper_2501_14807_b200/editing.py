@@ -110,6 +110,7 @@ class StrokeContext:
         self.tri_clip = torch.from_numpy(np.ascontiguousarray(clip)).to(device)
         self.tri_xy = surface.tri_xy
         self.edited = torch.zeros((surface.rows, surface.width), dtype=torch.uint8, device=device)
+        self.scratch = _native.tea_scratch(mesh.num_triangles, surface.rows * surface.width, device)
         self.device = device
 
 
@@ -132,7 +133,8 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
     args = (float(ctx.camera.width), float(ctx.camera.height), ctx.depth.plane, eps, sfx, sfy, bx, by,
             shape, layer.data, layer.mask, ctx.edited, tool.value)
     if s.overlap == 0 and not force_direct:
-        _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts)
+        _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
+                           scratch=ctx.scratch)
     else:
         _native.raster_tea(ctx.tri_xy, ctx.tri_clip, *args, height=s.height, row0=s.row0, counts=counts)
     return EditResult(edited_mask=ctx.edited, _counts=counts)
