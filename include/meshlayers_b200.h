@@ -105,8 +105,8 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
 /* ---- TEA over the cached triangle-id map (SURVEY.md 8 note N1) ---------------------------------
  * Bit-identical to ml_raster_tea when no two triangles overlap in uv space (overlap events == 0):
  * each covered texel re-evaluates KN:72-74 and KN:166-193 for its owner triangle.
- * tri_flags (device, [ntri] bytes, may be NULL): output of ml_tea_classify for THIS stroke;
- * texels of triangles flagged 0 are skipped (provably unaffected by the stroke).
+ * tri_flags (device bitmap of (ntri+31)/32 uint32 words, may be NULL): output of ml_tea_classify
+ * for THIS stroke; texels of triangles whose bit is 0 are skipped (provably unaffected).
  * worklist (device scratch, 8-byte aligned, may be NULL): when given, the id stream only COLLECTS
  * the 4-texel quads that need the float64 evaluation (8 bytes each, after a 16-byte header) and a
  * second kernel evaluates them with evenly spread parallelism; quads that do not fit are
@@ -114,14 +114,15 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
  * counters: [0] += newly edited texels, [1] += covered texels (== fragments). */
 int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
-                  const uint8_t* tri_flags, const ml_tea_params* params, void* worklist,
+                  const uint32_t* tri_flags, const ml_tea_params* params, void* worklist,
                   size_t worklist_bytes, void* data, int esize,
                   uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream);
 /* Per-stroke conservative triangle classification from the clip-space vertices alone:
- * flags[t] = 0 iff no fragment of triangle t can pass the w > 0, window and tool-range tests
- * (KN:174, 181, 189) -- see surface.cu for the rounding-error argument.  O(ntri), no texel work. */
+ * bit t (bit t&31 of word t>>5) = 0 iff no fragment of triangle t can pass the w > 0, window and
+ * tool-range tests (KN:174, 181, 189) -- see surface.cu for the rounding-error argument.
+ * flags: (ntri+31)/32 uint32 words.  O(ntri), no texel work. */
 int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_tea_params* params,
-                    uint8_t* flags, void* stream);
+                    uint32_t* flags, void* stream);
 
 /* ---- selection brushes (north star (2); definitions: ext_select_sphere / ext_select_threshold) -
  * Sphere brush over n texels of a position map (three float32 planes, stride pos_stride):

@@ -456,7 +456,8 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
     ctr = counts if counts is not None else _counters(2, dev)
     flags = work = None
     if classify:
-        # scratch = (flags[T] uint8, worklist int64[...]) may be supplied to avoid per-stroke allocation
+        # scratch = (triangle bitmap int32[(T+31)/32], worklist int64[...]) may be supplied to avoid
+        # per-stroke allocation
         if scratch is None:
             scratch = tea_scratch(tri.shape[0], rows * w, dev)
         flags, work = scratch
@@ -474,7 +475,7 @@ def tea_scratch(ntri, ntexels, device, max_quads=1 << 22):
     """Per-stroke scratch of ``tea_texels``: triangle flags and the quad work list (device)."""
     torch = _torch()
     cap = max(8, min((ntexels + 3) // 4, max_quads))
-    return (torch.empty(max(1, ntri), dtype=torch.uint8, device=device),
+    return (torch.empty(max(1, (ntri + 31) // 32), dtype=torch.int32, device=device),
             torch.empty(2 + cap, dtype=torch.int64, device=device))
 
 

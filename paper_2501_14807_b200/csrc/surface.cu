@@ -82,10 +82,12 @@ resolve_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, cons
 // which removes the float64 work for everything outside the tool footprint without changing a bit.
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
-tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p, uint8_t* __restrict__ flags) {
+tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p, uint32_t* __restrict__ bits) {
+    // output: a BITMAP (bit t&31 of word t>>5), 125 KB per million triangles, so the texel kernel
+    // can keep it in shared memory
     const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
-    if (t >= ntri) return;
-    const T* c = tri_clip + 12 * t;
+    const bool live = t < ntri;
+    const T* c = tri_clip + 12 * (live ? t : 0);
     double x[3], y[3], w[3];
 #pragma unroll
     for (int v = 0; v < 3; ++v) { x[v] = (double)c[4 * v]; y[v] = (double)c[4 * v + 1]; w[v] = (double)c[4 * v + 3]; }
@@ -112,8 +114,12 @@ tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p,
         const bool out_w = (xhi + dxn < -1.0) || (xlo - dxn > 1.0) || (yhi + dyn < -1.0) || (ylo - dyn > 1.0);
         if (out_s || out_t || out_w) keep = 0;
     }
-    flags[t] = keep;
+    const unsigned word = __ballot_sync(0xffffffffu, live && keep);
+    if ((threadIdx.x & 31) == 0 && live) bits[t >> 5] = word;
 }
+
+// flag lookup in the classification bitmap (global or shared memory); NULL bitmap = keep all
+ML_DEV bool tri_flag(const uint32_t* bits, int t) { return bits ? ((bits[t >> 5] >> (t & 31)) & 1u) != 0 : true; }
 
 // Full KN:166-193 evaluation of one covered texel for its owner triangle.  Kept out of line so
 // the streaming loop around it stays small.
@@ -154,14 +160,24 @@ struct TeaWork {
 // (4 B/texel is the whole algorithmic traffic) and a cached 1-byte flag gather per owner.  Quads
 // with at least one texel of a flagged triangle are appended (warp-aggregated atomic) to the work
 // list for the EVAL kernel; if the list is absent or full they are evaluated right here.
-template <typename T, int ES>
-__global__ void __launch_bounds__(BLOCK)
+// BS = threads per block; SMEM = the classification bitmap (nwords 32-bit words) is first copied
+// to dynamic shared memory, so the per-texel flag lookup is an LDS instead of a dependent L2 gather.
+template <typename T, int ES, int BS, bool SMEM>
+__global__ void __launch_bounds__(BS)
 tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
                   long long row0, long long n, const int* __restrict__ tri_id,
-                  const uint8_t* __restrict__ flags, TeaParams p, TeaWork wk,
+                  const uint32_t* __restrict__ gbits, long long nwords, TeaParams p, TeaWork wk,
                   void* __restrict__ data, int esize, uint32_t value,
                   uint8_t* __restrict__ mask, uint8_t* __restrict__ edited,
                   unsigned long long* counters) {
+    extern __shared__ uint32_t s_bits[];
+    constexpr int BLOCK = BS;            // shadows the file-level constant inside this kernel
+    const uint32_t* flags = gbits;
+    if (SMEM) {
+        for (long long k = threadIdx.x; k < nwords; k += BS) s_bits[k] = gbits[k];
+        __syncthreads();
+        flags = s_bits;
+    }
     long long newly = 0, frags = 0;
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
@@ -188,11 +204,9 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
                 keep[u] = 0;
                 if (qs[u] >= nq) continue;
                 const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
-                uint8_t f[4];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) f[e] = (t4[e] >= 0) ? (flags ? __ldg(flags + t4[e]) : (uint8_t)1) : (uint8_t)0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) { frags += t4[e] >= 0; keep[u] |= (f[e] != 0 ? 1u : 0u) << e; }
+                for (int e = 0; e < 4; ++e)
+                    if (t4[e] >= 0) { ++frags; if (tri_flag(flags, t4[e])) keep[u] |= 1u << e; }
             }
             if (wk.entries) {
                 // one atomic per warp per iteration reserves slots for all its kept quads
@@ -237,7 +251,7 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
         const int t = tri_id[i];
         if (t < 0) continue;
         ++frags;
-        if (flags && !flags[t]) continue;
+        if (!tri_flag(flags, t)) continue;
         int x, y;
         texel_xy(i, width, row0, small, x, y);
         if (!tea_texel_eval(tri_xy, tri_clip, t, x, y, p)) continue;
@@ -295,16 +309,48 @@ inline unsigned grid_for(long long n) {
     return (unsigned)blocks;
 }
 
+constexpr int TEA_BIG_BLOCK = 1024;                  // block size when the bitmap lives in shared memory
+constexpr long long TEA_SMEM_MAX_BYTES = 200 * 1024; // bitmap size limit for the shared-memory path
+
+template <typename T, int ES>
+int launch_tea_es(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
+                  const int* tri_id, const uint32_t* bits, long long ntri, const TeaParams& p, TeaWork wk,
+                  void* data, int esize, uint32_t value, uint8_t* mask, uint8_t* edited,
+                  unsigned long long* ctr, cudaStream_t st) {
+    const long long nwords = (ntri + 31) / 32;
+    const long long items = ES > 0 ? (n + 15) / 16 : n;     // 4 quads (16 texels) per thread iteration
+    const bool smem = ES > 0 && bits != nullptr && nwords * 4 <= TEA_SMEM_MAX_BYTES;
+    if (smem) {
+        // one 1024-thread block per SM (the bitmap takes most of its shared memory)
+        auto kern = tea_stream_kernel<T, ES, TEA_BIG_BLOCK, true>;
+        ML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nwords * 4)));
+        long long blocks = (items + TEA_BIG_BLOCK - 1) / TEA_BIG_BLOCK;
+        const long long cap = (long long)ml_sm_count() * (nwords * 4 <= 100 * 1024 ? 2 : 1);
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        kern<<<(unsigned)blocks, TEA_BIG_BLOCK, (size_t)(nwords * 4), st>>>(tri_xy, tri_clip, width, row0, n, tri_id,
+            bits, nwords, p, wk, data, esize, value, mask, edited, ctr);
+    } else {
+        long long blocks = (items + BLOCK - 1) / BLOCK;
+        const long long cap = (long long)ml_sm_count() * 16;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        tea_stream_kernel<T, ES, BLOCK, false><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, n,
+            tri_id, bits, nwords, p, wk, data, esize, value, mask, edited, ctr);
+    }
+    if (ES > 0 && wk.entries)
+        tea_eval_kernel<T, (ES > 0 ? ES : 1)><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, tri_clip, width,
+            row0, n, tri_id, p, wk, data, value, mask, edited, ctr);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
 template <typename T>
 int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
-                      const int* tri_id, const uint8_t* flags, const TeaParams& p, void* worklist,
+                      const int* tri_id, const uint32_t* bits, long long ntri, const TeaParams& p, void* worklist,
                       size_t worklist_bytes, void* data, int esize, uint32_t value, uint8_t* mask,
                       uint8_t* edited, unsigned long long* ctr, cudaStream_t st) {
     const bool vec = ((((uintptr_t)tri_id) | ((uintptr_t)data) | ((uintptr_t)mask) | ((uintptr_t)edited)) & 15) == 0;
-    long long blocks = ((vec ? (n + 15) / 16 : n) + BLOCK - 1) / BLOCK;
-    const long long cap = (long long)ml_sm_count() * 16;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
     TeaWork wk{nullptr, nullptr, 0};
     if (vec && worklist && worklist_bytes >= 64 && (((uintptr_t)worklist) & 7) == 0) {
         wk.count = (unsigned long long*)worklist;
@@ -312,16 +358,10 @@ int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long 
         wk.cap = (worklist_bytes - 16) / 8;
         ML_CUDA(cudaMemsetAsync(wk.count, 0, 8, st));
     }
-#define ML_LAUNCH_TEA(ES) tea_stream_kernel<T, ES><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, n, tri_id, flags, p, wk, data, esize, value, mask, edited, ctr)
-#define ML_LAUNCH_EVAL(ES) tea_eval_kernel<T, ES><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, n, tri_id, p, wk, data, value, mask, edited, ctr)
-    if (!vec) ML_LAUNCH_TEA(0);
-    else if (esize == 1) { ML_LAUNCH_TEA(1); if (wk.entries) ML_LAUNCH_EVAL(1); }
-    else if (esize == 2) { ML_LAUNCH_TEA(2); if (wk.entries) ML_LAUNCH_EVAL(2); }
-    else { ML_LAUNCH_TEA(4); if (wk.entries) ML_LAUNCH_EVAL(4); }
-#undef ML_LAUNCH_TEA
-#undef ML_LAUNCH_EVAL
-    ML_CUDA(cudaGetLastError());
-    return ML_OK;
+    if (!vec) return launch_tea_es<T, 0>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
+    if (esize == 1) return launch_tea_es<T, 1>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
+    if (esize == 2) return launch_tea_es<T, 2>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
+    return launch_tea_es<T, 4>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
 }
 
 }  // namespace
@@ -350,7 +390,7 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
 }
 
 int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_tea_params* tp,
-                    uint8_t* flags, void* stream) {
+                    uint32_t* flags, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (ntri <= 0) return ML_OK;
     TeaParams p = ml_make_tea_params(tp);
@@ -364,10 +404,9 @@ int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_
 
 int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
-                  const uint8_t* tri_flags, const ml_tea_params* tp, void* worklist,
+                  const uint32_t* tri_flags, const ml_tea_params* tp, void* worklist,
                   size_t worklist_bytes, void* data, int esize,
                   uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream) {
-    (void)ntri;
     cudaStream_t st = (cudaStream_t)stream;
     if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
     const long long n = (long long)rows * width;
@@ -375,10 +414,10 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
     TeaParams p = ml_make_tea_params(tp);
     unsigned long long* ctr = (unsigned long long*)counters;
     if (tri_dtype == ML_F32)
-        return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, width, row0, n, tri_id, tri_flags, p,
+        return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, width, row0, n, tri_id, tri_flags, ntri, p,
                                  worklist, worklist_bytes, data, esize, value_bits, mask, edited, ctr, st);
     if (tri_dtype == ML_F64)
-        return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, width, row0, n, tri_id, tri_flags, p,
+        return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, width, row0, n, tri_id, tri_flags, ntri, p,
                                  worklist, worklist_bytes, data, esize, value_bits, mask, edited, ctr, st);
     return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
 }

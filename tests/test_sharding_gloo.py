@@ -1,0 +1,97 @@
+"""world_size-2 tests of the multi-GPU host logic on CPU tensors with the gloo backend:
+stroke broadcast, area all-reduce, halo exchange, and "row slabs concatenate to the full plane"
+with the oracle standing in for the per-rank kernels (the test may use the oracle; the product
+never does)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import kn
+from paper_2501_14807_b200 import sharding, synth
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world_size, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        assert sharding.world() == (rank, world_size)
+        # ---- stroke broadcast: only rank 0 knows the strokes
+        mesh = synth.icosphere_mesh(2)
+        if rank == 0:
+            strokes, labels = synth.sphere_strokes(mesh, 5, seed=3, rmin_frac=0.1, rmax_frac=0.3)
+            layer_of = np.array([0, 1, 0, 1, 0], np.int32)
+            vals = labels.astype(np.uint32)
+        else:
+            strokes, layer_of, vals = np.zeros((0, 4)), np.zeros(0, np.int32), np.zeros(0, np.uint32)
+        s, lo, v = sharding.broadcast_strokes(strokes, layer_of, vals, "cpu")
+        want_s, want_l = synth.sphere_strokes(mesh, 5, seed=3, rmin_frac=0.1, rmax_frac=0.3)
+        assert np.array_equal(s, want_s) and np.array_equal(v, want_l.astype(np.uint32))
+        assert lo.tolist() == [0, 1, 0, 1, 0]
+
+        # ---- each rank computes its row slab (oracle as the local kernel), then all-reduces areas
+        A = 96
+        r0, rows = sharding.shard_rows(A, world_size, rank)
+        surf = kn.surface_map(mesh.tri_uv_texels(A, A), mesh.tri_pos(), mesh.tri_nrm(), A, A, rows=(r0, r0 + rows))
+        data = [np.zeros((rows, A), np.uint8) for _ in range(2)]
+        mask = [np.zeros((rows, A), np.uint8) for _ in range(2)]
+        edited = [np.zeros((rows, A), np.uint8) for _ in range(2)]
+        counts = torch.zeros(2, dtype=torch.int64)
+        for k in range(len(s)):
+            L = int(lo[k])
+            counts[L] += kn.select_sphere(surf["pos"], s[k, :3], s[k, 3], data[L], mask[L], edited[L], int(v[k]))
+        sums = torch.tensor([kn.layer_area(surf["area"], m)[0] for m in mask], dtype=torch.float64)
+        texels = torch.tensor([kn.layer_area(surf["area"], m)[1] for m in mask], dtype=torch.int64)
+        sharding.allreduce_areas(sums, texels)
+        sharding.allreduce_counts(counts)
+
+        # ---- halo exchange of a byte plane for a radius-2 stencil
+        cov = torch.from_numpy((surf["tri_id"] >= 0).astype(np.uint8))
+        ext, ext_row0 = sharding.exchange_halo(cov, r0, A, 2)
+        in0, in_rows = sharding.halo_bounds(r0, rows, A, 2)
+        assert ext_row0 == in0 and ext.shape[0] == in_rows
+        np.savez(os.path.join(out_dir, "rank%d.npz" % rank), data0=data[0], data1=data[1], mask0=mask[0], mask1=mask[1],
+                 sums=sums.numpy(), texels=texels.numpy(), counts=counts.numpy(), ext=ext.numpy(), ext_row0=ext_row0,
+                 r0=r0, rows=rows)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_two_rank_row_sharding_equals_single_rank(tmp_path):
+    ws = 2
+    mp.spawn(_worker, args=(ws, _free_port(), str(tmp_path)), nprocs=ws, join=True)
+    parts = [np.load(tmp_path / ("rank%d.npz" % r)) for r in range(ws)]
+    # single-process reference over the full atlas
+    mesh = synth.icosphere_mesh(2)
+    A = 96
+    surf = kn.surface_map(mesh.tri_uv_texels(A, A), mesh.tri_pos(), mesh.tri_nrm(), A, A)
+    strokes, labels = synth.sphere_strokes(mesh, 5, seed=3, rmin_frac=0.1, rmax_frac=0.3)
+    data = [np.zeros((A, A), np.uint8) for _ in range(2)]
+    mask = [np.zeros((A, A), np.uint8) for _ in range(2)]
+    edited = [np.zeros((A, A), np.uint8) for _ in range(2)]
+    counts = [0, 0]
+    for k, L in enumerate([0, 1, 0, 1, 0]):
+        counts[L] += kn.select_sphere(surf["pos"], strokes[k, :3], strokes[k, 3], data[L], mask[L], edited[L], int(labels[k]))
+    for L in range(2):
+        assert np.array_equal(np.concatenate([p["data%d" % L] for p in parts]), data[L])
+        assert np.array_equal(np.concatenate([p["mask%d" % L] for p in parts]), mask[L])
+        a, c = kn.layer_area(surf["area"], mask[L])
+        for p in parts:                                   # every rank holds the reduced totals
+            assert abs(p["sums"][L] - a) <= 1e-12 * max(a, 1e-300) and p["texels"][L] == c
+            assert p["counts"][L] == counts[L]
+    cov = (surf["tri_id"] >= 0).astype(np.uint8)
+    for p in parts:
+        e0 = int(p["ext_row0"])
+        assert np.array_equal(p["ext"], cov[e0:e0 + p["ext"].shape[0]])
+    assert sum(int(p["rows"]) for p in parts) == A
