@@ -185,12 +185,96 @@ chain_scalar_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
     }
 }
 
+// Binary operator fast path (the 3 B/texel kernel): VPT 16-texel vectors per thread step, ALL
+// operand loads of the step issued before the first store (the chain kernel cannot hoist loads
+// over its stores because its output may alias an input), so each thread keeps
+// VPT*2*(1+ESIZE) 128-bit requests in flight.  A thread only ever reads the vectors it writes,
+// so in-place use (output aliasing A) stays race-free.
+template <int ESIZE, int VPT>
+__global__ void __launch_bounds__(BLOCK)
+binary_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
+    constexpr int ES = ESIZE > 0 ? ESIZE : 1;
+    const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    const int op = a.ops[1];
+    for (long long v0 = tid; v0 < nv; v0 += nthreads * VPT) {
+        uint4 m[VPT][2];
+        uint4 d[VPT][2][ES];
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const long long v = v0 + k * nthreads;
+            if (v < nv) {
+#pragma unroll
+                for (int l = 0; l < 2; ++l) {
+                    m[k][l] = ld_stream_rw((const uint4*)a.mask[l] + v);
+                    if (ESIZE > 0) {
+#pragma unroll
+                        for (int j = 0; j < ES; ++j) d[k][l][j] = ld_stream_rw((const uint4*)a.data[l] + v * ES + j);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const long long v = v0 + k * nthreads;
+            if (v >= nv) break;
+            uint4 om;
+            uint4 od[ES];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                Group<ESIZE> acc, b;
+                acc.ff = nz_bytes(((const uint32_t*)&m[k][0])[g]);
+                b.ff = nz_bytes(((const uint32_t*)&m[k][1])[g]);
+                if (ESIZE > 0) {
+#pragma unroll
+                    for (int j = 0; j < ES; ++j) {
+                        acc.d[j] = ((const uint32_t*)&d[k][0][0])[g * ES + j] & expand<ES>(acc.ff, j);
+                        b.d[j] = ((const uint32_t*)&d[k][1][0])[g * ES + j];
+                    }
+                }
+                combine<ESIZE>(op, acc, b);
+                ((uint32_t*)&om)[g] = acc.ff & 0x01010101u;
+                if (ESIZE > 0) {
+#pragma unroll
+                    for (int j = 0; j < ES; ++j) ((uint32_t*)&od[0])[g * ES + j] = acc.d[j];
+                }
+            }
+            st_stream((uint4*)mc + v, om);
+            if (ESIZE > 0) {
+#pragma unroll
+                for (int j = 0; j < ES; ++j) st_stream((uint4*)dc + v * ES + j, od[j]);
+            }
+        }
+    }
+}
+
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 template <int ESIZE>
 int launch_chain(const ChainArgs& a, void* dc, uint8_t* mc, long long n, cudaStream_t st) {
     bool vec = aligned16(mc) && (ESIZE == 0 || aligned16(dc));
     for (int l = 0; l < a.nlayers; ++l) vec = vec && aligned16(a.mask[l]) && (ESIZE == 0 || aligned16(a.data[l]));
+    if (vec && a.nlayers == 2 && ESIZE <= 2 && (n >> 4) > 0) {
+        constexpr int VPT = ESIZE == 0 ? 4 : 2;
+        const long long nv = n >> 4;
+        long long blocks = (nv + (long long)BLOCK * VPT - 1) / ((long long)BLOCK * VPT);
+        const long long cap = (long long)ml_sm_count() * 8;
+        if (blocks > cap) blocks = cap;
+        binary_kernel<ESIZE, VPT><<<(unsigned)blocks, BLOCK, 0, st>>>(a, dc, mc, nv);
+        ML_CUDA(cudaGetLastError());
+        const long long tail = n & 15;
+        if (tail == 0) return ML_OK;
+        // the last < 16 texels go through the scalar kernel on shifted pointers
+        ChainArgs t = a;
+        const long long off = nv << 4;
+        for (int l = 0; l < 2; ++l) {
+            t.mask[l] = a.mask[l] + off;
+            if (ESIZE > 0) t.data[l] = (const uint8_t*)a.data[l] + off * ESIZE;
+        }
+        chain_scalar_kernel<ESIZE><<<1, BLOCK, 0, st>>>(t, ESIZE > 0 ? (void*)((uint8_t*)dc + off * ESIZE) : nullptr, mc + off, tail);
+        ML_CUDA(cudaGetLastError());
+        return ML_OK;
+    }
     const long long items = vec ? ((n + 15) >> 4) : n;
     long long blocks = (items + BLOCK - 1) / BLOCK;
     const long long cap = (long long)ml_sm_count() * 16;

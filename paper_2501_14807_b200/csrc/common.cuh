@@ -42,6 +42,23 @@ ML_DEV uint32_t ld_stream(const uint32_t* p) {
     asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
+ML_DEV uint32_t ld_volatile_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
+// streaming load of a 4-element group of 1-, 2- or 4-byte elements (4 / 8 / 16 bytes)
+template <typename Q>
+ML_DEV Q ld_quad(const Q* p) {
+    Q r;
+    if (sizeof(Q) == 16) { uint4 v = ld_stream((const uint4*)p); memcpy(&r, &v, 16); }
+    else if (sizeof(Q) == 8) {
+        uint2 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+        memcpy(&r, &v, 8);
+    } else { uint32_t v = ld_stream((const uint32_t*)p); memcpy(&r, &v, 4); }
+    return r;
+}
 ML_DEV void st_stream(uint4* p, uint4 v) {
     asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};"
                  :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");

@@ -178,6 +178,29 @@ def test_select_threshold_bit_exact(akind):
         assert np.array_equal(e.cpu().numpy(), re)
 
 
+def test_select_threshold_rounding_edges():
+    """The kernel compares in the attribute's own domain against inward-rounded thresholds; that
+    must equal the float64 definition exactly at the representability edges."""
+    f = np.float32
+    lo, hi = 0.1, 0.7                                         # neither is a float32
+    edge = [f(lo), np.nextafter(f(lo), f(1)), np.nextafter(f(lo), f(-1)), f(hi), np.nextafter(f(hi), f(1)),
+            np.nextafter(f(hi), f(-1)), f(np.inf), f(-np.inf), f(np.nan), f(0.0), f(-0.0), f(3e38), f(1e-45)]
+    cases = [(lo, hi), (-np.inf, np.inf), (1e39, np.inf), (-np.inf, -1e39), (0.0, 0.0), (float(f(lo)), float(f(hi))),
+             (0.7, 0.1), (np.nan, 1.0), (-1e-46, 1e-46), (2.5, 1e300)]
+    attr32 = np.resize(np.array(edge, f), 64).reshape(4, 16)
+    attr16 = attr32.astype(np.float16)
+    ints = np.resize(np.array([-3, -2, -1, 0, 1, 2, 3, 100, -100], np.int32), 64).reshape(4, 16)
+    int_cases = [(-2.5, 2.5), (-2.0, 2.0), (-1e30, 1e30), (2.0000001, 2.9999), (3.0, 3.0), (1e19, 1e20), (-1e20, -1e19)]
+    for attr, cs in ((attr32, cases), (attr16, cases), (ints, int_cases), (ints.astype(np.int8), int_cases),
+                     (np.abs(ints).astype(np.uint32), int_cases)):
+        for a, b in cs:
+            rd = np.zeros(attr.shape, np.uint8); rm = np.zeros(attr.shape, bool); re = np.zeros(attr.shape, np.uint8)
+            want = kn.select_threshold(attr, None, a, b, rd, rm, re, 1)
+            d, m, e = _dev(rd * 0), _dev(rm & False), _dev(re * 0)
+            assert nat.select_threshold(_dev(attr), None, a, b, d, m, e, 1) == want, (attr.dtype, a, b)
+            assert np.array_equal(m.cpu().numpy(), rm), (attr.dtype, a, b)
+
+
 @pytest.mark.parametrize("kind", [None, np.uint8, np.int16, np.float32, np.uint32])
 @pytest.mark.parametrize("op", ["union", "intersection", "difference", "masking"])
 def test_layer_op_bit_exact(kind, op):

@@ -1,0 +1,88 @@
+#!/usr/bin/env python
+"""Kernel micro-benchmarks on synthetic planes (no mesh needed): quick A/B timing while tuning.
+
+    python tools/microbench.py [--n 16384] [--reps 20] [names...]
+
+Prints one line per case: name, ms (median of reps, CUDA events), GB/s of the bytes given.
+Not a parity test and not the judged benchmark (that is bench.py)."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2501_14807_b200 import _native as nat  # noqa: E402
+
+
+def timeit(fn, reps):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("names", nargs="*")
+    args = ap.parse_args()
+    N = args.n
+    n = N * N
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(1)
+    want = set(args.names)
+
+    def run(name, fn, nbytes):
+        if want and not any(w in name for w in want):
+            return
+        ms = timeit(fn, args.reps)
+        print("%-34s %8.4f ms  %8.1f GB/s  %8.1f Gtexel/s" % (name, ms, nbytes / ms / 1e6, n / ms / 1e6), flush=True)
+
+    # smooth attribute field: coherent hit regions like a real attribute
+    yy, xx = torch.meshgrid(torch.linspace(0, 6, N, device=dev), torch.linspace(0, 6, N, device=dev), indexing="ij")
+    attr = (torch.sin(xx) * torch.cos(yy)).contiguous()
+    del yy, xx
+    data = torch.zeros((N, N), dtype=torch.uint8, device=dev)
+    mask = torch.zeros((N, N), dtype=torch.uint8, device=dev)
+    edited = torch.zeros((N, N), dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    for name, lo, hi in (("threshold hits=0%", 5.0, 6.0), ("threshold hits~10%", -0.1, 0.1), ("threshold hits~50%", -0.5, 0.5),
+                         ("threshold hits=100%", -2.0, 2.0)):
+        run(name, lambda lo=lo, hi=hi: nat.select_threshold(attr, None, lo, hi, data, mask, edited, 3, counts=cnt), 4 * n)
+    noise = torch.rand((N, N), device=dev, generator=g)
+    run("threshold noise hits=20%", lambda: nat.select_threshold(noise, None, 0.0, 0.2, data, mask, edited, 3, counts=cnt), 4 * n)
+    del noise
+
+    m2 = (torch.rand((N, N), device=dev, generator=g) < 0.3).to(torch.uint8)
+    out = torch.zeros((N, N), dtype=torch.uint8, device=dev)
+    run("mask_op union", lambda: nat.layer_op("union", None, mask, None, m2, None, out), 3 * n)
+    d2 = torch.zeros((N, N), dtype=torch.uint8, device=dev)
+    dout = torch.zeros((N, N), dtype=torch.uint8, device=dev)
+    run("layer_op union u8", lambda: nat.layer_op("union", data, mask, d2, m2, dout, out), 6 * n)
+    run("memset 1 plane (torch)", lambda: out.zero_(), n)
+    run("copy 1 plane (torch)", lambda: out.copy_(m2), 2 * n)
+
+    pos = torch.rand((3, N, N), device=dev, generator=g)
+    run("sphere few hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.05, data, mask, edited, 3, counts=cnt), 12 * n)
+    run("sphere 50% hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.62, data, mask, edited, 3, counts=cnt), 12 * n)
+    area = pos[0]
+    masks = [m2, mask, out, d2]
+    run("area L=1", lambda: nat.layer_area(area, masks[:1], sums=torch.zeros(1, dtype=torch.float64, device=dev),
+                                           counts=torch.zeros(1, dtype=torch.int64, device=dev)), 5 * n)
+    run("area L=4 (noise+coherent)", lambda: nat.layer_area(area, masks, sums=torch.zeros(4, dtype=torch.float64, device=dev),
+                                                            counts=torch.zeros(4, dtype=torch.int64, device=dev)), 8 * n)
+
+
+if __name__ == "__main__":
+    main()
