@@ -48,8 +48,8 @@ CHAIN_OPS = ["union", "intersection", "difference", "union", "masking", "differe
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--atlas", type=int, default=16384, help="atlas width and per-rank slab height")
     ap.add_argument("--layers", type=int, default=8)
@@ -97,13 +97,16 @@ class Workload:
                     batch=strokes[1:], batch_layers=np.arange(self.L, dtype=np.int32), batch_values=labels[1:])
 
     def algorithmic_bytes(self, n, stage, T, hits=0):
-        """Algorithmic HBM bytes of one launch over n texels; hit writes are
-        excluded (they are a few percent and stroke dependent) except where noted."""
+        """Algorithmic HBM bytes of one stage over n texels: the read stream plus,
+        for the brushes, `hits` texels x (1 B edited read + 1 B edited + 1 B mask + 1 B uint8 data
+        written).  tea additionally resets the 1 B/texel edited plane and reads the
+        clip coordinates of every triangle once for the classification pass."""
         L = self.L
-        return {"tea": 4 * n + T * 18 * 8 + self.cam.width * self.cam.height * 4,
+        base = {"tea": 4 * n + n + T * 12 * 8 + self.cam.width * self.cam.height * 4,
                 "sphere": 12 * n, "batch": 12 * n,
                 "chain": (self.chain_n + 1) * 2 * n, "mask_op": 3 * n,
                 "threshold": 4 * n, "area": (4 * -(-L // 8) + L) * n}[stage]
+        return base + 4 * int(hits)
 
 
 def sample_clocks(stop, out):
@@ -112,7 +115,7 @@ def sample_clocks(stop, out):
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     try:
-        p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits", "-lms", "200",
+        p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits", "-lms", "100",
                               "-i", os.environ.get("LOCAL_RANK", "0")], stdout=subprocess.PIPE, text=True)
     except OSError:
         return
@@ -425,25 +428,41 @@ def run_ours(args):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     h2d = 8 * 6 + 64 + (wl.L * (32 + 4 + 4) if "batch" in stages else 0)   # stroke records + 4x4 matrix
 
+    # ---- hit census (untimed): mean number of texels each brush stage writes per step, for the
+    # hit-write term of the algorithmic bytes.  Edited planes are cleared first so that the
+    # kernels' "newly edited" counters equal the hit counts.
+    hits = {s: 0.0 for s in stages}
+    for k in range(args.steps):
+        inp = inputs[args.warmup + k]
+        tool = make_tool(inp)
+        for e in edited:
+            e.zero_()
+        for st in stages:
+            if st in ("tea", "sphere", "batch", "threshold"):
+                r = stage_call(st, inp, tool, True)
+                hits[st] += float(r[0] if st != "batch" else sum(r)) / args.steps
+
     texel_passes = len(stages) * n * world_size
     value = texel_passes * args.steps / (total_ms * 1e-3) / 1e9
     e2e_value = texel_passes * args.steps / (e2e_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
     stage_info = {}
     for st in stages:
-        b = wl.algorithmic_bytes(n, st, T)
+        b = wl.algorithmic_bytes(n, st, T, hits[st])
         gbs = b / (stage_ms[st] * 1e-3) / 1e9
         stage_info[st] = {"ms": round(stage_ms[st], 4), "gtexel_s": round(n / (stage_ms[st] * 1e-3) / 1e9, 2),
                           "alg_bytes": b, "gb_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
-                          "launches": launches[st]}
+                          "hits_per_step": int(hits[st]), "launches": launches[st]}
     dom = max(stages, key=lambda s: stage_ms[s])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(dom)
-    dom_b = wl.algorithmic_bytes(n, dom, T) / launches[dom]
-    dom_ms = stage_ms[dom] / launches[dom]
+    # the dominant stage's main kernel: stage bytes / stage time (for tea the stage is 3 kernels
+    # + the edited-plane reset; its bytes include all of them)
+    dom_b = wl.algorithmic_bytes(n, dom, T, hits[dom])
+    dom_ms = stage_ms[dom]
 
     cpu = None
     if rank == 0 and world_size == 1 and not args.no_cpu:
