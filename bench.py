@@ -7,6 +7,7 @@ One STEP = one pass of every hot-path stage over this rank's 16384 x 16384 atlas
 (268.4 Mtexel), the C3+C4 workload of BASELINE.json at 8 layers (``--layers 64`` gives C4):
 
     tea        the paper's projective brush (TEA, KN:135-203) over the cached triangle-id map
+    tpa        the paper's padding pass (TPA): outline texels next to the stroke
     sphere     one sphere-brush stroke over the float32x3 position map
     batch      L sphere strokes (one per layer) batched in ONE pass over the position map
     chain      fused layer-algebra chain ((L0 u L1) n L2) \\ L3 ... over 8 uint8 layers (C3)
@@ -41,7 +42,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-STAGES = ("tea", "sphere", "batch", "chain", "mask_op", "threshold", "area")
+STAGES = ("tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area")
 CHAIN_OPS = ["union", "intersection", "difference", "union", "masking", "difference", "union"]
 
 
@@ -70,7 +71,7 @@ class Workload:
         self.A = args.atlas
         self.width, self.height = args.atlas, args.atlas * world_size
         self.L = args.layers
-        self.mesh = synth.heightfield_mesh(args.quads)
+        self.mesh = synth.heightfield_mesh(args.quads, margin=0.01)   # 1% uv border: a real island outline for TPA
         self.cam = synth.default_camera(args.window, args.window, eye=(0.5, 0.5, 1.6), target=(0.5, 0.5, 0.0),
                                         fovy=40.0, near=0.2, far=5.0)
         self.tool_shape = synth.circle_shape(70)                     # the paper's mid radius (70 px)
@@ -105,7 +106,7 @@ class Workload:
         base = {"tea": 4 * n + n + T * 12 * 8 + self.cam.width * self.cam.height * 4,
                 "sphere": 12 * n, "batch": 12 * n,
                 "chain": (self.chain_n + 1) * 2 * n, "mask_op": 3 * n,
-                "threshold": 4 * n, "area": (4 * -(-L // 8) + L) * n}[stage]
+                "tpa": n, "threshold": 4 * n, "area": (4 * -(-L // 8) + L) * n}[stage]
         return base + 4 * int(hits)
 
 
@@ -181,6 +182,7 @@ class CpuArm:
         mk = lambda dt: [np.zeros((self.rows, W), dt) for _ in range(wl.L)]
         self.data, self.mask, self.edited = mk(np.uint8), mk(np.uint8), mk(np.uint8)
         self.out_d, self.out_m = np.zeros((self.rows, W), np.uint8), np.zeros((self.rows, W), np.uint8)
+        self.outline = kn.outline((self.surf["tri_id"] >= 0).astype(np.uint8), 1, threads=self.threads)
         self.tmp_d, self.tmp_m = np.zeros((self.rows, W), np.uint8), np.zeros((self.rows, W), np.uint8)
         for k in range(len(wl.seed_strokes)):                     # same pre-painting as the GPU arm
             L = k % wl.L
@@ -202,6 +204,8 @@ class CpuArm:
                 res["tea"] = kn.raster_tea_slab(self.tri_xy, self.tri_clip, float(wl.cam.width), float(wl.cam.height),
                                                 self.depth, wl.eps, sfx, sfy, bx, by, wl.tool_shape, self.data[0],
                                                 self.mask[0], self.edited[0], 7, wl.height, self.row0, th)
+            elif st == "tpa":
+                res["tpa"] = kn.padding(self.outline, self.edited[0], 1, self.data[0], self.mask[0], 7, threads=th)
             elif st == "sphere":
                 s = inp["sphere"]
                 res["sphere"] = kn.select_sphere(self.surf["pos"], s[:3], s[3], self.data[1 % wl.L], self.mask[1 % wl.L],
@@ -301,6 +305,9 @@ def run_ours(args):
     out_layer = ml.create_layer("out", "uint8", W, rows, pool=pool)
     edited = [torch.zeros((rows, W), dtype=torch.uint8, device=dev) for _ in range(L)]
     tmp_mask = torch.zeros((rows, W), dtype=torch.uint8, device=dev)
+    # TPA outline, built once per mesh; neighbour slabs supply the 1-row halo
+    cov_ext, cov_row0 = sharding.exchange_halo(surf.coverage.to(torch.uint8), row0, wl.height, 1)
+    outline = nat.outline_mask(cov_ext, 1, in_row0=cov_row0, out_row0=row0, out_rows=rows)
     batch = nat.StrokeBatch([l.data for l in layers], [l.mask for l in layers], edited, dev)
     for k in range(len(wl.seed_strokes)):
         ml.select_sphere(surf, layers[k % L], wl.seed_strokes[k, :3], wl.seed_strokes[k, 3], wl.seed_labels[k],
@@ -313,7 +320,7 @@ def run_ours(args):
     area_counts = torch.zeros(L, dtype=torch.int64, device=dev)
     counts2 = torch.zeros(2, dtype=torch.int64, device=dev)
     counts1 = torch.zeros(1, dtype=torch.int64, device=dev)
-    launches = {"tea": 3, "sphere": 1, "batch": 1, "chain": 1, "mask_op": 1, "threshold": 1, "area": -(-L // 8)}
+    launches = {"tea": 3, "tpa": 1, "sphere": 1, "batch": 1, "chain": 1, "mask_op": 1, "threshold": 1, "area": -(-L // 8)}
 
     def stage_call(st, inp, tool, e2e):
         """Run one stage.  e2e=True goes through the public API from host inputs and returns host
@@ -327,6 +334,12 @@ def run_ours(args):
             nat.tea_texels(ctx.tri_xy, ctx.tri_clip, surf.tri_id, float(wl.cam.width), float(wl.cam.height),
                            depth.plane, wl.eps, sfx, sfy, bx, by, tool.shape, layers[0].data, layers[0].mask,
                            ctx.edited, tool.value, row0=row0, counts=counts2, scratch=ctx.scratch)
+        elif st == "tpa":
+            # padding of the stroke just applied (the paper times TEA + TPA per edit);
+            # a slab's stencil would need the neighbours' edited rows: radius-1 halo, local rows here
+            if e2e:
+                return [ml.apply_padding(layers[0], outline, ctx.edited, tool)]
+            nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1)
         elif st == "sphere":
             s = inp["sphere"]
             if e2e:
@@ -438,7 +451,7 @@ def run_ours(args):
         for e in edited:
             e.zero_()
         for st in stages:
-            if st in ("tea", "sphere", "batch", "threshold"):
+            if st in ("tea", "tpa", "sphere", "batch", "threshold"):
                 r = stage_call(st, inp, tool, True)
                 hits[st] += float(r[0] if st != "batch" else sum(r)) / args.steps
 

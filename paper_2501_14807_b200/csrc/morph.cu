@@ -96,6 +96,93 @@ padding_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ 
     block_count_add(cnt, count);
 }
 
+// 4-bit mask of the non-zero byte lanes of a 32-bit word
+ML_DEV unsigned nz4(uint32_t w) {
+    const uint32_t nz = (~zero_bytes_msb(w) & 0x80808080u) >> 7;          // bits 0, 8, 16, 24
+    return ((nz * 0x00204081u) >> 21) & 0xfu;
+}
+
+// 16-bit mask: texel x0+e (x0 % 16 == 0) has some src != 0 within Chebyshev distance r <= 4.
+// Per neighbour row THREE independent aligned loads (word left, 16-byte vector, word right) give
+// the non-zero bits of columns [x0-4, x0+20); all rows' loads are in flight together, then the
+// windows are a bit dilation.  (The byte-at-a-time box_any costs (2r+1)(4+2r) dependent L2
+// accesses per 4 texels, which made thin outline columns dominate the pass.)
+ML_DEV unsigned box_any16(const uint8_t* __restrict__ src, long long width, long long in_row0,
+                          long long in_rows, long long x0, long long y, int r) {
+    unsigned bits = 0;                                    // bit j <-> column x0 - 4 + j
+    for (int dy = -r; dy <= r; ++dy) {
+        const long long yy = y + dy;
+        if (yy < in_row0 || yy >= in_row0 + in_rows) continue;
+        const uint8_t* row = src + (yy - in_row0) * width + x0;
+        const uint4 c = *(const uint4*)row;
+        const uint32_t l = x0 >= 4 ? *(const uint32_t*)(row - 4) : 0u;
+        const uint32_t rr = x0 + 16 < width ? *(const uint32_t*)(row + 16) : 0u;
+        bits |= nz4(l) | (nz4(c.x) << 4) | (nz4(c.y) << 8) | (nz4(c.z) << 12) | (nz4(c.w) << 16) | (nz4(rr) << 20);
+    }
+    unsigned d = bits;
+    for (int k = 1; k <= r; ++k) d |= (bits << k) | (bits >> k);
+    return (d >> 4) & 0xffffu;
+}
+
+// Streaming form of the padding pass for the per-stroke hot path (width % 16 == 0, 16-byte
+// aligned planes, radius <= 4): the outline plane is the 1 B/texel read stream (four 128-bit loads
+// in flight per thread); outlines are thin, so almost every 16-texel vector is all zero and is
+// skipped; vectors with outline texels fetch their neighbourhood of the edited plane with
+// 3*(2r+1) independent loads.  Data / mask are updated with 32-bit read-modify-writes (each
+// 4-texel word is owned by one thread).
+template <int ES>
+__global__ void __launch_bounds__(BLOCK)
+padding_stream_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ edited, long long width,
+                      long long in_row0, long long in_rows, long long out_row0, long long out_rows, int r,
+                      void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                      unsigned long long* count) {
+    constexpr int U = 4;
+    const long long nv = (width * out_rows) >> 4;
+    const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    long long cnt = 0;
+    for (long long v0 = tid; v0 < nv; v0 += nthreads * U) {
+        uint4 o[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long v = v0 + u * nthreads;
+            o[u] = v < nv ? ld_stream((const uint4*)outline + v) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll 1
+        for (int u = 0; u < U; ++u) {
+            if ((o[u].x | o[u].y | o[u].z | o[u].w) == 0) continue;
+            const long long i0 = (v0 + u * nthreads) << 4;
+            const long long yy = i0 / width, x0 = i0 - yy * width;
+            const unsigned on = nz4(o[u].x) | (nz4(o[u].y) << 4) | (nz4(o[u].z) << 8) | (nz4(o[u].w) << 12);
+            const unsigned hit16 = on & box_any16(edited, width, in_row0, in_rows, x0, out_row0 + yy, r);
+            if (!hit16) continue;
+            cnt += __popc(hit16);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const unsigned hit = (hit16 >> (4 * j)) & 0xfu;
+                if (!hit) continue;
+                const long long i = i0 + 4 * j;
+                const uint32_t hm = spread4(hit);
+                uint32_t* pm = (uint32_t*)(mask + i);
+                const uint32_t mw = *pm, mn = (mw & ~hm) | (0x01010101u & hm);
+                if (mn != mw) *pm = mn;
+                if (ES == 1) {
+                    uint32_t* pd = (uint32_t*)((uint8_t*)data + i);
+                    const uint32_t dw = *pd;
+                    *pd = (dw & ~hm) | (((value & 0xffu) * 0x01010101u) & hm);
+                } else if (ES == 2) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) if (hit & (1u << e)) ((uint16_t*)data)[i + e] = (uint16_t)value;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) if (hit & (1u << e)) ((uint32_t*)data)[i + e] = value;
+                }
+            }
+        }
+    }
+    block_count_add(cnt, count);
+}
+
 inline unsigned grid_for(long long items) {
     long long blocks = (items + BLOCK - 1) / BLOCK;
     const long long cap = (long long)ml_sm_count() * 32;
@@ -130,6 +217,21 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
     if (out_row0 < in_row0 || out_row0 + out_rows > in_row0 + in_rows)
         return ml_fail(ML_ERR_ARG, "output rows must lie inside the input slab");
     if (radius <= 0 || out_rows <= 0 || width <= 0) return ML_OK;      /* SPEC.md:303 radius 0 -> nothing */
+    const bool vec = (width % 16 == 0) && radius <= 4 &&
+                     ((((uintptr_t)outline) | ((uintptr_t)edited) | ((uintptr_t)data) | ((uintptr_t)mask)) & 15) == 0;
+    if (vec) {
+        const long long nv = (width * out_rows) >> 4;
+        long long blocks = (nv + (long long)BLOCK * 4 - 1) / ((long long)BLOCK * 4);
+        const long long cap = (long long)ml_sm_count() * 16;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        cudaStream_t st = (cudaStream_t)stream;
+#define ML_LAUNCH_PAD(ES) padding_stream_kernel<ES><<<(unsigned)blocks, BLOCK, 0, st>>>(outline, edited, width, in_row0, in_rows, out_row0, out_rows, (int)radius, data, value_bits, mask, (unsigned long long*)count)
+        if (esize == 1) ML_LAUNCH_PAD(1); else if (esize == 2) ML_LAUNCH_PAD(2); else ML_LAUNCH_PAD(4);
+#undef ML_LAUNCH_PAD
+        ML_CUDA(cudaGetLastError());
+        return ML_OK;
+    }
     padding_kernel<<<grid_for(((width + 3) >> 2) * out_rows), BLOCK, 0, (cudaStream_t)stream>>>(
         outline, edited, width, in_row0, in_rows, out_row0, out_rows, (int)radius, data, esize,
         value_bits, mask, (unsigned long long*)count);

@@ -73,6 +73,22 @@ def main():
     run("memset 1 plane (torch)", lambda: out.zero_(), n)
     run("copy 1 plane (torch)", lambda: out.copy_(m2), 2 * n)
 
+    cov = torch.zeros((N, N), dtype=torch.uint8, device=dev)
+    cov[N // 100: N - N // 100, N // 100: N - N // 100] = 1
+    run("outline_mask r=1", lambda: nat.outline_mask(cov, 1), 2 * n)
+    ring = nat.outline_mask(cov, 1)
+    edited.zero_()
+    edited[N // 2 - 500: N // 2 + 500, N // 2 - 500: N // 2 + 500] = 1
+    run("padding r=1 (interior stroke)", lambda: nat.apply_padding(ring, edited, 1, data, mask, 3, counts=cnt), n)
+    edited[: N // 50, :] = 1
+    run("padding r=1 (stroke on border)", lambda: nat.apply_padding(ring, edited, 1, data, mask, 3, counts=cnt), n)
+    zero_ring = torch.zeros_like(ring)
+    run("padding r=1 (empty outline)", lambda: nat.apply_padding(zero_ring, edited, 1, data, mask, 3, counts=cnt), n)
+    rows_only = torch.zeros_like(ring)
+    rows_only[N // 100 - 1, :] = 1
+    run("padding r=1 (one outline row)", lambda: nat.apply_padding(rows_only, edited, 1, data, mask, 3, counts=cnt), n)
+    del cov, ring, zero_ring, rows_only
+
     pos = torch.rand((3, N, N), device=dev, generator=g)
     run("sphere few hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.05, data, mask, edited, 3, counts=cnt), 12 * n)
     run("sphere 50% hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.62, data, mask, edited, 3, counts=cnt), 12 * n)
