@@ -192,6 +192,18 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
                      int64_t radius, void* data, int esize, uint32_t value_bits, uint8_t* mask,
                      uint64_t* count, void* stream);
 
+/* ---- display + layer file helpers (definitions: ext_resolve_display, ext_pack_mask)
+ * SPEC:186-203 resolve_display: rgba_out[i] (4 bytes R,G,B,A) = mask[i] ? palette(u) : 0 with
+ * u = clamp((value-lower)/(upper-lower), 0, 1), piecewise-linear over npoints control points
+ * (HOST arrays: positions[npoints] strictly increasing from 0 to 1, rgba_points[npoints][4] in
+ * [0,1]); channel byte = floor(c*255 + 0.5).  kind is an ML_* plane kind. */
+int ml_resolve_display(const void* data, int kind, const uint8_t* mask, int64_t n,
+                       double lower, double upper, const double* positions, const double* rgba_points,
+                       int npoints, uint8_t* rgba_out, void* stream);
+/* SPEC:221 "mask as packed bits row-major": byte plane <-> (n+7)/8 packed bytes, MSB first. */
+int ml_pack_mask(const uint8_t* mask, int64_t n, uint8_t* bits, void* stream);
+int ml_unpack_mask(const uint8_t* bits, int64_t n, uint8_t* mask, void* stream);
+
 /* ---- host-buffer entry points: exact drop-ins for the reference's numpy signatures ------------
  * All pointers are HOST pointers; the call copies inputs to the device, runs the kernels above,
  * copies the planes back and synchronises.  tri arrays are float64 (the reference widens to

@@ -74,6 +74,10 @@ def lib():
         _lib.ext_padding.argtypes = [vp, vp, i64, i64, i64, vp, i64, vp, vp, i32]
         _lib.ext_mesh_surface_area.restype = dbl
         _lib.ext_mesh_surface_area.argtypes = [vp, i64]
+        _lib.ext_resolve_display.restype = None
+        _lib.ext_resolve_display.argtypes = [vp, i32, vp, i64, dbl, dbl, vp, vp, i32, vp]
+        _lib.ext_pack_mask.restype = None
+        _lib.ext_pack_mask.argtypes = [vp, i64, vp]
     return _lib
 
 
@@ -291,3 +295,22 @@ def padding(outline_mask, edited, radius, data, mask, value, threads=1):
 def mesh_surface_area(tri_pos):
     P = _f64(tri_pos, (3, 3))
     return float(lib().ext_mesh_surface_area(_p(P), P.shape[0]))
+
+
+def resolve_display(data, mask, lower, upper, positions, colours):
+    """(h, w, 4) uint8 RGBA plane of a layer (definition of SPEC.md:195-203 used by the GPU tests)."""
+    data = np.ascontiguousarray(data)
+    mask = np.ascontiguousarray(mask)
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    col = np.ascontiguousarray(colours, dtype=np.float64).reshape(-1, 4)
+    out = np.zeros(mask.shape + (4,), np.uint8)
+    lib().ext_resolve_display(_p(data), KINDS[data.dtype.name], _p(_bytes1(mask)), mask.size, float(lower), float(upper),
+                              _p(pos), _p(col), len(pos), _p(out))
+    return out
+
+
+def pack_mask(mask):
+    mask = np.ascontiguousarray(mask)
+    out = np.zeros((mask.size + 7) // 8, np.uint8)
+    lib().ext_pack_mask(_p(_bytes1(mask)), mask.size, _p(out))
+    return out

@@ -86,6 +86,9 @@ def lib():
         "ml_layer_stats": (i32, [vp, i32, vp, i64, vp, vp]),
         "ml_outline_mask": (i32, [vp, i64, i64, i64, i64, i64, i64, vp, vp]),
         "ml_apply_padding": (i32, [vp, vp, i64, i64, i64, i64, i64, i64, vp, i32, u32, vp, vp, vp]),
+        "ml_resolve_display": (i32, [vp, i32, vp, i64, dbl, dbl, vp, vp, i32, vp, vp]),
+        "ml_pack_mask": (i32, [vp, i64, vp, vp]),
+        "ml_unpack_mask": (i32, [vp, i64, vp, vp]),
         "ml_coverage_fill_host": (i32, [vp, i64, i64, i64, vp, vp]),
         "ml_raster_depth_host": (i32, [vp, vp, i64, vp, i64, i64, vp]),
         "ml_raster_tea_host": (i32, [vp, vp, i64, dbl, dbl, vp, i64, i64, dbl, i32, dbl, dbl, dbl, dbl,
@@ -104,7 +107,8 @@ EXPORTED_SYMBOLS = (
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve", "ml_tea_texels",
     "ml_tea_classify", "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
-    "ml_apply_padding", "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
+    "ml_apply_padding", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
+    "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
 
 
 def _check(rc):
@@ -713,3 +717,39 @@ def apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_
     _check(lib().ml_apply_padding(_ptr(outline), _ptr(edited), w, in_row0, in_rows, out_row0, out_rows,
                                   int(radius), _ptr(data), esize, bits, _ptr(mask), _ptr(ctr), _stream()))
     return None if counts is not None else int(ctr[0].item())
+
+
+def resolve_display(data, mask, lower, upper, positions, colours, out=None):
+    """(rows, width, 4) uint8 RGBA plane; mask false -> (0,0,0,0)."""
+    torch = require_cuda()
+    name = _np_dtype_of(data).name
+    if name not in KIND_CODES or data.numel() != mask.numel() or not data.is_contiguous():
+        raise TargetMismatch("data / mask planes disagree")
+    _byte_plane(mask, "mask")
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    col = np.ascontiguousarray(colours, dtype=np.float64).reshape(-1, 4)
+    if out is None:
+        out = torch.empty(tuple(mask.shape) + (4,), dtype=torch.uint8, device=data.device)
+    _check(lib().ml_resolve_display(_ptr(data), KIND_CODES[name], _ptr(mask), mask.numel(), float(lower), float(upper),
+                                    pos.ctypes.data, col.ctypes.data, len(pos), _ptr(out), _stream()))
+    return out
+
+
+def pack_mask(mask):
+    """Byte mask plane -> packed bits (MSB first), on the device."""
+    torch = require_cuda()
+    _byte_plane(mask, "mask")
+    n = mask.numel()
+    bits = torch.empty((n + 7) // 8, dtype=torch.uint8, device=mask.device)
+    _check(lib().ml_pack_mask(_ptr(mask), n, _ptr(bits), _stream()))
+    return bits
+
+
+def unpack_mask(bits, n, out):
+    """Packed bits -> 0/1 byte plane ``out`` (n texels), on the device."""
+    require_cuda()
+    _byte_plane(out, "mask")
+    if bits.numel() < (n + 7) // 8 or out.numel() != n:
+        raise TargetMismatch("packed mask size mismatch")
+    _check(lib().ml_unpack_mask(_ptr(bits), n, _ptr(out), _stream()))
+    return out

@@ -140,6 +140,10 @@ ML_DEV uint32_t spread4(unsigned hits) {            // 4 bits -> 4 byte lanes of
 ML_DEV uint32_t zero_bytes_msb(uint32_t w) {        // bit 7 of each byte lane set iff that byte == 0
     return ~((((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w)) & 0x80808080u;
 }
+ML_DEV unsigned nz_bits4(uint32_t w) {             // 4-bit mask of the non-zero byte lanes of a word
+    const uint32_t nz = (~zero_bytes_msb(w) & 0x80808080u) >> 7;          // bits 0, 8, 16, 24
+    return ((nz * 0x00204081u) >> 21) & 0xfu;
+}
 // `ew` is the already-loaded 32-bit word edited[i..i+3] (callers load the words of several quads
 // up front so the loads overlap instead of serialising behind the stores).
 template <int ES>

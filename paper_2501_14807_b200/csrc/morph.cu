@@ -97,10 +97,7 @@ padding_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ 
 }
 
 // 4-bit mask of the non-zero byte lanes of a 32-bit word
-ML_DEV unsigned nz4(uint32_t w) {
-    const uint32_t nz = (~zero_bytes_msb(w) & 0x80808080u) >> 7;          // bits 0, 8, 16, 24
-    return ((nz * 0x00204081u) >> 21) & 0xfu;
-}
+ML_DEV unsigned nz4(uint32_t w) { return nz_bits4(w); }
 
 // 16-bit mask: texel x0+e (x0 % 16 == 0) has some src != 0 within Chebyshev distance r <= 4.
 // Per neighbour row THREE independent aligned loads (word left, 16-byte vector, word right) give

@@ -79,6 +79,12 @@ class EditResult:
     duration_ms: float = 0.0
     transfer_bytes: int = TRANSFER_BYTES_PER_STROKE
     _cache: dict = field(default_factory=dict)
+    _padded: object = None
+
+    @property
+    def padded_count(self):
+        """Texels written by the padding pass of ``stroke``."""
+        return self.padded if self._padded is None else int(self._padded.item())
 
     def _read(self):
         if "c" not in self._cache:
@@ -138,6 +144,21 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
     else:
         _native.raster_tea(ctx.tri_xy, ctx.tri_clip, *args, height=s.height, row0=s.row0, counts=counts)
     return EditResult(edited_mask=ctx.edited, _counts=counts)
+
+
+def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):
+    """The service's ``stroke`` (the edit the paper times): TEA
+    (``apply_stroke``) followed by TPA (``apply_padding``) with the tool's padding radius.
+    ``outline`` is the layer-resolution outline mask (``build_outline_mask``).  The padded count
+    stays on the device like the other counters (``EditResult.padded_count``)."""
+    torch = _native._torch()
+    res = apply_stroke(ctx, tool, layer, eps=eps)
+    if tool.padding_radius > 0:
+        pc = torch.zeros(1, dtype=torch.int64, device=ctx.device)
+        as_u8 = outline.view(torch.uint8) if outline.dtype == torch.bool else outline
+        _native.apply_padding(as_u8, ctx.edited, tool.padding_radius, layer.data, layer.mask, tool.value, counts=pc)
+        res._padded = pc
+    return res
 
 
 # --------------------------------------------------------------------------------------------

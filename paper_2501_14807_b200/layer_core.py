@@ -15,10 +15,12 @@ class InformationLayer:
     """data plane + bool mask plane (+ display limits).  ``kind`` is one of
     NUMERIC_KINDS or "uint32" for database layers."""
 
-    def __init__(self, name, kind, data_handle, mask_handle, limits=(0.0, 1.0), table=None):
+    def __init__(self, name, kind, data_handle, mask_handle, limits=(0.0, 1.0), table=None, palette=None):
         if not limits[0] < limits[1]:
             raise TargetMismatch("layer limits must satisfy lower < upper")          # SPEC.md:169
+        from .display import Palette
         self.name, self.kind, self.limits, self.table = name, kind, tuple(limits), table
+        self.palette = palette if palette is not None else Palette.grayscale()
         self._data_handle, self._mask_handle = data_handle, mask_handle
 
     @property
@@ -60,7 +62,7 @@ def create_layer(name, kind, width, height, palette=None, limits=(0.0, 1.0), poo
     except Exception:
         data.release()
         raise
-    return InformationLayer(name, kind, data, mask, limits=limits, table=table)
+    return InformationLayer(name, kind, data, mask, limits=limits, table=table, palette=palette)
 
 
 def _check_pair(a, b, out):

@@ -1,0 +1,238 @@
+"""GPU tests of the SPEC-level surface (pool, layers, stroke pipeline, display, layer files) and
+the acceptance criteria that involve the hot path (SPEC.md:603-617 #1, #2, #4, #5, #9)."""
+import numpy as np
+import pytest
+
+import helpers
+import paper_2501_14807_b200 as ml
+from oracle import kn
+from paper_2501_14807_b200 import _native as nat
+from paper_2501_14807_b200 import synth
+from paper_2501_14807_b200.mesh_core import window_triangles
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ------------------------------------------------------------------ pool / layers
+
+def test_texture_pool_contract():
+    pool = ml.TexturePool(budget_texels=3 * 64 * 64 + 10)
+    a = pool.acquire(64, 64, "uint8")
+    b = pool.acquire(64, 64, "uint8")
+    c = pool.acquire(64, 64, "float32")
+    assert len(pool.keys) == 2 and pool.plane_count((64, 64, "uint8")) == 2
+    assert not bool(a.tensor.any()) and a.tensor.dtype.is_floating_point is False
+    a.tensor.fill_(7)
+    a.release()
+    a2 = pool.acquire(64, 64, "uint8")
+    assert a2.slot == a.slot and not bool(a2.tensor.any())
+    with pytest.raises(ml.CapacityExceeded):
+        pool.acquire(64, 64, "int16")
+    with pytest.raises(ml.TargetMismatch):
+        pool.acquire(0, 4, "uint8")
+    assert (b.kind, c.kind) == ("uint8", "float32")
+
+
+def test_create_layer_and_kinds():
+    pool = ml.TexturePool()
+    for kind in ("int8", "int16", "int32", "uint8", "float16", "float32", "uint32"):
+        L = ml.create_layer("k", kind, 40, 24, pool=pool)
+        assert L.shape == (24, 40) and L.valid_texels() == 0
+    assert (40, 24, "int8") in pool.keys
+    with pytest.raises(ml.TargetMismatch):
+        ml.create_layer("bad", "complex64", 4, 4, pool=pool)
+
+
+# ------------------------------------------------------------------ stroke pipeline vs the oracle
+
+def _scene(level=2, atlas=128, window=96):
+    mesh = synth.icosphere_mesh(level)
+    cam = synth.default_camera(window, window)
+    surf = ml.build_surface_map(mesh, atlas, atlas)
+    depth = ml.render_depth(mesh, cam)
+    return mesh, cam, surf, depth, ml.StrokeContext(mesh, cam, depth, surf)
+
+
+def _oracle_stroke(mesh, cam, tool, atlas, data, mask, edited, eps=1e-4):
+    xy, zn = window_triangles(mesh, cam)
+    d = np.ones((cam.height, cam.width), np.float32)
+    kn.raster_depth(xy, zn, d)
+    sfx, sfy, bx, by = ml.compute_tool_projection(cam, tool).kernel_factors
+    return kn.raster_tea(mesh.tri_uv_texels(atlas, atlas), cam.clip_coords(mesh.vertices)[mesh.triangles],
+                         float(cam.width), float(cam.height), d, eps, sfx, sfy, bx, by, np.asarray(tool.shape),
+                         data, mask, edited, tool.value)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_apply_stroke_equals_oracle_random_scenes(seed):              # SPEC.md:605 acceptance #1
+    """>= 20 randomised scenes: random camera + tool, edited set == oracle exactly, both TEA kernels."""
+    rng = np.random.default_rng(400 + seed)
+    mesh = synth.icosphere_mesh(2)
+    A, W = 128, int(rng.integers(48, 128))
+    eye = rng.normal(size=3)
+    eye = eye / np.linalg.norm(eye) * rng.uniform(1.6, 4.0)
+    cam = synth.default_camera(W, W, eye=tuple(eye), fovy=float(rng.uniform(30, 70)), near=0.3, far=12.0)
+    surf = ml.build_surface_map(mesh, A, A)
+    depth = ml.render_depth(mesh, cam)
+    ctx = ml.StrokeContext(mesh, cam, depth, surf)
+    r = int(rng.integers(3, 30))
+    shape = synth.circle_shape(r) if seed % 2 else synth.square_shape(2 * r)
+    tool = ml.EditingTool(px=float(rng.uniform(0, W)), py=float(rng.uniform(0, W)), shape=shape, value=int(rng.integers(1, 200)))
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool); edited = np.zeros((A, A), np.uint8)
+    want = _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+    for direct in (False, True):
+        layer = ml.create_layer("L", "uint8", A, A, pool=ml.TexturePool())
+        res = ml.apply_stroke(ctx, tool, layer, force_direct=direct)
+        assert (res.edited_count, res.fragments) == want
+        assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+        assert np.array_equal(res.edited_mask.cpu().numpy(), edited)
+        assert res.transfer_bytes == 64                                              # SPEC.md:609 acceptance #5
+
+
+def test_occlusion_safety_coaxial_quads():                            # SPEC.md:285, 606 acceptance #2
+    """Two coaxial quads, many random strokes over the front one: no texel of the occluded quad's
+    uv island (right half of the atlas) is ever edited."""
+    rng = np.random.default_rng(8)
+    mesh = synth.coaxial_quads_mesh()
+    A, W = 128, 128
+    cam = synth.default_camera(W, W, eye=(0.0, 0.0, 4.0), fovy=40.0, near=0.5, far=10.0)
+    surf = ml.build_surface_map(mesh, A, A)
+    ctx = ml.StrokeContext(mesh, cam, ml.render_depth(mesh, cam), surf)
+    layer = ml.create_layer("L", "uint8", A, A, pool=ml.TexturePool())
+    total = 0
+    for k in range(200):
+        tool = ml.EditingTool(px=float(rng.uniform(20, 108)), py=float(rng.uniform(20, 108)),
+                              shape=synth.circle_shape(int(rng.integers(2, 12))), value=1 + k % 200)
+        total += ml.apply_stroke(ctx, tool, layer).edited_count
+    m = layer.mask.cpu().numpy()
+    assert total > 0 and m[:, :A // 2].any()
+    assert not m[:, A // 2:].any()
+
+
+def test_stroke_over_background_and_errors():
+    mesh, cam, surf, depth, ctx = _scene()
+    layer = ml.create_layer("L", "uint8", 128, 128, pool=ml.TexturePool())
+    res = ml.apply_stroke(ctx, ml.EditingTool(px=2.0, py=2.0, shape=synth.circle_shape(2), value=3), layer)
+    assert res.edited_count == 0 and layer.valid_texels() == 0
+    cam.generation += 1                                              # camera moved, depth not re-rendered
+    with pytest.raises(ml.StaleDepth):
+        ml.apply_stroke(ctx, ml.EditingTool(px=48.0, py=48.0, shape=synth.circle_shape(8), value=3), layer)
+    cam.generation -= 1
+    with pytest.raises(ml.TargetMismatch):
+        ml.apply_stroke(ctx, ml.EditingTool(px=48.0, py=48.0, shape=synth.circle_shape(8)),
+                        ml.create_layer("small", "uint8", 64, 64, pool=ml.TexturePool()))
+
+
+def test_stroke_with_padding_equals_oracle():                         # SPEC.md:476, 298, 309; acceptance #4
+    mesh, cam, surf, depth, ctx = _scene()
+    A = 128
+    outline = ml.build_outline_mask(surf.coverage, thickness=1)
+    cov = (surf.tri_id >= 0).cpu().numpy()
+    ref_outline = kn.outline(cov.astype(np.uint8), 1)
+    assert np.array_equal(outline.cpu().numpy(), ref_outline != 0)
+    assert not (ref_outline.astype(bool) & cov).any()
+    tool = ml.EditingTool(px=48.0, py=48.0, shape=synth.circle_shape(14), value=9, padding_radius=1)
+    layer = ml.create_layer("L", "int16", A, A, pool=ml.TexturePool())
+    res = ml.stroke(ctx, tool, layer, outline)
+    data = np.zeros((A, A), np.int16); mask = np.zeros((A, A), bool); edited = np.zeros((A, A), np.uint8)
+    want = _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+    padded = kn.padding(ref_outline, edited, 1, data, mask, 9)
+    assert (res.edited_count, res.fragments) == want and res.padded_count == padded > 0
+    assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+    pad_set = mask & ~edited.astype(bool)
+    assert pad_set.sum() == padded and not (pad_set & cov).any()                     # disjoint, inside outline
+
+
+# ------------------------------------------------------------------ display + files (f3)
+
+@pytest.mark.parametrize("kind", ["uint8", "int16", "float32", "float16", "uint32", "int8", "int32"])
+def test_resolve_display_matches_oracle(kind):
+    import torch
+    rng = np.random.default_rng(11)
+    h, w = 37, 53
+    pal = ml.Palette([0, 0.3, 0.65, 1], rng.random((4, 4)))
+    layer = ml.create_layer("L", kind, w, h, palette=pal, limits=(-5.0, 90.0), pool=ml.TexturePool())
+    data = (rng.normal(size=(h, w)) * 60).astype(kind)
+    mask = rng.random((h, w)) < 0.6
+    if kind == "uint32":
+        layer.data.view(torch.int32).copy_(torch.from_numpy(data.view(np.int32)))
+    else:
+        layer.data.copy_(torch.from_numpy(data))
+    layer.mask.copy_(torch.from_numpy(mask))
+    out = ml.resolve_display(layer).cpu().numpy()
+    assert out.shape == (h, w, 4)
+    assert np.array_equal(out, kn.resolve_display(data, mask.view(np.uint8), -5.0, 90.0, pal.positions, pal.colours))
+    assert (out[~mask] == 0).all()
+
+
+def test_display_known_answers_and_pack():
+    import torch
+    layer = ml.create_layer("L", "float32", 8, 8, limits=(0.0, 10.0), pool=ml.TexturePool())
+    assert not bool(ml.resolve_display(layer).any())                                 # all-false mask
+    layer.data[3, 3] = 5.0
+    layer.mask[3, 3] = True
+    out = ml.resolve_display(layer).cpu().numpy()
+    assert out[3, 3].tolist() == [128, 128, 128, 255] and (out.reshape(-1, 4).any(axis=1).sum() == 1)
+    for n in (1, 7, 8, 9, 1000, 4099):
+        m = (np.random.default_rng(n).random(n) < 0.4).astype(np.uint8) * 3
+        bits = nat.pack_mask(_dev(m))
+        assert np.array_equal(bits.cpu().numpy(), np.packbits(m != 0))
+        back = torch.empty(n, dtype=torch.uint8, device="cuda")
+        assert np.array_equal(nat.unpack_mask(bits, n, back).cpu().numpy(), (m != 0).astype(np.uint8))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_save_load_layer_bit_identical(seed):                         # SPEC.md:207, 613 acceptance #9
+    import torch
+    rng = np.random.default_rng(600 + seed)
+    kind = ["int8", "int16", "int32", "uint8", "float16", "float32", "uint32"][seed % 7]
+    w, h = int(rng.integers(1, 90)), int(rng.integers(1, 90))
+    pal = ml.Palette(np.array([0, 0.5, 1], np.float32), rng.random((3, 4)).astype(np.float32))
+    layer = ml.create_layer("orig", kind, w, h, palette=pal, limits=(-1.0, 7.5), pool=ml.TexturePool(),
+                            table="records" if kind == "uint32" else None)
+    data = (rng.normal(size=(h, w)) * 50).astype(kind)
+    mask = rng.random((h, w)) < 0.5
+    (layer.data.view(torch.int32) if kind == "uint32" else layer.data).copy_(
+        torch.from_numpy(data.view(np.int32) if kind == "uint32" else data))
+    layer.mask.copy_(torch.from_numpy(mask))
+    blob = ml.save_layer(layer)
+    back = ml.load_layer(blob, name="copy", pool=ml.TexturePool())
+    got = back.data.view(torch.int32).cpu().numpy().view(np.uint32) if kind == "uint32" else back.data.cpu().numpy()
+    assert np.array_equal(got.view(np.uint8), data.view(np.uint8)) and np.array_equal(back.mask.cpu().numpy(), mask)
+    assert back.kind == kind and back.limits == (-1.0, 7.5) and back.table == layer.table
+    assert np.array_equal(back.palette.colours, pal.colours) and ml.save_layer(back) == blob
+    with pytest.raises(ml.ChecksumMismatch):
+        ml.load_layer(blob[:-1] + bytes([blob[-1] ^ 1]))
+
+
+# ------------------------------------------------------------------ engine-level algebra / area API
+
+def test_layer_algebra_and_area_api():
+    mesh, cam, surf, depth, ctx = _scene()
+    pool = ml.TexturePool()
+    a, b, c = (ml.create_layer(n, "uint8", 128, 128, pool=pool) for n in "abc")
+    ml.select_sphere(surf, a, (0.0, 0.0, 1.0), 0.5, 3)
+    ml.select_sphere(surf, b, (0.4, 0.0, 0.9), 0.5, 5)
+    na, nb = a.valid_texels(), b.valid_texels()
+    u = ml.layer_union(a, b, out=c)
+    nu = u.valid_texels()
+    i = ml.layer_intersection(a, b, out=ml.create_layer("i", "uint8", 128, 128, pool=pool))
+    d = ml.layer_difference(a, b, out=ml.create_layer("d", "uint8", 128, 128, pool=pool))
+    assert nu == na + nb - i.valid_texels() and d.valid_texels() == na - i.valid_texels()
+    areas, counts = ml.layers_area([a, b, u, i, d], surf)
+    assert counts.tolist() == [na, nb, nu, i.valid_texels(), d.valid_texels()]
+    assert abs(areas[2] - (areas[0] + areas[1] - areas[3])) < 1e-9 * areas[2]        # inclusion-exclusion
+    assert abs(ml.layer_area(d, surf) - areas[4]) < 1e-12
+    chain = ml.layer_chain([a, b, i], ["union", "difference"], ml.create_layer("x", "uint8", 128, 128, pool=pool))
+    assert chain.valid_texels() == nu - i.valid_texels()
+    lab_area, lab_count = ml.label_area(u, surf)
+    assert lab_count[3] == na and lab_count[5] == nu - na and abs(lab_area.sum() - areas[2]) < 1e-9 * areas[2]
+    cnt, s, mn, mx = ml.layer_stats(u)
+    assert (cnt, mn, mx) == (nu, 3.0, 5.0) and s == 3.0 * na + 5.0 * (nu - na)
+    with pytest.raises(ml.TargetMismatch):
+        ml.layer_union(a, ml.create_layer("small", "uint8", 64, 64, pool=pool))
