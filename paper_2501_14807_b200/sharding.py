@@ -116,16 +116,18 @@ def exchange_halo(plane, row0, height, radius):
         return plane, row0
     up_n = min(radius, row0)                                   # rows needed from rank-1 (above = lower rows)
     dn_n = min(radius, height - (row0 + rows))
-    reqs, up, dn = [], None, None
+    # all four transfers go into ONE batch (ncclGroupStart/End under NCCL): posting them one by one
+    # would deadlock, every rank's first operation being a receive
+    ops, up, dn = [], None, None
     if rank > 0:
         up = torch.empty((up_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=plane.device)
-        reqs.append(dist.irecv(up, src=rank - 1))
-        reqs.append(dist.isend(plane[:min(radius, rows)].contiguous(), dst=rank - 1))
+        ops.append(dist.P2POp(dist.irecv, up, rank - 1))
+        ops.append(dist.P2POp(dist.isend, plane[:min(radius, rows)].contiguous(), rank - 1))
     if rank < ws - 1:
         dn = torch.empty((dn_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=plane.device)
-        reqs.append(dist.irecv(dn, src=rank + 1))
-        reqs.append(dist.isend(plane[max(0, rows - radius):].contiguous(), dst=rank + 1))
-    for r in reqs:
+        ops.append(dist.P2POp(dist.irecv, dn, rank + 1))
+        ops.append(dist.P2POp(dist.isend, plane[max(0, rows - radius):].contiguous(), rank + 1))
+    for r in dist.batch_isend_irecv(ops):
         r.wait()
     parts = [p for p in (up, plane, dn) if p is not None]
     return torch.cat(parts, dim=0), row0 - (up.shape[0] if up is not None else 0)

@@ -49,6 +49,39 @@ def main():
         ms = timeit(fn, args.reps)
         print("%-34s %8.4f ms  %8.1f GB/s  %8.1f Gtexel/s" % (name, ms, nbytes / ms / 1e6, n / ms / 1e6), flush=True)
 
+    if not want or any("raster" in w for w in want):
+        # rasteriser: C2 mesh (999,698 triangles) into 4096^2 and 16384^2 atlases; Mtri/s
+        from paper_2501_14807_b200 import synth, mesh_core
+        import paper_2501_14807_b200 as ml
+        mesh = synth.heightfield_mesh(707, margin=0.01)
+        cam = synth.default_camera(1024, 1024, eye=(0.5, 0.5, 1.6), target=(0.5, 0.5, 0.0), fovy=40.0, near=0.2, far=5.0)
+        T = mesh.num_triangles
+        for A in (4096, 16384):
+            xy = torch.from_numpy(mesh.tri_uv_texels(A, A)).to(dev)
+            P, Nn = torch.from_numpy(mesh.tri_pos()).to(dev), torch.from_numpy(mesh.tri_nrm()).to(dev)
+            cov = torch.zeros((A, A), dtype=torch.uint8, device=dev)
+            c2 = torch.zeros(2, dtype=torch.int64, device=dev)
+            for nm, fn in (("raster coverage_fill", lambda: nat.coverage_fill(xy, A, A, cov, counts=c2)),
+                           ("raster surface_map (id+resolve)", lambda: nat.surface_map(xy, P, Nn, A, A))):
+                ms = timeit(fn, 5)
+                print("%-34s %8.3f ms  %8.1f Mtri/s  %8.2f Gtexel/s  (atlas %d^2)" % (nm, ms, T / ms / 1e3, A * A / ms / 1e6, A), flush=True)
+            clip = torch.from_numpy(np.ascontiguousarray(cam.clip_coords(mesh.vertices)[mesh.triangles])).to(dev)
+            depth = ml.render_depth(mesh, cam)
+            shape = nat._as_dev_bytes(synth.circle_shape(70), dev)
+            d = torch.zeros((A, A), dtype=torch.uint8, device=dev)
+            m = torch.zeros((A, A), dtype=torch.uint8, device=dev)
+            e = torch.zeros((A, A), dtype=torch.uint8, device=dev)
+            ms = timeit(lambda: nat.raster_tea(xy, clip, 1024.0, 1024.0, depth.plane, 1e-4, 3.66, 3.66, 0.5, 0.5, shape,
+                                               d, m, e, 7, counts=c2), 5)
+            print("%-34s %8.3f ms  %8.1f Mtri/s  %8.2f Gtexel/s  (atlas %d^2)" % ("raster_tea direct (KN:135)", ms, T / ms / 1e3, A * A / ms / 1e6, A), flush=True)
+            del xy, P, Nn, cov, clip, d, m, e
+        wxy, wzn = mesh_core.window_triangles(mesh, cam)
+        wxy, wzn = torch.from_numpy(wxy).to(dev), torch.from_numpy(wzn).to(dev)
+        dep = torch.ones((1024, 1024), dtype=torch.float32, device=dev)
+        ms = timeit(lambda: (dep.fill_(1.0), nat.raster_depth(wxy, wzn, dep)), 5)
+        print("%-34s %8.3f ms  %8.1f Mtri/s  (window 1024^2)" % ("raster_depth", ms, T / ms / 1e3), flush=True)
+        torch.cuda.empty_cache()
+
     # smooth attribute field: coherent hit regions like a real attribute
     yy, xx = torch.meshgrid(torch.linspace(0, 6, N, device=dev), torch.linspace(0, 6, N, device=dev), indexing="ij")
     attr = (torch.sin(xx) * torch.cos(yy)).contiguous()
