@@ -112,17 +112,31 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
  * second kernel evaluates them with evenly spread parallelism; quads that do not fit are
  * evaluated in the stream kernel, so any size >= 64 bytes is valid.  Results never depend on it.
  * counters: [0] += newly edited texels, [1] += covered texels (== fragments). */
+/* Footprint culling (optional, width % 128 == 0): tile_cur = the tile bitmap ml_tea_classify marked
+ * for this stroke -- row segments outside it are never read, and counters[1] += known_fragments
+ * (the slab's covered-texel count, which a skipping kernel cannot recount); tile_prev (may be NULL)
+ * = the bitmap of the previous stroke on this `edited` plane: its tiles are cleared in the same
+ * pass, which replaces the whole-plane reset of the EditedAreaMask.  Pass NULL, NULL, 0
+ * to stream every texel (then the caller resets `edited` itself). */
 int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
                   const uint32_t* tri_flags, const ml_tea_params* params, void* worklist,
-                  size_t worklist_bytes, void* data, int esize,
+                  size_t worklist_bytes, const uint32_t* tile_cur, const uint32_t* tile_prev,
+                  int64_t known_fragments, void* data, int esize,
                   uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream);
 /* Per-stroke conservative triangle classification from the clip-space vertices alone:
  * bit t (bit t&31 of word t>>5) = 0 iff no fragment of triangle t can pass the w > 0, window and
  * tool-range tests (KN:174, 181, 189) -- see surface.cu for the rounding-error argument.
- * flags: (ntri+31)/32 uint32 words.  O(ntri), no texel work. */
+ * flags: (ntri+31)/32 uint32 words.  O(ntri), no texel work.
+ * tile_bits (may be NULL; else ml_tea_tile_words(width, rows) words, zeroed here): additionally
+ * marks every 128x8-texel tile of the slab that the raster bbox of a flagged triangle touches
+ * (needs tri_xy [ntri][3][2] grid units and the slab geometry) -- the stroke's footprint. */
 int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_tea_params* params,
-                    uint32_t* flags, void* stream);
+                    uint32_t* flags, const void* tri_xy, int64_t width, int64_t height, int64_t row0,
+                    int64_t rows, uint32_t* tile_bits, void* stream);
+/* words of a footprint tile bitmap for a (rows x width) slab; 0 when culling is unavailable
+ * (width % 128 != 0) */
+int ml_tea_tile_words(int64_t width, int64_t rows);
 
 /* ---- selection brushes (north star (2); definitions: ext_select_sphere / ext_select_threshold) -
  * Sphere brush over n texels of a position map (three float32 planes, stride pos_stride):

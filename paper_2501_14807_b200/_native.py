@@ -74,8 +74,9 @@ def lib():
         "ml_raster_tri_id": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
         "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
         "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
-                                vp, i32, u32, vp, vp, vp, vp]),
-        "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp]),
+                                vp, vp, i64, vp, i32, u32, vp, vp, vp, vp]),
+        "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
+        "ml_tea_tile_words": (i32, [i64, i64]),
         "ml_select_sphere": (i32, [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
         "ml_select_sphere_batch": (i32, [vp, i64, i64, vp, vp, vp, i64, vp, vp, vp, i64, i32, vp, vp]),
         "ml_select_threshold": (i32, [vp, i32, vp, i64, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
@@ -105,7 +106,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve", "ml_tea_texels",
-    "ml_tea_classify", "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
+    "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
     "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
@@ -435,12 +436,17 @@ def raster_tri_id(tri_xy, width, height, *, row0=0, rows=None, device=None):
 
 
 def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
-               shape, data, mask, edited, value, *, row0=0, counts=None, classify=True, scratch=None):
+               shape, data, mask, edited, value, *, row0=0, counts=None, classify=True, scratch=None,
+               height=None, tiles=None, known_fragments=0):
     """TEA over the cached triangle-id map (SURVEY.md 8 note N1): same planes and counts as
     ``raster_tea`` when the uv layout has no overlaps.  Returns (edited_texels, fragments).
     ``classify`` runs the per-stroke triangle pre-pass (ml_tea_classify) so that texels of
     triangles outside the tool footprint skip the float64 evaluation; results are identical
-    either way."""
+    either way.  ``tiles=(cur, prev)`` (int32 tensors of ``tea_tile_words`` words, ``prev`` may be
+    None) switches on footprint culling: only tiles a flagged triangle's raster bbox touches are
+    read, the tiles of ``prev`` (the previous stroke's ``cur``) have their ``edited`` bytes
+    cleared, and ``known_fragments`` (the slab's covered texel count) is reported as fragments.
+    The caller must then NOT reset ``edited`` itself and must pass ``height``."""
     torch = require_cuda()
     rows, w = mask.shape
     dev = mask.device
@@ -465,9 +471,16 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
         if scratch is None:
             scratch = tea_scratch(tri.shape[0], rows * w, dev)
         flags, work = scratch
-        _check(lib().ml_tea_classify(_ptr(clip), dt, tri.shape[0], C.byref(p), _ptr(flags), _stream()))
+        cur = tiles[0] if tiles else None
+        if cur is not None and not classify:
+            raise TargetMismatch("footprint culling needs the classification pass")
+        _check(lib().ml_tea_classify(_ptr(clip), dt, tri.shape[0], C.byref(p), _ptr(flags), _ptr(tri), w,
+                                     int(height if height is not None else row0 + rows), row0, rows, _ptr(cur),
+                                     _stream()))
+    cur, prev = tiles if tiles else (None, None)
     _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
                                _ptr(flags), C.byref(p), _ptr(work), 0 if work is None else work.numel() * 8,
+                               _ptr(cur), _ptr(prev), int(known_fragments),
                                _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr), _stream()))
     if counts is not None:
         return None
@@ -481,6 +494,11 @@ def tea_scratch(ntri, ntexels, device, max_quads=1 << 22):
     cap = max(8, min((ntexels + 3) // 4, max_quads))
     return (torch.empty(max(1, (ntri + 31) // 32), dtype=torch.int32, device=device),
             torch.empty(2 + cap, dtype=torch.int64, device=device))
+
+
+def tea_tile_words(width, rows):
+    """Words of a footprint tile bitmap for a slab; 0 when culling is unavailable (width % 128)."""
+    return int(lib().ml_tea_tile_words(int(width), int(rows)))
 
 
 def _check_layer_planes(n, data, mask, edited):

@@ -80,9 +80,14 @@ resolve_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, cons
 //     KN:181 (xn outside [-1,1]).
 // Anything else (mixed signs of w, NaNs) keeps flag 1.  The texel kernel skips flag-0 triangles,
 // which removes the float64 work for everything outside the tool footprint without changing a bit.
+// footprint tiles: 128 texels (one warp-wide 128-bit load) x 8 rows
+constexpr int TILE_W_SHIFT = 7, TILE_H_SHIFT = 3;
+
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
-tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p, uint32_t* __restrict__ bits) {
+tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p, uint32_t* __restrict__ bits,
+                    const T* __restrict__ tri_xy, long long width, long long height, long long row0, long long rows,
+                    uint32_t* __restrict__ tile_bits) {
     // output: a BITMAP (bit t&31 of word t>>5), 125 KB per million triangles, so the texel kernel
     // can keep it in shared memory
     const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
@@ -116,6 +121,20 @@ tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p,
     }
     const unsigned word = __ballot_sync(0xffffffffu, live && keep);
     if ((threadIdx.x & 31) == 0 && live) bits[t >> 5] = word;
+    // Footprint tiles (TILE_W x TILE_H texels): every texel a flagged triangle can own lies in its
+    // raster bbox (the same tri_bbox the rasteriser used), so the marked tiles cover every texel
+    // this stroke can touch; the stream kernel never reads the others.
+    if (tile_bits && live && keep) {
+        TriSetup s;
+        if (tri_load_ccw(tri_xy + 6 * t, s) && tri_bbox(s, width, height, row0, rows)) {
+            const int segs = (int)(width >> TILE_W_SHIFT);
+            for (int ty = (int)(s.iy0 - row0) >> TILE_H_SHIFT; ty <= (int)(s.iy1 - row0) >> TILE_H_SHIFT; ++ty)
+                for (int tx = s.ix0 >> TILE_W_SHIFT; tx <= s.ix1 >> TILE_W_SHIFT; ++tx) {
+                    const int tile = ty * segs + tx;
+                    atomicOr(tile_bits + (tile >> 5), 1u << (tile & 31));
+                }
+        }
+    }
 }
 
 // flag lookup in the classification bitmap (global or shared memory); NULL bitmap = keep all
@@ -156,10 +175,80 @@ struct TeaWork {
     unsigned long long cap;
 };
 
-// STREAM kernel.  One thread per 4 consecutive texels: a 128-bit streaming load of the owner ids
-// (4 B/texel is the whole algorithmic traffic) and a cached 1-byte flag gather per owner.  Quads
-// with at least one texel of a flagged triangle are appended (warp-aggregated atomic) to the work
-// list for the EVAL kernel; if the list is absent or full they are evaluated right here.
+// Footprint culling (optional; needs width % 128 == 0).  tile_cur: tiles this stroke can touch
+// (marked by tea_classify); tile_prev: tiles the previous stroke on this edited plane could touch.
+// The TILE kernel below visits one 128x8 tile per warp: unmarked tiles cost one bitmap word, tiles
+// of tile_prev get their edited bytes cleared (this replaces the whole-plane reset of the
+// EditedAreaMask), tiles of tile_cur are processed like the stream kernel does.
+struct TeaCull {
+    const uint32_t* tile_cur;        // NULL: no culling (stream every texel, count fragments)
+    const uint32_t* tile_prev;       // may be NULL
+    int segs_per_row;
+    unsigned long long known_fragments;   // covered texels of the slab (a skipping kernel cannot count them)
+};
+ML_DEV bool tile_bit(const uint32_t* bits, int tile) { return (__ldg(bits + (tile >> 5)) >> (tile & 31)) & 1u; }
+
+// Shared per-step body of the stream and tile kernels.  Each lane holds U quads (index qs[u], owner
+// ids ids[u]; qs[u] >= nq marks "nothing").  Must be called by all 32 lanes of a warp.
+//   1. flag lookups of all 4*U owners are issued together (independent loads, shared by
+//      neighbouring texels); `keep` = texels of flagged triangles;
+//   2. kept quads are appended to the work list with ONE warp-aggregated atomic per call;
+//   3. whatever did not fit (or everything, without a list) is evaluated inline.
+template <typename T, int ES, int U, bool COUNT_FRAGS>
+ML_DEV void tea_process(const long long (&qs)[U], const uint4 (&ids)[U], long long nq, const uint32_t* flags,
+                        const TeaWork& wk, const TeaParams& p, const T* __restrict__ tri_xy,
+                        const T* __restrict__ tri_clip, long long width, long long row0, bool small,
+                        void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                        uint8_t* __restrict__ edited, int lane, long long& newly, long long& frags) {
+    unsigned keep[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        keep[u] = 0;
+        if (qs[u] >= nq) continue;
+        const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            if (t4[e] >= 0) { if (COUNT_FRAGS) ++frags; if (tri_flag(flags, t4[e])) keep[u] |= 1u << e; }
+    }
+    if (wk.entries) {
+        unsigned bal[U];
+        int total = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) { bal[u] = __ballot_sync(0xffffffffu, keep[u] != 0); total += __popc(bal[u]); }
+        if (total == 0) return;
+        unsigned long long slot = 0;
+        if (lane == 0) slot = atomicAdd(wk.count, (unsigned long long)total);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (keep[u]) {
+                const unsigned long long at = slot + __popc(bal[u] & ((1u << lane) - 1u));
+                if (at < wk.cap) { wk.entries[at] = ((unsigned long long)qs[u] << 4) | keep[u]; keep[u] = 0; }
+            }
+            slot += __popc(bal[u]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {          // inline evaluation: no list, or list overflow
+        if (!keep[u]) continue;
+        const long long q = qs[u];
+        const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
+        unsigned hits = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (!(keep[u] & (1u << e))) continue;
+            int x, y;
+            texel_xy((q << 2) + e, width, row0, small, x, y);
+            if (tea_texel_eval(tri_xy, tri_clip, t4[e], x, y, p)) hits |= 1u << e;
+        }
+        // exactly one thread owns these 4 texels in this kernel: the read-modify-write of
+        // KN:198-202 inside quad_write is race-free
+        if (hits) quad_write<(ES > 0 ? ES : 1)>(data, value, mask, edited, q << 2, hits, newly);
+    }
+}
+
+// STREAM kernel (no culling).  One thread per 4 consecutive texels: a 128-bit streaming load of the
+// owner ids (4 B/texel is the whole algorithmic traffic) and a flag lookup per owner.
 // BS = threads per block; SMEM = the classification bitmap (nwords 32-bit words) is first copied
 // to dynamic shared memory, so the per-texel flag lookup is an LDS instead of a dependent L2 gather.
 template <typename T, int ES, int BS, bool SMEM>
@@ -187,7 +276,7 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
     if (ES > 0) {
         const long long nq = n >> 2;
         constexpr int U = 4;
-        // block-uniform trip count so that the warp-collective append below is convergent
+        // block-uniform trip count so that the warp-collective append is convergent
         for (long long base = (long long)blockIdx.x * BLOCK; base < nq; base += nthreads * U) {
             uint4 ids[U];
             long long qs[U];
@@ -196,54 +285,8 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
                 qs[u] = base + u * nthreads + threadIdx.x;
                 if (qs[u] < nq) ids[u] = ld_stream((const uint4*)tri_id + qs[u]);
             }
-            // all flag gathers of the 16 owners are issued before any is used (independent loads in
-            // flight; neighbouring texels share owners, so they coalesce and hit L1)
-            unsigned keep[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                keep[u] = 0;
-                if (qs[u] >= nq) continue;
-                const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (t4[e] >= 0) { ++frags; if (tri_flag(flags, t4[e])) keep[u] |= 1u << e; }
-            }
-            if (wk.entries) {
-                // one atomic per warp per iteration reserves slots for all its kept quads
-                unsigned bal[U];
-                int total = 0;
-#pragma unroll
-                for (int u = 0; u < U; ++u) { bal[u] = __ballot_sync(0xffffffffu, keep[u] != 0); total += __popc(bal[u]); }
-                if (total == 0) continue;
-                unsigned long long slot = 0;
-                if (lane == 0) slot = atomicAdd(wk.count, (unsigned long long)total);
-                slot = __shfl_sync(0xffffffffu, slot, 0);
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (keep[u]) {
-                        const unsigned long long at = slot + __popc(bal[u] & ((1u << lane) - 1u));
-                        if (at < wk.cap) { wk.entries[at] = ((unsigned long long)qs[u] << 4) | keep[u]; keep[u] = 0; }
-                    }
-                    slot += __popc(bal[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {          // inline evaluation: no list, or list overflow
-                if (!keep[u]) continue;
-                const long long q = qs[u];
-                const int t4[4] = {(int)ids[u].x, (int)ids[u].y, (int)ids[u].z, (int)ids[u].w};
-                unsigned hits = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    if (!(keep[u] & (1u << e))) continue;
-                    int x, y;
-                    texel_xy((q << 2) + e, width, row0, small, x, y);
-                    if (tea_texel_eval(tri_xy, tri_clip, t4[e], x, y, p)) hits |= 1u << e;
-                }
-                // exactly one thread owns these 4 texels in this kernel: the read-modify-write of
-                // KN:198-202 inside quad_write is race-free
-                if (hits) quad_write<(ES > 0 ? ES : 1)>(data, value, mask, edited, q << 2, hits, newly);
-            }
+            tea_process<T, ES, U, true>(qs, ids, nq, flags, wk, p, tri_xy, tri_clip, width, row0, small,
+                                        data, value, mask, edited, lane, newly, frags);
         }
         done = nq << 2;
     }
@@ -260,6 +303,54 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
         mask[i] = 1;
         edited[i] = 1;
     }
+    block_count_add(newly, counters);
+    block_count_add(frags, counters + 1);
+}
+
+// TILE kernel (footprint culling).  One WARP per 128x8-texel tile, grid-stride over all tiles of
+// the slab: a tile outside both bitmaps costs one cached word; a tile of tile_prev has its edited
+// bytes cleared; a tile of tile_cur streams its 8 row segments (8 independent 128-bit id loads per
+// lane) through tea_process.  The stroke therefore reads O(footprint) texels, not O(atlas).
+template <typename T, int ES>
+__global__ void __launch_bounds__(BLOCK)
+tea_tile_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
+                long long row0, long long rows, const int* __restrict__ tri_id,
+                const uint32_t* __restrict__ flags, TeaParams p, TeaWork wk, TeaCull cull,
+                void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                uint8_t* __restrict__ edited, unsigned long long* counters) {
+    constexpr int U = 1 << TILE_H_SHIFT;
+    long long newly = 0, frags = 0;
+    const int lane = threadIdx.x & 31;
+    const long long n = rows * width, nq = n >> 2;
+    const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
+    const int segs = cull.segs_per_row;
+    const int tile_rows = (int)((rows + U - 1) >> TILE_H_SHIFT);
+    const int ntiles = segs * tile_rows;
+    const int nwarps = gridDim.x * (BLOCK / 32);
+    for (int tile = blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); tile < ntiles; tile += nwarps) {
+        const uint32_t cw = __ldg(cull.tile_cur + (tile >> 5));
+        const uint32_t pw = cull.tile_prev ? __ldg(cull.tile_prev + (tile >> 5)) : 0u;
+        const bool cur = (cw >> (tile & 31)) & 1u, prev = (pw >> (tile & 31)) & 1u;
+        if (!cur && !prev) continue;
+        const int ty = tile / segs, tx = tile - ty * segs;
+        long long qs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long yy = ((long long)ty << TILE_H_SHIFT) + u;
+            qs[u] = yy < rows ? ((yy * width + ((long long)tx << TILE_W_SHIFT)) >> 2) + lane : nq;
+        }
+        if (prev) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) if (qs[u] < nq) *(uint32_t*)(edited + (qs[u] << 2)) = 0u;
+        }
+        if (!cur) continue;
+        uint4 ids[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) if (qs[u] < nq) ids[u] = ld_stream((const uint4*)tri_id + qs[u]);
+        tea_process<T, ES, U, false>(qs, ids, nq, flags, wk, p, tri_xy, tri_clip, width, row0, small,
+                                     data, value, mask, edited, lane, newly, frags);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) frags = (long long)cull.known_fragments;
     block_count_add(newly, counters);
     block_count_add(frags, counters + 1);
 }
@@ -314,13 +405,22 @@ constexpr long long TEA_SMEM_MAX_BYTES = 200 * 1024; // bitmap size limit for th
 
 template <typename T, int ES>
 int launch_tea_es(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
-                  const int* tri_id, const uint32_t* bits, long long ntri, const TeaParams& p, TeaWork wk,
+                  const int* tri_id, const uint32_t* bits, long long ntri, const TeaParams& p, TeaWork wk, TeaCull cull,
                   void* data, int esize, uint32_t value, uint8_t* mask, uint8_t* edited,
                   unsigned long long* ctr, cudaStream_t st) {
     const long long nwords = (ntri + 31) / 32;
     const long long items = ES > 0 ? (n + 15) / 16 : n;     // 4 quads (16 texels) per thread iteration
     const bool smem = ES > 0 && bits != nullptr && nwords * 4 <= TEA_SMEM_MAX_BYTES;
-    if (smem) {
+    if (ES > 0 && cull.tile_cur) {
+        const long long rows = n / width;
+        const long long ntiles = (long long)cull.segs_per_row * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
+        long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);
+        const long long cap = (long long)ml_sm_count() * 8;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        tea_tile_kernel<T, (ES > 0 ? ES : 1)><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, rows,
+            tri_id, bits, p, wk, cull, data, value, mask, edited, ctr);
+    } else if (smem) {
         // one 1024-thread block per SM (the bitmap takes most of its shared memory)
         auto kern = tea_stream_kernel<T, ES, TEA_BIG_BLOCK, true>;
         ML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nwords * 4)));
@@ -348,7 +448,7 @@ int launch_tea_es(const T* tri_xy, const T* tri_clip, long long width, long long
 template <typename T>
 int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
                       const int* tri_id, const uint32_t* bits, long long ntri, const TeaParams& p, void* worklist,
-                      size_t worklist_bytes, void* data, int esize, uint32_t value, uint8_t* mask,
+                      size_t worklist_bytes, TeaCull cull, void* data, int esize, uint32_t value, uint8_t* mask,
                       uint8_t* edited, unsigned long long* ctr, cudaStream_t st) {
     const bool vec = ((((uintptr_t)tri_id) | ((uintptr_t)data) | ((uintptr_t)mask) | ((uintptr_t)edited)) & 15) == 0;
     TeaWork wk{nullptr, nullptr, 0};
@@ -358,10 +458,14 @@ int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long 
         wk.cap = (worklist_bytes - 16) / 8;
         ML_CUDA(cudaMemsetAsync(wk.count, 0, 8, st));
     }
-    if (!vec) return launch_tea_es<T, 0>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
-    if (esize == 1) return launch_tea_es<T, 1>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
-    if (esize == 2) return launch_tea_es<T, 2>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
-    return launch_tea_es<T, 4>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, data, esize, value, mask, edited, ctr, st);
+    if (!vec || (width & ((1 << TILE_W_SHIFT) - 1)) != 0 || bits == nullptr) {
+        if (cull.tile_cur) return ml_fail(ML_ERR_ARG, "footprint culling needs width % 128 == 0, aligned planes and triangle flags");
+    }
+    cull.segs_per_row = (int)(width >> TILE_W_SHIFT);
+    if (!vec) return launch_tea_es<T, 0>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
+    if (esize == 1) return launch_tea_es<T, 1>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
+    if (esize == 2) return launch_tea_es<T, 2>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
+    return launch_tea_es<T, 4>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
 }
 
 }  // namespace
@@ -389,14 +493,26 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
     return ML_OK;
 }
 
+int ml_tea_tile_words(int64_t width, int64_t rows) {
+    if (width <= 0 || rows <= 0 || (width & ((1 << TILE_W_SHIFT) - 1)) != 0) return 0;
+    const long long tiles = (width >> TILE_W_SHIFT) * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
+    return (int)((tiles + 31) / 32);
+}
+
 int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_tea_params* tp,
-                    uint32_t* flags, void* stream) {
+                    uint32_t* flags, const void* tri_xy, int64_t width, int64_t height, int64_t row0,
+                    int64_t rows, uint32_t* tile_bits, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (ntri <= 0) return ML_OK;
     TeaParams p = ml_make_tea_params(tp);
+    if (tile_bits) {
+        const int words = ml_tea_tile_words(width, rows);
+        if (words == 0 || tri_xy == nullptr) return ml_fail(ML_ERR_ARG, "tile marking needs tri_xy and width % 128 == 0");
+        ML_CUDA(cudaMemsetAsync(tile_bits, 0, (size_t)words * 4, st));
+    }
     const unsigned grid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
-    if (tri_dtype == ML_F32) tea_classify_kernel<float><<<grid, BLOCK, 0, st>>>((const float*)tri_clip, ntri, p, flags);
-    else if (tri_dtype == ML_F64) tea_classify_kernel<double><<<grid, BLOCK, 0, st>>>((const double*)tri_clip, ntri, p, flags);
+    if (tri_dtype == ML_F32) tea_classify_kernel<float><<<grid, BLOCK, 0, st>>>((const float*)tri_clip, ntri, p, flags, (const float*)tri_xy, width, height, row0, rows, tile_bits);
+    else if (tri_dtype == ML_F64) tea_classify_kernel<double><<<grid, BLOCK, 0, st>>>((const double*)tri_clip, ntri, p, flags, (const double*)tri_xy, width, height, row0, rows, tile_bits);
     else return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
     ML_CUDA(cudaGetLastError());
     return ML_OK;
@@ -405,7 +521,8 @@ int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_
 int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
                   const uint32_t* tri_flags, const ml_tea_params* tp, void* worklist,
-                  size_t worklist_bytes, void* data, int esize,
+                  size_t worklist_bytes, const uint32_t* tile_cur, const uint32_t* tile_prev,
+                  int64_t known_fragments, void* data, int esize,
                   uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
@@ -413,12 +530,13 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
     if (n <= 0) return ML_OK;
     TeaParams p = ml_make_tea_params(tp);
     unsigned long long* ctr = (unsigned long long*)counters;
+    TeaCull cull{tile_cur, tile_cur ? tile_prev : nullptr, 0, (unsigned long long)(known_fragments > 0 ? known_fragments : 0)};
     if (tri_dtype == ML_F32)
         return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, width, row0, n, tri_id, tri_flags, ntri, p,
-                                 worklist, worklist_bytes, data, esize, value_bits, mask, edited, ctr, st);
+                                 worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);
     if (tri_dtype == ML_F64)
         return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, width, row0, n, tri_id, tri_flags, ntri, p,
-                                 worklist, worklist_bytes, data, esize, value_bits, mask, edited, ctr, st);
+                                 worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);
     return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
 }
 

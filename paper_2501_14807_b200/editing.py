@@ -117,12 +117,19 @@ class StrokeContext:
         self.tri_xy = surface.tri_xy
         self.edited = torch.zeros((surface.rows, surface.width), dtype=torch.uint8, device=device)
         self.scratch = _native.tea_scratch(mesh.num_triangles, surface.rows * surface.width, device)
+        # footprint culling state: two tile bitmaps (this stroke / previous stroke) and whether the
+        # edited plane may hold marks outside the previous bitmap (then it is reset as a whole)
+        nwords = _native.tea_tile_words(surface.width, surface.rows)
+        self.tiles = [torch.zeros(nwords, dtype=torch.int32, device=device) for _ in range(2)] if nwords else None
+        self.edited_fully_dirty = False
         self.device = device
 
 
-def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False):
+def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False, cull=True):
     """SPEC.md:277-285 TEA.  Uses the per-texel kernel over the cached triangle-id map when the uv
-    layout has no overlaps (bit-identical), else the direct per-triangle kernel."""
+    layout has no overlaps (bit-identical), else the direct per-triangle kernel.
+    ``cull`` (default) restricts the per-texel kernel to the stroke's footprint tiles, so a stroke
+    costs O(triangles + footprint) instead of O(atlas); results are identical."""
     torch = _native._torch()
     if ctx.depth.generation != ctx.camera.generation:
         raise StaleDepth("depth map was rendered for camera generation %d, camera is at %d"
@@ -133,15 +140,29 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
     if s.covered == 0 and s.row0 == 0 and s.rows == s.height:
         raise LayerMeshMismatch("no uv coverage at layer resolution")
     sfx, sfy, bx, by = compute_tool_projection(ctx.camera, tool).kernel_factors
-    ctx.edited.zero_()
     counts = torch.zeros(2, dtype=torch.int64, device=ctx.device)
     shape = tool.shape if _native._is_cuda_tensor(tool.shape) else _native._as_dev_bytes(tool.shape, ctx.device)
     args = (float(ctx.camera.width), float(ctx.camera.height), ctx.depth.plane, eps, sfx, sfy, bx, by,
             shape, layer.data, layer.mask, ctx.edited, tool.value)
-    if s.overlap == 0 and not force_direct:
+    if s.overlap == 0 and not force_direct and ctx.tiles is not None and cull:
+        # footprint-culled path: the EditedAreaMask reset is done inside the kernel
+        # for the tiles the previous stroke could touch
+        if ctx.edited_fully_dirty:
+            ctx.edited.zero_()
+            ctx.tiles[1].zero_()
+            ctx.edited_fully_dirty = False
+        _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
+                           scratch=ctx.scratch, height=s.height, tiles=(ctx.tiles[0], ctx.tiles[1]),
+                           known_fragments=s.covered)
+        ctx.tiles.reverse()                                   # this stroke's footprint is the next one's "previous"
+    elif s.overlap == 0 and not force_direct:
+        ctx.edited.zero_()
+        ctx.edited_fully_dirty = True
         _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
                            scratch=ctx.scratch)
     else:
+        ctx.edited.zero_()
+        ctx.edited_fully_dirty = True
         _native.raster_tea(ctx.tri_xy, ctx.tri_clip, *args, height=s.height, row0=s.row0, counts=counts)
     return EditResult(edited_mask=ctx.edited, _counts=counts)
 

@@ -94,6 +94,35 @@ def test_apply_stroke_equals_oracle_random_scenes(seed):              # SPEC.md:
         assert res.transfer_bytes == 64                                              # SPEC.md:609 acceptance #5
 
 
+def test_footprint_culling_sequence_equals_oracle():
+    """A sequence of strokes on ONE context: with footprint culling the per-stroke EditedAreaMask
+    (cleared only where the previous stroke could have written) and the layer planes must equal
+    the oracle after every stroke, and the un-culled / direct paths interleaved in between."""
+    import torch
+    rng = np.random.default_rng(21)
+    mesh = synth.icosphere_mesh(3)
+    A, W = 256, 160
+    cam = synth.default_camera(W, W)
+    surf = ml.build_surface_map(mesh, A, A)
+    ctx = ml.StrokeContext(mesh, cam, ml.render_depth(mesh, cam), surf)
+    assert ctx.tiles is not None                                      # 256 % 128 == 0 -> culling available
+    layer = ml.create_layer("L", "uint8", A, A, pool=ml.TexturePool())
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool)
+    modes = ["cull", "cull", "cull", "stream", "cull", "direct", "cull", "cull", "stream", "cull", "cull", "cull"]
+    for k, mode in enumerate(modes):
+        tool = ml.EditingTool(px=float(rng.uniform(30, 130)), py=float(rng.uniform(30, 130)),
+                              shape=synth.circle_shape(int(rng.integers(3, 25))), value=k + 1)
+        edited = np.zeros((A, A), np.uint8)                           # the oracle's mask is fresh per stroke
+        want = _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+        res = ml.apply_stroke(ctx, tool, layer, cull=(mode == "cull"), force_direct=(mode == "direct"))
+        assert (res.edited_count, res.fragments) == want, (k, mode)
+        assert np.array_equal(res.edited_mask.cpu().numpy(), edited), (k, mode)
+        assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+    # a stroke over the background after many strokes leaves an all-zero edited mask
+    res = ml.apply_stroke(ctx, ml.EditingTool(px=1.0, py=1.0, shape=synth.circle_shape(2), value=9), layer)
+    assert res.edited_count == 0 and not bool(res.edited_mask.any())
+
+
 def test_occlusion_safety_coaxial_quads():                            # SPEC.md:285, 606 acceptance #2
     """Two coaxial quads, many random strokes over the front one: no texel of the occluded quad's
     uv island (right half of the atlas) is ever edited."""
