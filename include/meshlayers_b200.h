@@ -108,7 +108,7 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
  * tri_flags (device bitmap of (ntri+31)/32 uint32 words, may be NULL): output of ml_tea_classify
  * for THIS stroke; texels of triangles whose bit is 0 are skipped (provably unaffected).
  * worklist (device scratch, 8-byte aligned, may be NULL): when given, the id stream only COLLECTS
- * the 4-texel quads that need the float64 evaluation (8 bytes each, after a 16-byte header) and a
+ * the 4-texel quads that need the float64 evaluation (24 bytes each, after a 16-byte header) and a
  * second kernel evaluates them with evenly spread parallelism; quads that do not fit are
  * evaluated in the stream kernel, so any size >= 64 bytes is valid.  Results never depend on it.
  * counters: [0] += newly edited texels, [1] += covered texels (== fragments). */

@@ -493,7 +493,7 @@ def tea_scratch(ntri, ntexels, device, max_quads=1 << 22):
     torch = _torch()
     cap = max(8, min((ntexels + 3) // 4, max_quads))
     return (torch.empty(max(1, (ntri + 31) // 32), dtype=torch.int32, device=device),
-            torch.empty(2 + cap, dtype=torch.int64, device=device))
+            torch.empty(2 + 3 * cap, dtype=torch.int64, device=device))
 
 
 def tea_tile_words(width, rows):

@@ -140,11 +140,10 @@ tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p,
 // flag lookup in the classification bitmap (global or shared memory); NULL bitmap = keep all
 ML_DEV bool tri_flag(const uint32_t* bits, int t) { return bits ? ((bits[t >> 5] >> (t & 31)) & 1u) != 0 : true; }
 
-// Full KN:166-193 evaluation of one covered texel for its owner triangle.  Kept out of line so
-// the streaming loop around it stays small.
+// Full KN:166-193 evaluation of one covered texel for its owner triangle.
 template <typename T>
-__device__ __noinline__ bool tea_texel_eval(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
-                                            int t, int x, int y, const TeaParams& p) {
+ML_DEV bool tea_texel_eval_inline(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
+                                  int t, int x, int y, const TeaParams& p) {
     TriSetup s;
     tri_load_ccw(tri_xy + 6ll * t, s);
     double e0, e1, e2;
@@ -155,6 +154,13 @@ __device__ __noinline__ bool tea_texel_eval(const T* __restrict__ tri_xy, const 
 #pragma unroll
     for (int k = 0; k < 4; ++k) { c0[k] = (double)c[k]; c1[k] = (double)c[i1 + k]; c2[k] = (double)c[i2 + k]; }
     return tea_fragment(p, e0, e1, e2, c0, c1, c2);
+}
+// Out-of-line copy for the streaming kernels, whose (rarely taken) inline-evaluation path must not
+// bloat the hot loop; the EVAL kernel, which does nothing else, uses the inline version.
+template <typename T>
+__device__ __noinline__ bool tea_texel_eval(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
+                                            int t, int x, int y, const TeaParams& p) {
+    return tea_texel_eval_inline(tri_xy, tri_clip, t, x, y, p);
 }
 
 // Texel (x, y) of flat slab index i; 32-bit division when the slab is small enough.
@@ -168,7 +174,8 @@ ML_DEV void texel_xy(long long i, long long width, long long row0, bool small, i
     }
 }
 
-// Work list of quads that need the float64 evaluation: entry = (quad index << 4) | keep bits.
+// Work list of quads that need the float64 evaluation.  Entry = 3 x u64: (quad index << 4) | keep
+// bits, then the four owner ids (so the EVAL kernel does not gather them again).
 struct TeaWork {
     unsigned long long* entries;     // NULL: evaluate inline in the stream kernel
     unsigned long long* count;       // device counter (zeroed before the stream kernel)
@@ -223,7 +230,13 @@ ML_DEV void tea_process(const long long (&qs)[U], const uint4 (&ids)[U], long lo
         for (int u = 0; u < U; ++u) {
             if (keep[u]) {
                 const unsigned long long at = slot + __popc(bal[u] & ((1u << lane) - 1u));
-                if (at < wk.cap) { wk.entries[at] = ((unsigned long long)qs[u] << 4) | keep[u]; keep[u] = 0; }
+                if (at < wk.cap) {
+                    unsigned long long* e3 = wk.entries + 3 * at;
+                    e3[0] = ((unsigned long long)qs[u] << 4) | keep[u];
+                    e3[1] = (unsigned long long)ids[u].x | ((unsigned long long)ids[u].y << 32);
+                    e3[2] = (unsigned long long)ids[u].z | ((unsigned long long)ids[u].w << 32);
+                    keep[u] = 0;
+                }
             }
             slot += __popc(bal[u]);
         }
@@ -376,13 +389,14 @@ tea_eval_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, lo
         bool hit = false;
         long long q = 0;
         if (ent < count) {
-            const unsigned long long w = wk.entries[ent];
+            const unsigned long long w = wk.entries[3 * ent];
             q = (long long)(w >> 4);
             if (w & (1ull << e)) {
-                const long long i = (q << 2) + e;
+                const unsigned long long idw = wk.entries[3 * ent + 1 + (e >> 1)];
+                const int t = (int)((e & 1) ? (idw >> 32) : (idw & 0xffffffffull));
                 int x, y;
-                texel_xy(i, width, row0, small, x, y);
-                hit = tea_texel_eval(tri_xy, tri_clip, __ldg(tri_id + i), x, y, p);
+                texel_xy((q << 2) + e, width, row0, small, x, y);
+                hit = tea_texel_eval_inline(tri_xy, tri_clip, t, x, y, p);
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
@@ -455,7 +469,7 @@ int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long 
     if (vec && worklist && worklist_bytes >= 64 && (((uintptr_t)worklist) & 7) == 0) {
         wk.count = (unsigned long long*)worklist;
         wk.entries = wk.count + 2;
-        wk.cap = (worklist_bytes - 16) / 8;
+        wk.cap = (worklist_bytes - 16) / 24;
         ML_CUDA(cudaMemsetAsync(wk.count, 0, 8, st));
     }
     if (!vec || (width & ((1 << TILE_W_SHIFT) - 1)) != 0 || bits == nullptr) {
