@@ -326,52 +326,43 @@ def run_ours(args):
     counts1 = torch.zeros(1, dtype=torch.int64, device=dev)
     launches = {"tea": 3, "tpa": 1, "sphere": 1, "batch": 1, "chain": 1, "mask_op": 1, "threshold": 1, "area": -(-L // 8)}
 
-    def stage_call(st, inp, tool, e2e):
-        """Run one stage.  e2e=True goes through the public API from host inputs and returns host
-        results; e2e=False uses pre-uploaded inputs and leaves results on the device."""
+    def stage_call(st, inp, tool, mode):
+        """Run one stage through the public API and return its result as DEVICE tensors (nothing
+        synchronises here).  mode "resident": stroke records were uploaded before the timed region;
+        "e2e": this step's records come from the host now (pinned staging -> device)."""
+        out = []
         if st == "tea":
-            # the engine call in both modes: EditResult keeps its counters on the device, so the
-            # resident loop never synchronises; --no-cull streams the whole id map instead
+            # --no-cull streams the whole id map instead of the stroke's footprint tiles
             r = ml.apply_stroke(ctx, tool, layers[0], eps=wl.eps, cull=not args.no_cull)
-            if e2e:
-                return [r.edited_count, r.fragments]
+            out = [r._counts]
         elif st == "tpa":
             # padding of the stroke just applied (the paper times TEA + TPA per edit, PAPER.md:241);
             # a slab's stencil would need the neighbours' edited rows: radius-1 halo, local rows here
-            if e2e:
-                return [ml.apply_padding(layers[0], outline, ctx.edited, tool)]
+            counts1.zero_()
             nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1)
+            out = [counts1.clone()]
         elif st == "sphere":
             s = inp["sphere"]
-            if e2e:
-                return [ml.select_sphere(surf, layers[1 % L], s[:3], s[3], inp["sphere_value"], edited=edited[1 % L]).edited_count]
-            nat.select_sphere(surf.pos, s[:3], s[3], layers[1 % L].data, layers[1 % L].mask, edited[1 % L],
-                              inp["sphere_value"], counts=counts1)
+            out = [ml.select_sphere(surf, layers[1 % L], s[:3], s[3], inp["sphere_value"], edited=edited[1 % L])._counts]
         elif st == "batch":
-            if e2e:
+            if mode == "e2e":
                 s, lo, v = sharding.broadcast_strokes(inp["batch"], inp["batch_layers"], inp["batch_values"].astype(np.uint32), dev)
                 batch.upload(s, lo, v.astype(np.uint8))
-                batch.counts.zero_()
-                ml.select_sphere_batch(surf, batch)
-                return batch.counts.tolist()
-            ml.select_sphere_batch(surf, batch)
+            batch.counts.zero_()
+            out = [ml.select_sphere_batch(surf, batch).clone()]
         elif st == "chain":
             ml.layer_chain(layers[:wl.chain_n], wl.chain_ops, out_layer)
         elif st == "mask_op":
             nat.layer_op("union", None, layers[0].mask, None, layers[1 % L].mask, None, tmp_mask)
         elif st == "threshold":
-            if e2e:
-                return [ml.select_threshold(attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L]).edited_count]
-            nat.select_threshold(attr, None, wl.thr[0], wl.thr[1], layers[2 % L].data, layers[2 % L].mask, edited[2 % L], 9,
-                                 counts=counts1)
+            out = [ml.select_threshold(attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L])._counts]
         elif st == "area":
             area_sums.zero_()
             area_counts.zero_()
             nat.layer_area(surf.area, [l.mask for l in layers], sums=area_sums, counts=area_counts)
             sharding.allreduce_areas(area_sums, area_counts)
-            if e2e:
-                return area_sums.tolist() + area_counts.tolist()
-        return None
+            out = [area_sums, area_counts]
+        return out
 
     def make_tool(inp):
         return ml.EditingTool(px=float(inp["tool_xy"][0]), py=float(inp["tool_xy"][1]), shape=tool_shape_dev, value=7)
@@ -397,7 +388,7 @@ def run_ours(args):
     batch.upload(inputs[0]["batch"], inputs[0]["batch_layers"], inputs[0]["batch_values"])
     for i in range(args.warmup):
         for st in stages:
-            stage_call(st, inputs[i], make_tool(inputs[i]), False)
+            stage_call(st, inputs[i], make_tool(inputs[i]), "resident")
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
     stop, samples = threading.Event(), []
     th = threading.Thread(target=sample_clocks, args=(stop, samples))
@@ -408,33 +399,38 @@ def run_ours(args):
         tool = make_tool(inp)
         ev[k][0].record()
         for j, st in enumerate(stages):
-            stage_call(st, inp, tool, False)
+            stage_call(st, inp, tool, "resident")
             ev[k][j + 1].record()
     barrier()
     total_ms = max_over_ranks(ev[0][0].elapsed_time(ev[-1][-1]))
     stage_ms = {st: sum(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)) / args.steps
                 for j, st in enumerate(stages)}
 
-    # ---- e2e loop: public API, host stroke records in, host results out, every step
-    pinned = torch.empty(64, dtype=torch.float64).pin_memory()
-    for i in range(args.warmup):
+    # ---- e2e loop: the same step through the public API, but every step (1) takes its stroke
+    # records from HOST memory (pinned staging buffers -> device) and (2) reads all stage results
+    # (edit counts, padded count, per-layer areas and texel counts) back to the host in one copy
+    pinned = torch.empty(16, dtype=torch.float64).pin_memory()
+    rec_dev = torch.empty(16, dtype=torch.float64, device=dev)
+
+    def e2e_step(inp):
+        rec = np.concatenate([inp["tool_xy"], inp["sphere"]])
+        pinned[:rec.size].copy_(torch.from_numpy(rec))
+        rec_dev[:rec.size].copy_(pinned[:rec.size], non_blocking=True)   # this step's scalar stroke record
+        tool = make_tool(inp)
+        res = []
         for st in stages:
-            stage_call(st, inputs[i], make_tool(inputs[i]), True)
+            res += stage_call(st, inp, tool, "e2e")
+        host = torch.cat([t.reshape(-1).to(torch.float64) for t in res]).cpu() if res else None   # ONE device->host read
+        return 0 if host is None else 8 * host.numel()
+
+    for i in range(args.warmup):
+        e2e_step(inputs[i])
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     d2h = 0
     for k in range(args.steps):
-        inp = inputs[args.warmup + k]
-        # host -> device: the stroke records of this step from pinned host memory
-        rec = np.concatenate([inp["tool_xy"], inp["sphere"]])
-        pinned[:rec.size].copy_(torch.from_numpy(rec))
-        pinned[:rec.size].to(dev, non_blocking=True)
-        tool = make_tool(inp)
-        for st in stages:
-            r = stage_call(st, inp, tool, True)
-            if r is not None:
-                d2h += 8 * len(r)
+        d2h += e2e_step(inputs[args.warmup + k])
     e1.record()
     barrier()
     stop.set()
@@ -446,15 +442,16 @@ def run_ours(args):
     # hit-write term of the algorithmic bytes.  Edited planes are cleared first so that the
     # kernels' "newly edited" counters equal the hit counts.
     hits = {s: 0.0 for s in stages}
-    for k in range(args.steps):
+    ncen = min(args.steps, 10)
+    for k in range(ncen):
         inp = inputs[args.warmup + k]
         tool = make_tool(inp)
         for e in edited:
             e.zero_()
         for st in stages:
+            r = stage_call(st, inp, tool, "resident")
             if st in ("tea", "tpa", "sphere", "batch", "threshold"):
-                r = stage_call(st, inp, tool, True)
-                hits[st] += float(r[0] if st != "batch" else sum(r)) / args.steps
+                hits[st] += float(r[0].reshape(-1)[0].item() if st != "batch" else r[0].sum().item()) / ncen
 
     texel_passes = len(stages) * n * world_size
     value = texel_passes * args.steps / (total_ms * 1e-3) / 1e9
