@@ -15,7 +15,7 @@ import sys
 
 STAGE_OF = (("chain_kernel", "chain"), ("binary_kernel", "mask_op"), ("sphere_batch_kernel", "batch"),
             ("sphere_kernel", "sphere"), ("threshold_kernel", "threshold"), ("area_kernel", "area"),
-            ("tea_stream_kernel", "tea"))
+            ("tea_eval_kernel", "tea"))
 
 METRICS = [
     ("gpu__time_duration.sum", "time"),
