@@ -115,6 +115,15 @@ def coaxial_quads_mesh():
                         uvs=np.array(uv, np.float64), triangles=np.array(tris, np.int64))
 
 
+def flat_square_mesh(side=1.0):
+    """SPEC.md:539 / acceptance #8: flat square of ``side`` units in the z=0 plane whose uv chart fills
+    the whole atlas, so every texel is covered and precision = side^2 / resolution^2."""
+    P = [(0.0, 0.0, 0.0), (side, 0.0, 0.0), (side, side, 0.0), (0.0, side, 0.0)]
+    uv = [(0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0)]
+    return TriangleMesh(vertices=np.array(P, np.float64), normals=np.array([(0, 0, 1)] * 4, np.float64),
+                        uvs=np.array(uv, np.float64), triangles=np.array([(0, 1, 2), (0, 2, 3)], np.int64))
+
+
 def random_soup(rng, ntri, extent, dtype=np.float64, degenerate_frac=0.05, snap_frac=0.3):
     """Random overlapping triangle soup in grid units for rasteriser parity tests: mixes sizes,
     windings, vertices snapped to texel centres / corners (tie-rule stress) and degenerates."""
