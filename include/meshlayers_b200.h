@@ -96,11 +96,14 @@ int ml_raster_tri_id(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t wi
 /* Pass 2: per texel, interpolate the owner triangle's attributes.  pos / nrm are three float32
  * planes each (plane stride = rows*width elements), area one float32 plane.  Uncovered texels:
  * pos = NaN, nrm = 0, area = 0.  tri_pos / tri_nrm [ntri][3][3].  *covered (device, zeroed)
- * += covered texels. */
+ * += covered texels.  workspace: ml_surface_workspace_bytes(ntri) bytes of device scratch for the
+ * per-triangle records (CCW vertices, texel area) a pre-pass writes once per call. */
 int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_nrm, int tri_dtype,
                        int64_t ntri, int64_t width, int64_t row0, int64_t rows,
                        const int32_t* tri_id, float* pos, float* nrm, float* area,
-                       uint64_t* covered, void* stream);
+                       uint64_t* covered, void* workspace, size_t workspace_bytes, void* stream);
+/* Device scratch of ml_surface_resolve (64-byte per-triangle records; 16-byte aligned). */
+size_t ml_surface_workspace_bytes(int64_t ntri);
 
 /* ---- TEA over the cached triangle-id map (SURVEY.md 8 note N1) ---------------------------------
  * Bit-identical to ml_raster_tea when no two triangles overlap in uv space (overlap events == 0):

@@ -72,7 +72,8 @@ def lib():
         "ml_raster_tea": (i32, [vp, vp, i32, i64, i64, i64, i64, i64, C.POINTER(_TeaParams), vp, i32,
                                 u32, vp, vp, vp, vp, sz, vp]),
         "ml_raster_tri_id": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
-        "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
+        "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "ml_surface_workspace_bytes": (sz, [i64]),
         "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
                                 vp, vp, i64, vp, i32, u32, vp, vp, vp, vp]),
         "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
@@ -105,7 +106,8 @@ def lib():
 
 EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
-    "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve", "ml_tea_texels",
+    "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve",
+    "ml_surface_workspace_bytes", "ml_tea_texels",
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
@@ -412,9 +414,11 @@ def surface_map(tri_xy, tri_pos, tri_nrm, width, height, *, row0=0, rows=None, d
     ws, nb = _workspace(T, device)
     _check(L.ml_raster_tri_id(_ptr(tri), dt, T, width, height, row0, rows, _ptr(tri_id), _ptr(ctr),
                               _ptr(ws), nb, _stream()))
+    sb = int(L.ml_surface_workspace_bytes(T))
+    recs = torch.empty(sb, dtype=torch.uint8, device=device)       # per-triangle records, freed after the build
     _check(L.ml_surface_resolve(_ptr(tri), _ptr(P), _ptr(N), dt, T, width, row0, rows, _ptr(tri_id),
                                 _ptr(pos), _ptr(nrm), _ptr(area), C.c_void_p(ctr.data_ptr() + 16),
-                                _stream()))
+                                _ptr(recs), sb, _stream()))
     c = ctr.tolist()
     return dict(tri_id=tri_id, pos=pos, nrm=nrm, area=area, fragments=int(c[0]), overlap=int(c[1]),
                 covered=int(c[2]))

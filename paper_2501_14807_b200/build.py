@@ -18,6 +18,7 @@ NVCC_FLAGS = [
     "-lineinfo",
     "-fmad=false",            # the reference's arithmetic contract forbids contraction (setup.py:13)
     "-Xcompiler", "-fPIC", "-shared",
+    "--threads", "0",         # one compile job per source file
 ]
 
 

@@ -14,17 +14,87 @@ namespace {
 
 constexpr int BLOCK = 256;
 
+// Texel (x, y) of flat slab index i; 32-bit division when the slab is small enough.
+ML_DEV void texel_xy(long long i, long long width, long long row0, bool small, int& x, int& y) {
+    if (small) {
+        const unsigned yy = (unsigned)i / (unsigned)width;
+        x = (int)((unsigned)i - yy * (unsigned)width); y = (int)(row0 + yy);
+    } else {
+        const long long yy = i / width;
+        x = (int)(i - yy * width); y = (int)(row0 + yy);
+    }
+}
+
+// Per-triangle record of the resolve pass (208 bytes = 13 x 16, written once per build by
+// tri_prepare_kernel): the CCW-normalised uv vertices (KN:32-41), the texel area of the triangle
+// (3D area / uv area, constant over the triangle) and the position / normal attributes widened to
+// float64 in CCW vertex order (KN:40 swaps the attributes with the vertices).  The per-texel kernel
+// fetches it with thirteen independent 128-bit loads issued back to back, and neither re-derives
+// the winding nor repeats the cross product, square root and division for every texel.
+struct __align__(16) TriRec {
+    double x0, y0, x1, y1, x2, y2;
+    float area;
+    uint32_t flags;                   // bit 0 valid, bit 1 vertices 1 and 2 were exchanged
+    double pad;
+    double p[9];                      // p0.xyz, p1.xyz, p2.xyz (CCW order)
+    double nrm[9];
+};
+static_assert(sizeof(TriRec) == 208, "TriRec is thirteen 16-byte words");
+
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
-resolve_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, const T* __restrict__ tri_nrm,
-               long long width, long long row0, long long n, const int* __restrict__ tri_id,
-               float* __restrict__ pos, float* __restrict__ nrm, float* __restrict__ area,
-               unsigned long long* covered) {
+tri_prepare_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, const T* __restrict__ tri_nrm,
+                   long long ntri, TriRec* __restrict__ recs) {
+    const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    if (t >= ntri) return;
+    TriSetup s;
+    TriRec& r = recs[t];
+    if (!tri_load_ccw(tri_xy + 6 * t, s)) {       // degenerate / non-finite: never owns a texel
+        r.flags = 0u;
+        return;
+    }
+    r.x0 = s.x0; r.y0 = s.y0; r.x1 = s.x1; r.y1 = s.y1; r.x2 = s.x2; r.y2 = s.y2;
+    r.flags = 1u | (s.swapped ? 2u : 0u);
+    r.pad = 0.0;
+    const int i1 = s.swapped ? 6 : 3, i2 = s.swapped ? 3 : 6;
+    const T* P = tri_pos + 9 * t;
+    const T* N = tri_nrm + 9 * t;
+    double p0[3], p1[3], p2[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        p0[c] = (double)P[c]; p1[c] = (double)P[i1 + c]; p2[c] = (double)P[i2 + c];
+        r.p[c] = p0[c]; r.p[3 + c] = p1[c]; r.p[6 + c] = p2[c];
+        r.nrm[c] = (double)N[c]; r.nrm[3 + c] = (double)N[i1 + c]; r.nrm[6 + c] = (double)N[i2 + c];
+    }
+    const double ux = xsub(p1[0], p0[0]), uy = xsub(p1[1], p0[1]), uz = xsub(p1[2], p0[2]);
+    const double vx = xsub(p2[0], p0[0]), vy = xsub(p2[1], p0[1]), vz = xsub(p2[2], p0[2]);
+    const double crx = xsub(xmul(uy, vz), xmul(uz, vy));
+    const double cry = xsub(xmul(uz, vx), xmul(ux, vz));
+    const double crz = xsub(xmul(ux, vy), xmul(uy, vx));
+    const double a3 = xmul(__dsqrt_rn(xadd(xadd(xmul(crx, crx), xmul(cry, cry)), xmul(crz, crz))), 0.5);
+    // |area2| of the CCW-normalised triangle: swapping two vertices negates KN:35 exactly
+    const double area2 = xsub(xmul(s.cx, xsub(s.y2, s.y0)), xmul(s.cy, xsub(s.x2, s.x0)));
+    const double a2 = xmul(fabs(area2), 0.5);
+    r.area = (float)xdiv(a3, a2);
+}
+
+// One thread per texel, consecutive lanes on consecutive texels: id reads and the seven plane
+// stores are coalesced streams; the record gathers hit L1 because neighbours share owners.  The
+// next iteration's id is fetched before this iteration's arithmetic, and the whole record is loaded
+// before the first division (whose slow-path call would otherwise fence the remaining loads).
+template <bool SMALL>
+__global__ void __launch_bounds__(BLOCK, 2)
+resolve_kernel(const TriRec* __restrict__ recs, long long width, long long row0, long long n,
+               const int* __restrict__ tri_id, float* __restrict__ pos, float* __restrict__ nrm,
+               float* __restrict__ area, unsigned long long* covered) {
     long long cnt = 0;
     const long long stride = (long long)gridDim.x * BLOCK;
-    for (long long i = (long long)blockIdx.x * BLOCK + threadIdx.x; i < n; i += stride) {
-        const int t = tri_id[i];
-        if (t < 0) {
+    long long i = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    int t = i < n ? (int)ld_stream((const uint32_t*)tri_id + i) : -1;
+    for (; i < n; i += stride) {
+        const int tcur = t;
+        if (i + stride < n) t = (int)ld_stream((const uint32_t*)tri_id + i + stride);
+        if (tcur < 0) {
             const float qnan = __int_as_float(0x7fc00000);
             pos[i] = qnan; pos[n + i] = qnan; pos[2 * n + i] = qnan;
             nrm[i] = 0.f; nrm[n + i] = 0.f; nrm[2 * n + i] = 0.f;
@@ -32,37 +102,32 @@ resolve_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, cons
             continue;
         }
         ++cnt;
-        const long long yy = i / width;
-        const int x = (int)(i - yy * width), y = (int)(row0 + yy);
-        TriSetup s;
-        tri_load_ccw(tri_xy + 6ll * t, s);
-        double e0, e1, e2;
-        tri_inside(s, x, y, e0, e1, e2);
+        const double2* rp = (const double2*)(recs + tcur);
+        double2 w[13];
+#pragma unroll
+        for (int k = 0; k < 13; ++k) w[k] = __ldg(rp + k);
+        int x, y;
+        texel_xy(i, width, row0, SMALL, x, y);
+        const double x0 = w[0].x, y0 = w[0].y, x1 = w[1].x, y1 = w[1].y, x2 = w[2].x, y2 = w[2].y;
+        const double cx = xadd((double)x, 0.5), cy = xadd((double)y, 0.5);                    // KN:60, 63
+        const double e0 = xsub(xmul(xsub(x2, x1), xsub(cy, y1)), xmul(xsub(y2, y1), xsub(cx, x1)));   // KN:72
+        const double e1 = xsub(xmul(xsub(x0, x2), xsub(cy, y2)), xmul(xsub(y0, y2), xsub(cx, x2)));   // KN:73
+        const double e2 = xsub(xmul(xsub(x1, x0), xsub(cy, y0)), xmul(xsub(y1, y0), xsub(cx, x0)));   // KN:74
         const double esum = xadd(xadd(e0, e1), e2);
         const double l0 = xdiv(e0, esum), l1 = xdiv(e1, esum), l2 = xdiv(e2, esum);
-        const int i1 = s.swapped ? 6 : 3, i2 = s.swapped ? 3 : 6;
-        const T* P = tri_pos + 9ll * t;
-        const T* N = tri_nrm + 9ll * t;
-        double p0[3], p1[3], p2[3], nv[3];
+        // attributes: w[4..8] = p[0..8] and nrm[0], w[8].y.. = nrm
+        const double a[18] = {w[4].x, w[4].y, w[5].x, w[5].y, w[6].x, w[6].y, w[7].x, w[7].y, w[8].x,
+                              w[8].y, w[9].x, w[9].y, w[10].x, w[10].y, w[11].x, w[11].y, w[12].x, w[12].y};
+        double nv[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            p0[c] = (double)P[c]; p1[c] = (double)P[i1 + c]; p2[c] = (double)P[i2 + c];
-            pos[c * n + i] = (float)xadd(xadd(xmul(l0, p0[c]), xmul(l1, p1[c])), xmul(l2, p2[c]));
-            nv[c] = xadd(xadd(xmul(l0, (double)N[c]), xmul(l1, (double)N[i1 + c])), xmul(l2, (double)N[i2 + c]));
+            pos[c * n + i] = (float)xadd(xadd(xmul(l0, a[c]), xmul(l1, a[3 + c])), xmul(l2, a[6 + c]));
+            nv[c] = xadd(xadd(xmul(l0, a[9 + c]), xmul(l1, a[12 + c])), xmul(l2, a[15 + c]));
         }
         const double len = __dsqrt_rn(xadd(xadd(xmul(nv[0], nv[0]), xmul(nv[1], nv[1])), xmul(nv[2], nv[2])));
 #pragma unroll
         for (int c = 0; c < 3; ++c) nrm[c * n + i] = (len > 0.0) ? (float)xdiv(nv[c], len) : 0.f;
-        const double ux = xsub(p1[0], p0[0]), uy = xsub(p1[1], p0[1]), uz = xsub(p1[2], p0[2]);
-        const double vx = xsub(p2[0], p0[0]), vy = xsub(p2[1], p0[1]), vz = xsub(p2[2], p0[2]);
-        const double crx = xsub(xmul(uy, vz), xmul(uz, vy));
-        const double cry = xsub(xmul(uz, vx), xmul(ux, vz));
-        const double crz = xsub(xmul(ux, vy), xmul(uy, vx));
-        const double a3 = xmul(__dsqrt_rn(xadd(xadd(xmul(crx, crx), xmul(cry, cry)), xmul(crz, crz))), 0.5);
-        // |area2| of the CCW-normalised triangle: swapping two vertices negates KN:35 exactly
-        const double area2 = xsub(xmul(s.cx, xsub(s.y2, s.y0)), xmul(s.cy, xsub(s.x2, s.x0)));
-        const double a2 = xmul(fabs(area2), 0.5);
-        area[i] = (float)xdiv(a3, a2);
+        area[i] = __uint_as_float((uint32_t)__double_as_longlong(w[3].x));      // low word of bytes 48..55 = TriRec::area
     }
     block_count_add(cnt, covered);
 }
@@ -161,17 +226,6 @@ template <typename T>
 __device__ __noinline__ bool tea_texel_eval(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
                                             int t, int x, int y, const TeaParams& p) {
     return tea_texel_eval_inline(tri_xy, tri_clip, t, x, y, p);
-}
-
-// Texel (x, y) of flat slab index i; 32-bit division when the slab is small enough.
-ML_DEV void texel_xy(long long i, long long width, long long row0, bool small, int& x, int& y) {
-    if (small) {
-        const unsigned yy = (unsigned)i / (unsigned)width;
-        x = (int)((unsigned)i - yy * (unsigned)width); y = (int)(row0 + yy);
-    } else {
-        const long long yy = i / width;
-        x = (int)(i - yy * width); y = (int)(row0 + yy);
-    }
 }
 
 // Work list of quads that need the float64 evaluation.  Entry = 3 x u64: (quad index << 4) | keep
@@ -486,23 +540,30 @@ int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long 
 
 extern "C" {
 
+size_t ml_surface_workspace_bytes(int64_t ntri) { return (size_t)(ntri > 0 ? ntri : 0) * sizeof(TriRec) + 64; }
+
 int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_nrm, int tri_dtype,
                        int64_t ntri, int64_t width, int64_t row0, int64_t rows,
                        const int32_t* tri_id, float* pos, float* nrm, float* area,
-                       uint64_t* covered, void* stream) {
-    (void)ntri;
+                       uint64_t* covered, void* workspace, size_t workspace_bytes, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const long long n = (long long)rows * width;
     if (n <= 0) return ML_OK;
+    if (tri_dtype != ML_F32 && tri_dtype != ML_F64) return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+    if (workspace == nullptr || workspace_bytes < ml_surface_workspace_bytes(ntri) || (((uintptr_t)workspace) & 15))
+        return ml_fail(ML_ERR_ARG, "surface resolve needs a 16-byte aligned workspace of ml_surface_workspace_bytes(ntri)");
     unsigned long long* ctr = (unsigned long long*)covered;
-    if (tri_dtype == ML_F32)
-        resolve_kernel<float><<<grid_for(n), BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_pos,
-            (const float*)tri_nrm, width, row0, n, tri_id, pos, nrm, area, ctr);
-    else if (tri_dtype == ML_F64)
-        resolve_kernel<double><<<grid_for(n), BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_pos,
-            (const double*)tri_nrm, width, row0, n, tri_id, pos, nrm, area, ctr);
-    else
-        return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+    TriRec* recs = (TriRec*)workspace;
+    const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
+    const unsigned pgrid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
+    if (ntri > 0) {
+        if (tri_dtype == ML_F32)
+            tri_prepare_kernel<float><<<pgrid, BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_pos, (const float*)tri_nrm, ntri, recs);
+        else
+            tri_prepare_kernel<double><<<pgrid, BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_pos, (const double*)tri_nrm, ntri, recs);
+    }
+    if (small) resolve_kernel<true><<<grid_for(n), BLOCK, 0, st>>>(recs, width, row0, n, tri_id, pos, nrm, area, ctr);
+    else resolve_kernel<false><<<grid_for(n), BLOCK, 0, st>>>(recs, width, row0, n, tri_id, pos, nrm, area, ctr);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }
