@@ -144,23 +144,39 @@ ML_DEV unsigned nz_bits4(uint32_t w) {             // 4-bit mask of the non-zero
     const uint32_t nz = (~zero_bytes_msb(w) & 0x80808080u) >> 7;          // bits 0, 8, 16, 24
     return ((nz * 0x00204081u) >> 21) & 0xfu;
 }
-// `ew` is the already-loaded 32-bit word edited[i..i+3] (callers load the words of several quads
-// up front so the loads overlap instead of serialising behind the stores).
+// The write is split in two so that a thread holding several hit quads can issue ALL its old-word
+// loads before the first store (independent loads overlap; a load behind a store to a may-alias
+// plane would serialise a DRAM round trip per plane per quad):
+//   quad_load   : edited word (always, for the 0 -> 1 count); mask and 1-byte data words only when
+//                 the quad is partially hit (a fully hit quad overwrites them).
+//   quad_commit : merge + store, skipping stores that would not change the word.
 template <int ES>
-ML_DEV void quad_write_pre(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i,
-                           unsigned hits, uint32_t ew, long long& cnt) {
+ML_DEV void quad_load(const void* data, const uint8_t* mask, const uint8_t* edited, long long i,
+                      unsigned hits, uint32_t& ew, uint32_t& mw, uint32_t& dw) {
+    ew = 0u; mw = 0u; dw = 0u;
+    if (!hits) return;
+    ew = *(const uint32_t*)(edited + i);
+    if (hits != 0xfu) {
+        mw = *(const uint32_t*)(mask + i);
+        if (ES == 1) dw = *(const uint32_t*)((const uint8_t*)data + i);
+    }
+}
+template <int ES>
+ML_DEV void quad_commit(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i,
+                        unsigned hits, uint32_t ew, uint32_t mw, uint32_t dw, long long& cnt) {
+    if (!hits) return;
     const uint32_t hm = spread4(hits);
     cnt += __popc(zero_bytes_msb(ew) & hm);
     const uint32_t en = (ew & ~hm) | (0x01010101u & hm);
     if (en != ew) *(uint32_t*)(edited + i) = en;
     uint32_t* pm = (uint32_t*)(mask + i);
     if (hits == 0xfu) *pm = 0x01010101u;
-    else { const uint32_t mw = *pm, mn = (mw & ~hm) | (0x01010101u & hm); if (mn != mw) *pm = mn; }
+    else { const uint32_t mn = (mw & ~hm) | (0x01010101u & hm); if (mn != mw) *pm = mn; }
     if (ES == 1) {
         uint32_t* pd = (uint32_t*)((uint8_t*)data + i);
         const uint32_t vr = (value & 0xffu) * 0x01010101u;
         if (hits == 0xfu) *pd = vr;
-        else { const uint32_t dw = *pd; *pd = (dw & ~hm) | (vr & hm); }
+        else { const uint32_t dn = (dw & ~hm) | (vr & hm); if (dn != dw) *pd = dn; }
     } else if (ES == 2) {
         uint16_t* pd = (uint16_t*)data + i;
         if (hits == 0xfu) { const uint32_t vr = (value & 0xffffu) * 0x00010001u; *(uint2*)pd = make_uint2(vr, vr); }
@@ -180,7 +196,9 @@ ML_DEV void quad_write_pre(void* data, uint32_t value, uint8_t* mask, uint8_t* e
 template <int ES>
 ML_DEV void quad_write(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i,
                        unsigned hits, long long& cnt) {
-    quad_write_pre<ES>(data, value, mask, edited, i, hits, *(const uint32_t*)(edited + i), cnt);
+    uint32_t ew, mw, dw;
+    quad_load<ES>(data, mask, edited, i, hits, ew, mw, dw);
+    quad_commit<ES>(data, value, mask, edited, i, hits, ew, mw, dw, cnt);
 }
 
 // ---------------------------------------------------------------------------------------------

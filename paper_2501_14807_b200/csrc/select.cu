@@ -66,13 +66,18 @@ sphere_kernel(const float* __restrict__ px, const float* __restrict__ py, const 
                 const long long q = q0 + u * nthreads;
                 if (q < nq) { vx[u] = ld_stream(qx + q); vy[u] = ld_stream(qy + q); vz[u] = ld_stream(qz + q); }
             }
+            constexpr int E = ES > 0 ? ES : 1;
+            unsigned hits[UNROLL];
+            uint32_t ew[UNROLL], mw[UNROLL], dw[UNROLL];
 #pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                const long long q = q0 + u * nthreads;
-                if (q >= nq) break;
-                const unsigned hits = sphere_hits4(vx[u], vy[u], vz[u], cx, cy, cz, r2);
-                if (hits) quad_write<(ES > 0 ? ES : 1)>(data, value, mask, edited, q << 2, hits, cnt);
-            }
+            for (int u = 0; u < UNROLL; ++u)
+                hits[u] = (q0 + u * nthreads < nq) ? sphere_hits4(vx[u], vy[u], vz[u], cx, cy, cz, r2) : 0u;
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)      // old words of all hit quads first: the loads overlap
+                quad_load<E>(data, mask, edited, (q0 + u * nthreads) << 2, hits[u], ew[u], mw[u], dw[u]);
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u)
+                quad_commit<E>(data, value, mask, edited, (q0 + u * nthreads) << 2, hits[u], ew[u], mw[u], dw[u], cnt);
         }
         done = nq << 2;
     }
@@ -178,9 +183,13 @@ sphere_batch_kernel(BatchArgs a) {
                     const uint32_t value = __ldg(a.value_bits + k);
                     void* d = a.data[layer]; uint8_t* m = a.mask[layer]; uint8_t* ed = a.edited[layer];
                     long long c = 0;
+                    uint32_t ew[4], mw[4], dw[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (hits[u]) quad_write<ES>(d, value, m, ed, ((unit << 7) + u * 32 + lane) << 2, hits[u], c);
+                        quad_load<ES>(d, m, ed, ((unit << 7) + u * 32 + lane) << 2, hits[u], ew[u], mw[u], dw[u]);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        quad_commit<ES>(d, value, m, ed, ((unit << 7) + u * 32 + lane) << 2, hits[u], ew[u], mw[u], dw[u], c);
                     if (c) atomicAdd(smem_counts ? &s_counts[layer] : a.counts + layer, (unsigned long long)c);
                 }
             }
@@ -209,7 +218,7 @@ template <> struct AttrT<ML_FLOAT32> { typedef float T; static ML_DEV bool hit(T
 
 // 4 texels per step: one (4*sizeof(T))-byte attribute load + one 4-byte valid load.
 template <int KIND, int ES>
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, 4)
 threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ valid, long long n,
                  double lo, double hi, Thr thr, void* __restrict__ data, int esize, uint32_t value,
                  uint8_t* __restrict__ mask, uint8_t* __restrict__ edited, unsigned long long* counter) {
@@ -232,8 +241,9 @@ threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ val
                     vm[u] = valid ? ld_stream((const uint32_t*)valid + q) : 0x01010101u;
                 }
             }
+            constexpr int E = ES > 0 ? ES : 1;
             unsigned hits[TU];
-            uint32_t ew[TU];
+            uint32_t ew[TU], mw[TU], dw[TU];
 #pragma unroll
             for (int u = 0; u < TU; ++u) {
                 hits[u] = 0;
@@ -244,11 +254,11 @@ threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ val
                     if ((((vm[u] >> (8 * e)) & 0xffu) != 0) && AttrT<KIND>::hit(a[u].v[e], thr)) hits[u] |= 1u << e;
             }
 #pragma unroll
-            for (int u = 0; u < TU; ++u)      // edited words of all hit quads first: loads overlap
-                ew[u] = hits[u] ? *(const uint32_t*)(edited + ((q0 + u * nthreads) << 2)) : 0u;
+            for (int u = 0; u < TU; ++u)      // old words of all hit quads first: the loads overlap
+                quad_load<E>(data, mask, edited, (q0 + u * nthreads) << 2, hits[u], ew[u], mw[u], dw[u]);
 #pragma unroll
             for (int u = 0; u < TU; ++u)
-                if (hits[u]) quad_write_pre<(ES > 0 ? ES : 1)>(data, value, mask, edited, (q0 + u * nthreads) << 2, hits[u], ew[u], cnt);
+                quad_commit<E>(data, value, mask, edited, (q0 + u * nthreads) << 2, hits[u], ew[u], mw[u], dw[u], cnt);
         }
         done = nq << 2;
     }
