@@ -160,6 +160,30 @@ int ml_select_sphere_batch(const float* pos, int64_t pos_stride, int64_t n,
                            void* const* data, uint8_t* const* mask, uint8_t* const* edited,
                            int64_t L, int esize, uint64_t* counts, void* stream);
 
+/* Footprint-culled forms of the two brushes above: identical planes and counts, but a stroke reads
+ * only the 128 x 4-texel tiles of the position map its sphere can reach.
+ *   ml_tile_count            tiles of a (rows x width) slab; 0 when width % 128 != 0 (no culling).
+ *   ml_surface_tile_boxes    once per surface map: boxes [ntiles][8] float32 (lo.xyz, 0, hi.xyz, 0;
+ *                            lo > hi for a tile without covered texels), 16-byte aligned.
+ *   ml_tile_workspace_bytes  device scratch (tile list) the culled brushes need, 8-byte aligned.
+ * The box test is conservative (float64, margin 1e-12 relative, see select.cu box_may_hit); the
+ * per-texel decision and the write rule are those of ml_select_sphere / ml_select_sphere_batch. */
+int64_t ml_tile_count(int64_t width, int64_t rows);
+size_t ml_tile_workspace_bytes(int64_t width, int64_t rows);
+int ml_surface_tile_boxes(const float* pos, int64_t pos_stride, int64_t width, int64_t rows,
+                          float* boxes, void* stream);
+int ml_select_sphere_tiles(const float* pos, int64_t pos_stride, int64_t width, int64_t rows,
+                           const float* boxes, void* workspace, size_t workspace_bytes,
+                           double cx, double cy, double cz, double radius,
+                           void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
+                           uint64_t* count, void* stream);
+int ml_select_sphere_batch_tiles(const float* pos, int64_t pos_stride, int64_t width, int64_t rows,
+                                 const float* boxes, void* workspace, size_t workspace_bytes,
+                                 const double* strokes, const int32_t* layer_of,
+                                 const uint32_t* value_bits, int64_t K,
+                                 void* const* data, uint8_t* const* mask, uint8_t* const* edited,
+                                 int64_t L, int esize, uint64_t* counts, void* stream);
+
 /* Attribute threshold: hit = (valid == NULL || valid[i] != 0) && lo <= attr[i] <= hi (closed,
  * float64 compare of the widened attribute; attr_kind is an ML_* plane kind). */
 int ml_select_threshold(const void* attr, int attr_kind, const uint8_t* valid, int64_t n,
@@ -208,6 +232,14 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
                      int64_t in_row0, int64_t in_rows, int64_t out_row0, int64_t out_rows,
                      int64_t radius, void* data, int esize, uint32_t value_bits, uint8_t* mask,
                      uint64_t* count, void* stream);
+
+/* Footprint-culled padding for the stroke path (single slab: input rows == output rows; width % 128
+ * == 0, radius <= 4, 16-byte aligned planes): tile_bits is the 128 x 8-texel tile bitmap
+ * ml_tea_classify wrote for the stroke whose `edited` marks are being padded.  Only tiles with a
+ * marked tile in their 3 x 3 neighbourhood are read; planes and count equal ml_apply_padding's. */
+int ml_apply_padding_tiles(const uint8_t* outline, const uint8_t* edited, int64_t width, int64_t rows,
+                           int64_t radius, const uint32_t* tile_bits, void* data, int esize,
+                           uint32_t value_bits, uint8_t* mask, uint64_t* count, void* stream);
 
 /* ---- display + layer file helpers (definitions: ext_resolve_display, ext_pack_mask)
  * SPEC:186-203 resolve_display: rgba_out[i] (4 bytes R,G,B,A) = mask[i] ? palette(u) : 0 with

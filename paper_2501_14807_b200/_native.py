@@ -80,6 +80,13 @@ def lib():
         "ml_tea_tile_words": (i32, [i64, i64]),
         "ml_select_sphere": (i32, [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
         "ml_select_sphere_batch": (i32, [vp, i64, i64, vp, vp, vp, i64, vp, vp, vp, i64, i32, vp, vp]),
+        "ml_tile_count": (i64, [i64, i64]),
+        "ml_tile_workspace_bytes": (sz, [i64, i64]),
+        "ml_surface_tile_boxes": (i32, [vp, i64, i64, i64, vp, vp]),
+        "ml_select_sphere_tiles": (i32, [vp, i64, i64, i64, vp, vp, sz, dbl, dbl, dbl, dbl, vp, i32, u32, vp, vp,
+                                         vp, vp]),
+        "ml_select_sphere_batch_tiles": (i32, [vp, i64, i64, i64, vp, vp, sz, vp, vp, vp, i64, vp, vp, vp, i64,
+                                               i32, vp, vp]),
         "ml_select_threshold": (i32, [vp, i32, vp, i64, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
         "ml_layer_op": (i32, [i32, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
         "ml_layer_chain": (i32, [i64, vp, vp, vp, vp, vp, i32, i64, vp]),
@@ -88,6 +95,7 @@ def lib():
         "ml_layer_stats": (i32, [vp, i32, vp, i64, vp, vp]),
         "ml_outline_mask": (i32, [vp, i64, i64, i64, i64, i64, i64, vp, vp]),
         "ml_apply_padding": (i32, [vp, vp, i64, i64, i64, i64, i64, i64, vp, i32, u32, vp, vp, vp]),
+        "ml_apply_padding_tiles": (i32, [vp, vp, i64, i64, i64, vp, vp, i32, u32, vp, vp, vp]),
         "ml_resolve_display": (i32, [vp, i32, vp, i64, dbl, dbl, vp, vp, i32, vp, vp]),
         "ml_pack_mask": (i32, [vp, i64, vp, vp]),
         "ml_unpack_mask": (i32, [vp, i64, vp, vp]),
@@ -108,9 +116,11 @@ EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve",
     "ml_surface_workspace_bytes", "ml_tea_texels",
-    "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_select_threshold", "ml_layer_op",
+    "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
+    "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
+    "ml_select_threshold", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
-    "ml_apply_padding", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
+    "ml_apply_padding", "ml_apply_padding_tiles", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
     "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
 
 
@@ -515,8 +525,33 @@ def _check_layer_planes(n, data, mask, edited):
         raise TargetMismatch("data plane must be contiguous")
 
 
-def select_sphere(pos, center, radius, data, mask, edited, value, *, counts=None):
-    """Sphere brush over a (3, rows, width) float32 position map.  Returns newly edited texels."""
+class TileBoxes:
+    """Bounding boxes of the position map per 128 x 4-texel tile plus the tile-list scratch the
+    footprint-culled brushes use (one per surface map; ``None`` from ``tile_boxes`` when the slab
+    width is not a multiple of 128)."""
+
+    def __init__(self, boxes, scratch, nbytes):
+        self.boxes, self.scratch, self.nbytes = boxes, scratch, nbytes
+
+
+def tile_boxes(pos):
+    """Build the per-tile position boxes of a (3, rows, width) float32 position map."""
+    torch = require_cuda()
+    L = lib()
+    rows, width = int(pos.shape[1]), int(pos.shape[2])
+    nt = int(L.ml_tile_count(width, rows))
+    if nt == 0 or pos.data_ptr() % 16 or (rows * width) % 4:
+        return None
+    boxes = torch.empty((nt, 8), dtype=torch.float32, device=pos.device)
+    _check(L.ml_surface_tile_boxes(_ptr(pos), rows * width, width, rows, _ptr(boxes), _stream()))
+    nb = int(L.ml_tile_workspace_bytes(width, rows))
+    return TileBoxes(boxes, torch.empty(nb, dtype=torch.uint8, device=pos.device), nb)
+
+
+def select_sphere(pos, center, radius, data, mask, edited, value, *, counts=None, tiles=None):
+    """Sphere brush over a (3, rows, width) float32 position map.  Returns newly edited texels.
+    ``tiles`` (a TileBoxes of this position map) selects the footprint-culled kernels: same
+    planes and count, but only the tiles the sphere can reach are read."""
     torch = require_cuda()
     if pos.dtype != torch.float32 or pos.dim() != 3 or pos.shape[0] != 3 or not pos.is_contiguous():
         raise TargetMismatch("pos must be a contiguous (3, rows, width) float32 tensor")
@@ -524,9 +559,16 @@ def select_sphere(pos, center, radius, data, mask, edited, value, *, counts=None
     _check_layer_planes(n, data, mask, edited)
     bits, esize = value_bits(value, data)
     ctr = counts if counts is not None else _counters(1, pos.device)
-    _check(lib().ml_select_sphere(_ptr(pos), n, n, float(center[0]), float(center[1]), float(center[2]),
-                                  float(radius), _ptr(data), esize, bits, _ptr(mask), _ptr(edited),
-                                  _ptr(ctr), _stream()))
+    aligned = all(t.data_ptr() % 16 == 0 for t in (data, mask, edited))
+    if tiles is not None and aligned:
+        _check(lib().ml_select_sphere_tiles(_ptr(pos), n, int(pos.shape[2]), int(pos.shape[1]), _ptr(tiles.boxes),
+                                            _ptr(tiles.scratch), tiles.nbytes, float(center[0]), float(center[1]),
+                                            float(center[2]), float(radius), _ptr(data), esize, bits, _ptr(mask),
+                                            _ptr(edited), _ptr(ctr), _stream()))
+    else:
+        _check(lib().ml_select_sphere(_ptr(pos), n, n, float(center[0]), float(center[1]), float(center[2]),
+                                      float(radius), _ptr(data), esize, bits, _ptr(mask), _ptr(edited),
+                                      _ptr(ctr), _stream()))
     return None if counts is not None else int(ctr[0].item())
 
 
@@ -583,13 +625,22 @@ class StrokeBatch:
         return self
 
 
-def select_sphere_batch(pos, batch):
+def select_sphere_batch(pos, batch, *, tiles=None):
     """Apply ``batch`` (a StrokeBatch after ``upload``) in ONE pass over the position map.
-    Per-layer newly-edited counts accumulate into ``batch.counts`` (device)."""
+    Per-layer newly-edited counts accumulate into ``batch.counts`` (device).  ``tiles`` (TileBoxes)
+    restricts the pass to the tiles some stroke of the batch can reach."""
     torch = require_cuda()
     n = pos.shape[1] * pos.shape[2]
     for d, m, e in zip(batch.data, batch.mask, batch.edited):
         _check_layer_planes(n, d, m, e)
+    if tiles is not None:
+        _check(lib().ml_select_sphere_batch_tiles(_ptr(pos), n, int(pos.shape[2]), int(pos.shape[1]),
+                                                  _ptr(tiles.boxes), _ptr(tiles.scratch), tiles.nbytes,
+                                                  _ptr(batch.d_strokes), _ptr(batch.d_layer_of),
+                                                  _ptr(batch.d_values), batch.K, _ptr(batch.d_data),
+                                                  _ptr(batch.d_mask), _ptr(batch.d_edited), batch.L, batch.esize,
+                                                  _ptr(batch.counts), _stream()))
+        return
     _check(lib().ml_select_sphere_batch(_ptr(pos), n, n, _ptr(batch.d_strokes), _ptr(batch.d_layer_of),
                                         _ptr(batch.d_values), batch.K, _ptr(batch.d_data),
                                         _ptr(batch.d_mask), _ptr(batch.d_edited), batch.L, batch.esize,
@@ -725,8 +776,11 @@ def outline_mask(cov, thickness, *, in_row0=0, out_row0=None, out_rows=None, out
     return out
 
 
-def apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_row0=None, counts=None):
-    """SPEC.md:295-298.  ``edited`` is the input slab (with halo rows), the others output slabs."""
+def apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_row0=None, counts=None,
+                  tiles=None):
+    """SPEC.md:295-298.  ``edited`` is the input slab (with halo rows), the others output slabs.
+    ``tiles``: the TEA stroke's 128 x 8-texel tile bitmap (``tea_texels(..., tiles=...)``); the pass
+    then reads only the neighbourhood of the stroke's footprint (same result)."""
     require_cuda()
     in_rows, w = edited.shape
     out_rows = outline.shape[0]
@@ -736,8 +790,14 @@ def apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_
     _check_layer_planes(out_rows * w, data, mask, None)
     bits, esize = value_bits(value, data)
     ctr = counts if counts is not None else _counters(1, edited.device)
-    _check(lib().ml_apply_padding(_ptr(outline), _ptr(edited), w, in_row0, in_rows, out_row0, out_rows,
-                                  int(radius), _ptr(data), esize, bits, _ptr(mask), _ptr(ctr), _stream()))
+    culled = (tiles is not None and in_rows == out_rows and out_row0 == in_row0 and w % 128 == 0 and 0 < radius <= 4
+              and all(t.data_ptr() % 16 == 0 for t in (outline, edited, data, mask)))
+    if culled:
+        _check(lib().ml_apply_padding_tiles(_ptr(outline), _ptr(edited), w, in_rows, int(radius), _ptr(tiles),
+                                            _ptr(data), esize, bits, _ptr(mask), _ptr(ctr), _stream()))
+    else:
+        _check(lib().ml_apply_padding(_ptr(outline), _ptr(edited), w, in_row0, in_rows, out_row0, out_rows,
+                                      int(radius), _ptr(data), esize, bits, _ptr(mask), _ptr(ctr), _stream()))
     return None if counts is not None else int(ctr[0].item())
 
 

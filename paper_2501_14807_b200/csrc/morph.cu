@@ -127,6 +127,46 @@ ML_DEV unsigned box_any16(const uint8_t* __restrict__ src, long long width, long
 // skipped; vectors with outline texels fetch their neighbourhood of the edited plane with
 // 3*(2r+1) independent loads.  Data / mask are updated with 32-bit read-modify-writes (each
 // 4-texel word is owned by one thread).
+// One 16-texel vector of the padding pass: `o` = its outline bytes (non-zero somewhere), i0 = flat
+// index of its first texel.  Returns the number of padded texels.
+template <int ES>
+ML_DEV int pad_vector(const uint4& o, long long i0, const uint8_t* __restrict__ edited, long long width,
+                      long long in_row0, long long in_rows, long long out_row0, int r,
+                      void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask) {
+    const long long yy = i0 / width, x0 = i0 - yy * width;
+    const unsigned on = nz4(o.x) | (nz4(o.y) << 4) | (nz4(o.z) << 8) | (nz4(o.w) << 12);
+    const unsigned hit16 = on & box_any16(edited, width, in_row0, in_rows, x0, out_row0 + yy, r);
+    if (!hit16) return 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const unsigned hit = (hit16 >> (4 * j)) & 0xfu;
+        if (!hit) continue;
+        const long long i = i0 + 4 * j;
+        const uint32_t hm = spread4(hit);
+        uint32_t* pm = (uint32_t*)(mask + i);
+        const uint32_t mw = *pm, mn = (mw & ~hm) | (0x01010101u & hm);
+        if (mn != mw) *pm = mn;
+        if (ES == 1) {
+            uint32_t* pd = (uint32_t*)((uint8_t*)data + i);
+            const uint32_t dw = *pd;
+            *pd = (dw & ~hm) | (((value & 0xffu) * 0x01010101u) & hm);
+        } else if (ES == 2) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) if (hit & (1u << e)) ((uint16_t*)data)[i + e] = (uint16_t)value;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) if (hit & (1u << e)) ((uint32_t*)data)[i + e] = value;
+        }
+    }
+    return __popc(hit16);
+}
+
+// Streaming form of the padding pass for the per-stroke hot path (width % 16 == 0, 16-byte
+// aligned planes, radius <= 4): the outline plane is the 1 B/texel read stream (four 128-bit loads
+// in flight per thread); outlines are thin, so almost every 16-texel vector is all zero and is
+// skipped; vectors with outline texels fetch their neighbourhood of the edited plane with
+// 3*(2r+1) independent loads.  Data / mask are updated with 32-bit read-modify-writes (each
+// 4-texel word is owned by one thread).
 template <int ES>
 __global__ void __launch_bounds__(BLOCK)
 padding_stream_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ edited, long long width,
@@ -148,33 +188,50 @@ padding_stream_kernel(const uint8_t* __restrict__ outline, const uint8_t* __rest
 #pragma unroll 1
         for (int u = 0; u < U; ++u) {
             if ((o[u].x | o[u].y | o[u].z | o[u].w) == 0) continue;
-            const long long i0 = (v0 + u * nthreads) << 4;
-            const long long yy = i0 / width, x0 = i0 - yy * width;
-            const unsigned on = nz4(o[u].x) | (nz4(o[u].y) << 4) | (nz4(o[u].z) << 8) | (nz4(o[u].w) << 12);
-            const unsigned hit16 = on & box_any16(edited, width, in_row0, in_rows, x0, out_row0 + yy, r);
-            if (!hit16) continue;
-            cnt += __popc(hit16);
+            cnt += pad_vector<ES>(o[u], (v0 + u * nthreads) << 4, edited, width, in_row0, in_rows, out_row0, r, data, value, mask);
+        }
+    }
+    block_count_add(cnt, count);
+}
+
+// Footprint-culled form (single slab, width % 128 == 0, radius <= 4): `tile_bits` is the bitmap of
+// 128 x 8-texel tiles the TEA stroke could edit (ml_tea_classify).  A padded texel lies within
+// `radius` <= 4 texels of an edited one, i.e. in a marked tile or one of its 8 neighbours, so one
+// warp per tile tests the 3 x 3 tile neighbourhood in the bitmap and reads the outline bytes of
+// that tile only when some neighbour is marked.  Same planes and count as the streaming kernel.
+template <int ES>
+__global__ void __launch_bounds__(BLOCK)
+padding_tile_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ edited, long long width,
+                    long long rows, int r, const uint32_t* __restrict__ tile_bits,
+                    void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask, unsigned long long* count) {
+    const int lane = threadIdx.x & 31;
+    const int segs = (int)(width >> 7);
+    const int tile_rows = (int)((rows + 7) >> 3);
+    const int ntiles = segs * tile_rows;
+    const int nwarps = gridDim.x * (BLOCK / 32);
+    long long cnt = 0;
+    for (int tile = blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); tile < ntiles; tile += nwarps) {
+        const int ty = tile / segs, tx = tile - ty * segs;
+        bool near = false;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const unsigned hit = (hit16 >> (4 * j)) & 0xfu;
-                if (!hit) continue;
-                const long long i = i0 + 4 * j;
-                const uint32_t hm = spread4(hit);
-                uint32_t* pm = (uint32_t*)(mask + i);
-                const uint32_t mw = *pm, mn = (mw & ~hm) | (0x01010101u & hm);
-                if (mn != mw) *pm = mn;
-                if (ES == 1) {
-                    uint32_t* pd = (uint32_t*)((uint8_t*)data + i);
-                    const uint32_t dw = *pd;
-                    *pd = (dw & ~hm) | (((value & 0xffu) * 0x01010101u) & hm);
-                } else if (ES == 2) {
+        for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) if (hit & (1u << e)) ((uint16_t*)data)[i + e] = (uint16_t)value;
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) if (hit & (1u << e)) ((uint32_t*)data)[i + e] = value;
-                }
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int y = ty + dy, x = tx + dx;
+                if (y < 0 || y >= tile_rows || x < 0 || x >= segs) continue;
+                const int t = y * segs + x;
+                near |= ((__ldg(tile_bits + (t >> 5)) >> (t & 31)) & 1u) != 0;
             }
+        if (!near) continue;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int v = lane + 32 * k;                       // 64 vectors of 16 texels per tile
+            const long long yy = ((long long)ty << 3) + (v >> 3);
+            if (yy >= rows) continue;
+            const long long i0 = yy * width + ((long long)tx << 7) + ((v & 7) << 4);
+            const uint4 o = ld_stream((const uint4*)(outline + i0));
+            if ((o.x | o.y | o.z | o.w) == 0) continue;
+            cnt += pad_vector<ES>(o, i0, edited, width, 0, rows, 0, r, data, value, mask);
         }
     }
     block_count_add(cnt, count);
@@ -232,6 +289,26 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
     padding_kernel<<<grid_for(((width + 3) >> 2) * out_rows), BLOCK, 0, (cudaStream_t)stream>>>(
         outline, edited, width, in_row0, in_rows, out_row0, out_rows, (int)radius, data, esize,
         value_bits, mask, (unsigned long long*)count);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_apply_padding_tiles(const uint8_t* outline, const uint8_t* edited, int64_t width, int64_t rows,
+                           int64_t radius, const uint32_t* tile_bits, void* data, int esize,
+                           uint32_t value_bits, uint8_t* mask, uint64_t* count, void* stream) {
+    if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
+    if (radius <= 0 || rows <= 0 || width <= 0) return ML_OK;
+    if ((width % 128) != 0 || radius > 4 || tile_bits == nullptr ||
+        ((((uintptr_t)outline) | ((uintptr_t)edited) | ((uintptr_t)data) | ((uintptr_t)mask)) & 15) != 0)
+        return ml_fail(ML_ERR_ARG, "culled padding needs width % 128 == 0, radius <= 4, aligned planes and the stroke's tile bitmap");
+    const long long ntiles = (width >> 7) * ((rows + 7) >> 3);
+    long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);
+    const long long cap = (long long)ml_sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    cudaStream_t st = (cudaStream_t)stream;
+#define ML_LAUNCH_PADT(ES) padding_tile_kernel<ES><<<(unsigned)blocks, BLOCK, 0, st>>>(outline, edited, width, rows, (int)radius, tile_bits, data, value_bits, mask, (unsigned long long*)count)
+    if (esize == 1) ML_LAUNCH_PADT(1); else if (esize == 2) ML_LAUNCH_PADT(2); else ML_LAUNCH_PADT(4);
+#undef ML_LAUNCH_PADT
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

@@ -105,6 +105,89 @@ struct BatchArgs {
     unsigned long long* counts;
 };
 
+// conservative sphere / box test in float64: false only when NO point of the box [lo, hi] can pass
+// d2 <= r*r.  Per-axis distance from the centre to the box: max(lo - c, c - hi, 0).  Every point p
+// of the box has fl(d2(p)) >= dmin2*(1 - 8u): the box is provably missed only when
+// dmin2 > r*r*(1 + 1e-12); otherwise the stroke is kept.
+ML_DEV bool box_may_hit(double bl0, double bl1, double bl2, double bh0, double bh1, double bh2,
+                        double sx, double sy, double sz, double sr) {
+    const double ddx = fmax(fmax(xsub(bl0, sx), xsub(sx, bh0)), 0.0);
+    const double ddy = fmax(fmax(xsub(bl1, sy), xsub(sy, bh1)), 0.0);
+    const double ddz = fmax(fmax(xsub(bl2, sz), xsub(sz, bh2)), 0.0);
+    const double dmin2 = xadd(xadd(xmul(ddx, ddx), xmul(ddy, ddy)), xmul(ddz, ddz));
+    return !(dmin2 > xmul(xmul(sr, sr), 1.000000000001));
+}
+
+// All strokes of the batch against the 4 x 32 quads a warp holds in registers (quad u of lane l is
+// texel 4*qidx[u]; qidx[u] < 0 = nothing).  Strokes are culled 32 at a time against the box of the
+// held texels (lane k tests stroke k0+k) into a ballot mask -- ascending bit order is stroke order --
+// and every texel tests only the survivors, in order, so the result equals K successive
+// single-stroke passes (a later stroke overwrites an earlier one on the same layer).
+template <int ES>
+ML_DEV void batch_apply(const BatchArgs& a, const float4 (&vx)[4], const float4 (&vy)[4], const float4 (&vz)[4],
+                        const long long (&qidx)[4], double bl0, double bl1, double bl2, double bh0, double bh1,
+                        double bh2, int lane, bool smem_counts, unsigned long long* s_counts) {
+    for (long long k0 = 0; k0 < a.K; k0 += 32) {
+        const long long kk = k0 + lane;
+        bool keep = false;
+        if (kk < a.K)
+            keep = box_may_hit(bl0, bl1, bl2, bh0, bh1, bh2, a.strokes[4 * kk], a.strokes[4 * kk + 1],
+                               a.strokes[4 * kk + 2], a.strokes[4 * kk + 3]);
+        unsigned live = __ballot_sync(0xffffffffu, keep);
+        while (live) {
+            const int b = __ffs(live) - 1;
+            live &= live - 1;
+            const long long k = k0 + b;
+            const double sx = __ldg(a.strokes + 4 * k), sy = __ldg(a.strokes + 4 * k + 1),
+                         sz = __ldg(a.strokes + 4 * k + 2), sr = __ldg(a.strokes + 4 * k + 3);
+            const double r2 = xmul(sr, sr);
+            unsigned hits[4];
+            unsigned any = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                hits[u] = qidx[u] >= 0 ? sphere_hits4(vx[u], vy[u], vz[u], sx, sy, sz, r2) : 0u;
+                any |= hits[u];
+            }
+            if (any) {
+                const int layer = __ldg(a.layer_of + k);
+                const uint32_t value = __ldg(a.value_bits + k);
+                void* d = a.data[layer]; uint8_t* m = a.mask[layer]; uint8_t* ed = a.edited[layer];
+                long long c = 0;
+                uint32_t ew[4], mw[4], dw[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) quad_load<ES>(d, m, ed, qidx[u] << 2, hits[u], ew[u], mw[u], dw[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) quad_commit<ES>(d, value, m, ed, qidx[u] << 2, hits[u], ew[u], mw[u], dw[u], c);
+                if (c) atomicAdd(smem_counts ? &s_counts[layer] : a.counts + layer, (unsigned long long)c);
+            }
+        }
+    }
+}
+
+// box of the (NaN-free part of the) positions a warp holds, reduced over the warp
+ML_DEV bool warp_box(const float4 (&vx)[4], const float4 (&vy)[4], const float4 (&vz)[4], float (&lo)[3], float (&hi)[3]) {
+    const float inf = __int_as_float(0x7f800000);
+    lo[0] = lo[1] = lo[2] = inf; hi[0] = hi[1] = hi[2] = -inf;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {                    // fminf / fmaxf drop NaNs (uncovered texels)
+        lo[0] = fminf(lo[0], fminf(fminf(vx[u].x, vx[u].y), fminf(vx[u].z, vx[u].w)));
+        hi[0] = fmaxf(hi[0], fmaxf(fmaxf(vx[u].x, vx[u].y), fmaxf(vx[u].z, vx[u].w)));
+        lo[1] = fminf(lo[1], fminf(fminf(vy[u].x, vy[u].y), fminf(vy[u].z, vy[u].w)));
+        hi[1] = fmaxf(hi[1], fmaxf(fmaxf(vy[u].x, vy[u].y), fmaxf(vy[u].z, vy[u].w)));
+        lo[2] = fminf(lo[2], fminf(fminf(vz[u].x, vz[u].y), fminf(vz[u].z, vz[u].w)));
+        hi[2] = fmaxf(hi[2], fmaxf(fmaxf(vz[u].x, vz[u].y), fmaxf(vz[u].z, vz[u].w)));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+            hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+        }
+    }
+    return lo[0] <= hi[0];                           // false: no covered texel (warp-uniform)
+}
+
 template <int ES>
 __global__ void __launch_bounds__(BLOCK, 2)
 sphere_batch_kernel(BatchArgs a) {
@@ -116,13 +199,13 @@ sphere_batch_kernel(BatchArgs a) {
     const long long nq = a.n >> 2;                        // host guarantees n % 4 == 0
     const long long nunits = (nq + 127) >> 7;             // 128 quads = 512 texels per warp unit
     const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
-    const float inf = __int_as_float(0x7f800000);
     for (long long unit = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); unit < nunits; unit += nwarps) {
         float4 vx[4], vy[4], vz[4];
-        float lo[3] = {inf, inf, inf}, hi[3] = {-inf, -inf, -inf};
+        long long qidx[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const long long q = (unit << 7) + u * 32 + lane;
+            qidx[u] = q < nq ? q : -1;
             if (q < nq) {
                 vx[u] = ld_stream((const float4*)a.px + q);
                 vy[u] = ld_stream((const float4*)a.py + q);
@@ -132,68 +215,148 @@ sphere_batch_kernel(BatchArgs a) {
                 vx[u] = vy[u] = vz[u] = make_float4(qn, qn, qn, qn);
             }
         }
+        float lo[3], hi[3];
+        if (!warp_box(vx, vy, vz, lo, hi)) continue;
+        batch_apply<ES>(a, vx, vy, vz, qidx, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], lane, smem_counts, s_counts);
+    }
+    __syncthreads();
+    if (smem_counts && threadIdx.x < a.L && s_counts[threadIdx.x]) atomicAdd(a.counts + threadIdx.x, s_counts[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Footprint-culled brushes.  The surface map carries one float32 bounding box per 128 x 4-texel
+// TILE of the position planes (built once, ml_surface_tile_boxes: 32 bytes per 512 texels).  A
+// stroke first tests the boxes (one thread per tile, conservative float64 test above) and appends
+// the tiles it may touch to a list; a second launch walks the list with one warp per tile and runs
+// exactly the per-texel test and write rule of the streaming kernels.  A stroke then costs
+// O(tiles) * 32 B + O(footprint) * 12 B instead of 12 B for every texel of the atlas; the planes
+// and counts are identical because a culled tile provably contains no hit.
+constexpr int ST_W_SHIFT = 7, ST_H_SHIFT = 2;              // 128 texels x 4 rows
+
+struct TileGrid {
+    long long width, rows, nq;
+    int segs, tile_rows;
+    long long ntiles;
+};
+inline TileGrid tile_grid(long long width, long long rows) {
+    TileGrid g;
+    g.width = width; g.rows = rows; g.nq = (width * rows) >> 2;
+    g.segs = (int)(width >> ST_W_SHIFT);
+    g.tile_rows = (int)((rows + (1 << ST_H_SHIFT) - 1) >> ST_H_SHIFT);
+    g.ntiles = (long long)g.segs * g.tile_rows;
+    return g;
+}
+// quad index of (row u of the tile, lane) or -1 below the slab
+ML_DEV long long tile_quad(const TileGrid& g, long long tile, int u, int lane) {
+    const long long ty = tile / g.segs, tx = tile - ty * g.segs;
+    const long long yy = (ty << ST_H_SHIFT) + u;
+    return yy < g.rows ? ((yy * g.width + (tx << ST_W_SHIFT)) >> 2) + lane : -1;
+}
+ML_DEV void tile_load(const TileGrid& g, long long tile, int lane, const float* px, const float* py, const float* pz,
+                      float4 (&vx)[4], float4 (&vy)[4], float4 (&vz)[4], long long (&qidx)[4]) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {                    // fminf / fmaxf drop NaNs (uncovered texels)
-            lo[0] = fminf(lo[0], fminf(fminf(vx[u].x, vx[u].y), fminf(vx[u].z, vx[u].w)));
-            hi[0] = fmaxf(hi[0], fmaxf(fmaxf(vx[u].x, vx[u].y), fmaxf(vx[u].z, vx[u].w)));
-            lo[1] = fminf(lo[1], fminf(fminf(vy[u].x, vy[u].y), fminf(vy[u].z, vy[u].w)));
-            hi[1] = fmaxf(hi[1], fmaxf(fmaxf(vy[u].x, vy[u].y), fmaxf(vy[u].z, vy[u].w)));
-            lo[2] = fminf(lo[2], fminf(fminf(vz[u].x, vz[u].y), fminf(vz[u].z, vz[u].w)));
-            hi[2] = fmaxf(hi[2], fmaxf(fmaxf(vz[u].x, vz[u].y), fmaxf(vz[u].z, vz[u].w)));
+    for (int u = 0; u < 4; ++u) {
+        qidx[u] = tile_quad(g, tile, u, lane);
+        if (qidx[u] >= 0) {
+            vx[u] = ld_stream((const float4*)px + qidx[u]);
+            vy[u] = ld_stream((const float4*)py + qidx[u]);
+            vz[u] = ld_stream((const float4*)pz + qidx[u]);
+        } else {
+            const float qn = __int_as_float(0x7fc00000);
+            vx[u] = vy[u] = vz[u] = make_float4(qn, qn, qn, qn);
         }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                lo[c] = fminf(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
-                hi[c] = fmaxf(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
-            }
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+tile_box_kernel(const float* __restrict__ px, const float* __restrict__ py, const float* __restrict__ pz,
+                TileGrid g, float4* __restrict__ boxes) {
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    for (long long tile = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); tile < g.ntiles; tile += nwarps) {
+        float4 vx[4], vy[4], vz[4];
+        long long qidx[4];
+        tile_load(g, tile, lane, px, py, pz, vx, vy, vz, qidx);
+        float lo[3], hi[3];
+        warp_box(vx, vy, vz, lo, hi);                      // empty tile: lo = +inf > hi = -inf
+        if (lane == 0) {
+            boxes[2 * tile] = make_float4(lo[0], lo[1], lo[2], 0.f);
+            boxes[2 * tile + 1] = make_float4(hi[0], hi[1], hi[2], 0.f);
         }
-        if (!(lo[0] <= hi[0])) continue;                  // no covered texel in this unit (warp-uniform)
-        const double bl0 = lo[0], bl1 = lo[1], bl2 = lo[2], bh0 = hi[0], bh1 = hi[1], bh2 = hi[2];
-        for (long long k0 = 0; k0 < a.K; k0 += 32) {
-            const long long kk = k0 + lane;
-            bool keep = false;
-            if (kk < a.K) {
-                const double sx = a.strokes[4 * kk], sy = a.strokes[4 * kk + 1], sz = a.strokes[4 * kk + 2],
-                             sr = a.strokes[4 * kk + 3];
-                // per-axis distance from the centre to the box: max(lo - c, c - hi, 0)
-                const double ddx = fmax(fmax(xsub(bl0, sx), xsub(sx, bh0)), 0.0);
-                const double ddy = fmax(fmax(xsub(bl1, sy), xsub(sy, bh1)), 0.0);
-                const double ddz = fmax(fmax(xsub(bl2, sz), xsub(sz, bh2)), 0.0);
-                const double dmin2 = xadd(xadd(xmul(ddx, ddx), xmul(ddy, ddy)), xmul(ddz, ddz));
-                // every texel p of the unit has fl(d2(p)) >= dmin2*(1 - 8u): the box is provably
-                // missed only when dmin2 > r*r*(1 + 1e-12); otherwise keep the stroke.
-                keep = !(dmin2 > xmul(xmul(sr, sr), 1.000000000001));
-            }
-            unsigned live = __ballot_sync(0xffffffffu, keep);
-            while (live) {
-                const int b = __ffs(live) - 1;
-                live &= live - 1;
-                const long long k = k0 + b;
-                const double sx = __ldg(a.strokes + 4 * k), sy = __ldg(a.strokes + 4 * k + 1),
-                             sz = __ldg(a.strokes + 4 * k + 2), sr = __ldg(a.strokes + 4 * k + 3);
-                const double r2 = xmul(sr, sr);
-                unsigned hits[4];
-                unsigned any = 0;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) { hits[u] = sphere_hits4(vx[u], vy[u], vz[u], sx, sy, sz, r2); any |= hits[u]; }
-                if (any) {
-                    const int layer = __ldg(a.layer_of + k);
-                    const uint32_t value = __ldg(a.value_bits + k);
-                    void* d = a.data[layer]; uint8_t* m = a.mask[layer]; uint8_t* ed = a.edited[layer];
-                    long long c = 0;
-                    uint32_t ew[4], mw[4], dw[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        quad_load<ES>(d, m, ed, ((unit << 7) + u * 32 + lane) << 2, hits[u], ew[u], mw[u], dw[u]);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        quad_commit<ES>(d, value, m, ed, ((unit << 7) + u * 32 + lane) << 2, hits[u], ew[u], mw[u], dw[u], c);
-                    if (c) atomicAdd(smem_counts ? &s_counts[layer] : a.counts + layer, (unsigned long long)c);
-                }
-            }
+    }
+}
+
+// tile list in device scratch: [0] = count (u64), then u32 tile indices
+struct TileList { unsigned long long* count; uint32_t* tiles; };
+
+// one thread per tile; K == 1 for the single-stroke brush
+__global__ void __launch_bounds__(BLOCK)
+tile_classify_kernel(const float4* __restrict__ boxes, long long ntiles, const double* __restrict__ strokes,
+                     long long K, double cx, double cy, double cz, double cr, TileList list) {
+    const long long tile = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    bool keep = false;
+    if (tile < ntiles) {
+        const float4 lo = __ldg(boxes + 2 * tile), hi = __ldg(boxes + 2 * tile + 1);
+        if (lo.x <= hi.x) {
+            if (strokes == nullptr) keep = box_may_hit(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, cx, cy, cz, cr);
+            else
+                for (long long k = 0; k < K && !keep; ++k)
+                    keep = box_may_hit(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, __ldg(strokes + 4 * k), __ldg(strokes + 4 * k + 1),
+                                       __ldg(strokes + 4 * k + 2), __ldg(strokes + 4 * k + 3));
         }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (bal == 0) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(list.count, (unsigned long long)__popc(bal));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (keep) list.tiles[slot + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)tile;
+}
+
+template <int ES>
+__global__ void __launch_bounds__(BLOCK)
+sphere_tiles_kernel(const float* __restrict__ px, const float* __restrict__ py, const float* __restrict__ pz,
+                    TileGrid g, TileList list, double cx, double cy, double cz, double r2,
+                    void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                    uint8_t* __restrict__ edited, unsigned long long* counter) {
+    long long cnt = 0;
+    const int lane = threadIdx.x & 31;
+    const long long count = (long long)*list.count;
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    for (long long j = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); j < count; j += nwarps) {
+        float4 vx[4], vy[4], vz[4];
+        long long qidx[4];
+        tile_load(g, list.tiles[j], lane, px, py, pz, vx, vy, vz, qidx);
+        unsigned hits[4];
+        uint32_t ew[4], mw[4], dw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) hits[u] = qidx[u] >= 0 ? sphere_hits4(vx[u], vy[u], vz[u], cx, cy, cz, r2) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) quad_load<ES>(data, mask, edited, qidx[u] << 2, hits[u], ew[u], mw[u], dw[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) quad_commit<ES>(data, value, mask, edited, qidx[u] << 2, hits[u], ew[u], mw[u], dw[u], cnt);
+    }
+    block_count_add(cnt, counter);
+}
+
+template <int ES>
+__global__ void __launch_bounds__(BLOCK, 2)
+sphere_batch_tiles_kernel(BatchArgs a, TileGrid g, const float4* __restrict__ boxes, TileList list) {
+    __shared__ unsigned long long s_counts[64];
+    const bool smem_counts = a.L <= 64;
+    if (threadIdx.x < 64) s_counts[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long count = (long long)*list.count;
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    for (long long j = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); j < count; j += nwarps) {
+        const long long tile = list.tiles[j];
+        float4 vx[4], vy[4], vz[4];
+        long long qidx[4];
+        tile_load(g, tile, lane, a.px, a.py, a.pz, vx, vy, vz, qidx);
+        const float4 lo = __ldg(boxes + 2 * tile), hi = __ldg(boxes + 2 * tile + 1);
+        batch_apply<ES>(a, vx, vy, vz, qidx, lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, lane, smem_counts, s_counts);
     }
     __syncthreads();
     if (smem_counts && threadIdx.x < a.L && s_counts[threadIdx.x]) atomicAdd(a.counts + threadIdx.x, s_counts[threadIdx.x]);
@@ -351,6 +514,95 @@ int ml_select_sphere_batch(const float* pos, int64_t pos_stride, int64_t n,
     if (esize == 1) sphere_batch_kernel<1><<<(unsigned)blocks, BLOCK, 0, st>>>(a);
     else if (esize == 2) sphere_batch_kernel<2><<<(unsigned)blocks, BLOCK, 0, st>>>(a);
     else sphere_batch_kernel<4><<<(unsigned)blocks, BLOCK, 0, st>>>(a);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int64_t ml_tile_count(int64_t width, int64_t rows) {
+    if (width <= 0 || rows <= 0 || (width & ((1 << ST_W_SHIFT) - 1)) != 0) return 0;
+    return tile_grid(width, rows).ntiles;
+}
+
+size_t ml_tile_workspace_bytes(int64_t width, int64_t rows) {
+    return 16 + (size_t)ml_tile_count(width, rows) * sizeof(uint32_t);
+}
+
+int ml_surface_tile_boxes(const float* pos, int64_t pos_stride, int64_t width, int64_t rows,
+                          float* boxes, void* stream) {
+    const long long ntiles = ml_tile_count(width, rows);
+    if (ntiles == 0) return ml_fail(ML_ERR_ARG, "tile boxes need width % 128 == 0");
+    const float *px = pos, *py = pos + pos_stride, *pz = pos + 2 * pos_stride;
+    if (!(aligned(px, 16) && aligned(py, 16) && aligned(pz, 16) && aligned(boxes, 16)))
+        return ml_fail(ML_ERR_ARG, "tile boxes need 16-byte aligned planes");
+    long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);
+    const long long cap = (long long)ml_sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    tile_box_kernel<<<(unsigned)blocks, BLOCK, 0, (cudaStream_t)stream>>>(px, py, pz, tile_grid(width, rows), (float4*)boxes);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+static int tiles_prepare(int64_t width, int64_t rows, const float* boxes, void* workspace, size_t workspace_bytes,
+                         const double* strokes, long long K, double cx, double cy, double cz, double cr,
+                         TileGrid& g, TileList& list, cudaStream_t st) {
+    if (ml_tile_count(width, rows) == 0) return ml_fail(ML_ERR_ARG, "culled brushes need width % 128 == 0");
+    if (boxes == nullptr || !aligned(boxes, 16)) return ml_fail(ML_ERR_ARG, "culled brushes need the 16-byte aligned tile boxes");
+    if (workspace == nullptr || workspace_bytes < ml_tile_workspace_bytes(width, rows) || !aligned(workspace, 8))
+        return ml_fail(ML_ERR_ARG, "culled brushes need ml_tile_workspace_bytes() of 8-byte aligned scratch");
+    g = tile_grid(width, rows);
+    list.count = (unsigned long long*)workspace;
+    list.tiles = (uint32_t*)(list.count + 2);
+    ML_CUDA(cudaMemsetAsync(list.count, 0, 8, st));
+    tile_classify_kernel<<<(unsigned)((g.ntiles + BLOCK - 1) / BLOCK), BLOCK, 0, st>>>((const float4*)boxes, g.ntiles, strokes, K,
+                                                                                       cx, cy, cz, cr, list);
+    return ML_OK;
+}
+
+int ml_select_sphere_tiles(const float* pos, int64_t pos_stride, int64_t width, int64_t rows,
+                           const float* boxes, void* workspace, size_t workspace_bytes,
+                           double cx, double cy, double cz, double radius,
+                           void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
+                           uint64_t* count, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
+    if (width <= 0 || rows <= 0) return ML_OK;
+    const float *px = pos, *py = pos + pos_stride, *pz = pos + 2 * pos_stride;
+    if (!(aligned(px, 16) && aligned(py, 16) && aligned(pz, 16) && planes_aligned(data, mask, edited)))
+        return ml_fail(ML_ERR_ARG, "culled sphere brush needs 16-byte aligned planes");
+    TileGrid g; TileList list;
+    const int rc = tiles_prepare(width, rows, boxes, workspace, workspace_bytes, nullptr, 1, cx, cy, cz, radius, g, list, st);
+    if (rc != ML_OK) return rc;
+    const double r2 = radius * radius;      // host IEEE multiply == the oracle's r*r
+    const unsigned grid = (unsigned)(ml_sm_count() * 8);
+    unsigned long long* c = (unsigned long long*)count;
+    if (esize == 1) sphere_tiles_kernel<1><<<grid, BLOCK, 0, st>>>(px, py, pz, g, list, cx, cy, cz, r2, data, value_bits, mask, edited, c);
+    else if (esize == 2) sphere_tiles_kernel<2><<<grid, BLOCK, 0, st>>>(px, py, pz, g, list, cx, cy, cz, r2, data, value_bits, mask, edited, c);
+    else sphere_tiles_kernel<4><<<grid, BLOCK, 0, st>>>(px, py, pz, g, list, cx, cy, cz, r2, data, value_bits, mask, edited, c);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_select_sphere_batch_tiles(const float* pos, int64_t pos_stride, int64_t width, int64_t rows,
+                                 const float* boxes, void* workspace, size_t workspace_bytes,
+                                 const double* strokes, const int32_t* layer_of,
+                                 const uint32_t* value_bits, int64_t K,
+                                 void* const* data, uint8_t* const* mask, uint8_t* const* edited,
+                                 int64_t L, int esize, uint64_t* counts, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
+    if (width <= 0 || rows <= 0 || K <= 0) return ML_OK;
+    const float *px = pos, *py = pos + pos_stride, *pz = pos + 2 * pos_stride;
+    if (!(aligned(px, 16) && aligned(py, 16) && aligned(pz, 16)))
+        return ml_fail(ML_ERR_ARG, "batched sphere brush needs 16-byte aligned planes");
+    TileGrid g; TileList list;
+    const int rc = tiles_prepare(width, rows, boxes, workspace, workspace_bytes, strokes, K, 0.0, 0.0, 0.0, 0.0, g, list, st);
+    if (rc != ML_OK) return rc;
+    BatchArgs a{px, py, pz, (long long)width * rows, strokes, layer_of, value_bits, K, data, mask, edited, L,
+                (unsigned long long*)counts};
+    const unsigned grid = (unsigned)(ml_sm_count() * 8);
+    if (esize == 1) sphere_batch_tiles_kernel<1><<<grid, BLOCK, 0, st>>>(a, g, (const float4*)boxes, list);
+    else if (esize == 2) sphere_batch_tiles_kernel<2><<<grid, BLOCK, 0, st>>>(a, g, (const float4*)boxes, list);
+    else sphere_batch_tiles_kernel<4><<<grid, BLOCK, 0, st>>>(a, g, (const float4*)boxes, list);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

@@ -122,6 +122,7 @@ class StrokeContext:
         nwords = _native.tea_tile_words(surface.width, surface.rows)
         self.tiles = [torch.zeros(nwords, dtype=torch.int32, device=device) for _ in range(2)] if nwords else None
         self.edited_fully_dirty = False
+        self.stroke_tiles = None          # tile bitmap of the last culled stroke (footprint of ctx.edited)
         self.device = device
 
 
@@ -155,29 +156,34 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
                            scratch=ctx.scratch, height=s.height, tiles=(ctx.tiles[0], ctx.tiles[1]),
                            known_fragments=s.covered)
         ctx.tiles.reverse()                                   # this stroke's footprint is the next one's "previous"
+        ctx.stroke_tiles = ctx.tiles[1]                       # footprint of the marks now in ctx.edited (for TPA)
     elif s.overlap == 0 and not force_direct:
         ctx.edited.zero_()
         ctx.edited_fully_dirty = True
+        ctx.stroke_tiles = None
         _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
                            scratch=ctx.scratch)
     else:
         ctx.edited.zero_()
         ctx.edited_fully_dirty = True
+        ctx.stroke_tiles = None
         _native.raster_tea(ctx.tri_xy, ctx.tri_clip, *args, height=s.height, row0=s.row0, counts=counts)
     return EditResult(edited_mask=ctx.edited, _counts=counts)
 
 
-def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):
+def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True):
     """The service's ``stroke`` (the edit the paper times): TEA
     (``apply_stroke``) followed by TPA (``apply_padding``) with the tool's padding radius.
     ``outline`` is the layer-resolution outline mask (``build_outline_mask``).  The padded count
-    stays on the device like the other counters (``EditResult.padded_count``)."""
+    stays on the device like the other counters (``EditResult.padded_count``).  With ``cull`` both
+    passes touch only the stroke's footprint tiles."""
     torch = _native._torch()
-    res = apply_stroke(ctx, tool, layer, eps=eps)
+    res = apply_stroke(ctx, tool, layer, eps=eps, cull=cull)
     if tool.padding_radius > 0:
         pc = torch.zeros(1, dtype=torch.int64, device=ctx.device)
         as_u8 = outline.view(torch.uint8) if outline.dtype == torch.bool else outline
-        _native.apply_padding(as_u8, ctx.edited, tool.padding_radius, layer.data, layer.mask, tool.value, counts=pc)
+        _native.apply_padding(as_u8, ctx.edited, tool.padding_radius, layer.data, layer.mask, tool.value, counts=pc,
+                              tiles=ctx.stroke_tiles if cull else None)
         res._padded = pc
     return res
 
@@ -185,22 +191,26 @@ def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):
 # --------------------------------------------------------------------------------------------
 # north-star selection brushes
 
-def select_sphere(surface, layer, center, radius, value, edited=None):
+def select_sphere(surface, layer, center, radius, value, edited=None, *, cull=True):
     """Sphere brush: every covered texel whose surface point lies within ``radius`` of ``center``
-    gets data = value, mask = true (definition: oracle ext_select_sphere)."""
+    gets data = value, mask = true (definition: oracle ext_select_sphere).  ``cull`` (default) reads
+    only the position-map tiles the sphere can reach (identical result, O(footprint) traffic);
+    ``cull=False`` streams the whole map (12 B/texel)."""
     torch = _native._torch()
     if layer.shape != (surface.rows, surface.width):
         raise TargetMismatch("layer does not match the surface map")
     if edited is None:
         edited = torch.zeros(layer.shape, dtype=torch.uint8, device=surface.pos.device)
     counts = torch.zeros(1, dtype=torch.int64, device=surface.pos.device)
-    _native.select_sphere(surface.pos, center, radius, layer.data, layer.mask, edited, value, counts=counts)
+    _native.select_sphere(surface.pos, center, radius, layer.data, layer.mask, edited, value, counts=counts,
+                          tiles=surface.tiles if cull else None)
     return EditResult(edited_mask=edited, _counts=counts, transfer_bytes=40)
 
 
-def select_sphere_batch(surface, batch):
-    """K strokes over L layers in one pass (``batch`` = _native.StrokeBatch after upload)."""
-    _native.select_sphere_batch(surface.pos, batch)
+def select_sphere_batch(surface, batch, *, cull=True):
+    """K strokes over L layers in one pass (``batch`` = _native.StrokeBatch after upload); ``cull``
+    as in ``select_sphere``."""
+    _native.select_sphere_batch(surface.pos, batch, tiles=surface.tiles if cull else None)
     return batch.counts
 
 

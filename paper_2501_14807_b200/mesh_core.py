@@ -161,6 +161,8 @@ class SurfaceMap:
         self.width, self.height, self.row0 = width, height, row0
         self.rows = int(self.tri_id.shape[0])
         self.tri_xy = tri_xy                                    # device (T,3,2), reused by TEA
+        # per-tile position boxes for the footprint-culled sphere brushes (None: width % 128 != 0)
+        self.tiles = _native.tile_boxes(self.pos)
 
     @property
     def coverage(self):

@@ -177,6 +177,49 @@ def test_stroke_with_padding_equals_oracle():                         # SPEC.md:
     assert pad_set.sum() == padded and not (pad_set & cov).any()                     # disjoint, inside outline
 
 
+@pytest.mark.parametrize("kind,radius", [("uint8", 1), ("uint8", 4), ("int16", 2), ("uint32", 3)])
+def test_culled_stroke_sequence_with_padding_equals_oracle(kind, radius):
+    """stroke() = TEA + TPA with footprint culling in BOTH passes, a sequence of strokes on one
+    context (the edited mask is only cleared per footprint): planes, edit and padded counts equal
+    the oracle after every stroke, and equal the un-culled stroke()."""
+    rng = np.random.default_rng(33 + radius)
+    mesh = synth.icosphere_mesh(3)
+    A, W = 256, 160
+    cam = synth.default_camera(W, W)
+    surf = ml.build_surface_map(mesh, A, A)
+    depth = ml.render_depth(mesh, cam)
+    ctx = ml.StrokeContext(mesh, cam, depth, surf)
+    ctx_full = ml.StrokeContext(mesh, cam, depth, surf)
+    outline = ml.build_outline_mask(surf.coverage, thickness=radius)
+    ref_outline = kn.outline((surf.tri_id >= 0).cpu().numpy().astype(np.uint8), radius)
+    pool = ml.TexturePool()
+    layer = ml.create_layer("L", kind, A, A, pool=pool)
+    layer_full = ml.create_layer("F", kind, A, A, pool=pool)
+    npk = {"uint8": np.uint8, "int16": np.int16, "uint32": np.uint32}[kind]
+    data = np.zeros((A, A), npk); mask = np.zeros((A, A), bool)
+    total_padded = 0
+    for k in range(8):
+        tool = ml.EditingTool(px=float(rng.uniform(30, 130)), py=float(rng.uniform(30, 130)),
+                              shape=synth.circle_shape(int(rng.integers(3, 25))), value=k + 1, padding_radius=radius)
+        edited = np.zeros((A, A), np.uint8)
+        want = _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+        padded = kn.padding(ref_outline, edited, radius, data, mask, k + 1)
+        res = ml.stroke(ctx, tool, layer, outline)
+        assert ctx.stroke_tiles is not None
+        assert (res.edited_count, res.fragments) == want and res.padded_count == padded, k
+        got = layer.data.view(_torch_i32()) if kind == "uint32" else layer.data
+        assert np.array_equal(got.cpu().numpy().view(npk), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+        res2 = ml.stroke(ctx_full, tool, layer_full, outline, cull=False)
+        assert (res2.edited_count, res2.padded_count) == (want[0], padded)
+        total_padded += padded
+    assert total_padded > 0
+
+
+def _torch_i32():
+    import torch
+    return torch.int32
+
+
 # ------------------------------------------------------------------ display + files (f3)
 
 @pytest.mark.parametrize("kind", ["uint8", "int16", "float32", "float16", "uint32", "int8", "int32"])

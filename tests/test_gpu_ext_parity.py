@@ -156,6 +156,73 @@ def test_select_sphere_batch_equals_sequential(sphere_map, nlayers, K):
         assert np.array_equal(gm[L].cpu().numpy(), masks[L]) and np.array_equal(ge[L].cpu().numpy(), eds[L])
 
 
+def test_tile_boxes_bound_the_positions(sphere_map):
+    """Boxes of the 128 x 4-texel tiles: exact min / max of the covered positions, lo > hi when a
+    tile has no covered texel."""
+    _, ref, got = sphere_map
+    tiles = nat.tile_boxes(got["pos"])
+    assert tiles is not None and tiles.boxes.shape == (2 * 64, 8)
+    boxes = tiles.boxes.cpu().numpy()
+    pos = ref["pos"]
+    for ty in range(64):
+        for tx in range(2):
+            blk = pos[:, 4 * ty: 4 * ty + 4, 128 * tx: 128 * tx + 128].reshape(3, -1)
+            b = boxes[ty * 2 + tx]
+            if np.isnan(blk[0]).all():
+                assert b[0] > b[4]
+            else:
+                assert np.array_equal(b[0:3], np.nanmin(blk, axis=1)) and np.array_equal(b[4:7], np.nanmax(blk, axis=1))
+    assert nat.tile_boxes(got["pos"][:, :, :200].contiguous()) is None          # width % 128 != 0: no culling
+
+
+@pytest.mark.parametrize("kind,value", [(np.uint8, 9), (np.int16, -5), (np.uint32, 77777)])
+def test_select_sphere_culled_bit_exact(sphere_map, kind, value):
+    """Footprint-culled brush == oracle (planes and count), incl. a brush that misses everything, one
+    that covers everything, a zero radius on a surface point and ragged slab heights."""
+    _, ref, got = sphere_map
+    rng = np.random.default_rng(5)
+    onpoint = tuple(float(v) for v in ref["pos"][:, 130, 70])
+    assert not np.isnan(onpoint[0])
+    for rows in (256, 255, 3):
+        pos_ref = np.ascontiguousarray(ref["pos"][:, :rows])
+        pos_dev = got["pos"][:, :rows].contiguous()
+        tiles = nat.tile_boxes(pos_dev)
+        for center, radius in (((0.0, 0.0, 1.0), 0.25), ((0.6, -0.5, 0.3), 0.6), ((5.0, 5.0, 5.0), 0.1),
+                               ((0, 0, 0), 2.0), (onpoint, 0.0), ((0.0, 0.0, 1.0), 1e-3)):
+            data0 = rng.integers(0, 4, size=(rows, 256)).astype(kind)
+            mask0 = rng.random((rows, 256)) < 0.2
+            ed0 = (rng.random((rows, 256)) < 0.1).astype(np.uint8)
+            rd, rm, re = data0.copy(), mask0.copy(), ed0.copy()
+            want = kn.select_sphere(pos_ref, center, radius, rd, rm, re, value)
+            d, m, e = _dev(data0), _dev(mask0), _dev(ed0)
+            assert nat.select_sphere(pos_dev, center, radius, d, m, e, value, tiles=tiles) == want
+            assert np.array_equal(_bits(_host(d)), _bits(rd))
+            assert np.array_equal(m.cpu().numpy(), rm) and np.array_equal(e.cpu().numpy(), re)
+
+
+@pytest.mark.parametrize("nlayers,K", [(1, 40), (5, 64), (70, 150)])
+def test_select_sphere_batch_culled_equals_sequential(sphere_map, nlayers, K):
+    import torch
+    mesh, ref, got = sphere_map
+    strokes, labels = synth.sphere_strokes(mesh, K, seed=21 + K, rmin_frac=0.005, rmax_frac=0.2)
+    layer_of = (np.arange(K) * 7) % nlayers
+    datas = [np.zeros((256, 256), np.uint8) for _ in range(nlayers)]
+    masks = [np.zeros((256, 256), bool) for _ in range(nlayers)]
+    eds = [np.zeros((256, 256), np.uint8) for _ in range(nlayers)]
+    want = np.zeros(nlayers, np.int64)
+    for k in range(K):
+        L = layer_of[k]
+        want[L] += kn.select_sphere(ref["pos"], strokes[k, :3], strokes[k, 3], datas[L], masks[L], eds[L], labels[k])
+    mk = lambda dt: [torch.zeros((256, 256), dtype=dt, device="cuda") for _ in range(nlayers)]
+    gd, gm, ge = mk(torch.uint8), mk(torch.bool), mk(torch.uint8)
+    batch = nat.StrokeBatch(gd, gm, ge, "cuda").upload(strokes, layer_of, labels)
+    nat.select_sphere_batch(got["pos"], batch, tiles=nat.tile_boxes(got["pos"]))
+    assert np.array_equal(batch.counts.cpu().numpy(), want)
+    for L in range(nlayers):
+        assert np.array_equal(gd[L].cpu().numpy(), datas[L]), L
+        assert np.array_equal(gm[L].cpu().numpy(), masks[L]) and np.array_equal(ge[L].cpu().numpy(), eds[L])
+
+
 @pytest.mark.parametrize("akind", [np.float32, np.float16, np.uint8, np.int8, np.int16, np.int32, np.uint32])
 def test_select_threshold_bit_exact(akind):
     rng = np.random.default_rng(6)

@@ -106,6 +106,38 @@ def test_strokes_idempotent_and_algebra_identities(big):
     assert lc.sum() == counts[2] and abs(la.sum() - areas[2]) <= 1e-9 * areas[2]
 
 
+def test_culled_brushes_equal_streamed_at_full_size(big):
+    """16384^2: the footprint-culled sphere brush (single and batched) gives the planes and counts of
+    the whole-map streaming kernels."""
+    mesh, surf, cam, ctx, pool = big
+    import torch
+    assert surf.tiles is not None
+    strokes, labels = synth.sphere_strokes(mesh, 6, seed=13, rmin_frac=0.002, rmax_frac=0.08)
+    a = ml.create_layer("cull", "uint8", A, A, pool=pool)
+    b = ml.create_layer("full", "uint8", A, A, pool=pool)
+    ea = torch.zeros((A, A), dtype=torch.uint8, device="cuda")
+    eb = torch.zeros((A, A), dtype=torch.uint8, device="cuda")
+    for k in range(6):
+        ra = ml.select_sphere(surf, a, strokes[k, :3], strokes[k, 3], int(labels[k]), edited=ea)
+        rb = ml.select_sphere(surf, b, strokes[k, :3], strokes[k, 3], int(labels[k]), edited=eb, cull=False)
+        assert ra.edited_count == rb.edited_count
+    assert _checksum(a.data) == _checksum(b.data) and _checksum(ea) == _checksum(eb)
+    assert _checksum(a.mask.view(torch.uint8)) == _checksum(b.mask.view(torch.uint8))
+    a2 = ml.create_layer("cull2", "uint8", A, A, pool=pool)
+    b2 = ml.create_layer("full2", "uint8", A, A, pool=pool)
+    ea.zero_(); eb.zero_()
+    lo = np.zeros(6, np.int64)
+    ba = nat.StrokeBatch([a2.data], [a2.mask], [ea], "cuda").upload(strokes, lo, labels)
+    bb = nat.StrokeBatch([b2.data], [b2.mask], [eb], "cuda").upload(strokes, lo, labels)
+    ml.select_sphere_batch(surf, ba)
+    ml.select_sphere_batch(surf, bb, cull=False)
+    assert int(ba.counts[0]) == int(bb.counts[0]) > 0
+    assert _checksum(a2.data) == _checksum(b2.data) and _checksum(ea) == _checksum(eb)
+    assert _checksum(a2.data) == _checksum(a.data)               # batch == sequential
+    for l in (a, b, a2, b2):
+        l.release()
+
+
 def test_batched_strokes_equal_sequential_at_full_size(big):
     mesh, surf, cam, ctx, pool = big
     import torch

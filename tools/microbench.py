@@ -125,6 +125,16 @@ def main():
     pos = torch.rand((3, N, N), device=dev, generator=g)
     run("sphere few hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.05, data, mask, edited, 3, counts=cnt), 12 * n)
     run("sphere 50% hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.62, data, mask, edited, 3, counts=cnt), 12 * n)
+    # smooth "surface" positions (a heightfield over the atlas) for the footprint-culled brushes
+    if not want or any(w in "sphere culled" for w in want):
+        yy, xx = torch.meshgrid(torch.linspace(0, 1, N, device=dev), torch.linspace(0, 1, N, device=dev), indexing="ij")
+        spos = torch.stack([xx, yy, 0.1 * torch.sin(7 * xx) * torch.cos(5 * yy)]).contiguous()
+        del yy, xx
+        tiles = nat.tile_boxes(spos)
+        for r in (0.005, 0.02, 0.08, 0.3):
+            run("sphere stream  r=%.3f" % r, lambda r=r: nat.select_sphere(spos, (0.5, 0.5, 0.0), r, data, mask, edited, 3, counts=cnt), 12 * n)
+            run("sphere culled  r=%.3f" % r, lambda r=r: nat.select_sphere(spos, (0.5, 0.5, 0.0), r, data, mask, edited, 3, counts=cnt, tiles=tiles), 12 * n)
+        del spos, tiles
     area = pos[0]
     masks = [m2, mask, out, d2]
     run("area L=1", lambda: nat.layer_area(area, masks[:1], sums=torch.zeros(1, dtype=torch.float64, device=dev),
