@@ -10,6 +10,10 @@ One STEP = one pass of every hot-path stage over this rank's 16384 x 16384 atlas
     tpa        the paper's padding pass (TPA): outline texels next to the stroke
     sphere     one sphere-brush stroke over the float32x3 position map
     batch      L sphere strokes (one per layer) batched in ONE pass over the position map
+               (these four brush stages run the public API's default footprint-culled kernels: a
+               stroke reads only the tiles it can reach; ``--no-cull`` streams the whole atlas, and
+               the whole-atlas streaming kernels are ALSO timed on their own and reported under
+               ``config.stream_kernels`` -- they are the brush kernels' HBM-roofline evidence)
     chain      fused layer-algebra chain ((L0 u L1) n L2) \\ L3 ... over 8 uint8 layers (C3)
     mask_op    binary union of two bare uint8 mask planes (the 3 B/texel streaming kernel)
     threshold  attribute-threshold selection on the float32 attribute plane pos.z (C3)
@@ -58,7 +62,8 @@ def parse():
     ap.add_argument("--window", type=int, default=1024)
     ap.add_argument("--cpu-rows", type=int, default=1024, help="rows of the slab the CPU baseline processes")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-cull", action="store_true", help="TEA streams the whole triangle-id map (no footprint culling)")
+    ap.add_argument("--no-cull", action="store_true",
+                    help="brush stages (tea, tpa, sphere, batch) stream the whole atlas instead of their footprint tiles")
     ap.add_argument("--stages", default=",".join(STAGES))
     return ap.parse_args()
 
@@ -324,32 +329,36 @@ def run_ours(args):
     area_counts = torch.zeros(L, dtype=torch.int64, device=dev)
     counts2 = torch.zeros(2, dtype=torch.int64, device=dev)
     counts1 = torch.zeros(1, dtype=torch.int64, device=dev)
-    launches = {"tea": 3, "tpa": 1, "sphere": 1, "batch": 1, "chain": 1, "mask_op": 1, "threshold": 1, "area": -(-L // 8)}
+    culled = not args.no_cull and surf.tiles is not None
+    launches = {"tea": 3, "tpa": 1, "sphere": 2 if culled else 1, "batch": 2 if culled else 1, "chain": 1, "mask_op": 1,
+                "threshold": 1, "area": -(-L // 8)}
 
-    def stage_call(st, inp, tool, mode):
+    def stage_call(st, inp, tool, mode, cull=not args.no_cull):
         """Run one stage through the public API and return its result as DEVICE tensors (nothing
         synchronises here).  mode "resident": stroke records were uploaded before the timed region;
         "e2e": this step's records come from the host now (pinned staging -> device)."""
         out = []
         if st == "tea":
             # --no-cull streams the whole id map instead of the stroke's footprint tiles
-            r = ml.apply_stroke(ctx, tool, layers[0], eps=wl.eps, cull=not args.no_cull)
+            r = ml.apply_stroke(ctx, tool, layers[0], eps=wl.eps, cull=cull)
             out = [r._counts]
         elif st == "tpa":
             # padding of the stroke just applied (the paper times TEA + TPA per edit, PAPER.md:241);
             # a slab's stencil would need the neighbours' edited rows: radius-1 halo, local rows here
             counts1.zero_()
-            nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1)
+            nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1,
+                              tiles=ctx.stroke_tiles if cull else None)
             out = [counts1.clone()]
         elif st == "sphere":
             s = inp["sphere"]
-            out = [ml.select_sphere(surf, layers[1 % L], s[:3], s[3], inp["sphere_value"], edited=edited[1 % L])._counts]
+            out = [ml.select_sphere(surf, layers[1 % L], s[:3], s[3], inp["sphere_value"], edited=edited[1 % L],
+                                    cull=cull)._counts]
         elif st == "batch":
             if mode == "e2e":
                 s, lo, v = sharding.broadcast_strokes(inp["batch"], inp["batch_layers"], inp["batch_values"].astype(np.uint32), dev)
                 batch.upload(s, lo, v.astype(np.uint8))
             batch.counts.zero_()
-            out = [ml.select_sphere_batch(surf, batch).clone()]
+            out = [ml.select_sphere_batch(surf, batch, cull=cull).clone()]
         elif st == "chain":
             ml.layer_chain(layers[:wl.chain_n], wl.chain_ops, out_layer)
         elif st == "mask_op":
@@ -453,6 +462,28 @@ def run_ours(args):
             if st in ("tea", "tpa", "sphere", "batch", "threshold"):
                 hits[st] += float(r[0].reshape(-1)[0].item() if st != "batch" else r[0].sum().item()) / ncen
 
+    # ---- whole-atlas streaming forms of the brush stages, timed on their own (cull=False): the
+    # HBM-roofline evidence for the brush kernels (SURVEY.md 8(d) algorithmic bytes / time)
+    stream_info = {}
+    if not args.no_cull:
+        reps = max(5, min(20, args.steps))
+        for st in [s for s in ("tea", "tpa", "sphere", "batch") if s in stages]:
+            ms_acc = 0.0
+            for k in range(reps + 2):
+                inp = inputs[args.warmup + (k % args.steps)]
+                tool = make_tool(inp)
+                if st == "tpa":
+                    stage_call("tea", inp, tool, "resident", cull=False)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                stage_call(st, inp, tool, "resident", cull=False)
+                b.record()
+                torch.cuda.synchronize()
+                if k >= 2:
+                    ms_acc += a.elapsed_time(b)
+            stream_info[st] = ms_acc / reps
+        ctx.edited.zero_()
+
     texel_passes = len(stages) * n * world_size
     value = texel_passes * args.steps / (total_ms * 1e-3) / 1e9
     e2e_value = texel_passes * args.steps / (e2e_ms * 1e-3) / 1e9
@@ -464,6 +495,12 @@ def run_ours(args):
         stage_info[st] = {"ms": round(stage_ms[st], 4), "gtexel_s": round(n / (stage_ms[st] * 1e-3) / 1e9, 2),
                           "alg_bytes": b, "gb_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
                           "hits_per_step": int(hits[st]), "launches": launches[st]}
+        if st in ("tea", "tpa", "sphere", "batch"):
+            stage_info[st]["footprint_culled"] = not args.no_cull
+    peak_now = peak
+    stream_kernels = {st: {"ms": round(ms, 4), "gb_s": round(wl.algorithmic_bytes(n, st, T, hits[st]) / (ms * 1e-3) / 1e9, 1),
+                           "frac_of_peak": round(wl.algorithmic_bytes(n, st, T, hits[st]) / (ms * 1e-3) / 1e9 / peak_now, 4)}
+                      for st, ms in stream_info.items()}
     dom = max(stages, key=lambda s: stage_ms[s])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -496,7 +533,8 @@ def run_ours(args):
         cfg["stage_results"] = stage_info
         cfg["setup_s"] = round(setup_s, 2)
         cfg["surface_map"] = {"covered": surf.covered, "overlap": surf.overlap}
-        cfg["tea_footprint_culling"] = not args.no_cull
+        cfg["footprint_culling"] = not args.no_cull
+        cfg["stream_kernels"] = stream_kernels
         print(json.dumps({
             "metric": "brush-apply + layer-op texel passes per second at 16384^2 atlas",
             "value": value, "unit": "Gtexel/s", "n_gpus": world_size, "steps": args.steps, "warmup": args.warmup,

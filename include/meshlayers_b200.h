@@ -120,8 +120,15 @@ size_t ml_surface_workspace_bytes(int64_t ntri);
  * (the slab's covered-texel count, which a skipping kernel cannot recount); tile_prev (may be NULL)
  * = the bitmap of the previous stroke on this `edited` plane: its tiles are cleared in the same
  * pass, which replaces the whole-plane reset of the EditedAreaMask.  Pass NULL, NULL, 0
- * to stream every texel (then the caller resets `edited` itself). */
-int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
+ * to stream every texel (then the caller resets `edited` itself).
+ * A tile buffer is ml_tea_tile_words() words: [bitmap | u64 count | u32 list of marked tiles].
+ * tea_recs (may be NULL): per-triangle evaluation records written by ml_tea_prepare for the same
+ * tri_xy / tri_clip (CCW-normalised vertices + clip coordinates as float64, 144 bytes each); with
+ * them the evaluation does nine 128-bit loads per texel instead of re-deriving the winding. */
+size_t ml_tea_rec_bytes(int64_t ntri);
+int ml_tea_prepare(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri, void* recs,
+                   size_t rec_bytes, void* stream);
+int ml_tea_texels(const void* tri_xy, const void* tri_clip, const void* tea_recs, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
                   const uint32_t* tri_flags, const ml_tea_params* params, void* worklist,
                   size_t worklist_bytes, const uint32_t* tile_cur, const uint32_t* tile_prev,

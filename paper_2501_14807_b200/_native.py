@@ -74,8 +74,10 @@ def lib():
         "ml_raster_tri_id": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
         "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp]),
         "ml_surface_workspace_bytes": (sz, [i64]),
-        "ml_tea_texels": (i32, [vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
+        "ml_tea_texels": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
                                 vp, vp, i64, vp, i32, u32, vp, vp, vp, vp]),
+        "ml_tea_rec_bytes": (sz, [i64]),
+        "ml_tea_prepare": (i32, [vp, vp, i32, i64, vp, sz, vp]),
         "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
         "ml_tea_tile_words": (i32, [i64, i64]),
         "ml_select_sphere": (i32, [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
@@ -115,7 +117,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve",
-    "ml_surface_workspace_bytes", "ml_tea_texels",
+    "ml_surface_workspace_bytes", "ml_tea_texels", "ml_tea_rec_bytes", "ml_tea_prepare",
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
     "ml_select_threshold", "ml_layer_op",
@@ -451,7 +453,7 @@ def raster_tri_id(tri_xy, width, height, *, row0=0, rows=None, device=None):
 
 def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
                shape, data, mask, edited, value, *, row0=0, counts=None, classify=True, scratch=None,
-               height=None, tiles=None, known_fragments=0):
+               height=None, tiles=None, known_fragments=0, recs=None):
     """TEA over the cached triangle-id map (SURVEY.md 8 note N1): same planes and counts as
     ``raster_tea`` when the uv layout has no overlaps.  Returns (edited_texels, fragments).
     ``classify`` runs the per-stroke triangle pre-pass (ml_tea_classify) so that texels of
@@ -460,7 +462,9 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
     None) switches on footprint culling: only tiles a flagged triangle's raster bbox touches are
     read, the tiles of ``prev`` (the previous stroke's ``cur``) have their ``edited`` bytes
     cleared, and ``known_fragments`` (the slab's covered texel count) is reported as fragments.
-    The caller must then NOT reset ``edited`` itself and must pass ``height``."""
+    The caller must then NOT reset ``edited`` itself and must pass ``height``.  ``recs`` (from
+    ``tea_prepare`` for the same triangle arrays) makes the evaluation read one prepared 144-byte
+    record per triangle instead of re-deriving the winding per texel (identical result)."""
     torch = require_cuda()
     rows, w = mask.shape
     dev = mask.device
@@ -492,7 +496,7 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
                                      int(height if height is not None else row0 + rows), row0, rows, _ptr(cur),
                                      _stream()))
     cur, prev = tiles if tiles else (None, None)
-    _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
+    _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), _ptr(recs), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
                                _ptr(flags), C.byref(p), _ptr(work), 0 if work is None else work.numel() * 8,
                                _ptr(cur), _ptr(prev), int(known_fragments),
                                _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr), _stream()))
@@ -502,7 +506,22 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
     return int(c[0]), int(c[1])
 
 
-def tea_scratch(ntri, ntexels, device, max_quads=1 << 22):
+def tea_prepare(tri_xy, tri_clip, device=None):
+    """Per-triangle records of the TEA evaluation (CCW-normalised uv vertices + clip coordinates in
+    float64), valid while the triangle arrays and the camera do not change."""
+    torch = require_cuda()
+    dev = torch.device(device or tri_xy.device)
+    tri, _ = _tri_dev(tri_xy, (3, 2), dev)
+    clip, _ = _tri_dev(tri_clip, (3, 4), dev)
+    tri, clip = _same_dtype(tri, clip)
+    dt = ML_F32 if tri.dtype == torch.float32 else ML_F64
+    nb = int(lib().ml_tea_rec_bytes(tri.shape[0]))
+    recs = torch.empty(nb, dtype=torch.uint8, device=dev)
+    _check(lib().ml_tea_prepare(_ptr(tri), _ptr(clip), dt, tri.shape[0], _ptr(recs), nb, _stream()))
+    return recs
+
+
+def tea_scratch(ntri, ntexels, device, max_quads=1 << 24):
     """Per-stroke scratch of ``tea_texels``: triangle flags and the quad work list (device)."""
     torch = _torch()
     cap = max(8, min((ntexels + 3) // 4, max_quads))

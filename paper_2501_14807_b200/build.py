@@ -42,6 +42,7 @@ def build(force=False, verbose=False):
     cmd = [nvcc] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     if verbose:
         cmd += ["-Xptxas", "-v"]
+    cmd += os.environ.get("ML_NVCC_EXTRA", "").split()          # tuning experiments: extra -D flags
     cmd += ["-o", LIB] + sources()
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:

@@ -286,6 +286,30 @@ struct TeaParams {
     int eps_f32;            // 1: depth+eps rounded to float32 (numpy weak-scalar rule), 0: float64
 };
 
+// Filters after the clip-space interpolation: window KN:181, depth KN:185, tool range KN:189, shape
+// KN:193.  The three last ones are independent tests ANDed together; they are evaluated in the
+// order that lets the two dependent gathers (depth sample, shape sample) overlap each other and
+// the zn division.  zc is passed in (KN:172 is computed by the caller from the same l's).
+ML_DEV bool tea_filters(const TeaParams& p, double xc, double yc, double zc, double wc) {
+    const double xn = xdiv(xc, wc), yn = xdiv(yc, wc);                            // KN:176-177
+    const double xw = xmul(xmul(xadd(xn, 1.0), 0.5), p.ww);                       // KN:179
+    const double yw = xmul(xmul(xadd(yn, 1.0), 0.5), p.wh);                       // KN:180
+    if (!((xw >= 0.0) && (xw < p.ww) && (yw >= 0.0) && (yw < p.wh))) return false;    // KN:181
+    const long long px = (long long)xw, py = (long long)yw;                       // KN:182-183
+    const float dv = __ldg(p.depth + py * p.dw + px);
+    const double s = xadd(xmul(p.sfx, xn), p.bx);                                 // KN:187
+    const double t = xadd(xmul(p.sfy, yn), p.by);                                 // KN:188
+    if (!((s >= 0.0) && (s <= 1.0) && (t >= 0.0) && (t <= 1.0))) return false;    // KN:189
+    long long si = (long long)xmul(s, (double)p.tw), ti = (long long)xmul(t, (double)p.th);
+    if (si > p.tw - 1) si = p.tw - 1;                                             // KN:191
+    if (ti > p.th - 1) ti = p.th - 1;                                             // KN:192
+    const uint8_t sh = __ldg(p.shape + ti * p.tw + si);                           // KN:193
+    const double zn = xdiv(zc, wc);                                               // KN:178
+    const double df = xmul(xadd(zn, 1.0), 0.5);                                   // KN:184
+    const double lim = p.eps_f32 ? (double)__fadd_rn(dv, (float)p.eps) : xadd((double)dv, p.eps);
+    return (df <= lim) && (sh != 0);                                              // KN:185, 193
+}
+
 ML_DEV bool tea_fragment(const TeaParams& p, double e0, double e1, double e2,
                          const double* __restrict__ c0, const double* __restrict__ c1,
                          const double* __restrict__ c2) {
@@ -295,22 +319,6 @@ ML_DEV bool tea_fragment(const TeaParams& p, double e0, double e1, double e2,
     if (!(wc > 0.0)) return false;                                                // KN:174
     const double xc = xadd(xadd(xmul(l0, c0[0]), xmul(l1, c1[0])), xmul(l2, c2[0]));  // KN:170
     const double yc = xadd(xadd(xmul(l0, c0[1]), xmul(l1, c1[1])), xmul(l2, c2[1]));  // KN:171
-    const double xn = xdiv(xc, wc), yn = xdiv(yc, wc);                            // KN:176-177
-    const double xw = xmul(xmul(xadd(xn, 1.0), 0.5), p.ww);                       // KN:179
-    const double yw = xmul(xmul(xadd(yn, 1.0), 0.5), p.wh);                       // KN:180
-    if (!((xw >= 0.0) && (xw < p.ww) && (yw >= 0.0) && (yw < p.wh))) return false;    // KN:181
     const double zc = xadd(xadd(xmul(l0, c0[2]), xmul(l1, c1[2])), xmul(l2, c2[2]));  // KN:172
-    const double zn = xdiv(zc, wc);                                               // KN:178
-    const long long px = (long long)xw, py = (long long)yw;                       // KN:182-183
-    const double df = xmul(xadd(zn, 1.0), 0.5);                                   // KN:184
-    const float dv = __ldg(p.depth + py * p.dw + px);
-    const double lim = p.eps_f32 ? (double)__fadd_rn(dv, (float)p.eps) : xadd((double)dv, p.eps);
-    if (!(df <= lim)) return false;                                               // KN:185
-    const double s = xadd(xmul(p.sfx, xn), p.bx);                                 // KN:187
-    const double t = xadd(xmul(p.sfy, yn), p.by);                                 // KN:188
-    if (!((s >= 0.0) && (s <= 1.0) && (t >= 0.0) && (t <= 1.0))) return false;    // KN:189
-    long long si = (long long)xmul(s, (double)p.tw), ti = (long long)xmul(t, (double)p.th);
-    if (si > p.tw - 1) si = p.tw - 1;                                             // KN:191
-    if (ti > p.th - 1) ti = p.th - 1;                                             // KN:192
-    return __ldg(p.shape + ti * p.tw + si) != 0;                                  // KN:193
+    return tea_filters(p, xc, yc, zc, wc);
 }

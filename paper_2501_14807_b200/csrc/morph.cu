@@ -204,35 +204,54 @@ __global__ void __launch_bounds__(BLOCK)
 padding_tile_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ edited, long long width,
                     long long rows, int r, const uint32_t* __restrict__ tile_bits,
                     void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask, unsigned long long* count) {
-    const int lane = threadIdx.x & 31;
+    __shared__ int s_list[BLOCK];
+    __shared__ int s_n;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int segs = (int)(width >> 7);
     const int tile_rows = (int)((rows + 7) >> 3);
     const int ntiles = segs * tile_rows;
-    const int nwarps = gridDim.x * (BLOCK / 32);
     long long cnt = 0;
-    for (int tile = blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); tile < ntiles; tile += nwarps) {
-        const int ty = tile / segs, tx = tile - ty * segs;
+    // each thread tests ONE tile's 3 x 3 neighbourhood; the block compacts the tiles to visit into
+    // shared memory and its warps share them (the marked tiles of a stroke are clustered)
+    for (int base = blockIdx.x * BLOCK; base < ntiles; base += gridDim.x * BLOCK) {
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const int tile = base + threadIdx.x;
         bool near = false;
+        if (tile < ntiles) {
+            const int ty = tile / segs, tx = tile - ty * segs;
 #pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
+            for (int dy = -1; dy <= 1; ++dy)
 #pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int y = ty + dy, x = tx + dx;
-                if (y < 0 || y >= tile_rows || x < 0 || x >= segs) continue;
-                const int t = y * segs + x;
-                near |= ((__ldg(tile_bits + (t >> 5)) >> (t & 31)) & 1u) != 0;
-            }
-        if (!near) continue;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int v = lane + 32 * k;                       // 64 vectors of 16 texels per tile
-            const long long yy = ((long long)ty << 3) + (v >> 3);
-            if (yy >= rows) continue;
-            const long long i0 = yy * width + ((long long)tx << 7) + ((v & 7) << 4);
-            const uint4 o = ld_stream((const uint4*)(outline + i0));
-            if ((o.x | o.y | o.z | o.w) == 0) continue;
-            cnt += pad_vector<ES>(o, i0, edited, width, 0, rows, 0, r, data, value, mask);
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int y = ty + dy, x = tx + dx;
+                    if (y < 0 || y >= tile_rows || x < 0 || x >= segs) continue;
+                    const int t = y * segs + x;
+                    near |= ((__ldg(tile_bits + (t >> 5)) >> (t & 31)) & 1u) != 0;
+                }
         }
+        const unsigned bal = __ballot_sync(0xffffffffu, near);
+        int off = 0;
+        if (lane == 0 && bal) off = atomicAdd(&s_n, __popc(bal));
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (near) s_list[off + __popc(bal & ((1u << lane) - 1u))] = tile;
+        __syncthreads();
+        const int nlist = s_n;
+        for (int j = wid; j < nlist; j += BLOCK / 32) {
+            const int t = s_list[j];
+            const int ty = t / segs, tx = t - ty * segs;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int v = lane + 32 * k;                   // 64 vectors of 16 texels per tile
+                const long long yy = ((long long)ty << 3) + (v >> 3);
+                if (yy >= rows) continue;
+                const long long i0 = yy * width + ((long long)tx << 7) + ((v & 7) << 4);
+                const uint4 o = ld_stream((const uint4*)(outline + i0));
+                if ((o.x | o.y | o.z | o.w) == 0) continue;
+                cnt += pad_vector<ES>(o, i0, edited, width, 0, rows, 0, r, data, value, mask);
+            }
+        }
+        __syncthreads();
     }
     block_count_add(cnt, count);
 }
@@ -302,7 +321,7 @@ int ml_apply_padding_tiles(const uint8_t* outline, const uint8_t* edited, int64_
         ((((uintptr_t)outline) | ((uintptr_t)edited) | ((uintptr_t)data) | ((uintptr_t)mask)) & 15) != 0)
         return ml_fail(ML_ERR_ARG, "culled padding needs width % 128 == 0, radius <= 4, aligned planes and the stroke's tile bitmap");
     const long long ntiles = (width >> 7) * ((rows + 7) >> 3);
-    long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);
+    long long blocks = (ntiles + BLOCK - 1) / BLOCK;               // one tile per thread in the classification step
     const long long cap = (long long)ml_sm_count() * 8;
     if (blocks > cap) blocks = cap;
     cudaStream_t st = (cudaStream_t)stream;

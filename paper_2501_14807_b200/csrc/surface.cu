@@ -147,6 +147,16 @@ resolve_kernel(const TriRec* __restrict__ recs, long long width, long long row0,
 // which removes the float64 work for everything outside the tool footprint without changing a bit.
 // footprint tiles: 128 texels (one warp-wide 128-bit load) x 8 rows
 constexpr int TILE_W_SHIFT = 7, TILE_H_SHIFT = 3;
+// A tile buffer (ml_tea_tile_words 32-bit words) = [bitmap: tile_bitmap_words][count: u64][list:
+// ntiles u32].  The classification pass appends a tile to the list the first time it marks it, so
+// the texel pass walks a compact list (one warp per listed tile) instead of every tile of the slab.
+__host__ __device__ inline long long tile_bitmap_words(long long ntiles) { return ((ntiles + 63) / 64) * 2; }
+struct TileBuf {
+    uint32_t* bits; unsigned long long* count; uint32_t* list;
+    __host__ __device__ TileBuf(uint32_t* base, long long ntiles)
+        : bits(base), count((unsigned long long*)(base + (base ? tile_bitmap_words(ntiles) : 0))),
+          list(base + (base ? tile_bitmap_words(ntiles) + 2 : 0)) {}
+};
 
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
@@ -193,10 +203,13 @@ tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p,
         TriSetup s;
         if (tri_load_ccw(tri_xy + 6 * t, s) && tri_bbox(s, width, height, row0, rows)) {
             const int segs = (int)(width >> TILE_W_SHIFT);
+            const TileBuf tb(tile_bits, (long long)segs * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT));
             for (int ty = (int)(s.iy0 - row0) >> TILE_H_SHIFT; ty <= (int)(s.iy1 - row0) >> TILE_H_SHIFT; ++ty)
                 for (int tx = s.ix0 >> TILE_W_SHIFT; tx <= s.ix1 >> TILE_W_SHIFT; ++tx) {
                     const int tile = ty * segs + tx;
-                    atomicOr(tile_bits + (tile >> 5), 1u << (tile & 31));
+                    const uint32_t bit = 1u << (tile & 31);
+                    if (ld_volatile_u32(tb.bits + (tile >> 5)) & bit) continue;        // already marked
+                    if (!(atomicOr(tb.bits + (tile >> 5), bit) & bit)) tb.list[atomicAdd(tb.count, 1ull)] = (uint32_t)tile;
                 }
         }
     }
@@ -205,10 +218,57 @@ tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p,
 // flag lookup in the classification bitmap (global or shared memory); NULL bitmap = keep all
 ML_DEV bool tri_flag(const uint32_t* bits, int t) { return bits ? ((bits[t >> 5] >> (t & 31)) & 1u) != 0 : true; }
 
-// Full KN:166-193 evaluation of one covered texel for its owner triangle.
+// Per-triangle record of the TEA evaluation (144 bytes = 9 x 16, written once per camera by
+// tea_prepare_kernel): CCW-normalised uv vertices (KN:32-41) and the clip coordinates widened to
+// float64 in CCW vertex order (KN:40).  The evaluation fetches it with nine independent 128-bit
+// loads instead of 18 scalar gathers behind the winding test.
+struct __align__(16) TeaRec {
+    double x0, y0, x1, y1, x2, y2;
+    double c[12];                     // c0.xyzw, c1.xyzw, c2.xyzw (CCW order)
+};
+static_assert(sizeof(TeaRec) == 144, "TeaRec is nine 16-byte words");
+
+template <typename T>
+__global__ void __launch_bounds__(BLOCK)
+tea_prepare_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long ntri,
+                   TeaRec* __restrict__ recs) {
+    const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    if (t >= ntri) return;
+    TriSetup s;
+    if (!tri_load_ccw(tri_xy + 6 * t, s)) return;     // degenerate / non-finite: owns no texel, never read
+    TeaRec& r = recs[t];
+    r.x0 = s.x0; r.y0 = s.y0; r.x1 = s.x1; r.y1 = s.y1; r.x2 = s.x2; r.y2 = s.y2;
+    const T* c = tri_clip + 12 * t;
+    const int i1 = s.swapped ? 8 : 4, i2 = s.swapped ? 4 : 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { r.c[k] = (double)c[k]; r.c[4 + k] = (double)c[i1 + k]; r.c[8 + k] = (double)c[i2 + k]; }
+}
+
+// Full KN:166-193 evaluation of one covered texel for its owner triangle.  `recs` (may be NULL)
+// are the prepared per-triangle records; both branches compute the same bits.
 template <typename T>
 ML_DEV bool tea_texel_eval_inline(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
-                                  int t, int x, int y, const TeaParams& p) {
+                                  const TeaRec* __restrict__ recs, int t, int x, int y, const TeaParams& p) {
+    if (recs) {
+        // record words: 0..2 = uv vertices, 3/5/7 = (x, y) and 4/6/8 = (z, w) of clip vertices 0/1/2;
+        // fetched in three rounds in the order the arithmetic consumes them (register pressure)
+        const double2* rp = (const double2*)(recs + t);
+        const double2 v0 = __ldg(rp), v1 = __ldg(rp + 1), v2 = __ldg(rp + 2);
+        const double2 zw0 = __ldg(rp + 4), zw1 = __ldg(rp + 6), zw2 = __ldg(rp + 8);
+        const double cx = xadd((double)x, 0.5), cy = xadd((double)y, 0.5);                                    // KN:60, 63
+        const double e0 = xsub(xmul(xsub(v2.x, v1.x), xsub(cy, v1.y)), xmul(xsub(v2.y, v1.y), xsub(cx, v1.x)));   // KN:72
+        const double e1 = xsub(xmul(xsub(v0.x, v2.x), xsub(cy, v2.y)), xmul(xsub(v0.y, v2.y), xsub(cx, v2.x)));   // KN:73
+        const double e2 = xsub(xmul(xsub(v1.x, v0.x), xsub(cy, v0.y)), xmul(xsub(v1.y, v0.y), xsub(cx, v0.x)));   // KN:74
+        const double esum = xadd(xadd(e0, e1), e2);                                   // KN:166
+        const double l0 = xdiv(e0, esum), l1 = xdiv(e1, esum), l2 = xdiv(e2, esum);   // KN:167-169
+        const double wc = xadd(xadd(xmul(l0, zw0.y), xmul(l1, zw1.y)), xmul(l2, zw2.y));  // KN:173
+        if (!(wc > 0.0)) return false;                                                // KN:174
+        const double2 xy0 = __ldg(rp + 3), xy1 = __ldg(rp + 5), xy2 = __ldg(rp + 7);
+        const double xc = xadd(xadd(xmul(l0, xy0.x), xmul(l1, xy1.x)), xmul(l2, xy2.x));  // KN:170
+        const double yc = xadd(xadd(xmul(l0, xy0.y), xmul(l1, xy1.y)), xmul(l2, xy2.y));  // KN:171
+        const double zc = xadd(xadd(xmul(l0, zw0.x), xmul(l1, zw1.x)), xmul(l2, zw2.x));  // KN:172
+        return tea_filters(p, xc, yc, zc, wc);
+    }
     TriSetup s;
     tri_load_ccw(tri_xy + 6ll * t, s);
     double e0, e1, e2;
@@ -224,8 +284,8 @@ ML_DEV bool tea_texel_eval_inline(const T* __restrict__ tri_xy, const T* __restr
 // bloat the hot loop; the EVAL kernel, which does nothing else, uses the inline version.
 template <typename T>
 __device__ __noinline__ bool tea_texel_eval(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
-                                            int t, int x, int y, const TeaParams& p) {
-    return tea_texel_eval_inline(tri_xy, tri_clip, t, x, y, p);
+                                            const TeaRec* __restrict__ recs, int t, int x, int y, const TeaParams& p) {
+    return tea_texel_eval_inline(tri_xy, tri_clip, recs, t, x, y, p);
 }
 
 // Work list of quads that need the float64 evaluation.  Entry = 3 x u64: (quad index << 4) | keep
@@ -234,6 +294,7 @@ struct TeaWork {
     unsigned long long* entries;     // NULL: evaluate inline in the stream kernel
     unsigned long long* count;       // device counter (zeroed before the stream kernel)
     unsigned long long cap;
+    const TeaRec* recs;              // prepared per-triangle records (may be NULL)
 };
 
 // Footprint culling (optional; needs width % 128 == 0).  tile_cur: tiles this stroke can touch
@@ -306,7 +367,7 @@ ML_DEV void tea_process(const long long (&qs)[U], const uint4 (&ids)[U], long lo
             if (!(keep[u] & (1u << e))) continue;
             int x, y;
             texel_xy((q << 2) + e, width, row0, small, x, y);
-            if (tea_texel_eval(tri_xy, tri_clip, t4[e], x, y, p)) hits |= 1u << e;
+            if (tea_texel_eval(tri_xy, tri_clip, wk.recs, t4[e], x, y, p)) hits |= 1u << e;
         }
         // exactly one thread owns these 4 texels in this kernel: the read-modify-write of
         // KN:198-202 inside quad_write is race-free
@@ -364,7 +425,7 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
         if (!tri_flag(flags, t)) continue;
         int x, y;
         texel_xy(i, width, row0, small, x, y);
-        if (!tea_texel_eval(tri_xy, tri_clip, t, x, y, p)) continue;
+        if (!tea_texel_eval(tri_xy, tri_clip, wk.recs, t, x, y, p)) continue;
         if (edited[i] == 0) ++newly;
         store_value(data, esize, i, value);
         mask[i] = 1;
@@ -374,10 +435,12 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
     block_count_add(frags, counters + 1);
 }
 
-// TILE kernel (footprint culling).  One WARP per 128x8-texel tile, grid-stride over all tiles of
-// the slab: a tile outside both bitmaps costs one cached word; a tile of tile_prev has its edited
-// bytes cleared; a tile of tile_cur streams its 8 row segments (8 independent 128-bit id loads per
-// lane) through tea_process.  The stroke therefore reads O(footprint) texels, not O(atlas).
+// TILE kernel (footprint culling).  One WARP per LISTED 128x8-texel tile: first the tiles of the
+// previous stroke that this stroke does not revisit get their edited bytes cleared (this replaces
+// the whole-plane reset of the EditedAreaMask), then every tile of this stroke's list
+// is cleared if the previous stroke marked it and streams its 8 row segments (8 independent 128-bit
+// id loads per lane) through tea_process.  The stroke therefore reads O(footprint) texels, not
+// O(atlas), and the listed tiles spread evenly over the grid wherever the footprint lies.
 template <typename T, int ES>
 __global__ void __launch_bounds__(BLOCK)
 tea_tile_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
@@ -391,14 +454,15 @@ tea_tile_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, lo
     const long long n = rows * width, nq = n >> 2;
     const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
     const int segs = cull.segs_per_row;
-    const int tile_rows = (int)((rows + U - 1) >> TILE_H_SHIFT);
-    const int ntiles = segs * tile_rows;
-    const int nwarps = gridDim.x * (BLOCK / 32);
-    for (int tile = blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); tile < ntiles; tile += nwarps) {
-        const uint32_t cw = __ldg(cull.tile_cur + (tile >> 5));
-        const uint32_t pw = cull.tile_prev ? __ldg(cull.tile_prev + (tile >> 5)) : 0u;
-        const bool cur = (cw >> (tile & 31)) & 1u, prev = (pw >> (tile & 31)) & 1u;
-        if (!cur && !prev) continue;
+    const long long ntiles = (long long)segs * ((rows + U - 1) >> TILE_H_SHIFT);
+    const TileBuf cur((uint32_t*)cull.tile_cur, ntiles), prev((uint32_t*)cull.tile_prev, ntiles);
+    const long long ncur = (long long)*cur.count, nprev = cull.tile_prev ? (long long)*prev.count : 0;
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    for (long long j = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); j < ncur + nprev; j += nwarps) {
+        const bool is_cur = j < ncur;
+        const int tile = (int)(is_cur ? cur.list[j] : prev.list[j - ncur]);
+        const bool in_prev = cull.tile_prev && tile_bit(prev.bits, tile);
+        if (!is_cur && tile_bit(cur.bits, tile)) continue;           // handled by its entry in this stroke's list
         const int ty = tile / segs, tx = tile - ty * segs;
         long long qs[U];
 #pragma unroll
@@ -406,11 +470,11 @@ tea_tile_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, lo
             const long long yy = ((long long)ty << TILE_H_SHIFT) + u;
             qs[u] = yy < rows ? ((yy * width + ((long long)tx << TILE_W_SHIFT)) >> 2) + lane : nq;
         }
-        if (prev) {
+        if (in_prev || !is_cur) {
 #pragma unroll
             for (int u = 0; u < U; ++u) if (qs[u] < nq) *(uint32_t*)(edited + (qs[u] << 2)) = 0u;
         }
-        if (!cur) continue;
+        if (!is_cur) continue;
         uint4 ids[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) if (qs[u] < nq) ids[u] = ld_stream((const uint4*)tri_id + qs[u]);
@@ -425,10 +489,13 @@ tea_tile_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, lo
 // EVAL kernel.  Four adjacent lanes share one work-list quad, one lane per texel, so the float64
 // evaluation runs with full, evenly spread parallelism no matter how compact the tool footprint is
 // in atlas space.  The 4 hit bits are gathered with a ballot and lane 0 of the group writes.
+#ifndef ML_TEA_EVAL_MINB
+#define ML_TEA_EVAL_MINB 4
+#endif
 template <typename T, int ES>
-__global__ void __launch_bounds__(BLOCK)
-tea_eval_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
-                long long row0, long long n, const int* __restrict__ tri_id, TeaParams p, TeaWork wk,
+__global__ void __launch_bounds__(BLOCK, ML_TEA_EVAL_MINB)
+tea_eval_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, const TeaRec* __restrict__ recs,
+                long long width, long long row0, long long n, const int* __restrict__ tri_id, TeaParams p, TeaWork wk,
                 void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
                 uint8_t* __restrict__ edited, unsigned long long* counters) {
     long long newly = 0;
@@ -450,7 +517,7 @@ tea_eval_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, lo
                 const int t = (int)((e & 1) ? (idw >> 32) : (idw & 0xffffffffull));
                 int x, y;
                 texel_xy((q << 2) + e, width, row0, small, x, y);
-                hit = tea_texel_eval_inline(tri_xy, tri_clip, t, x, y, p);
+                hit = tea_texel_eval_inline(tri_xy, tri_clip, recs, t, x, y, p);
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
@@ -472,7 +539,7 @@ constexpr int TEA_BIG_BLOCK = 1024;                  // block size when the bitm
 constexpr long long TEA_SMEM_MAX_BYTES = 200 * 1024; // bitmap size limit for the shared-memory path
 
 template <typename T, int ES>
-int launch_tea_es(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
+int launch_tea_es(const T* tri_xy, const T* tri_clip, const TeaRec* recs, long long width, long long row0, long long n,
                   const int* tri_id, const uint32_t* bits, long long ntri, const TeaParams& p, TeaWork wk, TeaCull cull,
                   void* data, int esize, uint32_t value, uint8_t* mask, uint8_t* edited,
                   unsigned long long* ctr, cudaStream_t st) {
@@ -482,7 +549,7 @@ int launch_tea_es(const T* tri_xy, const T* tri_clip, long long width, long long
     if (ES > 0 && cull.tile_cur) {
         const long long rows = n / width;
         const long long ntiles = (long long)cull.segs_per_row * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
-        long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);
+        long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);      // the lists are never longer than this
         const long long cap = (long long)ml_sm_count() * 8;
         if (blocks > cap) blocks = cap;
         if (blocks < 1) blocks = 1;
@@ -507,19 +574,19 @@ int launch_tea_es(const T* tri_xy, const T* tri_clip, long long width, long long
             tri_id, bits, nwords, p, wk, data, esize, value, mask, edited, ctr);
     }
     if (ES > 0 && wk.entries)
-        tea_eval_kernel<T, (ES > 0 ? ES : 1)><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, tri_clip, width,
+        tea_eval_kernel<T, (ES > 0 ? ES : 1)><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, tri_clip, recs, width,
             row0, n, tri_id, p, wk, data, value, mask, edited, ctr);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }
 
 template <typename T>
-int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long long row0, long long n,
+int launch_tea_texels(const T* tri_xy, const T* tri_clip, const TeaRec* recs, long long width, long long row0, long long n,
                       const int* tri_id, const uint32_t* bits, long long ntri, const TeaParams& p, void* worklist,
                       size_t worklist_bytes, TeaCull cull, void* data, int esize, uint32_t value, uint8_t* mask,
                       uint8_t* edited, unsigned long long* ctr, cudaStream_t st) {
     const bool vec = ((((uintptr_t)tri_id) | ((uintptr_t)data) | ((uintptr_t)mask) | ((uintptr_t)edited)) & 15) == 0;
-    TeaWork wk{nullptr, nullptr, 0};
+    TeaWork wk{nullptr, nullptr, 0, recs};
     if (vec && worklist && worklist_bytes >= 64 && (((uintptr_t)worklist) & 7) == 0) {
         wk.count = (unsigned long long*)worklist;
         wk.entries = wk.count + 2;
@@ -530,10 +597,10 @@ int launch_tea_texels(const T* tri_xy, const T* tri_clip, long long width, long 
         if (cull.tile_cur) return ml_fail(ML_ERR_ARG, "footprint culling needs width % 128 == 0, aligned planes and triangle flags");
     }
     cull.segs_per_row = (int)(width >> TILE_W_SHIFT);
-    if (!vec) return launch_tea_es<T, 0>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
-    if (esize == 1) return launch_tea_es<T, 1>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
-    if (esize == 2) return launch_tea_es<T, 2>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
-    return launch_tea_es<T, 4>(tri_xy, tri_clip, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
+    if (!vec) return launch_tea_es<T, 0>(tri_xy, tri_clip, recs, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
+    if (esize == 1) return launch_tea_es<T, 1>(tri_xy, tri_clip, recs, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
+    if (esize == 2) return launch_tea_es<T, 2>(tri_xy, tri_clip, recs, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
+    return launch_tea_es<T, 4>(tri_xy, tri_clip, recs, width, row0, n, tri_id, bits, ntri, p, wk, cull, data, esize, value, mask, edited, ctr, st);
 }
 
 }  // namespace
@@ -571,7 +638,7 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
 int ml_tea_tile_words(int64_t width, int64_t rows) {
     if (width <= 0 || rows <= 0 || (width & ((1 << TILE_W_SHIFT) - 1)) != 0) return 0;
     const long long tiles = (width >> TILE_W_SHIFT) * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
-    return (int)((tiles + 31) / 32);
+    return (int)(tile_bitmap_words(tiles) + 2 + tiles);             // bitmap | count | list (TileBuf)
 }
 
 int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_tea_params* tp,
@@ -583,7 +650,8 @@ int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_
     if (tile_bits) {
         const int words = ml_tea_tile_words(width, rows);
         if (words == 0 || tri_xy == nullptr) return ml_fail(ML_ERR_ARG, "tile marking needs tri_xy and width % 128 == 0");
-        ML_CUDA(cudaMemsetAsync(tile_bits, 0, (size_t)words * 4, st));
+        const long long tiles = (width >> TILE_W_SHIFT) * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
+        ML_CUDA(cudaMemsetAsync(tile_bits, 0, (size_t)(tile_bitmap_words(tiles) + 2) * 4, st));   // bitmap + list count
     }
     const unsigned grid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
     if (tri_dtype == ML_F32) tea_classify_kernel<float><<<grid, BLOCK, 0, st>>>((const float*)tri_clip, ntri, p, flags, (const float*)tri_xy, width, height, row0, rows, tile_bits);
@@ -593,7 +661,23 @@ int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_
     return ML_OK;
 }
 
-int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
+size_t ml_tea_rec_bytes(int64_t ntri) { return (size_t)(ntri > 0 ? ntri : 0) * sizeof(TeaRec) + 16; }
+
+int ml_tea_prepare(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri, void* recs,
+                   size_t rec_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ntri <= 0) return ML_OK;
+    if (recs == nullptr || rec_bytes < ml_tea_rec_bytes(ntri) || (((uintptr_t)recs) & 15))
+        return ml_fail(ML_ERR_ARG, "ml_tea_prepare needs ml_tea_rec_bytes(ntri) bytes, 16-byte aligned");
+    const unsigned grid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
+    if (tri_dtype == ML_F32) tea_prepare_kernel<float><<<grid, BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_clip, ntri, (TeaRec*)recs);
+    else if (tri_dtype == ML_F64) tea_prepare_kernel<double><<<grid, BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_clip, ntri, (TeaRec*)recs);
+    else return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_tea_texels(const void* tri_xy, const void* tri_clip, const void* tea_recs, int tri_dtype, int64_t ntri,
                   int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
                   const uint32_t* tri_flags, const ml_tea_params* tp, void* worklist,
                   size_t worklist_bytes, const uint32_t* tile_cur, const uint32_t* tile_prev,
@@ -607,10 +691,10 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
     unsigned long long* ctr = (unsigned long long*)counters;
     TeaCull cull{tile_cur, tile_cur ? tile_prev : nullptr, 0, (unsigned long long)(known_fragments > 0 ? known_fragments : 0)};
     if (tri_dtype == ML_F32)
-        return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, width, row0, n, tri_id, tri_flags, ntri, p,
+        return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, (const TeaRec*)tea_recs, width, row0, n, tri_id, tri_flags, ntri, p,
                                  worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);
     if (tri_dtype == ML_F64)
-        return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, width, row0, n, tri_id, tri_flags, ntri, p,
+        return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, (const TeaRec*)tea_recs, width, row0, n, tri_id, tri_flags, ntri, p,
                                  worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);
     return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
 }

@@ -117,6 +117,7 @@ class StrokeContext:
         self.tri_xy = surface.tri_xy
         self.edited = torch.zeros((surface.rows, surface.width), dtype=torch.uint8, device=device)
         self.scratch = _native.tea_scratch(mesh.num_triangles, surface.rows * surface.width, device)
+        self.recs = _native.tea_prepare(self.tri_xy, self.tri_clip, device)      # per-triangle evaluation records
         # footprint culling state: two tile bitmaps (this stroke / previous stroke) and whether the
         # edited plane may hold marks outside the previous bitmap (then it is reset as a whole)
         nwords = _native.tea_tile_words(surface.width, surface.rows)
@@ -154,7 +155,7 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
             ctx.edited_fully_dirty = False
         _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
                            scratch=ctx.scratch, height=s.height, tiles=(ctx.tiles[0], ctx.tiles[1]),
-                           known_fragments=s.covered)
+                           known_fragments=s.covered, recs=ctx.recs)
         ctx.tiles.reverse()                                   # this stroke's footprint is the next one's "previous"
         ctx.stroke_tiles = ctx.tiles[1]                       # footprint of the marks now in ctx.edited (for TPA)
     elif s.overlap == 0 and not force_direct:
@@ -162,7 +163,7 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
         ctx.edited_fully_dirty = True
         ctx.stroke_tiles = None
         _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
-                           scratch=ctx.scratch)
+                           scratch=ctx.scratch, recs=ctx.recs)
     else:
         ctx.edited.zero_()
         ctx.edited_fully_dirty = True
