@@ -19,7 +19,10 @@ namespace {
 
 constexpr int BLOCK = 256;
 constexpr int UNROLL = 4;
-constexpr int TU = 4;          // measured: 8 lowers occupancy (116 regs) and is slower
+#ifndef ML_THR_TU
+#define ML_THR_TU 4
+#endif
+constexpr int TU = ML_THR_TU;  // quads in flight per thread of the threshold kernel
 
 ML_DEV void hit_write(void* data, int esize, uint32_t value, uint8_t* mask, uint8_t* edited,
                       long long i, long long& cnt) {
