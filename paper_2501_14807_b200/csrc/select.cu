@@ -289,32 +289,36 @@ tile_box_kernel(const float* __restrict__ px, const float* __restrict__ py, cons
     }
 }
 
-// tile list in device scratch: [0] = count (u64), then u32 tile indices
-struct TileList { unsigned long long* count; uint32_t* tiles; };
+// tile list in device scratch: [count u64][pad u64][bitmap ntiles/32 u32, rounded to 8 B][u32 tile indices]
+struct TileList { unsigned long long* count; uint32_t* bits; uint32_t* tiles; };
+inline long long tile_bitmap_words(long long ntiles) { return ((ntiles + 63) / 64) * 2; }
 
-// one thread per tile; K == 1 for the single-stroke brush
+// One thread per (tile, chunk of KC strokes): blockIdx.y selects the chunk, so a batch of many
+// strokes still fills the machine.  A tile is appended to the list by the first chunk that finds a
+// stroke reaching it (atomicOr on the tile bitmap decides who appends).  K == 1 / strokes == NULL is
+// the single-stroke brush.
+constexpr int KC = 32;
 __global__ void __launch_bounds__(BLOCK)
 tile_classify_kernel(const float4* __restrict__ boxes, long long ntiles, const double* __restrict__ strokes,
                      long long K, double cx, double cy, double cz, double cr, TileList list) {
     const long long tile = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    if (tile >= ntiles) return;
+    const uint32_t bit = 1u << (tile & 31);
+    if (gridDim.y > 1 && (ld_volatile_u32(list.bits + (tile >> 5)) & bit)) return;      // another chunk already kept it
+    const float4 lo = __ldg(boxes + 2 * tile), hi = __ldg(boxes + 2 * tile + 1);
+    if (!(lo.x <= hi.x)) return;                                                        // no covered texel
     bool keep = false;
-    if (tile < ntiles) {
-        const float4 lo = __ldg(boxes + 2 * tile), hi = __ldg(boxes + 2 * tile + 1);
-        if (lo.x <= hi.x) {
-            if (strokes == nullptr) keep = box_may_hit(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, cx, cy, cz, cr);
-            else
-                for (long long k = 0; k < K && !keep; ++k)
-                    keep = box_may_hit(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, __ldg(strokes + 4 * k), __ldg(strokes + 4 * k + 1),
-                                       __ldg(strokes + 4 * k + 2), __ldg(strokes + 4 * k + 3));
+    if (strokes == nullptr) keep = box_may_hit(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, cx, cy, cz, cr);
+    else {
+        for (long long k0 = (long long)blockIdx.y * KC; k0 < K && !keep; k0 += (long long)gridDim.y * KC) {
+            const long long k1 = k0 + KC < K ? k0 + KC : K;
+            for (long long k = k0; k < k1 && !keep; ++k)
+                keep = box_may_hit(lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, __ldg(strokes + 4 * k), __ldg(strokes + 4 * k + 1),
+                                   __ldg(strokes + 4 * k + 2), __ldg(strokes + 4 * k + 3));
         }
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (bal == 0) return;
-    const int lane = threadIdx.x & 31;
-    unsigned long long slot = 0;
-    if (lane == 0) slot = atomicAdd(list.count, (unsigned long long)__popc(bal));
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    if (keep) list.tiles[slot + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)tile;
+    if (keep && !(atomicOr(list.bits + (tile >> 5), bit) & bit))
+        list.tiles[atomicAdd(list.count, 1ull)] = (uint32_t)tile;
 }
 
 template <int ES>
@@ -527,7 +531,8 @@ int64_t ml_tile_count(int64_t width, int64_t rows) {
 }
 
 size_t ml_tile_workspace_bytes(int64_t width, int64_t rows) {
-    return 16 + (size_t)ml_tile_count(width, rows) * sizeof(uint32_t);
+    const long long nt = ml_tile_count(width, rows);
+    return 16 + (size_t)(tile_bitmap_words(nt) + nt) * sizeof(uint32_t);
 }
 
 int ml_surface_tile_boxes(const float* pos, int64_t pos_stride, int64_t width, int64_t rows,
@@ -554,10 +559,13 @@ static int tiles_prepare(int64_t width, int64_t rows, const float* boxes, void* 
         return ml_fail(ML_ERR_ARG, "culled brushes need ml_tile_workspace_bytes() of 8-byte aligned scratch");
     g = tile_grid(width, rows);
     list.count = (unsigned long long*)workspace;
-    list.tiles = (uint32_t*)(list.count + 2);
-    ML_CUDA(cudaMemsetAsync(list.count, 0, 8, st));
-    tile_classify_kernel<<<(unsigned)((g.ntiles + BLOCK - 1) / BLOCK), BLOCK, 0, st>>>((const float4*)boxes, g.ntiles, strokes, K,
-                                                                                       cx, cy, cz, cr, list);
+    list.bits = (uint32_t*)(list.count + 2);
+    list.tiles = list.bits + tile_bitmap_words(g.ntiles);
+    ML_CUDA(cudaMemsetAsync(workspace, 0, 16 + (size_t)tile_bitmap_words(g.ntiles) * 4, st));      // count + bitmap
+    long long chunks = strokes ? (K + KC - 1) / KC : 1;
+    if (chunks > 1024) chunks = 1024;                                 // the kernel strides over the rest
+    const dim3 grid((unsigned)((g.ntiles + BLOCK - 1) / BLOCK), (unsigned)chunks);
+    tile_classify_kernel<<<grid, BLOCK, 0, st>>>((const float4*)boxes, g.ntiles, strokes, K, cx, cy, cz, cr, list);
     return ML_OK;
 }
 
