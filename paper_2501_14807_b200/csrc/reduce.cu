@@ -190,14 +190,53 @@ ML_DEV void atomic_max_double(double* p, double v) {
     }
 }
 
-template <typename T>
+// 16 texels per thread and step: one 128-bit mask load + sizeof(T) 128-bit attribute loads, two steps
+// in flight; VEC = false (unaligned planes) and the tail take the scalar loop.  The float64 sum is
+// accumulated per thread, then warp shuffle -> one atomic per block (order-free within 1e-10, the
+// oracle comparison tolerance; count / min / max are exact).
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(BLOCK)
 stats_kernel(const T* __restrict__ attr, const uint8_t* __restrict__ mask, long long n, double* out) {
     __shared__ double s_mn[BLOCK / 32], s_mx[BLOCK / 32];
     double sum = 0.0, mn = INFINITY, mx = -INFINITY;
     long long cnt = 0;
+    const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
-    for (long long i = (long long)blockIdx.x * BLOCK + threadIdx.x; i < n; i += nthreads) {
+    long long done = 0;
+    if (VEC) {
+        constexpr int W = (int)sizeof(T);                    // 128-bit words per 16 attributes
+        struct __align__(16) Vec { T v[16]; };
+        const long long nv = n >> 4;
+        for (long long v0 = tid; v0 < nv; v0 += 2 * nthreads) {
+            uint4 m[2];
+            Vec a[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const long long v = v0 + u * nthreads;
+                m[u] = make_uint4(0, 0, 0, 0);
+                if (v < nv) {
+                    m[u] = ld_stream((const uint4*)mask + v);
+#pragma unroll
+                    for (int k = 0; k < W; ++k) ((uint4*)&a[u])[k] = ld_stream((const uint4*)attr + v * W + k);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t mw[4] = {m[u].x, m[u].y, m[u].z, m[u].w};
+                if ((mw[0] | mw[1] | mw[2] | mw[3]) == 0) continue;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    if (((mw[e >> 2] >> (8 * (e & 3))) & 0xffu) == 0) continue;
+                    const double x = widen(a[u].v[e]);
+                    sum = xadd(sum, x); ++cnt;
+                    if (x < mn) mn = x;
+                    if (x > mx) mx = x;
+                }
+            }
+        }
+        done = nv << 4;
+    }
+    for (long long i = done + tid; i < n; i += nthreads) {
         if (mask[i] == 0) continue;
         const double v = widen(attr[i]);
         sum = xadd(sum, v); ++cnt;
@@ -224,10 +263,13 @@ stats_kernel(const T* __restrict__ attr, const uint8_t* __restrict__ mask, long 
 
 template <typename T>
 int launch_stats(const void* attr, const uint8_t* mask, long long n, double* out, cudaStream_t st) {
-    long long blocks = (n + BLOCK - 1) / BLOCK;
+    const bool vec = ((((uintptr_t)attr) | ((uintptr_t)mask)) & 15) == 0;
+    long long blocks = ((vec ? (n + 31) / 32 : n) + BLOCK - 1) / BLOCK;
     const long long cap = (long long)ml_sm_count() * 8;
     if (blocks > cap) blocks = cap;
-    stats_kernel<T><<<(unsigned)blocks, BLOCK, 0, st>>>((const T*)attr, mask, n, out);
+    if (blocks < 1) blocks = 1;
+    if (vec) stats_kernel<T, true><<<(unsigned)blocks, BLOCK, 0, st>>>((const T*)attr, mask, n, out);
+    else stats_kernel<T, false><<<(unsigned)blocks, BLOCK, 0, st>>>((const T*)attr, mask, n, out);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

@@ -361,6 +361,27 @@ def test_label_area_and_stats(sphere_map):
         assert (gc, gmn, gmx) == (wc, wmn, wmx) and abs(gs - ws) <= 1e-9 * max(1.0, abs(ws))
 
 
+@pytest.mark.parametrize("akind", [np.uint8, np.int8, np.int16, np.int32, np.uint32, np.float16, np.float32])
+def test_layer_stats_all_kinds_ragged_and_unaligned(akind):
+    """Vector path (16 texels per step), its scalar tail (n % 16 != 0), planes at odd offsets, an
+    empty mask (count 0, min = +inf, max = -inf like the oracle) and a single valid texel."""
+    import torch
+    rng = np.random.default_rng(15)
+    for n, off in ((16 * 37 + 5, 0), (4099, 3), (7, 0)):
+        raw = (rng.normal(size=n + off) * 40).astype(akind)
+        rmask = (rng.random(n + off) < 0.6).astype(np.uint8)
+        attr, mask = raw[off:], rmask[off:]
+        d_attr, d_mask = _dev(raw)[off:], _dev(rmask)[off:]
+        for m_np, m_dev in ((mask, d_mask), (np.zeros_like(mask), torch.zeros_like(d_mask))):
+            want = kn.layer_stats(np.ascontiguousarray(attr), np.ascontiguousarray(m_np))
+            gc, gs, gmn, gmx = nat.layer_stats(d_attr, m_dev)
+            assert (gc, gmn, gmx) == (want[0], want[2], want[3])
+            assert abs(gs - want[1]) <= 1e-9 * max(1.0, abs(want[1]))
+    one = np.zeros(64, np.uint8); one[37] = 1
+    a = np.arange(64).astype(akind)
+    assert nat.layer_stats(_dev(a), _dev(one))[0::2] == (1, 37.0) and nat.layer_stats(_dev(a), _dev(one))[3] == 37.0
+
+
 def test_outline_and_padding_known_answers():
     """10x10 island in 64x64, thickness 1 -> 44 outline texels."""
     import torch
