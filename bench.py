@@ -293,11 +293,19 @@ def run_ours(args):
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     nat.require_cuda()
+    # ML_BENCH_BACKEND=gloo is a TEST hook: it lets several ranks share one GPU (NCCL refuses that) so
+    # the multi-rank code path can be exercised on a single-GPU box; the measured runs use NCCL
+    backend = os.environ.get("ML_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world_size > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     stages = [s for s in args.stages.split(",") if s]
     wl = Workload(args, world_size)
     A, W, L = wl.A, wl.width, wl.L

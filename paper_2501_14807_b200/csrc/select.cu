@@ -387,8 +387,11 @@ template <> struct AttrT<ML_F16> { typedef uint16_t T; static ML_DEV bool hit(T 
 template <> struct AttrT<ML_FLOAT32> { typedef float T; static ML_DEV bool hit(T v, const Thr& t) { return v >= t.lo_f && v <= t.hi_f; } static ML_DEV double get(T v) { return (double)v; } };
 
 // 4 texels per step: one (4*sizeof(T))-byte attribute load + one 4-byte valid load.
+#ifndef ML_THR_MINB
+#define ML_THR_MINB 4
+#endif
 template <int KIND, int ES>
-__global__ void __launch_bounds__(BLOCK, 4)
+__global__ void __launch_bounds__(BLOCK, ML_THR_MINB)
 threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ valid, long long n,
                  double lo, double hi, Thr thr, void* __restrict__ data, int esize, uint32_t value,
                  uint8_t* __restrict__ mask, uint8_t* __restrict__ edited, unsigned long long* counter) {

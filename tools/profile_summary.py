@@ -13,9 +13,10 @@ import json
 import subprocess
 import sys
 
-STAGE_OF = (("chain_kernel", "chain"), ("binary_kernel", "mask_op"), ("sphere_batch_kernel", "batch"),
-            ("sphere_kernel", "sphere"), ("threshold_kernel", "threshold"), ("area_kernel", "area"),
-            ("tea_eval_kernel", "tea"))
+STAGE_OF = (("chain_kernel", "chain"), ("binary_kernel", "mask_op"), ("sphere_batch_tiles_kernel", "batch"),
+            ("sphere_batch_kernel", "batch_stream"), ("sphere_tiles_kernel", "sphere"), ("sphere_kernel", "sphere_stream"),
+            ("threshold_kernel", "threshold"), ("area_kernel", "area"), ("tea_eval_kernel", "tea"),
+            ("padding_tile_kernel", "tpa"), ("padding_stream_kernel", "tpa_stream"), ("tea_stream_kernel", "tea_stream"))
 
 METRICS = [
     ("gpu__time_duration.sum", "time"),
@@ -66,7 +67,10 @@ def launches(src, dst):
 
 
 def full(src, dst, traffic_dst=None):
-    txt = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if src.endswith(".csv"):        # already exported on the GPU box: ncu -i x.ncu-rep --page raw --csv > x.csv
+        txt = open(src).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     hdr, units, data = rows[0], rows[1], rows[2:]
     kn = hdr.index("Kernel Name")
