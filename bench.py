@@ -277,7 +277,9 @@ def workload_config(args, wl, stages):
                         % (wl.A, wl.width, wl.L, wl.mesh.num_triangles, "+".join(stages)),
             "atlas": [wl.height, wl.width], "layers": wl.L, "triangles": wl.mesh.num_triangles,
             "window": [wl.cam.height, wl.cam.width], "stages": list(stages),
-            "l2": "every input plane (>= 268 MB) is larger than the 126 MB L2; no flush between iterations",
+            "l2": "no explicit flush: every streamed input plane (>= 268 MB) is larger than the 126 MB L2, and the "
+                  "streaming stages (chain, mask_op, threshold, area: >= 0.8 GB each, 10 GB together) run between the "
+                  "footprint-culled brush stages of consecutive iterations, which therefore start from a cold L2",
             "parallelism": "row-sharded x%d" % args.gpus}
 
 

@@ -636,8 +636,8 @@ class StrokeBatch:
         # stage through pinned host memory (one buffer per record array, grown on demand) so the
         # host->device copies are asynchronous DMA transfers
         cap = getattr(self, "_cap", 0)
-        if K > cap:
-            self._cap = max(K, 2 * cap)
+        if K > cap or cap == 0:                                  # (an empty first batch still needs buffers)
+            self._cap = max(K, 2 * cap, 1)
             self._pin = (torch.empty((self._cap, 4), dtype=torch.float64).pin_memory(),
                          torch.empty(self._cap, dtype=torch.int32).pin_memory(),
                          torch.empty(self._cap, dtype=torch.int32).pin_memory())

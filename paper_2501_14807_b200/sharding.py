@@ -117,17 +117,22 @@ def exchange_halo(plane, row0, height, radius):
     up_n = min(radius, row0)                                   # rows needed from rank-1 (above = lower rows)
     dn_n = min(radius, height - (row0 + rows))
     # all four transfers go into ONE batch (ncclGroupStart/End under NCCL): posting them one by one
-    # would deadlock, every rank's first operation being a receive
+    # would deadlock, every rank's first operation being a receive.  NCCL moves device rows directly;
+    # any other backend (gloo: CPU tests, single-GPU rehearsal of the multi-rank path) gets the few
+    # halo rows staged through host memory, because its point-to-point ops take host tensors only.
+    xdev = plane.device if (dist.get_backend() == "nccl" or not plane.is_cuda) else torch.device("cpu")
     ops, up, dn = [], None, None
     if rank > 0:
-        up = torch.empty((up_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=plane.device)
+        up = torch.empty((up_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=xdev)
         ops.append(dist.P2POp(dist.irecv, up, rank - 1))
-        ops.append(dist.P2POp(dist.isend, plane[:min(radius, rows)].contiguous(), rank - 1))
+        ops.append(dist.P2POp(dist.isend, plane[:min(radius, rows)].contiguous().to(xdev), rank - 1))
     if rank < ws - 1:
-        dn = torch.empty((dn_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=plane.device)
+        dn = torch.empty((dn_n,) + tuple(plane.shape[1:]), dtype=plane.dtype, device=xdev)
         ops.append(dist.P2POp(dist.irecv, dn, rank + 1))
-        ops.append(dist.P2POp(dist.isend, plane[max(0, rows - radius):].contiguous(), rank + 1))
+        ops.append(dist.P2POp(dist.isend, plane[max(0, rows - radius):].contiguous().to(xdev), rank + 1))
     for r in dist.batch_isend_irecv(ops):
         r.wait()
+    up = up.to(plane.device) if up is not None else None
+    dn = dn.to(plane.device) if dn is not None else None
     parts = [p for p in (up, plane, dn) if p is not None]
     return torch.cat(parts, dim=0), row0 - (up.shape[0] if up is not None else 0)

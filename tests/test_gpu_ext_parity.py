@@ -200,6 +200,35 @@ def test_select_sphere_culled_bit_exact(sphere_map, kind, value):
             assert np.array_equal(m.cpu().numpy(), rm) and np.array_equal(e.cpu().numpy(), re)
 
 
+def test_select_sphere_degenerate_strokes(sphere_map):
+    """NaN / infinite / negative radii and a NaN centre: streamed and culled kernels agree with the
+    oracle (NaN never hits, an infinite radius hits every covered texel, r enters only as r*r)."""
+    _, ref, got = sphere_map
+    tiles = nat.tile_boxes(got["pos"])
+    covered = int((ref["tri_id"] >= 0).sum())
+    for center, radius in (((0.0, 0.0, 1.0), float("nan")), ((0.0, 0.0, 1.0), float("inf")), ((0.0, 0.0, 1.0), -0.3),
+                           ((float("nan"), 0.0, 1.0), 0.5), ((0.0, 0.0, 1.0), 0.0)):
+        rd = np.zeros((256, 256), np.uint8); rm = np.zeros((256, 256), bool); re = np.zeros((256, 256), np.uint8)
+        want = kn.select_sphere(ref["pos"], center, radius, rd, rm, re, 5)
+        for tl in (None, tiles):
+            d, m, e = _dev(np.zeros((256, 256), np.uint8)), _dev(np.zeros((256, 256), bool)), _dev(np.zeros((256, 256), np.uint8))
+            assert nat.select_sphere(got["pos"], center, radius, d, m, e, 5, tiles=tl) == want
+            assert np.array_equal(d.cpu().numpy(), rd) and np.array_equal(m.cpu().numpy(), rm)
+        if radius == float("inf"):
+            assert want == covered
+        if radius != radius or center[0] != center[0]:
+            assert want == 0
+    # an empty batch is a no-op
+    import torch
+    gd = [torch.zeros((256, 256), dtype=torch.uint8, device="cuda")]
+    gm = [torch.zeros((256, 256), dtype=torch.bool, device="cuda")]
+    ge = [torch.zeros((256, 256), dtype=torch.uint8, device="cuda")]
+    batch = nat.StrokeBatch(gd, gm, ge, "cuda").upload(np.zeros((0, 4)), np.zeros(0, np.int64), np.zeros(0, np.uint8))
+    nat.select_sphere_batch(got["pos"], batch, tiles=tiles)
+    nat.select_sphere_batch(got["pos"], batch)
+    assert int(batch.counts.sum()) == 0 and not bool(gm[0].any())
+
+
 @pytest.mark.parametrize("nlayers,K", [(1, 40), (5, 64), (70, 150)])
 def test_select_sphere_batch_culled_equals_sequential(sphere_map, nlayers, K):
     import torch
