@@ -97,9 +97,13 @@ struct TeaFn {
     const T* tri_clip; TeaParams p;
     void* data; uint8_t* mask; uint8_t* edited;
     long long width, row0; uint32_t value; int esize;
-    struct Tri { double c0[4], c1[4], c2[4]; };
+    const uint32_t* flags;            // ml_tea_classify bitmap of this stroke (NULL: evaluate everything)
+    struct Tri { double c0[4], c1[4], c2[4]; bool keep; };
     ML_DEV Tri setup(long long t, const TriSetup& s) const {
         Tri r;
+        // a triangle the classification pass proved unreachable only counts its fragments (KN:158-161)
+        r.keep = flags ? ((flags[t >> 5] >> (t & 31)) & 1u) != 0 : true;
+        if (!r.keep) return r;
         const T* c = tri_clip + 12 * t;
         const int i1 = s.swapped ? 8 : 4, i2 = s.swapped ? 4 : 8;        // KN:40 swap attrs too
 #pragma unroll
@@ -111,7 +115,7 @@ struct TeaFn {
     ML_DEV void fragment(const Tri& a, long long, int x, int y, double e0, double e1, double e2,
                          long long& c0, long long& c1) const {
         ++c1;                                                            // fragments, KN:158-161
-        if (!tea_fragment(p, e0, e1, e2, a.c0, a.c1, a.c2)) return;
+        if (!a.keep || !tea_fragment(p, e0, e1, e2, a.c0, a.c1, a.c2)) return;
         const long long i = (y - row0) * width + x;
         if (byte_set1_was0(edited, i)) ++c0;                             // KN:198-199, 202
         store_value(data, esize, i, value);                              // KN:200
@@ -245,7 +249,7 @@ extern "C" {
 size_t ml_raster_workspace_bytes(int64_t ntri) {
     if (ntri < 0) ntri = 0;
     return 4 * sizeof(unsigned long long) + (size_t)(ntri + 1) * sizeof(unsigned long long) +
-           (size_t)ntri * sizeof(int) + 64;
+           (size_t)ntri * sizeof(int) + (size_t)((ntri + 31) / 32) * sizeof(uint32_t) + 64;   // + TEA triangle flags
 }
 
 int ml_coverage_fill(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
@@ -300,12 +304,22 @@ int ml_raster_tea(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
     if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
     TeaParams p = ml_make_tea_params(tp);
     unsigned long long* ctr = (unsigned long long*)counters;
+    // per-stroke triangle classification (surface.cu): triangles that provably cannot pass the
+    // w > 0 / window / tool-range filters skip the float64 evaluation; their fragments are still
+    // rasterised and counted, so planes and both counts are unchanged
+    uint32_t* flags = nullptr;
+    if (ntri > 0 && workspace && workspace_bytes >= ml_raster_workspace_bytes(ntri) && (tri_dtype == ML_F32 || tri_dtype == ML_F64)) {
+        flags = (uint32_t*)((char*)workspace + 4 * sizeof(unsigned long long) + (size_t)(ntri + 1) * sizeof(unsigned long long) +
+                            (size_t)ntri * sizeof(int));
+        const int rc = ml_tea_classify(tri_clip, tri_dtype, ntri, tp, flags, nullptr, width, height, row0, rows, nullptr, stream);
+        if (rc != ML_OK) return rc;
+    }
     if (tri_dtype == ML_F32) {
-        TeaFn<float> f{(const float*)tri_clip, p, data, mask, edited, width, row0, value_bits, esize};
+        TeaFn<float> f{(const float*)tri_clip, p, data, mask, edited, width, row0, value_bits, esize, flags};
         return raster_launch((const float*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
     }
     if (tri_dtype == ML_F64) {
-        TeaFn<double> f{(const double*)tri_clip, p, data, mask, edited, width, row0, value_bits, esize};
+        TeaFn<double> f{(const double*)tri_clip, p, data, mask, edited, width, row0, value_bits, esize, flags};
         return raster_launch((const double*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
     }
     return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
