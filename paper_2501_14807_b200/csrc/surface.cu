@@ -504,25 +504,43 @@ tea_eval_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, co
     const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
     const int lane = threadIdx.x & 31, e = lane & 3;
     const long long nthreads = (long long)gridDim.x * BLOCK;
+    const long long step = nthreads >> 2;                 // entries between two iterations of a thread
+    // Two-deep software pipeline over the work list: while entry i is evaluated, entry i+1 is already
+    // in registers (its triangle record is being prefetched into L1) and the loads of entry i+2 are
+    // in flight, so neither the list read nor the record gather sits on the dependent-load chain.
+    struct Entry { unsigned long long w, idw; };
+    auto load_entry = [&](long long ent) {
+        Entry r{0ull, 0ull};
+        if (ent < count) { r.w = wk.entries[3 * ent]; r.idw = wk.entries[3 * ent + 1 + (e >> 1)]; }
+        return r;
+    };
+    auto owner = [&](const Entry& en) { return (int)((e & 1) ? (en.idw >> 32) : (en.idw & 0xffffffffull)); };
+    auto prefetch_rec = [&](const Entry& en) {
+        if (recs && (en.w & (1ull << e))) {
+            const char* a = (const char*)(recs + owner(en));
+            asm volatile("prefetch.global.L1 [%0];" :: "l"(a));
+            asm volatile("prefetch.global.L1 [%0];" :: "l"(a + 128));
+        }
+    };
+    long long ent = ((long long)blockIdx.x * BLOCK + threadIdx.x) >> 2;
+    Entry cur = load_entry(ent), nxt = load_entry(ent + step);
+    prefetch_rec(cur);
     // block-uniform trip count: every lane reaches the ballot
-    for (long long base = (long long)blockIdx.x * BLOCK; base < count * 4; base += nthreads) {
-        const long long idx = base + threadIdx.x, ent = idx >> 2;
+    for (long long base = (long long)blockIdx.x * BLOCK; base < count * 4; base += nthreads, ent += step) {
+        const Entry nn = load_entry(ent + 2 * step);
+        prefetch_rec(nxt);
         bool hit = false;
-        long long q = 0;
-        if (ent < count) {
-            const unsigned long long w = wk.entries[3 * ent];
-            q = (long long)(w >> 4);
-            if (w & (1ull << e)) {
-                const unsigned long long idw = wk.entries[3 * ent + 1 + (e >> 1)];
-                const int t = (int)((e & 1) ? (idw >> 32) : (idw & 0xffffffffull));
-                int x, y;
-                texel_xy((q << 2) + e, width, row0, small, x, y);
-                hit = tea_texel_eval_inline(tri_xy, tri_clip, recs, t, x, y, p);
-            }
+        const long long q = (long long)(cur.w >> 4);
+        if (cur.w & (1ull << e)) {
+            int x, y;
+            texel_xy((q << 2) + e, width, row0, small, x, y);
+            hit = tea_texel_eval_inline(tri_xy, tri_clip, recs, owner(cur), x, y, p);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
         const unsigned hits = (bal >> (lane & ~3)) & 0xfu;
         if (e == 0 && hits) quad_write<ES>(data, value, mask, edited, q << 2, hits, newly);
+        cur = nxt;
+        nxt = nn;
     }
     block_count_add(newly, counters);
 }
