@@ -457,3 +457,40 @@ def test_outline_and_padding_random(seed, r):
         i0, i1 = max(0, r0 - r), min(h, r1 + r)
         parts.append(nat.outline_mask(_dev(cov[i0:i1]), r, in_row0=i0, out_row0=r0, out_rows=r1 - r0).cpu().numpy())
     assert np.array_equal(np.concatenate(parts), ref_out)
+
+
+def test_c_abi_argument_validation():
+    """Return codes of the C ABI for arguments the kernels cannot take (ML_ERR_ARG = 1 with a message
+    in ml_last_error); nothing is launched and no plane is touched."""
+    import ctypes as C
+    import torch
+    L = nat.lib()
+    z = torch.zeros((8, 200), dtype=torch.uint8, device="cuda")
+    pos = torch.zeros((3, 8, 200), dtype=torch.float32, device="cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())
+    none = C.c_void_p(0)
+    # culled brushes need width % 128 == 0, the boxes and the scratch
+    assert L.ml_tile_count(200, 8) == 0 and L.ml_tile_count(256, 9) == 2 * 3
+    assert L.ml_tile_workspace_bytes(200, 8) == 16
+    assert L.ml_surface_tile_boxes(p(pos), 1600, 200, 8, p(z), none) == 1
+    assert b"128" in L.ml_last_error()
+    assert L.ml_select_sphere_tiles(p(pos), 1600, 200, 8, none, none, 0, 0.0, 0.0, 0.0, 1.0, p(z), 1, 1, p(z), p(z), none, none) == 1
+    pos2 = torch.zeros((3, 8, 256), dtype=torch.float32, device="cuda")
+    z2 = torch.zeros((8, 256), dtype=torch.uint8, device="cuda")
+    assert L.ml_select_sphere_tiles(p(pos2), 2048, 256, 8, none, none, 0, 0.0, 0.0, 0.0, 1.0, p(z2), 1, 1, p(z2), p(z2), none, none) == 1
+    assert b"boxes" in L.ml_last_error()
+    boxes = torch.zeros((4, 8), dtype=torch.float32, device="cuda")
+    assert L.ml_select_sphere_tiles(p(pos2), 2048, 256, 8, p(boxes), none, 0, 0.0, 0.0, 0.0, 1.0, p(z2), 1, 1, p(z2), p(z2), none, none) == 1
+    assert b"scratch" in L.ml_last_error()
+    # element size / record buffers / padding tiles
+    assert L.ml_select_sphere(p(pos), 1600, 1600, 0.0, 0.0, 0.0, 1.0, p(z), 3, 1, p(z), p(z), none, none) == 1
+    assert L.ml_tea_prepare(p(pos), p(pos), 7, 10, p(z), 10 ** 6, none) == 1                 # buffer too small comes first
+    big = torch.zeros(int(L.ml_tea_rec_bytes(10)), dtype=torch.uint8, device="cuda")
+    assert L.ml_tea_prepare(p(pos), p(pos), 7, 10, p(big), big.numel(), none) == 1           # unknown dtype code
+    assert L.ml_tea_prepare(p(pos), p(pos), 7, 0, none, 0, none) == 0                        # no triangles: no-op
+    assert L.ml_apply_padding_tiles(p(z), p(z), 200, 8, 1, none, p(z), 1, 1, p(z), none, none) == 1
+    assert L.ml_apply_padding_tiles(p(z2), p(z2), 256, 8, 9, p(z2), p(z2), 1, 1, p(z2), none, none) == 1   # radius > 4
+    assert L.ml_apply_padding_tiles(p(z2), p(z2), 256, 8, 0, none, p(z2), 1, 1, p(z2), none, none) == 0    # radius 0: no-op (SPEC.md:303)
+    assert L.ml_surface_resolve(none, none, none, 1, 4, 256, 0, 8, none, none, none, none, none, none, 0, none) == 1
+    torch.cuda.synchronize()
+    assert not bool(z.any()) and not bool(z2.any())
