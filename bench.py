@@ -353,11 +353,16 @@ def run_ours(args):
             r = ml.apply_stroke(ctx, tool, layers[0], eps=wl.eps, cull=cull)
             out = [r._counts]
         elif st == "tpa":
-            # padding of the stroke just applied (the paper times TEA + TPA per edit);
-            # a slab's stencil would need the neighbours' edited rows: radius-1 halo, local rows here
+            # padding of the stroke just applied (the paper times TEA + TPA per edit); with
+            # several ranks the 1-row halo of the edited plane travels point-to-point first
             counts1.zero_()
-            nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1,
-                              tiles=ctx.stroke_tiles if cull else None)
+            if world_size > 1:
+                ext, ext_row0 = sharding.exchange_halo(ctx.edited, row0, wl.height, 1)
+                nat.apply_padding(outline, ext, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1,
+                                  in_row0=ext_row0, out_row0=row0)
+            else:
+                nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1,
+                                  tiles=ctx.stroke_tiles if cull else None)
             out = [counts1.clone()]
         elif st == "sphere":
             s = inp["sphere"]

@@ -172,19 +172,35 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
     return EditResult(edited_mask=ctx.edited, _counts=counts)
 
 
-def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True):
+def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, halo=None):
     """The service's ``stroke`` (the edit the paper times): TEA
     (``apply_stroke``) followed by TPA (``apply_padding``) with the tool's padding radius.
     ``outline`` is the layer-resolution outline mask (``build_outline_mask``).  The padded count
     stays on the device like the other counters (``EditResult.padded_count``).  With ``cull`` both
-    passes touch only the stroke's footprint tiles."""
+    passes touch only the stroke's footprint tiles.
+
+    Row-sharded atlases (the context's surface map is a slab of a taller atlas): the padding stencil
+    needs the neighbours' ``edited`` rows at the slab borders, so every rank calls ``stroke`` for
+    every stroke and the ``radius`` border rows are exchanged point-to-point
+    (``sharding.exchange_halo``; ``halo`` replaces that exchange, e.g. in single-process tests).  The
+    padding pass then streams the slab's outline plane instead of walking footprint tiles."""
     torch = _native._torch()
     res = apply_stroke(ctx, tool, layer, eps=eps, cull=cull)
-    if tool.padding_radius > 0:
+    radius = tool.padding_radius
+    if radius > 0:
+        s = ctx.surface
         pc = torch.zeros(1, dtype=torch.int64, device=ctx.device)
         as_u8 = outline.view(torch.uint8) if outline.dtype == torch.bool else outline
-        _native.apply_padding(as_u8, ctx.edited, tool.padding_radius, layer.data, layer.mask, tool.value, counts=pc,
-                              tiles=ctx.stroke_tiles if cull else None)
+        ext, ext_row0 = ctx.edited, s.row0
+        if s.rows != s.height:
+            from . import sharding
+            ext, ext_row0 = (halo or sharding.exchange_halo)(ctx.edited, s.row0, s.height, radius)
+        if ext is ctx.edited:
+            _native.apply_padding(as_u8, ctx.edited, radius, layer.data, layer.mask, tool.value, counts=pc,
+                                  tiles=ctx.stroke_tiles if cull else None)
+        else:
+            _native.apply_padding(as_u8, ext, radius, layer.data, layer.mask, tool.value, counts=pc,
+                                  in_row0=ext_row0, out_row0=s.row0)
         res._padded = pc
     return res
 

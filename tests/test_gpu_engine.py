@@ -215,6 +215,73 @@ def test_culled_stroke_sequence_with_padding_equals_oracle(kind, radius):
     assert total_padded > 0
 
 
+def test_row_sharded_strokes_equal_full_plane_oracle():
+    """The multi-GPU stroke path on one GPU: three row slabs (heights 100 / 28 / 128, the middle one
+    not a multiple of the 8-row tiles) each run the culled TEA + TPA of every stroke, the padding
+    halo rows come from the neighbour slabs' edited planes (what sharding.exchange_halo moves);
+    stacked slab planes and summed counts == the full-plane oracle after every stroke."""
+    import torch
+    rng = np.random.default_rng(61)
+    mesh = synth.icosphere_mesh(3)
+    A, W, radius = 256, 160, 2
+    cam = synth.default_camera(W, W)
+    depth = ml.render_depth(mesh, cam)
+    slabs = [(0, 100), (100, 28), (128, 128)]
+    full = ml.build_surface_map(mesh, A, A)
+    cov = full.coverage.to(torch.uint8)
+    ref_outline = kn.outline(cov.cpu().numpy(), radius)
+    pool = ml.TexturePool()
+    ctxs, layers, outlines = [], [], []
+    for r0, rows in slabs:
+        surf = ml.build_surface_map(mesh, A, A, row0=r0, rows=rows)
+        ctxs.append(ml.StrokeContext(mesh, cam, depth, surf))
+        layers.append(ml.create_layer("s%d" % r0, "uint8", A, rows, pool=pool))
+        lo, hi = max(0, r0 - radius), min(A, r0 + rows + radius)
+        outlines.append(nat.outline_mask(cov[lo:hi].contiguous(), radius, in_row0=lo, out_row0=r0, out_rows=rows))
+    assert np.array_equal(np.concatenate([o.cpu().numpy() for o in outlines]), ref_outline)
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool)
+    for k in range(6):
+        tool = ml.EditingTool(px=float(rng.uniform(40, 120)), py=float(rng.uniform(40, 120)),
+                              shape=synth.circle_shape(int(rng.integers(8, 30))), value=k + 1, padding_radius=radius)
+        edited = np.zeros((A, A), np.uint8)
+        want = _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+        padded = kn.padding(ref_outline, edited, radius, data, mask, k + 1)
+        # TEA on every slab first (its edited rows are the neighbours' halos), then the padding passes
+        res = [ml.apply_stroke(c, tool, l) for c, l in zip(ctxs, layers)]
+        got_padded = 0
+        for i, (r0, rows) in enumerate(slabs):
+            lo, hi = max(0, r0 - radius), min(A, r0 + rows + radius)
+            parts = []
+            if lo < r0:
+                parts.append(ctxs[i - 1].edited[-(r0 - lo):])
+            parts.append(ctxs[i].edited)
+            if hi > r0 + rows:
+                parts.append(ctxs[i + 1].edited[:hi - (r0 + rows)])
+            ext = torch.cat(parts, dim=0)
+            got_padded += nat.apply_padding(outlines[i], ext, radius, layers[i].data, layers[i].mask, k + 1,
+                                            in_row0=lo, out_row0=r0)
+        assert sum(r.edited_count for r in res) == want[0] and sum(r.fragments for r in res) == want[1]
+        assert got_padded == padded
+        assert np.array_equal(np.concatenate([l.data.cpu().numpy() for l in layers]), data), k
+        assert np.array_equal(np.concatenate([l.mask.cpu().numpy() for l in layers]), mask), k
+        assert np.array_equal(np.concatenate([c.edited.cpu().numpy() for c in ctxs]), edited), k
+    # the public stroke() with an injected halo exchange does the same on one slab
+    i, (r0, rows) = 1, slabs[1]
+    tool = ml.EditingTool(px=80.0, py=80.0, shape=synth.circle_shape(25), value=9, padding_radius=radius)
+    edited = np.zeros((A, A), np.uint8)
+    _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+    kn.padding(ref_outline, edited, radius, data, mask, 9)
+    for j in (0, 2):
+        ml.apply_stroke(ctxs[j], tool, layers[j])
+
+    def halo(plane, row0, height, rad):
+        lo, hi = max(0, row0 - rad), min(height, row0 + rows + rad)
+        return torch.cat([ctxs[0].edited[-(row0 - lo):], plane, ctxs[2].edited[:hi - (row0 + rows)]], dim=0), lo
+    ml.stroke(ctxs[1], tool, layers[1], outlines[1], halo=halo)
+    assert np.array_equal(layers[1].data.cpu().numpy(), data[r0:r0 + rows])
+    assert np.array_equal(layers[1].mask.cpu().numpy(), mask[r0:r0 + rows])
+
+
 def _torch_i32():
     import torch
     return torch.int32
