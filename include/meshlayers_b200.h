@@ -144,6 +144,12 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, const void* tea_recs
 int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_tea_params* params,
                     uint32_t* flags, const void* tri_xy, int64_t width, int64_t height, int64_t row0,
                     int64_t rows, uint32_t* tile_bits, void* stream);
+/* Same decision from the records of ml_tea_prepare: the classification then reads 16 bytes of
+ * outward-rounded NDC bounds per triangle instead of the 96-byte clip record (a superset of the
+ * triangles ml_tea_classify keeps, never a subset: flags stay conservative). */
+int ml_tea_classify_recs(const void* tea_recs, int tri_dtype, int64_t ntri, const ml_tea_params* params,
+                         uint32_t* flags, const void* tri_xy, int64_t width, int64_t height, int64_t row0,
+                         int64_t rows, uint32_t* tile_bits, void* stream);
 /* words of a footprint tile bitmap for a (rows x width) slab; 0 when culling is unavailable
  * (width % 128 != 0) */
 int ml_tea_tile_words(int64_t width, int64_t rows);
@@ -247,6 +253,31 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
 int ml_apply_padding_tiles(const uint8_t* outline, const uint8_t* edited, int64_t width, int64_t rows,
                            int64_t radius, const uint32_t* tile_bits, void* data, int esize,
                            uint32_t value_bits, uint8_t* mask, uint64_t* count, void* stream);
+
+/* ---- one call per edit: the paper's timed stroke = TEA + TPA -----------
+ * ml_stroke = ml_tea_classify_recs + ml_tea_texels + ml_apply_padding_tiles on one stream, for
+ * engines that keep everything resident (single slab or one rank's slab without padding halos).
+ * `cur` (0 or 1) selects the tile buffer this stroke writes; the other one must be the buffer the
+ * previous stroke on this `edited` plane wrote (zeroed before the first stroke) -- alternate it.
+ * counters (device, 3 x u64, zeroed here): newly edited texels, fragments, padded texels. */
+typedef struct ml_stroke_ctx {
+    const void* tri_xy;          /* [ntri][3][2] atlas grid units */
+    const void* tri_clip;        /* [ntri][3][4] clip coordinates */
+    const void* tea_recs;        /* ml_tea_prepare(tri_xy, tri_clip) */
+    int tri_dtype;               /* ML_F32 / ML_F64 */
+    int64_t ntri;
+    int64_t width, height, row0, rows;
+    const int32_t* tri_id;       /* ml_raster_tri_id map of the slab */
+    uint32_t* tri_flags;         /* (ntri+31)/32 words of scratch */
+    void* worklist;              /* quad work list scratch (see ml_tea_texels) */
+    size_t worklist_bytes;
+    uint32_t* tiles[2];          /* two tile buffers of ml_tea_tile_words(width, rows) words */
+    int64_t known_fragments;     /* covered texels of the slab */
+    uint8_t* edited;             /* the EditedAreaMask plane */
+    const uint8_t* outline;      /* outline mask for the padding pass, NULL = no TPA */
+} ml_stroke_ctx;
+int ml_stroke(const ml_stroke_ctx* ctx, int cur, const ml_tea_params* params, void* data, int esize,
+              uint32_t value_bits, uint8_t* mask, int64_t padding_radius, uint64_t* counters, void* stream);
 
 /* ---- display + layer file helpers (definitions: ext_resolve_display, ext_pack_mask)
  * SPEC:186-203 resolve_display: rgba_out[i] (4 bytes R,G,B,A) = mask[i] ? palette(u) : 0 with

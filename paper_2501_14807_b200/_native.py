@@ -48,6 +48,16 @@ class _TeaParams(C.Structure):
                 ("eps_f32", C.c_int32), ("reserved", C.c_int32)]
 
 
+class _StrokeCtx(C.Structure):
+    """include/meshlayers_b200.h ml_stroke_ctx."""
+    _fields_ = [("tri_xy", C.c_void_p), ("tri_clip", C.c_void_p), ("tea_recs", C.c_void_p),
+                ("tri_dtype", C.c_int), ("ntri", C.c_int64),
+                ("width", C.c_int64), ("height", C.c_int64), ("row0", C.c_int64), ("rows", C.c_int64),
+                ("tri_id", C.c_void_p), ("tri_flags", C.c_void_p), ("worklist", C.c_void_p),
+                ("worklist_bytes", C.c_size_t), ("tiles", C.c_void_p * 2), ("known_fragments", C.c_int64),
+                ("edited", C.c_void_p), ("outline", C.c_void_p)]
+
+
 def lib():
     """Load the C-ABI library (once).  Raises BackendUnavailable when it has not been built."""
     global _lib
@@ -76,6 +86,8 @@ def lib():
         "ml_surface_workspace_bytes": (sz, [i64]),
         "ml_tea_texels": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
                                 vp, vp, i64, vp, i32, u32, vp, vp, vp, vp]),
+        "ml_tea_classify_recs": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
+        "ml_stroke": (i32, [C.POINTER(_StrokeCtx), i32, C.POINTER(_TeaParams), vp, i32, u32, vp, i64, vp, vp]),
         "ml_tea_rec_bytes": (sz, [i64]),
         "ml_tea_prepare": (i32, [vp, vp, i32, i64, vp, sz, vp]),
         "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
@@ -118,6 +130,7 @@ EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve",
     "ml_surface_workspace_bytes", "ml_tea_texels", "ml_tea_rec_bytes", "ml_tea_prepare",
+    "ml_tea_classify_recs", "ml_stroke",
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
     "ml_select_threshold", "ml_layer_op",
@@ -505,9 +518,13 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
         cur = tiles[0] if tiles else None
         if cur is not None and not classify:
             raise TargetMismatch("footprint culling needs the classification pass")
-        _check(lib().ml_tea_classify(_ptr(clip), dt, tri.shape[0], C.byref(p), _ptr(flags), _ptr(tri), w,
-                                     int(height if height is not None else row0 + rows), row0, rows, _ptr(cur),
-                                     _stream()))
+        hh = int(height if height is not None else row0 + rows)
+        if recs is not None:          # 16-byte prepared bounds per triangle instead of the 96-byte clip record
+            _check(lib().ml_tea_classify_recs(_ptr(recs), dt, tri.shape[0], C.byref(p), _ptr(flags), _ptr(tri), w,
+                                              hh, row0, rows, _ptr(cur), _stream()))
+        else:
+            _check(lib().ml_tea_classify(_ptr(clip), dt, tri.shape[0], C.byref(p), _ptr(flags), _ptr(tri), w,
+                                         hh, row0, rows, _ptr(cur), _stream()))
     cur, prev = tiles if tiles else (None, None)
     _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), _ptr(recs), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
                                _ptr(flags), C.byref(p), _ptr(work), 0 if work is None else work.numel() * 8,
@@ -532,6 +549,36 @@ def tea_prepare(tri_xy, tri_clip, device=None):
     recs = torch.empty(nb, dtype=torch.uint8, device=dev)
     _check(lib().ml_tea_prepare(_ptr(tri), _ptr(clip), dt, tri.shape[0], _ptr(recs), nb, _stream()))
     return recs
+
+
+def stroke_ctx(tri_xy, tri_clip, recs, tri_id, flags, worklist, tiles, edited, outline, *, width, height, row0,
+               rows, known_fragments):
+    """Fill an ``ml_stroke_ctx`` for ``stroke_call`` (all arguments are resident CUDA tensors; the
+    caller keeps them alive)."""
+    torch = _torch()
+    c = _StrokeCtx()
+    c.tri_xy, c.tri_clip, c.tea_recs = tri_xy.data_ptr(), tri_clip.data_ptr(), recs.data_ptr()
+    c.tri_dtype = ML_F32 if tri_xy.dtype == torch.float32 else ML_F64
+    c.ntri = tri_xy.shape[0]
+    c.width, c.height, c.row0, c.rows = int(width), int(height), int(row0), int(rows)
+    c.tri_id, c.tri_flags = tri_id.data_ptr(), flags.data_ptr()
+    c.worklist, c.worklist_bytes = worklist.data_ptr(), worklist.numel() * 8
+    c.tiles[0], c.tiles[1] = tiles[0].data_ptr(), tiles[1].data_ptr()
+    c.known_fragments = int(known_fragments)
+    c.edited = edited.data_ptr()
+    c.outline = outline.data_ptr() if outline is not None else None
+    return c
+
+
+def stroke_call(cstruct, cur, ww, wh, depth, eps, sfx, sfy, bx, by, shape, data, mask, value, radius, counts):
+    """One C call per edit (``ml_stroke``): classification, TEA and padding on the current stream.
+    ``counts`` (int64[3], device) receives edited / fragments / padded."""
+    shape = _as_dev_bytes(shape, data.device)
+    _check_window(ww, wh, depth.shape, shape.shape)
+    p = _tea_params(ww, wh, depth, eps, sfx, sfy, bx, by, shape)
+    bits, esize = value_bits(value, data)
+    _check(lib().ml_stroke(C.byref(cstruct), int(cur), C.byref(p), _ptr(data), esize, bits, _ptr(mask), int(radius),
+                           _ptr(counts), _stream()))
 
 
 def tea_scratch(ntri, ntexels, device, max_quads=1 << 24):

@@ -158,6 +158,25 @@ struct TileBuf {
           list(base + (base ? tile_bitmap_words(ntiles) + 2 : 0)) {}
 };
 
+// Footprint tiles (TILE_W x TILE_H texels): every texel a flagged triangle can own lies in its raster
+// bbox (the same tri_bbox the rasteriser used), so the marked tiles cover every texel this stroke can
+// touch.  A tile is appended to the buffer's list by whoever marks it first.
+template <typename T>
+ML_DEV void mark_tiles(const T* __restrict__ xy, long long width, long long height, long long row0, long long rows,
+                       uint32_t* __restrict__ tile_bits) {
+    TriSetup s;
+    if (!tri_load_ccw(xy, s) || !tri_bbox(s, width, height, row0, rows)) return;
+    const int segs = (int)(width >> TILE_W_SHIFT);
+    const TileBuf tb(tile_bits, (long long)segs * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT));
+    for (int ty = (int)(s.iy0 - row0) >> TILE_H_SHIFT; ty <= (int)(s.iy1 - row0) >> TILE_H_SHIFT; ++ty)
+        for (int tx = s.ix0 >> TILE_W_SHIFT; tx <= s.ix1 >> TILE_W_SHIFT; ++tx) {
+            const int tile = ty * segs + tx;
+            const uint32_t bit = 1u << (tile & 31);
+            if (ld_volatile_u32(tb.bits + (tile >> 5)) & bit) continue;        // already marked
+            if (!(atomicOr(tb.bits + (tile >> 5), bit) & bit)) tb.list[atomicAdd(tb.count, 1ull)] = (uint32_t)tile;
+        }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
 tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p, uint32_t* __restrict__ bits,
@@ -199,20 +218,7 @@ tea_classify_kernel(const T* __restrict__ tri_clip, long long ntri, TeaParams p,
     // Footprint tiles (TILE_W x TILE_H texels): every texel a flagged triangle can own lies in its
     // raster bbox (the same tri_bbox the rasteriser used), so the marked tiles cover every texel
     // this stroke can touch; the stream kernel never reads the others.
-    if (tile_bits && live && keep) {
-        TriSetup s;
-        if (tri_load_ccw(tri_xy + 6 * t, s) && tri_bbox(s, width, height, row0, rows)) {
-            const int segs = (int)(width >> TILE_W_SHIFT);
-            const TileBuf tb(tile_bits, (long long)segs * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT));
-            for (int ty = (int)(s.iy0 - row0) >> TILE_H_SHIFT; ty <= (int)(s.iy1 - row0) >> TILE_H_SHIFT; ++ty)
-                for (int tx = s.ix0 >> TILE_W_SHIFT; tx <= s.ix1 >> TILE_W_SHIFT; ++tx) {
-                    const int tile = ty * segs + tx;
-                    const uint32_t bit = 1u << (tile & 31);
-                    if (ld_volatile_u32(tb.bits + (tile >> 5)) & bit) continue;        // already marked
-                    if (!(atomicOr(tb.bits + (tile >> 5), bit) & bit)) tb.list[atomicAdd(tb.count, 1ull)] = (uint32_t)tile;
-                }
-        }
-    }
+    if (tile_bits && live && keep) mark_tiles(tri_xy + 6 * t, width, height, row0, rows, tile_bits);
 }
 
 // flag lookup in the classification bitmap (global or shared memory); NULL bitmap = keep all
@@ -228,20 +234,76 @@ struct __align__(16) TeaRec {
 };
 static_assert(sizeof(TeaRec) == 144, "TeaRec is nine 16-byte words");
 
+// Conservative NDC bounds of a triangle for the per-stroke classification, float32 rounded OUTWARD
+// (16 bytes per triangle instead of the 96-byte clip record): [x] = xlo - dxn, [y] = xhi + dxn,
+// [z] = ylo - dyn, [w] = yhi + dyn with the margins of tea_classify_kernel; an empty interval
+// (+inf, -inf) = no fragment can pass (all w <= 0), (-inf, +inf) = always evaluate (mixed signs of w).
+template <typename T>
+ML_DEV float4 tea_bounds(const T* __restrict__ c) {
+    const float inf = __int_as_float(0x7f800000);
+    double x[3], y[3], w[3];
+#pragma unroll
+    for (int v = 0; v < 3; ++v) { x[v] = (double)c[4 * v]; y[v] = (double)c[4 * v + 1]; w[v] = (double)c[4 * v + 3]; }
+    const int npos = (w[0] > 0.0) + (w[1] > 0.0) + (w[2] > 0.0);
+    const int nnonpos = (w[0] <= 0.0) + (w[1] <= 0.0) + (w[2] <= 0.0);
+    if (nnonpos == 3) return make_float4(inf, -inf, inf, -inf);
+    if (npos != 3) return make_float4(-inf, inf, -inf, inf);
+    const double wmin = fmin(fmin(w[0], w[1]), w[2]);
+    const double ax = fmax(fmax(fabs(x[0]), fabs(x[1])), fabs(x[2])) / wmin;
+    const double ay = fmax(fmax(fabs(y[0]), fabs(y[1])), fabs(y[2])) / wmin;
+    const double xn0 = x[0] / w[0], xn1 = x[1] / w[1], xn2 = x[2] / w[2];
+    const double yn0 = y[0] / w[0], yn1 = y[1] / w[1], yn2 = y[2] / w[2];
+    const double dxn = 1e-9 * (1.0 + ax), dyn = 1e-9 * (1.0 + ay);
+    return make_float4(__double2float_rd(fmin(fmin(xn0, xn1), xn2) - dxn), __double2float_ru(fmax(fmax(xn0, xn1), xn2) + dxn),
+                       __double2float_rd(fmin(fmin(yn0, yn1), yn2) - dyn), __double2float_ru(fmax(fmax(yn0, yn1), yn2) + dyn));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
 tea_prepare_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long ntri,
-                   TeaRec* __restrict__ recs) {
+                   TeaRec* __restrict__ recs, float4* __restrict__ bounds) {
     const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
     if (t >= ntri) return;
+    const T* c = tri_clip + 12 * t;
+    bounds[t] = tea_bounds(c);
     TriSetup s;
-    if (!tri_load_ccw(tri_xy + 6 * t, s)) return;     // degenerate / non-finite: owns no texel, never read
+    if (!tri_load_ccw(tri_xy + 6 * t, s)) return;     // degenerate / non-finite: owns no texel, record never read
     TeaRec& r = recs[t];
     r.x0 = s.x0; r.y0 = s.y0; r.x1 = s.x1; r.y1 = s.y1; r.x2 = s.x2; r.y2 = s.y2;
-    const T* c = tri_clip + 12 * t;
     const int i1 = s.swapped ? 8 : 4, i2 = s.swapped ? 4 : 8;
 #pragma unroll
     for (int k = 0; k < 4; ++k) { r.c[k] = (double)c[k]; r.c[4 + k] = (double)c[i1 + k]; r.c[8 + k] = (double)c[i2 + k]; }
+}
+
+// Classification from the prepared bounds.  Same decision rule as tea_classify_kernel with the
+// triangle side of the margins folded into the stored bounds; the per-stroke side (rounding of
+// s = sfx*xn + bx, at most 2u relative) is covered by ds >= 1e-9 * (|bx| + 1 + |sfx|*(1 + |xlo| + |xhi|)).
+// Infinite bounds ("always") make every comparison below false, i.e. keep.
+template <typename T>
+__global__ void __launch_bounds__(BLOCK)
+tea_classify_bounds_kernel(const float4* __restrict__ bounds, long long ntri, TeaParams p, uint32_t* __restrict__ bits,
+                           const T* __restrict__ tri_xy, long long width, long long height, long long row0, long long rows,
+                           uint32_t* __restrict__ tile_bits) {
+    const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    const bool live = t < ntri;
+    bool keep = false;
+    if (live) {
+        const float4 b = __ldg(bounds + t);
+        if (b.x <= b.y) {
+            const double xlo = b.x, xhi = b.y, ylo = b.z, yhi = b.w;
+            const double s0 = p.sfx * xlo + p.bx, s1 = p.sfx * xhi + p.bx;
+            const double t0 = p.sfy * ylo + p.by, t1 = p.sfy * yhi + p.by;
+            const double ds = 1e-9 * (fabs(p.bx) + 1.0 + fabs(p.sfx) * (1.0 + fabs(xlo) + fabs(xhi)));
+            const double dt = 1e-9 * (fabs(p.by) + 1.0 + fabs(p.sfy) * (1.0 + fabs(ylo) + fabs(yhi)));
+            const bool out_s = (fmax(s0, s1) + ds < 0.0) || (fmin(s0, s1) - ds > 1.0);
+            const bool out_t = (fmax(t0, t1) + dt < 0.0) || (fmin(t0, t1) - dt > 1.0);
+            const bool out_w = (xhi < -1.0) || (xlo > 1.0) || (yhi < -1.0) || (ylo > 1.0);
+            keep = !(out_s || out_t || out_w);
+        }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0 && live) bits[t >> 5] = word;
+    if (tile_bits && keep) mark_tiles(tri_xy + 6 * t, width, height, row0, rows, tile_bits);
 }
 
 // Full KN:166-193 evaluation of one covered texel for its owner triangle.  `recs` (may be NULL)
@@ -679,7 +741,9 @@ int ml_tea_classify(const void* tri_clip, int tri_dtype, int64_t ntri, const ml_
     return ML_OK;
 }
 
-size_t ml_tea_rec_bytes(int64_t ntri) { return (size_t)(ntri > 0 ? ntri : 0) * sizeof(TeaRec) + 16; }
+// record buffer = [TeaRec x ntri][float4 bounds x ntri]
+size_t ml_tea_rec_bytes(int64_t ntri) { return (size_t)(ntri > 0 ? ntri : 0) * (sizeof(TeaRec) + sizeof(float4)) + 16; }
+static inline float4* tea_bounds_of(const void* recs, int64_t ntri) { return (float4*)((char*)recs + (size_t)ntri * sizeof(TeaRec)); }
 
 int ml_tea_prepare(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri, void* recs,
                    size_t rec_bytes, void* stream) {
@@ -688,8 +752,30 @@ int ml_tea_prepare(const void* tri_xy, const void* tri_clip, int tri_dtype, int6
     if (recs == nullptr || rec_bytes < ml_tea_rec_bytes(ntri) || (((uintptr_t)recs) & 15))
         return ml_fail(ML_ERR_ARG, "ml_tea_prepare needs ml_tea_rec_bytes(ntri) bytes, 16-byte aligned");
     const unsigned grid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
-    if (tri_dtype == ML_F32) tea_prepare_kernel<float><<<grid, BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_clip, ntri, (TeaRec*)recs);
-    else if (tri_dtype == ML_F64) tea_prepare_kernel<double><<<grid, BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_clip, ntri, (TeaRec*)recs);
+    if (tri_dtype == ML_F32) tea_prepare_kernel<float><<<grid, BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_clip, ntri, (TeaRec*)recs, tea_bounds_of(recs, ntri));
+    else if (tri_dtype == ML_F64) tea_prepare_kernel<double><<<grid, BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_clip, ntri, (TeaRec*)recs, tea_bounds_of(recs, ntri));
+    else return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_tea_classify_recs(const void* tea_recs, int tri_dtype, int64_t ntri, const ml_tea_params* tp,
+                         uint32_t* flags, const void* tri_xy, int64_t width, int64_t height, int64_t row0,
+                         int64_t rows, uint32_t* tile_bits, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ntri <= 0) return ML_OK;
+    if (tea_recs == nullptr) return ml_fail(ML_ERR_ARG, "ml_tea_classify_recs needs the records of ml_tea_prepare");
+    TeaParams p = ml_make_tea_params(tp);
+    if (tile_bits) {
+        const int words = ml_tea_tile_words(width, rows);
+        if (words == 0 || tri_xy == nullptr) return ml_fail(ML_ERR_ARG, "tile marking needs tri_xy and width % 128 == 0");
+        const long long tiles = (width >> TILE_W_SHIFT) * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
+        ML_CUDA(cudaMemsetAsync(tile_bits, 0, (size_t)(tile_bitmap_words(tiles) + 2) * 4, st));   // bitmap + list count
+    }
+    const unsigned grid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
+    const float4* bounds = tea_bounds_of(tea_recs, ntri);
+    if (tri_dtype == ML_F32) tea_classify_bounds_kernel<float><<<grid, BLOCK, 0, st>>>(bounds, ntri, p, flags, (const float*)tri_xy, width, height, row0, rows, tile_bits);
+    else if (tri_dtype == ML_F64) tea_classify_bounds_kernel<double><<<grid, BLOCK, 0, st>>>(bounds, ntri, p, flags, (const double*)tri_xy, width, height, row0, rows, tile_bits);
     else return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
     ML_CUDA(cudaGetLastError());
     return ML_OK;
@@ -715,6 +801,23 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, const void* tea_recs
         return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, (const TeaRec*)tea_recs, width, row0, n, tri_id, tri_flags, ntri, p,
                                  worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);
     return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+}
+
+int ml_stroke(const ml_stroke_ctx* c, int cur, const ml_tea_params* tp, void* data, int esize,
+              uint32_t value_bits, uint8_t* mask, int64_t padding_radius, uint64_t* counters, void* stream) {
+    if (c == nullptr || (cur != 0 && cur != 1)) return ml_fail(ML_ERR_ARG, "ml_stroke: bad context / tile buffer index");
+    if (c->tiles[0] == nullptr || c->tiles[1] == nullptr || c->tea_recs == nullptr || c->tri_flags == nullptr)
+        return ml_fail(ML_ERR_ARG, "ml_stroke needs the prepared records, the triangle flags and both tile buffers");
+    ML_CUDA(cudaMemsetAsync(counters, 0, 3 * sizeof(uint64_t), (cudaStream_t)stream));
+    int rc = ml_tea_classify_recs(c->tea_recs, c->tri_dtype, c->ntri, tp, c->tri_flags, c->tri_xy, c->width, c->height,
+                                  c->row0, c->rows, c->tiles[cur], stream);
+    if (rc != ML_OK) return rc;
+    rc = ml_tea_texels(c->tri_xy, c->tri_clip, c->tea_recs, c->tri_dtype, c->ntri, c->width, c->row0, c->rows, c->tri_id,
+                       c->tri_flags, tp, c->worklist, c->worklist_bytes, c->tiles[cur], c->tiles[cur ^ 1],
+                       c->known_fragments, data, esize, value_bits, mask, c->edited, counters, stream);
+    if (rc != ML_OK || padding_radius <= 0 || c->outline == nullptr) return rc;
+    return ml_apply_padding_tiles(c->outline, c->edited, c->width, c->rows, padding_radius, c->tiles[cur], data, esize,
+                                  value_bits, mask, counters + 2, stream);
 }
 
 }  // extern "C"

@@ -124,7 +124,38 @@ class StrokeContext:
         self.tiles = [torch.zeros(nwords, dtype=torch.int32, device=device) for _ in range(2)] if nwords else None
         self.edited_fully_dirty = False
         self.stroke_tiles = None          # tile bitmap of the last culled stroke (footprint of ctx.edited)
+        self.cur = 0                      # tile buffer the next culled stroke writes; the other one is "previous"
         self.device = device
+        self._cstruct = None              # (outline data_ptr, ml_stroke_ctx) of the one-call stroke path
+
+
+def _begin_culled_stroke(self):
+    """Footprint-culled strokes clear the edited plane per footprint; after a whole-plane stroke the
+    plane and the "previous" tile buffer are reset once."""
+    if self.edited_fully_dirty:
+        self.edited.zero_()
+        self.tiles[self.cur ^ 1].zero_()
+        self.edited_fully_dirty = False
+
+
+def _end_culled_stroke(self):
+    self.stroke_tiles = self.tiles[self.cur]      # footprint of the marks now in ctx.edited (for TPA)
+    self.cur ^= 1                                  # this stroke's footprint is the next one's "previous"
+
+
+StrokeContext.begin_culled_stroke = _begin_culled_stroke
+StrokeContext.end_culled_stroke = _end_culled_stroke
+
+
+def _stroke_checks(ctx, layer):
+    s = ctx.surface
+    if ctx.depth.generation != ctx.camera.generation:
+        raise StaleDepth("depth map was rendered for camera generation %d, camera is at %d"
+                         % (ctx.depth.generation, ctx.camera.generation))              # SPEC.md:281
+    if layer.shape != (s.rows, s.width):
+        raise TargetMismatch("layer is %s, surface map slab is %s" % (layer.shape, (s.rows, s.width)))
+    if s.covered == 0 and s.row0 == 0 and s.rows == s.height:
+        raise LayerMeshMismatch("no uv coverage at layer resolution")                  # SPEC.md:281
 
 
 def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False, cull=True):
@@ -133,14 +164,8 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
     ``cull`` (default) restricts the per-texel kernel to the stroke's footprint tiles, so a stroke
     costs O(triangles + footprint) instead of O(atlas); results are identical."""
     torch = _native._torch()
-    if ctx.depth.generation != ctx.camera.generation:
-        raise StaleDepth("depth map was rendered for camera generation %d, camera is at %d"
-                         % (ctx.depth.generation, ctx.camera.generation))              # SPEC.md:281
+    _stroke_checks(ctx, layer)
     s = ctx.surface
-    if layer.shape != (s.rows, s.width):
-        raise TargetMismatch("layer is %s, surface map slab is %s" % (layer.shape, (s.rows, s.width)))
-    if s.covered == 0 and s.row0 == 0 and s.rows == s.height:
-        raise LayerMeshMismatch("no uv coverage at layer resolution")                  # SPEC.md:281
     sfx, sfy, bx, by = compute_tool_projection(ctx.camera, tool).kernel_factors
     counts = torch.zeros(2, dtype=torch.int64, device=ctx.device)
     shape = tool.shape if _native._is_cuda_tensor(tool.shape) else _native._as_dev_bytes(tool.shape, ctx.device)
@@ -149,15 +174,11 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
     if s.overlap == 0 and not force_direct and ctx.tiles is not None and cull:
         # footprint-culled path: the EditedAreaMask reset is done inside the kernel
         # for the tiles the previous stroke could touch
-        if ctx.edited_fully_dirty:
-            ctx.edited.zero_()
-            ctx.tiles[1].zero_()
-            ctx.edited_fully_dirty = False
+        ctx.begin_culled_stroke()
         _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
-                           scratch=ctx.scratch, height=s.height, tiles=(ctx.tiles[0], ctx.tiles[1]),
+                           scratch=ctx.scratch, height=s.height, tiles=(ctx.tiles[ctx.cur], ctx.tiles[ctx.cur ^ 1]),
                            known_fragments=s.covered, recs=ctx.recs)
-        ctx.tiles.reverse()                                   # this stroke's footprint is the next one's "previous"
-        ctx.stroke_tiles = ctx.tiles[1]                       # footprint of the marks now in ctx.edited (for TPA)
+        ctx.end_culled_stroke()
     elif s.overlap == 0 and not force_direct:
         ctx.edited.zero_()
         ctx.edited_fully_dirty = True
@@ -185,12 +206,28 @@ def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, halo
     (``sharding.exchange_halo``; ``halo`` replaces that exchange, e.g. in single-process tests).  The
     padding pass then streams the slab's outline plane instead of walking footprint tiles."""
     torch = _native._torch()
-    res = apply_stroke(ctx, tool, layer, eps=eps, cull=cull)
     radius = tool.padding_radius
+    s = ctx.surface
+    as_u8 = outline.view(torch.uint8) if outline.dtype == torch.bool else outline
+    one_call = (cull and ctx.tiles is not None and s.overlap == 0 and s.rows == s.height and 0 < radius <= 4
+                and all(t.data_ptr() % 16 == 0 for t in (layer.data, layer.mask, as_u8)))
+    if one_call:
+        # the whole edit in ONE C call (ml_stroke: classify + TEA + TPA); counters stay on the device
+        _stroke_checks(ctx, layer)
+        ctx.begin_culled_stroke()
+        if ctx._cstruct is None or ctx._cstruct[0] != as_u8.data_ptr():
+            ctx._cstruct = (as_u8.data_ptr(), _native.stroke_ctx(
+                ctx.tri_xy, ctx.tri_clip, ctx.recs, s.tri_id, ctx.scratch[0], ctx.scratch[1], ctx.tiles, ctx.edited, as_u8,
+                width=s.width, height=s.height, row0=s.row0, rows=s.rows, known_fragments=s.covered))
+        sfx, sfy, bx, by = compute_tool_projection(ctx.camera, tool).kernel_factors
+        counts = torch.empty(3, dtype=torch.int64, device=ctx.device)
+        _native.stroke_call(ctx._cstruct[1], ctx.cur, float(ctx.camera.width), float(ctx.camera.height), ctx.depth.plane,
+                            eps, sfx, sfy, bx, by, tool.shape, layer.data, layer.mask, tool.value, radius, counts)
+        ctx.end_culled_stroke()
+        return EditResult(edited_mask=ctx.edited, _counts=counts[:2], _padded=counts[2:])
+    res = apply_stroke(ctx, tool, layer, eps=eps, cull=cull)
     if radius > 0:
-        s = ctx.surface
         pc = torch.zeros(1, dtype=torch.int64, device=ctx.device)
-        as_u8 = outline.view(torch.uint8) if outline.dtype == torch.bool else outline
         ext, ext_row0 = ctx.edited, s.row0
         if s.rows != s.height:
             from . import sharding
