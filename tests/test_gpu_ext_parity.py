@@ -494,3 +494,46 @@ def test_c_abi_argument_validation():
     assert L.ml_surface_resolve(none, none, none, 1, 4, 256, 0, 8, none, none, none, none, none, none, 0, none) == 1
     torch.cuda.synchronize()
     assert not bool(z.any()) and not bool(z2.any())
+
+
+def test_classification_from_bounds_is_a_superset():
+    """ml_tea_classify_recs (16-byte outward-rounded bounds) must keep every triangle ml_tea_classify
+    keeps -- on random clip-space triangles incl. mixed signs of w, w == 0, NaN / inf coordinates, huge
+    and tiny magnitudes, and random tool maps (negative scales, degenerate zero scale)."""
+    import ctypes as C
+    import torch
+    L = nat.lib()
+    rng = np.random.default_rng(77)
+    T = 20000
+    clip = np.empty((T, 3, 4))
+    w = rng.uniform(0.05, 4.0, size=(T, 3)) * np.exp(rng.uniform(-6, 6, size=(T, 1)))
+    w[rng.random((T, 3)) < 0.1] *= -1.0
+    w[rng.random((T, 3)) < 0.01] = 0.0
+    clip[..., 3] = w
+    clip[..., 0] = rng.uniform(-3, 3, size=(T, 3)) * np.abs(w) + rng.normal(size=(T, 3)) * 1e-3
+    clip[..., 1] = rng.uniform(-3, 3, size=(T, 3)) * np.abs(w)
+    clip[..., 2] = rng.uniform(-1, 1, size=(T, 3)) * np.abs(w)
+    bad = rng.random(T) < 0.01
+    clip[bad, rng.integers(0, 3, bad.sum()), rng.integers(0, 4, bad.sum())] = rng.choice([np.nan, np.inf, -np.inf], bad.sum())
+    xy = rng.uniform(0, 256, size=(T, 3, 2))
+    depth = torch.ones((64, 64), dtype=torch.float32, device="cuda")
+    shape = torch.ones((8, 8), dtype=torch.uint8, device="cuda")
+    for dt in (np.float64, np.float32):
+        d_clip, d_xy = _dev(clip.astype(dt)), _dev(xy.astype(dt))
+        code = nat.ML_F64 if dt == np.float64 else nat.ML_F32
+        recs = nat.tea_prepare(d_xy, d_clip)
+        nw = (T + 31) // 32
+        for k in range(12):
+            sfx, sfy = rng.uniform(-20, 20, size=2) * (0.0 if k == 11 else 1.0)
+            bx, by = rng.uniform(-8, 8, size=2)
+            p = nat._tea_params(64.0, 64.0, depth, 1e-4, sfx, sfy, bx, by, shape)
+            f0 = torch.zeros(nw, dtype=torch.int32, device="cuda")
+            f1 = torch.zeros(nw, dtype=torch.int32, device="cuda")
+            assert L.ml_tea_classify(C.c_void_p(d_clip.data_ptr()), code, T, C.byref(p), C.c_void_p(f0.data_ptr()), None,
+                                     256, 256, 0, 256, None, None) == 0
+            assert L.ml_tea_classify_recs(C.c_void_p(recs.data_ptr()), code, T, C.byref(p), C.c_void_p(f1.data_ptr()), None,
+                                          256, 256, 0, 256, None, None) == 0
+            a, b = f0.cpu().numpy().view(np.uint32), f1.cpu().numpy().view(np.uint32)
+            assert not (a & ~b).any(), (dt, k)
+            kept0 = int(np.unpackbits(a.view(np.uint8)).sum()); kept1 = int(np.unpackbits(b.view(np.uint8)).sum())
+            assert kept0 <= kept1 <= kept0 + max(50, kept0 // 50)           # and not much looser
