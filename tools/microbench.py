@@ -125,6 +125,23 @@ def main():
     pos = torch.rand((3, N, N), device=dev, generator=g)
     run("sphere few hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.05, data, mask, edited, 3, counts=cnt), 12 * n)
     run("sphere 50% hits", lambda: nat.select_sphere(pos, (0.5, 0.5, 0.5), 0.62, data, mask, edited, 3, counts=cnt), 12 * n)
+    if not want or any(w in "display pack" for w in want):
+        from paper_2501_14807_b200.display import Palette
+        pal = Palette.grayscale()
+        pos_pts, col_pts = np.asarray(pal.positions, dtype=np.float64), np.asarray(pal.colours, dtype=np.float64)
+        rgba = torch.empty((N, N, 4), dtype=torch.uint8, device=dev)
+        dd = torch.randint(0, 256, (N, N), device=dev, generator=g, dtype=torch.int32).to(torch.uint8)
+        half = (torch.rand((N, N), device=dev, generator=g) < 0.5).to(torch.uint8)
+        full = torch.ones((N, N), dtype=torch.uint8, device=dev)
+        run("display u8 (all valid)", lambda: nat.resolve_display(dd, full, 0.0, 255.0, pos_pts, col_pts, out=rgba), 6 * n)
+        run("display u8 (50% noise mask)", lambda: nat.resolve_display(dd, half, 0.0, 255.0, pos_pts, col_pts, out=rgba), 6 * n)
+        df = torch.rand((N, N), device=dev, generator=g)
+        run("display f32 (all valid)", lambda: nat.resolve_display(df, full, 0.0, 1.0, pos_pts, col_pts, out=rgba), 9 * n)
+        bits = nat.pack_mask(half)
+        run("pack_mask", lambda: nat.pack_mask(half), n + n // 8)
+        outm = torch.empty((N, N), dtype=torch.uint8, device=dev)
+        run("unpack_mask", lambda: nat.unpack_mask(bits, N * N, outm), n + n // 8)
+        del rgba, dd, half, full, df, bits
     # smooth "surface" positions (a heightfield over the atlas) for the footprint-culled brushes
     if not want or any(w in "sphere culled" for w in want):
         yy, xx = torch.meshgrid(torch.linspace(0, 1, N, device=dev), torch.linspace(0, 1, N, device=dev), indexing="ij")
