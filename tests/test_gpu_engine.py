@@ -94,6 +94,33 @@ def test_apply_stroke_equals_oracle_random_scenes(seed):              # SPEC.md:
         assert res.transfer_bytes == 64                                              # SPEC.md:609 acceptance #5
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_strokes_with_camera_inside_the_mesh(seed):
+    """Camera INSIDE the sphere with a wide field of view: many triangles have vertices behind the
+    camera (w <= 0, mixed signs of w within a triangle), window coordinates far outside the viewport
+    and random non-convex tool shapes -- the conservative classification must keep every triangle
+    the per-fragment filters could accept.  Culled, streamed and direct kernels == oracle."""
+    rng = np.random.default_rng(900 + seed)
+    mesh = synth.icosphere_mesh(3)
+    A, W = 256, 96
+    eye = rng.uniform(-0.4, 0.4, size=3)
+    target = eye + rng.normal(size=3)
+    cam = synth.default_camera(W, W, eye=tuple(eye), target=tuple(target), fovy=float(rng.uniform(60, 140)), near=0.05, far=4.0)
+    surf = ml.build_surface_map(mesh, A, A)
+    depth = ml.render_depth(mesh, cam)
+    ctx = ml.StrokeContext(mesh, cam, depth, surf)
+    shape = (rng.random((int(rng.integers(5, 60)), int(rng.integers(5, 60)))) < 0.6).astype(np.uint8)
+    tool = ml.EditingTool(px=float(rng.uniform(-10, W + 10)), py=float(rng.uniform(-10, W + 10)), shape=shape, value=5)
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool); edited = np.zeros((A, A), np.uint8)
+    want = _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+    pool = ml.TexturePool()
+    for mode in ("cull", "stream", "direct"):
+        layer = ml.create_layer(mode, "uint8", A, A, pool=pool)
+        res = ml.apply_stroke(ctx, tool, layer, cull=(mode == "cull"), force_direct=(mode == "direct"))
+        assert (res.edited_count, res.fragments) == want, mode
+        assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(res.edited_mask.cpu().numpy(), edited), mode
+
+
 def test_footprint_culling_sequence_equals_oracle():
     """A sequence of strokes on ONE context: with footprint culling the per-stroke EditedAreaMask
     (cleared only where the previous stroke could have written) and the layer planes must equal
