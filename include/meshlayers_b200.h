@@ -89,7 +89,8 @@ int ml_raster_tea(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
 
 /* ---- surface map (north star (1); definition: oracle/kn_port.c ext_surface_map) ---------------
  * Pass 1: tri_id[y][x] = largest index of a triangle covering the texel centre, -1 if none.
- * counters (device, zeroed): [0] += fragments, [1] += overlap events (= fragments - covered). */
+ * counters (device, zeroed): [0] += fragments.  Overlap events (0 iff no two triangles overlap in uv
+ * space) = fragments - covered texels, the latter counted by ml_surface_resolve. */
 int ml_raster_tri_id(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
                      int64_t row0, int64_t rows, int32_t* tri_id, uint64_t* counters,
                      void* workspace, size_t workspace_bytes, void* stream);

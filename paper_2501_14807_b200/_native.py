@@ -458,7 +458,7 @@ def surface_map(tri_xy, tri_pos, tri_nrm, width, height, *, row0=0, rows=None, d
                                 _ptr(pos), _ptr(nrm), _ptr(area), C.c_void_p(ctr.data_ptr() + 16),
                                 _ptr(recs), sb, _stream()))
     c = ctr.tolist()
-    return dict(tri_id=tri_id, pos=pos, nrm=nrm, area=area, fragments=int(c[0]), overlap=int(c[1]),
+    return dict(tri_id=tri_id, pos=pos, nrm=nrm, area=area, fragments=int(c[0]), overlap=int(c[0]) - int(c[2]),
                 covered=int(c[2]))
 
 
@@ -473,8 +473,8 @@ def raster_tri_id(tri_xy, width, height, *, row0=0, rows=None, device=None):
     ws, nb = _workspace(tri.shape[0], device)
     _check(lib().ml_raster_tri_id(_ptr(tri), dt, tri.shape[0], width, height, row0, rows, _ptr(tri_id),
                                   _ptr(ctr), _ptr(ws), nb, _stream()))
-    c = ctr.tolist()
-    return tri_id, int(c[0]), int(c[1])
+    fragments = int(ctr[0].item())
+    return tri_id, fragments, fragments - int((tri_id >= 0).sum().item())       # overlap = fragments - covered
 
 
 def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,

@@ -8,7 +8,8 @@
 //   * the depth plane equals min(initial, min_t float32(d_t)) for any order.
 //
 // Work distribution (B200: 148 SMs, thousands of resident warps):
-//   pass A  one WARP per triangle; lanes stride over the bbox in row-major order.  Triangles
+//   pass A  one WARP per triangle: per-row covered spans by bisection on the exact edge predicate,
+//           then the covered texels are enumerated 32 at a time (see raster_warp_kernel).  Triangles
 //           whose bbox exceeds SMALL_MAX texels are not rasterised here but appended to a
 //           "large" list together with their number of CHUNK-texel chunks.
 //   pass B  single-block exclusive scan of the chunk counts.
@@ -39,6 +40,7 @@ struct LargeList {
 // Planes are slab-local: texel (x, y) lives at (y - row0) * width + x.
 
 struct CoverageFn {
+    static constexpr bool NEEDS_E = false;        // fragment() ignores the edge-function values
     uint8_t* out; long long width, row0;
     struct Tri {};
     ML_DEV Tri setup(long long, const TriSetup&) const { return Tri(); }
@@ -49,20 +51,23 @@ struct CoverageFn {
 };
 
 struct TriIdFn {
+    static constexpr bool NEEDS_E = false;
     int* tri_id; long long width, row0;
     struct Tri {};
     ML_DEV Tri setup(long long, const TriSetup&) const { return Tri(); }
     ML_DEV void fragment(const Tri&, long long t, int x, int y, double, double, double,
-                         long long& c0, long long& c1) const {
-        // last triangle in submission order owns the texel
-        int old = atomicMax(tri_id + (y - row0) * width + x, (int)t);
+                         long long& c0, long long&) const {
+        // last triangle in submission order owns the texel.  The old value is not
+        // used, so this is a fire-and-forget reduction (RED.MAX): no lane waits for the L2 round trip.
+        // Overlap events = fragments - covered texels; the resolve pass counts the covered ones.
+        atomicMax(tri_id + (y - row0) * width + x, (int)t);
         ++c0;                               // fragments
-        if (old >= 0) ++c1;                 // overlap events = fragments - covered texels
     }
 };
 
 template <typename T>
 struct DepthFn {
+    static constexpr bool NEEDS_E = true;
     const T* tri_zn; float* depth; long long width;
     struct Tri { double z0, z1, z2; };
     ML_DEV Tri setup(long long t, const TriSetup& s) const {
@@ -94,6 +99,7 @@ struct DepthFn {
 
 template <typename T>
 struct TeaFn {
+    static constexpr bool NEEDS_E = true;
     const T* tri_clip; TeaParams p;
     void* data; uint8_t* mask; uint8_t* edited;
     long long width, row0; uint32_t value; int esize;
@@ -124,7 +130,50 @@ struct TeaFn {
 };
 
 // ------------------------------------------------------------------ pass A
-template <typename T, typename F>
+// Row spans.  For a fixed row the edge function e_i(x) = fl(K_i - fl(m_i * fl(cx - xo_i))) is a
+// MONOTONE function of the column (floating-point subtraction, multiplication by a constant and
+// rounding are all monotone), so the accepted columns of each edge form a prefix (m_i > 0), a suffix
+// (m_i < 0) or everything / nothing (m_i == 0), and the covered texels of the row are one interval.
+// Its ends are found by bisection on the EXACT predicate of KN:72-80 -- no analytic intersection, so
+// the covered set is bit-for-bit the one the per-texel test gives -- in O(log w) probes per edge.
+struct RowEdge { double K, m, xo; bool tie; };            // e(x) = K - m * ((x + 0.5) - xo)
+ML_DEV bool edge_accepts(const RowEdge& g, int x) {
+    const double e = xsub(g.K, xmul(g.m, xsub(xadd((double)x, 0.5), g.xo)));
+    return (e > 0.0) || ((e == 0.0) && g.tie);                                   // KN:78-80
+}
+// clip [xa, xb] to the columns edge g accepts
+ML_DEV void edge_clip(const RowEdge& g, int& xa, int& xb) {
+    if (xa > xb) return;
+    if (g.m == 0.0) { if (!edge_accepts(g, xa)) xb = xa - 1; return; }
+    if (g.m > 0.0) {                       // non-increasing in x: accepted columns are a prefix
+        if (!edge_accepts(g, xa)) { xb = xa - 1; return; }
+        int lo = xa, hi = xb;              // invariant: lo accepted; answer = last accepted in [lo, hi]
+        while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (edge_accepts(g, mid)) lo = mid; else hi = mid - 1; }
+        xb = lo;
+    } else {                               // non-decreasing: accepted columns are a suffix
+        if (!edge_accepts(g, xb)) { xb = xa - 1; return; }
+        int lo = xa, hi = xb;              // invariant: hi accepted; answer = first accepted in [lo, hi]
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (edge_accepts(g, mid)) hi = mid; else lo = mid + 1; }
+        xa = hi;
+    }
+}
+// covered interval of row y (empty: xa > xb)
+ML_DEV void row_span(const TriSetup& s, int y, int& xa, int& xb) {
+    const double cy = xadd((double)y, 0.5);                                      // KN:63
+    xa = s.ix0; xb = s.ix1;
+    edge_clip(RowEdge{xmul(s.ax, xsub(cy, s.y1)), s.ay, s.x1, s.t0}, xa, xb);    // KN:72
+    edge_clip(RowEdge{xmul(s.bx, xsub(cy, s.y2)), s.by, s.x2, s.t1}, xa, xb);    // KN:73
+    edge_clip(RowEdge{xmul(s.cx, xsub(cy, s.y0)), s.cy, s.x0, s.t2}, xa, xb);    // KN:74
+}
+
+// One WARP per triangle.  Tiny boxes (<= 32 texels) are tested texel by texel in one step.  Larger
+// ones: (1) lane r finds the span of row r by bisection, (2) a warp prefix sum over the span lengths
+// enumerates the covered texels, (3) lanes take them 32 at a time in row-major order (neighbouring
+// lanes on neighbouring texels), so no lane is spent on an uncovered texel of the box.
+// SPANS = false keeps only the texel-by-texel walk (lanes stride over the box): the leaner kernel for
+// inputs whose triangles cover a few texels each (depth pass, coarse atlases); the host picks the
+// variant from the average texels per triangle -- both give identical results for any input.
+template <typename T, typename F, bool SPANS>
 __global__ void __launch_bounds__(BLOCK)
 raster_warp_kernel(const T* __restrict__ tri_xy, long long ntri, long long width, long long height,
                    long long row0, long long rows, F f, LargeList ll,
@@ -147,10 +196,42 @@ raster_warp_kernel(const T* __restrict__ tri_xy, long long ntri, long long width
             continue;
         }
         const typename F::Tri a = f.setup(t, s);
-        for (int j = lane; j < (int)n; j += 32) {
-            const int yy = j / bw, x = s.ix0 + (j - yy * bw), y = s.iy0 + yy;
-            double e0, e1, e2;
-            if (tri_inside(s, x, y, e0, e1, e2)) f.fragment(a, t, x, y, e0, e1, e2, c0, c1);
+        if (!SPANS || n <= 64) {
+            for (int j = lane; j < (int)n; j += 32) {
+                const int yy = j / bw, x = s.ix0 + (j - yy * bw), y = s.iy0 + yy;
+                double e0, e1, e2;
+                if (tri_inside(s, x, y, e0, e1, e2)) f.fragment(a, t, x, y, e0, e1, e2, c0, c1);
+            }
+            continue;
+        }
+        for (int rb = 0; rb < bh; rb += 32) {
+            int xa = 1, xb = 0;
+            if (rb + lane < bh) row_span(s, s.iy0 + rb + lane, xa, xb);
+            const int len = xb >= xa ? xb - xa + 1 : 0;
+            int pre = len;                                   // inclusive prefix sum of the span lengths
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, pre, o); if (lane >= o) pre += v; }
+            const int total = __shfl_sync(0xffffffffu, pre, 31);
+            const int excl = pre - len;
+#pragma unroll 2
+            for (int kb = 0; kb < total; kb += 32) {
+                const int k = kb + lane;
+                int lo = 0, hi = 31;                         // first lane whose inclusive prefix exceeds k
+#pragma unroll
+                for (int step = 0; step < 5; ++step) {
+                    const int mid = (lo + hi) >> 1;
+                    const int pm = __shfl_sync(0xffffffffu, pre, mid);
+                    if (k < pm) hi = mid; else lo = mid + 1;
+                }
+                const int r = lo & 31;
+                const int ex = __shfl_sync(0xffffffffu, excl, r), xs = __shfl_sync(0xffffffffu, xa, r);
+                if (k < total) {
+                    const int x = xs + (k - ex), y = s.iy0 + rb + r;
+                    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+                    if (F::NEEDS_E) tri_inside(s, x, y, e0, e1, e2);             // barycentric numerators, KN:72-74
+                    f.fragment(a, t, x, y, e0, e1, e2, c0, c1);
+                }
+            }
         }
     }
     block_count_add(c0, counters);
@@ -235,7 +316,10 @@ int raster_launch(const T* tri_xy, long long ntri, long long width, long long he
     long long blocks = (ntri + warps_per_block - 1) / warps_per_block;
     const long long cap = (long long)ml_sm_count() * 64;
     if (blocks > cap) blocks = cap;
-    raster_warp_kernel<T, F><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr);
+    if ((double)width * (double)rows >= 40.0 * (double)ntri)          // >= ~40 texels per triangle: row spans pay off
+        raster_warp_kernel<T, F, true><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr);
+    else
+        raster_warp_kernel<T, F, false><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr);
     scan_kernel<<<1, 1024, 0, st>>>(ll);
     raster_chunk_kernel<T, F><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, width, height, row0, rows, f, ll, ctr);
     ML_CUDA(cudaGetLastError());
