@@ -41,8 +41,24 @@ struct LargeList {
 
 struct CoverageFn {
     static constexpr bool NEEDS_E = false;        // fragment() ignores the edge-function values
+    static constexpr bool WORD_SPANS = true;      // spans are written word by word (span_words below)
     uint8_t* out; long long width, row0;
     struct Tri {};
+    // Set the bytes `ones` (0x01 in every byte lane to set) of one aligned 32-bit word with ONE atomic
+    // and count the lanes that were 0 (KN:97-99 for up to four texels).  A lane that held some other
+    // non-zero value is forced to exactly 1 afterwards (byte_set1_was0), which cannot change the count.
+    ML_DEV uintptr_t row_address(int y) const { return (uintptr_t)(out + (y - row0) * width); }
+    ML_DEV void word_fragment(uint32_t* word, uint32_t ones, long long& c0) const {
+        const uint32_t old = atomicOr(word, ones);
+        const uint32_t lanes = ones * 0x80u;                          // bit 7 of every byte lane to set
+        c0 += __popc(zero_bytes_msb(old) & lanes);
+        uint32_t odd = (old & ~0x01010101u) & (ones * 0xffu);         // lanes holding neither 0 nor 1
+        while (odd) {
+            const int b = (__ffs(odd) - 1) >> 3;
+            odd &= ~(0xffu << (8 * b));
+            byte_set1_was0((uint8_t*)word, b);
+        }
+    }
     ML_DEV Tri setup(long long, const TriSetup&) const { return Tri(); }
     ML_DEV void fragment(const Tri&, long long, int x, int y, double, double, double,
                          long long& c0, long long&) const {
@@ -52,6 +68,7 @@ struct CoverageFn {
 
 struct TriIdFn {
     static constexpr bool NEEDS_E = false;
+    static constexpr bool WORD_SPANS = false;
     int* tri_id; long long width, row0;
     struct Tri {};
     ML_DEV Tri setup(long long, const TriSetup&) const { return Tri(); }
@@ -68,6 +85,7 @@ struct TriIdFn {
 template <typename T>
 struct DepthFn {
     static constexpr bool NEEDS_E = true;
+    static constexpr bool WORD_SPANS = false;
     const T* tri_zn; float* depth; long long width;
     struct Tri { double z0, z1, z2; };
     ML_DEV Tri setup(long long t, const TriSetup& s) const {
@@ -100,6 +118,7 @@ struct DepthFn {
 template <typename T>
 struct TeaFn {
     static constexpr bool NEEDS_E = true;
+    static constexpr bool WORD_SPANS = false;
     const T* tri_clip; TeaParams p;
     void* data; uint8_t* mask; uint8_t* edited;
     long long width, row0; uint32_t value; int esize;
@@ -207,8 +226,13 @@ raster_warp_kernel(const T* __restrict__ tri_xy, long long ntri, long long width
         for (int rb = 0; rb < bh; rb += 32) {
             int xa = 1, xb = 0;
             if (rb + lane < bh) row_span(s, s.iy0 + rb + lane, xa, xb);
-            const int len = xb >= xa ? xb - xa + 1 : 0;
-            int pre = len;                                   // inclusive prefix sum of the span lengths
+            // items to enumerate: covered texels, or (byte planes) the aligned 32-bit words they occupy
+            int len = xb >= xa ? xb - xa + 1 : 0, mis = 0;
+            if constexpr (F::WORD_SPANS) {
+                mis = (int)(f.row_address(s.iy0 + rb + lane) & 3);        // misalignment of the row start
+                if (len) len = ((mis + xb) >> 2) - ((mis + xa) >> 2) + 1;
+            }
+            int pre = len;                                   // inclusive prefix sum of the item counts
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) { const int v = __shfl_up_sync(0xffffffffu, pre, o); if (lane >= o) pre += v; }
             const int total = __shfl_sync(0xffffffffu, pre, 31);
@@ -225,6 +249,16 @@ raster_warp_kernel(const T* __restrict__ tri_xy, long long ntri, long long width
                 }
                 const int r = lo & 31;
                 const int ex = __shfl_sync(0xffffffffu, excl, r), xs = __shfl_sync(0xffffffffu, xa, r);
+                if constexpr (F::WORD_SPANS) {
+                    const int xe = __shfl_sync(0xffffffffu, xb, r), ms = __shfl_sync(0xffffffffu, mis, r);
+                    if (k < total) {
+                        const int w = ((ms + xs) >> 2) + (k - ex);            // word of the row, from its aligned base
+                        const int b0 = max(ms + xs - 4 * w, 0), b1 = min(ms + xe - 4 * w, 3);   // byte lanes b0..b1
+                        const uint32_t ones = 0x01010101u & (0xffffffffu >> (8 * (3 - b1))) & (0xffffffffu << (8 * b0));
+                        f.word_fragment((uint32_t*)(f.row_address(s.iy0 + rb + r) - ms) + w, ones, c0);
+                    }
+                    continue;
+                }
                 if (k < total) {
                     const int x = xs + (k - ex), y = s.iy0 + rb + r;
                     double e0 = 0.0, e1 = 0.0, e2 = 0.0;

@@ -123,6 +123,36 @@ def test_eps_promotion_mode_golden():
 
 # ------------------------------------------------------------------ random scenes vs the oracle
 
+@pytest.mark.parametrize("seed", range(6))
+def test_coverage_span_path_dirty_misaligned(seed):
+    """Row-span rasteriser (few, large triangles -> the span variant) writing byte planes word by
+    word: odd widths, a plane view starting at an odd byte offset, planes pre-dirtied with values
+    other than 0 / 1 (KN:97-99 sets them to exactly 1 and does not count them), overlapping
+    triangles racing on the same words; the texel-walk variant (many small triangles) agrees."""
+    import torch
+    from paper_2501_14807_b200 import synth
+    rng = np.random.default_rng(3000 + seed)
+    w, h = int(rng.integers(61, 260)) | 1, int(rng.integers(40, 200))
+    ntri = 40
+    tri = synth.random_soup(rng, ntri, float(max(w, h)), dtype=np.float64, degenerate_frac=0.05, snap_frac=0.5)
+    dirty = rng.choice(np.array([0, 0, 0, 1, 2, 255], np.uint8), size=(h, w))
+    ref = dirty.copy()
+    want = kn.coverage_fill(tri, w, h, ref)
+    off = int(rng.integers(1, 4))
+    buf = torch.zeros(h * w + 8, dtype=torch.uint8, device="cuda")
+    out = buf[off:off + h * w].view(h, w)
+    out.copy_(_dev(dirty))
+    assert nat.coverage_fill(_dev(tri), w, h, out) == want
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert not bool(buf[:off].any()) and not bool(buf[off + h * w:].any())          # neighbours of the view untouched
+    # same scene cut into many small triangles takes the texel-walk variant: same plane
+    small = synth.random_soup(rng, 4000, float(max(w, h)), dtype=np.float64)
+    ref2 = dirty.copy()
+    want2 = kn.coverage_fill(small, w, h, ref2)
+    out.copy_(_dev(dirty))
+    assert nat.coverage_fill(_dev(small), w, h, out) == want2 and np.array_equal(out.cpu().numpy(), ref2)
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_coverage_random_vs_oracle(seed):
     from paper_2501_14807_b200 import synth
