@@ -66,41 +66,45 @@ def launches(src, dst):
     print("wrote", dst)
 
 
-def full(src, dst, traffic_dst=None):
+def _raw_csv(src):
     if src.endswith(".csv"):        # already exported on the GPU box: ncu -i x.ncu-rep --page raw --csv > x.csv
-        txt = open(src).read()
-    else:
-        txt = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(txt.splitlines()))
-    hdr, units, data = rows[0], rows[1], rows[2:]
-    kn = hdr.index("Kernel Name")
-    stall = [(i, h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""))
-             for i, h in enumerate(hdr) if "smsp__average_warps_issue_stalled" in h and h.endswith("_per_issue_active.ratio")]
+        return open(src).read()
+    return subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+
+
+def full(srcs, dst, traffic_dst=None):
+    """``srcs``: one report / raw CSV or several separated by commas (each keeps its own unit row)."""
     seen, traffic = set(), {}
     with open(dst, "w") as f:
         f.write("# ncu --set full --clock-control none: key metrics per kernel (first captured launch of each)\n\n")
-        f.write("Source report: `%s` (not committed; regenerate with the command in profiles/README.md).\n\n" % src)
-        for r in data:
-            name = short(r[kn])
-            if name in seen:
-                continue
-            seen.add(name)
-            f.write("## `%s`\n\n| metric | value |\n|---|---|\n" % name)
-            vals = {}
-            for m, label in METRICS:
-                if m in hdr:
-                    i = hdr.index(m)
-                    vals[m] = r[i]
-                    f.write("| %s | %s %s |\n" % (label, r[i], units[i]))
-            top = sorted(((float(r[i]), h) for i, h in stall if r[i]), reverse=True)[:4]
-            f.write("| top stalls (warps per issue) | %s |\n\n" % ", ".join("%s %.2f" % (h, v) for v, h in top))
-            for key, stage in STAGE_OF:
-                if key in name and stage not in traffic and "dram__bytes_read.sum" in vals:
-                    def tobytes(m):
+        f.write("Source reports: `%s` (not committed; regenerate with the commands in profiles/README.md).\n\n" % srcs)
+        for src in srcs.split(","):
+            rows = list(csv.reader(_raw_csv(src).splitlines()))
+            hdr, units, data = rows[0], rows[1], rows[2:]
+            kn = hdr.index("Kernel Name")
+            stall = [(i, h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""))
+                     for i, h in enumerate(hdr) if "smsp__average_warps_issue_stalled" in h and h.endswith("_per_issue_active.ratio")]
+
+            def tobytes(r, m):
+                i = hdr.index(m)
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[i]]
+                return float(r[i].replace(",", "")) * scale
+            for r in data:
+                name = short(r[kn])
+                if name in seen:
+                    continue
+                seen.add(name)
+                f.write("## `%s`\n\n| metric | value |\n|---|---|\n" % name)
+                for m, label in METRICS:
+                    if m in hdr:
                         i = hdr.index(m)
-                        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[i]]
-                        return float(r[i].replace(",", "")) * scale
-                    traffic[stage] = tobytes("dram__bytes_read.sum") + tobytes("dram__bytes_write.sum")
+                        f.write("| %s | %s %s |\n" % (label, r[i], units[i]))
+                top = sorted(((float(r[i]), h) for i, h in stall if r[i]), reverse=True)[:4]
+                f.write("| top stalls (warps per issue) | %s |\n\n" % ", ".join("%s %.2f" % (h, v) for v, h in top))
+                for key, stage in STAGE_OF:
+                    if key in name and stage not in traffic and "dram__bytes_read.sum" in hdr:
+                        traffic[stage] = tobytes(r, "dram__bytes_read.sum") + tobytes(r, "dram__bytes_write.sum")
+                        break
     print("wrote", dst)
     if traffic_dst:
         json.dump(traffic, open(traffic_dst, "w"), indent=1, sort_keys=True)
