@@ -82,8 +82,11 @@ tri_prepare_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, 
 // stores are coalesced streams; the record gathers hit L1 because neighbours share owners.  The
 // next iteration's id is fetched before this iteration's arithmetic, and the whole record is loaded
 // before the first division (whose slow-path call would otherwise fence the remaining loads).
+#ifndef ML_RESOLVE_MINB
+#define ML_RESOLVE_MINB 4
+#endif
 template <bool SMALL>
-__global__ void __launch_bounds__(BLOCK, 2)
+__global__ void __launch_bounds__(BLOCK, ML_RESOLVE_MINB)
 resolve_kernel(const TriRec* __restrict__ recs, long long width, long long row0, long long n,
                const int* __restrict__ tri_id, float* __restrict__ pos, float* __restrict__ nrm,
                float* __restrict__ area, unsigned long long* covered) {
@@ -102,32 +105,36 @@ resolve_kernel(const TriRec* __restrict__ recs, long long width, long long row0,
             continue;
         }
         ++cnt;
+        // The 208-byte record is consumed in three rounds (uv vertices -> barycentrics, positions,
+        // normals), each fetched right before its arithmetic: the kernel then fits 64 registers and
+        // twice as many warps hide the float64 latency (the record's lines are in L1 after round 1).
         const double2* rp = (const double2*)(recs + tcur);
-        double2 w[13];
-#pragma unroll
-        for (int k = 0; k < 13; ++k) w[k] = __ldg(rp + k);
+        const double2 v0 = __ldg(rp), v1 = __ldg(rp + 1), v2 = __ldg(rp + 2), af = __ldg(rp + 3);
         int x, y;
         texel_xy(i, width, row0, SMALL, x, y);
-        const double x0 = w[0].x, y0 = w[0].y, x1 = w[1].x, y1 = w[1].y, x2 = w[2].x, y2 = w[2].y;
-        const double cx = xadd((double)x, 0.5), cy = xadd((double)y, 0.5);                    // KN:60, 63
-        const double e0 = xsub(xmul(xsub(x2, x1), xsub(cy, y1)), xmul(xsub(y2, y1), xsub(cx, x1)));   // KN:72
-        const double e1 = xsub(xmul(xsub(x0, x2), xsub(cy, y2)), xmul(xsub(y0, y2), xsub(cx, x2)));   // KN:73
-        const double e2 = xsub(xmul(xsub(x1, x0), xsub(cy, y0)), xmul(xsub(y1, y0), xsub(cx, x0)));   // KN:74
+        const double cx = xadd((double)x, 0.5), cy = xadd((double)y, 0.5);                            // KN:60, 63
+        const double e0 = xsub(xmul(xsub(v2.x, v1.x), xsub(cy, v1.y)), xmul(xsub(v2.y, v1.y), xsub(cx, v1.x)));   // KN:72
+        const double e1 = xsub(xmul(xsub(v0.x, v2.x), xsub(cy, v2.y)), xmul(xsub(v0.y, v2.y), xsub(cx, v2.x)));   // KN:73
+        const double e2 = xsub(xmul(xsub(v1.x, v0.x), xsub(cy, v0.y)), xmul(xsub(v1.y, v0.y), xsub(cx, v0.x)));   // KN:74
+        area[i] = __uint_as_float((uint32_t)__double_as_longlong(af.x));      // low word of bytes 48..55 = TriRec::area
         const double esum = xadd(xadd(e0, e1), e2);
         const double l0 = xdiv(e0, esum), l1 = xdiv(e1, esum), l2 = xdiv(e2, esum);
-        // attributes: w[4..8] = p[0..8] and nrm[0], w[8].y.. = nrm
-        const double a[18] = {w[4].x, w[4].y, w[5].x, w[5].y, w[6].x, w[6].y, w[7].x, w[7].y, w[8].x,
-                              w[8].y, w[9].x, w[9].y, w[10].x, w[10].y, w[11].x, w[11].y, w[12].x, w[12].y};
-        double nv[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            pos[c * n + i] = (float)xadd(xadd(xmul(l0, a[c]), xmul(l1, a[3 + c])), xmul(l2, a[6 + c]));
-            nv[c] = xadd(xadd(xmul(l0, a[9 + c]), xmul(l1, a[12 + c])), xmul(l2, a[15 + c]));
+        {   // positions: record words 4..8 = p0.xyz, p1.xyz, p2.xyz (+ nrm[0] in w8.y)
+            const double2 w4 = __ldg(rp + 4), w5 = __ldg(rp + 5), w6 = __ldg(rp + 6), w7 = __ldg(rp + 7), w8 = __ldg(rp + 8);
+            pos[i] = (float)xadd(xadd(xmul(l0, w4.x), xmul(l1, w5.y)), xmul(l2, w7.x));
+            pos[n + i] = (float)xadd(xadd(xmul(l0, w4.y), xmul(l1, w6.x)), xmul(l2, w7.y));
+            pos[2 * n + i] = (float)xadd(xadd(xmul(l0, w5.x), xmul(l1, w6.y)), xmul(l2, w8.x));
         }
-        const double len = __dsqrt_rn(xadd(xadd(xmul(nv[0], nv[0]), xmul(nv[1], nv[1])), xmul(nv[2], nv[2])));
-#pragma unroll
-        for (int c = 0; c < 3; ++c) nrm[c * n + i] = (len > 0.0) ? (float)xdiv(nv[c], len) : 0.f;
-        area[i] = __uint_as_float((uint32_t)__double_as_longlong(w[3].x));      // low word of bytes 48..55 = TriRec::area
+        // normals: record words 8.y .. 12 = n0.xyz, n1.xyz, n2.xyz
+        const double2 w8 = __ldg(rp + 8), w9 = __ldg(rp + 9), w10 = __ldg(rp + 10), w11 = __ldg(rp + 11), w12 = __ldg(rp + 12);
+        const double nx = xadd(xadd(xmul(l0, w8.y), xmul(l1, w10.x)), xmul(l2, w11.y));
+        const double ny = xadd(xadd(xmul(l0, w9.x), xmul(l1, w10.y)), xmul(l2, w12.x));
+        const double nz = xadd(xadd(xmul(l0, w9.y), xmul(l1, w11.x)), xmul(l2, w12.y));
+        const double len = __dsqrt_rn(xadd(xadd(xmul(nx, nx), xmul(ny, ny)), xmul(nz, nz)));
+        const bool ok = len > 0.0;
+        nrm[i] = ok ? (float)xdiv(nx, len) : 0.f;
+        nrm[n + i] = ok ? (float)xdiv(ny, len) : 0.f;
+        nrm[2 * n + i] = ok ? (float)xdiv(nz, len) : 0.f;
     }
     block_count_add(cnt, covered);
 }
