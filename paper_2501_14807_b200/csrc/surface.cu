@@ -510,24 +510,30 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
 // is cleared if the previous stroke marked it and streams its 8 row segments (8 independent 128-bit
 // id loads per lane) through tea_process.  The stroke therefore reads O(footprint) texels, not
 // O(atlas), and the listed tiles spread evenly over the grid wherever the footprint lies.
+#ifndef ML_TEA_TILE_MINB
+#define ML_TEA_TILE_MINB 3
+#endif
 template <typename T, int ES>
-__global__ void __launch_bounds__(BLOCK)
+__global__ void __launch_bounds__(BLOCK, ML_TEA_TILE_MINB)
 tea_tile_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
                 long long row0, long long rows, const int* __restrict__ tri_id,
                 const uint32_t* __restrict__ flags, TeaParams p, TeaWork wk, TeaCull cull,
                 void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
                 uint8_t* __restrict__ edited, unsigned long long* counters) {
-    constexpr int U = 1 << TILE_H_SHIFT;
+    constexpr int U = 4;                                   // a warp takes HALF a tile (4 of its 8 rows) per step:
+    constexpr int HALVES = (1 << TILE_H_SHIFT) / U;        // fewer registers, three blocks per SM
     long long newly = 0, frags = 0;
     const int lane = threadIdx.x & 31;
     const long long n = rows * width, nq = n >> 2;
     const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
     const int segs = cull.segs_per_row;
-    const long long ntiles = (long long)segs * ((rows + U - 1) >> TILE_H_SHIFT);
+    const long long ntiles = (long long)segs * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
     const TileBuf cur((uint32_t*)cull.tile_cur, ntiles), prev((uint32_t*)cull.tile_prev, ntiles);
     const long long ncur = (long long)*cur.count, nprev = cull.tile_prev ? (long long)*prev.count : 0;
     const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
-    for (long long j = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); j < ncur + nprev; j += nwarps) {
+    for (long long jj = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); jj < (ncur + nprev) * HALVES; jj += nwarps) {
+        const long long j = jj / HALVES;
+        const int half = (int)(jj - j * HALVES);
         const bool is_cur = j < ncur;
         const int tile = (int)(is_cur ? cur.list[j] : prev.list[j - ncur]);
         const bool in_prev = cull.tile_prev && tile_bit(prev.bits, tile);
@@ -536,7 +542,7 @@ tea_tile_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, lo
         long long qs[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const long long yy = ((long long)ty << TILE_H_SHIFT) + u;
+            const long long yy = ((long long)ty << TILE_H_SHIFT) + half * U + u;
             qs[u] = yy < rows ? ((yy * width + ((long long)tx << TILE_W_SHIFT)) >> 2) + lane : nq;
         }
         if (in_prev || !is_cur) {
@@ -636,8 +642,8 @@ int launch_tea_es(const T* tri_xy, const T* tri_clip, const TeaRec* recs, long l
     if (ES > 0 && cull.tile_cur) {
         const long long rows = n / width;
         const long long ntiles = (long long)cull.segs_per_row * ((rows + (1 << TILE_H_SHIFT) - 1) >> TILE_H_SHIFT);
-        long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);      // the lists are never longer than this
-        const long long cap = (long long)ml_sm_count() * 8;
+        long long blocks = (2 * ntiles + BLOCK / 32 - 1) / (BLOCK / 32);  // the lists are never longer than this (half tiles)
+        const long long cap = (long long)ml_sm_count() * 12;
         if (blocks > cap) blocks = cap;
         if (blocks < 1) blocks = 1;
         tea_tile_kernel<T, (ES > 0 ? ES : 1)><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, rows,
