@@ -1,0 +1,40 @@
+"""bench.py --impl reference runs on the CPU (the oracle's C restatement with OpenMP): smoke-run it at a
+tiny size and check the JSON contract of the line the driver parses (keys, types, the e2e and
+cpu_baseline objects); ranks other than 0 print nothing."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ARGS = ["--impl", "reference", "--steps", "2", "--warmup", "1", "--atlas", "256", "--cpu-rows", "64", "--quads", "24",
+        "--window", "96", "--layers", "4"]
+
+
+def _run(env_extra):
+    env = dict(os.environ, **env_extra)
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + ARGS, capture_output=True, text=True, env=env,
+                          timeout=600)
+
+
+def test_reference_arm_json_contract():
+    r = _run({})
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "Gtexel/s" and d["higher_is_better"] is True
+    assert d["metric"].startswith("brush-apply + layer-op") and d["scaling"] == "weak" and d["vs_baseline"] is None
+    assert d["steps"] == 2 and d["warmup"] == 1 and d["value"] > 0 and d["ms_per_step"] > 0
+    assert d["data"] == "synthetic" and "workload" in d["config"] and d["config"]["layers"] == 4
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and "rows" in cb["sample"]
+    assert set(cb["stage_ms"]) == {"tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area"}
+    e = d["e2e"]
+    assert e["value"] == d["value"] and e["unit"] == d["unit"]
+    assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+
+
+def test_reference_arm_other_ranks_are_silent():
+    r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert r.returncode == 0 and r.stdout.strip() == ""
