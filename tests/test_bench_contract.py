@@ -38,3 +38,33 @@ def test_reference_arm_json_contract():
 def test_reference_arm_other_ranks_are_silent():
     r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+import pytest
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", [[], ["--no-cull"]])
+def test_gpu_arm_json_contract(extra):
+    """bench.py (our arm) at a tiny atlas: one JSON line with every key of the contract."""
+    args = ["--steps", "3", "--warmup", "3", "--atlas", "512", "--cpu-rows", "64", "--quads", "48", "--window", "128",
+            "--layers", "4"] + extra
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["value"] > 0 and d["vs_baseline"] is None
+    ro = d["roofline"]
+    assert ro["bound"] == "hbm" and ro["unit"] == "GB/s" and ro["peak"] > 0 and abs(ro["frac"] - ro["achieved"] / ro["peak"]) < 1e-9
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["unit"] == d["unit"]
+    per_step = 12 if not extra else 10
+    assert d["gpu_launches"] == per_step * 3
+    assert set(d["config"]["stage_results"]) == {"tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area"}
+    assert d["config"]["footprint_culling"] == (not extra)
+    assert ("stream_kernels" in d["config"]) and (bool(d["config"]["stream_kernels"]) == (not extra))
