@@ -94,6 +94,11 @@ int ml_raster_tea(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
 int ml_raster_tri_id(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
                      int64_t row0, int64_t rows, int32_t* tri_id, uint64_t* counters,
                      void* workspace, size_t workspace_bytes, void* stream);
+/* SPEC:129-137 rasterize with a per-triangle output: out[i] = values[tri_id[i]] for every covered
+ * texel whose owner triangle is kept (keep == NULL or keep[t] != 0); other texels are not touched.
+ * values: [ntri] elements of esize bytes; *written (device, zeroed) += texels written. */
+int ml_owner_values(const int32_t* tri_id, int64_t n, const void* values, const uint8_t* keep, int esize,
+                    void* out, uint64_t* written, void* stream);
 /* Pass 2: per texel, interpolate the owner triangle's attributes.  pos / nrm are three float32
  * planes each (plane stride = rows*width elements), area one float32 plane.  Uncovered texels:
  * pos = NaN, nrm = 0, area = 0.  tri_pos / tri_nrm [ntri][3][3].  *covered (device, zeroed)

@@ -4,7 +4,7 @@ Drop-in surface
   * ``_native``  -- kernel backend with the reference's ``_kernels_numpy`` signatures
                     (``coverage_fill``, ``raster_depth``, ``raster_tea``), backed by
                     ``libmeshlayers_b200.so`` (C ABI: ``include/meshlayers_b200.h``).
-  * SPEC operation names: ``pool_acquire``, ``create_layer``, ``uv_coverage``, ``render_depth``,
+  * SPEC operation names: ``pool_acquire``, ``rasterize``, ``create_layer``, ``uv_coverage``, ``render_depth``,
     ``compute_tool_projection``, ``project_fragment``, ``apply_stroke``, ``build_outline_mask``,
     ``apply_padding``, ``mesh_surface_area``.
 Extensions named by the north star (not in the reference): ``build_surface_map``,
@@ -19,7 +19,7 @@ from . import errors
 from .errors import *  # noqa: F401,F403
 from .mesh_core import (Camera, DepthMap, SurfaceMap, TriangleMesh, build_surface_map,
                         mesh_surface_area, render_depth, uv_coverage)
-from .raster_device import TexturePool, default_pool, pool_acquire
+from .raster_device import TexturePool, default_pool, pool_acquire, rasterize
 from .layer_core import (InformationLayer, create_layer, label_area, layer_area, layer_chain,
                          layer_difference, layer_intersection, layer_mask, layer_precision,
                          layer_stats, layer_union, layers_area)

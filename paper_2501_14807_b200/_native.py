@@ -84,6 +84,7 @@ def lib():
         "ml_raster_tri_id": (i32, [vp, i32, i64, i64, i64, i64, i64, vp, vp, vp, sz, vp]),
         "ml_surface_resolve": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp]),
         "ml_surface_workspace_bytes": (sz, [i64]),
+        "ml_owner_values": (i32, [vp, i64, vp, vp, i32, vp, vp, vp]),
         "ml_tea_texels": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
                                 vp, vp, i64, vp, i32, u32, vp, vp, vp, vp]),
         "ml_tea_classify_recs": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
@@ -129,7 +130,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve",
-    "ml_surface_workspace_bytes", "ml_tea_texels", "ml_tea_rec_bytes", "ml_tea_prepare",
+    "ml_surface_workspace_bytes", "ml_owner_values", "ml_tea_texels", "ml_tea_rec_bytes", "ml_tea_prepare",
     "ml_tea_classify_recs", "ml_stroke",
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
@@ -475,6 +476,21 @@ def raster_tri_id(tri_xy, width, height, *, row0=0, rows=None, device=None):
                                   _ptr(ctr), _ptr(ws), nb, _stream()))
     fragments = int(ctr[0].item())
     return tri_id, fragments, fragments - int((tri_id >= 0).sum().item())       # overlap = fragments - covered
+
+
+def owner_values(tri_id, values, out, keep=None):
+    """out[texel] = values[owner triangle] for covered texels (optionally only kept triangles).
+    Returns the number of texels written."""
+    torch = require_cuda()
+    if tuple(tri_id.shape) != tuple(out.shape) or not out.is_contiguous():
+        raise TargetMismatch("target plane does not match the triangle-id map")
+    esize = _np_dtype_of(out).itemsize
+    if _np_dtype_of(values).itemsize != esize or not values.is_contiguous():
+        raise TargetMismatch("per-triangle values must have the target's element kind")
+    ctr = _counters(1, tri_id.device)
+    _check(lib().ml_owner_values(_ptr(tri_id), tri_id.numel(), _ptr(values), _ptr(keep), esize, _ptr(out), _ptr(ctr),
+                                 _stream()))
+    return int(ctr[0].item())
 
 
 def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,

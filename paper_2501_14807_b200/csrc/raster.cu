@@ -331,6 +331,24 @@ raster_chunk_kernel(const T* __restrict__ tri_xy, long long width, long long hei
     block_count_add(c1, counters + 1);
 }
 
+// SPEC.md:129-137 ``rasterize`` with a per-triangle output value: after the owner pass (last triangle
+// in submission order wins) every covered texel takes its owner's value unless the rule
+// discarded that triangle.  4 texels per thread (128-bit id load), 1 / 2 / 4-byte elements.
+template <typename E>
+__global__ void __launch_bounds__(BLOCK)
+owner_values_kernel(const int* __restrict__ tri_id, long long n, const E* __restrict__ values,
+                    const uint8_t* __restrict__ keep, E* __restrict__ out, unsigned long long* written) {
+    long long cnt = 0;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    for (long long i = (long long)blockIdx.x * BLOCK + threadIdx.x; i < n; i += nthreads) {
+        const int t = tri_id[i];
+        if (t < 0 || (keep && keep[t] == 0)) continue;
+        out[i] = values[t];
+        ++cnt;
+    }
+    block_count_add(cnt, written);
+}
+
 template <typename T, typename F>
 int raster_launch(const T* tri_xy, long long ntri, long long width, long long height,
                   long long row0, long long rows, const F& f, void* workspace, size_t ws_bytes,
@@ -396,6 +414,22 @@ int ml_raster_tri_id(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t wi
     if (tri_dtype == ML_F64)
         return raster_launch((const double*)tri_xy, ntri, width, height, row0, rows, f, workspace, workspace_bytes, ctr, st);
     return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+}
+
+int ml_owner_values(const int32_t* tri_id, int64_t n, const void* values, const uint8_t* keep, int esize,
+                    void* out, uint64_t* written, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) return ML_OK;
+    long long blocks = (n + BLOCK - 1) / BLOCK;
+    const long long cap = (long long)ml_sm_count() * 32;
+    if (blocks > cap) blocks = cap;
+    unsigned long long* w = (unsigned long long*)written;
+    if (esize == 1) owner_values_kernel<uint8_t><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_id, n, (const uint8_t*)values, keep, (uint8_t*)out, w);
+    else if (esize == 2) owner_values_kernel<uint16_t><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_id, n, (const uint16_t*)values, keep, (uint16_t*)out, w);
+    else if (esize == 4) owner_values_kernel<uint32_t><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_id, n, (const uint32_t*)values, keep, (uint32_t*)out, w);
+    else return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
 }
 
 int ml_raster_depth(const void* tri_xy, const void* tri_zn, int tri_dtype, int64_t ntri,

@@ -128,23 +128,17 @@ class StrokeContext:
         self.device = device
         self._cstruct = None              # (outline data_ptr, ml_stroke_ctx) of the one-call stroke path
 
+    def begin_culled_stroke(self):
+        """Footprint-culled strokes clear the edited plane per footprint; after a whole-plane stroke
+        the plane and the "previous" tile buffer are reset once."""
+        if self.edited_fully_dirty:
+            self.edited.zero_()
+            self.tiles[self.cur ^ 1].zero_()
+            self.edited_fully_dirty = False
 
-def _begin_culled_stroke(self):
-    """Footprint-culled strokes clear the edited plane per footprint; after a whole-plane stroke the
-    plane and the "previous" tile buffer are reset once."""
-    if self.edited_fully_dirty:
-        self.edited.zero_()
-        self.tiles[self.cur ^ 1].zero_()
-        self.edited_fully_dirty = False
-
-
-def _end_culled_stroke(self):
-    self.stroke_tiles = self.tiles[self.cur]      # footprint of the marks now in ctx.edited (for TPA)
-    self.cur ^= 1                                  # this stroke's footprint is the next one's "previous"
-
-
-StrokeContext.begin_culled_stroke = _begin_culled_stroke
-StrokeContext.end_culled_stroke = _end_culled_stroke
+    def end_culled_stroke(self):
+        self.stroke_tiles = self.tiles[self.cur]      # footprint of the marks now in ctx.edited (for TPA)
+        self.cur ^= 1                                  # this stroke's footprint is the next one's "previous"
 
 
 def _stroke_checks(ctx, layer):

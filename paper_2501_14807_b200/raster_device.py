@@ -102,3 +102,34 @@ def default_pool():
 def pool_acquire(width, height, kind, pool=None):
     """Module-level spelling of SPEC.md:120."""
     return (pool or default_pool()).acquire(width, height, kind)
+
+
+def rasterize(tri_xy, targets, values, keep=None):
+    """SPEC.md:129-137 ``rasterize`` for the fragment rules a device backend can take without a
+    host callback: every texel whose centre lies inside a triangle (top-left rule, RasterRules) is
+    offered to the rule "triangle t keeps its fragments iff keep[t], and writes values[k][t] into
+    target k"; writes are atomic per texel and the last triangle in submission order wins on overlap
+    (SPEC.md:132).  ``tri_xy`` (T,3,2) in texel units; ``targets`` a list of plane handles / CUDA
+    tensors sharing dimensions; ``values`` one scalar or (T,) array per target; ``keep`` an optional
+    (T,) bool array ("always discard" = all False).  Returns the count of written texels."""
+    torch = _native.require_cuda()
+    planes = [t.tensor if isinstance(t, PlaneHandle) else t for t in targets]
+    if not planes:
+        return 0
+    shape = tuple(planes[0].shape[:2])
+    if any(tuple(p.shape[:2]) != shape for p in planes):
+        raise TargetMismatch("targets disagree in dimensions")                       # SPEC.md:133
+    import numpy as np
+    T = int(tri_xy.shape[0])
+    tri_id, _, _ = _native.raster_tri_id(tri_xy, shape[1], shape[0], device=planes[0].device)
+    if T == 0:
+        return 0
+    dev = planes[0].device
+    keep_dev = None if keep is None else _native._as_dev_bytes(np.asarray(keep).astype(np.uint8), dev)
+    written = 0
+    for plane, vals in zip(planes, values):
+        dt = _native._np_dtype_of(plane)
+        v = np.broadcast_to(np.asarray(vals).astype(dt), (T,)).copy()
+        vt = torch.from_numpy(v.view({1: np.uint8, 2: np.int16, 4: np.int32}[dt.itemsize])).to(dev)
+        written = _native.owner_values(tri_id, vt, plane, keep_dev)
+    return written

@@ -402,3 +402,32 @@ def test_layer_algebra_and_area_api():
     assert (cnt, mn, mx) == (nu, 3.0, 5.0) and s == 3.0 * na + 5.0 * (nu - na)
     with pytest.raises(ml.TargetMismatch):
         ml.layer_union(a, ml.create_layer("small", "uint8", 64, 64, pool=pool))
+
+
+def test_rasterize_known_answers():
+    """rule "always keep, write 7" fills exactly the covered centres; "always
+    discard" writes nothing; two overlapping triangles writing 1 then 2 leave 2 on the overlap; targets
+    of different dimensions raise TargetMismatch."""
+    import torch
+    pool = ml.TexturePool()
+    tri = np.array([[[1.0, 1.0], [3.2, 1.0], [1.0, 3.2]]])                         # covers centres (1,1), (2,1), (1,2)
+    a = pool.acquire(6, 6, "uint8")
+    assert ml.rasterize(tri, [a], [7]) == 3
+    got = a.tensor.cpu().numpy()
+    want = np.zeros((6, 6), np.uint8); want[1, 1] = want[1, 2] = want[2, 1] = 7     # [row=y, col=x]
+    assert np.array_equal(got, want)
+    ref = np.zeros((6, 6), np.uint8)
+    assert kn.coverage_fill(tri, 6, 6, ref) == 3 and np.array_equal(ref * 7, want)
+    b = pool.acquire(6, 6, "int16")
+    assert ml.rasterize(tri, [b], [5], keep=[False]) == 0 and not bool(b.tensor.any())          # always discard
+    two = np.array([[[0.0, 0.0], [5.0, 0.0], [0.0, 5.0]], [[1.0, 1.0], [6.0, 1.0], [1.0, 6.0]]])
+    c, d = pool.acquire(6, 6, "uint8"), pool.acquire(6, 6, "float32")
+    n = ml.rasterize(two, [c, d], [np.array([1, 2]), np.array([0.5, 0.25])])
+    r1, r2 = np.zeros((6, 6), np.uint8), np.zeros((6, 6), np.uint8)
+    kn.coverage_fill(two[:1], 6, 6, r1); kn.coverage_fill(two[1:], 6, 6, r2)
+    exp = np.where(r2 != 0, 2, r1).astype(np.uint8)                                # submission order: 2 wins on overlap
+    assert n == int((exp != 0).sum()) and np.array_equal(c.tensor.cpu().numpy(), exp)
+    assert np.array_equal(d.tensor.cpu().numpy(), np.where(exp == 2, 0.25, np.where(exp == 1, 0.5, 0.0)).astype(np.float32))
+    with pytest.raises(ml.TargetMismatch):
+        ml.rasterize(tri, [a, pool.acquire(8, 6, "uint8")], [1, 1])
+    assert ml.rasterize(np.zeros((0, 3, 2)), [a], [1]) == 0
