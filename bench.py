@@ -10,8 +10,9 @@ One STEP = one pass of every hot-path stage over this rank's 16384 x 16384 atlas
     tpa        the paper's padding pass (TPA): outline texels next to the stroke
     sphere     one sphere-brush stroke over the float32x3 position map
     batch      L sphere strokes (one per layer) batched in ONE pass over the position map
-               (these four brush stages run the public API's default footprint-culled kernels: a
-               stroke reads only the tiles it can reach; ``--no-cull`` streams the whole atlas, and
+               (the brush / selection stages tea, tpa, sphere, batch and threshold run the
+               footprint-culled kernels: a stroke reads only the tiles it can reach, the threshold
+               only tiles whose height range meets the window; ``--no-cull`` streams the whole atlas, and
                the whole-atlas streaming kernels are ALSO timed on their own and reported under
                ``config.stream_kernels`` -- they are the brush kernels' HBM-roofline evidence)
     chain      fused layer-algebra chain ((L0 u L1) n L2) \\ L3 ... over 8 uint8 layers (C3)
@@ -332,6 +333,7 @@ def run_ours(args):
         ml.select_sphere(surf, layers[k % L], wl.seed_strokes[k, :3], wl.seed_strokes[k, 3], wl.seed_labels[k],
                          edited=edited[k % L])
     attr = surf.pos[2]
+    attr_tiles = nat.attr_tiles(attr)              # per-tile height ranges for the culled threshold selection
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     T = wl.mesh.num_triangles
@@ -341,7 +343,7 @@ def run_ours(args):
     counts1 = torch.zeros(1, dtype=torch.int64, device=dev)
     culled = not args.no_cull and surf.tiles is not None
     launches = {"tea": 3, "tpa": 1, "sphere": 2 if culled else 1, "batch": 2 if culled else 1, "chain": 1, "mask_op": 1,
-                "threshold": 1, "area": -(-L // 8)}
+                "threshold": 2 if (culled and attr_tiles is not None) else 1, "area": -(-L // 8)}
 
     def stage_call(st, inp, tool, mode, cull=not args.no_cull):
         """Run one stage through the public API and return its result as DEVICE tensors (nothing
@@ -379,7 +381,8 @@ def run_ours(args):
         elif st == "mask_op":
             nat.layer_op("union", None, layers[0].mask, None, layers[1 % L].mask, None, tmp_mask)
         elif st == "threshold":
-            out = [ml.select_threshold(attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L])._counts]
+            out = [ml.select_threshold(attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L],
+                                       tiles=attr_tiles if cull else None)._counts]
         elif st == "area":
             area_sums.zero_()
             area_counts.zero_()
@@ -482,7 +485,7 @@ def run_ours(args):
     stream_info = {}
     if not args.no_cull:
         reps = max(5, min(20, args.steps))
-        for st in [s for s in ("tea", "tpa", "sphere", "batch") if s in stages]:
+        for st in [s for s in ("tea", "tpa", "sphere", "batch", "threshold") if s in stages]:
             ms_acc = 0.0
             for k in range(reps + 2):
                 inp = inputs[args.warmup + (k % args.steps)]
@@ -510,7 +513,7 @@ def run_ours(args):
         stage_info[st] = {"ms": round(stage_ms[st], 4), "gtexel_s": round(n / (stage_ms[st] * 1e-3) / 1e9, 2),
                           "alg_bytes": b, "gb_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
                           "hits_per_step": int(hits[st]), "launches": launches[st]}
-        if st in ("tea", "tpa", "sphere", "batch"):
+        if st in ("tea", "tpa", "sphere", "batch", "threshold"):
             stage_info[st]["footprint_culled"] = not args.no_cull
     peak_now = peak
     stream_kernels = {st: {"ms": round(ms, 4), "gb_s": round(wl.algorithmic_bytes(n, st, T, hits[st]) / (ms * 1e-3) / 1e9, 1),

@@ -209,6 +209,17 @@ int ml_select_threshold(const void* attr, int attr_kind, const uint8_t* valid, i
                         double lo, double hi, void* data, int esize, uint32_t value_bits,
                         uint8_t* mask, uint8_t* edited, uint64_t* count, void* stream);
 
+/* Footprint-culled threshold selection for a float32 attribute plane that does not change between
+ * selections (geometry-derived attributes such as height): ml_plane_tile_range writes [min, max] of the
+ * non-NaN values per 128 x 4-texel tile (ranges [ntiles][2] float32, once per plane);
+ * ml_select_threshold_tiles then reads only tiles whose range meets [lo, hi] (exact float test, no
+ * margin needed) -- same planes and count as ml_select_threshold.  Scratch: ml_tile_workspace_bytes. */
+int ml_plane_tile_range(const float* attr, int64_t width, int64_t rows, float* ranges, void* stream);
+int ml_select_threshold_tiles(const float* attr, const uint8_t* valid, int64_t width, int64_t rows,
+                              const float* ranges, void* workspace, size_t workspace_bytes,
+                              double lo, double hi, void* data, int esize, uint32_t value_bits,
+                              uint8_t* mask, uint8_t* edited, uint64_t* count, void* stream);
+
 /* ---- layer algebra (north star (3); definition: ext_layer_op) ---------------------------------
  * (dc, mc) = (da, ma) op (db, mb) over n texels; mask bytes are true iff non-zero, output mask
  * bytes are exactly 0/1.  Data planes may all be NULL (esize 0, mask-only algebra: 3 B/texel).

@@ -103,6 +103,8 @@ def lib():
         "ml_select_sphere_batch_tiles": (i32, [vp, i64, i64, i64, vp, vp, sz, vp, vp, vp, i64, vp, vp, vp, i64,
                                                i32, vp, vp]),
         "ml_select_threshold": (i32, [vp, i32, vp, i64, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
+        "ml_plane_tile_range": (i32, [vp, i64, i64, vp, vp]),
+        "ml_select_threshold_tiles": (i32, [vp, vp, i64, i64, vp, vp, sz, dbl, dbl, vp, i32, u32, vp, vp, vp, vp]),
         "ml_layer_op": (i32, [i32, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
         "ml_layer_chain": (i32, [i64, vp, vp, vp, vp, vp, i32, i64, vp]),
         "ml_layer_area": (i32, [vp, vp, i64, i64, vp, vp, vp]),
@@ -134,7 +136,7 @@ EXPORTED_SYMBOLS = (
     "ml_tea_classify_recs", "ml_stroke",
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
-    "ml_select_threshold", "ml_layer_op",
+    "ml_select_threshold", "ml_plane_tile_range", "ml_select_threshold_tiles", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_apply_padding_tiles", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
     "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
@@ -742,9 +744,37 @@ def select_sphere_batch(pos, batch, *, tiles=None):
                                         _ptr(batch.counts), _stream()))
 
 
-def select_threshold(attr, valid, lo, hi, data, mask, edited, value, *, counts=None):
+class AttrTiles:
+    """[min, max] of a float32 attribute plane per 128 x 4-texel tile plus the tile-list scratch of
+    the culled threshold selection.  Valid while the plane's contents do not change."""
+
+    def __init__(self, attr, ranges, scratch, nbytes):
+        self.attr_ptr, self.shape = attr.data_ptr(), tuple(attr.shape)
+        self.ranges, self.scratch, self.nbytes = ranges, scratch, nbytes
+
+
+def attr_tiles(attr):
+    """Per-tile value ranges of a (rows, width) float32 plane; None when the layout has no tiles
+    (width % 128 != 0, unaligned) or the plane is not float32."""
+    torch = require_cuda()
+    L = lib()
+    if attr.dtype != torch.float32 or attr.dim() != 2 or not attr.is_contiguous() or attr.data_ptr() % 16:
+        return None
+    rows, width = int(attr.shape[0]), int(attr.shape[1])
+    nt = int(L.ml_tile_count(width, rows))
+    if nt == 0 or (rows * width) % 4:
+        return None
+    ranges = torch.empty((nt, 2), dtype=torch.float32, device=attr.device)
+    _check(L.ml_plane_tile_range(_ptr(attr), width, rows, _ptr(ranges), _stream()))
+    nb = int(L.ml_tile_workspace_bytes(width, rows))
+    return AttrTiles(attr, ranges, torch.empty(nb, dtype=torch.uint8, device=attr.device), nb)
+
+
+def select_threshold(attr, valid, lo, hi, data, mask, edited, value, *, counts=None, tiles=None):
     """Attribute-threshold selection: lo <= attr <= hi (closed) where ``valid`` (byte plane or
-    None) is non-zero.  Returns newly edited texels."""
+    None) is non-zero.  Returns newly edited texels.  ``tiles`` (``attr_tiles(attr)``, for planes that
+    do not change between selections) restricts the pass to tiles whose value range meets
+    [lo, hi]; same planes and count."""
     require_cuda()
     n = attr.numel()
     name = _np_dtype_of(attr).name
@@ -757,9 +787,16 @@ def select_threshold(attr, valid, lo, hi, data, mask, edited, value, *, counts=N
             raise TargetMismatch("valid plane does not match the attribute plane")
     bits, esize = value_bits(value, data)
     ctr = counts if counts is not None else _counters(1, attr.device)
-    _check(lib().ml_select_threshold(_ptr(attr), KIND_CODES[name], _ptr(valid), n, float(lo), float(hi),
-                                     _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr),
-                                     _stream()))
+    culled = (tiles is not None and tiles.attr_ptr == attr.data_ptr() and tiles.shape == tuple(attr.shape)
+              and all(t.data_ptr() % 16 == 0 for t in (data, mask, edited)) and (valid is None or valid.data_ptr() % 4 == 0))
+    if culled:
+        _check(lib().ml_select_threshold_tiles(_ptr(attr), _ptr(valid), int(attr.shape[1]), int(attr.shape[0]),
+                                               _ptr(tiles.ranges), _ptr(tiles.scratch), tiles.nbytes, float(lo), float(hi),
+                                               _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr), _stream()))
+    else:
+        _check(lib().ml_select_threshold(_ptr(attr), KIND_CODES[name], _ptr(valid), n, float(lo), float(hi),
+                                         _ptr(data), esize, bits, _ptr(mask), _ptr(edited), _ptr(ctr),
+                                         _stream()))
     return None if counts is not None else int(ctr[0].item())
 
 

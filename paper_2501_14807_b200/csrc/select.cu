@@ -443,6 +443,106 @@ threshold_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ val
     block_count_add(cnt, counter);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Footprint-culled threshold selection for float32 attribute planes that do not change between
+// selections (geometry-derived attributes such as height = pos.z): the plane carries its [min, max]
+// per 128 x 4-texel tile (ml_plane_tile_range, NaN = "no value" dropped).  The tile test is exact in
+// the attribute's own domain -- a texel hits iff lo_f <= v <= hi_f with the inward-rounded float
+// thresholds of launch_threshold, so a tile with max < lo_f or min > hi_f holds no hit -- and kept
+// tiles run the per-texel test and write rule of threshold_kernel.
+__global__ void __launch_bounds__(BLOCK)
+tile_range_kernel(const float* __restrict__ attr, TileGrid g, float2* __restrict__ ranges) {
+    const int lane = threadIdx.x & 31;
+    const float inf = __int_as_float(0x7f800000);
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    for (long long tile = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); tile < g.ntiles; tile += nwarps) {
+        float lo = inf, hi = -inf;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long q = tile_quad(g, tile, u, lane);
+            if (q < 0) continue;
+            const float4 v = ld_stream((const float4*)attr + q);
+            lo = fminf(lo, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));      // fminf / fmaxf drop NaNs
+            hi = fmaxf(hi, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) ranges[tile] = make_float2(lo, hi);
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK)
+range_classify_kernel(const float2* __restrict__ ranges, long long ntiles, float lo_f, float hi_f, TileList list) {
+    const long long tile = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    bool keep = false;
+    if (tile < ntiles) {
+        const float2 r = __ldg(ranges + tile);
+        keep = (r.x <= r.y) && !(r.y < lo_f) && !(r.x > hi_f);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (bal == 0) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(list.count, (unsigned long long)__popc(bal));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (keep) list.tiles[slot + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)tile;
+}
+
+template <int ES>
+__global__ void __launch_bounds__(BLOCK, 4)
+threshold_tiles_kernel(const float* __restrict__ attr, const uint8_t* __restrict__ valid, TileGrid g, TileList list,
+                       Thr thr, void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                       uint8_t* __restrict__ edited, unsigned long long* counter) {
+    long long cnt = 0;
+    const int lane = threadIdx.x & 31;
+    const long long count = (long long)*list.count;
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    for (long long j = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); j < count; j += nwarps) {
+        const long long tile = list.tiles[j];
+        long long q[4];
+        float4 a[4];
+        uint32_t vm[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            q[u] = tile_quad(g, tile, u, lane);
+            if (q[u] >= 0) {
+                a[u] = ld_stream((const float4*)attr + q[u]);
+                vm[u] = valid ? ld_stream((const uint32_t*)valid + q[u]) : 0x01010101u;
+            }
+        }
+        unsigned hits[4];
+        uint32_t ew[4], mw[4], dw[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            hits[u] = 0;
+            if (q[u] < 0) continue;
+            const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if ((((vm[u] >> (8 * e)) & 0xffu) != 0) && AttrT<ML_FLOAT32>::hit(v[e], thr)) hits[u] |= 1u << e;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) quad_load<ES>(data, mask, edited, q[u] << 2, hits[u], ew[u], mw[u], dw[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) quad_commit<ES>(data, value, mask, edited, q[u] << 2, hits[u], ew[u], mw[u], dw[u], cnt);
+    }
+    block_count_add(cnt, counter);
+}
+
+// thresholds rounded inward once, in every attribute domain; false for an empty or NaN interval
+inline bool make_thr(double lo, double hi, Thr& thr) {
+    if (!(lo <= hi)) return false;
+    thr.lo_f = (float)lo; if ((double)thr.lo_f < lo) thr.lo_f = nextafterf(thr.lo_f, INFINITY);
+    thr.hi_f = (float)hi; if ((double)thr.hi_f > hi) thr.hi_f = nextafterf(thr.hi_f, -INFINITY);
+    const double big = 9.2e18;
+    thr.lo_i = lo <= -big ? LLONG_MIN : (lo >= big ? LLONG_MAX : (long long)ceil(lo));
+    thr.hi_i = hi >= big ? LLONG_MAX : (hi <= -big ? LLONG_MIN : (long long)floor(hi));
+    return true;
+}
+
 inline unsigned stream_grid(long long items_per_thread_iter, long long n_items) {
     long long blocks = (n_items + (long long)BLOCK * items_per_thread_iter - 1) / ((long long)BLOCK * items_per_thread_iter);
     const long long cap = (long long)ml_sm_count() * 16;
@@ -461,13 +561,8 @@ int launch_threshold(const void* attr, const uint8_t* valid, long long n, double
     typedef typename AttrT<KIND>::T T;
     const bool vec = aligned(attr, sizeof(T) * 4) && (!valid || aligned(valid, 4)) && planes_aligned(data, mask, edited);
     const unsigned grid = stream_grid(4 * TU, n);
-    if (!(lo <= hi)) return ML_OK;             // empty or NaN interval: nothing can hit
     Thr thr;
-    thr.lo_f = (float)lo; if ((double)thr.lo_f < lo) thr.lo_f = nextafterf(thr.lo_f, INFINITY);
-    thr.hi_f = (float)hi; if ((double)thr.hi_f > hi) thr.hi_f = nextafterf(thr.hi_f, -INFINITY);
-    const double big = 9.2e18;
-    thr.lo_i = lo <= -big ? LLONG_MIN : (lo >= big ? LLONG_MAX : (long long)ceil(lo));
-    thr.hi_i = hi >= big ? LLONG_MAX : (hi <= -big ? LLONG_MIN : (long long)floor(hi));
+    if (!make_thr(lo, hi, thr)) return ML_OK;  // empty or NaN interval: nothing can hit
 #define ML_LAUNCH_THR(ES) threshold_kernel<KIND, ES><<<grid, BLOCK, 0, st>>>(attr, valid, n, lo, hi, thr, data, esize, value, mask, edited, counter)
     if (!vec) ML_LAUNCH_THR(0);
     else if (esize == 1) ML_LAUNCH_THR(1);
@@ -617,6 +712,50 @@ int ml_select_sphere_batch_tiles(const float* pos, int64_t pos_stride, int64_t w
     if (esize == 1) sphere_batch_tiles_kernel<1><<<grid, BLOCK, 0, st>>>(a, g, (const float4*)boxes, list);
     else if (esize == 2) sphere_batch_tiles_kernel<2><<<grid, BLOCK, 0, st>>>(a, g, (const float4*)boxes, list);
     else sphere_batch_tiles_kernel<4><<<grid, BLOCK, 0, st>>>(a, g, (const float4*)boxes, list);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_plane_tile_range(const float* attr, int64_t width, int64_t rows, float* ranges, void* stream) {
+    const long long ntiles = ml_tile_count(width, rows);
+    if (ntiles == 0) return ml_fail(ML_ERR_ARG, "tile ranges need width % 128 == 0");
+    if (!aligned(attr, 16) || !aligned(ranges, 8)) return ml_fail(ML_ERR_ARG, "tile ranges need a 16-byte aligned plane");
+    long long blocks = (ntiles + BLOCK / 32 - 1) / (BLOCK / 32);
+    const long long cap = (long long)ml_sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    tile_range_kernel<<<(unsigned)blocks, BLOCK, 0, (cudaStream_t)stream>>>(attr, tile_grid(width, rows), (float2*)ranges);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_select_threshold_tiles(const float* attr, const uint8_t* valid, int64_t width, int64_t rows,
+                              const float* ranges, void* workspace, size_t workspace_bytes,
+                              double lo, double hi, void* data, int esize, uint32_t value_bits,
+                              uint8_t* mask, uint8_t* edited, uint64_t* count, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
+    if (width <= 0 || rows <= 0) return ML_OK;
+    if (ml_tile_count(width, rows) == 0) return ml_fail(ML_ERR_ARG, "culled threshold needs width % 128 == 0");
+    if (ranges == nullptr || !aligned(ranges, 8) || !aligned(attr, 16) || (valid && !aligned(valid, 4)) ||
+        !planes_aligned(data, mask, edited))
+        return ml_fail(ML_ERR_ARG, "culled threshold needs the tile ranges and 16-byte aligned planes");
+    if (workspace == nullptr || workspace_bytes < ml_tile_workspace_bytes(width, rows) || !aligned(workspace, 8))
+        return ml_fail(ML_ERR_ARG, "culled threshold needs ml_tile_workspace_bytes() of 8-byte aligned scratch");
+    Thr thr;
+    if (!make_thr(lo, hi, thr)) return ML_OK;
+    const TileGrid g = tile_grid(width, rows);
+    TileList list;
+    list.count = (unsigned long long*)workspace;
+    list.bits = (uint32_t*)(list.count + 2);
+    list.tiles = list.bits + tile_bitmap_words(g.ntiles);
+    ML_CUDA(cudaMemsetAsync(workspace, 0, 16, st));
+    range_classify_kernel<<<(unsigned)((g.ntiles + BLOCK - 1) / BLOCK), BLOCK, 0, st>>>((const float2*)ranges, g.ntiles,
+                                                                                       thr.lo_f, thr.hi_f, list);
+    const unsigned grid = (unsigned)(ml_sm_count() * 16);
+    unsigned long long* c = (unsigned long long*)count;
+    if (esize == 1) threshold_tiles_kernel<1><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c);
+    else if (esize == 2) threshold_tiles_kernel<2><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c);
+    else threshold_tiles_kernel<4><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

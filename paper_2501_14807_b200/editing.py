@@ -262,15 +262,18 @@ def select_sphere_batch(surface, batch, *, cull=True):
     return batch.counts
 
 
-def select_threshold(attr, valid, lo, hi, layer, value, edited=None):
-    """Attribute-threshold selection into ``layer`` (definition: oracle ext_select_threshold)."""
+def select_threshold(attr, valid, lo, hi, layer, value, edited=None, *, tiles=None):
+    """Attribute-threshold selection into ``layer`` (definition: oracle ext_select_threshold).
+    ``tiles`` = ``_native.attr_tiles(attr)`` of a float32 attribute plane that does not change between
+    selections (e.g. the surface map's height plane): only tiles whose value range meets [lo, hi]
+    are read (identical result)."""
     torch = _native._torch()
     if tuple(attr.shape) != layer.shape:
         raise TargetMismatch("attribute plane does not match the layer")
     if edited is None:
         edited = torch.zeros(layer.shape, dtype=torch.uint8, device=attr.device)
     counts = torch.zeros(1, dtype=torch.int64, device=attr.device)
-    _native.select_threshold(attr, valid, lo, hi, layer.data, layer.mask, edited, value, counts=counts)
+    _native.select_threshold(attr, valid, lo, hi, layer.data, layer.mask, edited, value, counts=counts, tiles=tiles)
     return EditResult(edited_mask=edited, _counts=counts, transfer_bytes=24)
 
 

@@ -63,7 +63,7 @@ def test_gpu_arm_json_contract(extra):
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] > 0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0 and e["unit"] == d["unit"]
-    per_step = 12 if not extra else 10
+    per_step = 13 if not extra else 10
     assert d["gpu_launches"] == per_step * 3
     assert set(d["config"]["stage_results"]) == {"tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area"}
     assert d["config"]["footprint_culling"] == (not extra)

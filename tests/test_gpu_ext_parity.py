@@ -537,3 +537,39 @@ def test_classification_from_bounds_is_a_superset():
             assert not (a & ~b).any(), (dt, k)
             kept0 = int(np.unpackbits(a.view(np.uint8)).sum()); kept1 = int(np.unpackbits(b.view(np.uint8)).sum())
             assert kept0 <= kept1 <= kept0 + max(50, kept0 // 50)           # and not much looser
+
+
+@pytest.mark.parametrize("kind,value", [(np.uint8, 9), (np.int16, -5), (np.float32, 0.25)])
+def test_select_threshold_culled_bit_exact(sphere_map, kind, value):
+    """Tile-range culled threshold on a float32 attribute with NaN holes (the surface map's z plane)
+    == oracle: windows that miss everything, hit everything, sit on exact attribute values, have
+    +-inf ends, are empty (lo > hi) or NaN; with and without a valid plane; ragged slab heights."""
+    _, ref, got = sphere_map
+    rng = np.random.default_rng(8)
+    z_ref = np.ascontiguousarray(ref["pos"][2])
+    some = float(z_ref[130, 70])
+    assert some == some
+    for rows in (256, 255, 6):
+        attr_ref = np.ascontiguousarray(z_ref[:rows])
+        attr_dev = got["pos"][2][:rows].contiguous()
+        tiles = nat.attr_tiles(attr_dev)
+        assert tiles is not None
+        ranges = tiles.ranges.cpu().numpy()
+        blk = attr_ref[:4, :128]
+        if not np.isnan(blk).all():
+            assert ranges[0, 0] == np.nanmin(blk) and ranges[0, 1] == np.nanmax(blk)
+        valid_np = (rng.random((rows, 256)) < 0.7).astype(np.uint8)
+        for lo, hi in ((-0.2, 0.3), (5.0, 6.0), (-9.0, 9.0), (some, some), (-np.inf, 0.0), (0.5, np.inf), (0.3, -0.3),
+                       (np.nan, 1.0), (np.nextafter(some, 2.0), 0.99)):
+            for valid in (None, valid_np):
+                data0 = rng.integers(0, 4, size=(rows, 256)).astype(kind)
+                mask0 = rng.random((rows, 256)) < 0.2
+                ed0 = (rng.random((rows, 256)) < 0.1).astype(np.uint8)
+                rd, rm, re = data0.copy(), mask0.copy(), ed0.copy()
+                want = kn.select_threshold(attr_ref, valid, lo, hi, rd, rm, re, value)
+                d, m, e = _dev(data0), _dev(mask0), _dev(ed0)
+                assert nat.select_threshold(attr_dev, None if valid is None else _dev(valid), lo, hi, d, m, e, value,
+                                            tiles=tiles) == want, (rows, lo, hi)
+                assert np.array_equal(_bits(_host(d)), _bits(rd))
+                assert np.array_equal(m.cpu().numpy(), rm) and np.array_equal(e.cpu().numpy(), re)
+    assert nat.attr_tiles(got["pos"][2][:, :200].contiguous()) is None and nat.attr_tiles(got["tri_id"]) is None

@@ -138,6 +138,27 @@ def test_culled_brushes_equal_streamed_at_full_size(big):
         l.release()
 
 
+def test_culled_threshold_equals_streamed_at_full_size(big):
+    """16384^2: threshold selection on the height plane with tile ranges == the streaming kernel."""
+    mesh, surf, cam, ctx, pool = big
+    import torch
+    attr = surf.pos[2]
+    tiles = nat.attr_tiles(attr)
+    z = mesh.vertices[:, 2]
+    a = ml.create_layer("thr_cull", "uint8", A, A, pool=pool)
+    b = ml.create_layer("thr_full", "uint8", A, A, pool=pool)
+    ea = torch.zeros((A, A), dtype=torch.uint8, device="cuda")
+    eb = torch.zeros((A, A), dtype=torch.uint8, device="cuda")
+    for k, (p0, p1) in enumerate(((40, 60), (0, 3), (99.5, 100), (10, 90))):
+        lo, hi = float(np.percentile(z, p0)), float(np.percentile(z, p1))
+        ra = ml.select_threshold(attr, None, lo, hi, a, k + 1, edited=ea, tiles=tiles)
+        rb = ml.select_threshold(attr, None, lo, hi, b, k + 1, edited=eb)
+        assert ra.edited_count == rb.edited_count
+        assert _checksum(a.data) == _checksum(b.data) and _checksum(ea) == _checksum(eb)
+    assert _checksum(a.mask.view(torch.uint8)) == _checksum(b.mask.view(torch.uint8)) and a.valid_texels() > 0
+    a.release(); b.release()
+
+
 def test_batched_strokes_equal_sequential_at_full_size(big):
     mesh, surf, cam, ctx, pool = big
     import torch
