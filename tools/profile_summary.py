@@ -15,7 +15,8 @@ import sys
 
 STAGE_OF = (("chain_kernel", "chain"), ("binary_kernel", "mask_op"), ("sphere_batch_tiles_kernel", "batch"),
             ("sphere_batch_kernel", "batch_stream"), ("sphere_tiles_kernel", "sphere"), ("sphere_kernel", "sphere_stream"),
-            ("threshold_kernel", "threshold"), ("area_kernel", "area"), ("tea_eval_kernel", "tea"),
+            ("threshold_tiles_kernel", "threshold"), ("threshold_kernel", "threshold_stream"), ("area_kernel", "area"),
+            ("tea_eval_kernel", "tea"),
             ("padding_tile_kernel", "tpa"), ("padding_stream_kernel", "tpa_stream"), ("tea_stream_kernel", "tea_stream"))
 
 METRICS = [
