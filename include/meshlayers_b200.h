@@ -296,6 +296,14 @@ typedef struct ml_stroke_ctx {
 int ml_stroke(const ml_stroke_ctx* ctx, int cur, const ml_tea_params* params, void* data, int esize,
               uint32_t value_bits, uint8_t* mask, int64_t padding_radius, uint64_t* counters, void* stream);
 
+/* A drag gesture: n strokes (the pointer samples of SPEC:569) on one layer in ONE host call, applied in
+ * order exactly like n ml_stroke calls starting with tile buffer `first_cur` (the buffers alternate;
+ * after the call the next stroke uses (first_cur + n) & 1).  params / value_bits are HOST arrays of n
+ * records; counters (device) receives 3 x u64 per stroke. */
+int ml_stroke_sequence(const ml_stroke_ctx* ctx, int first_cur, int64_t n, const ml_tea_params* params, void* data,
+                       int esize, const uint32_t* value_bits, uint8_t* mask, int64_t padding_radius,
+                       uint64_t* counters, void* stream);
+
 /* ---- display + layer file helpers (definitions: ext_resolve_display, ext_pack_mask)
  * SPEC:186-203 resolve_display: rgba_out[i] (4 bytes R,G,B,A) = mask[i] ? palette(u) : 0 with
  * u = clamp((value-lower)/(upper-lower), 0, 1), piecewise-linear over npoints control points

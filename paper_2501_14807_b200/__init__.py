@@ -25,7 +25,7 @@ from .layer_core import (InformationLayer, create_layer, label_area, layer_area,
                          layer_stats, layer_union, layers_area)
 from .editing import (EditingTool, EditProjection, EditResult, StrokeContext, apply_padding,
                       apply_stroke, build_outline_mask, compute_tool_projection, project_fragment,
-                      select_sphere, select_sphere_batch, select_threshold, stroke)
+                      select_sphere, select_sphere_batch, select_threshold, stroke, stroke_gesture)
 from .display import Palette, map_value_to_color, resolve_display
 from .layer_io import decode_layer, encode_layer, load_layer, save_layer
 

@@ -89,6 +89,8 @@ def lib():
                                 vp, vp, i64, vp, i32, u32, vp, vp, vp, vp]),
         "ml_tea_classify_recs": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
         "ml_stroke": (i32, [C.POINTER(_StrokeCtx), i32, C.POINTER(_TeaParams), vp, i32, u32, vp, i64, vp, vp]),
+        "ml_stroke_sequence": (i32, [C.POINTER(_StrokeCtx), i32, i64, C.POINTER(_TeaParams), vp, i32, C.POINTER(C.c_uint32), vp,
+                                     i64, vp, vp]),
         "ml_tea_rec_bytes": (sz, [i64]),
         "ml_tea_prepare": (i32, [vp, vp, i32, i64, vp, sz, vp]),
         "ml_tea_classify": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
@@ -133,7 +135,7 @@ EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve",
     "ml_surface_workspace_bytes", "ml_owner_values", "ml_tea_texels", "ml_tea_rec_bytes", "ml_tea_prepare",
-    "ml_tea_classify_recs", "ml_stroke",
+    "ml_tea_classify_recs", "ml_stroke", "ml_stroke_sequence",
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
     "ml_select_threshold", "ml_plane_tile_range", "ml_select_threshold_tiles", "ml_layer_op",
@@ -597,6 +599,24 @@ def stroke_call(cstruct, cur, ww, wh, depth, eps, sfx, sfy, bx, by, shape, data,
     bits, esize = value_bits(value, data)
     _check(lib().ml_stroke(C.byref(cstruct), int(cur), C.byref(p), _ptr(data), esize, bits, _ptr(mask), int(radius),
                            _ptr(counts), _stream()))
+
+
+def stroke_sequence_call(cstruct, first_cur, ww, wh, depth, eps, tool_maps, shapes, data, mask, values, radius, counts):
+    """``ml_stroke_sequence``: n strokes in one C call.  ``tool_maps`` = n tuples (sfx, sfy, bx, by),
+    ``shapes`` = n device shape planes, ``values`` = n stroke values, ``counts`` int64[n,3] on the device."""
+    n = len(tool_maps)
+    params = (_TeaParams * n)()
+    vbits = (C.c_uint32 * n)()
+    esize = 1
+    alive = []                     # uploaded shape planes must outlive the queued kernels of ALL strokes
+    for k in range(n):
+        shape = _as_dev_bytes(shapes[k], data.device)
+        alive.append(shape)
+        _check_window(ww, wh, depth.shape, shape.shape)
+        params[k] = _tea_params(ww, wh, depth, eps, *tool_maps[k], shape)
+        vbits[k], esize = value_bits(values[k], data)
+    _check(lib().ml_stroke_sequence(C.byref(cstruct), int(first_cur), n, params, _ptr(data), esize, vbits, _ptr(mask),
+                                    int(radius), _ptr(counts), _stream()))
 
 
 def tea_scratch(ntri, ntexels, device, max_quads=1 << 24):

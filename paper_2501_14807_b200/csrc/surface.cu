@@ -833,4 +833,16 @@ int ml_stroke(const ml_stroke_ctx* c, int cur, const ml_tea_params* tp, void* da
                                   value_bits, mask, counters + 2, stream);
 }
 
+int ml_stroke_sequence(const ml_stroke_ctx* c, int first_cur, int64_t n, const ml_tea_params* tp, void* data, int esize,
+                       const uint32_t* value_bits, uint8_t* mask, int64_t padding_radius, uint64_t* counters,
+                       void* stream) {
+    if (n < 0 || tp == nullptr || value_bits == nullptr) return ml_fail(ML_ERR_ARG, "ml_stroke_sequence: bad arguments");
+    for (int64_t k = 0; k < n; ++k) {
+        const int rc = ml_stroke(c, (first_cur + (int)(k & 1)) & 1, tp + k, data, esize, value_bits[k], mask, padding_radius,
+                                 counters + 3 * k, stream);
+        if (rc != ML_OK) return rc;
+    }
+    return ML_OK;
+}
+
 }  // extern "C"

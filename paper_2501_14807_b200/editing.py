@@ -236,6 +236,41 @@ def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, halo
     return res
 
 
+def stroke_gesture(ctx, tools, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):
+    """A drag gesture (every pointer sample is one stroke): the strokes of ``tools`` are
+    applied in order to ``layer`` -- same planes and counts as calling ``stroke`` for each -- but queued
+    with ONE host call (``ml_stroke_sequence``), so the per-stroke cost is the device work, not the
+    host's issue latency.  All tools share the padding radius.  Returns one ``EditResult`` per stroke
+    (lazy device counters).  Contexts that cannot take the one-call path (slabs, overlapping uv
+    layouts, radius 0 or > 4) fall back to a loop over ``stroke``."""
+    torch = _native._torch()
+    tools = list(tools)
+    if not tools:
+        return []
+    s = ctx.surface
+    radius = tools[0].padding_radius
+    as_u8 = outline.view(torch.uint8) if outline.dtype == torch.bool else outline
+    one_call = (ctx.tiles is not None and s.overlap == 0 and s.rows == s.height and 0 < radius <= 4
+                and all(t.padding_radius == radius for t in tools)
+                and all(t.data_ptr() % 16 == 0 for t in (layer.data, layer.mask, as_u8)))
+    if not one_call:
+        return [stroke(ctx, t, layer, outline, eps=eps) for t in tools]
+    _stroke_checks(ctx, layer)
+    ctx.begin_culled_stroke()
+    if ctx._cstruct is None or ctx._cstruct[0] != as_u8.data_ptr():
+        ctx._cstruct = (as_u8.data_ptr(), _native.stroke_ctx(
+            ctx.tri_xy, ctx.tri_clip, ctx.recs, s.tri_id, ctx.scratch[0], ctx.scratch[1], ctx.tiles, ctx.edited, as_u8,
+            width=s.width, height=s.height, row0=s.row0, rows=s.rows, known_fragments=s.covered))
+    maps = [compute_tool_projection(ctx.camera, t).kernel_factors for t in tools]
+    counts = torch.empty((len(tools), 3), dtype=torch.int64, device=ctx.device)
+    _native.stroke_sequence_call(ctx._cstruct[1], ctx.cur, float(ctx.camera.width), float(ctx.camera.height),
+                                 ctx.depth.plane, eps, maps, [t.shape for t in tools], layer.data, layer.mask,
+                                 [t.value for t in tools], radius, counts)
+    for _ in tools:
+        ctx.end_culled_stroke()
+    return [EditResult(edited_mask=ctx.edited, _counts=counts[k, :2], _padded=counts[k, 2:]) for k in range(len(tools))]
+
+
 # --------------------------------------------------------------------------------------------
 # north-star selection brushes
 

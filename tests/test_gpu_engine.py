@@ -309,6 +309,44 @@ def test_row_sharded_strokes_equal_full_plane_oracle():
     assert np.array_equal(layers[1].mask.cpu().numpy(), mask[r0:r0 + rows])
 
 
+def test_stroke_gesture_equals_stroke_loop():
+    """ml_stroke_sequence: a drag gesture of 9 strokes (host-side numpy shapes of different sizes,
+    different values) in one C call == the same strokes through stroke() one by one == the oracle."""
+    rng = np.random.default_rng(71)
+    mesh = synth.icosphere_mesh(3)
+    A, W = 256, 160
+    cam = synth.default_camera(W, W)
+    surf = ml.build_surface_map(mesh, A, A)
+    depth = ml.render_depth(mesh, cam)
+    outline = ml.build_outline_mask(surf.coverage, thickness=1)
+    ref_outline = kn.outline((surf.tri_id >= 0).cpu().numpy().astype(np.uint8), 1)
+    tools = [ml.EditingTool(px=40.0 + 9.0 * k, py=float(rng.uniform(40, 120)), shape=synth.circle_shape(int(rng.integers(3, 22))),
+                            value=k + 1, padding_radius=1) for k in range(9)]
+    pool = ml.TexturePool()
+    g_layer, l_layer = ml.create_layer("g", "uint8", A, A, pool=pool), ml.create_layer("l", "uint8", A, A, pool=pool)
+    g_ctx, l_ctx = ml.StrokeContext(mesh, cam, depth, surf), ml.StrokeContext(mesh, cam, depth, surf)
+    ml.stroke(g_ctx, tools[0], g_layer, outline)                      # odd starting parity of the tile buffers
+    ml.stroke(l_ctx, tools[0], l_layer, outline)
+    got = ml.stroke_gesture(g_ctx, tools, g_layer, outline)
+    loop = [ml.stroke(l_ctx, t, l_layer, outline) for t in tools]
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool)
+    for t in [tools[0]] + tools:
+        edited = np.zeros((A, A), np.uint8)
+        want = _oracle_stroke(mesh, cam, t, A, data, mask, edited)
+        padded = kn.padding(ref_outline, edited, 1, data, mask, t.value)
+    assert [(r.edited_count, r.fragments, r.padded_count) for r in got] == [(r.edited_count, r.fragments, r.padded_count) for r in loop]
+    assert (got[-1].edited_count, got[-1].fragments, got[-1].padded_count) == (want[0], want[1], padded)
+    for layer in (g_layer, l_layer):
+        assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+    assert np.array_equal(g_ctx.edited.cpu().numpy(), edited) and g_ctx.cur == l_ctx.cur
+    # a following single stroke continues correctly on both contexts
+    extra = ml.EditingTool(px=100.0, py=100.0, shape=synth.square_shape(9), value=77)
+    a, b = ml.stroke(g_ctx, extra, g_layer, outline), ml.stroke(l_ctx, extra, l_layer, outline)
+    assert a.edited_count == b.edited_count and np.array_equal(g_layer.data.cpu().numpy(), l_layer.data.cpu().numpy())
+    assert np.array_equal(g_ctx.edited.cpu().numpy(), l_ctx.edited.cpu().numpy())
+    assert ml.stroke_gesture(g_ctx, [], g_layer, outline) == []
+
+
 def _torch_i32():
     import torch
     return torch.int32
