@@ -103,6 +103,19 @@ def main():
     d2 = torch.zeros((N, N), dtype=torch.uint8, device=dev)
     dout = torch.zeros((N, N), dtype=torch.uint8, device=dev)
     run("layer_op union u8", lambda: nat.layer_op("union", data, mask, d2, m2, dout, out), 6 * n)
+    if not want or any(w in "layer chain" for w in want):
+        ops = ["union", "union", "intersection", "difference", "union", "masking", "difference", "union"]   # ops[0] is ignored
+        for label, p in (("sparse (5%% blobs)", 0.05), ("dense (60%% blobs)", 0.6)):
+            cm = []
+            for k in range(8):          # coherent blobs: threshold a smooth field
+                yy, xx = torch.meshgrid(torch.linspace(0, 9 + k, N, device=dev), torch.linspace(0, 7 + k, N, device=dev), indexing="ij")
+                f = torch.sin(xx + k) * torch.cos(yy - k)
+                thr_v = torch.quantile(f[::64, ::64].flatten(), 1.0 - p)
+                cm.append((f > thr_v).to(torch.uint8))
+                del yy, xx, f
+            cd = [torch.full((N, N), k + 1, dtype=torch.uint8, device=dev) for k in range(8)]
+            run("layer chain 8 u8 " + label % (), lambda: nat.layer_chain(cd, cm, ops, dout, out), 18 * n)
+            del cm, cd
     run("memset 1 plane (torch)", lambda: out.zero_(), n)
     run("copy 1 plane (torch)", lambda: out.copy_(m2), 2 * n)
 
