@@ -1,3 +1,7 @@
+#!/usr/bin/env python
+"""Device time per stroke (apply_stroke = TEA, stroke = TEA + TPA through ml_stroke) at 16384^2 with the
+1M-triangle mesh for tool radii 10 / 70 / 200 px: 50 strokes back to back between two CUDA events.
+Tuning aid; the paper-style sweep with the SPEC's CSV is `python -m paper_2501_14807_b200.bench`."""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
