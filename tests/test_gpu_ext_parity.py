@@ -352,6 +352,41 @@ def test_layer_chain_equals_sequential_ops(kind):
         assert np.array_equal(_bits(_host(gd)), _bits(cd))
 
 
+@pytest.mark.parametrize("seed", range(10))
+def test_layer_chain_lazy_random_sequences(seed):
+    """Chains of 3..8 one-byte layers take the lazy-data kernel: random operator sequences, sparse /
+    dense / coherent masks, mask bytes other than 0 / 1 (any non-zero byte is valid), ragged length
+    (scalar tail), and the output aliasing the first operand -- fused result == step-by-step oracle."""
+    rng = np.random.default_rng(500 + seed)
+    n = 16 * int(rng.integers(50, 900)) + int(rng.integers(0, 16))
+    N = int(rng.integers(3, 9))
+    kind = np.uint8 if seed % 2 else np.int8
+    ops = [str(rng.choice(["union", "intersection", "difference", "masking"])) for _ in range(N - 1)]
+    masks = []
+    for k in range(N):
+        p = float(rng.choice([0.02, 0.3, 0.9]))
+        if rng.random() < 0.5:                                   # coherent runs
+            m = np.repeat(rng.random(n // 40 + 1) < p, 40)[:n]
+        else:
+            m = rng.random(n) < p
+        m = m.astype(np.uint8) * rng.choice(np.array([1, 1, 1, 2, 255], np.uint8), size=n)
+        masks.append(m)
+    datas = [rng.integers(-100 if kind == np.int8 else 1, 100, n).astype(kind) for _ in range(N)]
+    cd, cm = datas[0].copy(), (masks[0] != 0).astype(np.uint8)
+    cd[cm == 0] = 0
+    for j in range(1, N):
+        nd, nm = np.empty(n, kind), np.empty(n, np.uint8)
+        kn.layer_op(ops[j - 1], cd, cm, datas[j], masks[j], nd, nm)
+        cd, cm = nd, nm
+    d_dev, m_dev = [_dev(d) for d in datas], [_dev(m) for m in masks]
+    gd, gm = _dev(np.zeros(n, kind)), _dev(np.zeros(n, np.uint8))
+    nat.layer_chain(d_dev, m_dev, [None] + ops, gd, gm)
+    assert np.array_equal(gm.cpu().numpy(), cm) and np.array_equal(_bits(_host(gd)), _bits(cd)), ops
+    # in place: the result overwrites layer 0
+    nat.layer_chain(d_dev, m_dev, [None] + ops, d_dev[0], m_dev[0])
+    assert np.array_equal(m_dev[0].cpu().numpy(), cm) and np.array_equal(_bits(_host(d_dev[0])), _bits(cd)), ops
+
+
 @pytest.mark.parametrize("L", [1, 3, 8, 13, 64])
 def test_layer_area_matches_oracle(sphere_map, L):
     _, ref, got = sphere_map
