@@ -12,7 +12,8 @@ One STEP = one pass of every hot-path stage over this rank's 16384 x 16384 atlas
     batch      L sphere strokes (one per layer) batched in ONE pass over the position map
                (the brush / selection stages tea, tpa, sphere, batch and threshold run the
                footprint-culled kernels: a stroke reads only the tiles it can reach, the threshold
-               only tiles whose height range meets the window; ``--no-cull`` streams the whole atlas, and
+               only tiles whose height range meets the window, the chain reads a data vector only
+               where the masks let it reach the result; ``--no-cull`` streams the whole atlas, and
                the whole-atlas streaming kernels are ALSO timed on their own and reported under
                ``config.stream_kernels`` -- they are the brush kernels' HBM-roofline evidence)
     chain      fused layer-algebra chain ((L0 u L1) n L2) \\ L3 ... over 8 uint8 layers (C3)
@@ -64,7 +65,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=1024, help="rows of the slab the CPU baseline processes")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-cull", action="store_true",
-                    help="brush stages (tea, tpa, sphere, batch) stream the whole atlas instead of their footprint tiles")
+                    help="every stage streams the whole atlas: brush / selection stages ignore their footprint tiles, the "
+                         "chain reads every data vector")
     ap.add_argument("--stages", default=",".join(STAGES))
     return ap.parse_args()
 
@@ -377,7 +379,7 @@ def run_ours(args):
             batch.counts.zero_()
             out = [ml.select_sphere_batch(surf, batch, cull=cull).clone()]
         elif st == "chain":
-            ml.layer_chain(layers[:wl.chain_n], wl.chain_ops, out_layer)
+            ml.layer_chain(layers[:wl.chain_n], wl.chain_ops, out_layer, lazy=cull)
         elif st == "mask_op":
             nat.layer_op("union", None, layers[0].mask, None, layers[1 % L].mask, None, tmp_mask)
         elif st == "threshold":
@@ -485,7 +487,7 @@ def run_ours(args):
     stream_info = {}
     if not args.no_cull:
         reps = max(5, min(20, args.steps))
-        for st in [s for s in ("tea", "tpa", "sphere", "batch", "threshold") if s in stages]:
+        for st in [s for s in ("tea", "tpa", "sphere", "batch", "threshold", "chain") if s in stages]:
             ms_acc = 0.0
             for k in range(reps + 2):
                 inp = inputs[args.warmup + (k % args.steps)]
@@ -518,7 +520,7 @@ def run_ours(args):
         if st == "chain":
             # (N+1)*2 B/texel is an upper bound: the chain kernel fetches a data vector only where the masks
             # say it can contribute, so its "frac_of_peak" can exceed 1 (bytes that were never read)
-            stage_info[st]["lazy_data_reads"] = True
+            stage_info[st]["lazy_data_reads"] = not args.no_cull
     peak_now = peak
     stream_kernels = {st: {"ms": round(ms, 4), "gb_s": round(wl.algorithmic_bytes(n, st, T, hits[st]) / (ms * 1e-3) / 1e9, 1),
                            "frac_of_peak": round(wl.algorithmic_bytes(n, st, T, hits[st]) / (ms * 1e-3) / 1e9 / peak_now, 4)}

@@ -840,8 +840,13 @@ def layer_op(op, da, ma, db, mb, dc, mc):
                              _ptr(mb), _ptr(dc), _ptr(mc), esize, n, _stream()))
 
 
-def layer_chain(datas, masks, ops, dc, mc):
-    """Fused left-to-right chain ((L0 ops[1] L1) ops[2] L2) ... in one pass.  ``ops[0]`` ignored."""
+ML_CHAIN_EAGER = 0x100
+
+
+def layer_chain(datas, masks, ops, dc, mc, *, lazy=True):
+    """Fused left-to-right chain ((L0 ops[1] L1) ops[2] L2) ... in one pass.  ``ops[0]`` ignored.
+    ``lazy=False`` forces the streaming kernel that reads every data vector (the default reads the
+    data of 3..8 one-byte layers only where the masks let it contribute; same result)."""
     require_cuda()
     N = len(masks)
     n = mc.numel()
@@ -856,7 +861,7 @@ def layer_chain(datas, masks, ops, dc, mc):
                 raise TargetMismatch("data planes disagree in kind or size")
     dptr = (C.c_void_p * N)(*[(d.data_ptr() if esize else None) for d in (datas if esize else [None] * N)])
     mptr = (C.c_void_p * N)(*[m.data_ptr() for m in masks])
-    codes = (C.c_int32 * N)(*[0] + [OPS[o] if isinstance(o, str) else int(o) for o in list(ops)[1:]])
+    codes = (C.c_int32 * N)(*[0 if lazy else ML_CHAIN_EAGER] + [OPS[o] if isinstance(o, str) else int(o) for o in list(ops)[1:]])
     _check(lib().ml_layer_chain(N, dptr, mptr, codes, _ptr(dc), _ptr(mc), esize, n, _stream()))
 
 

@@ -71,6 +71,7 @@ chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
     const long long nv = n >> 4;
+    const bool eager = (a.ops[0] & ML_CHAIN_EAGER) != 0;
     for (long long v = tid; v < nv; v += nthreads) {
         Group<ESIZE> acc[4];                      // four 4-texel groups of the 16-texel vector
         for (int l0 = 0; l0 < a.nlayers; l0 += GL) {
@@ -81,8 +82,12 @@ chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
                 if (l0 + k < a.nlayers) {
                     m[k] = ld_stream_rw((const uint4*)a.mask[l0 + k] + v);
                     if (ESIZE > 0) {
+                        // only the first operand and union operands can supply a data value (combine():
+                        // take_b); the data planes of the other operands are not read unless ML_CHAIN_EAGER
+                        const bool need = eager || l0 + k == 0 || a.ops[l0 + k] == ML_OP_UNION;
 #pragma unroll
-                        for (int j = 0; j < ES; ++j) d[k][j] = ld_stream_rw((const uint4*)a.data[l0 + k] + v * ES + j);
+                        for (int j = 0; j < ES; ++j)
+                            d[k][j] = need ? ld_stream_rw((const uint4*)a.data[l0 + k] + v * ES + j) : make_uint4(0u, 0u, 0u, 0u);
                     }
                 }
             }
@@ -263,6 +268,7 @@ binary_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
     const int op = a.ops[1];
+    const bool need_b = op == ML_OP_UNION;     // only a union can take a data value from B (combine(): take_b)
     for (long long v0 = tid; v0 < nv; v0 += nthreads * VPT) {
         uint4 m[VPT][2];
         uint4 d[VPT][2][ES];
@@ -275,7 +281,9 @@ binary_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
                     m[k][l] = ld_stream_rw((const uint4*)a.mask[l] + v);
                     if (ESIZE > 0) {
 #pragma unroll
-                        for (int j = 0; j < ES; ++j) d[k][l][j] = ld_stream_rw((const uint4*)a.data[l] + v * ES + j);
+                        for (int j = 0; j < ES; ++j)
+                            d[k][l][j] = (l == 0 || need_b) ? ld_stream_rw((const uint4*)a.data[l] + v * ES + j)
+                                                            : make_uint4(0u, 0u, 0u, 0u);
                     }
                 }
             }
@@ -341,7 +349,7 @@ int launch_chain(const ChainArgs& a, void* dc, uint8_t* mc, long long n, cudaStr
         ML_CUDA(cudaGetLastError());
         return ML_OK;
     }
-    if (vec && ESIZE == 1 && a.nlayers > 2 && a.nlayers <= 8 && (n >> 4) > 0) {
+    if (vec && ESIZE == 1 && a.nlayers > 2 && a.nlayers <= 8 && (n >> 4) > 0 && !(a.ops[0] & ML_CHAIN_EAGER)) {
         const long long nv = n >> 4;
         long long blocks = (nv + BLOCK - 1) / BLOCK;
         const long long cap = (long long)ml_sm_count() * 16;
@@ -403,7 +411,7 @@ int ml_layer_chain(int64_t nlayers, const void* const* data, const uint8_t* cons
     for (int l = 0; l < a.nlayers; ++l) {
         a.data[l] = esize > 0 ? data[l] : nullptr;
         a.mask[l] = mask[l];
-        a.ops[l] = l == 0 ? 0 : ops[l];
+        a.ops[l] = l == 0 ? (ops[0] & ML_CHAIN_EAGER) : ops[l];      // ops[0] carries flags only
         if (l > 0 && (ops[l] < ML_OP_UNION || ops[l] > ML_OP_MASKING)) return ml_fail(ML_ERR_ARG, "unknown layer operator");
     }
     return dispatch_chain(a, dc, mc, esize, n, (cudaStream_t)stream);

@@ -107,16 +107,18 @@ def layer_mask(a, selector, out=None):
     return out
 
 
-def layer_chain(layers, ops, out):
+def layer_chain(layers, ops, out, *, lazy=True):
     """((L0 ops[0] L1) ops[1] L2) ... in ONE pass over the atlas (reads N layers, writes 1).
-    ``ops`` has len(layers)-1 entries from {"union","intersection","difference","masking"}."""
+    ``ops`` has len(layers)-1 entries from {"union","intersection","difference","masking"}.
+    ``lazy`` (default): data planes of 3..8 one-byte layers are read only where the masks let them
+    reach the result; ``lazy=False`` streams every plane (same result)."""
     if len(ops) != len(layers) - 1:
         raise TargetMismatch("need one operator between each pair of layers")
     for l in layers:
         if l.shape != out.shape or l.kind != out.kind:
             raise TargetMismatch("chain layers must share dimensions and kind")
     _native.layer_chain([l.data for l in layers], [l.mask for l in layers], [None] + list(ops),
-                        out.data, out.mask)
+                        out.data, out.mask, lazy=lazy)
     return out
 
 

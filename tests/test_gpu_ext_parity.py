@@ -380,8 +380,10 @@ def test_layer_chain_lazy_random_sequences(seed):
         cd, cm = nd, nm
     d_dev, m_dev = [_dev(d) for d in datas], [_dev(m) for m in masks]
     gd, gm = _dev(np.zeros(n, kind)), _dev(np.zeros(n, np.uint8))
-    nat.layer_chain(d_dev, m_dev, [None] + ops, gd, gm)
-    assert np.array_equal(gm.cpu().numpy(), cm) and np.array_equal(_bits(_host(gd)), _bits(cd)), ops
+    for lazy in (True, False):                                   # lazy-data kernel and the streaming (eager) kernel
+        gd.zero_(); gm.zero_()
+        nat.layer_chain(d_dev, m_dev, [None] + ops, gd, gm, lazy=lazy)
+        assert np.array_equal(gm.cpu().numpy(), cm) and np.array_equal(_bits(_host(gd)), _bits(cd)), (ops, lazy)
     # in place: the result overwrites layer 0
     nat.layer_chain(d_dev, m_dev, [None] + ops, d_dev[0], m_dev[0])
     assert np.array_equal(m_dev[0].cpu().numpy(), cm) and np.array_equal(_bits(_host(d_dev[0])), _bits(cd)), ops

@@ -13,7 +13,7 @@ import json
 import subprocess
 import sys
 
-STAGE_OF = (("chain_kernel", "chain"), ("binary_kernel", "mask_op"), ("sphere_batch_tiles_kernel", "batch"),
+STAGE_OF = (("chain_lazy_kernel", "chain"), ("chain_kernel", "chain_stream"), ("binary_kernel", "mask_op"), ("sphere_batch_tiles_kernel", "batch"),
             ("sphere_batch_kernel", "batch_stream"), ("sphere_tiles_kernel", "sphere"), ("sphere_kernel", "sphere_stream"),
             ("threshold_tiles_kernel", "threshold"), ("threshold_kernel", "threshold_stream"), ("area_kernel", "area"),
             ("tea_eval_kernel", "tea"),
