@@ -46,45 +46,47 @@ area_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
     const long long nthreads = (long long)gridDim.x * BLOCK;
     long long done = 0;
     if (VECTOR) {
+        // Layer masks are spatially coherent and mostly empty, so the area vector of a 16-texel step is
+        // fetched only when some mask of the group has a texel in it.  That makes the area load depend
+        // on the mask loads; the dependency is hidden by requesting the masks of the thread's NEXT step
+        // before the area of the current one (software pipelining), so the bytes in flight stay those of
+        // an unconditional stream.  Most vectors lie entirely outside or entirely inside a layer (mask
+        // bytes written by this library are exactly 0 / 1): whole 4-texel words are skipped or added as
+        // one pre-summed double; only words on a mask boundary, or masks using other non-zero byte
+        // values, take the per-texel path.  Summation order is free (1e-6 relative, north star).
         const long long nv = n >> 4;
+        uint4 mn[G];
+        if (tid < nv) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) mn[g] = ld_stream((const uint4*)a.mask[g] + tid);
+        }
         for (long long v = tid; v < nv; v += nthreads) {
-            float4 ar[4];
             uint4 m[G];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) ar[j] = ld_stream((const float4*)area + v * 4 + j);
+            for (int g = 0; g < G; ++g) m[g] = mn[g];
+            if (v + nthreads < nv) {
 #pragma unroll
-            for (int g = 0; g < G; ++g) m[g] = ld_stream((const uint4*)a.mask[g] + v);
-            // Layer masks are spatially coherent and the mask bytes this library writes are exactly
-            // 0 / 1, so most 16-texel vectors lie entirely outside (skip) or entirely inside (add the
-            // shared 16-texel sum) a layer; only vectors on a mask boundary, or masks using other
-            // non-zero byte values, take the per-texel path.  Summation order is free (1e-6 rel).
+                for (int g = 0; g < G; ++g) mn[g] = ld_stream((const uint4*)a.mask[g] + v + nthreads);
+            }
             uint32_t anyset = 0;
 #pragma unroll
             for (int g = 0; g < G; ++g) anyset |= m[g].x | m[g].y | m[g].z | m[g].w;
             if (anyset == 0) continue;
-            double d[16];
+            float4 ar[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ar[j] = ld_stream((const float4*)area + v * 4 + j);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                d[4 * j] = (double)ar[j].x; d[4 * j + 1] = (double)ar[j].y;
-                d[4 * j + 2] = (double)ar[j].z; d[4 * j + 3] = (double)ar[j].w;
-            }
-            double s4[4];
+                const double d[4] = {(double)ar[j].x, (double)ar[j].y, (double)ar[j].z, (double)ar[j].w};
+                const double s4 = xadd(xadd(d[0], d[1]), xadd(d[2], d[3]));
 #pragma unroll
-            for (int j = 0; j < 4; ++j) s4[j] = xadd(xadd(d[4 * j], d[4 * j + 1]), xadd(d[4 * j + 2], d[4 * j + 3]));
-            const double s16 = xadd(xadd(s4[0], s4[1]), xadd(s4[2], s4[3]));
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const uint32_t o = m[g].x | m[g].y | m[g].z | m[g].w;
-                if (o == 0) continue;
-                if ((m[g].x & m[g].y & m[g].z & m[g].w) == 0x01010101u) { acc[g] = xadd(acc[g], s16); cnt[g] += 16; continue; }
-                const uint32_t w[4] = {m[g].x, m[g].y, m[g].z, m[g].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (w[j] == 0) continue;
-                    if (w[j] == 0x01010101u) { acc[g] = xadd(acc[g], s4[j]); cnt[g] += 4; continue; }
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t w = ((const uint32_t*)&m[g])[j];
+                    if (w == 0) continue;
+                    if (w == 0x01010101u) { acc[g] = xadd(acc[g], s4); cnt[g] += 4; continue; }
 #pragma unroll
                     for (int e = 0; e < 4; ++e)
-                        if (w[j] & (0xffu << (8 * e))) { acc[g] = xadd(acc[g], d[4 * j + e]); ++cnt[g]; }
+                        if (w & (0xffu << (8 * e))) { acc[g] = xadd(acc[g], d[e]); ++cnt[g]; }
                 }
             }
         }
