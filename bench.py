@@ -4,7 +4,8 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One STEP = one pass of every hot-path stage over this rank's 16384 x 16384 atlas slab
-(268.4 Mtexel), the C3+C4 workload of BASELINE.json at 8 layers (``--layers 64`` gives C4):
+(268.4 Mtexel), the C3+C4 workload of BASELINE.json at 8 layers (``--layers 64`` gives C4); the
+stages run in the order of ``STAGES`` below (streaming stages first), listed here by kind:
 
     tea        the paper's projective brush (TEA, KN:135-203) over the cached triangle-id map
     tpa        the paper's padding pass (TPA): outline texels next to the stroke
@@ -48,7 +49,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-STAGES = ("tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area")
+# The long streaming stages come first: after the end-of-step read-back of the e2e loop the host queues
+# them in a few microseconds and prepares the (host-heavier) brush calls while the GPU is busy.
+STAGES = ("chain", "mask_op", "area", "threshold", "tea", "tpa", "sphere", "batch")
 CHAIN_OPS = ["union", "intersection", "difference", "union", "masking", "difference", "union"]
 
 
