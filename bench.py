@@ -533,7 +533,9 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(dom)
+            tj = json.load(f)
+        # whole-atlas (--no-cull) runs launch the streaming forms of the kernels: "<stage>_stream" entries
+        traffic = tj.get(dom + "_stream", tj.get(dom)) if args.no_cull else tj.get(dom)
     # the dominant stage's main kernel: stage bytes / stage time (for tea the stage is 3 kernels
     # + the edited-plane reset; its bytes include all of them)
     dom_b = wl.algorithmic_bytes(n, dom, T, hits[dom])
