@@ -229,8 +229,8 @@ int ml_layer_op(int op, const void* da, const uint8_t* ma, const void* db, const
 
 /* Fused left-to-right chain  ((L0 op1 L1) op2 L2) ... op_{N-1} L_{N-1}  in one pass:
  * reads N layers, writes 1.  HOST arrays of N device pointers / N ops, N <= 16.  ops[0] is not an
- * operator: it carries flags (0, or ML_CHAIN_EAGER).  Chains of 3..8 one-byte layers read a data
- * vector only where the masks say it can contribute to the result (identical planes, fewer bytes);
+ * operator: it carries flags (0, or ML_CHAIN_EAGER).  Chains of 3..8 layers read a data vector only
+ * where the masks say it can contribute to the result (identical planes, fewer bytes);
  * ML_CHAIN_EAGER forces the streaming form that reads every vector of every plane. */
 enum { ML_CHAIN_EAGER = 0x100 };
 int ml_layer_chain(int64_t nlayers, const void* const* data, const uint8_t* const* mask,

@@ -159,7 +159,7 @@ chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
     }
 }
 
-// Chains of up to 8 one-byte layers (the common label-layer case) read their data planes LAZILY.
+// Chains of 3 to 8 layers with data (label layers of 1, 2 or 4 bytes) read their data planes LAZILY.
 // The masks alone decide which layers can contribute a data value to a 16-texel vector: the first
 // operand where its mask is set, a union operand where it fills texels the accumulator does not hold
 // yet; intersection / difference / masking operands never do.  A dry run of the mask fold finds
@@ -167,6 +167,7 @@ chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
 // are never read (8 masks + 2 output bytes per texel instead of 18).  The mask -> data dependency is
 // hidden by software pipelining: the masks of the thread's NEXT vector are requested before the data
 // of the current one, so as many bytes are in flight as in the eager kernel.
+template <int ESIZE>
 __global__ void __launch_bounds__(BLOCK, 2)
 chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
     constexpr int GL = 8;
@@ -186,42 +187,67 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
             for (int k = 0; k < GL; ++k) if (k < a.nlayers) mn[k] = ld_stream_rw((const uint4*)a.mask[k] + v + nthreads);
         }
         // dry run of the mask fold: which layers' data can reach the result of this vector?
-        uint4 d[GL];
+        unsigned need = 0;
         uint32_t sim[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int k = 0; k < GL; ++k) {
-            bool need = false;
             if (k < a.nlayers) {
                 const int op = a.ops[k];
+                bool nd = false;
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
                     const uint32_t bff = nz_bytes(((const uint32_t*)&m[k])[g]);
-                    if (k == 0) { need |= bff != 0u; sim[g] = bff; }
-                    else if (op == ML_OP_UNION) { need |= (bff & ~sim[g]) != 0u; sim[g] |= bff; }
+                    if (k == 0) { nd |= bff != 0u; sim[g] = bff; }
+                    else if (op == ML_OP_UNION) { nd |= (bff & ~sim[g]) != 0u; sim[g] |= bff; }
                     else if (op == ML_OP_DIFFERENCE) sim[g] &= ~bff;
                     else sim[g] &= bff;
                 }
+                if (nd) need |= 1u << k;
             }
-            d[k] = need ? ld_stream_rw((const uint4*)a.data[k] + v) : make_uint4(0u, 0u, 0u, 0u);
         }
-        Group<1> acc[4];
+        // one-byte layers: all needed vectors are requested together; wider layers (64 bytes per
+        // layer and vector) are fetched one layer at a time inside the fold to bound the registers
+        uint4 d1[ESIZE == 1 ? GL : 1];
+        if (ESIZE == 1) {
+#pragma unroll
+            for (int k = 0; k < GL; ++k)
+                d1[k] = ((need >> k) & 1u) ? ld_stream_rw((const uint4*)a.data[k] + v) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        Group<ESIZE> acc[4];
 #pragma unroll
         for (int k = 0; k < GL; ++k) {
             if (k < a.nlayers) {
                 const int op = a.ops[k];
+                uint4 dk[ESIZE];
+                if (ESIZE == 1) dk[0] = d1[k];
+                else {
+#pragma unroll
+                    for (int j = 0; j < ESIZE; ++j)
+                        dk[j] = ((need >> k) & 1u) ? ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j) : make_uint4(0u, 0u, 0u, 0u);
+                }
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    Group<1> b;
+                    Group<ESIZE> b;
                     b.ff = nz_bytes(((const uint32_t*)&m[k])[g]);
-                    b.d[0] = ((const uint32_t*)&d[k])[g];
-                    if (k == 0) { acc[g].ff = b.ff; acc[g].d[0] = b.d[0] & b.ff; }
-                    else combine<1>(op, acc[g], b);
+#pragma unroll
+                    for (int j = 0; j < ESIZE; ++j) b.d[j] = ((const uint32_t*)&dk[0])[g * ESIZE + j];
+                    if (k == 0) {
+                        acc[g].ff = b.ff;
+#pragma unroll
+                        for (int j = 0; j < ESIZE; ++j) acc[g].d[j] = b.d[j] & expand<ESIZE>(b.ff, j);
+                    } else combine<ESIZE>(op, acc[g], b);
                 }
             }
         }
         st_stream((uint4*)mc + v, make_uint4(acc[0].ff & 0x01010101u, acc[1].ff & 0x01010101u, acc[2].ff & 0x01010101u,
                                               acc[3].ff & 0x01010101u));
-        st_stream((uint4*)dc + v, make_uint4(acc[0].d[0], acc[1].d[0], acc[2].d[0], acc[3].d[0]));
+        uint4 od[ESIZE];
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int j = 0; j < ESIZE; ++j) ((uint32_t*)&od[0])[g * ESIZE + j] = acc[g].d[j];
+#pragma unroll
+        for (int j = 0; j < ESIZE; ++j) st_stream((uint4*)dc + v * ESIZE + j, od[j]);
     }
 }
 
@@ -349,19 +375,19 @@ int launch_chain(const ChainArgs& a, void* dc, uint8_t* mc, long long n, cudaStr
         ML_CUDA(cudaGetLastError());
         return ML_OK;
     }
-    if (vec && ESIZE == 1 && a.nlayers > 2 && a.nlayers <= 8 && (n >> 4) > 0 && !(a.ops[0] & ML_CHAIN_EAGER)) {
+    if (vec && ESIZE >= 1 && a.nlayers > 2 && a.nlayers <= 8 && (n >> 4) > 0 && !(a.ops[0] & ML_CHAIN_EAGER)) {
         const long long nv = n >> 4;
         long long blocks = (nv + BLOCK - 1) / BLOCK;
         const long long cap = (long long)ml_sm_count() * 16;
         if (blocks > cap) blocks = cap;
-        chain_lazy_kernel<<<(unsigned)blocks, BLOCK, 0, st>>>(a, dc, mc, nv);
+        chain_lazy_kernel<(ESIZE > 0 ? ESIZE : 1)><<<(unsigned)blocks, BLOCK, 0, st>>>(a, dc, mc, nv);
         ML_CUDA(cudaGetLastError());
         const long long tail = n & 15;
         if (tail == 0) return ML_OK;
         ChainArgs t = a;
         const long long off = nv << 4;
-        for (int l = 0; l < a.nlayers; ++l) { t.mask[l] = a.mask[l] + off; t.data[l] = (const uint8_t*)a.data[l] + off; }
-        chain_scalar_kernel<ESIZE><<<1, BLOCK, 0, st>>>(t, (void*)((uint8_t*)dc + off), mc + off, tail);
+        for (int l = 0; l < a.nlayers; ++l) { t.mask[l] = a.mask[l] + off; t.data[l] = (const uint8_t*)a.data[l] + off * ESIZE; }
+        chain_scalar_kernel<ESIZE><<<1, BLOCK, 0, st>>>(t, (void*)((uint8_t*)dc + off * ESIZE), mc + off, tail);
         ML_CUDA(cudaGetLastError());
         return ML_OK;
     }

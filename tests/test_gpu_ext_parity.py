@@ -354,13 +354,13 @@ def test_layer_chain_equals_sequential_ops(kind):
 
 @pytest.mark.parametrize("seed", range(10))
 def test_layer_chain_lazy_random_sequences(seed):
-    """Chains of 3..8 one-byte layers take the lazy-data kernel: random operator sequences, sparse /
+    """Chains of 3..8 layers with 1-, 2- or 4-byte data take the lazy-data kernel: random operator sequences, sparse /
     dense / coherent masks, mask bytes other than 0 / 1 (any non-zero byte is valid), ragged length
     (scalar tail), and the output aliasing the first operand -- fused result == step-by-step oracle."""
     rng = np.random.default_rng(500 + seed)
     n = 16 * int(rng.integers(50, 900)) + int(rng.integers(0, 16))
     N = int(rng.integers(3, 9))
-    kind = np.uint8 if seed % 2 else np.int8
+    kind = (np.uint8, np.int8, np.int16, np.uint32, np.float32)[seed % 5]
     ops = [str(rng.choice(["union", "intersection", "difference", "masking"])) for _ in range(N - 1)]
     masks = []
     for k in range(N):
@@ -371,7 +371,7 @@ def test_layer_chain_lazy_random_sequences(seed):
             m = rng.random(n) < p
         m = m.astype(np.uint8) * rng.choice(np.array([1, 1, 1, 2, 255], np.uint8), size=n)
         masks.append(m)
-    datas = [rng.integers(-100 if kind == np.int8 else 1, 100, n).astype(kind) for _ in range(N)]
+    datas = [rng.integers(-100 if kind in (np.int8, np.int16, np.float32) else 1, 100, n).astype(kind) for _ in range(N)]
     cd, cm = datas[0].copy(), (masks[0] != 0).astype(np.uint8)
     cd[cm == 0] = 0
     for j in range(1, N):

@@ -115,7 +115,12 @@ def main():
                 del yy, xx, f
             cd = [torch.full((N, N), k + 1, dtype=torch.uint8, device=dev) for k in range(8)]
             run("layer chain 8 u8 " + label % (), lambda: nat.layer_chain(cd, cm, ops, dout, out), 18 * n)
-            del cm, cd
+            run("layer chain 8 u8 eager " + label % (), lambda: nat.layer_chain(cd, cm, ops, dout, out, lazy=False), 18 * n)
+            cd32 = [torch.full((N, N), k + 1, dtype=torch.int32, device=dev) for k in range(4)]
+            d32 = torch.zeros((N, N), dtype=torch.int32, device=dev)
+            run("layer chain 4 i32 " + label % (), lambda: nat.layer_chain(cd32, cm[:4], ops[:4], d32, out), 25 * n)
+            run("layer chain 4 i32 eager " + label % (), lambda: nat.layer_chain(cd32, cm[:4], ops[:4], d32, out, lazy=False), 25 * n)
+            del cm, cd, cd32, d32
     run("memset 1 plane (torch)", lambda: out.zero_(), n)
     run("copy 1 plane (torch)", lambda: out.copy_(m2), 2 * n)
 
