@@ -114,6 +114,7 @@ def main():
                 cm.append((f > thr_v).to(torch.uint8))
                 del yy, xx, f
             cd = [torch.full((N, N), k + 1, dtype=torch.uint8, device=dev) for k in range(8)]
+            run("layer chain 2 (layer_op union u8) " + label % (), lambda: nat.layer_op("union", cd[0], cm[0], cd[1], cm[1], dout, out), 6 * n)
             run("layer chain 8 u8 " + label % (), lambda: nat.layer_chain(cd, cm, ops, dout, out), 18 * n)
             run("layer chain 8 u8 eager " + label % (), lambda: nat.layer_chain(cd, cm, ops, dout, out, lazy=False), 18 * n)
             cd32 = [torch.full((N, N), k + 1, dtype=torch.int32, device=dev) for k in range(4)]
