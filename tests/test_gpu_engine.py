@@ -469,3 +469,53 @@ def test_rasterize_known_answers():
     with pytest.raises(ml.TargetMismatch):
         ml.rasterize(tri, [a, pool.acquire(8, 6, "uint8")], [1, 1])
     assert ml.rasterize(np.zeros((0, 3, 2)), [a], [1]) == 0
+
+
+def test_non_square_atlas_and_window_whole_pipeline():
+    """Atlas 384 x 200 (wider than tall, height not a multiple of the 4- / 8-row tiles) and a 160 x 96
+    window: surface map, culled strokes with padding (one-call stroke), culled sphere brush, culled
+    height threshold and areas all == oracle."""
+    import torch
+    rng = np.random.default_rng(91)
+    mesh = synth.icosphere_mesh(3)
+    AW, AH, WW, WH = 384, 200, 160, 96
+    cam = synth.default_camera(WW, WH)
+    surf = ml.build_surface_map(mesh, AW, AH)
+    txy = mesh.tri_uv_texels(AW, AH)
+    ref = kn.surface_map(txy, mesh.tri_pos(), mesh.tri_nrm(), AW, AH)
+    assert np.array_equal(surf.tri_id.cpu().numpy(), ref["tri_id"]) and surf.tiles is not None
+    assert np.array_equal(surf.pos.cpu().numpy().view(np.uint32), ref["pos"].view(np.uint32))
+    depth = ml.render_depth(mesh, cam)
+    xy, zn = window_triangles(mesh, cam)
+    d_ref = np.ones((WH, WW), np.float32)
+    kn.raster_depth(xy, zn, d_ref)
+    assert np.array_equal(depth.plane.cpu().numpy().view(np.uint32), d_ref.view(np.uint32))
+    ctx = ml.StrokeContext(mesh, cam, depth, surf)
+    outline = ml.build_outline_mask(surf.coverage, thickness=1)
+    ref_outline = kn.outline((ref["tri_id"] >= 0).astype(np.uint8), 1)
+    assert np.array_equal(outline.cpu().numpy(), ref_outline != 0)
+    pool = ml.TexturePool()
+    layer = ml.create_layer("L", "uint8", AW, AH, pool=pool)
+    data = np.zeros((AH, AW), np.uint8); mask = np.zeros((AH, AW), bool)
+    clip = cam.clip_coords(mesh.vertices)[mesh.triangles]
+    for k in range(5):
+        tool = ml.EditingTool(px=float(rng.uniform(30, 130)), py=float(rng.uniform(20, 76)),
+                              shape=synth.circle_shape(int(rng.integers(4, 20))), value=k + 1)
+        sfx, sfy, bx, by = ml.compute_tool_projection(cam, tool).kernel_factors
+        edited = np.zeros((AH, AW), np.uint8)
+        want = kn.raster_tea(txy, clip, float(WW), float(WH), d_ref, 1e-4, sfx, sfy, bx, by, tool.shape, data, mask, edited, k + 1)
+        padded = kn.padding(ref_outline, edited, 1, data, mask, k + 1)
+        res = ml.stroke(ctx, tool, layer, outline)
+        assert (res.edited_count, res.fragments, res.padded_count) == (want[0], want[1], padded), k
+        assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+    ed = torch.zeros((AH, AW), dtype=torch.uint8, device="cuda")
+    e_ref = np.zeros((AH, AW), np.uint8)
+    n = kn.select_sphere(ref["pos"], (0.2, 0.1, 0.95), 0.35, data, mask, e_ref, 9)
+    assert ml.select_sphere(surf, layer, (0.2, 0.1, 0.95), 0.35, 9, edited=ed).edited_count == n > 0
+    tiles = nat.attr_tiles(surf.pos[2])
+    n = kn.select_threshold(np.ascontiguousarray(ref["pos"][2]), None, -0.1, 0.2, data, mask, e_ref, 11)
+    assert ml.select_threshold(surf.pos[2], None, -0.1, 0.2, layer, 11, edited=ed, tiles=tiles).edited_count == n > 0
+    assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+    assert np.array_equal(ed.cpu().numpy(), e_ref)
+    a_ref = kn.layer_area(ref["area"], mask.astype(np.uint8))[0]
+    assert abs(ml.layer_area(layer, surf) - a_ref) <= 1e-9 * a_ref
