@@ -149,3 +149,33 @@ def test_empty_inputs():                                   # KN: loops simply do
     depth = np.ones((4, 4), np.float32)
     assert kn.raster_depth(np.zeros((0, 3, 2)), np.zeros((0, 3)), depth) == 0
     assert (depth == 1.0).all()
+
+
+# ------------------------------------------------------------------ exact brute force (oracle/brute.py)
+
+@pytest.mark.parametrize("seed", range(6))
+def test_oracle_coverage_matches_exact_rational_bruteforce(seed):
+    """Second opinion on the C restatement: for triangles on a 1/8-texel grid every product in
+    KN:35, 72-74 is exact in float64, so the rational-arithmetic definition (centre inside, top-left
+    ties) must give the same coverage plane, owner map and outline -- watertightness included
+    (triangles sharing an edge never both cover, and never both miss, a texel on it)."""
+    from oracle import brute
+    rng = np.random.default_rng(700 + seed)
+    w, h, T = 19, 15, 14
+    tri = np.round(rng.uniform(-2, 21, size=(T, 3, 2)) * 8.0) / 8.0
+    tri[0] = [[2, 2], [12, 2], [2, 12]]                       # two triangles sharing the edge (12,2)-(2,12),
+    tri[1] = [[12, 2], [12, 12], [2, 12]]                     # whose centres-on-the-edge test the tie rule
+    tri[2, 2] = tri[2, 1]                                     # one degenerate triangle
+    ref = np.zeros((h, w), np.uint8)
+    n = kn.coverage_fill(tri, w, h, ref)
+    want = brute.coverage(tri, w, h)
+    assert np.array_equal(ref, want) and n == int(want.sum())
+    pair = np.zeros((h, w), np.uint8)
+    a = kn.coverage_fill(tri[:1], w, h, pair)
+    b = kn.coverage_fill(tri[1:2], w, h, pair)
+    assert a + b == int(brute.coverage(tri[:2], w, h).sum())  # no texel of the shared edge counted twice or dropped
+    P = rng.normal(size=(T, 3, 3))
+    sm = kn.surface_map(tri, P, P, w, h)
+    assert np.array_equal(sm["tri_id"], brute.owner(tri, w, h))
+    for r in (1, 2):
+        assert np.array_equal(kn.outline(want, r), brute.outline(want, r))
