@@ -78,6 +78,13 @@ def lib():
         _lib.ext_resolve_display.argtypes = [vp, i32, vp, i64, dbl, dbl, vp, vp, i32, vp]
         _lib.ext_pack_mask.restype = None
         _lib.ext_pack_mask.argtypes = [vp, i64, vp]
+        _lib.kn_expand_pairs_ordered.restype = i64
+        _lib.kn_expand_pairs_ordered.argtypes = [vp, vp, vp, vp, vp, i64, vp, dbl, vp, vp]
+        _lib.kn_morton3.restype = C.c_uint64
+        _lib.kn_morton3.argtypes = [C.c_uint64] * 3
+        _lib.kn_raycast.restype = None
+        _lib.kn_raycast.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, dbl, i64,
+                                    vp, i64, i64, vp, vp, vp, i32]
     return _lib
 
 
@@ -314,3 +321,58 @@ def pack_mask(mask):
     out = np.zeros((mask.size + 7) // 8, np.uint8)
     lib().ext_pack_mask(_p(_bytes1(mask)), mask.size, _p(out))
     return out
+
+
+def morton_encode(x, y, z):
+    """The key convention of the octree kernels: bit interleave, x in bit 0, y in bit 1, z in
+    bit 2 of every triple (the octant code of KN:267).  numpy, vectorised; this is the callable
+    a caller hands to the reference's ``raycast`` (KN:362)."""
+    def spread(v):
+        v = np.asarray(v).astype(np.uint64) & np.uint64(0x1fffff)
+        v = (v | (v << np.uint64(32))) & np.uint64(0x1f00000000ffff)
+        v = (v | (v << np.uint64(16))) & np.uint64(0x1f0000ff0000ff)
+        v = (v | (v << np.uint64(8))) & np.uint64(0x100f00f00f00f00f)
+        v = (v | (v << np.uint64(4))) & np.uint64(0x10c30c30c30c30c3)
+        v = (v | (v << np.uint64(2))) & np.uint64(0x1249249249249249)
+        return v
+    return spread(x) | (spread(y) << np.uint64(1)) | (spread(z) << np.uint64(2))
+
+
+def expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri, cube_min, child_h):
+    """KN:303-329, same positional signature and return value."""
+    npair = int(np.asarray(pair_parent).shape[0])
+    verts = np.ascontiguousarray(verts, np.float64)
+    tris = np.ascontiguousarray(tris, np.int64)
+    pc = np.ascontiguousarray(parent_cells, np.int64).reshape(-1, 3)
+    pp = np.ascontiguousarray(pair_parent, np.int64)
+    pt = np.ascontiguousarray(pair_tri, np.int64)
+    cm = np.ascontiguousarray(cube_min, np.float64)
+    cells = np.zeros((8 * npair, 3), np.uint32)
+    tri = np.zeros(8 * npair, np.int32)
+    m = lib().kn_expand_pairs_ordered(_p(verts), _p(tris), _p(pc), _p(pp), _p(pt), npair, _p(cm),
+                                      float(child_h), _p(cells), _p(tri))
+    return cells[:m].copy(), tri[:m].copy()
+
+
+def raycast(origins, dirs, keys, offsets, tri_idx, verts, tris, cube_min, h, n_cells, coarse,
+            coarse_shift, morton_encode=None, threads=1):
+    """KN:361-525, same positional signature and return value (float64 inputs; the Morton
+    convention is fixed, see ``morton_encode`` above)."""
+    origins = np.ascontiguousarray(origins, np.float64)
+    dirs = np.ascontiguousarray(dirs, np.float64)
+    keys = np.ascontiguousarray(keys, np.uint64)
+    offsets = np.ascontiguousarray(offsets, np.int64)
+    tri_idx = np.ascontiguousarray(tri_idx, np.int32)
+    verts = np.ascontiguousarray(verts, np.float64)
+    tris = np.ascontiguousarray(tris, np.int64)
+    cm = np.ascontiguousarray(cube_min, np.float64)
+    n = origins.shape[0]
+    cz = None if coarse is None else np.ascontiguousarray(coarse != 0, np.uint8)
+    best_t = np.empty(n, np.float64)
+    best_tri = np.empty(n, np.int32)
+    leaf = np.empty(n, np.int64)
+    lib().kn_raycast(_p(origins), _p(dirs), n, _p(keys), keys.shape[0], _p(offsets), _p(tri_idx),
+                     _p(verts), _p(tris), _p(cm), float(h), int(n_cells), _p(cz),
+                     0 if cz is None else cz.shape[0], int(coarse_shift or 0),
+                     _p(best_t), _p(best_tri), _p(leaf), int(threads))
+    return best_t, best_tri, leaf

@@ -105,8 +105,84 @@ def _coverage_count(tri_xy, atlas):
     return KN.coverage_fill(tri_xy, atlas, atlas, out)
 
 
+def gen_expand(seed, ntri, npar, npair, dtype, snap):
+    """expand_pairs_ordered (KN:303) on random (parent cell, triangle) pairs; ``snap`` puts vertices
+    on cell faces / corners so the closed-box (touching counts) rule of KN:213-214 is exercised."""
+    rng = np.random.default_rng(seed)
+    level = 3
+    child_h = 1.0 / (1 << (level + 1))
+    cube_min = np.array([-0.5, -0.25, 0.125])
+    parent_cells = rng.integers(0, 1 << level, size=(npar, 3)).astype(np.uint32)
+    ctr = cube_min + (rng.integers(0, 1 << level, size=(ntri, 1, 3)) + 0.5) * (2.0 * child_h)
+    pts = ctr + rng.normal(0.0, 1.5 * child_h, size=(ntri, 3, 3))
+    if snap:
+        m = rng.random(pts.shape) < 0.5
+        pts[m] = (cube_min + np.round((pts - cube_min) / child_h) * child_h)[m]
+    verts = pts.reshape(-1, 3).astype(dtype)
+    tris = np.arange(3 * ntri, dtype=np.int64).reshape(ntri, 3)
+    dup = rng.random(ntri) < 0.1
+    tris[dup, 2] = tris[dup, 0]                                     # degenerate (segment) triangles
+    pair_tri = rng.integers(0, ntri, size=npair).astype(np.int32)
+    # parents near their triangle so that a good share of the octants is hit
+    want = np.clip(np.floor((pts[pair_tri].mean(1) - cube_min) / (2.0 * child_h)), 0, (1 << level) - 1)
+    far = rng.random(npair) < 0.3
+    pair_parent = np.empty(npair, np.int64)
+    for i in range(npair):
+        if far[i]:
+            pair_parent[i] = rng.integers(0, npar)
+        else:
+            d = np.abs(parent_cells.astype(np.int64) - want[i].astype(np.int64)).sum(1)
+            pair_parent[i] = int(np.argmin(d))
+    cells, tri = KN.expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri, cube_min, child_h)
+    return dict(verts=verts, tris=tris, parent_cells=parent_cells, pair_parent=pair_parent,
+                pair_tri=pair_tri, cube_min=cube_min, child_h=np.float64(child_h), cells=cells, tri=tri)
+
+
+def gen_octree_scene(level, depth, window, coarse_bits, seed, nrandom):
+    """Surface octree of an icosphere built with the REFERENCE's expand_pairs_ordered, then the
+    reference's raycast (KN:361) for a window of camera rays plus random / axis-parallel / outside /
+    zero-direction rays.  The per-level expansion inputs and outputs are stored too."""
+    rng = np.random.default_rng(seed)
+    mesh = synth.icosphere_mesh(int(level))
+    verts = np.ascontiguousarray(mesh.vertices, np.float64)
+    tris = np.ascontiguousarray(mesh.triangles, np.int64)
+    cube_min, side = helpers.bounding_cube(verts)
+    g = helpers.build_leaf_grid(KN.expand_pairs_ordered, verts, tris, cube_min, side, depth, coarse_bits)
+    cam = synth.default_camera(window, window)
+    ys, xs = np.mgrid[0:window, 0:window]
+    o, d = helpers.camera_rays(cam, np.stack([xs.ravel(), ys.ravel()], 1))
+    ro = rng.uniform(-1.6, 1.6, size=(nrandom, 3))
+    rd = rng.normal(size=(nrandom, 3))
+    rd[: nrandom // 4, rng.integers(0, 3)] = 0.0                    # axis-parallel slabs (KN:393-396)
+    rd[nrandom // 4: nrandom // 3] = np.round(rd[nrandom // 4: nrandom // 3])   # ties between t_max axes
+    rd[-3:] = 0.0                                                   # zero direction: marches in place
+    ro[-2] = 0.0
+    ro[-1] = (0.2, -0.1, 0.95)
+    origins = np.concatenate([o, ro])
+    dirs = np.concatenate([d, rd])
+    best_t, best_tri, leaf = KN.raycast(origins, dirs, g["keys"], g["offsets"], g["tri_idx"], verts, tris,
+                                        cube_min, g["h"], g["n_cells"], g["coarse"], g["coarse_shift"],
+                                        helpers.morton3)
+    nc_t, nc_tri, nc_leaf = KN.raycast(origins, dirs, g["keys"], g["offsets"], g["tri_idx"], verts, tris,
+                                       cube_min, g["h"], g["n_cells"], None, 0, helpers.morton3)
+    assert np.array_equal(nc_t, best_t) and np.array_equal(nc_tri, best_tri) and np.array_equal(nc_leaf, leaf)
+    out = dict(level=level, depth=depth, cube_min=cube_min, side=np.float64(side), origins=origins, dirs=dirs,
+               keys=g["keys"], offsets=g["offsets"], tri_idx=g["tri_idx"], h=np.float64(g["h"]),
+               n_cells=g["n_cells"], coarse=g["coarse"], coarse_shift=g["coarse_shift"],
+               best_t=best_t, best_tri=best_tri, leaf_pos=leaf)
+    for i, (c, t) in enumerate(g["levels"]):
+        out["level%d_cells" % (i + 1)] = c
+        out["level%d_tri" % (i + 1)] = t
+    return out
+
+
 def main():
     out = {}
+    out["octree_expand_a"] = gen_expand(51, 60, 40, 400, np.float64, snap=False)
+    out["octree_expand_snap"] = gen_expand(52, 60, 40, 400, np.float64, snap=True)
+    out["octree_expand_f32"] = gen_expand(53, 50, 30, 300, np.float32, snap=True)
+    out["octree_scene_d4"] = gen_octree_scene(2, 4, 24, 2, 61, 120)
+    out["octree_scene_d6"] = gen_octree_scene(3, 6, 32, 3, 62, 160)
     out["coverage_a"] = gen_coverage(11, 160, 48, 40, np.float64, dirty=False)
     out["coverage_b"] = gen_coverage(12, 160, 33, 57, np.float32, dirty=True)
     out["coverage_big"] = gen_coverage(13, 12, 96, 96, np.float64, dirty=False)
@@ -137,7 +213,8 @@ def main():
     for name, d in out.items():
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
         print(name, {k: (v.shape if hasattr(v, "shape") and getattr(v, "ndim", 0) else v) for k, v in d.items()
-                     if k in ("written", "edited_count", "fragments", "cov_count")})
+                     if k in ("written", "edited_count", "fragments", "cov_count")},
+              {k: v.shape for k, v in d.items() if k in ("cells", "keys", "best_t")})
 
 
 if __name__ == "__main__":

@@ -69,3 +69,66 @@ def random_tea_case(seed, ntri=200, w=64, h=64, plane_dtype=np.uint8, value=7, t
 def tea_args(c):
     return (c["tri_xy"], c["tri_clip"], c["ww"], c["wh"], c["depth"], c["eps"], c["sfx"], c["sfy"],
             c["bx"], c["by"], c["shape"])
+
+
+def morton3(x, y, z):
+    """Bit interleave, x in bit 0 / y in bit 1 / z in bit 2 of every triple (octant code of KN:267)."""
+    def spread(v):
+        v = np.asarray(v).astype(np.uint64) & np.uint64(0x1fffff)
+        for s, m in ((32, 0x1f00000000ffff), (16, 0x1f0000ff0000ff), (8, 0x100f00f00f00f00f),
+                     (4, 0x10c30c30c30c30c3), (2, 0x1249249249249249)):
+            v = (v | (v << np.uint64(s))) & np.uint64(m)
+        return v
+    return spread(x) | (spread(y) << np.uint64(1)) | (spread(z) << np.uint64(2))
+
+
+def bounding_cube(verts, pad=1e-3):
+    """Root cube of SPEC:333: the bounding box cubified to its largest extent (slightly padded)."""
+    lo, hi = verts.min(0), verts.max(0)
+    side = float((hi - lo).max()) * (1.0 + pad)
+    centre = 0.5 * (lo + hi)
+    return (centre - 0.5 * side).astype(np.float64), side
+
+
+def build_leaf_grid(expand, verts, tris, cube_min, side, depth, coarse_bits=2):
+    """Level-by-level surface octree built with ``expand`` (any implementation of
+    KN:303 ``expand_pairs_ordered``); returns the leaf arrays ``raycast`` (KN:361) consumes and the
+    per-level (cells, tri) lists for comparing implementations."""
+    T = tris.shape[0]
+    parent_cells = np.zeros((1, 3), np.uint32)
+    pair_parent = np.zeros(T, np.int64)
+    pair_tri = np.arange(T, dtype=np.int32)
+    levels = []
+    cells = np.zeros((T, 3), np.uint32)
+    for lvl in range(1, depth + 1):
+        child_h = side / float(1 << lvl)
+        cells, pair_tri = expand(verts, tris, parent_cells, pair_parent, pair_tri, cube_min, child_h)
+        levels.append((cells, pair_tri))
+        key = morton3(cells[:, 0], cells[:, 1], cells[:, 2])
+        ukeys, first, inv = np.unique(key, return_index=True, return_inverse=True)
+        parent_cells, pair_parent = cells[first], inv.astype(np.int64)
+    key = morton3(cells[:, 0], cells[:, 1], cells[:, 2])
+    order = np.lexsort((pair_tri, key))
+    keys, counts = np.unique(key[order], return_counts=True)
+    offsets = np.zeros(keys.shape[0] + 1, np.int64)
+    offsets[1:] = np.cumsum(counts)
+    n_cells = 1 << depth
+    cb = min(coarse_bits, depth)
+    shift = depth - cb
+    coarse = np.zeros((1 << cb,) * 3, np.uint8)
+    coarse[cells[:, 0] >> shift, cells[:, 1] >> shift, cells[:, 2] >> shift] = 1
+    return dict(keys=keys.astype(np.uint64), offsets=offsets, tri_idx=pair_tri[order].astype(np.int32),
+                h=side / float(n_cells), n_cells=n_cells, coarse=coarse, coarse_shift=shift,
+                levels=levels)
+
+
+def camera_rays(cam, pixels):
+    """World-space rays through window pixel centres (origin = eye), float64; ``pixels`` (N,2)."""
+    inv = np.linalg.inv(np.asarray(cam.mvp, np.float64))
+    px = (np.asarray(pixels, np.float64) + 0.5)
+    ndc = np.stack([px[:, 0] / cam.width * 2.0 - 1.0, px[:, 1] / cam.height * 2.0 - 1.0], 1)
+    near = np.concatenate([ndc, -np.ones((len(px), 1)), np.ones((len(px), 1))], 1) @ inv.T
+    far = np.concatenate([ndc, np.ones((len(px), 1)), np.ones((len(px), 1))], 1) @ inv.T
+    near, far = near[:, :3] / near[:, 3:], far[:, :3] / far[:, 3:]
+    d = far - near
+    return np.ascontiguousarray(near), np.ascontiguousarray(d / np.linalg.norm(d, axis=1, keepdims=True))

@@ -179,3 +179,64 @@ def test_oracle_coverage_matches_exact_rational_bruteforce(seed):
     assert np.array_equal(sm["tri_id"], brute.owner(tri, w, h))
     for r in (1, 2):
         assert np.array_equal(kn.outline(want, r), brute.outline(want, r))
+
+
+# ---- octree baseline kernels: KN:303 expand_pairs_ordered, KN:361 raycast ----
+
+def _icosphere_arrays(level):
+    from paper_2501_14807_b200 import synth
+    mesh = synth.icosphere_mesh(int(level))
+    return (np.ascontiguousarray(mesh.vertices, np.float64),
+            np.ascontiguousarray(mesh.triangles, np.int64))
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("octree_expand"))
+def test_oracle_expand_pairs_matches_reference(name):
+    f = helpers.golden(name)
+    cells, tri = kn.expand_pairs_ordered(f["verts"], f["tris"], f["parent_cells"], f["pair_parent"],
+                                         f["pair_tri"], f["cube_min"], float(f["child_h"]))
+    assert cells.dtype == np.uint32 and tri.dtype == np.int32
+    assert np.array_equal(cells, f["cells"]) and np.array_equal(tri, f["tri"])
+
+
+@pytest.mark.parametrize("name", helpers.golden_names("octree_scene"))
+def test_oracle_octree_build_and_raycast_match_reference(name):
+    f = helpers.golden(name)
+    verts, tris = _icosphere_arrays(f["level"])
+    g = helpers.build_leaf_grid(kn.expand_pairs_ordered, verts, tris, f["cube_min"], float(f["side"]),
+                                int(f["depth"]), 2)
+    for i, (c, t) in enumerate(g["levels"]):
+        assert np.array_equal(c, f["level%d_cells" % (i + 1)])
+        assert np.array_equal(t, f["level%d_tri" % (i + 1)])
+    assert np.array_equal(g["keys"], f["keys"]) and np.array_equal(g["offsets"], f["offsets"])
+    for coarse in (f["coarse"], None):
+        for threads in (1, 3):
+            bt, btri, leaf = kn.raycast(f["origins"], f["dirs"], f["keys"], f["offsets"], f["tri_idx"],
+                                        verts, tris, f["cube_min"], float(f["h"]), int(f["n_cells"]),
+                                        coarse, int(f["coarse_shift"]), threads=threads)
+            assert np.array_equal(bt, f["best_t"])               # bit-exact incl. inf for misses
+            assert np.array_equal(btri, f["best_tri"]) and np.array_equal(leaf, f["leaf_pos"])
+    assert np.isfinite(f["best_t"]).sum() > 100 and (f["best_tri"] < 0).sum() > 100
+
+
+def test_octree_spec_known_answers():
+    """SPEC:346-349: depth 0 = one leaf with every triangle; unit cube at depth 1 = all 8 children;
+    flat square at z = -0.5 in [-1,1]^3 = exactly the four lower octants."""
+    from paper_2501_14807_b200 import synth
+    sq = synth.flat_square_mesh(1.0)
+    v = np.ascontiguousarray(sq.vertices, np.float64)
+    v = (v - v.mean(0)) * 1.6
+    v[:, 2] = -0.5
+    t = np.ascontiguousarray(sq.triangles, np.int64)
+    cells, tri = kn.expand_pairs_ordered(v, t, np.zeros((1, 3), np.uint32), np.zeros(len(t), np.int64),
+                                         np.arange(len(t), dtype=np.int32), np.array([-1.0, -1.0, -1.0]), 1.0)
+    assert set(map(tuple, cells.tolist())) == {(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0)}
+    # a face lying exactly on the shared plane z = 0 touches both halves (closed cubes, SPEC:386)
+    v[:, 2] = 0.0
+    cells, _ = kn.expand_pairs_ordered(v, t, np.zeros((1, 3), np.uint32), np.zeros(len(t), np.int64),
+                                       np.arange(len(t), dtype=np.int32), np.array([-1.0, -1.0, -1.0]), 1.0)
+    assert len(set(map(tuple, cells.tolist()))) == 8
+    # empty input (KN:307-309)
+    cells, tri = kn.expand_pairs_ordered(v, t, np.zeros((1, 3), np.uint32), np.zeros(0, np.int64),
+                                         np.zeros(0, np.int32), np.array([-1.0, -1.0, -1.0]), 1.0)
+    assert cells.shape == (0, 3) and tri.shape == (0,)
