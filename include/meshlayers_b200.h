@@ -320,6 +320,37 @@ int ml_resolve_display(const void* data, int kind, const uint8_t* mask, int64_t 
 int ml_pack_mask(const uint8_t* mask, int64_t n, uint8_t* bits, void* stream);
 int ml_unpack_mask(const uint8_t* bits, int64_t n, uint8_t* mask, void* stream);
 
+/* ---- octree baseline kernels: the remaining two callables of the reference's
+ * compiled-backend slot.  float64 geometry, int32 triangle indices, uint32 cell coordinates.
+ *
+ * KN:303-329 expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri, cube_min, child_h)
+ *   -> (child_cells uint32 (M,3), child_tri int32 (M,)): every (parent cell, triangle) pair is tested
+ * against the parent's 8 child cubes with the closed-box separating-axis test of KN:208-258; output
+ * order is pair-major, octant-minor (octant = x | y<<1 | z<<2).  M is data dependent, so the device
+ * form is two stream-ordered calls sharing `workspace`: _count writes M to *total (device), the
+ * caller sizes the outputs, _emit writes them.  cube_min is a HOST array of 3 doubles. */
+size_t ml_expand_pairs_workspace_bytes(int64_t npair);
+int ml_expand_pairs_count(const double* verts, const int32_t* tris, const uint32_t* parent_cells,
+                          const int32_t* pair_parent, const int32_t* pair_tri, int64_t npair,
+                          const double* cube_min, double child_h, void* workspace, size_t workspace_bytes,
+                          uint64_t* total, void* stream);
+int ml_expand_pairs_emit(const uint32_t* parent_cells, const int32_t* pair_parent, const int32_t* pair_tri,
+                         int64_t npair, const void* workspace, uint32_t* out_cells, int32_t* out_tri,
+                         void* stream);
+
+/* KN:361-525 raycast(origins, dirs, keys, offsets, tri_idx, verts, tris, cube_min, h, n_cells, coarse,
+ *   coarse_shift, morton_encode) -> (best_t, best_tri, leaf_pos): 3D-DDA through the n_cells^3 leaf grid,
+ * Moeller-Trumbore (KN:335-358) against the triangle list of every visited leaf found in the sorted
+ * `keys` (nkeys Morton codes; leaf i owns tri_idx[offsets[i] .. offsets[i+1])), best hit = lexicographic
+ * minimum of (t, triangle index), leaf_pos = index in `keys` of the leaf containing the hit point (-1 and
+ * t = +inf on a miss).  morton_encode is fixed to the bit interleave with x in bit 0, y in bit 1, z in
+ * bit 2 of every triple (n_cells <= 2^21).  coarse: optional (coarse_side^3 bytes, [x][y][z]) occupancy
+ * map of the cells >> coarse_shift, NULL = none (KN:447).  cube_min is a HOST array of 3 doubles. */
+int ml_raycast(const double* origins, const double* dirs, int64_t nrays, const uint64_t* keys, int64_t nkeys,
+               const int64_t* offsets, const int32_t* tri_idx, const double* verts, const int32_t* tris,
+               const double* cube_min, double h, int64_t n_cells, const uint8_t* coarse, int64_t coarse_side,
+               int coarse_shift, double* best_t, int32_t* best_tri, int64_t* leaf_pos, void* stream);
+
 /* ---- host-buffer entry points: exact drop-ins for the reference's numpy signatures ------------
  * All pointers are HOST pointers; the call copies inputs to the device, runs the kernels above,
  * copies the planes back and synchronises.  tri arrays are float64 (the reference widens to
@@ -334,6 +365,18 @@ int ml_raster_tea_host(const double* tri_xy, const double* tri_clip, int64_t ntr
                        const uint8_t* shape, int64_t shape_w, int64_t shape_h,
                        void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
                        int64_t width, int64_t height, int64_t* edited_count, int64_t* fragments);
+
+/* KN:303: *count = M; rows are written only when M <= capacity (re-call with a larger buffer otherwise) */
+int ml_expand_pairs_ordered_host(const double* verts, int64_t nverts, const int32_t* tris, int64_t ntri,
+                                 const uint32_t* parent_cells, int64_t nparents, const int32_t* pair_parent,
+                                 const int32_t* pair_tri, int64_t npair, const double* cube_min, double child_h,
+                                 uint32_t* out_cells, int32_t* out_tri, int64_t capacity, int64_t* count);
+/* KN:361 */
+int ml_raycast_host(const double* origins, const double* dirs, int64_t nrays, const uint64_t* keys, int64_t nkeys,
+                    const int64_t* offsets, const int32_t* tri_idx, const double* verts, int64_t nverts,
+                    const int32_t* tris, int64_t ntri, const double* cube_min, double h, int64_t n_cells,
+                    const uint8_t* coarse, int64_t coarse_side, int coarse_shift,
+                    double* best_t, int32_t* best_tri, int64_t* leaf_pos);
 
 #ifdef __cplusplus
 }

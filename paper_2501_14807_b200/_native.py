@@ -10,6 +10,13 @@ return conventions:
     raster_tea(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
                shape, data, mask, edited, value) -> (int, int)             KN:135-136
 
+and so do the two octree-baseline kernels (the paper's competitor):
+
+    expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri,
+                         cube_min, child_h) -> (cells, tri)                KN:303
+    raycast(origins, dirs, keys, offsets, tri_idx, verts, tris, cube_min, h,
+            n_cells, coarse, coarse_shift, morton_encode) -> (t, tri, leaf) KN:361
+
 They accept either numpy arrays (HOST buffers, exactly like the reference: the call uploads,
 runs the CUDA kernels, downloads the planes in place) or torch CUDA tensors (device resident:
 nothing is copied).  Everything below them is an extension for the north-star operations
@@ -122,6 +129,13 @@ def lib():
         "ml_raster_depth_host": (i32, [vp, vp, i64, vp, i64, i64, vp]),
         "ml_raster_tea_host": (i32, [vp, vp, i64, dbl, dbl, vp, i64, i64, dbl, i32, dbl, dbl, dbl, dbl,
                                      vp, i64, i64, vp, i32, u32, vp, vp, i64, i64, vp, vp]),
+        "ml_expand_pairs_workspace_bytes": (sz, [i64]),
+        "ml_expand_pairs_count": (i32, [vp, vp, vp, vp, vp, i64, vp, dbl, vp, sz, vp, vp]),
+        "ml_expand_pairs_emit": (i32, [vp, vp, vp, i64, vp, vp, vp, vp]),
+        "ml_raycast": (i32, [vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, dbl, i64, vp, i64, i32, vp, vp, vp, vp]),
+        "ml_expand_pairs_ordered_host": (i32, [vp, i64, vp, i64, vp, i64, vp, vp, i64, vp, dbl, vp, vp, i64, vp]),
+        "ml_raycast_host": (i32, [vp, vp, i64, vp, i64, vp, vp, vp, i64, vp, i64, vp, dbl, i64, vp, i64, i32,
+                                  vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -141,7 +155,9 @@ EXPORTED_SYMBOLS = (
     "ml_select_threshold", "ml_plane_tile_range", "ml_select_threshold_tiles", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_apply_padding_tiles", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
-    "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host")
+    "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host",
+    "ml_expand_pairs_workspace_bytes", "ml_expand_pairs_count", "ml_expand_pairs_emit", "ml_raycast",
+    "ml_expand_pairs_ordered_host", "ml_raycast_host")
 
 
 def _check(rc):
@@ -426,6 +442,193 @@ def _as_dev_bytes(a, device):
     elif _np_dtype_of(a).itemsize != 1:
         a = (a != 0).to(torch.uint8)
     return a.contiguous()
+
+
+# ---- octree baseline kernels (KN:303, KN:361) -------------------------------------------------
+
+def morton_encode(x, y, z):
+    """The Morton convention compiled into ``raycast``: bit interleave with x in bit 0, y in bit 1,
+    z in bit 2 of every triple (the octant code of KN:267), 21 bits per axis.  This is the callable
+    to hand to the reference's ``raycast`` (KN:362) when comparing; numpy arrays or torch tensors."""
+    if _is_cuda_tensor(x) or type(x).__module__.startswith("torch"):
+        torch = _torch()
+
+        def spread(v):
+            v = v.to(torch.int64) & 0x1fffff
+            for sh, m in ((32, 0x1f00000000ffff), (16, 0x1f0000ff0000ff), (8, 0x100f00f00f00f00f),
+                          (4, 0x10c30c30c30c30c3), (2, 0x1249249249249249)):
+                v = (v | (v << sh)) & m
+            return v
+        return spread(x) | (spread(y) << 1) | (spread(z) << 2)         # int64: 63 bits are enough
+
+    def spread(v):
+        v = np.asarray(v).astype(np.uint64) & np.uint64(0x1fffff)
+        for sh, m in ((32, 0x1f00000000ffff), (16, 0x1f0000ff0000ff), (8, 0x100f00f00f00f00f),
+                      (4, 0x10c30c30c30c30c3), (2, 0x1249249249249249)):
+            v = (v | (v << np.uint64(sh))) & np.uint64(m)
+        return v
+    return spread(x) | (spread(y) << np.uint64(1)) | (spread(z) << np.uint64(2))
+
+
+_MORTON_PROBE = (np.array([1, 0, 0, 5, 65535, 2], np.uint64), np.array([0, 1, 0, 3, 1, 40000], np.uint64),
+                 np.array([0, 0, 1, 6, 7, 9], np.uint64))
+
+
+def _check_morton(fn):
+    """``raycast`` takes the key function as an argument in the reference (KN:362); the kernel has one
+    convention compiled in, so a different callable must fail loudly instead of missing every leaf."""
+    if fn is None or fn is morton_encode:
+        return
+    got = np.asarray(fn(*_MORTON_PROBE)).astype(np.uint64)
+    if not np.array_equal(got, morton_encode(*_MORTON_PROBE)):
+        raise TargetMismatch("raycast: morton_encode differs from the compiled convention "
+                             "(bit interleave, x lowest; see _native.morton_encode)")
+
+
+def _host_array(a, dtype, tail=None):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    if tail is not None and a.shape[1:] != tail:
+        raise TargetMismatch("expected an array of shape (N,%s), got %s" % (tail, a.shape))
+    return a
+
+
+def _dev_array(a, dtype, device, tail=None):
+    torch = _torch()
+    if not _is_cuda_tensor(a):
+        a = np.ascontiguousarray(a)
+        if a.dtype.kind == "u" and a.dtype.itemsize > 1:              # torch has no arithmetic on them
+            a = a.astype(np.int64)
+        a = torch.from_numpy(a).to(device)
+    a = a.to(dtype).contiguous()
+    if tail is not None and tuple(a.shape[1:]) != tail:
+        raise TargetMismatch("expected an array of shape (N,%s), got %s" % (tail, tuple(a.shape)))
+    return a
+
+
+def _cube_min3(cube_min):
+    cm = cube_min.detach().cpu().numpy() if hasattr(cube_min, "detach") else cube_min
+    cm = np.ascontiguousarray(cm, dtype=np.float64).reshape(-1)
+    if cm.shape[0] != 3:
+        raise TargetMismatch("cube_min must have 3 components")
+    return cm
+
+
+def expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri, cube_min, child_h):
+    """KN:303-329: refine (parent cell, triangle) pairs one octree level down; returns
+    ``(child_cells uint32 (M,3), child_tri int32 (M,))`` pair-major, octant-minor.  numpy inputs
+    (HOST buffers, like the reference) return numpy arrays; if ``pair_tri`` is a torch CUDA tensor
+    everything stays on the device and torch tensors come back (cells as int32: coordinates are
+    below 2^21, so the bits equal the reference's uint32).
+    Geometry is widened to float64 exactly as KN:312-324 does before its first arithmetic."""
+    L = lib()
+    cm = _cube_min3(cube_min)
+    if not _is_cuda_tensor(pair_tri):
+        v = _host_array(verts, np.float64, (3,))
+        t = _host_array(tris, np.int32, (3,))
+        pc = _host_array(parent_cells, np.uint32, (3,))
+        pp = _host_array(pair_parent, np.int32)
+        pt = _host_array(pair_tri, np.int32)
+        npair = pp.shape[0]
+        if pt.shape[0] != npair:
+            raise TargetMismatch("pair_parent / pair_tri lengths differ")
+        cap = min(8 * npair, max(2 * npair, 4096))
+        count = C.c_int64(0)
+        while True:
+            cells = np.empty((cap, 3), np.uint32)
+            tri = np.empty(cap, np.int32)
+            _check(L.ml_expand_pairs_ordered_host(v.ctypes.data, v.shape[0], t.ctypes.data, t.shape[0],
+                                                  pc.ctypes.data, pc.shape[0], pp.ctypes.data, pt.ctypes.data,
+                                                  npair, cm.ctypes.data, float(child_h), cells.ctypes.data,
+                                                  tri.ctypes.data, cap, C.addressof(count)))
+            if count.value <= cap:
+                break
+            cap = int(count.value)
+        return cells[:count.value].copy(), tri[:count.value].copy()
+    torch = require_cuda()
+    dev = pair_tri.device
+    v = _dev_array(verts, torch.float64, dev, (3,))
+    t = _dev_array(tris, torch.int32, dev, (3,))
+    pc = _dev_array(parent_cells, torch.int32, dev, (3,))
+    pp = _dev_array(pair_parent, torch.int32, dev)
+    pt = _dev_array(pair_tri, torch.int32, dev)
+    npair = pp.shape[0]
+    if pt.shape[0] != npair:
+        raise TargetMismatch("pair_parent / pair_tri lengths differ")
+    nb = int(L.ml_expand_pairs_workspace_bytes(npair))
+    ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(L.ml_expand_pairs_count(_ptr(v), _ptr(t), _ptr(pc), _ptr(pp), _ptr(pt), npair, cm.ctypes.data,
+                                   float(child_h), _ptr(ws), nb, _ptr(total), _stream()))
+    m = int(total.item())
+    cells = torch.empty((m, 3), dtype=torch.int32, device=dev)        # coordinates < 2^21: int32 == uint32
+    tri = torch.empty(m, dtype=torch.int32, device=dev)
+    if m:
+        _check(L.ml_expand_pairs_emit(_ptr(pc), _ptr(pp), _ptr(pt), npair, _ptr(ws), _ptr(cells), _ptr(tri),
+                                      _stream()))
+    return cells, tri
+
+
+def raycast(origins, dirs, keys, offsets, tri_idx, verts, tris, cube_min, h, n_cells, coarse,
+            coarse_shift, morton_encode=None):
+    """KN:361-525: march every ray front to back through the leaf grid; returns
+    ``(best_t float64, best_tri int32, leaf_pos int64)``.  numpy inputs return numpy arrays, torch CUDA
+    ``origins`` keep everything on the device.  float64 geometry (the reference would compute partly in
+    float32 for float32 inputs, KN:340, 381; such inputs are widened first here).  ``morton_encode`` must
+    be the compiled convention (``_native.morton_encode``) or None."""
+    L = lib()
+    _check_morton(morton_encode)
+    cm = _cube_min3(cube_min)
+    n_cells = int(n_cells)
+    shift = int(coarse_shift or 0)
+    if coarse is not None and (coarse.ndim != 3 or len(set(coarse.shape)) != 1):
+        raise TargetMismatch("coarse must be a cubic 3-D occupancy array")
+    if not _is_cuda_tensor(origins):
+        o = _host_array(origins, np.float64, (3,))
+        d = _host_array(dirs, np.float64, (3,))
+        k = _host_array(keys, np.uint64)
+        off = _host_array(offsets, np.int64)
+        idx = _host_array(tri_idx, np.int32)
+        v = _host_array(verts, np.float64, (3,))
+        t = _host_array(tris, np.int32, (3,))
+        if d.shape != o.shape or off.shape[0] != k.shape[0] + 1:
+            raise TargetMismatch("raycast: origins/dirs or keys/offsets shapes disagree")
+        cz = None if coarse is None else np.ascontiguousarray(np.asarray(coarse) != 0, dtype=np.uint8)
+        n = o.shape[0]
+        best_t = np.full(n, np.inf)
+        best_tri = np.full(n, -1, np.int32)
+        leaf = np.full(n, -1, np.int64)
+        _check(L.ml_raycast_host(o.ctypes.data, d.ctypes.data, n, k.ctypes.data, k.shape[0], off.ctypes.data,
+                                 idx.ctypes.data, v.ctypes.data, v.shape[0], t.ctypes.data, t.shape[0],
+                                 cm.ctypes.data, float(h), n_cells, None if cz is None else cz.ctypes.data,
+                                 0 if cz is None else cz.shape[0], shift, best_t.ctypes.data,
+                                 best_tri.ctypes.data, leaf.ctypes.data))
+        return best_t, best_tri, leaf
+    torch = require_cuda()
+    dev = origins.device
+    o = _dev_array(origins, torch.float64, dev, (3,))
+    d = _dev_array(dirs, torch.float64, dev, (3,))
+    if _is_cuda_tensor(keys) and keys.dtype in (torch.int64, torch.uint64):
+        k = keys.contiguous()
+    else:
+        k = torch.from_numpy(np.ascontiguousarray(keys, dtype=np.uint64).view(np.int64)).to(dev)
+    off = _dev_array(offsets, torch.int64, dev)
+    idx = _dev_array(tri_idx, torch.int32, dev)
+    v = _dev_array(verts, torch.float64, dev, (3,))
+    t = _dev_array(tris, torch.int32, dev, (3,))
+    if d.shape != o.shape or off.shape[0] != k.shape[0] + 1:
+        raise TargetMismatch("raycast: origins/dirs or keys/offsets shapes disagree")
+    cz = None
+    if coarse is not None:
+        cz = coarse if _is_cuda_tensor(coarse) else torch.from_numpy(np.ascontiguousarray(coarse)).to(dev)
+        cz = (cz != 0).to(torch.uint8).contiguous()
+    n = o.shape[0]
+    best_t = torch.empty(n, dtype=torch.float64, device=dev)
+    best_tri = torch.empty(n, dtype=torch.int32, device=dev)
+    leaf = torch.empty(n, dtype=torch.int64, device=dev)
+    _check(L.ml_raycast(_ptr(o), _ptr(d), n, _ptr(k), k.shape[0], _ptr(off), _ptr(idx), _ptr(v), _ptr(t),
+                        cm.ctypes.data, float(h), n_cells, _ptr(cz), 0 if cz is None else cz.shape[0], shift,
+                        _ptr(best_t), _ptr(best_tri), _ptr(leaf), _stream()))
+    return best_t, best_tri, leaf
 
 
 # =============================================================================================
