@@ -28,5 +28,7 @@ from .editing import (EditingTool, EditProjection, EditResult, StrokeContext, ap
                       select_sphere, select_sphere_batch, select_threshold, stroke, stroke_gesture)
 from .display import Palette, map_value_to_color, resolve_display
 from .layer_io import decode_layer, encode_layer, load_layer, save_layer
+from .octree import (OctreeLayer, SurfaceOctree, build_octree, create_octree_layer, octree_edit,
+                     octree_precision, octree_upload_size)
 
 __version__ = "0.1.0"

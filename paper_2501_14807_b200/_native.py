@@ -513,13 +513,15 @@ def _cube_min3(cube_min):
     return cm
 
 
-def expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri, cube_min, child_h):
+def expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri, cube_min, child_h, *,
+                         max_rows=None):
     """KN:303-329: refine (parent cell, triangle) pairs one octree level down; returns
     ``(child_cells uint32 (M,3), child_tri int32 (M,))`` pair-major, octant-minor.  numpy inputs
     (HOST buffers, like the reference) return numpy arrays; if ``pair_tri`` is a torch CUDA tensor
     everything stays on the device and torch tensors come back (cells as int32: coordinates are
     below 2^21, so the bits equal the reference's uint32).
-    Geometry is widened to float64 exactly as KN:312-324 does before its first arithmetic."""
+    Geometry is widened to float64 exactly as KN:312-324 does before its first arithmetic.
+    ``max_rows`` (device form): raise ``MemoryBudgetExceeded`` before allocating more output rows."""
     L = lib()
     cm = _cube_min3(cube_min)
     if not _is_cuda_tensor(pair_tri):
@@ -560,6 +562,10 @@ def expand_pairs_ordered(verts, tris, parent_cells, pair_parent, pair_tri, cube_
     _check(L.ml_expand_pairs_count(_ptr(v), _ptr(t), _ptr(pc), _ptr(pp), _ptr(pt), npair, cm.ctypes.data,
                                    float(child_h), _ptr(ws), nb, _ptr(total), _stream()))
     m = int(total.item())
+    if max_rows is not None and m > max_rows:
+        from .errors import MemoryBudgetExceeded
+        raise MemoryBudgetExceeded("octree level needs %d (cell, triangle) rows, the budget allows %d"
+                                   % (m, max_rows))
     cells = torch.empty((m, 3), dtype=torch.int32, device=dev)        # coordinates < 2^21: int32 == uint32
     tri = torch.empty(m, dtype=torch.int32, device=dev)
     if m:

@@ -6,7 +6,7 @@ engine, emitted as CSV with the frozen column set of SPEC.md:549.
 
 Plan JSON (every key optional except ``meshes``):
     {"meshes": ["sphere:5", "terrain:707", "square"],   # procedural stand-ins
-     "engine": "texture",                                # the octree engine is out of scope here
+     "engine": "texture",                                # or "octree" (levels = depths)
      "resolutions": [2048, 4096, 8192],                  # SPEC.md:505 defaults
      "depths": [11, 12, 13],                             # matched pairwise with resolutions
      "radii": [10, 40, 70, 100, 200],                    # px, Fig 5
@@ -14,8 +14,10 @@ Plan JSON (every key optional except ``meshes``):
 
 The timed call is ``editing.stroke`` (TEA + TPA, the edit the paper times), measured
 with CUDA events around the engine call only, one warm-up discarded, medians over
-the completed repetitions.  The octree engine (the paper's CPU
-competitor) is not part of this package: ``engine="octree"`` raises ``BackendUnavailable``.
+the completed repetitions.  ``engine="octree"`` runs the OCT-TR baseline of
+``octree.py`` (the paper's CPU competitor, here on the same GPU kernels' C ABI): its timed
+call is ``octree_edit`` (ray set-up on the host + ``raycast`` + leaf update), timed with the host clock
+around a device synchronise because the edit has host work the events would not see.
 """
 import csv
 import hashlib
@@ -27,7 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native, synth
-from .errors import BackendUnavailable, BadRequest, MemoryBudgetExceeded
+from .errors import BadRequest, MemoryBudgetExceeded
 
 #: SPEC.md:549 -- column set and order are frozen (golden-file test: tests/test_bench_csv.py)
 CSV_COLUMNS = ("mesh", "engine", "level", "radius", "rep", "time_ms", "cells", "transfer_bytes",
@@ -221,17 +223,59 @@ def _tool(camera, radius):
     return EditingTool(px=0.5 * camera.width, py=0.5 * camera.height, shape=synth.circle_shape(radius), value=7)
 
 
-def _require_texture(plan):
-    if plan.engine != "texture":
-        raise BackendUnavailable("the octree baseline (SPEC.md:327) is out of scope of this package; "
-                                 "only engine='texture' is implemented")
+class _OctreeSetup:
+    """What the octree engine builds once per (mesh, depth): the surface octree and one uint8 layer."""
+
+    def __init__(self, mesh, depth, budget_bytes=0):
+        from . import octree
+        self.octree = octree.build_octree(mesh, depth, budget_bytes=budget_bytes)
+        self.layer = octree.create_octree_layer(self.octree, "uint8")
+        self.build_ms = self.octree.build_ms
+        self.peak_bytes = self.octree.peak_bytes
+
+
+def _octree_radius_sweep(plan):
+    import time
+    from . import octree
+    torch = _native.require_cuda()
+    records = []
+    for spec in plan.meshes:
+        mesh = make_mesh(spec)
+        camera = make_camera(spec, plan.window)
+        for level in plan.levels:
+            try:
+                setup = _OctreeSetup(mesh, level, plan.budget_bytes)
+            except MemoryBudgetExceeded:
+                torch.cuda.empty_cache()
+                records += [BenchRecord(spec, plan.engine, level, r, outcome="memory_budget_exceeded")
+                            for r in plan.radii]
+                continue
+            for radius in plan.radii:
+                tool = _tool(camera, radius)
+                rec = BenchRecord(spec, plan.engine, level, radius, build_ms=setup.build_ms,
+                                  peak_bytes=setup.peak_bytes)
+                res = None
+                for rep in range(plan.repetitions + 1):              # rep 0 = discarded warm-up
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    res = octree.octree_edit(setup.octree, setup.layer, mesh, camera, tool)
+                    torch.cuda.synchronize()
+                    if rep:
+                        rec.times_ms.append((time.perf_counter() - t0) * 1e3)
+                rec.cells = res.edited_count
+                rec.transfer_bytes = res.transfer_bytes
+                records.append(rec)
+            del setup
+            torch.cuda.empty_cache()
+    return records
 
 
 def run_radius_sweep(plan, cull=True):
     """one record per (mesh, level, radius); identical camera and stroke position
     for every point.  A level over the plan's memory budget is recorded as a missing data point."""
     from . import editing
-    _require_texture(plan)
+    if plan.engine == "octree":
+        return _octree_radius_sweep(plan)
     torch = _native.require_cuda()
     records = []
     for spec in plan.meshes:
@@ -275,7 +319,23 @@ def run_transfer_report(plan):
     """CPU->GPU bytes per stroke; the texture engine moves the 64-byte matrix in
     every configuration."""
     from .editing import TRANSFER_BYTES_PER_STROKE
-    _require_texture(plan)
+    if plan.engine == "octree":                                      # SPEC.md:526: crossed leaves x 4
+        from . import octree
+        out = []
+        for spec in plan.meshes:
+            mesh = make_mesh(spec)
+            for level in plan.levels:
+                try:
+                    tree = octree.build_octree(mesh, level, budget_bytes=plan.budget_bytes)
+                except MemoryBudgetExceeded:
+                    out += [BenchRecord(spec, plan.engine, level, r, outcome="memory_budget_exceeded")
+                            for r in plan.radii]
+                    continue
+                out += [BenchRecord(spec, plan.engine, level, r, cells=tree.leaf_count,
+                                    transfer_bytes=octree.octree_upload_size(tree), build_ms=tree.build_ms,
+                                    peak_bytes=tree.peak_bytes) for r in plan.radii]
+                del tree
+        return out
     return [BenchRecord(spec, plan.engine, level, r, transfer_bytes=TRANSFER_BYTES_PER_STROKE)
             for spec in plan.meshes for level in plan.levels for r in plan.radii]
 
@@ -284,13 +344,18 @@ def run_precision_table(plan):
     """layer precision = surface area / covered texels, in cm^2.  Returns dicts
     {mesh, level, covered, area_cm2, precision_cm2}."""
     from . import layer_core, mesh_core
-    _require_texture(plan)
     _native.require_cuda()
     out = []
     for spec in plan.meshes:
         mesh = make_mesh(spec)
         area_cm2 = mesh_core.mesh_surface_area(mesh) * plan.units_to_cm ** 2
         for level in plan.levels:
+            if plan.engine == "octree":                              # SPEC.md:369: area / crossed leaves
+                from . import octree
+                tree = octree.build_octree(mesh, level, budget_bytes=plan.budget_bytes)
+                out.append({"mesh": spec, "level": level, "covered": tree.leaf_count, "area_cm2": area_cm2,
+                            "precision_cm2": octree.octree_precision(tree, mesh, plan.units_to_cm)})
+                continue
             covered = int(mesh_core.uv_coverage(mesh, level).sum().item())
             out.append({"mesh": spec, "level": level, "covered": covered, "area_cm2": area_cm2,
                         "precision_cm2": layer_core.layer_precision(covered, area_cm2) if covered else None})

@@ -54,10 +54,16 @@ def test_transfer_report_is_64_bytes_everywhere():
     assert len(recs) == 3 * 3 * 5 and {r.transfer_bytes for r in recs} == {64}
 
 
-def test_octree_engine_is_out_of_scope():
-    plan = bench.BenchPlan(meshes=["square"], engine="octree")
+def test_octree_engine_has_no_cpu_fallback():
+    """The octree baseline runs on the CUDA kernels like everything else: without a device it raises."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    plan = bench.BenchPlan(meshes=["square"], engine="octree", resolutions=(64,), depths=(2,))
     with pytest.raises(ml.BackendUnavailable):
         bench.run_transfer_report(plan)
+    with pytest.raises(ml.BackendUnavailable):
+        bench.run_radius_sweep(plan)
 
 
 def test_stroke_input_hash_depends_on_every_input():
