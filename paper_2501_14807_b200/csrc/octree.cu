@@ -418,7 +418,7 @@ int ml_raycast(const double* origins, const double* dirs, int64_t nrays, const u
     for (int k = 0; k < 3; ++k) a.cmin[k] = cube_min[k];
     a.coarse = coarse; a.coarse_side = coarse_side; a.coarse_shift = coarse_shift;
     a.best_t = best_t; a.best_tri = best_tri; a.leaf_pos = leaf_pos;
-    raycast_kernel<<<(unsigned)((nrays + 127) / 128), 128, 0, (cudaStream_t)stream>>>(a);
+    raycast_kernel<<<(unsigned)((nrays + 63) / 64), 64, 0, (cudaStream_t)stream>>>(a);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

@@ -83,7 +83,7 @@ class OctreeEditResult:
     """edited leaf set (indices into the octree's key order), rays cast, transfer bytes."""
     edited_leaves: object
     rays: int
-    hits: int
+    _hits: object
     transfer_bytes: int
     duration_ms: float = 0.0
     _cache: dict = field(default_factory=dict)
@@ -91,6 +91,11 @@ class OctreeEditResult:
     @property
     def edited_count(self):
         return int(self.edited_leaves.shape[0])
+
+    @property
+    def hits(self):
+        """Rays whose nearest hit lies in a leaf of the octree (read from the device on demand)."""
+        return int(self._hits)
 
 
 def bounding_cube(vertices, pad=1e-3):
@@ -176,33 +181,44 @@ def create_octree_layer(octree, kind="uint8", device="cuda"):
                        valid=torch.zeros(n, dtype=torch.bool, device=device), kind=kind)
 
 
-def tool_rays(camera, tool):
+def tool_rays(camera, tool, device=None):
     """One ray per window pixel inside the tool shape: pixel centres through the inverse
-    view-projection, origin on the near plane, unit direction; float64 (N,3) arrays.  A pixel is
-    inside the tool when its centre maps into the tool bitmap through the texture engine's own tool
-    map (KN:187-193 with the factors of ``compute_tool_projection``; half-open at the far edges so that
-    a (2r+1)-pixel square covers (2r+1)^2 pixels): both engines edit under one footprint."""
-    shape = tool.shape.cpu().numpy() if _native._is_cuda_tensor(tool.shape) else np.asarray(tool.shape)
-    th, tw = shape.shape
+    view-projection, origin on the near plane, unit direction; float64 (N,3).  A pixel is inside the
+    tool when its centre maps into the tool bitmap through the texture engine's own tool map
+    (KN:187-193 with the factors of ``compute_tool_projection``; half-open at the far edges so that a
+    (2r+1)-pixel square covers (2r+1)^2 pixels): both engines edit under one footprint.
+    ``device=None`` returns numpy arrays, otherwise the rays are generated on that device (torch)."""
+    torch = _native._torch()
+    dev = device if device is not None else "cpu"
+    shape = tool.shape if type(tool.shape).__module__.startswith("torch") else torch.from_numpy(
+        np.ascontiguousarray(tool.shape))
+    shape = shape.to(dev)
+    th, tw = int(shape.shape[0]), int(shape.shape[1])
     left, bottom = tool.px - 0.5 * tw, tool.py - 0.5 * th
-    xs = np.arange(max(0, int(np.floor(left))), min(camera.width, int(np.ceil(left + tw)) + 1))
-    ys = np.arange(max(0, int(np.floor(bottom))), min(camera.height, int(np.ceil(bottom + th)) + 1))
-    gx, gy = np.meshgrid(xs + 0.5, ys + 0.5)
+    x0, x1 = max(0, int(np.floor(left))), min(camera.width, int(np.ceil(left + tw)) + 1)
+    y0, y1 = max(0, int(np.floor(bottom))), min(camera.height, int(np.ceil(bottom + th)) + 1)
+    if x1 <= x0 or y1 <= y0:
+        z = torch.zeros((0, 3), dtype=torch.float64, device=dev)
+        return (z, z.clone()) if device is not None else (z.numpy(), z.clone().numpy())
+    xs = torch.arange(x0, x1, dtype=torch.float64, device=dev) + 0.5
+    ys = torch.arange(y0, y1, dtype=torch.float64, device=dev) + 0.5
+    gy, gx = torch.meshgrid(ys, xs, indexing="ij")
     s, t = (gx - left) / tw, (gy - bottom) / th                     # the tool map of KN:187-192 per pixel
-    inside = (s >= 0.0) & (s < 1.0) & (t >= 0.0) & (t < 1.0)       # half open: (2r+1)^2 pixels, SPEC.md:358
-    si = np.minimum((s * tw).astype(np.int64), tw - 1).clip(0)
-    ti = np.minimum((t * th).astype(np.int64), th - 1).clip(0)
+    inside = (s >= 0.0) & (s < 1.0) & (t >= 0.0) & (t < 1.0)        # half open: (2r+1)^2 pixels
+    si = (s * tw).to(torch.int64).clamp_(0, tw - 1)
+    ti = (t * th).to(torch.int64).clamp_(0, th - 1)
     keep = inside & (shape[ti, si] != 0)
     x, y = gx[keep], gy[keep]
-    inv = np.linalg.inv(np.asarray(camera.mvp, dtype=np.float64))
-    one = np.ones_like(x)
-    ndc = np.stack([x / camera.width * 2.0 - 1.0, y / camera.height * 2.0 - 1.0], 1)
-    near = np.concatenate([ndc, -one[:, None], one[:, None]], 1) @ inv.T
-    far = np.concatenate([ndc, one[:, None], one[:, None]], 1) @ inv.T
+    inv = torch.from_numpy(np.linalg.inv(np.asarray(camera.mvp, dtype=np.float64))).to(dev)
+    one = torch.ones_like(x)
+    nx, ny = x / camera.width * 2.0 - 1.0, y / camera.height * 2.0 - 1.0
+    near = torch.stack([nx, ny, -one, one], 1) @ inv.T
+    far = torch.stack([nx, ny, one, one], 1) @ inv.T
     near, far = near[:, :3] / near[:, 3:], far[:, :3] / far[:, 3:]
     d = far - near
-    d /= np.linalg.norm(d, axis=1, keepdims=True)
-    return np.ascontiguousarray(near), np.ascontiguousarray(d)
+    d = d / torch.linalg.norm(d, dim=1, keepdim=True)
+    near, d = near.contiguous(), d.contiguous()
+    return (near, d) if device is not None else (near.numpy(), d.numpy())
 
 
 def octree_edit(octree, layer, mesh, camera, tool, value=None):
@@ -213,14 +229,13 @@ def octree_edit(octree, layer, mesh, camera, tool, value=None):
     torch = _native.require_cuda()
     if layer.leaf_count != octree.leaf_count:
         raise TargetMismatch("layer has %d leaves, the octree %d" % (layer.leaf_count, octree.leaf_count))
-    origins, dirs = tool_rays(camera, tool)
-    n = origins.shape[0]
     dev = octree.keys.device
+    origins, dirs = tool_rays(camera, tool, device=dev)
+    n = origins.shape[0]
     if n == 0:
         empty = torch.zeros(0, dtype=torch.int64, device=dev)
         return OctreeEditResult(empty, 0, 0, octree_upload_size(layer))
-    best_t, best_tri, leaf = _native.raycast(torch.from_numpy(origins).to(dev), torch.from_numpy(dirs).to(dev),
-                                             octree.keys, octree.offsets, octree.tri_idx, octree.verts,
+    best_t, best_tri, leaf = _native.raycast(origins, dirs, octree.keys, octree.offsets, octree.tri_idx, octree.verts,
                                              octree.tris, octree.cube_min, octree.h, octree.n_cells,
                                              octree.coarse, octree.coarse_shift, None)
     hit = leaf >= 0
@@ -228,7 +243,7 @@ def octree_edit(octree, layer, mesh, camera, tool, value=None):
     v = tool.value if value is None else value
     layer.values[leaves] = torch.as_tensor(v).to(layer.values.dtype).to(dev)
     layer.valid[leaves] = True
-    return OctreeEditResult(leaves, n, int(hit.sum().item()), octree_upload_size(layer))
+    return OctreeEditResult(leaves, n, hit.sum(), octree_upload_size(layer))
 
 
 def octree_upload_size(layer):

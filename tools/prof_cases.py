@@ -5,7 +5,8 @@
         -o gpurun_out/x python tools/prof_cases.py surface
 
 Cases: surface (16384^2 surface-map build of the C2 mesh), sphere (few hits, 50% hits),
-threshold (coherent 50%, noise 20%), tpa (outline build + padding), area (L=1, L=4)."""
+threshold (coherent 50%, noise 20%), tpa (outline build + padding), area (L=1, L=4),
+octree (only when named: depth-12 octree of the C2 mesh + one r=200 ray-cast edit)."""
 import os
 import sys
 
@@ -18,6 +19,21 @@ from paper_2501_14807_b200 import _native as nat, synth  # noqa: E402
 
 def main():
     want = set(sys.argv[1:]) or {"surface", "sphere", "threshold", "tpa", "area"}
+    if "octree" in want:
+        import paper_2501_14807_b200 as ml
+        from paper_2501_14807_b200 import bench
+        mesh = bench.make_mesh("terrain:707")
+        cam = bench.make_camera("terrain:707", (1024, 1024))
+        tree = ml.build_octree(mesh, 12)
+        layer = ml.create_octree_layer(tree)
+        tool = ml.EditingTool(px=512.0, py=512.0, shape=synth.circle_shape(200), value=7)
+        ml.octree_edit(tree, layer, mesh, cam, tool)
+        torch.cuda.synchronize()
+        del tree, layer
+        torch.cuda.empty_cache()
+        want.discard("octree")
+        if not want:
+            return
     N = int(os.environ.get("PROF_N", "16384"))
     n = N * N
     dev = "cuda"
