@@ -27,6 +27,9 @@ Inputs are far larger than the 126 MB L2 (every plane is >= 268 MB), so no expli
 needed between iterations.  ``value`` is timed with CUDA events with everything resident in HBM;
 ``e2e`` runs the same step through the public API from HOST stroke records (pinned memory ->
 device every step) and reads every stage's result (edit counts, areas) back to the host.
+``config.host_plane_call`` additionally times ONE drop-in call of the KN twin ``raster_tea`` with numpy
+planes in host memory (upload + kernel + download inside the call, the way the reference's numpy
+backend is called): the PCIe cost the resident design exists to avoid, reported beside ``e2e``.
 
 Multi-GPU (torchrun, one rank per GPU): weak scaling -- the atlas grows to 16384 x (16384*N) and
 each rank owns one 16384-row slab; the only collectives are the stroke broadcast and the area
@@ -507,6 +510,37 @@ def run_ours(args):
             stream_info[st] = ms_acc / reps
         ctx.edited.zero_()
 
+    # ---- the drop-in call with HOST planes (untimed part of the run, reported under config.host_plane_call):
+    # the KN twin `raster_tea` (KN:135) called the way the reference calls it, numpy planes in host memory,
+    # uploaded, edited and downloaded inside the call.  This is the PCIe cost the resident design avoids.
+    host_call = None
+    if rank == 0 and world_size == 1 and not args.no_cpu and "tea" in stages:
+        inp = inputs[args.warmup]
+        tool = make_tool(inp)
+        sfx, sfy, bx, by = ml.compute_tool_projection(wl.cam, tool).kernel_factors
+        tri_xy = np.ascontiguousarray(wl.mesh.tri_uv_texels(W, wl.height))
+        clip = np.ascontiguousarray(wl.cam.clip_coords(wl.mesh.vertices)[wl.mesh.triangles])
+        depth_np = depth.plane.cpu().numpy()
+        shape_np = np.ascontiguousarray(wl.tool_shape).astype(np.uint8)
+        planes = [np.zeros((rows, W), np.uint8) for _ in range(3)]
+        ctx.edited.zero_()
+        want = int(stage_call("tea", inp, tool, "resident")[0].reshape(-1)[0].item())
+        ctx.edited.zero_()
+        t_host = []
+        got = None
+        for _ in range(2):
+            planes[2][:] = 0
+            t0 = time.perf_counter()
+            got = nat.raster_tea(tri_xy, clip, float(wl.cam.width), float(wl.cam.height), depth_np, wl.eps, sfx, sfy,
+                                 bx, by, shape_np, planes[0], planes[1], planes[2], 7)
+            t_host.append((time.perf_counter() - t0) * 1e3)
+        moved = tri_xy.nbytes + clip.nbytes + depth_np.nbytes + shape_np.nbytes + 3 * planes[0].nbytes
+        host_call = {"op": "raster_tea (KN:135-136) with numpy planes: upload + direct per-triangle kernel + download",
+                     "ms": round(min(t_host), 2), "gtexel_s": round(n / (min(t_host) * 1e-3) / 1e9, 2),
+                     "h2d_bytes": moved, "d2h_bytes": 3 * planes[0].nbytes,
+                     "edited": int(got[0]), "equal_to_resident_stroke": int(got[0]) == want}
+        del planes, tri_xy, clip
+
     texel_passes = len(stages) * n * world_size
     value = texel_passes * args.steps / (total_ms * 1e-3) / 1e9
     e2e_value = texel_passes * args.steps / (e2e_ms * 1e-3) / 1e9
@@ -569,6 +603,8 @@ def run_ours(args):
         cfg["surface_map"] = {"covered": surf.covered, "overlap": surf.overlap}
         cfg["footprint_culling"] = not args.no_cull
         cfg["stream_kernels"] = stream_kernels
+        if host_call:
+            cfg["host_plane_call"] = host_call
         print(json.dumps({
             "metric": "brush-apply + layer-op texel passes per second at 16384^2 atlas",
             "value": value, "unit": "Gtexel/s", "n_gpus": world_size, "steps": args.steps, "warmup": args.warmup,
