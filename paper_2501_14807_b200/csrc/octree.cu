@@ -276,14 +276,15 @@ __global__ void __launch_bounds__(128) raycast_kernel(RayArgs a) {
     }
     bool live = t_lo <= t_hi;
     if (live) {
+        // n_cells <= 2^21 (checked by ml_raycast): 32-bit cell arithmetic in the march loop
+        const int nc = (int)a.n_cells;
         const double t_start = np_max(t_lo, 0.0);
-        int64_t cell[3];
-        int step[3];
+        int cell[3], step[3];
         double t_max[3], t_delta[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {                                // KN:400-416
             const double p = o[k] + t_start * u[k];
-            cell[k] = cell_of(__ddiv_rn(p - a.cmin[k], a.h), a.n_cells);
+            cell[k] = (int)cell_of(__ddiv_rn(p - a.cmin[k], a.h), a.n_cells);
             step[k] = u[k] > 0.0 ? 1 : (u[k] < 0.0 ? -1 : 0);
             t_max[k] = INFINITY;
             t_delta[k] = INFINITY;
@@ -294,13 +295,16 @@ __global__ void __launch_bounds__(128) raycast_kernel(RayArgs a) {
                 t_delta[k] = a.h * fabs(inv_u[k]);
             }
         }
+        const int cs = a.coarse_shift;
+        const unsigned int side = (unsigned int)a.coarse_side;
+        double limit = np_min(best_t, t_hi);                         // min(best_t, t_hi) of KN:502
         const int64_t max_iter = 3 * a.n_cells + 3;
         for (int64_t it = 0; it < max_iter && live; ++it) {          // KN:420-503
             bool maybe = true;
             if (a.coarse)
-                maybe = __ldg(a.coarse + ((cell[0] >> a.coarse_shift) * a.coarse_side +
-                                          (cell[1] >> a.coarse_shift)) * a.coarse_side +
-                              (cell[2] >> a.coarse_shift)) != 0;
+                maybe = __ldg(a.coarse + ((size_t)((unsigned int)(cell[0] >> cs) * side +
+                                                   (unsigned int)(cell[1] >> cs)) * side +
+                                          (unsigned int)(cell[2] >> cs))) != 0;
             if (maybe) {
                 const int64_t pos = find_key(a.keys, a.nkeys, morton3(cell[0], cell[1], cell[2]));
                 if (pos >= 0) {
@@ -314,22 +318,22 @@ __global__ void __launch_bounds__(128) raycast_kernel(RayArgs a) {
                         if (t < best_t || (t == best_t && f < best_tri)) {   // KN:470-487
                             best_t = t;
                             best_tri = f;
+                            limit = np_min(best_t, t_hi);
                         }
                     }
                 }
             }
-            int axis;                                                // KN:490-503
-            if (t_max[0] <= t_max[1] && t_max[0] <= t_max[2]) axis = 0;
-            else if (t_max[1] <= t_max[2]) axis = 1;
-            else axis = 2;
-            // dynamic register-array indexing would spill: select by hand
-            const double cur = axis == 0 ? t_max[0] : (axis == 1 ? t_max[1] : t_max[2]);
-            int64_t c;
-            if (axis == 0) { cell[0] += step[0]; t_max[0] += t_delta[0]; c = cell[0]; }
-            else if (axis == 1) { cell[1] += step[1]; t_max[1] += t_delta[1]; c = cell[1]; }
-            else { cell[2] += step[2]; t_max[2] += t_delta[2]; c = cell[2]; }
-            const bool out = c < 0 || c >= a.n_cells;
-            if (out || cur > np_min(best_t, t_hi)) live = false;
+            // KN:490-503; dynamic register-array indexing would spill: select by hand
+            double cur;
+            int c;
+            if (t_max[0] <= t_max[1] && t_max[0] <= t_max[2]) {
+                cur = t_max[0]; cell[0] += step[0]; t_max[0] += t_delta[0]; c = cell[0];
+            } else if (t_max[1] <= t_max[2]) {
+                cur = t_max[1]; cell[1] += step[1]; t_max[1] += t_delta[1]; c = cell[1];
+            } else {
+                cur = t_max[2]; cell[2] += step[2]; t_max[2] += t_delta[2]; c = cell[2];
+            }
+            if ((unsigned int)c >= (unsigned int)nc || cur > limit) live = false;
         }
         if (isfinite(best_t) && best_tri >= 0) {                     // KN:506-524
             int64_t lc[3];

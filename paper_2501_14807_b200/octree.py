@@ -109,7 +109,7 @@ def bounding_cube(vertices, pad=1e-3):
     return np.ascontiguousarray(centre - 0.5 * side, dtype=np.float64), side
 
 
-def build_octree(mesh, depth, *, budget_bytes=0, coarse_bits=5, cube=None, device="cuda"):
+def build_octree(mesh, depth, *, budget_bytes=0, coarse_bits=8, cube=None, device="cuda"):
     """SPEC.md:342-349.  Level-by-level refinement: every (cell, triangle) pair of level k-1 is tested
     against the 8 child cubes (closed-box SAT, touching counts); children crossed by no
     triangle never exist.  ``budget_bytes`` > 0 raises ``MemoryBudgetExceeded`` as soon as a level's
