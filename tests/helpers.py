@@ -132,3 +132,34 @@ def camera_rays(cam, pixels):
     near, far = near[:, :3] / near[:, 3:], far[:, :3] / far[:, 3:]
     d = far - near
     return np.ascontiguousarray(near), np.ascontiguousarray(d / np.linalg.norm(d, axis=1, keepdims=True))
+
+
+def brute_raycast(origins, dirs, verts, tris):
+    """Per-ray nearest hit over ALL triangles with the reference's Moeller-Trumbore expression order
+    (numpy, vectorised over triangles): the brute-force oracle of SPEC.md:358, 380."""
+    v0, v1, v2 = verts[tris[:, 0]], verts[tris[:, 1]], verts[tris[:, 2]]
+    e1, e2 = v1 - v0, v2 - v0
+    best_t = np.full(len(origins), np.inf)
+    best_tri = np.full(len(origins), -1, np.int64)
+    for i, (o, u) in enumerate(zip(origins, dirs)):
+        px = u[1] * e2[:, 2] - u[2] * e2[:, 1]
+        py = u[2] * e2[:, 0] - u[0] * e2[:, 2]
+        pz = u[0] * e2[:, 1] - u[1] * e2[:, 0]
+        det = e1[:, 0] * px + e1[:, 1] * py + e1[:, 2] * pz
+        ok = det != 0.0
+        inv = 1.0 / np.where(ok, det, 1.0)
+        tv = o - v0
+        bu = (tv[:, 0] * px + tv[:, 1] * py + tv[:, 2] * pz) * inv
+        ok &= (bu >= 0.0) & (bu <= 1.0)
+        qx = tv[:, 1] * e1[:, 2] - tv[:, 2] * e1[:, 1]
+        qy = tv[:, 2] * e1[:, 0] - tv[:, 0] * e1[:, 2]
+        qz = tv[:, 0] * e1[:, 1] - tv[:, 1] * e1[:, 0]
+        bv = (u[0] * qx + u[1] * qy + u[2] * qz) * inv
+        ok &= (bv >= 0.0) & (bu + bv <= 1.0)
+        t = (e2[:, 0] * qx + e2[:, 1] * qy + e2[:, 2] * qz) * inv
+        ok &= t >= 0.0
+        t = np.where(ok, t, np.inf)
+        j = int(np.argmin(t))                                         # first minimum = smallest index
+        if np.isfinite(t[j]):
+            best_t[i], best_tri[i] = t[j], j
+    return best_t, best_tri

@@ -240,3 +240,27 @@ def test_octree_spec_known_answers():
     cells, tri = kn.expand_pairs_ordered(v, t, np.zeros((1, 3), np.uint32), np.zeros(0, np.int64),
                                          np.zeros(0, np.int32), np.array([-1.0, -1.0, -1.0]), 1.0)
     assert cells.shape == (0, 3) and tri.shape == (0,)
+
+
+def test_oracle_raycast_equals_bruteforce_over_all_triangles():
+    """Independent of the reference: the DDA traversal must return the globally nearest hit (smallest
+    triangle index on ties) -- the same (t, triangle) a brute-force Moeller-Trumbore over every triangle
+    finds -- for every ray whose hit lies inside the root cube."""
+    from paper_2501_14807_b200 import synth
+    rng = np.random.default_rng(77)
+    verts, tris = _icosphere_arrays(2)
+    verts = verts * np.array([1.0, 0.8, 1.2])
+    cube_min, side = helpers.bounding_cube(verts)
+    cam = synth.default_camera(40, 40, eye=(0.3, -0.2, 3.0))
+    ys, xs = np.mgrid[0:40, 0:40]
+    o, d = helpers.camera_rays(cam, np.stack([xs.ravel(), ys.ravel()], 1))
+    ro = rng.uniform(-0.4, 0.4, size=(400, 3))                            # origins inside the mesh too
+    rd = rng.normal(size=(400, 3))
+    origins, dirs = np.concatenate([o, ro]), np.concatenate([d, rd])
+    bt, btri = helpers.brute_raycast(origins, dirs, verts, tris)
+    for depth in (3, 5):
+        g = helpers.build_leaf_grid(kn.expand_pairs_ordered, verts, tris, cube_min, side, depth, 2)
+        t, tri, leaf = kn.raycast(origins, dirs, g["keys"], g["offsets"], g["tri_idx"], verts, tris, cube_min,
+                                  g["h"], g["n_cells"], g["coarse"], g["coarse_shift"])
+        assert np.array_equal(t, bt) and np.array_equal(tri, btri.astype(np.int32))
+        assert np.array_equal(leaf >= 0, np.isfinite(bt)) and np.isfinite(bt).sum() > 800
