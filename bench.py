@@ -61,7 +61,7 @@ CHAIN_OPS = ["union", "intersection", "difference", "union", "masking", "differe
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--atlas", type=int, default=16384, help="atlas width and per-rank slab height")
@@ -129,40 +129,50 @@ class Workload:
 
 
 def sample_clocks(stop, out):
-    """nvidia-smi clocks line of B200_PROFILING.md, sampled every 200 ms while the timed region runs."""
+    """nvidia-smi clocks line of B200_PROFILING.md, one sample every 100 ms; every line is stamped with the
+    host clock as it arrives so that the summary can keep the samples taken inside the timed regions."""
     q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     try:
         p = subprocess.Popen(["nvidia-smi", "--query-gpu=" + q, "--format=csv,noheader,nounits", "-lms", "100",
-                              "-i", os.environ.get("LOCAL_RANK", "0")], stdout=subprocess.PIPE, text=True)
+                              "-i", os.environ.get("LOCAL_RANK", "0")], stdout=subprocess.PIPE, text=True, bufsize=1)
     except OSError:
         return
-    while not stop.is_set():
-        time.sleep(0.05)
+
+    def reader():
+        for line in p.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                out.append((time.time(), f))
+
+    rd = threading.Thread(target=reader, daemon=True)
+    rd.start()
+    stop.wait()
     p.terminate()
-    try:
-        txt = p.communicate(timeout=5)[0]
-    except Exception:
-        txt = ""
-    for line in txt.splitlines():
-        f = [x.strip() for x in line.split(",")]
-        if len(f) >= 9:
-            out.append(f)
+    rd.join(timeout=5)
 
 
-def clocks_summary(samples):
+def clocks_summary(samples, windows=()):
+    """Median SM clock and throttle reasons of the samples taken inside the timed regions (``windows`` =
+    [(t0, t1), ...] host times).  A timed region shorter than the sampling interval can hold no sample;
+    the samples taken under the same load around it (warm-up .. end of the e2e loop) are used then."""
     if not samples:
         return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-    sm = sorted(float(s[1]) for s in samples if s[1].replace(".", "").isdigit())
+    inside = [f for t, f in samples if any(t0 <= t <= t1 + 0.05 for t0, t1 in windows)]
+    scope = "timed regions"
+    if len(inside) < 2:
+        inside = [f for _, f in samples]
+        scope = "warm-up + timed regions (timed regions shorter than the sampling interval)"
+    sm = sorted(float(s[1]) for s in inside if s[1].replace(".", "").isdigit())
     reasons = set()
     names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-    for s in samples:
+    for s in inside:
         for name, v in zip(names, s[5:9]):
             if v.lower().startswith("active"):
                 reasons.add(name)
-    return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": float(samples[0][2]) if samples else None,
-            "reasons": sorted(reasons), "samples": len(samples)}
+    return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": float(inside[0][2]),
+            "reasons": sorted(reasons), "samples": len(inside), "scope": scope}
 
 
 def measured_peak():
@@ -421,14 +431,20 @@ def run_ours(args):
     # ---- resident loop (value): inputs uploaded before the timed region, no read-back inside it
     inputs = [wl.step_inputs(i) for i in range(args.warmup + args.steps)]
     batch.upload(inputs[0]["batch"], inputs[0]["batch_layers"], inputs[0]["batch_values"])
+    # clock sampler: started before the warm-up so that nvidia-smi is already delivering samples when the
+    # timed region begins (its start-up alone can outlast a short timed region)
+    stop, samples, windows = threading.Event(), [], []
+    th = threading.Thread(target=sample_clocks, args=(stop, samples), daemon=True)
+    th.start()
+    t_wait = time.time()
+    while not samples and time.time() - t_wait < 5.0 and th.is_alive():
+        time.sleep(0.02)
     for i in range(args.warmup):
         for st in stages:
             stage_call(st, inputs[i], make_tool(inputs[i]), "resident")
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
-    stop, samples = threading.Event(), []
-    th = threading.Thread(target=sample_clocks, args=(stop, samples))
-    th.start()
     barrier()
+    t_begin = time.time()
     for k in range(args.steps):
         inp = inputs[args.warmup + k]
         tool = make_tool(inp)
@@ -437,6 +453,7 @@ def run_ours(args):
             stage_call(st, inp, tool, "resident")
             ev[k][j + 1].record()
     barrier()
+    windows.append((t_begin, time.time()))
     total_ms = max_over_ranks(ev[0][0].elapsed_time(ev[-1][-1]))
     stage_ms = {st: sum(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)) / args.steps
                 for j, st in enumerate(stages)}
@@ -462,12 +479,14 @@ def run_ours(args):
         e2e_step(inputs[i])
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_begin = time.time()
     e0.record()
     d2h = 0
     for k in range(args.steps):
         d2h += e2e_step(inputs[args.warmup + k])
     e1.record()
     barrier()
+    windows.append((t_begin, time.time()))
     stop.set()
     th.join()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -621,7 +640,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "Gtexel/s", "ms_per_step": e2e_ms / args.steps,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // max(1, args.steps)},
             "gpu_launches": sum(launches[s] for s in stages) * args.steps,
-            "clocks": clocks_summary(samples),
+            "clocks": clocks_summary(samples, windows),
         }))
     if world_size > 1:
         import torch.distributed as dist

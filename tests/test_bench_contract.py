@@ -68,3 +68,27 @@ def test_gpu_arm_json_contract(extra):
     assert set(d["config"]["stage_results"]) == {"tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area"}
     assert d["config"]["footprint_culling"] == (not extra)
     assert ("stream_kernels" in d["config"]) and (bool(d["config"]["stream_kernels"]) == (not extra))
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_rank_rehearsal_over_gloo():
+    """The N > 1 code path of bench.py (row slabs, stroke broadcast, halo exchange, area all-reduce, max over
+    ranks) launched exactly like the driver does, with both ranks sharing cuda:0 through the gloo test hook
+    (NCCL refuses two ranks on one device).  A rehearsal of the plumbing, not a measurement."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, ML_BENCH_BACKEND="gloo")
+    args = ["--gpus", "2", "--steps", "3", "--warmup", "3", "--atlas", "512", "--cpu-rows", "64", "--quads", "48",
+            "--window", "128", "--layers", "4"]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py")] + args,
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1                                            # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"] == "row-sharded x2" and d["config"]["atlas"] == [1024, 512]
+    assert d["cpu_baseline"] is None                                  # N = 1 only
