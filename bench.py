@@ -377,9 +377,10 @@ def run_ours(args):
             # several ranks the 1-row halo of the edited plane travels point-to-point first
             counts1.zero_()
             if world_size > 1:
-                ext, ext_row0 = sharding.exchange_halo(ctx.edited, row0, wl.height, 1)
-                nat.apply_padding(outline, ext, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1,
-                                  in_row0=ext_row0, out_row0=row0)
+                # interior rows: footprint-culled tile pass; the border row next to each neighbour: streaming pass
+                # over the exchanged halo row (16 KB point-to-point per neighbour)
+                ml.editing.pad_slab(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts1,
+                                    row0=row0, height=wl.height, tiles=ctx.stroke_tiles if cull else None)
             else:
                 nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1,
                                   tiles=ctx.stroke_tiles if cull else None)

@@ -274,6 +274,14 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
 int ml_apply_padding_tiles(const uint8_t* outline, const uint8_t* edited, int64_t width, int64_t rows,
                            int64_t radius, const uint32_t* tile_bits, void* data, int esize,
                            uint32_t value_bits, uint8_t* mask, uint64_t* count, void* stream);
+/* Same, restricted to the output rows [row_lo, row_hi) of the slab.  Row-sharded atlases:
+ * the `radius` rows next to a slab border need the neighbour's edited rows; the caller pads them with
+ * ml_apply_padding over the exchanged halo and lets this call do the interior, so every texel is
+ * visited -- and counted -- exactly once. */
+int ml_apply_padding_tiles_rows(const uint8_t* outline, const uint8_t* edited, int64_t width, int64_t rows,
+                                int64_t row_lo, int64_t row_hi, int64_t radius, const uint32_t* tile_bits,
+                                void* data, int esize, uint32_t value_bits, uint8_t* mask, uint64_t* count,
+                                void* stream);
 
 /* ---- one call per edit: the paper's timed stroke = TEA + TPA -----------
  * ml_stroke = ml_tea_classify_recs + ml_tea_texels + ml_apply_padding_tiles on one stream, for

@@ -122,6 +122,7 @@ def lib():
         "ml_outline_mask": (i32, [vp, i64, i64, i64, i64, i64, i64, vp, vp]),
         "ml_apply_padding": (i32, [vp, vp, i64, i64, i64, i64, i64, i64, vp, i32, u32, vp, vp, vp]),
         "ml_apply_padding_tiles": (i32, [vp, vp, i64, i64, i64, vp, vp, i32, u32, vp, vp, vp]),
+        "ml_apply_padding_tiles_rows": (i32, [vp, vp, i64, i64, i64, i64, i64, vp, vp, i32, u32, vp, vp, vp]),
         "ml_resolve_display": (i32, [vp, i32, vp, i64, dbl, dbl, vp, vp, i32, vp, vp]),
         "ml_pack_mask": (i32, [vp, i64, vp, vp]),
         "ml_unpack_mask": (i32, [vp, i64, vp, vp]),
@@ -154,7 +155,7 @@ EXPORTED_SYMBOLS = (
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
     "ml_select_threshold", "ml_plane_tile_range", "ml_select_threshold_tiles", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
-    "ml_apply_padding", "ml_apply_padding_tiles", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
+    "ml_apply_padding", "ml_apply_padding_tiles", "ml_apply_padding_tiles_rows", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
     "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host",
     "ml_expand_pairs_workspace_bytes", "ml_expand_pairs_count", "ml_expand_pairs_emit", "ml_raycast",
     "ml_expand_pairs_ordered_host", "ml_raycast_host")
@@ -1143,10 +1144,11 @@ def outline_mask(cov, thickness, *, in_row0=0, out_row0=None, out_rows=None, out
 
 
 def apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_row0=None, counts=None,
-                  tiles=None):
+                  tiles=None, row_range=None):
     """SPEC.md:295-298.  ``edited`` is the input slab (with halo rows), the others output slabs.
     ``tiles``: the TEA stroke's 128 x 8-texel tile bitmap (``tea_texels(..., tiles=...)``); the pass
-    then reads only the neighbourhood of the stroke's footprint (same result)."""
+    then reads only the neighbourhood of the stroke's footprint (same result).  ``row_range`` (culled
+    form only) restricts the pass to the output rows [lo, hi) of the slab."""
     require_cuda()
     in_rows, w = edited.shape
     out_rows = outline.shape[0]
@@ -1158,7 +1160,13 @@ def apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_
     ctr = counts if counts is not None else _counters(1, edited.device)
     culled = (tiles is not None and in_rows == out_rows and out_row0 == in_row0 and w % 128 == 0 and 0 < radius <= 4
               and all(t.data_ptr() % 16 == 0 for t in (outline, edited, data, mask)))
-    if culled:
+    if row_range is not None and not culled:
+        raise TargetMismatch("row_range needs the tile-culled padding path")
+    if culled and row_range is not None:
+        _check(lib().ml_apply_padding_tiles_rows(_ptr(outline), _ptr(edited), w, in_rows, int(row_range[0]),
+                                                 int(row_range[1]), int(radius), _ptr(tiles), _ptr(data), esize, bits,
+                                                 _ptr(mask), _ptr(ctr), _stream()))
+    elif culled:
         _check(lib().ml_apply_padding_tiles(_ptr(outline), _ptr(edited), w, in_rows, int(radius), _ptr(tiles),
                                             _ptr(data), esize, bits, _ptr(mask), _ptr(ctr), _stream()))
     else:

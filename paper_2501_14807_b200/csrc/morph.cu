@@ -224,7 +224,7 @@ padding_stream_kernel(const uint8_t* __restrict__ outline, const uint8_t* __rest
 template <int ES>
 __global__ void __launch_bounds__(BLOCK)
 padding_tile_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ edited, long long width,
-                    long long rows, int r, const uint32_t* __restrict__ tile_bits,
+                    long long rows, long long row_lo, long long row_hi, int r, const uint32_t* __restrict__ tile_bits,
                     void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask, unsigned long long* count) {
     __shared__ int s_list[BLOCK];
     __shared__ int s_n;
@@ -266,7 +266,7 @@ padding_tile_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restri
             for (int k = 0; k < 2; ++k) {
                 const int v = lane + 32 * k;                   // 64 vectors of 16 texels per tile
                 const long long yy = ((long long)ty << 3) + (v >> 3);
-                if (yy >= rows) continue;
+                if (yy < row_lo || yy >= row_hi) continue;     // rows outside [row_lo, row_hi) belong to the caller's border pass
                 const long long i0 = yy * width + ((long long)tx << 7) + ((v & 7) << 4);
                 const uint4 o = ld_stream((const uint4*)(outline + i0));
                 if ((o.x | o.y | o.z | o.w) == 0) continue;
@@ -341,8 +341,18 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
 int ml_apply_padding_tiles(const uint8_t* outline, const uint8_t* edited, int64_t width, int64_t rows,
                            int64_t radius, const uint32_t* tile_bits, void* data, int esize,
                            uint32_t value_bits, uint8_t* mask, uint64_t* count, void* stream) {
+    return ml_apply_padding_tiles_rows(outline, edited, width, rows, 0, rows, radius, tile_bits, data, esize,
+                                       value_bits, mask, count, stream);
+}
+
+int ml_apply_padding_tiles_rows(const uint8_t* outline, const uint8_t* edited, int64_t width, int64_t rows,
+                                int64_t row_lo, int64_t row_hi, int64_t radius, const uint32_t* tile_bits,
+                                void* data, int esize, uint32_t value_bits, uint8_t* mask, uint64_t* count,
+                                void* stream) {
     if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
-    if (radius <= 0 || rows <= 0 || width <= 0) return ML_OK;
+    if (row_lo < 0) row_lo = 0;
+    if (row_hi > rows) row_hi = rows;
+    if (radius <= 0 || rows <= 0 || width <= 0 || row_lo >= row_hi) return ML_OK;
     if ((width % 128) != 0 || radius > 4 || tile_bits == nullptr ||
         ((((uintptr_t)outline) | ((uintptr_t)edited) | ((uintptr_t)data) | ((uintptr_t)mask)) & 15) != 0)
         return ml_fail(ML_ERR_ARG, "culled padding needs width % 128 == 0, radius <= 4, aligned planes and the stroke's tile bitmap");
@@ -351,7 +361,7 @@ int ml_apply_padding_tiles(const uint8_t* outline, const uint8_t* edited, int64_
     const long long cap = (long long)ml_sm_count() * 8;
     if (blocks > cap) blocks = cap;
     cudaStream_t st = (cudaStream_t)stream;
-#define ML_LAUNCH_PADT(ES) padding_tile_kernel<ES><<<(unsigned)blocks, BLOCK, 0, st>>>(outline, edited, width, rows, (int)radius, tile_bits, data, value_bits, mask, (unsigned long long*)count)
+#define ML_LAUNCH_PADT(ES) padding_tile_kernel<ES><<<(unsigned)blocks, BLOCK, 0, st>>>(outline, edited, width, rows, row_lo, row_hi, (int)radius, tile_bits, data, value_bits, mask, (unsigned long long*)count)
     if (esize == 1) ML_LAUNCH_PADT(1); else if (esize == 2) ML_LAUNCH_PADT(2); else ML_LAUNCH_PADT(4);
 #undef ML_LAUNCH_PADT
     ML_CUDA(cudaGetLastError());

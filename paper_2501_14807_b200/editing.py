@@ -222,18 +222,60 @@ def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, halo
     res = apply_stroke(ctx, tool, layer, eps=eps, cull=cull)
     if radius > 0:
         pc = torch.zeros(1, dtype=torch.int64, device=ctx.device)
-        ext, ext_row0 = ctx.edited, s.row0
-        if s.rows != s.height:
-            from . import sharding
-            ext, ext_row0 = (halo or sharding.exchange_halo)(ctx.edited, s.row0, s.height, radius)
-        if ext is ctx.edited:
+        if s.rows == s.height:
             _native.apply_padding(as_u8, ctx.edited, radius, layer.data, layer.mask, tool.value, counts=pc,
                                   tiles=ctx.stroke_tiles if cull else None)
         else:
-            _native.apply_padding(as_u8, ext, radius, layer.data, layer.mask, tool.value, counts=pc,
-                                  in_row0=ext_row0, out_row0=s.row0)
+            pad_slab(as_u8, ctx.edited, radius, layer.data, layer.mask, tool.value, pc, row0=s.row0, height=s.height,
+                     tiles=ctx.stroke_tiles if cull else None, halo=halo)
         res._padded = pc
     return res
+
+
+def pad_slab(outline, edited, radius, data, mask, value, counts, *, row0, height, tiles=None, halo=None):
+    """TPA on one row slab of a taller atlas.  The ``radius`` rows next to a slab border need the
+    neighbour's ``edited`` rows: they are exchanged point-to-point (``sharding.exchange_halo``, 16 KB per
+    neighbour at 16384 texels; ``halo`` replaces the exchange in single-process tests and returns either
+    ``(rows_above, rows_below)`` or an extended plane ``(ext, ext_row0)``) and those few border rows are
+    padded by the streaming kernel over a 3 x radius-row window; the interior rows -- whose stencil never
+    leaves the slab -- keep the footprint-culled tile pass.  Every output row is visited by exactly one of
+    the passes, so planes and count equal the whole-plane result."""
+    torch = _native._torch()
+    rows, w = edited.shape
+    if halo is None:
+        from . import sharding
+        up, dn = sharding.exchange_halo(edited, row0, height, radius, parts=True)
+    else:
+        got = halo(edited, row0, height, radius)
+        if not (got[1] is None or torch.is_tensor(got[1])):              # (ext, ext_row0) form
+            ext, ext_row0 = got
+            k = row0 - ext_row0
+            up = ext[:k] if k > 0 else None
+            dn = ext[k + rows:] if ext.shape[0] > k + rows else None
+        else:
+            up, dn = got
+    top = min(radius, rows) if up is not None and up.shape[0] else 0
+    bot = min(radius, rows - top) if dn is not None and dn.shape[0] else 0
+    culled = (tiles is not None and w % 128 == 0 and 0 < radius <= 4 and rows >= 2 * radius
+              and all(t.data_ptr() % 16 == 0 for t in (outline, edited, data, mask)))
+    if not culled:
+        # no tile list: one streaming pass over the slab with the halo rows attached
+        pieces = [p for p in (up, edited, dn) if p is not None and p.shape[0]]
+        ext = torch.cat(pieces, 0) if len(pieces) > 1 else edited
+        _native.apply_padding(outline, ext, radius, data, mask, value, counts=counts,
+                              in_row0=row0 - (up.shape[0] if up is not None else 0), out_row0=row0)
+        return
+    _native.apply_padding(outline, edited, radius, data, mask, value, counts=counts, tiles=tiles,
+                          row_range=(top, rows - bot))
+    if top:      # output rows [0, top): stencil rows [-radius, top + radius)
+        win = torch.cat([up, edited[:min(rows, top + radius)]], 0)
+        _native.apply_padding(outline[:top], win, radius, data[:top], mask[:top], value, counts=counts,
+                              in_row0=row0 - up.shape[0], out_row0=row0)
+    if bot:      # output rows [rows - bot, rows)
+        lo = max(0, rows - bot - radius)
+        win = torch.cat([edited[lo:], dn], 0)
+        _native.apply_padding(outline[rows - bot:], win, radius, data[rows - bot:], mask[rows - bot:], value,
+                              counts=counts, in_row0=row0 + lo, out_row0=row0 + rows - bot)
 
 
 def stroke_gesture(ctx, tools, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):

@@ -104,16 +104,18 @@ def halo_bounds(row0, rows, height, radius):
     return lo, hi - lo
 
 
-def exchange_halo(plane, row0, height, radius):
+def exchange_halo(plane, row0, height, radius, parts=False):
     """Return the rank's slab of a byte plane extended by up to ``radius`` rows from each
     neighbour, plus the global row index of its first row.  Neighbour rows travel point-to-point
-    (isend/irecv); interior-only when world_size == 1."""
+    (isend/irecv); interior-only when world_size == 1.  ``parts=True`` returns the received rows
+    alone, ``(rows_from_above_or_None, rows_from_below_or_None)``, without building the extended
+    plane (per-stroke path: the slab is 268 MB, the halo 16 KB)."""
     import torch
     dist = _dist()
     rank, ws = world()
     rows = plane.shape[0]
     if ws == 1 or radius <= 0:
-        return plane, row0
+        return (None, None) if parts else (plane, row0)
     up_n = min(radius, row0)                                   # rows needed from rank-1 (above = lower rows)
     dn_n = min(radius, height - (row0 + rows))
     # all four transfers go into ONE batch (ncclGroupStart/End under NCCL): posting them one by one
@@ -134,5 +136,7 @@ def exchange_halo(plane, row0, height, radius):
         r.wait()
     up = up.to(plane.device) if up is not None else None
     dn = dn.to(plane.device) if dn is not None else None
-    parts = [p for p in (up, plane, dn) if p is not None]
-    return torch.cat(parts, dim=0), row0 - (up.shape[0] if up is not None else 0)
+    if parts:
+        return up, dn
+    pieces = [p for p in (up, plane, dn) if p is not None]
+    return torch.cat(pieces, dim=0), row0 - (up.shape[0] if up is not None else 0)

@@ -309,6 +309,58 @@ def test_row_sharded_strokes_equal_full_plane_oracle():
     assert np.array_equal(layers[1].mask.cpu().numpy(), mask[r0:r0 + rows])
 
 
+@pytest.mark.parametrize("radius,slabs", [(1, [(0, 96), (96, 32), (128, 128)]), (2, [(0, 100), (100, 28), (128, 128)]),
+                                          (4, [(0, 120), (120, 8), (128, 3), (131, 125)])])
+def test_slab_padding_tile_pass_plus_border_rows_equals_full_plane_oracle(radius, slabs):
+    """editing.pad_slab (the per-stroke TPA of a row-sharded atlas): footprint-culled tile pass over the
+    interior rows + streaming pass over the `radius` border rows with the neighbours' halo rows, on ragged
+    slabs (one thinner than the radius window).  Stacked planes and the summed padded count == the
+    full-plane oracle after every stroke, strokes centred on the slab borders included."""
+    import torch
+    from paper_2501_14807_b200 import editing
+    rng = np.random.default_rng(67 + radius)
+    mesh = synth.icosphere_mesh(3)
+    A, W = 256, 160
+    cam = synth.default_camera(W, W)
+    depth = ml.render_depth(mesh, cam)
+    full = ml.build_surface_map(mesh, A, A)
+    cov = full.coverage.to(torch.uint8)
+    ref_outline = kn.outline(cov.cpu().numpy(), radius)
+    pool = ml.TexturePool()
+    ctxs, layers, outlines = [], [], []
+    for r0, rows in slabs:
+        surf = ml.build_surface_map(mesh, A, A, row0=r0, rows=rows)
+        ctxs.append(ml.StrokeContext(mesh, cam, depth, surf))
+        layers.append(ml.create_layer("p%d" % r0, "uint8", A, rows, pool=pool))
+        lo, hi = max(0, r0 - radius), min(A, r0 + rows + radius)
+        outlines.append(nat.outline_mask(cov[lo:hi].contiguous(), radius, in_row0=lo, out_row0=r0, out_rows=rows))
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool)
+    stacked = lambda: torch.cat([c.edited for c in ctxs], 0)             # noqa: E731
+
+    def halo_rows(plane, row0, height, rad):                              # what exchange_halo(parts=True) returns
+        allr = stacked()
+        rows = plane.shape[0]
+        up = allr[max(0, row0 - rad):row0] if row0 > 0 else None
+        dn = allr[row0 + rows:min(height, row0 + rows + rad)] if row0 + rows < height else None
+        return up, dn
+    for k in range(8):
+        tool = ml.EditingTool(px=float(rng.uniform(30, 130)), py=float(rng.uniform(30, 130)),
+                              shape=synth.circle_shape(int(rng.integers(6, 34))), value=k + 1, padding_radius=radius)
+        edited = np.zeros((A, A), np.uint8)
+        _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+        padded = kn.padding(ref_outline, edited, radius, data, mask, k + 1)
+        for c, l in zip(ctxs, layers):
+            ml.apply_stroke(c, tool, l)
+        pc = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for i, (r0, rows) in enumerate(slabs):
+            editing.pad_slab(outlines[i], ctxs[i].edited, radius, layers[i].data, layers[i].mask, k + 1, pc,
+                             row0=r0, height=A, tiles=ctxs[i].stroke_tiles, halo=halo_rows)
+        assert int(pc.item()) == padded, k
+        assert np.array_equal(torch.cat([l.data for l in layers], 0).cpu().numpy(), data), k
+        assert np.array_equal(torch.cat([l.mask for l in layers], 0).cpu().numpy(), mask), k
+    assert mask.any() and any(c.stroke_tiles is not None for c in ctxs)
+
+
 def test_stroke_gesture_equals_stroke_loop():
     """ml_stroke_sequence: a drag gesture of 9 strokes (host-side numpy shapes of different sizes,
     different values) in one C call == the same strokes through stroke() one by one == the oracle."""

@@ -60,6 +60,14 @@ def _worker(rank, world_size, port, out_dir):
         ext, ext_row0 = sharding.exchange_halo(cov, r0, A, 2)
         in0, in_rows = sharding.halo_bounds(r0, rows, A, 2)
         assert ext_row0 == in0 and ext.shape[0] == in_rows
+        # the per-stroke form: only the received rows, no extended copy of the slab
+        up, dn = sharding.exchange_halo(cov, r0, A, 2, parts=True)
+        k = r0 - ext_row0
+        assert (up is None) == (k == 0) and (dn is None) == (ext.shape[0] == k + rows)
+        if up is not None:
+            assert torch.equal(up, ext[:k])
+        if dn is not None:
+            assert torch.equal(dn, ext[k + rows:])
         np.savez(os.path.join(out_dir, "rank%d.npz" % rank), data0=data[0], data1=data[1], mask0=mask[0], mask1=mask[1],
                  sums=sums.numpy(), texels=texels.numpy(), counts=counts.numpy(), ext=ext.numpy(), ext_row0=ext_row0,
                  r0=r0, rows=rows)
