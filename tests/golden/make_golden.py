@@ -176,8 +176,28 @@ def gen_octree_scene(level, depth, window, coarse_bits, seed, nrandom):
     return out
 
 
+def gen_c1_digests():
+    """BASELINE config C1 at full size through the REFERENCE: the planes are 1 MB each, so the fixture
+    stores their SHA-256 digests and the counts; the inputs are rebuilt from helpers.tea_scene_inputs."""
+    import hashlib
+    A, W, r = 1024, 512, 40
+    s = helpers.tea_scene_inputs(5, A, W, r, (W / 2.0, W / 2.0))
+    dig = lambda a: np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)  # noqa: E731
+    cov = np.zeros((A, A), np.uint8)
+    written = KN.coverage_fill(s["tri_xy"], A, A, cov)
+    depth = np.ones((W, W), np.float32)
+    KN.raster_depth(s["win_xy"], s["win_zn"], depth)
+    data, mask, edited = np.zeros((A, A), np.uint8), np.zeros((A, A), bool), np.zeros((A, A), bool)
+    ec, fr = KN.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, 1e-4, s["sfx"], s["sfy"], s["bx"],
+                           s["by"], s["shape"], data, mask, edited, 7)
+    return dict(level=5, atlas=A, window=W, tool_r=r, tool_xy=np.array([W / 2.0, W / 2.0]), eps=1e-4, value=7,
+                written=written, edited_count=ec, fragments=fr, cov_sha=dig(cov), depth_sha=dig(depth),
+                data_sha=dig(data), mask_sha=dig(mask.view(np.uint8)), edited_sha=dig(edited.view(np.uint8)))
+
+
 def main():
     out = {}
+    out["c1_digests"] = gen_c1_digests()
     out["octree_expand_a"] = gen_expand(51, 60, 40, 400, np.float64, snap=False)
     out["octree_expand_snap"] = gen_expand(52, 60, 40, 400, np.float64, snap=True)
     out["octree_expand_f32"] = gen_expand(53, 50, 30, 300, np.float32, snap=True)

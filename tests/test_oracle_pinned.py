@@ -264,3 +264,28 @@ def test_oracle_raycast_equals_bruteforce_over_all_triangles():
                                   g["h"], g["n_cells"], g["coarse"], g["coarse_shift"])
         assert np.array_equal(t, bt) and np.array_equal(tri, btri.astype(np.int32))
         assert np.array_equal(leaf >= 0, np.isfinite(bt)) and np.isfinite(bt).sum() > 800
+
+
+def _sha(a):
+    import hashlib
+    return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)
+
+
+def test_oracle_matches_reference_on_config_c1_full_size():
+    """BASELINE config C1 (icosphere level 5 = 20,480 triangles, 1024^2 atlas, 512^2 window, r = 40 px stroke)
+    through all three reference kernels: SHA-256 of every plane and the counts recorded from the reference."""
+    f = helpers.golden("c1_digests")
+    A, W = int(f["atlas"]), int(f["window"])
+    s = helpers.tea_scene_inputs(int(f["level"]), A, W, int(f["tool_r"]), tuple(f["tool_xy"]))
+    cov = np.zeros((A, A), np.uint8)
+    assert kn.coverage_fill(s["tri_xy"], A, A, cov, threads=0) == int(f["written"])
+    assert np.array_equal(_sha(cov), f["cov_sha"])
+    depth = np.ones((W, W), np.float32)
+    kn.raster_depth(s["win_xy"], s["win_zn"], depth, threads=0)
+    assert np.array_equal(_sha(depth), f["depth_sha"])
+    data, mask, edited = np.zeros((A, A), np.uint8), np.zeros((A, A), bool), np.zeros((A, A), bool)
+    got = kn.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, float(f["eps"]), s["sfx"], s["sfy"],
+                        s["bx"], s["by"], s["shape"], data, mask, edited, int(f["value"]), threads=0)
+    assert tuple(got) == (int(f["edited_count"]), int(f["fragments"]))
+    assert np.array_equal(_sha(data), f["data_sha"]) and np.array_equal(_sha(mask.view(np.uint8)), f["mask_sha"])
+    assert np.array_equal(_sha(edited.view(np.uint8)), f["edited_sha"])
