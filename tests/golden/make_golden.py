@@ -195,7 +195,36 @@ def gen_c1_digests():
                 data_sha=dig(data), mask_sha=dig(mask.view(np.uint8)), edited_sha=dig(edited.view(np.uint8)))
 
 
+def gen_c2_digests():
+    """BASELINE config C2's mesh (999,698 triangles) at a 4096^2 atlas through the REFERENCE -- about ten
+    minutes of numpy per-triangle loops, so it only runs with `make_golden.py --c2`."""
+    import hashlib
+    import time
+    Q, A, W, r = 707, 4096, 1024, 70
+    s = helpers.terrain_scene_inputs(Q, A, W, r)
+    dig = lambda a: np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)  # noqa: E731
+    t0 = time.time()
+    cov = np.zeros((A, A), np.uint8)
+    written = KN.coverage_fill(s["tri_xy"], A, A, cov)
+    print("coverage", written, time.time() - t0, flush=True)
+    depth = np.ones((W, W), np.float32)
+    KN.raster_depth(s["win_xy"], s["win_zn"], depth)
+    print("depth", time.time() - t0, flush=True)
+    data, mask, edited = np.zeros((A, A), np.uint8), np.zeros((A, A), bool), np.zeros((A, A), bool)
+    ec, fr = KN.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, 1e-4, s["sfx"], s["sfy"], s["bx"],
+                           s["by"], s["shape"], data, mask, edited, 7)
+    print("tea", ec, fr, time.time() - t0, flush=True)
+    return dict(quads=Q, atlas=A, window=W, tool_r=r, eps=1e-4, value=7, triangles=s["mesh"].num_triangles,
+                written=written, edited_count=ec, fragments=fr, cov_sha=dig(cov), depth_sha=dig(depth),
+                data_sha=dig(data), mask_sha=dig(mask.view(np.uint8)), edited_sha=dig(edited.view(np.uint8)),
+                reference_seconds=time.time() - t0)
+
+
 def main():
+    if "--c2" in sys.argv:
+        d = gen_c2_digests()
+        np.savez_compressed(os.path.join(HERE, "c2_digests.npz"), **d)
+        return
     out = {}
     out["c1_digests"] = gen_c1_digests()
     out["octree_expand_a"] = gen_expand(51, 60, 40, 400, np.float64, snap=False)

@@ -36,6 +36,22 @@ def tea_scene_inputs(level, atlas, window, tool_r, tool_xy):
                 shape=shape, sfx=float(sfx), sfy=float(sfy), bx=float(bx), by=float(by))
 
 
+def terrain_scene_inputs(quads, atlas, window, tool_r):
+    """BASELINE config C2's mesh (heightfield, quads x quads cells; 707 -> 999,698 triangles) with the bench
+    camera and a circular tool at the window centre: the inputs of the three reference kernels."""
+    mesh = synth.heightfield_mesh(int(quads), margin=0.01)
+    cam = synth.default_camera(int(window), int(window), eye=(0.5, 0.5, 1.6), target=(0.5, 0.5, 0.0), fovy=40.0,
+                               near=0.2, far=5.0)
+    win_xy, win_zn = window_triangles(mesh, cam)
+    tri_xy = mesh.tri_uv_texels(int(atlas), int(atlas))
+    clip = cam.clip_coords(mesh.vertices)[mesh.triangles]
+    shape = synth.circle_shape(int(tool_r))
+    tw = th = shape.shape[0]
+    sfx, sfy = window / (2.0 * tw), window / (2.0 * th)
+    return dict(mesh=mesh, cam=cam, win_xy=win_xy, win_zn=win_zn, tri_xy=tri_xy, tri_clip=clip, shape=shape,
+                sfx=float(sfx), sfy=float(sfy), bx=0.5, by=0.5)
+
+
 def eps_of(fix):
     """Fixture eps with the Python type the reference was called with (float vs np.float64)."""
     return np.float64(fix["eps"]) if bool(fix["eps_is_np64"]) else float(fix["eps"])

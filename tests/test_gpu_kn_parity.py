@@ -322,3 +322,46 @@ def test_cuda_matches_reference_on_config_c1_full_size():
     assert np.array_equal(sha(layer.data.cpu().numpy()), f["data_sha"])
     assert np.array_equal(sha(layer.mask.cpu().numpy().view(np.uint8)), f["mask_sha"])
     assert np.array_equal(sha(res.edited_mask.cpu().numpy().view(np.uint8)), f["edited_sha"])
+
+
+def test_cuda_matches_reference_on_config_c2_mesh():
+    """BASELINE config C2's mesh (999,698 triangles, 4096^2 atlas, 1024^2 window, r = 70 px) against the
+    REFERENCE's recorded plane digests (tests/golden/c2_digests.npz, ~10 min of reference time): host-buffer
+    twins of all three kernels, and the resident stroke pipeline."""
+    import hashlib
+    import paper_2501_14807_b200 as ml
+    from paper_2501_14807_b200 import synth
+
+    def sha(a):
+        return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)
+    if "c2_digests" not in helpers.golden_names("c2_"):
+        pytest.skip("tests/golden/c2_digests.npz not generated (python tests/golden/make_golden.py --c2)")
+    f = helpers.golden("c2_digests")
+    A, W = int(f["atlas"]), int(f["window"])
+    s = helpers.terrain_scene_inputs(int(f["quads"]), A, W, int(f["tool_r"]))
+    cov = np.zeros((A, A), np.uint8)
+    assert nat.coverage_fill(s["tri_xy"], A, A, cov) == int(f["written"]) and np.array_equal(sha(cov), f["cov_sha"])
+    depth = np.ones((W, W), np.float32)
+    nat.raster_depth(s["win_xy"], s["win_zn"], depth)
+    assert np.array_equal(sha(depth), f["depth_sha"])
+    data, mask, edited = np.zeros((A, A), np.uint8), np.zeros((A, A), bool), np.zeros((A, A), bool)
+    got = nat.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, float(f["eps"]), s["sfx"], s["sfy"],
+                       s["bx"], s["by"], s["shape"], data, mask, edited, int(f["value"]))
+    assert tuple(got) == (int(f["edited_count"]), int(f["fragments"]))
+    assert np.array_equal(sha(data), f["data_sha"]) and np.array_equal(sha(mask.view(np.uint8)), f["mask_sha"])
+    assert np.array_equal(sha(edited.view(np.uint8)), f["edited_sha"])
+    # the resident pipeline (surface map + render_depth + culled apply_stroke) lands on the same planes
+    mesh, cam = s["mesh"], s["cam"]
+    surf = ml.build_surface_map(mesh, A, A)
+    dmap = ml.render_depth(mesh, cam)
+    assert np.array_equal(sha(dmap.plane.cpu().numpy()), f["depth_sha"])
+    assert np.array_equal(sha(surf.coverage.cpu().numpy().astype(np.uint8)), f["cov_sha"])
+    ctx = ml.StrokeContext(mesh, cam, dmap, surf)
+    layer = ml.create_layer("c2", "uint8", A, A, pool=ml.TexturePool())
+    tool = ml.EditingTool(px=0.5 * W, py=0.5 * W, shape=synth.circle_shape(int(f["tool_r"])),
+                          value=int(f["value"]))
+    res = ml.apply_stroke(ctx, tool, layer)
+    assert (res.edited_count, res.fragments) == (int(f["edited_count"]), int(f["fragments"]))
+    assert np.array_equal(sha(layer.data.cpu().numpy()), f["data_sha"])
+    assert np.array_equal(sha(layer.mask.cpu().numpy().view(np.uint8)), f["mask_sha"])
+    assert np.array_equal(sha(res.edited_mask.cpu().numpy().view(np.uint8)), f["edited_sha"])

@@ -289,3 +289,26 @@ def test_oracle_matches_reference_on_config_c1_full_size():
     assert tuple(got) == (int(f["edited_count"]), int(f["fragments"]))
     assert np.array_equal(_sha(data), f["data_sha"]) and np.array_equal(_sha(mask.view(np.uint8)), f["mask_sha"])
     assert np.array_equal(_sha(edited.view(np.uint8)), f["edited_sha"])
+
+
+def test_oracle_matches_reference_on_config_c2_mesh():
+    """BASELINE config C2's mesh (999,698 triangles, 4096^2 atlas, 1024^2 window, r = 70 px stroke): the
+    reference needed ~10 minutes of numpy loops for these digests (make_golden.py --c2)."""
+    if "c2_digests" not in helpers.golden_names("c2_"):
+        pytest.skip("tests/golden/c2_digests.npz not generated (python tests/golden/make_golden.py --c2)")
+    f = helpers.golden("c2_digests")
+    A, W = int(f["atlas"]), int(f["window"])
+    s = helpers.terrain_scene_inputs(int(f["quads"]), A, W, int(f["tool_r"]))
+    assert s["mesh"].num_triangles == int(f["triangles"])
+    cov = np.zeros((A, A), np.uint8)
+    assert kn.coverage_fill(s["tri_xy"], A, A, cov, threads=0) == int(f["written"])
+    assert np.array_equal(_sha(cov), f["cov_sha"])
+    depth = np.ones((W, W), np.float32)
+    kn.raster_depth(s["win_xy"], s["win_zn"], depth, threads=0)
+    assert np.array_equal(_sha(depth), f["depth_sha"])
+    data, mask, edited = np.zeros((A, A), np.uint8), np.zeros((A, A), bool), np.zeros((A, A), bool)
+    got = kn.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, float(f["eps"]), s["sfx"], s["sfy"],
+                        s["bx"], s["by"], s["shape"], data, mask, edited, int(f["value"]), threads=0)
+    assert tuple(got) == (int(f["edited_count"]), int(f["fragments"]))
+    assert np.array_equal(_sha(data), f["data_sha"]) and np.array_equal(_sha(mask.view(np.uint8)), f["mask_sha"])
+    assert np.array_equal(_sha(edited.view(np.uint8)), f["edited_sha"])
