@@ -220,7 +220,34 @@ def gen_c2_digests():
                 reference_seconds=time.time() - t0)
 
 
+def gen_octree_digests():
+    """A larger octree scene through the REFERENCE (icosphere level 5 = 20,480 triangles, depth 8, 16k camera
+    rays + 4k random rays): digests of the leaf arrays and of the ray-cast results; inputs are rebuilt from
+    seeds by the tests."""
+    import hashlib
+    dig = lambda a: np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)  # noqa: E731
+    level, depth, window, cb, seed, nrandom = 5, 8, 128, 4, 63, 4096
+    mesh = synth.icosphere_mesh(level)
+    verts = np.ascontiguousarray(mesh.vertices, np.float64)
+    tris = np.ascontiguousarray(mesh.triangles, np.int64)
+    cube_min, side = helpers.bounding_cube(verts)
+    g = helpers.build_leaf_grid(KN.expand_pairs_ordered, verts, tris, cube_min, side, depth, cb)
+    origins, dirs = helpers.octree_rays(window, seed, nrandom)
+    bt, btri, leaf = KN.raycast(origins, dirs, g["keys"], g["offsets"], g["tri_idx"], verts, tris, cube_min, g["h"],
+                                g["n_cells"], g["coarse"], g["coarse_shift"], helpers.morton3)
+    return dict(level=level, depth=depth, window=window, coarse_bits=cb, seed=seed, nrandom=nrandom,
+                leaves=g["keys"].shape[0], rows=g["tri_idx"].shape[0], hits=int(np.isfinite(bt).sum()),
+                keys_sha=dig(g["keys"]), offsets_sha=dig(g["offsets"]), tri_idx_sha=dig(g["tri_idx"]),
+                level_rows=np.array([len(t) for _, t in g["levels"]]),
+                best_t_sha=dig(bt), best_tri_sha=dig(btri.astype(np.int32)), leaf_sha=dig(leaf.astype(np.int64)))
+
+
 def main():
+    if "--octree" in sys.argv:
+        d = gen_octree_digests()
+        np.savez_compressed(os.path.join(HERE, "octree_digests.npz"), **d)
+        print({k: v for k, v in d.items() if not k.endswith("_sha")})
+        return
     if "--c2" in sys.argv:
         d = gen_c2_digests()
         np.savez_compressed(os.path.join(HERE, "c2_digests.npz"), **d)

@@ -179,3 +179,18 @@ def brute_raycast(origins, dirs, verts, tris):
         if np.isfinite(t[j]):
             best_t[i], best_tri[i] = t[j], j
     return best_t, best_tri
+
+
+def octree_rays(window, seed, nrandom):
+    """Camera rays of a window x window view of the unit sphere plus seeded random rays (axis-parallel,
+    integer-direction and interior-origin cases included); float64 (N,3) origins and directions."""
+    rng = np.random.default_rng(seed)
+    cam = synth.default_camera(int(window), int(window), eye=(0.4, 0.3, 3.2))
+    ys, xs = np.mgrid[0:window, 0:window]
+    o, d = camera_rays(cam, np.stack([xs.ravel(), ys.ravel()], 1))
+    ro = rng.uniform(-1.5, 1.5, size=(nrandom, 3))
+    rd = rng.normal(size=(nrandom, 3))
+    rd[: nrandom // 8, 1] = 0.0
+    rd[nrandom // 8: nrandom // 4] = np.round(rd[nrandom // 8: nrandom // 4])
+    ro[nrandom // 2:] *= 0.3                                              # origins inside the sphere
+    return np.concatenate([o, ro]), np.concatenate([d, rd])

@@ -312,3 +312,26 @@ def test_oracle_matches_reference_on_config_c2_mesh():
     assert tuple(got) == (int(f["edited_count"]), int(f["fragments"]))
     assert np.array_equal(_sha(data), f["data_sha"]) and np.array_equal(_sha(mask.view(np.uint8)), f["mask_sha"])
     assert np.array_equal(_sha(edited.view(np.uint8)), f["edited_sha"])
+
+
+def _octree_digest_scene(f):
+    verts, tris = _icosphere_arrays(f["level"])
+    cube_min, side = helpers.bounding_cube(verts)
+    origins, dirs = helpers.octree_rays(int(f["window"]), int(f["seed"]), int(f["nrandom"]))
+    return verts, tris, cube_min, side, origins, dirs
+
+
+def test_oracle_matches_reference_on_larger_octree_scene():
+    """20,480 triangles, depth 8 (307,904 leaves, 549,464 rows), 20,480 rays: digests of the reference's leaf
+    arrays and ray-cast results (make_golden.py --octree)."""
+    f = helpers.golden("octree_digests")
+    verts, tris, cube_min, side, origins, dirs = _octree_digest_scene(f)
+    g = helpers.build_leaf_grid(kn.expand_pairs_ordered, verts, tris, cube_min, side, int(f["depth"]), int(f["coarse_bits"]))
+    assert [len(t) for _, t in g["levels"]] == f["level_rows"].tolist()
+    assert np.array_equal(_sha(g["keys"]), f["keys_sha"]) and np.array_equal(_sha(g["offsets"]), f["offsets_sha"])
+    assert np.array_equal(_sha(g["tri_idx"]), f["tri_idx_sha"])
+    bt, btri, leaf = kn.raycast(origins, dirs, g["keys"], g["offsets"], g["tri_idx"], verts, tris, cube_min, g["h"],
+                                g["n_cells"], g["coarse"], g["coarse_shift"], threads=0)
+    assert int(np.isfinite(bt).sum()) == int(f["hits"])
+    assert np.array_equal(_sha(bt), f["best_t_sha"]) and np.array_equal(_sha(btri), f["best_tri_sha"])
+    assert np.array_equal(_sha(leaf), f["leaf_sha"])
