@@ -242,7 +242,36 @@ def gen_octree_digests():
                 best_t_sha=dig(bt), best_tri_sha=dig(btri.astype(np.int32)), leaf_sha=dig(leaf.astype(np.int64)))
 
 
+def gen_c1_session_digests():
+    """A session of eight strokes on config C1 through the REFERENCE (the layer planes accumulate, the edited
+    mask is fresh per stroke): counts per stroke and digests of the planes after every stroke."""
+    import hashlib
+    A, W = 1024, 512
+    s = helpers.tea_scene_inputs(5, A, W, 10, (W / 2.0, W / 2.0))
+    dig = lambda a: np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)  # noqa: E731
+    depth = np.ones((W, W), np.float32)
+    KN.raster_depth(s["win_xy"], s["win_zn"], depth)
+    data, mask = np.zeros((A, A), np.uint8), np.zeros((A, A), bool)
+    counts, dsha, msha, esha = [], [], [], []
+    for st in helpers.c1_stroke_script(W):
+        shape = synth.square_shape(2 * st["r"] + 1) if st["square"] else synth.circle_shape(st["r"])
+        th, tw = shape.shape
+        sfx, sfy = W / (2.0 * tw), W / (2.0 * th)
+        bx, by = 0.5 - (st["px"] - 0.5 * W) / tw, 0.5 - (st["py"] - 0.5 * W) / th
+        edited = np.zeros((A, A), bool)
+        counts.append(KN.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, 1e-4, sfx, sfy, bx, by,
+                                    shape, data, mask, edited, st["value"]))
+        dsha.append(dig(data)); msha.append(dig(mask.view(np.uint8))); esha.append(dig(edited.view(np.uint8)))
+    return dict(atlas=A, window=W, counts=np.array(counts, np.int64), data_sha=np.stack(dsha), mask_sha=np.stack(msha),
+                edited_sha=np.stack(esha))
+
+
 def main():
+    if "--session" in sys.argv:
+        d = gen_c1_session_digests()
+        np.savez_compressed(os.path.join(HERE, "c1_session_digests.npz"), **d)
+        print(d["counts"])
+        return
     if "--octree" in sys.argv:
         d = gen_octree_digests()
         np.savez_compressed(os.path.join(HERE, "octree_digests.npz"), **d)

@@ -194,3 +194,22 @@ def octree_rays(window, seed, nrandom):
     rd[nrandom // 8: nrandom // 4] = np.round(rd[nrandom // 8: nrandom // 4])
     ro[nrandom // 2:] *= 0.3                                              # origins inside the sphere
     return np.concatenate([o, ro]), np.concatenate([d, rd])
+
+
+def c1_stroke_script(window):
+    """Eight strokes of a session on config C1: positions, radii, values and the tool bitmaps' kind."""
+    rng = np.random.default_rng(81)
+    out = []
+    for k in range(8):
+        r = int(rng.integers(4, 60))
+        out.append(dict(px=float(rng.uniform(0.2, 0.8) * window), py=float(rng.uniform(0.2, 0.8) * window), r=r,
+                        square=bool(k % 3 == 2), value=int(rng.integers(1, 250))))
+    return out
+
+
+def stroke_tool_map(st, window):
+    """Tool bitmap and the kernel's (sfx, sfy, bx, by) of one scripted stroke (KN:187-188 via SPEC:259-267)."""
+    shape = synth.square_shape(2 * st["r"] + 1) if st["square"] else synth.circle_shape(st["r"])
+    th, tw = shape.shape
+    return shape, (window / (2.0 * tw), window / (2.0 * th), 0.5 - (st["px"] - 0.5 * window) / tw,
+                   0.5 - (st["py"] - 0.5 * window) / th)

@@ -365,3 +365,30 @@ def test_cuda_matches_reference_on_config_c2_mesh():
     assert np.array_equal(sha(layer.data.cpu().numpy()), f["data_sha"])
     assert np.array_equal(sha(layer.mask.cpu().numpy().view(np.uint8)), f["mask_sha"])
     assert np.array_equal(sha(res.edited_mask.cpu().numpy().view(np.uint8)), f["edited_sha"])
+
+
+def test_cuda_stroke_session_matches_reference_digests():
+    """Eight strokes accumulating in one layer on config C1 through the resident pipeline -- culled, streamed
+    and direct TEA kernels interleaved on ONE context, so the per-stroke reset of the edited mask (SPEC:253-255,
+    done tile-wise by the culled path) is exercised -- against the REFERENCE's per-stroke counts and plane
+    digests (tests/golden/c1_session_digests.npz)."""
+    import hashlib
+    import paper_2501_14807_b200 as ml
+
+    def sha(a):
+        return np.frombuffer(hashlib.sha256(np.ascontiguousarray(a).tobytes()).digest(), np.uint8)
+    f = helpers.golden("c1_session_digests")
+    A, W = int(f["atlas"]), int(f["window"])
+    s = helpers.tea_scene_inputs(5, A, W, 10, (W / 2.0, W / 2.0))
+    mesh, cam = s["mesh"], s["cam"]
+    ctx = ml.StrokeContext(mesh, cam, ml.render_depth(mesh, cam), ml.build_surface_map(mesh, A, A))
+    layer = ml.create_layer("session", "uint8", A, A, pool=ml.TexturePool())
+    modes = ["cull", "cull", "stream", "cull", "direct", "cull", "cull", "stream"]
+    for k, st in enumerate(helpers.c1_stroke_script(W)):
+        shape, _ = helpers.stroke_tool_map(st, W)
+        tool = ml.EditingTool(px=st["px"], py=st["py"], shape=shape, value=st["value"])
+        res = ml.apply_stroke(ctx, tool, layer, cull=(modes[k] == "cull"), force_direct=(modes[k] == "direct"))
+        assert (res.edited_count, res.fragments) == tuple(f["counts"][k]), (k, modes[k])
+        assert np.array_equal(sha(layer.data.cpu().numpy()), f["data_sha"][k]), (k, modes[k])
+        assert np.array_equal(sha(layer.mask.cpu().numpy().view(np.uint8)), f["mask_sha"][k]), (k, modes[k])
+        assert np.array_equal(sha(res.edited_mask.cpu().numpy().view(np.uint8)), f["edited_sha"][k]), (k, modes[k])

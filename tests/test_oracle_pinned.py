@@ -335,3 +335,22 @@ def test_oracle_matches_reference_on_larger_octree_scene():
     assert int(np.isfinite(bt).sum()) == int(f["hits"])
     assert np.array_equal(_sha(bt), f["best_t_sha"]) and np.array_equal(_sha(btri), f["best_tri_sha"])
     assert np.array_equal(_sha(leaf), f["leaf_sha"])
+
+
+def test_oracle_matches_reference_on_c1_stroke_session():
+    """Eight strokes accumulating in one layer on config C1 (make_golden.py --session): counts of every stroke
+    and plane digests after every stroke equal the reference's."""
+    f = helpers.golden("c1_session_digests")
+    A, W = int(f["atlas"]), int(f["window"])
+    s = helpers.tea_scene_inputs(5, A, W, 10, (W / 2.0, W / 2.0))
+    depth = np.ones((W, W), np.float32)
+    kn.raster_depth(s["win_xy"], s["win_zn"], depth, threads=0)
+    data, mask = np.zeros((A, A), np.uint8), np.zeros((A, A), bool)
+    for k, st in enumerate(helpers.c1_stroke_script(W)):
+        shape, (sfx, sfy, bx, by) = helpers.stroke_tool_map(st, W)
+        edited = np.zeros((A, A), bool)
+        got = kn.raster_tea(s["tri_xy"], s["tri_clip"], float(W), float(W), depth, 1e-4, sfx, sfy, bx, by, shape,
+                            data, mask, edited, st["value"], threads=0)
+        assert tuple(got) == tuple(f["counts"][k])
+        assert np.array_equal(_sha(data), f["data_sha"][k]) and np.array_equal(_sha(mask.view(np.uint8)), f["mask_sha"][k])
+        assert np.array_equal(_sha(edited.view(np.uint8)), f["edited_sha"][k])
