@@ -359,6 +359,15 @@ int ml_raycast(const double* origins, const double* dirs, int64_t nrays, const u
                const double* cube_min, double h, int64_t n_cells, const uint8_t* coarse, int64_t coarse_side,
                int coarse_shift, double* best_t, int32_t* best_tri, int64_t* leaf_pos, void* stream);
 
+/* Ray set-up of an octree edit ("one ray per window pixel inside the tool shape"): for the
+ * nx x ny window pixels starting at (x0, y0), the ray through the pixel centre (origin on the near plane, unit
+ * direction, inv_view_proj = HOST array of 16 doubles, row major) if the centre maps into a set texel of the tool
+ * bitmap centred at (tool_px, tool_py) -- the tool map of KN:187-192, half open at the far edges -- and a NaN
+ * direction otherwise (ml_raycast reports such a ray as a miss).  *count (device, zeroed) += rays generated. */
+int ml_tool_rays(const double* inv_view_proj, int64_t cam_w, int64_t cam_h, double tool_px, double tool_py,
+                 const uint8_t* shape, int64_t shape_w, int64_t shape_h, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
+                 double* origins, double* dirs, uint64_t* count, void* stream);
+
 /* ---- host-buffer entry points: exact drop-ins for the reference's numpy signatures ------------
  * All pointers are HOST pointers; the call copies inputs to the device, runs the kernels above,
  * copies the planes back and synchronises.  tri arrays are float64 (the reference widens to

@@ -134,6 +134,7 @@ def lib():
         "ml_expand_pairs_count": (i32, [vp, vp, vp, vp, vp, i64, vp, dbl, vp, sz, vp, vp]),
         "ml_expand_pairs_emit": (i32, [vp, vp, vp, i64, vp, vp, vp, vp]),
         "ml_raycast": (i32, [vp, vp, i64, vp, i64, vp, vp, vp, vp, vp, dbl, i64, vp, i64, i32, vp, vp, vp, vp]),
+        "ml_tool_rays": (i32, [vp, i64, i64, dbl, dbl, vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]),
         "ml_expand_pairs_ordered_host": (i32, [vp, i64, vp, i64, vp, i64, vp, vp, i64, vp, dbl, vp, vp, i64, vp]),
         "ml_raycast_host": (i32, [vp, vp, i64, vp, i64, vp, vp, vp, i64, vp, i64, vp, dbl, i64, vp, i64, i32,
                                   vp, vp, vp]),
@@ -158,7 +159,7 @@ EXPORTED_SYMBOLS = (
     "ml_apply_padding", "ml_apply_padding_tiles", "ml_apply_padding_tiles_rows", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
     "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host",
     "ml_expand_pairs_workspace_bytes", "ml_expand_pairs_count", "ml_expand_pairs_emit", "ml_raycast",
-    "ml_expand_pairs_ordered_host", "ml_raycast_host")
+    "ml_expand_pairs_ordered_host", "ml_raycast_host", "ml_tool_rays")
 
 
 def _check(rc):

@@ -252,6 +252,7 @@ def _octree_radius_sweep(plan):
                 continue
             for radius in plan.radii:
                 tool = _tool(camera, radius)
+                tool.shape = _native._as_dev_bytes(tool.shape, "cuda")   # like the texture engine's sweep
                 rec = BenchRecord(spec, plan.engine, level, radius, build_ms=setup.build_ms,
                                   peak_bytes=setup.peak_bytes)
                 res = None

@@ -349,6 +349,66 @@ __global__ void __launch_bounds__(128) raycast_kernel(RayArgs a) {
     a.leaf_pos[i] = leaf;
 }
 
+// ---------------------------------------------------------------------------------------------
+// ray set-up of an octree edit (one ray per window pixel inside the tool shape)
+
+struct ToolRayArgs {
+    double inv[16];                 // inverse view-projection, row major
+    double left, bottom;            // window position of the tool bitmap's lower-left corner
+    int x0, y0, nx, ny;             // pixel box of the tool in the window
+    int cam_w, cam_h, tw, th;
+    const uint8_t* shape;
+    double* origins;
+    double* dirs;
+    unsigned long long* count;
+};
+
+// One thread per pixel of the tool's box.  A pixel whose centre maps into a set texel of the tool bitmap
+// (the tool map of KN:187-192, half open at the far edges) gets the ray through its centre: origin on the
+// near plane, unit direction.  Every other pixel gets a NaN direction, which ml_raycast reports as a miss
+// after the slab test -- so the edit needs no stream compaction.
+__global__ void __launch_bounds__(256) tool_rays_kernel(ToolRayArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = a.nx * a.ny;
+    bool keep = false;
+    if (i < n) {
+        const int iy = i / a.nx, ix = i - iy * a.nx;
+        const double gx = (double)(a.x0 + ix) + 0.5, gy = (double)(a.y0 + iy) + 0.5;
+        const double s = (gx - a.left) / (double)a.tw, t = (gy - a.bottom) / (double)a.th;
+        if (s >= 0.0 && s < 1.0 && t >= 0.0 && t < 1.0) {
+            int si = (int)(s * (double)a.tw), ti = (int)(t * (double)a.th);
+            si = si > a.tw - 1 ? a.tw - 1 : si;
+            ti = ti > a.th - 1 ? a.th - 1 : ti;
+            keep = a.shape[(size_t)ti * a.tw + si] != 0;
+        }
+        double o[3] = {0.0, 0.0, 0.0}, d[3] = {NAN, NAN, NAN};
+        if (keep) {
+            const double vx = gx / (double)a.cam_w * 2.0 - 1.0, vy = gy / (double)a.cam_h * 2.0 - 1.0;
+            double pn[4], pf[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double base = (a.inv[4 * r] * vx + a.inv[4 * r + 1] * vy) + a.inv[4 * r + 3];
+                pn[r] = base - a.inv[4 * r + 2];
+                pf[r] = base + a.inv[4 * r + 2];
+            }
+            double len2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                o[k] = pn[k] / pn[3];
+                d[k] = pf[k] / pf[3] - o[k];
+                len2 += d[k] * d[k];
+            }
+            const double len = sqrt(len2);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) d[k] /= len;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { a.origins[3 * (size_t)i + k] = o[k]; a.dirs[3 * (size_t)i + k] = d[k]; }
+    }
+    const unsigned int b = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0 && b && a.count) atomicAdd(a.count, (unsigned long long)__popc(b));
+}
+
 inline int64_t chunks_of(int64_t npair) { return (npair + EXP_CHUNK - 1) / EXP_CHUNK; }
 
 }  // namespace
@@ -423,6 +483,26 @@ int ml_raycast(const double* origins, const double* dirs, int64_t nrays, const u
     a.coarse = coarse; a.coarse_side = coarse_side; a.coarse_shift = coarse_shift;
     a.best_t = best_t; a.best_tri = best_tri; a.leaf_pos = leaf_pos;
     raycast_kernel<<<(unsigned)((nrays + 63) / 64), 64, 0, (cudaStream_t)stream>>>(a);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+int ml_tool_rays(const double* inv_view_proj, int64_t cam_w, int64_t cam_h, double tool_px, double tool_py,
+                 const uint8_t* shape, int64_t shape_w, int64_t shape_h, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
+                 double* origins, double* dirs, uint64_t* count, void* stream) {
+    if (!inv_view_proj || cam_w < 1 || cam_h < 1 || shape_w < 1 || shape_h < 1 || nx < 0 || ny < 0 ||
+        nx * ny > (int64_t)1 << 30)
+        return ml_fail(ML_ERR_ARG, "ml_tool_rays: bad arguments");
+    if (nx == 0 || ny == 0) return ML_OK;
+    if (!shape || !origins || !dirs) return ml_fail(ML_ERR_ARG, "ml_tool_rays: null pointer");
+    ToolRayArgs a;
+    for (int k = 0; k < 16; ++k) a.inv[k] = inv_view_proj[k];
+    a.left = tool_px - 0.5 * (double)shape_w;
+    a.bottom = tool_py - 0.5 * (double)shape_h;
+    a.x0 = (int)x0; a.y0 = (int)y0; a.nx = (int)nx; a.ny = (int)ny;
+    a.cam_w = (int)cam_w; a.cam_h = (int)cam_h; a.tw = (int)shape_w; a.th = (int)shape_h;
+    a.shape = shape; a.origins = origins; a.dirs = dirs; a.count = (unsigned long long*)count;
+    tool_rays_kernel<<<(unsigned)((nx * ny + 255) / 256), 256, 0, (cudaStream_t)stream>>>(a);
     ML_CUDA(cudaGetLastError());
     return ML_OK;
 }

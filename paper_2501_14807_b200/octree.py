@@ -82,7 +82,7 @@ class OctreeLayer:
 class OctreeEditResult:
     """edited leaf set (indices into the octree's key order), rays cast, transfer bytes."""
     edited_leaves: object
-    rays: int
+    _rays: object
     _hits: object
     transfer_bytes: int
     duration_ms: float = 0.0
@@ -91,6 +91,11 @@ class OctreeEditResult:
     @property
     def edited_count(self):
         return int(self.edited_leaves.shape[0])
+
+    @property
+    def rays(self):
+        """Rays cast = window pixels inside the tool shape (read from the device on demand)."""
+        return int(self._rays)
 
     @property
     def hits(self):
@@ -189,6 +194,10 @@ def tool_rays(camera, tool, device=None):
     (2r+1)-pixel square covers (2r+1)^2 pixels): both engines edit under one footprint.
     ``device=None`` returns numpy arrays, otherwise the rays are generated on that device (torch)."""
     torch = _native._torch()
+    if device is not None and torch.device(device).type == "cuda":
+        o, d, _ = _tool_rays_padded(camera, tool, device)          # the rays octree_edit casts, compacted
+        keep = ~torch.isnan(d[:, 0])
+        return o[keep].contiguous(), d[keep].contiguous()
     dev = device if device is not None else "cpu"
     shape = tool.shape if type(tool.shape).__module__.startswith("torch") else torch.from_numpy(
         np.ascontiguousarray(tool.shape))
@@ -221,6 +230,28 @@ def tool_rays(camera, tool, device=None):
     return (near, d) if device is not None else (near.numpy(), d.numpy())
 
 
+def _tool_rays_padded(camera, tool, device):
+    """Device-side ray set-up (``ml_tool_rays``): rays for EVERY pixel of the tool's window box, pixels outside
+    the tool shape carrying a NaN direction (a miss for ``raycast``); returns (origins, dirs, count tensor)."""
+    import ctypes as C
+    torch = _native.require_cuda()
+    shape = _native._as_dev_bytes(tool.shape, device)
+    th, tw = int(shape.shape[0]), int(shape.shape[1])
+    left, bottom = tool.px - 0.5 * tw, tool.py - 0.5 * th
+    x0, x1 = max(0, int(np.floor(left))), min(camera.width, int(np.ceil(left + tw)) + 1)
+    y0, y1 = max(0, int(np.floor(bottom))), min(camera.height, int(np.ceil(bottom + th)) + 1)
+    nx, ny = max(0, x1 - x0), max(0, y1 - y0)
+    origins = torch.empty((nx * ny, 3), dtype=torch.float64, device=device)
+    dirs = torch.empty((nx * ny, 3), dtype=torch.float64, device=device)
+    count = torch.zeros(1, dtype=torch.int64, device=device)
+    inv = np.ascontiguousarray(np.linalg.inv(np.asarray(camera.mvp, dtype=np.float64)))
+    _native._check(_native.lib().ml_tool_rays(inv.ctypes.data, camera.width, camera.height, float(tool.px),
+                                              float(tool.py), _native._ptr(shape), tw, th, x0, y0, nx, ny,
+                                              _native._ptr(origins), _native._ptr(dirs), _native._ptr(count),
+                                              _native._stream()))
+    return origins, dirs, count
+
+
 def octree_edit(octree, layer, mesh, camera, tool, value=None):
     """cast the camera ray of every window pixel inside the tool shape, take the
     nearest ray-triangle hit (front-to-back DDA, KN:361) and set the value and validity of the leaf
@@ -230,9 +261,8 @@ def octree_edit(octree, layer, mesh, camera, tool, value=None):
     if layer.leaf_count != octree.leaf_count:
         raise TargetMismatch("layer has %d leaves, the octree %d" % (layer.leaf_count, octree.leaf_count))
     dev = octree.keys.device
-    origins, dirs = tool_rays(camera, tool, device=dev)
-    n = origins.shape[0]
-    if n == 0:
+    origins, dirs, n = _tool_rays_padded(camera, tool, dev)
+    if origins.shape[0] == 0:
         empty = torch.zeros(0, dtype=torch.int64, device=dev)
         return OctreeEditResult(empty, 0, 0, octree_upload_size(layer))
     best_t, best_tri, leaf = _native.raycast(origins, dirs, octree.keys, octree.offsets, octree.tri_idx, octree.verts,
