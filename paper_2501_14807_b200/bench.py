@@ -16,7 +16,7 @@ The timed call is ``editing.stroke`` (TEA + TPA, the edit the paper times, PAPER
 with CUDA events around the engine call only, one warm-up discarded, medians over
 the completed repetitions.  ``engine="octree"`` runs the OCT-TR baseline of
 ``octree.py`` (the paper's CPU competitor, here on the same GPU kernels' C ABI): its timed
-call is ``octree_edit`` (ray set-up on the host + ``raycast`` + leaf update), timed with the host clock
+call is ``octree_edit`` (``ml_tool_rays`` + ``raycast`` + leaf update), timed with the host clock
 around a device synchronise because the edit has host work the events would not see.
 """
 import csv
