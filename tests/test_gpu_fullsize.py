@@ -179,3 +179,42 @@ def test_batched_strokes_equal_sequential_at_full_size(big):
     for l in range(L):
         assert _checksum(bat[l].data) == _checksum(seq[l].data)
         assert _checksum(bat[l].mask.view(torch.uint8)) == _checksum(seq[l].mask.view(torch.uint8))
+
+
+def test_row_sharded_stroke_with_padding_equals_whole_plane_at_full_size(big):
+    """Two 8192-row slabs of the 16384^2 atlas (what a 2-GPU run holds) each run the culled TEA of a stroke
+    that straddles the slab border, then editing.pad_slab with the neighbour's halo row; stacked planes and
+    summed counts equal the whole-plane stroke() (ml_stroke: TEA + tile-culled TPA in one call)."""
+    import torch
+    from paper_2501_14807_b200 import editing
+    mesh, surf, cam, ctx, pool = big
+    outline = ml.build_outline_mask(surf.coverage, thickness=1)
+    # a tool whose footprint crosses atlas row 8192: project the surface point at uv = (0.5, 0.5) into the window
+    tool = ml.EditingTool(px=512.0, py=512.0, shape=synth.circle_shape(70), value=11, padding_radius=1)
+    whole = ml.create_layer("whole", "uint8", A, A, pool=pool)
+    res = ml.stroke(ctx, tool, whole, outline)
+    want = (res.edited_count, res.padded_count)
+    ed = ctx.edited.clone()
+    assert bool(ed[:A // 2].any()) and bool(ed[A // 2:].any())            # the stroke really straddles the border
+    assert want[1] >= 0
+    halves, layers = [], []
+    for r0 in (0, A // 2):
+        s = ml.build_surface_map(mesh, A, A, row0=r0, rows=A // 2)
+        c = ml.StrokeContext(mesh, cam, ctx.depth, s)
+        l = ml.create_layer("half%d" % r0, "uint8", A, A // 2, pool=pool)
+        halves.append(c); layers.append(l)
+    got_e = sum(ml.apply_stroke(c, tool, l).edited_count for c, l in zip(halves, layers))
+    assert torch.equal(torch.cat([c.edited for c in halves], 0), ed)
+    pc = torch.zeros(1, dtype=torch.int64, device="cuda")
+
+    def halo(plane, row0, height, rad):
+        other = halves[1].edited if row0 == 0 else halves[0].edited
+        return (None, other[:rad]) if row0 == 0 else (other[-rad:], None)
+    for i, r0 in enumerate((0, A // 2)):
+        editing.pad_slab(outline[r0:r0 + A // 2].view(torch.uint8), halves[i].edited, 1, layers[i].data, layers[i].mask,
+                         tool.value, pc, row0=r0, height=A, tiles=halves[i].stroke_tiles, halo=halo)
+    assert (got_e, int(pc.item())) == want
+    assert torch.equal(torch.cat([l.data for l in layers], 0), whole.data)
+    assert torch.equal(torch.cat([l.mask for l in layers], 0), whole.mask)
+    for l in layers + [whole]:
+        l.release() if hasattr(l, "release") else None
