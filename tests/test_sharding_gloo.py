@@ -103,3 +103,83 @@ def test_two_rank_row_sharding_equals_single_rank(tmp_path):
         e0 = int(p["ext_row0"])
         assert np.array_equal(p["ext"], cov[e0:e0 + p["ext"].shape[0]])
     assert sum(int(p["rows"]) for p in parts) == A
+
+
+# ---- per-stroke TPA on row slabs: editing.pad_slab with a real gloo halo exchange --------------------
+
+_CALLS = []
+
+
+def _oracle_apply_padding(outline, edited, radius, data, mask, value, *, in_row0=0, out_row0=None, counts=None,
+                          tiles=None, row_range=None):
+    """Stand-in for _native.apply_padding on CPU tensors (the test may use the oracle; the product never
+    does): same arguments, the oracle's padding over the given input window, restricted to `row_range`."""
+    out_row0 = in_row0 if out_row0 is None else out_row0
+    rows, w = outline.shape
+    _CALLS.append("interior" if row_range is not None else "border")
+    lo, hi = (0, rows) if row_range is None else row_range
+    if hi <= lo:
+        return
+    # input window as a plane whose row 0 is global row in_row0; outputs start at global row out_row0
+    ed = edited.numpy()
+    off = out_row0 - in_row0
+    # pad the window so that the oracle sees [out_row0 - radius, out_row0 + rows + radius)
+    full = np.zeros((rows + 2 * radius, w), np.uint8)
+    for r in range(rows + 2 * radius):
+        src = off - radius + r
+        if 0 <= src < ed.shape[0]:
+            full[r] = ed[src]
+    o = np.zeros_like(full)
+    o[radius + lo:radius + hi] = outline.numpy()[lo:hi]
+    d = np.zeros_like(full)
+    m = np.zeros_like(full)
+    d[radius:radius + rows] = data.numpy()
+    m[radius:radius + rows] = mask.numpy()
+    n = kn.padding(o, full, radius, d, m, value)
+    data.copy_(torch.from_numpy(d[radius:radius + rows]))
+    mask.copy_(torch.from_numpy(m[radius:radius + rows]))
+    counts += n
+
+
+def _pad_worker(rank, world_size, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world_size)
+    try:
+        from paper_2501_14807_b200 import _native, editing
+        _native.apply_padding = _oracle_apply_padding                     # no GPU in this test
+        H, W, radius = 96, 128, 2
+        rng = np.random.default_rng(5)
+        outline = (rng.random((H, W)) < 0.3).astype(np.uint8)
+        edited = np.zeros((H, W), np.uint8)
+        edited[28:36, 20:90] = 1                                           # straddles the 32-row slab border
+        edited[60:66, 5:40] = 1                                            # and the second one
+        edited[rng.random((H, W)) < 0.01] = 1
+        r0, rows = sharding.shard_rows(H, world_size, rank)
+        data = torch.zeros((rows, W), dtype=torch.uint8)
+        mask = torch.zeros((rows, W), dtype=torch.uint8)
+        counts = torch.zeros(1, dtype=torch.int64)
+        editing.pad_slab(torch.from_numpy(outline[r0:r0 + rows].copy()), torch.from_numpy(edited[r0:r0 + rows].copy()),
+                         radius, data, mask, 7, counts, row0=r0, height=H, tiles=torch.zeros(1, dtype=torch.int32))
+        # the decomposition under test really ran: one interior pass + one border pass per neighbour
+        assert _CALLS.count("interior") == 1 and _CALLS.count("border") == (rank > 0) + (rank < world_size - 1), _CALLS
+        sharding.allreduce_counts(counts)
+        np.savez(os.path.join(out_dir, "pad%d.npz" % rank), data=data.numpy(), mask=mask.numpy(), count=counts.numpy(),
+                 outline=outline, edited=edited)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_three_rank_slab_padding_equals_whole_plane(tmp_path):
+    """editing.pad_slab on three ranks (gloo, CPU tensors, the oracle standing in for the padding kernels): the
+    interior / border-row decomposition with the exchanged halo rows pads exactly the texels the whole-plane
+    pass pads, and counts every one once."""
+    ws = 3
+    mp.spawn(_pad_worker, args=(ws, _free_port(), str(tmp_path)), nprocs=ws, join=True)
+    parts = [np.load(tmp_path / ("pad%d.npz" % r)) for r in range(ws)]
+    outline, edited = parts[0]["outline"], parts[0]["edited"]
+    data, mask = np.zeros_like(outline), np.zeros_like(outline)
+    want = kn.padding(outline, edited, 2, data, mask, 7)
+    assert want > 0 and all(int(p["count"][0]) == want for p in parts)
+    assert np.array_equal(np.concatenate([p["data"] for p in parts]), data)
+    assert np.array_equal(np.concatenate([p["mask"] for p in parts]), mask)
