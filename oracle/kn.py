@@ -56,6 +56,14 @@ def lib():
         _lib.kn_max_threads.restype = i32
         _lib.ext_surface_map.restype = i64
         _lib.ext_surface_map.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp]
+        _lib.ext_surface_map_mt.restype = i64
+        _lib.ext_surface_map_mt.argtypes = [vp, vp, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, i32]
+        _lib.ext_select_sphere_batch_fused.restype = None
+        _lib.ext_select_sphere_batch_fused.argtypes = [vp, i64, i64, vp, i64, vp, vp, i64, vp, vp, vp, vp, i64, i32]
+        _lib.ext_layer_chain.restype = None
+        _lib.ext_layer_chain.argtypes = [i64, vp, vp, vp, vp, vp, i64, i64, i32]
+        _lib.ext_layers_area.restype = None
+        _lib.ext_layers_area.argtypes = [vp, vp, i64, i64, vp, vp, i32]
         _lib.ext_select_sphere.restype = i64
         _lib.ext_select_sphere.argtypes = [vp, i64, i64, dbl, dbl, dbl, dbl, vp, i64, vp, vp, vp, i32]
         _lib.ext_select_threshold.restype = i64
@@ -202,8 +210,9 @@ def raster_tea_slab(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
 
 # ------------------------------------------------------------------ extension definitions
 
-def surface_map(tri_xy, tri_pos, tri_nrm, width, height, rows=None):
-    """Returns dict(tri_id, pos[3,h,w], nrm[3,h,w], area, covered, overlap) for rows [r0,r1)."""
+def surface_map(tri_xy, tri_pos, tri_nrm, width, height, rows=None, threads=0):
+    """Returns dict(tri_id, pos[3,h,w], nrm[3,h,w], area, covered, overlap) for rows [r0,r1).
+    threads > 0: row-parallel form (same arrays)."""
     tri = _f64(tri_xy, (3, 2))
     P = _f64(tri_pos, (3, 3))
     N = _f64(tri_nrm, (3, 3))
@@ -214,8 +223,12 @@ def surface_map(tri_xy, tri_pos, tri_nrm, width, height, rows=None):
     nrm = np.empty((3, n, width), np.float32)
     area = np.empty((n, width), np.float32)
     ov = C.c_int64(0)
-    cov = lib().ext_surface_map(_p(tri), _p(P), _p(N), tri.shape[0], width, height, r0, r1,
-                                _p(tri_id), _p(pos), _p(nrm), _p(area), C.addressof(ov))
+    if threads:
+        cov = lib().ext_surface_map_mt(_p(tri), _p(P), _p(N), tri.shape[0], width, height, r0, r1,
+                                       _p(tri_id), _p(pos), _p(nrm), _p(area), C.addressof(ov), threads)
+    else:
+        cov = lib().ext_surface_map(_p(tri), _p(P), _p(N), tri.shape[0], width, height, r0, r1,
+                                    _p(tri_id), _p(pos), _p(nrm), _p(area), C.addressof(ov))
     return dict(tri_id=tri_id, pos=pos, nrm=nrm, area=area, covered=int(cov), overlap=int(ov.value))
 
 
@@ -228,6 +241,30 @@ def select_sphere(pos, center, radius, data, mask, edited, value, threads=1):
                                        float(center[2]), float(radius), _p(_plane(data)),
                                        data.dtype.itemsize, _p(val), _p(_bytes1(_plane(mask))),
                                        _p(_bytes1(_plane(edited))), threads))
+
+
+def _ptr_array(arrs):
+    return (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+
+
+def select_sphere_batch(pos, strokes, layer_of, values, data, mask, edited, threads=1):
+    """K strokes (rows of `strokes` = cx, cy, cz, r) in ONE pass; stroke k writes values[k] into layer
+    layer_of[k] of the plane lists.  Returns the per-layer edited counts (int64 array, len(data))."""
+    assert pos.dtype == np.float32 and pos.flags.c_contiguous and pos.shape[0] == 3
+    L = len(data)
+    n = mask[0].size
+    assert pos[0].size == n
+    strokes = np.ascontiguousarray(strokes, np.float64).reshape(-1, 4)
+    K = strokes.shape[0]
+    lo = np.ascontiguousarray(layer_of, np.int32)
+    vals = np.ascontiguousarray(np.asarray(values).astype(data[0].dtype)).reshape(K)
+    for a in list(data) + list(mask) + list(edited):
+        _plane(a)
+    counts = np.zeros(L, np.int64)
+    lib().ext_select_sphere_batch_fused(_p(pos), n, n, _p(strokes), K, _p(lo), _ptr_array(data),
+                                        data[0].dtype.itemsize, _p(vals.view(np.uint8)), _ptr_array(mask),
+                                        _ptr_array(edited), _p(counts), L, threads)
+    return counts
 
 
 def select_threshold(attr, valid, lo, hi, data, mask, edited, value, threads=1):
@@ -254,6 +291,30 @@ def layer_op(op, da, ma, db, mb, dc, mc, threads=1):
     es = 0 if da is None else da.dtype.itemsize
     lib().ext_layer_op(OPS[op], _p(da), _p(_bytes1(ma)), _p(db), _p(_bytes1(mb)), _p(dc),
                        _p(_bytes1(_plane(mc))), es, n, threads)
+
+
+def layer_chain(ops, data, mask, dc, mc, threads=1):
+    """Fused left fold ((L0 op0 L1) op1 L2) ... in one pass; `data` may be None (mask-only)."""
+    nl = len(mask)
+    assert len(ops) == nl - 1
+    code = np.array([OPS[o] for o in ops], np.int32)
+    es = 0 if data is None else data[0].dtype.itemsize
+    for m in mask:
+        assert m.flags.c_contiguous
+        _bytes1(m)
+    lib().ext_layer_chain(nl, _p(code), None if data is None else _ptr_array(data), _ptr_array(mask),
+                          _p(dc), _p(_bytes1(_plane(mc))), es, mask[0].size, threads)
+
+
+def layers_area(area, masks, threads=1):
+    """Areas and texel counts of several layers in one pass: (float64[L], int64[L])."""
+    assert area.dtype == np.float32
+    area = np.ascontiguousarray(area)
+    L = len(masks)
+    sums, counts = np.zeros(L, np.float64), np.zeros(L, np.int64)
+    keep = [_bytes1(np.ascontiguousarray(m)) for m in masks]          # keeps any copy alive across the call
+    lib().ext_layers_area(_p(area), _ptr_array(keep), L, masks[0].size, _p(sums), _p(counts), threads)
+    return sums, counts
 
 
 def layer_area(area, mask, threads=1):

@@ -134,3 +134,91 @@ def test_outline_and_padding_known_answers():
     assert kn.padding(out, edited, 1, data, mask, 5) == 5                        # 3 + 3 - 1 corner neighbours
     assert kn.padding(out, edited, 0, data, mask, 5) == 0
     assert mask.sum() == 5 and (data[mask] == 5).all() and not (mask & (cov != 0)).any()
+
+
+# ---------------------------------------------------------------------------------------------
+# Row-parallel / fused forms used by the full-size parity tests and the CPU baseline: they must
+# equal the serial, op-by-op definitions above bit for bit.
+
+def _soup_scene(seed, ntri, w, h):
+    rng = np.random.default_rng(seed)
+    tri_xy = synth.random_soup(rng, ntri, float(max(w, h)))
+    return rng, tri_xy, rng.normal(size=(ntri, 3, 3)), rng.normal(size=(ntri, 3, 3))
+
+
+@pytest.mark.parametrize("threads", [1, 3, 8])
+@pytest.mark.parametrize("rows", [None, (5, 37), (0, 1), (30, 31)])
+def test_surface_map_row_parallel_equals_serial(threads, rows):
+    _, tri_xy, P, N = _soup_scene(11, 300, 48, 40)
+    tri_xy[7] = tri_xy[7][[0, 0, 1]]                       # a degenerate triangle
+    want = kn.surface_map(tri_xy, P, N, 48, 40, rows=rows)
+    got = kn.surface_map(tri_xy, P, N, 48, 40, rows=rows, threads=threads)
+    assert got["covered"] == want["covered"] and got["overlap"] == want["overlap"] and want["overlap"] > 0
+    assert np.array_equal(got["tri_id"], want["tri_id"])
+    for k in ("pos", "nrm", "area"):
+        assert np.array_equal(got[k].view(np.uint32), want[k].view(np.uint32)), k
+
+
+def test_tea_slab_with_band_lists_equals_full_plane_rows():
+    from helpers import random_tea_case
+    c = random_tea_case(5, ntri=400, w=96, h=80)
+    full = [c["data"].copy(), c["mask"].copy(), c["edited"].copy()]
+    args = (c["tri_xy"], c["tri_clip"], c["ww"], c["wh"], c["depth"], c["eps"], c["sfx"], c["sfy"], c["bx"], c["by"], c["shape"])
+    want = kn.raster_tea(*args, *full, c["value"], threads=0)
+    got_e = got_f = 0
+    for r0, r1 in ((0, 17), (17, 18), (18, 80)):
+        slab = [c["data"][r0:r1].copy(), c["mask"][r0:r1].copy().view(np.uint8), c["edited"][r0:r1].copy()]
+        e, f = kn.raster_tea_slab(*args, *slab, c["value"], 80, r0, threads=5)
+        got_e += e
+        got_f += f
+        for a, b in zip(slab, full):
+            assert np.array_equal(a, b[r0:r1])
+    assert (got_e, got_f) == want and want[0] > 0
+
+
+@pytest.mark.parametrize("esize_dtype", [np.uint8, np.int16, np.uint32])
+def test_fused_chain_equals_op_by_op(esize_dtype):
+    rng = np.random.default_rng(3)
+    n, nl = (37, 53), 6
+    ops = ["union", "intersection", "difference", "union", "masking"]
+    data = [rng.integers(1, 100, size=n).astype(esize_dtype) for _ in range(nl)]
+    mask = [(rng.random(n) < p).astype(np.uint8) * rng.integers(1, 255, size=n).astype(np.uint8)
+            for p in (0.5, 0.4, 0.7, 0.3, 0.2, 0.8)]            # "true" = any non-zero byte
+    cd, cm = data[0], mask[0]
+    for j in range(1, nl):
+        od, om = np.zeros(n, esize_dtype), np.zeros(n, np.uint8)
+        kn.layer_op(ops[j - 1], cd, cm, data[j], mask[j], od, om)
+        cd, cm = od, om
+    for threads in (1, 4):
+        fd, fm = np.full(n, 77, esize_dtype), np.full(n, 9, np.uint8)
+        kn.layer_chain(ops, data, mask, fd, fm, threads=threads)
+        assert np.array_equal(fd, cd) and np.array_equal(fm, cm)
+    mm = np.full(n, 9, np.uint8)
+    kn.layer_chain(ops, None, mask, None, mm, threads=2)          # mask-only chain
+    assert np.array_equal(mm, cm)
+
+
+def test_fused_batch_and_areas_equal_sequential():
+    rng = np.random.default_rng(4)
+    h, w, L, K = 40, 64, 5, 12
+    pos = rng.uniform(-1, 1, size=(3, h, w)).astype(np.float32)
+    pos[:, rng.random((h, w)) < 0.2] = np.nan
+    strokes = np.concatenate([rng.uniform(-1, 1, size=(K, 3)), rng.uniform(0.2, 0.9, size=(K, 1))], axis=1)
+    layer_of = rng.integers(0, L, size=K).astype(np.int32)
+    values = rng.integers(1, 250, size=K)
+    mk = lambda: [np.zeros((h, w), np.uint8) for _ in range(L)]
+    d1, m1, e1 = mk(), mk(), mk()
+    want = np.zeros(L, np.int64)
+    for k in range(K):
+        l = layer_of[k]
+        want[l] += kn.select_sphere(pos, strokes[k, :3], strokes[k, 3], d1[l], m1[l], e1[l], values[k])
+    d2, m2, e2 = mk(), mk(), mk()
+    got = kn.select_sphere_batch(pos, strokes, layer_of, values, d2, m2, e2, threads=3)
+    assert np.array_equal(got, want) and want.sum() > 0
+    for a, b in zip(d1 + m1 + e1, d2 + m2 + e2):
+        assert np.array_equal(a, b)
+    area = rng.random((h, w)).astype(np.float32)
+    sums, counts = kn.layers_area(area, m2, threads=3)
+    for l in range(L):
+        a, c = kn.layer_area(area, m2[l])
+        assert counts[l] == c and abs(sums[l] - a) <= 1e-12 * max(a, 1.0)
