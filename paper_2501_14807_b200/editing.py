@@ -112,12 +112,12 @@ class StrokeContext:
     def __init__(self, mesh, camera, depth, surface, device="cuda"):
         torch = _native.require_cuda()
         self.mesh, self.camera, self.depth, self.surface = mesh, camera, depth, surface
-        clip = camera.clip_coords(mesh.vertices)[mesh.triangles]            # (T,3,4) float64
-        self.tri_clip = torch.from_numpy(np.ascontiguousarray(clip)).to(device)
+        self.device = device
         self.tri_xy = surface.tri_xy
         self.edited = torch.zeros((surface.rows, surface.width), dtype=torch.uint8, device=device)
         self.scratch = _native.tea_scratch(mesh.num_triangles, surface.rows * surface.width, device)
-        self.recs = _native.tea_prepare(self.tri_xy, self.tri_clip, device)      # per-triangle evaluation records
+        self._cstruct = None              # (outline data_ptr, ml_stroke_ctx) of the one-call stroke path
+        self.refresh_camera()
         # footprint culling state: two tile bitmaps (this stroke / previous stroke) and whether the
         # edited plane may hold marks outside the previous bitmap (then it is reset as a whole)
         nwords = _native.tea_tile_words(surface.width, surface.rows)
@@ -125,8 +125,16 @@ class StrokeContext:
         self.edited_fully_dirty = False
         self.stroke_tiles = None          # tile bitmap of the last culled stroke (footprint of ctx.edited)
         self.cur = 0                      # tile buffer the next culled stroke writes; the other one is "previous"
-        self.device = device
-        self._cstruct = None              # (outline data_ptr, ml_stroke_ctx) of the one-call stroke path
+
+    def refresh_camera(self):
+        """(Re)derive everything that depends on the camera: clip coordinates MVP * vertex per triangle and
+        the per-triangle evaluation records; remembers which camera state they belong to."""
+        torch = _native._torch()
+        clip = self.camera.clip_coords(self.mesh.vertices)[self.mesh.triangles]     # (T,3,4) float64
+        self.tri_clip = torch.from_numpy(np.ascontiguousarray(clip)).to(self.device)
+        self.recs = _native.tea_prepare(self.tri_xy, self.tri_clip, self.device)    # per-triangle evaluation records
+        self.camera_key = self.camera.state_key()
+        self._cstruct = None              # the one-call stroke struct holds pointers to tri_clip / recs
 
     def begin_culled_stroke(self):
         """Footprint-culled strokes clear the edited plane per footprint; after a whole-plane stroke
@@ -143,9 +151,15 @@ class StrokeContext:
 
 def _stroke_checks(ctx, layer):
     s = ctx.surface
-    if ctx.depth.generation != ctx.camera.generation:
+    key = ctx.camera.state_key()
+    dkey = getattr(ctx.depth, "camera_key", None)
+    if ctx.depth.generation != ctx.camera.generation or (dkey is not None and dkey != key):
         raise StaleDepth("depth map was rendered for camera generation %d, camera is at %d"
                          % (ctx.depth.generation, ctx.camera.generation))
+    if ctx.camera_key != key:
+        # the camera moved and the caller supplied a fresh depth map: the projected triangles and the
+        # evaluation records of the context still belong to the old MVP -- rebuild them before any stroke
+        ctx.refresh_camera()
     if layer.shape != (s.rows, s.width):
         raise TargetMismatch("layer is %s, surface map slab is %s" % (layer.shape, (s.rows, s.width)))
     if s.covered == 0 and s.row0 == 0 and s.rows == s.height:

@@ -77,15 +77,52 @@ class Camera:
     height: int
     generation: int = field(default=0)
 
+    _TRACKED = ("view", "projection", "width", "height")
+
     def __post_init__(self):
-        self.view = np.asarray(self.view, dtype=np.float64).reshape(4, 4)
-        self.projection = np.asarray(self.projection, dtype=np.float64).reshape(4, 4)
+        object.__setattr__(self, "view", np.asarray(self.view, dtype=np.float64).reshape(4, 4))
+        object.__setattr__(self, "projection", np.asarray(self.projection, dtype=np.float64).reshape(4, 4))
+        self._validate()
+        object.__setattr__(self, "_ready", True)
+
+    def _validate(self):
         if self.width < 1 or self.height < 1:
             raise DegenerateCamera("viewport must be at least 1x1")
         m = self.projection @ self.view
         if not np.all(np.isfinite(m)) or abs(np.linalg.det(self.projection)) == 0.0 \
                 or abs(np.linalg.det(self.view)) == 0.0:
             raise DegenerateCamera("camera transforms must be finite and invertible")
+
+    def __setattr__(self, name, value):
+        """Assigning a new view / projection / viewport after construction is a camera change: the
+        generation counter is bumped here, so a depth map or stroke context made for the
+        old state is detected as stale without relying on the caller to count."""
+        if name in self._TRACKED and getattr(self, "_ready", False):
+            if name in ("view", "projection"):
+                value = np.asarray(value, dtype=np.float64).reshape(4, 4)
+            old = getattr(self, name)
+            object.__setattr__(self, name, value)
+            try:
+                self._validate()
+            except DegenerateCamera:
+                object.__setattr__(self, name, old)
+                raise
+            object.__setattr__(self, "generation", self.generation + 1)
+            return
+        object.__setattr__(self, name, value)
+
+    def set_view(self, view):
+        self.view = view
+        return self.generation
+
+    def set_projection(self, projection):
+        self.projection = projection
+        return self.generation
+
+    def state_key(self):
+        """Identity of the camera state a depth map / stroke context was derived from: generation,
+        viewport and the bytes of MVP (the last catches in-place edits of the matrices)."""
+        return (self.generation, int(self.width), int(self.height), self.mvp.tobytes())
 
     @property
     def mvp(self):
@@ -122,9 +159,10 @@ class DepthMap:
     """float32 plane on the device, 1.0 = background, tagged with the camera
     generation it was rendered for (StaleDepth detection)."""
 
-    def __init__(self, plane, generation):
+    def __init__(self, plane, generation, camera_key=None):
         self.plane = plane
         self.generation = generation
+        self.camera_key = camera_key          # Camera.state_key() at render time (None: caller-made plane)
 
     @property
     def shape(self):
@@ -138,7 +176,7 @@ def render_depth(mesh, camera, device="cuda"):
     xy, zn = window_triangles(mesh, camera)
     if xy.shape[0]:
         _native.raster_depth(torch.from_numpy(xy).to(device), torch.from_numpy(zn).to(device), depth)
-    return DepthMap(depth, camera.generation)
+    return DepthMap(depth, camera.generation, camera.state_key())
 
 
 def uv_coverage(mesh, resolution, device="cuda"):

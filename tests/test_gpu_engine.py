@@ -184,6 +184,42 @@ def test_stroke_over_background_and_errors():                         # SPEC.md:
                         ml.create_layer("small", "uint8", 64, 64, pool=ml.TexturePool()))
 
 
+def test_camera_move_rebuilds_the_stroke_context():                   # SPEC.md:281, 459 (stale MVP)
+    """Moving the camera bumps its generation by itself; a stroke with the old depth map raises StaleDepth, and
+    once the caller supplies a depth map of the new view the context re-derives its projected triangles, so the
+    stroke lands where the oracle puts it for the NEW camera (culled, streamed and one-call paths)."""
+    mesh, cam, surf, depth, ctx = _scene()
+    A = 128
+    tool = ml.EditingTool(px=50.0, py=44.0, shape=synth.circle_shape(10), value=6)
+    pool = ml.TexturePool()
+    ml.apply_stroke(ctx, tool, ml.create_layer("before", "uint8", A, A, pool=pool))
+    g0 = cam.generation
+    cam.set_view(synth.look_at((2.0, 1.0, 2.0), (0.0, 0.0, 0.0)))
+    assert cam.generation == g0 + 1
+    with pytest.raises(ml.StaleDepth):
+        ml.apply_stroke(ctx, tool, ml.create_layer("stale", "uint8", A, A, pool=pool))
+    ctx.depth = ml.render_depth(mesh, cam)
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool); edited = np.zeros((A, A), np.uint8)
+    want = _oracle_stroke(mesh, cam, tool, A, data, mask, edited)
+    assert want[0] > 0
+    outline = ml.build_outline_mask(surf.coverage, thickness=1)
+    for mode in ("cull", "stream", "one_call"):
+        layer = ml.create_layer(mode, "uint8", A, A, pool=pool)
+        if mode == "one_call":
+            t0 = ml.EditingTool(px=tool.px, py=tool.py, shape=tool.shape, value=tool.value, padding_radius=1)
+            res = ml.stroke(ctx, t0, layer, outline)
+            assert (res.edited_count, res.fragments) == want
+            assert np.array_equal(res.edited_mask.cpu().numpy(), edited)
+        else:
+            res = ml.apply_stroke(ctx, tool, layer, cull=(mode == "cull"))
+            assert (res.edited_count, res.fragments) == want, mode
+            assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+    # an in-place edit of the matrices (no setter involved) is caught through the MVP bytes in the key
+    cam.view[0, 3] += 0.25
+    with pytest.raises(ml.StaleDepth):
+        ml.apply_stroke(ctx, tool, ml.create_layer("inplace", "uint8", A, A, pool=pool))
+
+
 def test_stroke_with_padding_equals_oracle():                         # SPEC.md:476, 298, 309; acceptance #4
     mesh, cam, surf, depth, ctx = _scene()
     A = 128

@@ -138,6 +138,22 @@ def test_degenerate_camera_and_mesh_validation():
         ml.TriangleMesh(np.zeros((3, 3)), np.zeros((3, 3)), None, np.array([[0, 1, 2]]))
 
 
+def test_camera_generation_follows_every_change():
+    cam = synth.default_camera(64, 48)
+    k0, g0 = cam.state_key(), cam.generation
+    cam.set_view(synth.look_at((1.0, 2.0, 3.0), (0.0, 0.0, 0.0)))
+    assert cam.generation == g0 + 1 and cam.state_key() != k0
+    cam.projection = synth.perspective(30.0, 64 / 48, 0.1, 9.0)
+    cam.width = 32
+    assert cam.generation == g0 + 3
+    with pytest.raises(ml.DegenerateCamera):
+        cam.set_projection(np.zeros((4, 4)))
+    assert cam.generation == g0 + 3 and np.linalg.det(cam.projection) != 0.0          # a rejected change leaves no trace
+    k1 = cam.state_key()
+    cam.view[1, 3] += 1.0                                                             # in-place edit: same generation,
+    assert cam.generation == g0 + 3 and cam.state_key() != k1                         # different key
+
+
 def test_mesh_surface_area_known_answers():
     tri = ml.TriangleMesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0.0]]), None, np.zeros((3, 2)), np.array([[0, 1, 2]]))
     assert ml.mesh_surface_area(tri) == 0.5
