@@ -140,6 +140,18 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, const void* tea_recs
                   size_t worklist_bytes, const uint32_t* tile_cur, const uint32_t* tile_prev,
                   int64_t known_fragments, void* data, int esize,
                   uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream);
+/* Whole-atlas (no footprint culling) form of ml_tea_texels with the EditedAreaMask reset folded in:
+ * reset_edited != 0 clears `edited` inside the id stream -- each quad's edited bytes are
+ * zeroed by the thread that then processes the quad -- so the caller does not run a separate
+ * 1 B/texel memset pass.  The id map travels through a cp.async.bulk shared-memory ring (TMA) when
+ * the planes are 16-byte aligned.  known_fragments > 0 (the slab's covered-texel count, e.g. from
+ * ml_surface_resolve) is reported as counters[1] instead of being recounted.  Same planes and counters as ml_tea_texels(..., NULL, NULL, 0, ...)
+ * preceded by a memset of `edited`. */
+int ml_tea_stream(const void* tri_xy, const void* tri_clip, const void* tea_recs, int tri_dtype, int64_t ntri,
+                  int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
+                  const uint32_t* tri_flags, const ml_tea_params* params, void* worklist,
+                  size_t worklist_bytes, int reset_edited, int64_t known_fragments, void* data, int esize,
+                  uint32_t value_bits, uint8_t* mask, uint8_t* edited, uint64_t* counters, void* stream);
 /* Per-stroke conservative triangle classification from the clip-space vertices alone:
  * bit t (bit t&31 of word t>>5) = 0 iff no fragment of triangle t can pass the w > 0, window and
  * tool-range tests (KN:174, 181, 189) -- see surface.cu for the rounding-error argument.

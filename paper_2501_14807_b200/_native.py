@@ -94,6 +94,8 @@ def lib():
         "ml_owner_values": (i32, [vp, i64, vp, vp, i32, vp, vp, vp]),
         "ml_tea_texels": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
                                 vp, vp, i64, vp, i32, u32, vp, vp, vp, vp]),
+        "ml_tea_stream": (i32, [vp, vp, vp, i32, i64, i64, i64, i64, vp, vp, C.POINTER(_TeaParams), vp, sz,
+                                i32, i64, vp, i32, u32, vp, vp, vp, vp]),
         "ml_tea_classify_recs": (i32, [vp, i32, i64, C.POINTER(_TeaParams), vp, vp, i64, i64, i64, i64, vp, vp]),
         "ml_stroke": (i32, [C.POINTER(_StrokeCtx), i32, C.POINTER(_TeaParams), vp, i32, u32, vp, i64, vp, vp]),
         "ml_stroke_sequence": (i32, [C.POINTER(_StrokeCtx), i32, i64, C.POINTER(_TeaParams), vp, i32, C.POINTER(C.c_uint32), vp,
@@ -150,7 +152,7 @@ def lib():
 EXPORTED_SYMBOLS = (
     "ml_version", "ml_last_error", "ml_sm_count", "ml_raster_workspace_bytes", "ml_coverage_fill",
     "ml_raster_depth", "ml_raster_tea", "ml_raster_tri_id", "ml_surface_resolve",
-    "ml_surface_workspace_bytes", "ml_owner_values", "ml_tea_texels", "ml_tea_rec_bytes", "ml_tea_prepare",
+    "ml_surface_workspace_bytes", "ml_owner_values", "ml_tea_texels", "ml_tea_stream", "ml_tea_rec_bytes", "ml_tea_prepare",
     "ml_tea_classify_recs", "ml_stroke", "ml_stroke_sequence",
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
@@ -710,7 +712,7 @@ def owner_values(tri_id, values, out, keep=None):
 
 def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
                shape, data, mask, edited, value, *, row0=0, counts=None, classify=True, scratch=None,
-               height=None, tiles=None, known_fragments=0, recs=None):
+               height=None, tiles=None, known_fragments=0, recs=None, reset_edited=False):
     """TEA over the cached triangle-id map (SURVEY.md 8 note N1): same planes and counts as
     ``raster_tea`` when the uv layout has no overlaps.  Returns (edited_texels, fragments).
     ``classify`` runs the per-stroke triangle pre-pass (ml_tea_classify) so that texels of
@@ -721,7 +723,9 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
     cleared, and ``known_fragments`` (the slab's covered texel count) is reported as fragments.
     The caller must then NOT reset ``edited`` itself and must pass ``height``.  ``recs`` (from
     ``tea_prepare`` for the same triangle arrays) makes the evaluation read one prepared 144-byte
-    record per triangle instead of re-deriving the winding per texel (identical result)."""
+    record per triangle instead of re-deriving the winding per texel (identical result).
+    ``reset_edited`` (whole-atlas form only, i.e. without ``tiles``): the kernel clears ``edited``
+     while it streams the id map, instead of the caller running a memset pass first."""
     torch = require_cuda()
     rows, w = mask.shape
     dev = mask.device
@@ -757,6 +761,17 @@ def tea_texels(tri_xy, tri_clip, tri_id, ww, wh, depth, eps, sfx, sfy, bx, by,
             _check(lib().ml_tea_classify(_ptr(clip), dt, tri.shape[0], C.byref(p), _ptr(flags), _ptr(tri), w,
                                          hh, row0, rows, _ptr(cur), _stream()))
     cur, prev = tiles if tiles else (None, None)
+    if reset_edited and cur is not None:
+        raise TargetMismatch("reset_edited belongs to the whole-atlas form; culled strokes clear their footprint tiles")
+    if cur is None and (reset_edited or os.environ.get("ML_TEA_STREAM_ENTRY")):
+        _check(lib().ml_tea_stream(_ptr(tri), _ptr(clip), _ptr(recs), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
+                                   _ptr(flags), C.byref(p), _ptr(work), 0 if work is None else work.numel() * 8,
+                                   1 if reset_edited else 0, int(known_fragments), _ptr(data), esize, bits, _ptr(mask), _ptr(edited),
+                                   _ptr(ctr), _stream()))
+        if counts is not None:
+            return None
+        c = ctr.tolist()
+        return int(c[0]), int(c[1])
     _check(lib().ml_tea_texels(_ptr(tri), _ptr(clip), _ptr(recs), dt, tri.shape[0], w, row0, rows, _ptr(tri_id),
                                _ptr(flags), C.byref(p), _ptr(work), 0 if work is None else work.numel() * 8,
                                _ptr(cur), _ptr(prev), int(known_fragments),

@@ -201,6 +201,71 @@ ML_DEV void quad_write(void* data, uint32_t value, uint8_t* mask, uint8_t* edite
     quad_commit<ES>(data, value, mask, edited, i, hits, ew, mw, dw, cnt);
 }
 
+// 16-texel form of the quad write for threads that own 16 consecutive texels (i0 % 16 == 0, planes
+// 16-byte aligned): the byte planes move as ONE 128-bit access per plane and thread instead of four
+// 32-bit ones (a quarter of the memory instructions, 512 contiguous bytes per warp access).  hit16
+// bit e <-> texel i0 + e.  Same rule as quad_load / quad_commit: edited is always read (0 -> 1
+// count), mask / 1-byte data only when the vector is partially hit.
+template <int ES>
+ML_DEV void vec16_load(const void* data, const uint8_t* mask, const uint8_t* edited, long long i0,
+                       unsigned hit16, uint4& ew, uint4& mw, uint4& dw) {
+    ew = mw = dw = make_uint4(0u, 0u, 0u, 0u);
+    if (!hit16) return;
+    ew = *(const uint4*)(edited + i0);
+    if (hit16 != 0xffffu) {
+        mw = *(const uint4*)(mask + i0);
+        if (ES == 1) dw = *(const uint4*)((const uint8_t*)data + i0);
+    }
+}
+ML_DEV uint32_t merge_word(uint32_t old, uint32_t hm, uint32_t rep) { return (old & ~hm) | (rep & hm); }
+template <int ES>
+ML_DEV void vec16_commit(void* data, uint32_t value, uint8_t* mask, uint8_t* edited, long long i0,
+                         unsigned hit16, const uint4& ew, const uint4& mw, const uint4& dw, long long& cnt) {
+    if (!hit16) return;
+    const uint32_t h0 = spread4(hit16 & 0xfu), h1 = spread4((hit16 >> 4) & 0xfu),
+                   h2 = spread4((hit16 >> 8) & 0xfu), h3 = spread4((hit16 >> 12) & 0xfu);
+    cnt += __popc(zero_bytes_msb(ew.x) & h0) + __popc(zero_bytes_msb(ew.y) & h1) +
+           __popc(zero_bytes_msb(ew.z) & h2) + __popc(zero_bytes_msb(ew.w) & h3);
+    const uint32_t one = 0x01010101u;
+    const uint4 en = make_uint4(merge_word(ew.x, h0, one), merge_word(ew.y, h1, one), merge_word(ew.z, h2, one), merge_word(ew.w, h3, one));
+    if ((en.x ^ ew.x) | (en.y ^ ew.y) | (en.z ^ ew.z) | (en.w ^ ew.w)) *(uint4*)(edited + i0) = en;
+    if (hit16 == 0xffffu) *(uint4*)(mask + i0) = make_uint4(one, one, one, one);
+    else {
+        const uint4 mn = make_uint4(merge_word(mw.x, h0, one), merge_word(mw.y, h1, one), merge_word(mw.z, h2, one), merge_word(mw.w, h3, one));
+        if ((mn.x ^ mw.x) | (mn.y ^ mw.y) | (mn.z ^ mw.z) | (mn.w ^ mw.w)) *(uint4*)(mask + i0) = mn;
+    }
+    if (ES == 1) {
+        const uint32_t vr = (value & 0xffu) * 0x01010101u;
+        if (hit16 == 0xffffu) *(uint4*)((uint8_t*)data + i0) = make_uint4(vr, vr, vr, vr);
+        else {
+            const uint4 dn = make_uint4(merge_word(dw.x, h0, vr), merge_word(dw.y, h1, vr), merge_word(dw.z, h2, vr), merge_word(dw.w, h3, vr));
+            if ((dn.x ^ dw.x) | (dn.y ^ dw.y) | (dn.z ^ dw.z) | (dn.w ^ dw.w)) *(uint4*)((uint8_t*)data + i0) = dn;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned hits = (hit16 >> (4 * j)) & 0xfu;
+            if (!hits) continue;
+            const long long i = i0 + 4 * j;
+            if (ES == 2) {
+                uint16_t* pd = (uint16_t*)data + i;
+                if (hits == 0xfu) { const uint32_t vr = (value & 0xffffu) * 0x00010001u; *(uint2*)pd = make_uint2(vr, vr); }
+                else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) if (hits & (1u << e)) pd[e] = (uint16_t)value;
+                }
+            } else {
+                uint32_t* pd = (uint32_t*)data + i;
+                if (hits == 0xfu) *(uint4*)pd = make_uint4(value, value, value, value);
+                else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) if (hits & (1u << e)) pd[e] = value;
+                }
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Triangle setup: KN:32-41 (_ccw), KN:44-47 (tie rule), KN:50-59 (bbox, tightened).
 struct TriSetup {

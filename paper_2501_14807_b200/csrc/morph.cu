@@ -9,7 +9,9 @@
 // Each thread produces 4 horizontally adjacent texels: for every neighbour row it scans the
 // bytes [x-r, x+3+r] once and derives the four windows from a running byte mask, so the stencil
 // costs (2r+1)*(4+2r) byte reads per 4 texels, served from L1/L2.
+#include <stdlib.h>
 #include "common.cuh"
+#include "bulk.cuh"
 #include "meshlayers_b200.h"
 #include "internal.h"
 
@@ -216,6 +218,107 @@ padding_stream_kernel(const uint8_t* __restrict__ outline, const uint8_t* __rest
     block_count_add(cnt, count);
 }
 
+// Bulk-copy form of the streaming padding pass (the default for aligned planes): the outline plane
+// -- the kernel's whole 1 B/texel read stream -- is fetched by ONE producer lane per block with
+// cp.async.bulk into a PAD_STAGES x PAD_CHUNK shared-memory ring (bulk.cuh); the eight consumer warps
+// read their two 16-texel vectors of a chunk with conflict-free 128-bit LDS, release the stage and
+// only then look at the (rare) vectors that hold outline texels.  The register form above keeps
+// 64 B per thread in flight and stalls the whole block behind its slowest load (ncu r1: 28 % of the
+// DRAM peak, barrier + long-scoreboard stalls); here blocks/SM x PAD_STAGES x 8 KB are in flight
+// whatever the consumers are doing.
+#ifndef ML_PAD_STAGES
+#define ML_PAD_STAGES 4
+#endif
+constexpr int PAD_STAGES = ML_PAD_STAGES;
+constexpr int PAD_CHUNK = 8192;                       // bytes == texels per chunk
+constexpr int PAD_CONSUMER_WARPS = 8;
+constexpr int PAD_THREADS = 32 * (PAD_CONSUMER_WARPS + 1);
+constexpr int PAD_VPT = PAD_CHUNK / (16 * 32 * PAD_CONSUMER_WARPS);     // 16-texel vectors per consumer thread and chunk
+typedef BulkRing<PAD_STAGES, PAD_CHUNK> PadRing;
+
+// Vectors that hold outline texels are rare (an outline is a thin curve) but expensive: their
+// 3 x (2r+1) neighbourhood loads of `edited` are a dependent DRAM round trip.  Handled in place
+// they serialise the stream behind one lane per chunk (ncu r2: long_scoreboard 19.9 per issue, 37 %
+// of the DRAM peak -- the left / right island border puts one such vector into EVERY chunk, always
+// in the same warp).  Instead each warp queues the vector indices in shared memory and, once 32 are
+// waiting (and at the end), processes them one per lane, so 32 neighbourhood fetches overlap.
+constexpr int PAD_QCAP = 64;                          // queue slots per consumer warp (flushed at >= 32)
+
+template <int ES>
+ML_DEV long long pad_flush(long long* q, int count, int lane, const uint8_t* __restrict__ outline,
+                           const uint8_t* __restrict__ edited, long long width, long long in_row0, long long in_rows,
+                           long long out_row0, int r, void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask) {
+    long long cnt = 0;
+    __syncwarp();
+    if (lane < count) {
+        const long long i0 = q[lane];
+        const uint4 o = *(const uint4*)(outline + i0);
+        cnt = pad_vector<ES>(o, i0, edited, width, in_row0, in_rows, out_row0, r, data, value, mask);
+    }
+    __syncwarp();
+    return cnt;
+}
+
+template <int ES>
+__global__ void __launch_bounds__(PAD_THREADS)
+padding_bulk_kernel(const uint8_t* __restrict__ outline, const uint8_t* __restrict__ edited, long long width,
+                    long long in_row0, long long in_rows, long long out_row0, long long out_rows, int r,
+                    void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                    unsigned long long* count) {
+    extern __shared__ __align__(128) uint8_t pad_smem[];
+    PadRing& ring = *reinterpret_cast<PadRing*>(pad_smem);
+    __shared__ long long s_queue[PAD_CONSUMER_WARPS][PAD_QCAP];
+    const long long n = width * out_rows;                  // multiple of 16 (host checks width % 16 == 0)
+    const long long nchunks = (n + PAD_CHUNK - 1) / PAD_CHUNK;
+    if (threadIdx.x == 0) ring.init(PAD_CONSUMER_WARPS);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long cnt = 0;
+    RingPos<PAD_STAGES> pos;
+    if (warp == PAD_CONSUMER_WARPS) {
+        if (lane == 0) {
+            const uint64_t policy = l2_policy_evict_first();
+            for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
+                const long long base = c * PAD_CHUNK;
+                const unsigned bytes = (unsigned)(n - base < PAD_CHUNK ? n - base : PAD_CHUNK);
+                ring.produce(pos, outline + base, bytes, policy);
+            }
+        }
+    } else {
+        long long* q = s_queue[warp];
+        int queued = 0;                                    // warp-uniform
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
+            const long long base = c * PAD_CHUNK;
+            const unsigned bytes = (unsigned)(n - base < PAD_CHUNK ? n - base : PAD_CHUNK);
+            const uint8_t* b = ring.acquire(pos);
+            bool nz[PAD_VPT];
+#pragma unroll
+            for (int u = 0; u < PAD_VPT; ++u) {
+                const unsigned off = (unsigned)(u * 32 * PAD_CONSUMER_WARPS + threadIdx.x) << 4;
+                uint4 o = make_uint4(0, 0, 0, 0);
+                if (off < bytes) o = *(const uint4*)(b + off);
+                nz[u] = (o.x | o.y | o.z | o.w) != 0;
+            }
+            ring.release(pos);
+#pragma unroll
+            for (int u = 0; u < PAD_VPT; ++u) {
+                const unsigned bal = __ballot_sync(0xffffffffu, nz[u]);
+                if (bal == 0) continue;
+                if (nz[u]) q[queued + __popc(bal & ((1u << lane) - 1u))] = base + ((unsigned)(u * 32 * PAD_CONSUMER_WARPS + threadIdx.x) << 4);
+                queued += __popc(bal);
+                if (queued >= 32) {
+                    cnt += pad_flush<ES>(q, 32, lane, outline, edited, width, in_row0, in_rows, out_row0, r, data, value, mask);
+                    if (lane < queued - 32) q[lane] = q[32 + lane];       // <= 32 left over: move to the front
+                    queued -= 32;
+                    __syncwarp();
+                }
+            }
+        }
+        if (queued) cnt += pad_flush<ES>(q, queued, lane, outline, edited, width, in_row0, in_rows, out_row0, r, data, value, mask);
+    }
+    block_count_add(cnt, count);
+}
+
 // Footprint-culled form (single slab, width % 128 == 0, radius <= 4): `tile_bits` is the bitmap of
 // 128 x 8-texel tiles the TEA stroke could edit (ml_tea_classify).  A padded texel lies within
 // `radius` <= 4 texels of an edited one, i.e. in a marked tile or one of its 8 neighbours, so one
@@ -325,6 +428,26 @@ int ml_apply_padding(const uint8_t* outline, const uint8_t* edited, int64_t widt
         if (blocks > cap) blocks = cap;
         if (blocks < 1) blocks = 1;
         cudaStream_t st = (cudaStream_t)stream;
+        static const bool reg_form = getenv("ML_PAD_REGISTER_STREAM") != nullptr;       // the round-1 kernel, kept for comparison
+        if (!reg_form && nv * 16 >= 4 * PAD_CHUNK) {
+            static int per_sm[3] = {0, 0, 0};
+            const int k = esize == 1 ? 0 : (esize == 2 ? 1 : 2);
+            const void* fn = esize == 1 ? (const void*)padding_bulk_kernel<1> : (esize == 2 ? (const void*)padding_bulk_kernel<2> : (const void*)padding_bulk_kernel<4>);
+            if (!per_sm[k]) {
+                ML_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PadRing)));
+                int nb = 0;
+                ML_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, PAD_THREADS, sizeof(PadRing)));
+                per_sm[k] = nb > 0 ? nb : 1;
+            }
+            const long long nchunks = (nv * 16 + PAD_CHUNK - 1) / PAD_CHUNK;
+            long long g = (long long)ml_sm_count() * per_sm[k];
+            if (g > nchunks) g = nchunks;
+#define ML_LAUNCH_PADB(ES) padding_bulk_kernel<ES><<<(unsigned)g, PAD_THREADS, sizeof(PadRing), st>>>(outline, edited, width, in_row0, in_rows, out_row0, out_rows, (int)radius, data, value_bits, mask, (unsigned long long*)count)
+            if (esize == 1) ML_LAUNCH_PADB(1); else if (esize == 2) ML_LAUNCH_PADB(2); else ML_LAUNCH_PADB(4);
+#undef ML_LAUNCH_PADB
+            ML_CUDA(cudaGetLastError());
+            return ML_OK;
+        }
 #define ML_LAUNCH_PAD(ES) padding_stream_kernel<ES><<<(unsigned)blocks, BLOCK, 0, st>>>(outline, edited, width, in_row0, in_rows, out_row0, out_rows, (int)radius, data, value_bits, mask, (unsigned long long*)count)
         if (esize == 1) ML_LAUNCH_PAD(1); else if (esize == 2) ML_LAUNCH_PAD(2); else ML_LAUNCH_PAD(4);
 #undef ML_LAUNCH_PAD

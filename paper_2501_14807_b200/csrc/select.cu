@@ -10,8 +10,11 @@
 // quad_write), so hit-dense strokes do not degenerate into partial-sector byte stores.
 #include <cuda_fp16.h>
 #include <limits.h>
+#include <stdlib.h>
+#include <string.h>
 #include <math.h>
 #include "common.cuh"
+#include "bulk.cuh"
 #include "meshlayers_b200.h"
 #include "internal.h"
 
@@ -532,6 +535,239 @@ threshold_tiles_kernel(const float* __restrict__ attr, const uint8_t* __restrict
     block_count_add(cnt, counter);
 }
 
+// 16-texel form (default when attribute, valid and layer planes are 16-byte aligned).  A warp owns
+// 512 consecutive texels per step.  The ATTRIBUTE bytes are fetched lane-interleaved -- load k of
+// lane l is the 16-byte chunk k*32 + l of the warp's 512*S attribute bytes, so every load
+// instruction is one fully coalesced 512-byte access -- and the chunk hit bits are then moved with S
+// shuffles to the lane that owns the texels in BYTE-plane order (lane L owns texels 16L .. 16L+15),
+// where valid / edited / mask / data move as one 128-bit access per plane (vec16_load / _commit).
+// Compared with the quad form: the same attribute loads, a quarter of the byte-plane memory
+// instructions, and VT * S * 16 bytes in flight per thread.
+#ifndef ML_THR_VEC_MINB
+#define ML_THR_VEC_MINB 3
+#endif
+#ifndef ML_THR_PIPE
+#define ML_THR_PIPE 0
+#endif
+#ifndef ML_THR_WAVES
+#define ML_THR_WAVES 1      // grid = resident blocks x this
+#endif
+template <int KIND, int ES, bool HV = true>
+struct ThrTile {                               // one warp tile (512 texels) as held by one lane; HV: a valid plane exists
+    typedef typename AttrT<KIND>::T T;
+    static constexpr int S = (int)sizeof(T);   // 16-byte attribute chunks per 16 texels
+    static constexpr int EPC = 16 / S;         // texels per chunk
+    struct __align__(16) Chunk { T v[EPC]; };
+    Chunk a[S];
+    uint4 vm;
+
+    // issue the tile's loads: S lane-interleaved attribute chunks (+ the valid bytes of this lane's vector)
+    ML_DEV void load(const T* attr, const uint8_t* valid, long long tile, long long nv, int lane) {
+        const long long vec = (tile << 5) + lane;
+        vm = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+        if (valid && vec < nv) vm = ld_stream((const uint4*)valid + vec);
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const long long chunk = (tile << 5) * S + k * 32 + lane;
+            uint4 w = make_uint4(0u, 0u, 0u, 0u);
+            if (chunk < nv * S) w = ld_stream((const uint4*)attr + chunk);
+            memcpy(&a[k], &w, 16);
+        }
+    }
+    // same from a shared-memory copy of the tile's attribute bytes (`tile_smem`), of which `avail` bytes exist
+    ML_DEV void load_smem(const uint8_t* tile_smem, unsigned avail, const uint8_t* valid, long long tile, long long nv, int lane) {
+        const long long vec = (tile << 5) + lane;
+        vm = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+        if (HV && valid && vec < nv) vm = ld_stream((const uint4*)valid + vec);
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const unsigned off = (unsigned)(k * 32 + lane) << 4;
+            uint4 w = make_uint4(0u, 0u, 0u, 0u);
+            if (off < avail) w = *(const uint4*)(tile_smem + off);
+            memcpy(&a[k], &w, 16);
+        }
+    }
+    // hit bits of this lane's 16 texels (byte-plane order) from the lane-interleaved chunks
+    ML_DEV unsigned hits(const Thr& thr, long long tile, long long nv, int lane) const {
+        unsigned pk = 0;                       // S fields of EPC hit bits, field k = chunk k*32 + lane
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const long long chunk = (tile << 5) * S + k * 32 + lane;
+            unsigned h = 0;
+            if (chunk < nv * S) {
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) if (AttrT<KIND>::hit(a[k].v[e], thr)) h |= 1u << e;
+            }
+            pk |= h << (k * EPC);
+        }
+        // lane L's texels 16L .. 16L+15 are chunks L*S + j (j < S): load (L*S + j) / 32 of lane (L*S + j) % 32
+        unsigned mine = 0;
+        if (S == 1) mine = pk;
+        else {
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                const int ci = lane * S + j;
+                const unsigned got = __shfl_sync(0xffffffffu, pk, ci & 31);
+                mine |= ((got >> ((ci >> 5) * EPC)) & ((1u << EPC) - 1u)) << (j * EPC);
+            }
+        }
+        unsigned vbits = 0xffffu;
+        if (HV) vbits = nz_bits4(vm.x) | (nz_bits4(vm.y) << 4) | (nz_bits4(vm.z) << 8) | (nz_bits4(vm.w) << 12);
+        return ((tile << 5) + lane < nv) ? (mine & vbits) : 0u;
+    }
+};
+
+// Software pipeline: the loads of the warp's NEXT tile are issued before the hits of the current one
+// are written, so the dependent read of the `edited` bytes (hit vectors only) overlaps the next
+// attribute fetch instead of adding a second DRAM round trip to every step.  The grid is exactly
+// the resident blocks (persistent warps, static stride): no partial last wave.
+template <int KIND, int ES>
+__global__ void __launch_bounds__(BLOCK, ML_THR_VEC_MINB)
+threshold_vec_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ valid, long long n,
+                     double lo, double hi, Thr thr, void* __restrict__ data, int esize, uint32_t value,
+                     uint8_t* __restrict__ mask, uint8_t* __restrict__ edited, unsigned long long* counter) {
+    typedef typename AttrT<KIND>::T T;
+    const T* attr = (const T*)attr_;
+    long long cnt = 0;
+    const int lane = threadIdx.x & 31;
+    const long long nv = n >> 4;                                       // whole 16-texel vectors
+    const long long ntiles = (nv + 31) >> 5;                           // 512-texel warp tiles
+    const long long nwarps = ((long long)gridDim.x * BLOCK) >> 5;
+    long long t = ((long long)blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    ThrTile<KIND, ES> A, B;
+    auto commit = [&](const ThrTile<KIND, ES>& X, long long tile) {
+        const unsigned hit16 = X.hits(thr, tile, nv, lane);
+        const long long i0 = ((tile << 5) + lane) << 4;
+        uint4 ew, mw, dw;
+        vec16_load<ES>(data, mask, edited, i0, hit16, ew, mw, dw);
+        vec16_commit<ES>(data, value, mask, edited, i0, hit16, ew, mw, dw, cnt);
+    };
+#if ML_THR_PIPE
+    if (t < ntiles) {
+        A.load(attr, valid, t, nv, lane);
+        while (true) {
+            if (t + nwarps < ntiles) B.load(attr, valid, t + nwarps, nv, lane);
+            commit(A, t);
+            t += nwarps;
+            if (t >= ntiles) break;
+            if (t + nwarps < ntiles) A.load(attr, valid, t + nwarps, nv, lane);
+            commit(B, t);
+            t += nwarps;
+            if (t >= ntiles) break;
+        }
+    }
+#else
+    for (; t < ntiles; t += 2 * nwarps) {          // two tiles in flight per warp, no carry-over between steps
+        A.load(attr, valid, t, nv, lane);
+        if (t + nwarps < ntiles) B.load(attr, valid, t + nwarps, nv, lane);
+        const unsigned ha = A.hits(thr, t, nv, lane);
+        const unsigned hb = t + nwarps < ntiles ? B.hits(thr, t + nwarps, nv, lane) : 0u;
+        const long long ia = ((t << 5) + lane) << 4, ib = (((t + nwarps) << 5) + lane) << 4;
+        uint4 ew[2], mw[2], dw[2];
+        vec16_load<ES>(data, mask, edited, ia, ha, ew[0], mw[0], dw[0]);
+        vec16_load<ES>(data, mask, edited, ib, hb, ew[1], mw[1], dw[1]);
+        vec16_commit<ES>(data, value, mask, edited, ia, ha, ew[0], mw[0], dw[0], cnt);
+        vec16_commit<ES>(data, value, mask, edited, ib, hb, ew[1], mw[1], dw[1], cnt);
+    }
+#endif
+    const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    const long long nthreads = (long long)gridDim.x * BLOCK;
+    for (long long i = (nv << 4) + tid; i < n; i += nthreads) {           // < 16 texels of tail
+        if (valid && valid[i] == 0) continue;
+        const double v = AttrT<KIND>::get(attr[i]);
+        if (lo <= v && v <= hi) hit_write(data, esize, value, mask, edited, i, cnt);
+    }
+    block_count_add(cnt, counter);
+}
+
+// Bulk-copy form (default): the attribute plane -- the kernel's read stream -- travels through a
+// THB_STAGES x 16 KB shared-memory ring filled by one producer lane per block with cp.async.bulk
+// (bulk.cuh), so the HBM pipe stays full while a consumer warp waits for the `edited` bytes of its
+// hit vectors (the register forms above alternate between the two round trips and top out near
+// 0.6 of the peak with the bench's 19 % coherent hits).  Consumer warps read their tiles from the
+// stage lane-interleaved (conflict-free 128-bit LDS) and use the same shuffle transposition and
+// 128-bit byte-plane accesses as threshold_vec_kernel.
+#ifndef ML_THB_STAGES
+#define ML_THB_STAGES 2
+#endif
+#ifndef ML_THB_CHUNK
+#define ML_THB_CHUNK 32768
+#endif
+#ifndef ML_THB_CW
+#define ML_THB_CW 8
+#endif
+constexpr int THB_STAGES = ML_THB_STAGES;
+constexpr int THB_CHUNK = ML_THB_CHUNK;                // attribute bytes per chunk
+constexpr int THB_CW = ML_THB_CW;                      // consumer warps
+constexpr int THB_THREADS = 32 * (THB_CW + 1);
+typedef BulkRing<THB_STAGES, THB_CHUNK> ThrRing;
+
+template <int KIND, int ES, bool HV>
+__global__ void __launch_bounds__(THB_THREADS)
+threshold_bulk_kernel(const void* __restrict__ attr_, const uint8_t* __restrict__ valid, long long n,
+                      double lo, double hi, Thr thr, void* __restrict__ data, int esize, uint32_t value,
+                      uint8_t* __restrict__ mask, uint8_t* __restrict__ edited, unsigned long long* counter) {
+    typedef typename AttrT<KIND>::T T;
+    constexpr int S = (int)sizeof(T);
+    constexpr int TILE_BYTES = 512 * S;                     // attribute bytes of one 512-texel warp tile
+    constexpr int TPW = THB_CHUNK / TILE_BYTES / THB_CW;    // tiles per consumer warp and chunk (1, 2, 4)
+    static_assert(TPW >= 1, "chunk too small for the consumer warps");
+    extern __shared__ __align__(128) uint8_t thb_smem[];
+    ThrRing& ring = *reinterpret_cast<ThrRing*>(thb_smem);
+    const T* attr = (const T*)attr_;
+    const long long nv = n >> 4;                            // whole 16-texel vectors
+    const long long abytes = nv * 16 * S;                   // their attribute bytes
+    const long long nchunks = (abytes + THB_CHUNK - 1) / THB_CHUNK;
+    if (threadIdx.x == 0) ring.init(THB_CW);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long cnt = 0;
+    RingPos<THB_STAGES> pos;
+    if (warp == THB_CW) {
+        if (lane == 0) {
+            const uint64_t policy = l2_policy_evict_first();
+            for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
+                const long long base = c * THB_CHUNK;
+                const unsigned bytes = (unsigned)(abytes - base < THB_CHUNK ? abytes - base : THB_CHUNK);
+                ring.produce(pos, (const uint8_t*)attr + base, bytes, policy);
+            }
+        }
+    } else {
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
+            const long long base = c * THB_CHUNK;
+            const unsigned bytes = (unsigned)(abytes - base < THB_CHUNK ? abytes - base : THB_CHUNK);
+            const uint8_t* b = ring.acquire(pos);
+            ThrTile<KIND, ES, HV> X[TPW];
+            const long long tile0 = base / TILE_BYTES + warp * TPW;        // this warp's first tile of the chunk
+#pragma unroll
+            for (int j = 0; j < TPW; ++j) {
+                const unsigned toff = (unsigned)(warp * TPW + j) * TILE_BYTES;
+                X[j].load_smem(b + toff, bytes > toff ? bytes - toff : 0u, valid, tile0 + j, nv, lane);
+            }
+            ring.release(pos);
+            unsigned hit16[TPW];
+            uint4 ew[TPW], mw[TPW], dw[TPW];
+#pragma unroll
+            for (int j = 0; j < TPW; ++j) hit16[j] = X[j].hits(thr, tile0 + j, nv, lane);
+#pragma unroll
+            for (int j = 0; j < TPW; ++j)
+                vec16_load<ES>(data, mask, edited, (((tile0 + j) << 5) + lane) << 4, hit16[j], ew[j], mw[j], dw[j]);
+#pragma unroll
+            for (int j = 0; j < TPW; ++j)
+                vec16_commit<ES>(data, value, mask, edited, (((tile0 + j) << 5) + lane) << 4, hit16[j], ew[j], mw[j], dw[j], cnt);
+        }
+        if (blockIdx.x == 0) {
+            for (long long i = (nv << 4) + threadIdx.x; i < n; i += 32 * THB_CW) {       // < 16 texels of tail
+                if (valid && valid[i] == 0) continue;
+                const double v = AttrT<KIND>::get(attr[i]);
+                if (lo <= v && v <= hi) hit_write(data, esize, value, mask, edited, i, cnt);
+            }
+        }
+    }
+    block_count_add(cnt, counter);
+}
+
+// ---------------------------------------------------------------------------------------------
 // thresholds rounded inward once, in every attribute domain; false for an empty or NaN interval
 inline bool make_thr(double lo, double hi, Thr& thr) {
     if (!(lo <= hi)) return false;
@@ -563,6 +799,49 @@ int launch_threshold(const void* attr, const uint8_t* valid, long long n, double
     const unsigned grid = stream_grid(4 * TU, n);
     Thr thr;
     if (!make_thr(lo, hi, thr)) return ML_OK;  // empty or NaN interval: nothing can hit
+    static const bool quad_form = getenv("ML_THR_QUAD_STREAM") != nullptr;              // the round-1 kernel, kept for comparison
+    if (vec && !quad_form && aligned(attr, 16) && (!valid || aligned(valid, 16)) && n >= 512) {
+        static const bool reg_form = getenv("ML_THR_REGISTER_STREAM") != nullptr;     // threshold_vec_kernel, kept for comparison
+        if (!reg_form && n >= 4 * THB_CHUNK) {
+            static int per_sm_b[6] = {0, 0, 0, 0, 0, 0};
+            const int kb = (esize == 1 ? 0 : (esize == 2 ? 1 : 2)) + (valid ? 3 : 0);
+            const void* fb = valid ? (esize == 1 ? (const void*)threshold_bulk_kernel<KIND, 1, true>
+                                   : (esize == 2 ? (const void*)threshold_bulk_kernel<KIND, 2, true> : (const void*)threshold_bulk_kernel<KIND, 4, true>))
+                                   : (esize == 1 ? (const void*)threshold_bulk_kernel<KIND, 1, false>
+                                   : (esize == 2 ? (const void*)threshold_bulk_kernel<KIND, 2, false> : (const void*)threshold_bulk_kernel<KIND, 4, false>));
+            if (!per_sm_b[kb]) {
+                ML_CUDA(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ThrRing)));
+                int nb = 0;
+                ML_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fb, THB_THREADS, sizeof(ThrRing)));
+                per_sm_b[kb] = nb > 0 ? nb : 1;
+            }
+            const long long nchunks = ((n >> 4) * 16 * (long long)sizeof(T) + THB_CHUNK - 1) / THB_CHUNK;
+            long long gb = (long long)ml_sm_count() * per_sm_b[kb];
+            if (gb > nchunks) gb = nchunks;
+            void* kargs[] = {(void*)&attr, (void*)&valid, (void*)&n, (void*)&lo, (void*)&hi, (void*)&thr, (void*)&data, (void*)&esize,
+                             (void*)&value, (void*)&mask, (void*)&edited, (void*)&counter};
+            ML_CUDA(cudaLaunchKernel(fb, dim3((unsigned)gb), dim3(THB_THREADS), kargs, sizeof(ThrRing), st));
+            return ML_OK;
+        }
+        static int per_sm[3] = {0, 0, 0};                             // resident blocks per SM of each instantiation
+        const int k = esize == 1 ? 0 : (esize == 2 ? 1 : 2);
+        const void* fn = esize == 1 ? (const void*)threshold_vec_kernel<KIND, 1>
+                       : (esize == 2 ? (const void*)threshold_vec_kernel<KIND, 2> : (const void*)threshold_vec_kernel<KIND, 4>);
+        if (!per_sm[k]) {
+            int nb = 0;
+            ML_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, BLOCK, 0));
+            per_sm[k] = nb > 0 ? nb : 1;
+        }
+        long long g16 = (long long)ml_sm_count() * per_sm[k] * ML_THR_WAVES;
+        const long long need = ((n >> 9) + BLOCK / 32) / (BLOCK / 32);       // one warp tile per warp at least
+        if (g16 > need) g16 = need;
+        if (g16 < 1) g16 = 1;
+#define ML_LAUNCH_THRV(ES) threshold_vec_kernel<KIND, ES><<<(unsigned)g16, BLOCK, 0, st>>>(attr, valid, n, lo, hi, thr, data, esize, value, mask, edited, counter)
+        if (esize == 1) ML_LAUNCH_THRV(1); else if (esize == 2) ML_LAUNCH_THRV(2); else ML_LAUNCH_THRV(4);
+#undef ML_LAUNCH_THRV
+        ML_CUDA(cudaGetLastError());
+        return ML_OK;
+    }
 #define ML_LAUNCH_THR(ES) threshold_kernel<KIND, ES><<<grid, BLOCK, 0, st>>>(attr, valid, n, lo, hi, thr, data, esize, value, mask, edited, counter)
     if (!vec) ML_LAUNCH_THR(0);
     else if (esize == 1) ML_LAUNCH_THR(1);

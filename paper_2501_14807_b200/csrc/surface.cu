@@ -6,7 +6,9 @@
 // One thread per texel, consecutive threads on consecutive texels of a row: the 4-byte id read
 // is a coalesced stream; the triangle records are gathers that hit L1/L2 because neighbouring
 // texels share their owner.
+#include <stdlib.h>
 #include "common.cuh"
+#include "bulk.cuh"
 #include "meshlayers_b200.h"
 #include "internal.h"
 
@@ -376,6 +378,7 @@ struct TeaCull {
     const uint32_t* tile_prev;       // may be NULL
     int segs_per_row;
     unsigned long long known_fragments;   // covered texels of the slab (a skipping kernel cannot count them)
+    int reset_edited;                // stream form only: the kernel clears the edited plane while it streams
 };
 ML_DEV bool tile_bit(const uint32_t* bits, int tile) { return (__ldg(bits + (tile >> 5)) >> (tile & 31)) & 1u; }
 
@@ -504,6 +507,175 @@ tea_stream_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, 
     block_count_add(frags, counters + 1);
 }
 
+// STREAM kernel, bulk-copy form (default for aligned planes with the classification bitmap and a
+// work list).  The owner-id map -- 4 B/texel, the whole algorithmic traffic of the pass -- is fetched
+// by one producer lane per block with cp.async.bulk into a TS_STAGES x TS_CHUNK shared-memory ring
+// (bulk.cuh) that sits beside the triangle bitmap; TS_CW consumer warps read their quads of a chunk
+// with 128-bit LDS and release the stage.  The register form above keeps 64 B per thread in flight
+// (one 1024-thread block per SM next to the 125 KB bitmap = 64 KB per SM) and, worse, spends ~100
+// instructions per quad in the generic tea_process (ncu r2: 60 % issue-active at 44 % of the DRAM
+// peak -- issue bound).  This kernel's hot loop is ~30 instructions per quad:
+//   * the bitmap is stored one word late (s_bits[0] = 0), so an uncovered texel (id -1 -> word
+//     index -1 + 1 = 0, bit 31) reads "not flagged" without a compare / select;
+//   * 32-bit offsets relative to the chunk; nothing but the flag lookups, the edited reset and one
+//     ballot per quad row in the loop; quads with flagged texels (the stroke's footprint, a few per
+//     cent of the atlas) leave through an out-of-line append to the evaluation work list.
+// RESET: the kernel also clears the edited plane (SPEC.md:255 EditedAreaMask reset) -- each thread
+// zeroes the 4 edited bytes of a quad before the quad can be appended, so the separate 1 B/texel
+// memset pass (and its launch) disappears into this stream.
+#ifndef ML_TS_STAGES
+#define ML_TS_STAGES 3
+#endif
+#ifndef ML_TS_CW
+#define ML_TS_CW 16
+#endif
+#ifndef ML_TS_QPT
+#define ML_TS_QPT 4
+#endif
+constexpr int TS_STAGES = ML_TS_STAGES;
+constexpr int TS_CW = ML_TS_CW;                        // consumer warps
+constexpr int TS_QPT = ML_TS_QPT;                      // quads per consumer thread and chunk
+constexpr int TS_CT = 32 * TS_CW;                      // consumer threads
+constexpr int TS_CHUNK = 16 * TS_CT * TS_QPT;          // bytes of ids per chunk (32 KB = 8192 texels)
+constexpr int TS_THREADS = TS_CT + 32;
+typedef BulkRing<TS_STAGES, TS_CHUNK> TeaRing;
+
+// out-of-line: a warp in which some lane holds a quad with flagged texels appends those quads to the
+// work list (one warp-aggregated atomic); whatever does not fit is evaluated here
+template <typename T, int ES>
+__device__ __noinline__ void tea_stream_append(unsigned keep, long long q, uint4 ids, const TeaWork wk, const TeaParams& p,
+                                               const T* __restrict__ tri_xy, const T* __restrict__ tri_clip,
+                                               long long width, long long row0, bool small, void* __restrict__ data,
+                                               uint32_t value, uint8_t* __restrict__ mask, uint8_t* __restrict__ edited,
+                                               unsigned long long* counters) {
+    const int lane = threadIdx.x & 31;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep != 0);
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(wk.count, (unsigned long long)__popc(bal));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (!keep) return;
+    const unsigned long long at = slot + __popc(bal & ((1u << lane) - 1u));
+    if (at < wk.cap) {
+        unsigned long long* e3 = wk.entries + 3 * at;
+        e3[0] = ((unsigned long long)q << 4) | keep;
+        e3[1] = (unsigned long long)ids.x | ((unsigned long long)ids.y << 32);
+        e3[2] = (unsigned long long)ids.z | ((unsigned long long)ids.w << 32);
+        return;
+    }
+    const int t4[4] = {(int)ids.x, (int)ids.y, (int)ids.z, (int)ids.w};
+    unsigned hits = 0;
+    for (int e = 0; e < 4; ++e) {
+        if (!(keep & (1u << e))) continue;
+        int x, y;
+        texel_xy((q << 2) + e, width, row0, small, x, y);
+        if (tea_texel_eval(tri_xy, tri_clip, wk.recs, t4[e], x, y, p)) hits |= 1u << e;
+    }
+    long long newly = 0;
+    if (hits) quad_write<ES>(data, value, mask, edited, q << 2, hits, newly);
+    if (newly) atomicAdd(counters, (unsigned long long)newly);
+}
+
+template <typename T, int ES, bool SMEM, bool RESET, bool COUNT>
+__global__ void __launch_bounds__(TS_THREADS, 1)
+tea_stream_bulk_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_clip, long long width,
+                       long long row0, long long n, const int* __restrict__ tri_id,
+                       const uint32_t* __restrict__ gbits, long long nwords, TeaParams p, TeaWork wk,
+                       void* __restrict__ data, int esize, uint32_t value,
+                       uint8_t* __restrict__ mask, uint8_t* __restrict__ edited,
+                       unsigned long long* counters, unsigned long long known_frags) {
+    extern __shared__ __align__(128) uint8_t ts_smem[];
+    TeaRing& ring = *reinterpret_cast<TeaRing*>(ts_smem);
+    uint32_t* s_bits = reinterpret_cast<uint32_t*>(ts_smem + sizeof(TeaRing));      // [0] = 0, [1 + k] = gbits[k]
+    const long long nq = n >> 2;
+    const long long id_bytes = nq << 4;
+    const long long nchunks = (id_bytes + TS_CHUNK - 1) / TS_CHUNK;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) ring.init(TS_CW);
+    __syncthreads();
+    RingPos<TS_STAGES> pos;
+    long long frags = 0;
+    const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
+    if (warp == TS_CW) {
+        // producer: the id stream starts while the consumers still copy the bitmap
+        if (lane == 0) {
+            const uint64_t policy = l2_policy_evict_first();
+            for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
+                const long long base = c * TS_CHUNK;
+                const unsigned bytes = (unsigned)(id_bytes - base < TS_CHUNK ? id_bytes - base : TS_CHUNK);
+                ring.produce(pos, (const uint8_t*)tri_id + base, bytes, policy);
+            }
+        }
+    } else {
+        if (SMEM) {
+            if (threadIdx.x == 0) s_bits[0] = 0u;
+            for (long long k = threadIdx.x; k < nwords; k += TS_CT) s_bits[1 + k] = gbits[k];
+            asm volatile("bar.sync 1, %0;" :: "n"(TS_CT) : "memory");                // consumers only
+        }
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
+            const long long base = c * TS_CHUNK;
+            const unsigned bytes = (unsigned)(id_bytes - base < TS_CHUNK ? id_bytes - base : TS_CHUNK);
+            const uint8_t* b = ring.acquire(pos);
+            uint4 ids[TS_QPT];
+#pragma unroll
+            for (int u = 0; u < TS_QPT; ++u) {
+                const unsigned off = (unsigned)(u * TS_CT + threadIdx.x) << 4;
+                ids[u] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                if (off < bytes) ids[u] = *(const uint4*)(b + off);
+            }
+            ring.release(pos);
+            uint8_t* ed = edited + (base >> 2);                        // the chunk's edited bytes
+            const long long q0 = base >> 4;                            // the chunk's first quad
+#pragma unroll
+            for (int u = 0; u < TS_QPT; ++u) {
+                const unsigned qo = (unsigned)(u * TS_CT + threadIdx.x);           // quad offset in the chunk
+                const int t0 = (int)ids[u].x, t1 = (int)ids[u].y, t2 = (int)ids[u].z, t3 = (int)ids[u].w;
+                unsigned keep;
+                if (SMEM) {
+                    keep = (__funnelshift_r(s_bits[1 + (t0 >> 5)], 0u, (unsigned)t0) & 1u)
+                         | ((__funnelshift_r(s_bits[1 + (t1 >> 5)], 0u, (unsigned)t1) & 1u) << 1)
+                         | ((__funnelshift_r(s_bits[1 + (t2 >> 5)], 0u, (unsigned)t2) & 1u) << 2)
+                         | ((__funnelshift_r(s_bits[1 + (t3 >> 5)], 0u, (unsigned)t3) & 1u) << 3);
+                } else {
+                    keep = (t0 >= 0 ? (__ldg(gbits + (t0 >> 5)) >> (t0 & 31)) & 1u : 0u)
+                         | ((t1 >= 0 ? (__ldg(gbits + (t1 >> 5)) >> (t1 & 31)) & 1u : 0u) << 1)
+                         | ((t2 >= 0 ? (__ldg(gbits + (t2 >> 5)) >> (t2 & 31)) & 1u : 0u) << 2)
+                         | ((t3 >= 0 ? (__ldg(gbits + (t3 >> 5)) >> (t3 & 31)) & 1u : 0u) << 3);
+                }
+                const bool present = (qo << 4) < bytes;
+                if (COUNT) {
+                    if ((t0 | t1 | t2 | t3) >= 0) frags += 4;
+                    else if (present) frags += 4 + ((t0 >> 31) + (t1 >> 31) + (t2 >> 31) + (t3 >> 31));
+                }
+                if (RESET && present) *(uint32_t*)(ed + (qo << 2)) = 0u;
+                if (__any_sync(0xffffffffu, keep != 0))
+                    tea_stream_append<T, ES>(keep, q0 + qo, ids[u], wk, p, tri_xy, tri_clip, width, row0, small,
+                                             data, value, mask, edited, counters);
+            }
+        }
+        // tail (n % 4 texels) by the first consumer threads of block 0
+        if (blockIdx.x == 0) {
+            long long newly = 0;
+            for (long long i = (nq << 2) + threadIdx.x; i < n; i += TS_CT) {
+                if (RESET) edited[i] = 0;
+                const int t = tri_id[i];
+                if (t < 0) continue;
+                if (COUNT) ++frags;
+                if (!tri_flag(gbits, t)) continue;
+                int x, y;
+                texel_xy(i, width, row0, small, x, y);
+                if (!tea_texel_eval(tri_xy, tri_clip, wk.recs, t, x, y, p)) continue;
+                if (edited[i] == 0) ++newly;
+                store_value(data, esize, i, value);
+                mask[i] = 1;
+                edited[i] = 1;
+            }
+            if (newly) atomicAdd(counters, (unsigned long long)newly);
+        }
+    }
+    if (COUNT) block_count_add(frags, counters + 1);
+    else if (blockIdx.x == 0 && threadIdx.x == 0 && known_frags) atomicAdd(counters + 1, known_frags);
+}
+
 // TILE kernel (footprint culling).  One WARP per LISTED 128x8-texel tile: first the tiles of the
 // previous stroke that this stroke does not revisit get their edited bytes cleared (this replaces
 // the whole-plane reset of the EditedAreaMask), then every tile of this stroke's list
@@ -628,6 +800,11 @@ inline unsigned grid_for(long long n) {
     return (unsigned)blocks;
 }
 
+inline bool tea_register_stream() {                   // ML_TEA_REGISTER_STREAM: the round-1 stream kernel, kept for comparison
+    static const bool v = getenv("ML_TEA_REGISTER_STREAM") != nullptr;
+    return v;
+}
+
 constexpr int TEA_BIG_BLOCK = 1024;                  // block size when the bitmap lives in shared memory
 constexpr long long TEA_SMEM_MAX_BYTES = 200 * 1024; // bitmap size limit for the shared-memory path
 
@@ -648,7 +825,27 @@ int launch_tea_es(const T* tri_xy, const T* tri_clip, const TeaRec* recs, long l
         if (blocks < 1) blocks = 1;
         tea_tile_kernel<T, (ES > 0 ? ES : 1)><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, tri_clip, width, row0, rows,
             tri_id, bits, p, wk, cull, data, value, mask, edited, ctr);
+    } else if (ES > 0 && !tea_register_stream() && n >= TS_CHUNK && bits != nullptr && wk.entries != nullptr) {
+        // bulk-copy ring form: one block per SM; the bitmap sits in shared memory beside the ring when it fits
+        const bool sm_bits = (size_t)(nwords + 1) * 4 + sizeof(TeaRing) + 128 <= (size_t)227 * 1024;
+        const size_t shmem = sizeof(TeaRing) + (sm_bits ? (size_t)(nwords + 1) * 4 : 0);
+        const long long nchunks = ((n >> 2) * 16 + TS_CHUNK - 1) / TS_CHUNK;
+        long long blocks = ml_sm_count();
+        if (blocks > nchunks) blocks = nchunks;
+        constexpr int E = ES > 0 ? ES : 1;
+        const bool count = cull.known_fragments == 0;      // the caller knows the slab's covered-texel count: nothing to recount
+#define ML_LAUNCH_TSB(SM, RS, CN) do { \
+            auto kern = tea_stream_bulk_kernel<T, E, SM, RS, CN>; \
+            ML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem)); \
+            kern<<<(unsigned)blocks, TS_THREADS, shmem, st>>>(tri_xy, tri_clip, width, row0, n, tri_id, bits, nwords, p, wk, \
+                data, esize, value, mask, edited, ctr, cull.known_fragments); } while (0)
+#define ML_LAUNCH_TSB2(SM, RS) do { if (count) ML_LAUNCH_TSB(SM, RS, true); else ML_LAUNCH_TSB(SM, RS, false); } while (0)
+        if (sm_bits) { if (cull.reset_edited) ML_LAUNCH_TSB2(true, true); else ML_LAUNCH_TSB2(true, false); }
+        else { if (cull.reset_edited) ML_LAUNCH_TSB2(false, true); else ML_LAUNCH_TSB2(false, false); }
+#undef ML_LAUNCH_TSB2
+#undef ML_LAUNCH_TSB
     } else if (smem) {
+        if (cull.reset_edited) ML_CUDA(cudaMemsetAsync(edited, 0, (size_t)n, st));
         // one 1024-thread block per SM (the bitmap takes most of its shared memory)
         auto kern = tea_stream_kernel<T, ES, TEA_BIG_BLOCK, true>;
         ML_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(nwords * 4)));
@@ -659,6 +856,7 @@ int launch_tea_es(const T* tri_xy, const T* tri_clip, const TeaRec* recs, long l
         kern<<<(unsigned)blocks, TEA_BIG_BLOCK, (size_t)(nwords * 4), st>>>(tri_xy, tri_clip, width, row0, n, tri_id,
             bits, nwords, p, wk, data, esize, value, mask, edited, ctr);
     } else {
+        if (cull.reset_edited) ML_CUDA(cudaMemsetAsync(edited, 0, (size_t)n, st));
         long long blocks = (items + BLOCK - 1) / BLOCK;
         const long long cap = (long long)ml_sm_count() * 16;
         if (blocks > cap) blocks = cap;
@@ -806,7 +1004,28 @@ int ml_tea_texels(const void* tri_xy, const void* tri_clip, const void* tea_recs
     if (n <= 0) return ML_OK;
     TeaParams p = ml_make_tea_params(tp);
     unsigned long long* ctr = (unsigned long long*)counters;
-    TeaCull cull{tile_cur, tile_cur ? tile_prev : nullptr, 0, (unsigned long long)(known_fragments > 0 ? known_fragments : 0)};
+    TeaCull cull{tile_cur, tile_cur ? tile_prev : nullptr, 0, (unsigned long long)(known_fragments > 0 ? known_fragments : 0), 0};
+    if (tri_dtype == ML_F32)
+        return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, (const TeaRec*)tea_recs, width, row0, n, tri_id, tri_flags, ntri, p,
+                                 worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);
+    if (tri_dtype == ML_F64)
+        return launch_tea_texels((const double*)tri_xy, (const double*)tri_clip, (const TeaRec*)tea_recs, width, row0, n, tri_id, tri_flags, ntri, p,
+                                 worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);
+    return ml_fail(ML_ERR_ARG, "tri_dtype must be ML_F32 or ML_F64");
+}
+
+int ml_tea_stream(const void* tri_xy, const void* tri_clip, const void* tea_recs, int tri_dtype, int64_t ntri,
+                  int64_t width, int64_t row0, int64_t rows, const int32_t* tri_id,
+                  const uint32_t* tri_flags, const ml_tea_params* tp, void* worklist, size_t worklist_bytes,
+                  int reset_edited, int64_t known_fragments, void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
+                  uint64_t* counters, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
+    const long long n = (long long)rows * width;
+    if (n <= 0) return ML_OK;
+    TeaParams p = ml_make_tea_params(tp);
+    unsigned long long* ctr = (unsigned long long*)counters;
+    TeaCull cull{nullptr, nullptr, 0, (unsigned long long)(known_fragments > 0 ? known_fragments : 0), reset_edited ? 1 : 0};
     if (tri_dtype == ML_F32)
         return launch_tea_texels((const float*)tri_xy, (const float*)tri_clip, (const TeaRec*)tea_recs, width, row0, n, tri_id, tri_flags, ntri, p,
                                  worklist, worklist_bytes, cull, data, esize, value_bits, mask, edited, ctr, st);

@@ -188,11 +188,11 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
                            known_fragments=s.covered, recs=ctx.recs)
         ctx.end_culled_stroke()
     elif s.overlap == 0 and not force_direct:
-        ctx.edited.zero_()
+        # whole-atlas form: the EditedAreaMask reset is folded into the id stream
         ctx.edited_fully_dirty = True
         ctx.stroke_tiles = None
         _native.tea_texels(ctx.tri_xy, ctx.tri_clip, s.tri_id, *args, row0=s.row0, counts=counts,
-                           scratch=ctx.scratch, recs=ctx.recs)
+                           scratch=ctx.scratch, recs=ctx.recs, reset_edited=True, known_fragments=s.covered)
     else:
         ctx.edited.zero_()
         ctx.edited_fully_dirty = True

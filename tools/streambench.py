@@ -64,6 +64,7 @@ def main():
     ap.add_argument("--inner", type=int, default=10)
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--eager", action="store_true", help="three plain calls per case and no timing (for ncu captures)")
     ap.add_argument("names", nargs="*")
     a = ap.parse_args()
     args = argparse.Namespace(atlas=a.atlas, layers=a.layers, quads=707, window=1024)
@@ -113,6 +114,8 @@ def main():
         ("tpa stream", lambda: nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, 7, counts=c1), wl.algorithmic_bytes(n, "tpa", T)),
         ("tea stream (stage: reset+classify+stream+eval)", lambda: ml.apply_stroke(ctx, tool, layers[0], eps=wl.eps, cull=False), wl.algorithmic_bytes(n, "tea", T)),
         ("threshold stream", lambda: nat.select_threshold(attr, None, wl.thr[0], wl.thr[1], layers[2].data, layers[2].mask, edited[2], 9, counts=c1), 4 * n),
+        ("thr-nohit stream", lambda: nat.select_threshold(attr, None, 50.0, 60.0, layers[2].data, layers[2].mask, edited[2], 9, counts=c1), 4 * n),
+        ("thr-allhit stream", lambda: nat.select_threshold(attr, None, -50.0, 60.0, layers[2].data, layers[2].mask, edited[2], 9, counts=c1), 8 * n),
         ("mask_op", lambda: nat.layer_op("union", None, layers[0].mask, None, layers[1].mask, None, tmp_mask), 3 * n),
         ("layer_op union u8 (6 B/texel)", lambda: nat.layer_op("union", layers[0].data, layers[0].mask, layers[1].data, layers[1].mask, out_layer.data, out_layer.mask), 6 * n),
         ("area L=%d bench masks" % L, lambda: nat.layer_area(surf.area, [l.mask for l in layers], sums=sums, counts=cnts), wl.algorithmic_bytes(n, "area", T)),
@@ -129,6 +132,11 @@ def main():
             continue
         if "dense" in name:
             dense_masks()
+        if a.eager:
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            continue
         ms, graphed = time_graph(fn, a.inner, a.reps)
         gbs = nbytes / ms / 1e6
         res[name] = {"ms": round(ms, 4), "gb_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4), "graph": graphed}
