@@ -86,6 +86,8 @@ int ml_raster_tea(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
                   const ml_tea_params* params, void* data, int esize, uint32_t value_bits,
                   uint8_t* mask, uint8_t* edited, uint64_t* counters,
                   void* workspace, size_t workspace_bytes, void* stream);
+/* data and mask may be NULL: the kernel then only marks the stroke's texels in `edited` (what the
+ * host-buffer twin uses to bring back the written SET instead of whole planes). */
 
 /* ---- surface map (north star (1); definition: oracle/kn_port.c ext_surface_map) ---------------
  * Pass 1: tri_id[y][x] = largest index of a triangle covering the texel centre, -1 if none.
@@ -381,19 +383,30 @@ int ml_tool_rays(const double* inv_view_proj, int64_t cam_w, int64_t cam_h, doub
                  double* origins, double* dirs, uint64_t* count, void* stream);
 
 /* ---- host-buffer entry points: exact drop-ins for the reference's numpy signatures ------------
- * All pointers are HOST pointers; the call copies inputs to the device, runs the kernels above,
- * copies the planes back and synchronises.  tri arrays are float64 (the reference widens to
- * float64 anyway).  Returns ML_OK / error; counts through out-params. */
-int ml_coverage_fill_host(const double* tri_xy, int64_t ntri, int64_t width, int64_t height,
+ * (KN:84 coverage_fill, KN:103 raster_depth, KN:135-136 raster_tea.)  All pointers are HOST pointers
+ * to ordinary pageable memory; planes are mutated in place, counts come back through out-params, the
+ * call returns when the caller's planes are final.  tri arrays are float32 or float64 (tri_dtype =
+ * ML_F32 / ML_F64; the kernels widen per use like KN:88, 113, 151).
+ *
+ * Implementation (csrc/hostpath.cu): a persistent per-process arena (device scratch, pinned staging
+ * chunks, streams, worker threads -- nothing is allocated per call once warm) and pipelined uploads.
+ * coverage_fill and raster_tea never upload the caller's planes: the kernels mark the texels they
+ * write in a zeroed device plane, that SET returns over PCIe as a bitmap (or as the list of its
+ * non-zero 64-texel words when that is smaller) and the reference's write rule (KN:97-99, 198-202:
+ * count target bytes that are 0, then store) is applied to the caller's planes by the worker threads.
+ * One call at a time per process (the reference's single-writer rule); ml_host_release()
+ * frees the arena. */
+int ml_coverage_fill_host(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
                           uint8_t* out, int64_t* written);
-int ml_raster_depth_host(const double* tri_xy, const double* tri_zn, int64_t ntri,
+int ml_raster_depth_host(const void* tri_xy, const void* tri_zn, int tri_dtype, int64_t ntri,
                          float* depth, int64_t width, int64_t height, int64_t* updated);
-int ml_raster_tea_host(const double* tri_xy, const double* tri_clip, int64_t ntri,
+int ml_raster_tea_host(const void* tri_xy, const void* tri_clip, int tri_dtype, int64_t ntri,
                        double ww, double wh, const float* depth, int64_t depth_w, int64_t depth_h,
                        double eps, int eps_f32, double sfx, double sfy, double bx, double by,
                        const uint8_t* shape, int64_t shape_w, int64_t shape_h,
                        void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
                        int64_t width, int64_t height, int64_t* edited_count, int64_t* fragments);
+void ml_host_release(void);
 
 /* KN:303: *count = M; rows are written only when M <= capacity (re-call with a larger buffer otherwise) */
 int ml_expand_pairs_ordered_host(const double* verts, int64_t nverts, const int32_t* tris, int64_t ntri,

@@ -128,10 +128,11 @@ def lib():
         "ml_resolve_display": (i32, [vp, i32, vp, i64, dbl, dbl, vp, vp, i32, vp, vp]),
         "ml_pack_mask": (i32, [vp, i64, vp, vp]),
         "ml_unpack_mask": (i32, [vp, i64, vp, vp]),
-        "ml_coverage_fill_host": (i32, [vp, i64, i64, i64, vp, vp]),
-        "ml_raster_depth_host": (i32, [vp, vp, i64, vp, i64, i64, vp]),
-        "ml_raster_tea_host": (i32, [vp, vp, i64, dbl, dbl, vp, i64, i64, dbl, i32, dbl, dbl, dbl, dbl,
+        "ml_coverage_fill_host": (i32, [vp, i32, i64, i64, i64, vp, vp]),
+        "ml_raster_depth_host": (i32, [vp, vp, i32, i64, vp, i64, i64, vp]),
+        "ml_raster_tea_host": (i32, [vp, vp, i32, i64, dbl, dbl, vp, i64, i64, dbl, i32, dbl, dbl, dbl, dbl,
                                      vp, i64, i64, vp, i32, u32, vp, vp, i64, i64, vp, vp]),
+        "ml_host_release": (None, []),
         "ml_expand_pairs_workspace_bytes": (sz, [i64]),
         "ml_expand_pairs_count": (i32, [vp, vp, vp, vp, vp, i64, vp, dbl, vp, sz, vp, vp]),
         "ml_expand_pairs_emit": (i32, [vp, vp, vp, i64, vp, vp, vp, vp]),
@@ -159,7 +160,7 @@ EXPORTED_SYMBOLS = (
     "ml_select_threshold", "ml_plane_tile_range", "ml_select_threshold_tiles", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_apply_padding_tiles", "ml_apply_padding_tiles_rows", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
-    "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host",
+    "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host", "ml_host_release",
     "ml_expand_pairs_workspace_bytes", "ml_expand_pairs_count", "ml_expand_pairs_emit", "ml_raycast",
     "ml_expand_pairs_ordered_host", "ml_raycast_host", "ml_tool_rays")
 
@@ -287,6 +288,14 @@ def _counters(n, device):
 # KN twins
 # =============================================================================================
 
+def _tri_host(*arrays):
+    """Host triangle arrays as the host twins take them: C-contiguous, all float32 (when every input
+    is float32 -- half the PCIe bytes) or all float64.  Returns (arrays..., ML dtype code)."""
+    f32 = all(isinstance(a, np.ndarray) and a.dtype == np.float32 for a in arrays)
+    dt = np.float32 if f32 else np.float64
+    return tuple(np.ascontiguousarray(a, dtype=dt) for a in arrays) + (ML_F32 if f32 else ML_F64,)
+
+
 def coverage_fill(tri_xy, width, height, out, *, row0=0, counts=None):
     """KN:84-100.  ``out``: (rows, width) uint8/bool plane, numpy (host) or torch CUDA (device).
     Returns the number of texels that went 0 -> 1 (or None when ``counts`` is supplied)."""
@@ -294,11 +303,11 @@ def coverage_fill(tri_xy, width, height, out, *, row0=0, counts=None):
     if isinstance(out, np.ndarray):
         if out.shape != (height, width) or out.dtype.itemsize != 1 or not out.flags.c_contiguous:
             raise TargetMismatch("out must be a contiguous (height, width) uint8 plane")
-        tri = np.ascontiguousarray(tri_xy, dtype=np.float64)
+        tri, dt = _tri_host(tri_xy)
         if tri.shape[1:] != (3, 2):
             raise TargetMismatch("tri_xy must be (T,3,2)")
         written = C.c_int64(0)
-        _check(L.ml_coverage_fill_host(tri.ctypes.data, tri.shape[0], width, height,
+        _check(L.ml_coverage_fill_host(tri.ctypes.data, dt, tri.shape[0], width, height,
                                        out.ctypes.data, C.addressof(written)))
         return int(written.value)
     require_cuda()
@@ -314,21 +323,21 @@ def coverage_fill(tri_xy, width, height, out, *, row0=0, counts=None):
     return None if counts is not None else int(ctr[0].item())
 
 
-def raster_depth(tri_xy, tri_zn, depth):
+def raster_depth(tri_xy, tri_zn, depth, *, count=True):
     """KN:103-132.  ``depth``: (Wh, Ww) float32 plane updated in place.  The reference's return
     value depends on triangle order; this returns the number of texels whose
-    depth changed instead."""
+    depth changed instead.  ``count=False`` (device planes) skips that count -- it costs a copy of
+    the plane and a host read-back -- and returns None."""
     L = lib()
     if isinstance(depth, np.ndarray):
         if depth.dtype != np.float32 or depth.ndim != 2 or not depth.flags.c_contiguous:
             raise TargetMismatch("depth must be a contiguous 2-D float32 plane")
-        tri = np.ascontiguousarray(tri_xy, dtype=np.float64)
-        zn = np.ascontiguousarray(tri_zn, dtype=np.float64)
+        tri, zn, dt = _tri_host(tri_xy, tri_zn)
         if tri.shape[1:] != (3, 2) or zn.shape != (tri.shape[0], 3):
             raise TargetMismatch("tri_xy must be (T,3,2) and tri_zn (T,3)")
         upd = C.c_int64(0)
         h, w = depth.shape
-        _check(L.ml_raster_depth_host(tri.ctypes.data, zn.ctypes.data, tri.shape[0],
+        _check(L.ml_raster_depth_host(tri.ctypes.data, zn.ctypes.data, dt, tri.shape[0],
                                       depth.ctypes.data, w, h, C.addressof(upd)))
         return int(upd.value)
     torch = require_cuda()
@@ -340,11 +349,13 @@ def raster_depth(tri_xy, tri_zn, depth):
     dt = ML_F32 if tri.dtype == torch.float32 else ML_F64
     if zn.shape[0] != tri.shape[0]:
         raise TargetMismatch("tri_xy / tri_zn triangle counts differ")
-    before = depth.clone()
+    before = depth.clone() if count else None
     ws, nb = _workspace(tri.shape[0], depth.device)
     h, w = depth.shape
     _check(L.ml_raster_depth(_ptr(tri), _ptr(zn), dt, tri.shape[0], _ptr(depth), w, h,
                              _ptr(ws), nb, _stream()))
+    if not count:
+        return None
     return int((before.view(torch.int32) != depth.view(torch.int32)).sum().item())
 
 
@@ -379,8 +390,7 @@ def raster_tea(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
                 raise TargetMismatch(nm + " plane must be C-contiguous")
         if mask.dtype.itemsize != 1 or edited.dtype.itemsize != 1:
             raise TargetMismatch("mask / edited planes must be bool or uint8")
-        tri = np.ascontiguousarray(tri_xy, dtype=np.float64)
-        clip = np.ascontiguousarray(tri_clip, dtype=np.float64)
+        tri, clip, dt = _tri_host(tri_xy, tri_clip)
         if tri.shape[1:] != (3, 2) or clip.shape != (tri.shape[0], 3, 4):
             raise TargetMismatch("tri_xy must be (T,3,2) and tri_clip (T,3,4)")
         dep = np.ascontiguousarray(depth, dtype=np.float32)
@@ -390,7 +400,7 @@ def raster_tea(tri_xy, tri_clip, ww, wh, depth, eps, sfx, sfy, bx, by,
         _check_window(ww, wh, dep.shape, shp.shape)
         bits, esize = value_bits(value, data)
         ec, fr = C.c_int64(0), C.c_int64(0)
-        _check(L.ml_raster_tea_host(tri.ctypes.data, clip.ctypes.data, tri.shape[0], float(ww), float(wh),
+        _check(L.ml_raster_tea_host(tri.ctypes.data, clip.ctypes.data, dt, tri.shape[0], float(ww), float(wh),
                                     dep.ctypes.data, dep.shape[1], dep.shape[0], float(eps),
                                     int(eps_is_f32(eps)), float(sfx), float(sfy), float(bx), float(by),
                                     shp.ctypes.data, shp.shape[1], shp.shape[0], data.ctypes.data, esize,

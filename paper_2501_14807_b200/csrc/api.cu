@@ -1,6 +1,5 @@
-// Library plumbing (errors, device query) and the host-buffer entry points that mirror the
-// reference's numpy signatures one-to-one (KN:84, 103, 135-136): host pointers in, planes
-// mutated in place, counts out.  These are what a `meshlayers._native` stub binds directly.
+// Library plumbing (errors, device query) and the host-buffer forms of the octree baseline kernels.
+// The host-buffer twins of the hot path (KN:84, 103, 135-136) live in hostpath.cu.
 #include <stdio.h>
 #include <string.h>
 #include <math.h>
@@ -48,112 +47,6 @@ int ml_sm_count(void) {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
     g_sm_count = n;
     return n;
-}
-
-int ml_coverage_fill_host(const double* tri_xy, int64_t ntri, int64_t width, int64_t height,
-                          uint8_t* out, int64_t* written) {
-    if (written) *written = 0;
-    if (width <= 0 || height <= 0) return ML_OK;
-    if (ml_sm_count() <= 0) return ml_fail(ML_ERR_NO_DEVICE, "no CUDA device");
-    const size_t plane = (size_t)width * height, ws = ml_raster_workspace_bytes(ntri);
-    DevBuf d_tri, d_out, d_ws, d_cnt;
-    ML_CUDA(d_tri.alloc((size_t)ntri * 6 * sizeof(double)));
-    ML_CUDA(d_out.alloc(plane));
-    ML_CUDA(d_ws.alloc(ws));
-    ML_CUDA(d_cnt.alloc(2 * sizeof(uint64_t)));
-    ML_CUDA(cudaMemcpyAsync(d_tri.p, tri_xy, (size_t)ntri * 6 * sizeof(double), cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_out.p, out, plane, cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemsetAsync(d_cnt.p, 0, 2 * sizeof(uint64_t), 0));
-    ML_TRY(ml_coverage_fill(d_tri.p, ML_F64, ntri, width, height, 0, height, d_out.as<uint8_t>(),
-                            d_cnt.as<uint64_t>(), d_ws.p, ws, nullptr));
-    uint64_t c[2] = {0, 0};
-    ML_CUDA(cudaMemcpyAsync(out, d_out.p, plane, cudaMemcpyDeviceToHost, 0));
-    ML_CUDA(cudaMemcpyAsync(c, d_cnt.p, sizeof c, cudaMemcpyDeviceToHost, 0));
-    ML_CUDA(cudaStreamSynchronize(0));
-    if (written) *written = (int64_t)c[0];
-    return ML_OK;
-}
-
-int ml_raster_depth_host(const double* tri_xy, const double* tri_zn, int64_t ntri,
-                         float* depth, int64_t width, int64_t height, int64_t* updated) {
-    if (updated) *updated = 0;
-    if (width <= 0 || height <= 0) return ML_OK;
-    if (ml_sm_count() <= 0) return ml_fail(ML_ERR_NO_DEVICE, "no CUDA device");
-    const size_t plane = (size_t)width * height * sizeof(float), ws = ml_raster_workspace_bytes(ntri);
-    DevBuf d_tri, d_zn, d_depth, d_ws;
-    ML_CUDA(d_tri.alloc((size_t)ntri * 6 * sizeof(double)));
-    ML_CUDA(d_zn.alloc((size_t)ntri * 3 * sizeof(double)));
-    ML_CUDA(d_depth.alloc(plane));
-    ML_CUDA(d_ws.alloc(ws));
-    ML_CUDA(cudaMemcpyAsync(d_tri.p, tri_xy, (size_t)ntri * 6 * sizeof(double), cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_zn.p, tri_zn, (size_t)ntri * 3 * sizeof(double), cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_depth.p, depth, plane, cudaMemcpyHostToDevice, 0));
-    ML_TRY(ml_raster_depth(d_tri.p, d_zn.p, ML_F64, ntri, d_depth.as<float>(), width, height, d_ws.p, ws, nullptr));
-    // the reference's count is order dependent; report texels whose value changed
-    float* after = (float*)malloc(plane);
-    if (!after) return ml_fail(ML_ERR_ARG, "out of host memory");
-    cudaError_t e = cudaMemcpy(after, d_depth.p, plane, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) { free(after); return ml_fail_cuda(e, "depth read-back"); }
-    int64_t changed = 0;
-    const size_t n = (size_t)width * height;
-    for (size_t i = 0; i < n; ++i) changed += memcmp(after + i, depth + i, sizeof(float)) != 0;
-    memcpy(depth, after, plane);
-    free(after);
-    if (updated) *updated = changed;
-    return ML_OK;
-}
-
-int ml_raster_tea_host(const double* tri_xy, const double* tri_clip, int64_t ntri,
-                       double ww, double wh, const float* depth, int64_t depth_w, int64_t depth_h,
-                       double eps, int eps_f32, double sfx, double sfy, double bx, double by,
-                       const uint8_t* shape, int64_t shape_w, int64_t shape_h,
-                       void* data, int esize, uint32_t value_bits, uint8_t* mask, uint8_t* edited,
-                       int64_t width, int64_t height, int64_t* edited_count, int64_t* fragments) {
-    if (edited_count) *edited_count = 0;
-    if (fragments) *fragments = 0;
-    if (width <= 0 || height <= 0) return ML_OK;
-    if (esize != 1 && esize != 2 && esize != 4) return ml_fail(ML_ERR_ARG, "esize must be 1, 2 or 4");
-    if (!(depth_w >= ceil(ww) && depth_h >= ceil(wh)))
-        return ml_fail(ML_ERR_ARG, "depth plane smaller than the window");
-    if (shape_w <= 0 || shape_h <= 0) return ml_fail(ML_ERR_ARG, "empty tool shape");
-    if (ml_sm_count() <= 0) return ml_fail(ML_ERR_NO_DEVICE, "no CUDA device");
-    const size_t plane = (size_t)width * height, ws = ml_raster_workspace_bytes(ntri);
-    DevBuf d_tri, d_clip, d_depth, d_shape, d_data, d_mask, d_edited, d_ws, d_cnt;
-    ML_CUDA(d_tri.alloc((size_t)ntri * 6 * sizeof(double)));
-    ML_CUDA(d_clip.alloc((size_t)ntri * 12 * sizeof(double)));
-    ML_CUDA(d_depth.alloc((size_t)depth_w * depth_h * sizeof(float)));
-    ML_CUDA(d_shape.alloc((size_t)shape_w * shape_h));
-    ML_CUDA(d_data.alloc(plane * esize));
-    ML_CUDA(d_mask.alloc(plane));
-    ML_CUDA(d_edited.alloc(plane));
-    ML_CUDA(d_ws.alloc(ws));
-    ML_CUDA(d_cnt.alloc(2 * sizeof(uint64_t)));
-    ML_CUDA(cudaMemcpyAsync(d_tri.p, tri_xy, (size_t)ntri * 6 * sizeof(double), cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_clip.p, tri_clip, (size_t)ntri * 12 * sizeof(double), cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_depth.p, depth, (size_t)depth_w * depth_h * sizeof(float), cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_shape.p, shape, (size_t)shape_w * shape_h, cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_data.p, data, plane * esize, cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_mask.p, mask, plane, cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemcpyAsync(d_edited.p, edited, plane, cudaMemcpyHostToDevice, 0));
-    ML_CUDA(cudaMemsetAsync(d_cnt.p, 0, 2 * sizeof(uint64_t), 0));
-    ml_tea_params tp;
-    memset(&tp, 0, sizeof tp);
-    tp.ww = ww; tp.wh = wh; tp.eps = eps; tp.sfx = sfx; tp.sfy = sfy; tp.bx = bx; tp.by = by;
-    tp.depth = d_depth.as<float>(); tp.shape = d_shape.as<uint8_t>();
-    tp.depth_w = depth_w; tp.depth_h = depth_h; tp.shape_w = shape_w; tp.shape_h = shape_h;
-    tp.eps_f32 = eps_f32;
-    ML_TRY(ml_raster_tea(d_tri.p, d_clip.p, ML_F64, ntri, width, height, 0, height, &tp, d_data.p, esize,
-                         value_bits, d_mask.as<uint8_t>(), d_edited.as<uint8_t>(), d_cnt.as<uint64_t>(),
-                         d_ws.p, ws, nullptr));
-    uint64_t c[2] = {0, 0};
-    ML_CUDA(cudaMemcpyAsync(data, d_data.p, plane * esize, cudaMemcpyDeviceToHost, 0));
-    ML_CUDA(cudaMemcpyAsync(mask, d_mask.p, plane, cudaMemcpyDeviceToHost, 0));
-    ML_CUDA(cudaMemcpyAsync(edited, d_edited.p, plane, cudaMemcpyDeviceToHost, 0));
-    ML_CUDA(cudaMemcpyAsync(c, d_cnt.p, sizeof c, cudaMemcpyDeviceToHost, 0));
-    ML_CUDA(cudaStreamSynchronize(0));
-    if (edited_count) *edited_count = (int64_t)c[0];
-    if (fragments) *fragments = (int64_t)c[1];
-    return ML_OK;
 }
 
 // KN:303-329 with host buffers.  *count = number of (cell, triangle) rows the expansion produces;

@@ -143,8 +143,8 @@ struct TeaFn {
         if (!a.keep || !tea_fragment(p, e0, e1, e2, a.c0, a.c1, a.c2)) return;
         const long long i = (y - row0) * width + x;
         if (byte_set1_was0(edited, i)) ++c0;                             // KN:198-199, 202
-        store_value(data, esize, i, value);                              // KN:200
-        mask[i] = 1;                                                     // KN:201
+        if (data) store_value(data, esize, i, value);                    // KN:200 (NULL: the caller only wants the hit set)
+        if (mask) mask[i] = 1;                                           // KN:201
     }
 };
 

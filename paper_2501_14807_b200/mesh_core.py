@@ -175,7 +175,7 @@ def render_depth(mesh, camera, device="cuda"):
     depth = torch.ones((camera.height, camera.width), dtype=torch.float32, device=device)
     xy, zn = window_triangles(mesh, camera)
     if xy.shape[0]:
-        _native.raster_depth(torch.from_numpy(xy).to(device), torch.from_numpy(zn).to(device), depth)
+        _native.raster_depth(torch.from_numpy(xy).to(device), torch.from_numpy(zn).to(device), depth, count=False)
     return DepthMap(depth, camera.generation, camera.state_key())
 
 

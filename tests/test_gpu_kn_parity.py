@@ -203,6 +203,34 @@ def test_tea_random_vs_oracle(seed):
     assert np.array_equal(m.cpu().numpy(), rm) and np.array_equal(e.cpu().numpy(), re)
 
 
+@pytest.mark.parametrize("seed", range(14))
+def test_host_plane_twins_vs_oracle(seed):
+    """The host-buffer twins (numpy planes, KN call shape): nothing of the caller's planes is uploaded, the
+    written SET comes back as a bitmap (dense strokes) or as a word list (sparse strokes) and is applied to
+    pre-dirtied host planes.  Ragged plane sizes (texel count not a multiple of 64), float32 and float64
+    triangles, every plane kind, planes holding bytes other than 0 / 1."""
+    kinds = [(np.uint8, 200), (np.int8, -7), (np.int16, 3000), (np.int32, -123456), (np.uint32, 3123456789),
+             (np.float16, 1.5), (np.float32, -0.25)]
+    dt, val = kinds[seed % len(kinds)]
+    w, h = [(96, 128), (50, 37), (129, 65), (64, 64)][seed % 4]
+    c = helpers.random_tea_case(5000 + seed, ntri=40 if seed % 2 else 900, w=w, h=h, plane_dtype=dt, value=val,
+                                tri_dtype=np.float32 if seed % 3 == 0 else np.float64)
+    rng = np.random.default_rng(seed)
+    dirty = rng.integers(0, 4, size=(h, w)).astype(np.uint8) * (rng.random((h, w)) < 0.2)      # bytes 0..3
+    c["edited"] = dirty.copy()
+    rd, rm, re = c["data"].copy(), c["mask"].copy(), c["edited"].copy()
+    want = kn.raster_tea(*helpers.tea_args(c), rd, rm, re, val)
+    d, m, e = c["data"].copy(), c["mask"].copy(), c["edited"].copy()
+    got = nat.raster_tea(*helpers.tea_args(c), d, m, e, val)
+    assert got == want
+    assert np.array_equal(d.view(np.uint8), rd.view(np.uint8)) and np.array_equal(m, rm) and np.array_equal(e, re)
+    # coverage_fill into a dirty plane, and twice (second call writes nothing new)
+    out, ref = dirty.copy(), dirty.copy()
+    assert nat.coverage_fill(c["tri_xy"], w, h, out) == kn.coverage_fill(c["tri_xy"], w, h, ref)
+    assert np.array_equal(out, ref)
+    assert nat.coverage_fill(c["tri_xy"], w, h, out) == 0 and np.array_equal(out, ref)
+
+
 def test_tea_idempotent():                                   # SPEC.md:308
     c = helpers.random_tea_case(77, ntri=200, w=64, h=64)
     d, m, e = _plane_dev(c["data"]), _dev(c["mask"]), _dev(np.zeros((64, 64), np.uint8))
