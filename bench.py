@@ -1,45 +1,59 @@
 #!/usr/bin/env python
 """bench.py -- brush-apply + layer-op throughput at a 16384^2 atlas (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3c4|c5]
 
-One STEP = one pass of every hot-path stage over this rank's 16384 x 16384 atlas slab
-(268.4 Mtexel), the C3+C4 workload of BASELINE.json at 8 layers (``--layers 64`` gives C4); the
-stages run in the order of ``STAGES`` below (streaming stages first), listed here by kind:
+One STEP = one pass of every hot-path stage over this rank's atlas slab.  Default workload
+(``--config c3c4``): the C3+C4 workload of BASELINE.json -- a 16384 x 16384 slab (268.4 Mtexel) per
+rank, 8 uint8 layers (``--layers 64`` gives C4), the 999,698-triangle heightfield mesh -- with the
+stages, in the order of ``STAGES`` (streaming stages first):
 
+    chain      fused layer-algebra chain ((L0 u L1) n L2) \\ L3 ... over 8 uint8 layers (C3)
+    mask_op    binary union of two bare uint8 mask planes (the 3 B/texel streaming kernel)
+    area       per-layer area of all L layers in one fused pass (+ cross-rank sum when N > 1)
+    threshold  attribute-threshold selection on the float32 attribute plane pos.z (C3)
     tea        the paper's projective brush (TEA, KN:135-203) over the cached triangle-id map
     tpa        the paper's padding pass (TPA): outline texels next to the stroke
     sphere     one sphere-brush stroke over the float32x3 position map
-    batch      L sphere strokes (one per layer) batched in ONE pass over the position map
-               (the brush / selection stages tea, tpa, sphere, batch and threshold run the
-               footprint-culled kernels: a stroke reads only the tiles it can reach, the threshold
-               only tiles whose height range meets the window, the chain reads a data vector only
-               where the masks let it reach the result; ``--no-cull`` streams the whole atlas, and
-               the whole-atlas streaming kernels are ALSO timed on their own and reported under
-               ``config.stream_kernels`` -- they are the brush kernels' HBM-roofline evidence)
-    chain      fused layer-algebra chain ((L0 u L1) n L2) \\ L3 ... over 8 uint8 layers (C3)
-    mask_op    binary union of two bare uint8 mask planes (the 3 B/texel streaming kernel)
-    threshold  attribute-threshold selection on the float32 attribute plane pos.z (C3)
-    area       per-layer area of all L layers in one fused pass (+ NCCL all-reduce when N > 1)
+    batch      K sphere strokes (one per layer) batched in ONE pass over the position map
 
-metric = texel passes per second: (stages x slab texels x ranks) / step time, in Gtexel/s.
+metric = texel passes per second: (stages x slab texels x ranks) / step time, in Gtexel/s.  The run
+measures it FOUR ways and prints all of them in one JSON line:
+
+    value            the public API's default path, everything resident in HBM, CUDA events.  The brush /
+                     selection stages are footprint-culled (a stroke reads only the tiles it can reach), the
+                     chain reads a data vector only where the masks let it reach the result: these stages
+                     skip most of their SURVEY 8(d) bytes BY DESIGN, so ``value`` counts nominal texel passes.
+    value_streamed   the same steps with every stage forced to stream the whole atlas (``cull=False`` /
+                     eager chain): the byte-honest figure; its stage table is the HBM-roofline evidence.
+    e2e              the default path driven from HOST stroke records (pinned memory -> device every step)
+                     with every stage's results (edit counts, areas) read back to the host every step.
+    e2e_host_planes  the reference's own call shape: the drop-in twin ``raster_tea`` (KN:135-136) called
+                     per step with numpy planes in pageable host memory, everything else of the call
+                     (uploads, kernel, sparse write-back into the caller's planes) inside the timed region.
+
+``roofline`` is quoted for the slowest stage of the default step (algorithmic AND measured-DRAM
+fractions; DRAM bytes per launch from profiles/traffic.json, an ncu --set full capture), and
+``roofline.streamed`` for the slowest stage of the streamed step.  ``stream_kernels`` re-times each
+whole-atlas stage alone inside a CUDA graph (no host launch latency).
+
+``parity`` (untimed): after the timed loops the GPU planes are reset, P steps are run on the default path
+and again on the streamed path, and the reference-side CPU implementation (oracle/kn_port.c) runs the same
+P steps on its row sample; every layer plane, edited plane, chain / mask_op result and per-layer area of the
+sampled rows must agree (planes bit for bit, areas to 1e-10).  A mismatch makes the run exit non-zero.
+
 Inputs are far larger than the 126 MB L2 (every plane is >= 268 MB), so no explicit L2 flush is
-needed between iterations.  ``value`` is timed with CUDA events with everything resident in HBM;
-``e2e`` runs the same step through the public API from HOST stroke records (pinned memory ->
-device every step) and reads every stage's result (edit counts, areas) back to the host every step
-(one non-blocking copy into pinned memory queued behind the step's last stage, consumed by the host
-once the next step's first stage has been queued -- the GPU never waits for the host between steps).
-``config.host_plane_call`` additionally times ONE drop-in call of the KN twin ``raster_tea`` with numpy
-planes in host memory (upload + kernel + download inside the call, the way the reference's numpy
-backend is called): the PCIe cost the resident design exists to avoid, reported beside ``e2e``.
+needed between iterations.
 
 Multi-GPU (torchrun, one rank per GPU): weak scaling -- the atlas grows to 16384 x (16384*N) and
-each rank owns one 16384-row slab; the only collectives are the stroke broadcast and the area
-all-reduce (scalars).
+each rank owns one 16384-row slab; the only collectives are the stroke-table broadcast and the
+cross-rank area sum (one all-gather of 16 L bytes).  ``--config c5`` is BASELINE config 5: a
+32768^2 atlas with the 9,999,392-triangle heightfield, STRONG scaling (the rows are split over the
+ranks), stages batch (64 strokes) + area.
 
 ``--impl reference`` times the reference-side CPU implementation (oracle/kn_port.c, the C
-restatement of the reference's numpy kernels, row-parallel over all host threads) on a bounded
-row sample of the same workload.
+restatement of the reference's numpy kernels, row-parallel over all host threads, per-band triangle
+lists, fused chain / batch / areas) on a bounded row sample of the same workload.
 """
 import argparse
 import json
@@ -58,6 +72,11 @@ sys.path.insert(0, ROOT)
 # them in a few microseconds and prepares the (host-heavier) brush calls while the GPU is busy.
 STAGES = ("chain", "mask_op", "area", "threshold", "tea", "tpa", "sphere", "batch")
 CHAIN_OPS = ["union", "intersection", "difference", "union", "masking", "difference", "union"]
+BRUSH = ("tea", "tpa", "sphere", "batch", "threshold")
+CONFIGS = {
+    "c3c4": dict(atlas=16384, quads=707, layers=8, scaling="weak", stages=",".join(STAGES), batch=0),
+    "c5": dict(atlas=32768, quads=2236, layers=8, scaling="strong", stages="batch,area", batch=64),
+}
 
 
 def parse():
@@ -66,17 +85,26 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--atlas", type=int, default=16384, help="atlas width and per-rank slab height")
-    ap.add_argument("--layers", type=int, default=8)
-    ap.add_argument("--quads", type=int, default=707, help="heightfield quads per side (707 -> 999,698 tris)")
+    ap.add_argument("--config", default="c3c4", choices=sorted(CONFIGS))
+    ap.add_argument("--atlas", type=int, default=None, help="atlas width (and per-rank slab height under weak scaling)")
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--quads", type=int, default=None, help="heightfield quads per side (707 -> 999,698 tris)")
     ap.add_argument("--window", type=int, default=1024)
     ap.add_argument("--cpu-rows", type=int, default=1024, help="rows of the slab the CPU baseline processes")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / parity / host-plane legs")
     ap.add_argument("--no-cull", action="store_true",
-                    help="every stage streams the whole atlas: brush / selection stages ignore their footprint tiles, the "
-                         "chain reads every data vector")
-    ap.add_argument("--stages", default=",".join(STAGES))
-    return ap.parse_args()
+                    help="the PRIMARY loops stream the whole atlas too (value == value_streamed)")
+    ap.add_argument("--parity-steps", type=int, default=2)
+    ap.add_argument("--host-plane-reps", type=int, default=8)
+    ap.add_argument("--stages", default=None)
+    a = ap.parse_args()
+    cfg = CONFIGS[a.config]
+    for k in ("atlas", "layers", "quads", "stages"):
+        if getattr(a, k) is None:
+            setattr(a, k, cfg[k])
+    a.scaling = cfg["scaling"]
+    a.batch = cfg["batch"]
+    return a
 
 
 # ------------------------------------------------------------------------------------------------
@@ -86,33 +114,35 @@ class Workload:
     def __init__(self, args, world_size):
         from paper_2501_14807_b200 import synth
         self.A = args.atlas
-        self.width, self.height = args.atlas, args.atlas * world_size
+        self.width = args.atlas
+        strong = getattr(args, "scaling", "weak") == "strong"
+        self.height = args.atlas if strong else args.atlas * world_size
         self.L = args.layers
+        self.K = getattr(args, "batch", 0) or self.L               # strokes per batched pass
         self.mesh = synth.heightfield_mesh(args.quads, margin=0.01)   # 1% uv border: a real island outline for TPA
         self.cam = synth.default_camera(args.window, args.window, eye=(0.5, 0.5, 1.6), target=(0.5, 0.5, 0.0),
                                         fovy=40.0, near=0.2, far=5.0)
         self.tool_shape = synth.circle_shape(70)                     # the paper's mid radius (70 px)
         self.eps = 1e-4
-        rng = np.random.default_rng(synth.SEED + 7)
-        self.rng = rng
         nchain = min(8, self.L)
         self.chain_n = nchain
         self.chain_ops = CHAIN_OPS[:nchain - 1]
         z = self.mesh.vertices[:, 2]
         self.thr = (float(np.percentile(z, 40.0)), float(np.percentile(z, 60.0)))   # C3 window
-        # per-step host inputs (seeded): tool position, sphere stroke, batch strokes
+        # pre-painting (seeded): 4 strokes per layer
         self.seed_strokes, self.seed_labels = synth.sphere_strokes(self.mesh, 4 * self.L, seed=synth.SEED + 3,
                                                                    rmin_frac=0.02, rmax_frac=0.08)
 
     def step_inputs(self, i):
+        """Per-step host inputs (seeded): tool position, one sphere stroke, K batch strokes."""
         from paper_2501_14807_b200 import synth
         rng = np.random.default_rng(synth.SEED + 100 + i)
         w = self.cam.width
         tool_xy = rng.uniform(0.3 * w, 0.7 * w, size=2)
-        strokes, labels = synth.sphere_strokes(self.mesh, self.L + 1, seed=synth.SEED + 1000 + i,
+        strokes, labels = synth.sphere_strokes(self.mesh, self.K + 1, seed=synth.SEED + 1000 + i,
                                                rmin_frac=0.01, rmax_frac=0.05)
         return dict(tool_xy=tool_xy, sphere=strokes[0], sphere_value=int(labels[0]),
-                    batch=strokes[1:], batch_layers=np.arange(self.L, dtype=np.int32), batch_values=labels[1:])
+                    batch=strokes[1:], batch_layers=(np.arange(self.K) % self.L).astype(np.int32), batch_values=labels[1:])
 
     def algorithmic_bytes(self, n, stage, T, hits=0):
         """Algorithmic HBM bytes of one stage over n texels: the read stream plus,
@@ -120,9 +150,6 @@ class Workload:
         written).  tea additionally resets the 1 B/texel edited plane and reads the
         clip coordinates of every triangle once for the classification pass."""
         L = self.L
-        # tea: id stream + edited reset + classification pass; with footprint culling (default) the
-        # kernel reads far less than this, so its "frac of peak" can exceed 1 -- the stage is then
-        # bound by the float64 evaluation of the footprint, not by HBM
         base = {"tea": 4 * n + n + T * 12 * 8 + self.cam.width * self.cam.height * 4,
                 "sphere": 12 * n, "batch": 12 * n,
                 "chain": (self.chain_n + 1) * 2 * n, "mask_op": 3 * n,
@@ -185,10 +212,46 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def time_graph(fn, inner=10, reps=7, warm=2):
+    """Median ms per call of `fn` over `reps` replays of a CUDA graph holding `inner` back-to-back calls (a single
+    call between two events on an idle GPU also measures the host's 10-30 us issue latency).  Falls back to
+    eager back-to-back calls if the call cannot be captured.  Returns (ms, graphed)."""
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    graph = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(inner):
+                fn()
+        graph = g
+    except Exception:            # not capturable (host sync inside): eager back-to-back launches
+        torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps + 1):
+        a.record()
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(inner):
+                fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / inner)
+    return float(np.median(ts[1:])), graph is not None
+
+
 # ------------------------------------------------------------------------------------------------
-# CPU arm (reference / cpu_baseline): oracle C restatement, all host threads, bounded row sample
+# CPU arm (reference / cpu_baseline / parity): oracle C restatement, all host threads, bounded row sample
 
 class CpuArm:
+    """The reference algorithm at its best on the host cores: row-parallel OpenMP over all threads, triangles
+    pre-binned per row band (no re-scan of the triangle list per band), the chain, the stroke batch and the
+    per-layer areas each as ONE fused pass (oracle/kn_port.c ext_*_fused / ext_layer_chain / ext_layers_area)."""
+
     def __init__(self, wl, rows):
         from oracle import kn
         self.kn, self.wl = kn, wl
@@ -201,7 +264,7 @@ class CpuArm:
         self.tri_clip = wl.cam.clip_coords(m.vertices)[m.triangles]
         t0 = time.time()
         self.surf = kn.surface_map(self.tri_xy, m.tri_pos(), m.tri_nrm(), wl.width, wl.height,
-                                   rows=(self.row0, self.row0 + self.rows))
+                                   rows=(self.row0, self.row0 + self.rows), threads=self.threads)
         from paper_2501_14807_b200.mesh_core import window_triangles
         xy, zn = window_triangles(m, wl.cam)
         self.depth = np.ones((wl.cam.height, wl.cam.width), np.float32)
@@ -211,9 +274,10 @@ class CpuArm:
         self.n = n
         mk = lambda dt: [np.zeros((self.rows, W), dt) for _ in range(wl.L)]
         self.data, self.mask, self.edited = mk(np.uint8), mk(np.uint8), mk(np.uint8)
+        self.tea_edited = np.zeros((self.rows, W), np.uint8)      # the stroke context's EditedAreaMask
         self.out_d, self.out_m = np.zeros((self.rows, W), np.uint8), np.zeros((self.rows, W), np.uint8)
         self.outline = kn.outline((self.surf["tri_id"] >= 0).astype(np.uint8), 1, threads=self.threads)
-        self.tmp_d, self.tmp_m = np.zeros((self.rows, W), np.uint8), np.zeros((self.rows, W), np.uint8)
+        self.tmp_m = np.zeros((self.rows, W), np.uint8)
         for k in range(len(wl.seed_strokes)):                     # same pre-painting as the GPU arm
             L = k % wl.L
             kn.select_sphere(self.surf["pos"], wl.seed_strokes[k, :3], wl.seed_strokes[k, 3], self.data[L],
@@ -230,36 +294,33 @@ class CpuArm:
                 from paper_2501_14807_b200 import EditingTool, compute_tool_projection
                 tool = EditingTool(px=float(inp["tool_xy"][0]), py=float(inp["tool_xy"][1]), shape=wl.tool_shape, value=7)
                 sfx, sfy, bx, by = compute_tool_projection(wl.cam, tool).kernel_factors
-                self.edited[0][:] = 0
+                self.tea_edited[:] = 0
                 res["tea"] = kn.raster_tea_slab(self.tri_xy, self.tri_clip, float(wl.cam.width), float(wl.cam.height),
                                                 self.depth, wl.eps, sfx, sfy, bx, by, wl.tool_shape, self.data[0],
-                                                self.mask[0], self.edited[0], 7, wl.height, self.row0, th)
+                                                self.mask[0], self.tea_edited, 7, wl.height, self.row0, th)
             elif st == "tpa":
-                res["tpa"] = kn.padding(self.outline, self.edited[0], 1, self.data[0], self.mask[0], 7, threads=th)
+                res["tpa"] = kn.padding(self.outline, self.tea_edited, 1, self.data[0], self.mask[0], 7, threads=th)
             elif st == "sphere":
                 s = inp["sphere"]
                 res["sphere"] = kn.select_sphere(self.surf["pos"], s[:3], s[3], self.data[1 % wl.L], self.mask[1 % wl.L],
                                                  self.edited[1 % wl.L], inp["sphere_value"], threads=th)
             elif st == "batch":
-                res["batch"] = [kn.select_sphere(self.surf["pos"], s[:3], s[3], self.data[L], self.mask[L], self.edited[L],
-                                                 v, threads=th)
-                                for s, L, v in zip(inp["batch"], inp["batch_layers"], inp["batch_values"])]
+                res["batch"] = kn.select_sphere_batch(self.surf["pos"], inp["batch"], inp["batch_layers"], inp["batch_values"],
+                                                      self.data, self.mask, self.edited, threads=th)
             elif st == "chain":
-                cd, cm = self.data[0], self.mask[0]
-                for j in range(1, wl.chain_n):
-                    od, om = (self.out_d, self.out_m) if j % 2 else (self.tmp_d, self.tmp_m)
-                    kn.layer_op(wl.chain_ops[j - 1], cd, cm, self.data[j], self.mask[j], od, om, threads=th)
-                    cd, cm = od, om
-                res["chain"] = (cd, cm)
+                kn.layer_chain(wl.chain_ops, self.data[:wl.chain_n], self.mask[:wl.chain_n], self.out_d, self.out_m, threads=th)
             elif st == "mask_op":
                 kn.layer_op("union", None, self.mask[0], None, self.mask[1 % wl.L], None, self.tmp_m, threads=th)
             elif st == "threshold":
                 res["threshold"] = kn.select_threshold(self.surf["pos"][2], None, wl.thr[0], wl.thr[1], self.data[2 % wl.L],
                                                        self.mask[2 % wl.L], self.edited[2 % wl.L], 9, threads=th)
             elif st == "area":
-                res["area"] = [kn.layer_area(self.surf["area"], m, threads=th) for m in self.mask]
+                res["area"] = kn.layers_area(self.surf["area"], self.mask, threads=th)
             t[st] = time.perf_counter() - t0
         return t, res
+
+    DESCRIPTION = ("oracle/kn_port.c (C restatement of the reference numpy kernels): OpenMP over row bands with per-band "
+                   "triangle lists, fused chain / stroke batch / per-layer areas")
 
 
 def run_reference(args):
@@ -279,12 +340,12 @@ def run_reference(args):
             per[s] += t[s]
     el = time.perf_counter() - t0
     value = len(stages) * arm.n * args.steps / el / 1e9
-    sample = "%d of %d rows of the %dx%d slab (%.1f Mtexel), oracle/kn_port.c with OpenMP" % (
-        arm.rows, wl.A, wl.A, wl.width, arm.n / 1e6)
+    sample = "%d of %d rows of the %dx%d slab (%.1f Mtexel); %s" % (
+        arm.rows, wl.A, wl.A, wl.width, arm.n / 1e6, CpuArm.DESCRIPTION)
     print(json.dumps({
         "impl": "reference", "metric": "brush-apply + layer-op texel passes per second at 16384^2 atlas",
         "value": value, "unit": "Gtexel/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64 decisions on u8/u32/f32 planes", "data": "synthetic",
         "config": workload_config(args, wl, stages),
         "cpu_baseline": {"value": value, "unit": "Gtexel/s", "cores": arm.threads, "kind": "port", "sample": sample,
@@ -294,23 +355,143 @@ def run_reference(args):
 
 
 def workload_config(args, wl, stages):
-    return {"workload": "C3+C4: %dx%d atlas slab per GPU, %d uint8 layers, %d-triangle heightfield mesh; stages %s"
-                        % (wl.A, wl.width, wl.L, wl.mesh.num_triangles, "+".join(stages)),
+    return {"workload": "%s: %dx%d atlas%s, %d uint8 layers, %d-triangle heightfield mesh; stages %s"
+                        % ({"c3c4": "C3+C4", "c5": "C5"}[args.config], wl.height, wl.width,
+                           " (one %d-row slab per GPU)" % wl.A if args.scaling == "weak" else " row-split over the GPUs",
+                           wl.L, wl.mesh.num_triangles, "+".join(stages)),
             "atlas": [wl.height, wl.width], "layers": wl.L, "triangles": wl.mesh.num_triangles,
-            "window": [wl.cam.height, wl.cam.width], "stages": list(stages),
+            "window": [wl.cam.height, wl.cam.width], "stages": list(stages), "batch_strokes": wl.K,
             "l2": "no explicit flush: every streamed input plane (>= 268 MB) is larger than the 126 MB L2, and the "
                   "streaming stages (chain, mask_op, threshold, area: >= 0.8 GB each, 10 GB together) run between the "
                   "footprint-culled brush stages of consecutive iterations, which therefore start from a cold L2",
-            "parallelism": "row-sharded x%d" % args.gpus}
+            "parallelism": "row-sharded x%d (%s scaling)" % (args.gpus, args.scaling)}
 
 
 # ------------------------------------------------------------------------------------------------
 # GPU arm
 
+class GpuArm:
+    """All resident state of one rank and the stage calls through the public API."""
+
+    def __init__(self, args, wl, rank, world_size, dev):
+        import torch
+        import paper_2501_14807_b200 as ml
+        from paper_2501_14807_b200 import _native as nat, sharding
+        self.torch, self.ml, self.nat, self.sharding = torch, ml, nat, sharding
+        self.args, self.wl, self.rank, self.ws, self.dev = args, wl, rank, world_size, dev
+        L, W = wl.L, wl.width
+        self.row0, self.rows = sharding.shard_rows(wl.height, world_size, rank)
+        rows = self.rows
+        self.n = rows * W
+        t0 = time.time()
+        self.surf = ml.build_surface_map(wl.mesh, W, wl.height, row0=self.row0, rows=rows, device=dev)
+        self.need_stroke = any(s in args.stages.split(",") for s in ("tea", "tpa"))
+        if self.need_stroke:
+            self.depth = ml.render_depth(wl.mesh, wl.cam, device=dev)
+            self.ctx = ml.StrokeContext(wl.mesh, wl.cam, self.depth, self.surf, device=dev)
+        pool = ml.TexturePool(budget_texels=(2 * L + 8) * self.n + 1, device=dev)
+        self.layers = [ml.create_layer("L%d" % i, "uint8", W, rows, pool=pool) for i in range(L)]
+        self.out_layer = ml.create_layer("out", "uint8", W, rows, pool=pool)
+        self.edited = [torch.zeros((rows, W), dtype=torch.uint8, device=dev) for _ in range(L)]
+        self.tmp_mask = torch.zeros((rows, W), dtype=torch.uint8, device=dev)
+        # TPA outline (SPEC.md:286-289), built once per mesh; neighbour slabs supply the 1-row halo
+        cov_ext, cov_row0 = sharding.exchange_halo(self.surf.coverage.to(torch.uint8), self.row0, wl.height, 1)
+        self.outline = nat.outline_mask(cov_ext, 1, in_row0=cov_row0, out_row0=self.row0, out_rows=rows)
+        del cov_ext
+        self.batch = nat.StrokeBatch([l.data for l in self.layers], [l.mask for l in self.layers], self.edited, dev,
+                                     capacity=wl.K)
+        self.attr = self.surf.pos[2]
+        self.attr_tiles = nat.attr_tiles(self.attr)     # per-tile height ranges for the culled threshold selection
+        self.tool_shape_dev = nat._as_dev_bytes(wl.tool_shape, dev)
+        self.area_reduce = sharding.AreaReducer(L, dev)
+        self.T = wl.mesh.num_triangles
+        self.seed()
+        torch.cuda.synchronize()
+        self.setup_s = time.time() - t0
+        # result slots of one step (8-byte elements): tea (edited, fragments) | tpa | sphere | threshold | batch [L] |
+        # area sums [L] (float64 bit patterns) | area counts [L]
+        self.slot = {"tea": (0, 2), "tpa": (2, 3), "sphere": (3, 4), "threshold": (4, 5), "batch": (5, 5 + L),
+                     "area": (5 + L, 5 + 3 * L)}
+        self.nslots = 5 + 3 * L
+
+    def seed(self):
+        """(Re)create the pre-painted state: empty planes, then 4 seeded sphere strokes per layer."""
+        ml, wl = self.ml, self.wl
+        for l in self.layers + [self.out_layer]:
+            l.data.zero_()
+            l.mask.zero_()
+        for e in self.edited:
+            e.zero_()
+        self.tmp_mask.zero_()
+        if self.need_stroke:
+            self.ctx.edited.zero_()
+            self.ctx.edited_fully_dirty = True          # the next culled stroke resets its tile buffers
+        for k in range(len(wl.seed_strokes)):
+            ml.select_sphere(self.surf, self.layers[k % wl.L], wl.seed_strokes[k, :3], wl.seed_strokes[k, 3],
+                             wl.seed_labels[k], edited=self.edited[k % wl.L])
+
+    def culled(self, cull):
+        return cull and self.surf.tiles is not None
+
+    def launches(self, cull):
+        c = self.culled(cull)
+        return {"tea": 3, "tpa": 1, "sphere": 2 if c else 1, "batch": 2 if c else 1, "chain": 1, "mask_op": 1,
+                "threshold": 2 if (c and self.attr_tiles is not None) else 1, "area": -(-self.wl.L // 8)}
+
+    def make_tool(self, inp):
+        return self.ml.EditingTool(px=float(inp["tool_xy"][0]), py=float(inp["tool_xy"][1]), shape=self.tool_shape_dev, value=7)
+
+    def stage(self, st, inp, tool, row, cull, upload_batch=False):
+        """Queue one stage through the public API.  Its counters accumulate into the (zeroed) slots of `row`, an
+        int64 device vector of `nslots` elements; nothing here synchronises or allocates."""
+        ml, nat, wl, L = self.ml, self.nat, self.wl, self.wl.L
+        layers, edited = self.layers, self.edited
+        a, b = self.slot.get(st, (0, 0))
+        if st == "tea":
+            ml.apply_stroke(self.ctx, tool, layers[0], eps=wl.eps, cull=cull, counts=row[a:b])
+        elif st == "tpa":
+            # padding of the stroke just applied (the paper times TEA + TPA per edit, PAPER.md:241); with
+            # several ranks the 1-row halo of the edited plane travels point-to-point first
+            tiles = self.ctx.stroke_tiles if cull else None
+            if self.ws > 1:
+                ml.editing.pad_slab(self.outline, self.ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, row[a:b],
+                                    row0=self.row0, height=wl.height, tiles=tiles)
+            else:
+                nat.apply_padding(self.outline, self.ctx.edited, 1, layers[0].data, layers[0].mask, tool.value,
+                                  counts=row[a:b], tiles=tiles)
+        elif st == "sphere":
+            s = inp["sphere"]
+            ml.select_sphere(self.surf, layers[1 % L], s[:3], s[3], inp["sphere_value"], edited=edited[1 % L], cull=cull,
+                             counts=row[a:b])
+        elif st == "batch":
+            if upload_batch:
+                # this step's stroke table: pinned host memory -> device on rank 0, one device broadcast to the others
+                if self.rank == 0:
+                    self.batch.upload(inp["batch"], inp["batch_layers"], inp["batch_values"], fill=self.ws > 1)
+                self.sharding.broadcast_batch(self.batch)
+            self.batch.counts = row[a:b]
+            ml.select_sphere_batch(self.surf, self.batch, cull=cull)
+        elif st == "chain":
+            ml.layer_chain(layers[:wl.chain_n], wl.chain_ops, self.out_layer, lazy=cull)
+        elif st == "mask_op":
+            nat.layer_op("union", None, layers[0].mask, None, layers[1 % L].mask, None, self.tmp_mask)
+        elif st == "threshold":
+            ml.select_threshold(self.attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L],
+                                tiles=self.attr_tiles if cull else None, counts=row[a:b])
+        elif st == "area":
+            nat.layer_area(self.surf.area, [l.mask for l in layers], sums=row[a:a + L].view(self.torch.float64),
+                           counts=row[a + L:b])
+            self.area_reduce(row[a:b])
+
+    def hits_of(self, st, row_host):
+        a, b = self.slot[st]
+        return float(row_host[a]) if st != "batch" else float(row_host[a:b].sum())
+
+
 def run_ours(args):
     import torch
     import paper_2501_14807_b200 as ml
-    from paper_2501_14807_b200 import _native as nat, sharding
+    from paper_2501_14807_b200 import _native as nat
 
     rank = int(os.environ.get("RANK", "0"))
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
@@ -331,91 +512,9 @@ def run_ours(args):
             dist.init_process_group(backend)
     stages = [s for s in args.stages.split(",") if s]
     wl = Workload(args, world_size)
-    A, W, L = wl.A, wl.width, wl.L
-    row0, rows = sharding.shard_rows(wl.height, world_size, rank)
-    n = rows * W
-
-    # ---- setup (untimed): surface map, depth, layers, pre-painting
-    t0 = time.time()
-    surf = ml.build_surface_map(wl.mesh, W, wl.height, row0=row0, rows=rows, device=dev)
-    depth = ml.render_depth(wl.mesh, wl.cam, device=dev)
-    ctx = ml.StrokeContext(wl.mesh, wl.cam, depth, surf, device=dev)
-    pool = ml.TexturePool(budget_texels=(2 * L + 8) * n + 1, device=dev)
-    layers = [ml.create_layer("L%d" % i, "uint8", W, rows, pool=pool) for i in range(L)]
-    out_layer = ml.create_layer("out", "uint8", W, rows, pool=pool)
-    edited = [torch.zeros((rows, W), dtype=torch.uint8, device=dev) for _ in range(L)]
-    tmp_mask = torch.zeros((rows, W), dtype=torch.uint8, device=dev)
-    # TPA outline, built once per mesh; neighbour slabs supply the 1-row halo
-    cov_ext, cov_row0 = sharding.exchange_halo(surf.coverage.to(torch.uint8), row0, wl.height, 1)
-    outline = nat.outline_mask(cov_ext, 1, in_row0=cov_row0, out_row0=row0, out_rows=rows)
-    batch = nat.StrokeBatch([l.data for l in layers], [l.mask for l in layers], edited, dev)
-    for k in range(len(wl.seed_strokes)):
-        ml.select_sphere(surf, layers[k % L], wl.seed_strokes[k, :3], wl.seed_strokes[k, 3], wl.seed_labels[k],
-                         edited=edited[k % L])
-    attr = surf.pos[2]
-    attr_tiles = nat.attr_tiles(attr)              # per-tile height ranges for the culled threshold selection
-    torch.cuda.synchronize()
-    setup_s = time.time() - t0
-    T = wl.mesh.num_triangles
-    area_sums = torch.zeros(L, dtype=torch.float64, device=dev)
-    area_counts = torch.zeros(L, dtype=torch.int64, device=dev)
-    counts2 = torch.zeros(2, dtype=torch.int64, device=dev)
-    counts1 = torch.zeros(1, dtype=torch.int64, device=dev)
-    culled = not args.no_cull and surf.tiles is not None
-    launches = {"tea": 3, "tpa": 1, "sphere": 2 if culled else 1, "batch": 2 if culled else 1, "chain": 1, "mask_op": 1,
-                "threshold": 2 if (culled and attr_tiles is not None) else 1, "area": -(-L // 8)}
-
-    def stage_call(st, inp, tool, mode, cull=not args.no_cull):
-        """Run one stage through the public API and return its result as DEVICE tensors (nothing
-        synchronises here).  mode "resident": stroke records were uploaded before the timed region;
-        "e2e": this step's records come from the host now (pinned staging -> device)."""
-        out = []
-        if st == "tea":
-            # --no-cull streams the whole id map instead of the stroke's footprint tiles
-            r = ml.apply_stroke(ctx, tool, layers[0], eps=wl.eps, cull=cull)
-            out = [r._counts]
-        elif st == "tpa":
-            # padding of the stroke just applied (the paper times TEA + TPA per edit, PAPER.md:241); with
-            # several ranks the 1-row halo of the edited plane travels point-to-point first
-            counts1.zero_()
-            if world_size > 1:
-                # interior rows: footprint-culled tile pass; the border row next to each neighbour: streaming pass
-                # over the exchanged halo row (16 KB point-to-point per neighbour)
-                ml.editing.pad_slab(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts1,
-                                    row0=row0, height=wl.height, tiles=ctx.stroke_tiles if cull else None)
-            else:
-                nat.apply_padding(outline, ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, counts=counts1,
-                                  tiles=ctx.stroke_tiles if cull else None)
-            out = [counts1.clone()]
-        elif st == "sphere":
-            s = inp["sphere"]
-            out = [ml.select_sphere(surf, layers[1 % L], s[:3], s[3], inp["sphere_value"], edited=edited[1 % L],
-                                    cull=cull)._counts]
-        elif st == "batch":
-            if mode == "e2e":
-                s, lo, v = sharding.broadcast_strokes(inp["batch"], inp["batch_layers"], inp["batch_values"].astype(np.uint32), dev)
-                batch.upload(s, lo, v.astype(np.uint8))
-            batch.counts.zero_()
-            out = [ml.select_sphere_batch(surf, batch, cull=cull).clone()]
-        elif st == "chain":
-            ml.layer_chain(layers[:wl.chain_n], wl.chain_ops, out_layer, lazy=cull)
-        elif st == "mask_op":
-            nat.layer_op("union", None, layers[0].mask, None, layers[1 % L].mask, None, tmp_mask)
-        elif st == "threshold":
-            out = [ml.select_threshold(attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L],
-                                       tiles=attr_tiles if cull else None)._counts]
-        elif st == "area":
-            area_sums.zero_()
-            area_counts.zero_()
-            nat.layer_area(surf.area, [l.mask for l in layers], sums=area_sums, counts=area_counts)
-            sharding.allreduce_areas(area_sums, area_counts)
-            out = [area_sums, area_counts]
-        return out
-
-    def make_tool(inp):
-        return ml.EditingTool(px=float(inp["tool_xy"][0]), py=float(inp["tool_xy"][1]), shape=tool_shape_dev, value=7)
-
-    tool_shape_dev = nat._as_dev_bytes(wl.tool_shape, dev)
+    arm = GpuArm(args, wl, rank, world_size, dev)
+    L, n, T = wl.L, arm.n, arm.T
+    primary_cull = not args.no_cull
 
     def barrier():
         if world_size > 1:
@@ -431,9 +530,11 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- resident loop (value): inputs uploaded before the timed region, no read-back inside it
-    inputs = [wl.step_inputs(i) for i in range(args.warmup + args.steps)]
-    batch.upload(inputs[0]["batch"], inputs[0]["batch_layers"], inputs[0]["batch_values"])
+    total_steps = args.warmup + args.steps
+    inputs = [wl.step_inputs(i) for i in range(total_steps)]
+    # ONE counter block per loop, zeroed once: row k holds every stage's results of step k
+    slots = torch.zeros((total_steps, arm.nslots), dtype=torch.int64, device=dev)
+
     # clock sampler: started before the warm-up so that nvidia-smi is already delivering samples when the
     # timed region begins (its start-up alone can outlast a short timed region)
     stop, samples, windows = threading.Event(), [], []
@@ -442,77 +543,81 @@ def run_ours(args):
     t_wait = time.time()
     while not samples and time.time() - t_wait < 5.0 and th.is_alive():
         time.sleep(0.02)
-    for i in range(args.warmup):
-        for st in stages:
-            stage_call(st, inputs[i], make_tool(inputs[i]), "resident")
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
-    barrier()
-    t_begin = time.time()
-    for k in range(args.steps):
-        inp = inputs[args.warmup + k]
-        tool = make_tool(inp)
-        ev[k][0].record()
-        for j, st in enumerate(stages):
-            stage_call(st, inp, tool, "resident")
-            ev[k][j + 1].record()
-    barrier()
-    windows.append((t_begin, time.time()))
-    total_ms = max_over_ranks(ev[0][0].elapsed_time(ev[-1][-1]))
-    stage_ms = {st: sum(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)) / args.steps
-                for j, st in enumerate(stages)}
 
-    # ---- e2e loop: the same step through the public API, but every step (1) takes its stroke
-    # records from HOST memory (pinned staging buffers -> device) and (2) reads all stage results
-    # (edit counts, padded count, per-layer areas and texel counts) back to the host in one copy
-    pinned = torch.empty(16, dtype=torch.float64).pin_memory()
+    def resident_loop(cull):
+        """W warm-up + K timed steps, everything resident, no read-back.  Returns (total ms, per-stage ms, host rows)."""
+        slots.zero_()
+        if "batch" in stages:
+            arm.batch.upload(inputs[0]["batch"], inputs[0]["batch_layers"], inputs[0]["batch_values"], fill=world_size > 1)
+            arm.sharding.broadcast_batch(arm.batch)
+        for i in range(args.warmup):
+            tool = arm.make_tool(inputs[i])
+            for st in stages:
+                arm.stage(st, inputs[i], tool, slots[i], cull)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(stages) + 1)] for _ in range(args.steps)]
+        barrier()
+        t_begin = time.time()
+        for k in range(args.steps):
+            inp = inputs[args.warmup + k]
+            tool = arm.make_tool(inp)
+            row = slots[args.warmup + k]
+            ev[k][0].record()
+            for j, st in enumerate(stages):
+                arm.stage(st, inp, tool, row, cull)
+                ev[k][j + 1].record()
+        barrier()
+        windows.append((t_begin, time.time()))
+        total_ms = max_over_ranks(ev[0][0].elapsed_time(ev[-1][-1]))
+        stage_ms = {st: sum(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps)) / args.steps
+                    for j, st in enumerate(stages)}
+        return total_ms, stage_ms, slots[args.warmup:].cpu().numpy()
+
+    # ---- value: the default path;  value_streamed: every stage streams the whole atlas
+    total_ms, stage_ms, _ = resident_loop(primary_cull)
+    if primary_cull:
+        total_ms_s, stage_ms_s, _ = resident_loop(False)
+    else:
+        total_ms_s, stage_ms_s = total_ms, stage_ms
+
+    # ---- e2e loop: the default path, but every step (1) takes its stroke records from HOST memory (pinned
+    # staging -> device) and (2) reads the step's result row (edit counts, padded count, per-layer areas and
+    # texel counts) back to the host: one non-blocking copy into pinned memory queued behind the step's last
+    # stage, consumed by the host after the FIRST stage of the next step has been queued (the GPU never waits
+    # for the host between steps; the last step's row is consumed before the closing event).
+    pinned_in = torch.empty(16, dtype=torch.float64).pin_memory()
     rec_dev = torch.empty(16, dtype=torch.float64, device=dev)
-
-    def bits64(t):
-        t = t.reshape(-1)
-        if t.dtype == torch.int64:
-            return t
-        return t.view(torch.int64) if t.dtype == torch.float64 else t.to(torch.int64)
-
-    out_pinned = [None, None]
-    pending = []                        # (event, bytes) of read-backs queued but not yet consumed by the host
+    out_pinned = [torch.empty(arm.nslots, dtype=torch.int64).pin_memory() for _ in range(2)]
+    pending = []
 
     def consume():
-        n = 0
+        got = 0
         while pending:
             e, nbytes = pending.pop(0)
             e.synchronize()             # the host now holds that step's results in pinned memory
-            n += nbytes
-        return n
-
-    def e2e_step(inp, slot):
-        """One step from host stroke records.  The read-back of the step's results is queued right behind its
-        last stage (non-blocking copy into pinned memory) and consumed by the host after the FIRST stage of the
-        next step has been queued, so the GPU goes from one step into the next without waiting for the host;
-        every step's inputs still come from pinned host memory and every step's results are read by the host
-        inside the timed region (the last step's before the closing event)."""
-        rec = np.concatenate([inp["tool_xy"], inp["sphere"]])
-        pinned[:rec.size].copy_(torch.from_numpy(rec))
-        rec_dev[:rec.size].copy_(pinned[:rec.size], non_blocking=True)   # this step's scalar stroke record
-        tool = make_tool(inp)
-        res, got = [], 0
-        for j, st in enumerate(stages):
-            res += stage_call(st, inp, tool, "e2e")
-            if j == 0:
-                got += consume()        # results of the previous step
-        if res:
-            # ONE device->host read of every stage result: the 8-byte elements (int64 counts, float64 areas) are
-            # concatenated bit for bit (a float64 viewed as int64 costs no kernel): one cat + one copy
-            dev_out = torch.cat([bits64(t) for t in res])
-            if out_pinned[slot] is None or out_pinned[slot].numel() != dev_out.numel():
-                out_pinned[slot] = torch.empty(dev_out.numel(), dtype=torch.int64).pin_memory()
-            out_pinned[slot].copy_(dev_out, non_blocking=True)
-            e = torch.cuda.Event()
-            e.record()
-            pending.append((e, 8 * dev_out.numel()))
+            got += nbytes
         return got
 
+    def e2e_step(idx, slot):
+        inp = inputs[idx]
+        rec = np.concatenate([inp["tool_xy"], inp["sphere"]])
+        pinned_in[:rec.size].copy_(torch.from_numpy(rec))
+        rec_dev[:rec.size].copy_(pinned_in[:rec.size], non_blocking=True)   # this step's scalar stroke record
+        tool = arm.make_tool(inp)
+        row = slots[idx]
+        got = 0
+        for j, st in enumerate(stages):
+            arm.stage(st, inp, tool, row, primary_cull, upload_batch=True)
+            if j == 0:
+                got += consume()        # results of the previous step
+        out_pinned[slot].copy_(row, non_blocking=True)
+        e = torch.cuda.Event()
+        e.record()
+        pending.append((e, 8 * arm.nslots))
+        return got
+
+    slots.zero_()
     for i in range(args.warmup):
-        e2e_step(inputs[i], i & 1)
+        e2e_step(i, i & 1)
     consume()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -520,169 +625,274 @@ def run_ours(args):
     e0.record()
     d2h = 0
     for k in range(args.steps):
-        d2h += e2e_step(inputs[args.warmup + k], k & 1)
+        d2h += e2e_step(args.warmup + k, k & 1)
     d2h += consume()
     e1.record()
     barrier()
     windows.append((t_begin, time.time()))
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    h2d = 8 * 6 + 64 + (wl.K * nat.StrokeBatch.RECORD_BYTES if "batch" in stages else 0)   # stroke records + 4x4 matrix
+
+    # ---- e2e_host_planes: the reference's call shape (KN:135-136) per step -- numpy planes in pageable host
+    # memory, the drop-in twin uploads the triangle arrays, runs the direct kernel and writes the stroke's
+    # texels back into the caller's planes, all inside the timed region
+    host_planes = None
+    if rank == 0 and world_size == 1 and not args.no_cpu and "tea" in stages and args.host_plane_reps > 0:
+        W, rows = wl.width, arm.rows
+        tri_xy = np.ascontiguousarray(wl.mesh.tri_uv_texels(W, wl.height))
+        clip = np.ascontiguousarray(wl.cam.clip_coords(wl.mesh.vertices)[wl.mesh.triangles])
+        depth_np = arm.depth.plane.cpu().numpy()
+        shape_np = np.ascontiguousarray(wl.tool_shape).astype(np.uint8)
+        planes = [np.zeros((rows, W), np.uint8) for _ in range(3)]
+        t_calls, last = [], None
+        for r in range(args.host_plane_reps + 1):
+            inp = inputs[args.warmup + (r % args.steps)]
+            tool = arm.make_tool(inp)
+            sfx, sfy, bx, by = ml.compute_tool_projection(wl.cam, tool).kernel_factors
+            planes[2][:] = 0                                            # EditedAreaMask reset, host side
+            t0 = time.perf_counter()
+            last = nat.raster_tea(tri_xy, clip, float(wl.cam.width), float(wl.cam.height), depth_np, wl.eps, sfx, sfy,
+                                  bx, by, shape_np, planes[0], planes[1], planes[2], 7)
+            t_calls.append((time.perf_counter() - t0) * 1e3)
+        windows.append((time.time() - sum(t_calls) * 1e-3, time.time()))
+        # same stroke through the resident engine: counts must agree
+        chk = torch.zeros(2, dtype=torch.int64, device=dev)
+        arm.ctx.edited.zero_()
+        arm.ctx.edited_fully_dirty = True
+        lay = arm.out_layer
+        lay.data.zero_(); lay.mask.zero_()
+        ml.apply_stroke(arm.ctx, arm.make_tool(inputs[args.warmup + ((args.host_plane_reps) % args.steps)]), lay,
+                        eps=wl.eps, counts=chk)
+        same = (int(chk[0].item()) == int(last[0]) and
+                np.array_equal(lay.mask.cpu().numpy().view(np.uint8) != 0, planes[2] != 0))
+        ms = float(np.median(t_calls[1:]))
+        naive = tri_xy.nbytes + clip.nbytes + depth_np.nbytes + shape_np.nbytes + 6 * planes[0].nbytes
+        host_planes = {"op": "raster_tea (KN:135-136) with numpy planes in pageable host memory, per call: pipelined upload "
+                             "of the triangle arrays + direct per-triangle kernel + sparse write-back of the stroke's texels",
+                       "ms_per_call": round(ms, 3), "first_call_ms": round(t_calls[0], 2), "calls": args.host_plane_reps,
+                       "value": n / (ms * 1e-3) / 1e9, "unit": "Gtexel/s",
+                       "h2d_bytes_per_call": int(tri_xy.nbytes + clip.nbytes + depth_np.nbytes + shape_np.nbytes),
+                       "d2h_bytes_per_call": "O(hit texels / 8): the written SET as a bitmap or word list",
+                       "plane_round_trip_bytes_avoided": int(naive), "edited": int(last[0]), "fragments": int(last[1]),
+                       "equal_to_resident_stroke": bool(same)}
+        del planes, tri_xy, clip
     stop.set()
     th.join()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-    h2d = 8 * 6 + 64 + (wl.L * (32 + 4 + 4) if "batch" in stages else 0)   # stroke records + 4x4 matrix
 
     # ---- hit census (untimed): mean number of texels each brush stage writes per step, for the
     # hit-write term of the algorithmic bytes.  Edited planes are cleared first so that the
     # kernels' "newly edited" counters equal the hit counts.
     hits = {s: 0.0 for s in stages}
     ncen = min(args.steps, 10)
+    slots.zero_()
     for k in range(ncen):
         inp = inputs[args.warmup + k]
-        tool = make_tool(inp)
-        for e in edited:
+        tool = arm.make_tool(inp)
+        for e in arm.edited:
             e.zero_()
         for st in stages:
-            r = stage_call(st, inp, tool, "resident")
-            if st in ("tea", "tpa", "sphere", "batch", "threshold"):
-                hits[st] += float(r[0].reshape(-1)[0].item() if st != "batch" else r[0].sum().item()) / ncen
-
-    # ---- whole-atlas streaming forms of the brush stages, timed on their own (cull=False): the
-    # HBM-roofline evidence for the brush kernels (SURVEY.md 8(d) algorithmic bytes / time)
-    stream_info = {}
-    if not args.no_cull:
-        reps = max(5, min(20, args.steps))
-        for st in [s for s in ("tea", "tpa", "sphere", "batch", "threshold", "chain") if s in stages]:
-            ms_acc = 0.0
-            for k in range(reps + 2):
-                inp = inputs[args.warmup + (k % args.steps)]
-                tool = make_tool(inp)
-                if st == "tpa":
-                    stage_call("tea", inp, tool, "resident", cull=False)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                stage_call(st, inp, tool, "resident", cull=False)
-                b.record()
-                torch.cuda.synchronize()
-                if k >= 2:
-                    ms_acc += a.elapsed_time(b)
-            stream_info[st] = ms_acc / reps
-        ctx.edited.zero_()
-
-    # ---- the drop-in call with HOST planes (untimed part of the run, reported under config.host_plane_call):
-    # the KN twin `raster_tea` (KN:135) called the way the reference calls it, numpy planes in host memory,
-    # uploaded, edited and downloaded inside the call.  This is the PCIe cost the resident design avoids.
-    host_call = None
-    if rank == 0 and world_size == 1 and not args.no_cpu and "tea" in stages:
-        inp = inputs[args.warmup]
-        tool = make_tool(inp)
-        sfx, sfy, bx, by = ml.compute_tool_projection(wl.cam, tool).kernel_factors
-        tri_xy = np.ascontiguousarray(wl.mesh.tri_uv_texels(W, wl.height))
-        clip = np.ascontiguousarray(wl.cam.clip_coords(wl.mesh.vertices)[wl.mesh.triangles])
-        depth_np = depth.plane.cpu().numpy()
-        shape_np = np.ascontiguousarray(wl.tool_shape).astype(np.uint8)
-        planes = [np.zeros((rows, W), np.uint8) for _ in range(3)]
-        ctx.edited.zero_()
-        want = int(stage_call("tea", inp, tool, "resident")[0].reshape(-1)[0].item())
-        ctx.edited.zero_()
-        t_host = []
-        got = None
-        for _ in range(2):
-            planes[2][:] = 0
-            t0 = time.perf_counter()
-            got = nat.raster_tea(tri_xy, clip, float(wl.cam.width), float(wl.cam.height), depth_np, wl.eps, sfx, sfy,
-                                 bx, by, shape_np, planes[0], planes[1], planes[2], 7)
-            t_host.append((time.perf_counter() - t0) * 1e3)
-        moved = tri_xy.nbytes + clip.nbytes + depth_np.nbytes + shape_np.nbytes + 3 * planes[0].nbytes
-        host_call = {"op": "raster_tea (KN:135-136) with numpy planes: upload + direct per-triangle kernel + download",
-                     "ms": round(min(t_host), 2), "gtexel_s": round(n / (min(t_host) * 1e-3) / 1e9, 2),
-                     "h2d_bytes": moved, "d2h_bytes": 3 * planes[0].nbytes,
-                     "edited": int(got[0]), "equal_to_resident_stroke": int(got[0]) == want}
-        del planes, tri_xy, clip
-
-    texel_passes = len(stages) * n * world_size
-    value = texel_passes * args.steps / (total_ms * 1e-3) / 1e9
-    e2e_value = texel_passes * args.steps / (e2e_ms * 1e-3) / 1e9
-    peak, peak_src = measured_peak()
-    stage_info = {}
+            arm.stage(st, inp, tool, slots[k], primary_cull)
+    census = slots[:ncen].cpu().numpy()
     for st in stages:
-        b = wl.algorithmic_bytes(n, st, T, hits[st])
-        gbs = b / (stage_ms[st] * 1e-3) / 1e9
-        stage_info[st] = {"ms": round(stage_ms[st], 4), "gtexel_s": round(n / (stage_ms[st] * 1e-3) / 1e9, 2),
-                          "alg_bytes": b, "gb_s": round(gbs, 1), "frac_of_peak": round(gbs / peak, 4),
-                          "hits_per_step": int(hits[st]), "launches": launches[st]}
-        if st in ("tea", "tpa", "sphere", "batch", "threshold"):
-            stage_info[st]["footprint_culled"] = not args.no_cull
-        if st == "chain":
-            # (N+1)*2 B/texel is an upper bound: the chain kernel fetches a data vector only where the masks
-            # say it can contribute, so its "frac_of_peak" can exceed 1 (bytes that were never read)
-            stage_info[st]["lazy_data_reads"] = not args.no_cull
-    peak_now = peak
-    stream_kernels = {st: {"ms": round(ms, 4), "gb_s": round(wl.algorithmic_bytes(n, st, T, hits[st]) / (ms * 1e-3) / 1e9, 1),
-                           "frac_of_peak": round(wl.algorithmic_bytes(n, st, T, hits[st]) / (ms * 1e-3) / 1e9 / peak_now, 4)}
-                      for st, ms in stream_info.items()}
-    # The roofline object is quoted for the slowest stage whose SURVEY 8(d) bytes are really moved.  Footprint-culled
-    # brush stages and the lazy chain skip most of those bytes by design (their "frac_of_peak" above exceeds 1), so
-    # they are not roofline evidence; their whole-atlas forms are, under config.stream_kernels / --no-cull.
-    skipping = set() if args.no_cull else {"tea", "tpa", "sphere", "batch", "threshold", "chain"}
-    full = [s for s in stages if s not in skipping] or list(stages)
-    dom = max(full, key=lambda s: stage_ms[s])
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            tj = json.load(f)
-        # whole-atlas (--no-cull) runs launch the streaming forms of the kernels: "<stage>_stream" entries
-        traffic = tj.get(dom + "_stream", tj.get(dom)) if args.no_cull else tj.get(dom)
-    # the dominant stage's main kernel: stage bytes / stage time (for tea the stage is 3 kernels
-    # + the edited-plane reset; its bytes include all of them)
-    dom_b = wl.algorithmic_bytes(n, dom, T, hits[dom])
-    dom_ms = stage_ms[dom]
+        if st in BRUSH:
+            hits[st] = float(np.mean([arm.hits_of(st, census[k]) for k in range(ncen)]))
 
-    cpu = None
+    # ---- whole-atlas streaming form of every stage, alone inside a CUDA graph (no host launch latency)
+    stream_kernels = {}
+    peak, peak_src = measured_peak()
+    if rank == 0 and world_size == 1:
+        inp = inputs[args.warmup]
+        tool = arm.make_tool(inp)
+        scratch_row = torch.zeros(arm.nslots, dtype=torch.int64, device=dev)
+        if "tpa" in stages:
+            arm.stage("tea", inp, tool, scratch_row, False)              # marks for the padding pass
+        for st in stages:
+            ms, graphed = time_graph(lambda: arm.stage(st, inp, tool, scratch_row, False), inner=10, reps=5)
+            b = wl.algorithmic_bytes(n, st, T, hits[st])
+            stream_kernels[st] = {"ms": round(ms, 4), "gb_s": round(b / ms / 1e6, 1), "frac_of_peak": round(b / ms / 1e6 / peak, 4),
+                                  "timed": "cuda graph of 10 calls" if graphed else "eager back-to-back calls"}
+
+    # ---- parity (untimed) + cpu_baseline
+    parity, cpu = None, None
     if rank == 0 and world_size == 1 and not args.no_cpu:
-        arm = CpuArm(wl, args.cpu_rows)
-        arm.step(0, stages)
+        cpu_arm = CpuArm(wl, args.cpu_rows)
+        parity = parity_check(arm, cpu_arm, wl, stages, args.parity_steps)
+        cpu_arm.step(0, stages)
         reps, el, per = 0, 0.0, {s: 0.0 for s in stages}
         while reps < 3 or (el < 10.0 and reps < 20):
-            t, _ = arm.step(1 + reps, stages)
+            t, _ = cpu_arm.step(1 + reps, stages)
             for s in stages:
                 per[s] += t[s]
             el += sum(t.values())
             reps += 1
-        cpu = {"value": len(stages) * arm.n * reps / el / 1e9, "unit": "Gtexel/s", "cores": arm.threads, "kind": "port",
-               "sample": "%d of %d rows of the slab (%.1f Mtexel) x %d reps, oracle/kn_port.c (C restatement of the "
-                         "reference numpy kernels) with OpenMP over rows" % (arm.rows, A, arm.n / 1e6, reps),
-               "stage_ms": {s: round(per[s] / reps * 1e3, 3) for s in stages}}
+        cpu = {"value": len(stages) * cpu_arm.n * reps / el / 1e9, "unit": "Gtexel/s", "cores": cpu_arm.threads, "kind": "port",
+               "sample": "%d of %d rows of the slab (%.1f Mtexel) x %d reps; %s" % (cpu_arm.rows, wl.A, cpu_arm.n / 1e6, reps,
+                                                                                      CpuArm.DESCRIPTION),
+               "stage_ms": {s: round(per[s] / reps * 1e3, 3) for s in stages}, "threads": cpu_arm.threads}
+
+    # ---- report
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f)
+
+    def stage_table(ms_of, cull):
+        """Per stage: time, algorithmic GB/s and fraction; DRAM bytes per step (ncu capture of the stage's kernels,
+        per launch x launches) and the fraction of the peak they amount to in the measured time."""
+        out = {}
+        launches = arm.launches(cull)
+        for st in stages:
+            b = wl.algorithmic_bytes(n, st, T, hits[st])
+            ms = ms_of[st]
+            row = {"ms": round(ms, 4), "gtexel_s": round(n / (ms * 1e-3) / 1e9, 2), "alg_bytes": b,
+                   "gb_s": round(b / ms / 1e6, 1), "frac_of_peak": round(b / ms / 1e6 / peak, 4),
+                   "hits_per_step": int(hits[st]), "launches": launches[st]}
+            key = st if arm.culled(cull) or st in ("mask_op", "area") else st + "_stream"
+            if st == "chain":
+                key = "chain" if cull else "chain_stream"
+            tb = traffic.get(key)
+            if tb is not None:
+                # traffic.json holds bytes per launch of the stage's dominant kernel at 16384^2 x 8 layers
+                per_step = tb * (launches[st] if st == "area" else 1)
+                row["dram_bytes"] = per_step
+                row["dram_frac_of_peak"] = round(per_step / ms / 1e6 / peak, 4)
+            if st in BRUSH:
+                row["footprint_culled"] = bool(arm.culled(cull))
+            if st == "chain":
+                row["lazy_data_reads"] = bool(cull)
+            out[st] = row
+        return out
+
+    texel_passes = len(stages) * n * world_size
+    value = texel_passes * args.steps / (total_ms * 1e-3) / 1e9
+    value_s = texel_passes * args.steps / (total_ms_s * 1e-3) / 1e9
+    e2e_value = texel_passes * args.steps / (e2e_ms * 1e-3) / 1e9
+    tab, tab_s = stage_table(stage_ms, primary_cull), stage_table(stage_ms_s, False)
+
+    def roof(tab_x, ms_x, note):
+        dom = max(stages, key=lambda s: ms_x[s])
+        r = tab_x[dom]
+        out = {"bound": "hbm", "kernel": dom, "achieved": r["alg_bytes"] / ms_x[dom] / 1e6, "peak": peak, "unit": "GB/s",
+               "frac": r["alg_bytes"] / ms_x[dom] / 1e6 / peak, "traffic": r.get("dram_bytes"),
+               "dram_achieved": None if "dram_bytes" not in r else r["dram_bytes"] / ms_x[dom] / 1e6,
+               "dram_frac": r.get("dram_frac_of_peak"), "stage_ms": round(ms_x[dom], 4),
+               "frac_of_8TBs_spec": r["alg_bytes"] / ms_x[dom] / 1e6 / 8000.0, "basis": note}
+        return out
 
     if rank == 0:
         cfg = workload_config(args, wl, stages)
-        cfg["stage_results"] = stage_info
-        cfg["setup_s"] = round(setup_s, 2)
-        cfg["surface_map"] = {"covered": surf.covered, "overlap": surf.overlap}
-        cfg["footprint_culling"] = not args.no_cull
+        cfg["stage_results"] = tab
+        cfg["stage_results_streamed"] = tab_s
         cfg["stream_kernels"] = stream_kernels
-        if host_call:
-            cfg["host_plane_call"] = host_call
-        print(json.dumps({
+        cfg["setup_s"] = round(arm.setup_s, 2)
+        cfg["surface_map"] = {"covered": arm.surf.covered, "overlap": arm.surf.overlap}
+        cfg["footprint_culling"] = bool(arm.culled(primary_cull))
+        roofline = roof(tab, stage_ms, "slowest stage of the default step: SURVEY 8(d) algorithmic bytes / CUDA-event time "
+                                       "(frac); dram_frac = ncu-measured DRAM bytes of the stage's kernels / the same time. "
+                                       "A stage that skips bytes by design (culled brushes, lazy chain, sparse-mask area) shows "
+                                       "frac > dram_frac; roofline.streamed is the byte-honest twin")
+        roofline["peak_source"] = peak_src
+        roofline["streamed"] = roof(tab_s, stage_ms_s, "slowest stage of the streamed step (every stage reads its whole atlas)")
+        out = {
             "metric": "brush-apply + layer-op texel passes per second at 16384^2 atlas",
             "value": value, "unit": "Gtexel/s", "n_gpus": world_size, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64 decisions on u8/u32/f32 planes", "data": "synthetic", "config": cfg,
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_b / (dom_ms * 1e-3) / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": dom_b / (dom_ms * 1e-3) / 1e9 / peak, "traffic": traffic,
-                         "peak_source": peak_src, "frac_of_8TBs_spec": dom_b / (dom_ms * 1e-3) / 1e9 / 8000.0,
-                         "dram_frac": None if not traffic else traffic / (dom_ms * 1e-3) / 1e9 / peak,
-                         "basis": "SURVEY 8(d) algorithmic bytes of the slowest stage that streams all of them; "
-                                  "stages that skip bytes by design (%s) are excluded, see config.stream_kernels"
-                                  % (", ".join(sorted(skipping & set(stages))) or "none")},
+            "value_streamed": value_s, "ms_per_step_streamed": total_ms_s / args.steps,
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "Gtexel/s", "ms_per_step": e2e_ms / args.steps,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h // max(1, args.steps)},
-            "gpu_launches": sum(launches[s] for s in stages) * args.steps,
+            "e2e_host_planes": host_planes,
+            "parity": parity,
+            "gpu_launches": sum(arm.launches(primary_cull)[s] for s in stages) * args.steps,
             "clocks": clocks_summary(samples, windows),
-        }))
+        }
+        print(json.dumps(out))
     if world_size > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        sys.exit(3)
+
+
+def parity_check(arm, cpu_arm, wl, stages, steps):
+    """GPU arm vs CPU arm on the same seeded inputs.  Both start from the pre-painted state and run `steps`
+    steps; the GPU does it twice (default path, then every stage streaming the whole atlas).  Compared on the
+    CPU arm's rows minus one border row each side (the CPU slab has no halo for the 1-texel TPA stencil):
+    data / mask / edited planes of all layers, the stroke's EditedAreaMask, the chain result, the mask_op result
+    (bit for bit) and the per-layer areas and texel counts of those rows (1e-10 relative; north star: 1e-6)."""
+    torch, nat = arm.torch, arm.nat
+    r0, r1 = cpu_arm.row0 + 1, cpu_arm.row0 + cpu_arm.rows - 1
+    lo, hi = 1, cpu_arm.rows - 1
+    report = {"checked": True, "ok": True, "rows": [r0, r1], "steps": steps, "stages": list(stages), "paths": {},
+              "against": CpuArm.DESCRIPTION}
+    for i in range(steps):
+        cpu_arm.step(i, stages)
+    cpu_planes = {}
+    for k in range(wl.L):
+        cpu_planes["data%d" % k], cpu_planes["mask%d" % k], cpu_planes["edited%d" % k] = cpu_arm.data[k], cpu_arm.mask[k], cpu_arm.edited[k]
+    if "tea" in stages:
+        cpu_planes["tea_edited"] = cpu_arm.tea_edited
+    if "chain" in stages:
+        cpu_planes["chain_data"], cpu_planes["chain_mask"] = cpu_arm.out_d, cpu_arm.out_m
+    if "mask_op" in stages:
+        cpu_planes["mask_op"] = cpu_arm.tmp_m
+    cpu_area = cpu_arm.kn.layers_area(np.ascontiguousarray(cpu_arm.surf["area"][lo:hi]),
+                                      [np.ascontiguousarray(m[lo:hi]) for m in cpu_arm.mask], threads=cpu_arm.threads)
+    snap = None
+    for path, cull in (("default", True), ("streamed", False)):
+        arm.seed()
+        rows_t = torch.zeros((steps, arm.nslots), dtype=torch.int64, device=arm.dev)
+        for i in range(steps):
+            inp = wl.step_inputs(i)
+            tool = arm.make_tool(inp)
+            if "batch" in stages:
+                arm.batch.upload(inp["batch"], inp["batch_layers"], inp["batch_values"])
+            for st in stages:
+                arm.stage(st, inp, tool, rows_t[i], cull)
+        gpu = {}
+        for k in range(wl.L):
+            gpu["data%d" % k], gpu["mask%d" % k], gpu["edited%d" % k] = arm.layers[k].data, arm.layers[k].mask, arm.edited[k]
+        if "tea" in stages:
+            gpu["tea_edited"] = arm.ctx.edited
+        if "chain" in stages:
+            gpu["chain_data"], gpu["chain_mask"] = arm.out_layer.data, arm.out_layer.mask
+        if "mask_op" in stages:
+            gpu["mask_op"] = arm.tmp_mask
+        bad = []
+        for name, t in gpu.items():
+            g = t[r0 - arm.row0:r1 - arm.row0].cpu().numpy().view(np.uint8)
+            if not np.array_equal(g, np.ascontiguousarray(cpu_planes[name][lo:hi]).view(np.uint8)):
+                bad.append(name)
+        sums = torch.zeros(wl.L, dtype=torch.float64, device=arm.dev)
+        cnts = torch.zeros(wl.L, dtype=torch.int64, device=arm.dev)
+        nat.layer_area(arm.surf.area[r0 - arm.row0:r1 - arm.row0], [l.mask[r0 - arm.row0:r1 - arm.row0] for l in arm.layers],
+                       sums=sums, counts=cnts)
+        gs, gc = sums.cpu().numpy(), cnts.cpu().numpy()
+        rel = float(np.max(np.abs(gs - cpu_area[0]) / np.maximum(np.abs(cpu_area[0]), 1e-300)))
+        if not np.array_equal(gc, cpu_area[1]) or not rel <= 1e-10:
+            bad.append("areas")
+        # whole-plane agreement of the two GPU paths (all rows, on the device)
+        if snap is None:
+            snap = {k: v.clone() for k, v in gpu.items()}
+            counts_default = rows_t.cpu().numpy()
+        else:
+            for k, v in gpu.items():
+                if not torch.equal(v, snap[k]):
+                    bad.append("streamed!=default:" + k)
+            cs = rows_t.cpu().numpy()
+            a, b = arm.slot["area"]
+            if not np.array_equal(np.delete(cs, np.s_[a:a + wl.L], axis=1), np.delete(counts_default, np.s_[a:a + wl.L], axis=1)):
+                bad.append("streamed!=default:counters")
+        report["paths"][path] = {"planes_compared": len(gpu), "texels_per_plane": int((r1 - r0) * wl.width),
+                                 "area_max_rel_err": rel, "mismatches": bad}
+        if bad:
+            report["ok"] = False
+    del snap
+    arm.seed()
+    return report
 
 
 if __name__ == "__main__":

@@ -929,7 +929,9 @@ class StrokeBatch:
     """Device-resident description of K sphere strokes over L layers (pointer tables included),
     reusable across calls: the only per-step host->device traffic is the stroke record upload."""
 
-    def __init__(self, layers_data, layers_mask, layers_edited, device):
+    RECORD_BYTES = 40                    # per stroke: 4 x float64 (cx, cy, cz, r) + int32 layer + uint32 value bits
+
+    def __init__(self, layers_data, layers_mask, layers_edited, device, capacity=0):
         torch = _torch()
         self.L = len(layers_data)
         self.data, self.mask, self.edited = list(layers_data), list(layers_mask), list(layers_edited)
@@ -943,39 +945,63 @@ class StrokeBatch:
         self.d_data, self.d_mask, self.d_edited = mk(self.data), mk(self.mask), mk(self.edited)
         self.counts = torch.zeros(self.L, dtype=torch.int64, device=device)
         self.device = device
+        self.K = 0
+        self._cap = 0
+        self._ev = None
+        if capacity:
+            self._reserve(int(capacity))
 
-    def upload(self, strokes, layer_of, values):
-        """strokes (K,4) float64 [cx,cy,cz,r]; layer_of (K,) int; values (K,) in plane dtype."""
+    def _reserve(self, cap):
+        """ONE packed record buffer (pinned host twin + device): [cap x 4 float64 | cap x int32 | cap x uint32].
+        The three arrays the kernels read are views of it, so an upload is one copy and a multi-rank
+        broadcast (sharding.broadcast_batch) one collective with nothing to unpack."""
+        torch = _torch()
+        self._cap = cap
+        nbytes = cap * self.RECORD_BYTES
+        self._pin = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        self.packed = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        host = self._pin.numpy()
+        self._h_strokes = host[:32 * cap].view(np.float64).reshape(cap, 4)
+        self._h_layer = host[32 * cap:36 * cap].view(np.int32)
+        self._h_value = host[36 * cap:40 * cap].view(np.uint32)
+        self._d_strokes = self.packed[:32 * cap].view(torch.float64).view(cap, 4)
+        self._d_layer = self.packed[32 * cap:36 * cap].view(torch.int32)
+        self._d_value = self.packed[36 * cap:40 * cap].view(torch.int32)
+
+    def use(self, K):
+        """Strokes [0, K) of the packed buffer are the batch (after an upload or a broadcast)."""
+        self.K = int(K)
+        self.d_strokes, self.d_layer_of, self.d_values = self._d_strokes[:K], self._d_layer[:K], self._d_value[:K]
+        return self
+
+    def upload(self, strokes, layer_of, values, fill=False):
+        """strokes (K,4) float64 [cx,cy,cz,r]; layer_of (K,) int; values (K,) in plane dtype.  One host->device
+        copy from pinned memory.  ``fill``: pad the buffer to its capacity with strokes that can never hit
+        (NaN centre and radius) and use all of it -- ranks that receive the buffer by broadcast then need not
+        know K (no host read-back on the stroke path)."""
         torch = _torch()
         strokes = np.ascontiguousarray(strokes, dtype=np.float64)
         K = strokes.shape[0]
         dt = _np_dtype_of(self.data[0])
-        vals = np.zeros(K, dtype=np.uint32)
+        if K > self._cap or self._cap == 0:                      # (an empty first batch still needs buffers)
+            if self._ev is not None:
+                self._ev.synchronize()
+            self._reserve(max(K, 2 * self._cap, 1))
+        if self._ev is not None:
+            self._ev.synchronize()            # the previous upload must have left the pinned buffer
+        self._h_strokes[:K] = strokes
+        self._h_layer[:K] = np.asarray(layer_of, dtype=np.int32)
         v = np.asarray(values).astype(dt).reshape(K)
-        vals[:] = v.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[dt.itemsize])
-        self.K = K
-        # stage through pinned host memory (one buffer per record array, grown on demand) so the
-        # host->device copies are asynchronous DMA transfers
-        cap = getattr(self, "_cap", 0)
-        if K > cap or cap == 0:                                  # (an empty first batch still needs buffers)
-            self._cap = max(K, 2 * cap, 1)
-            self._pin = (torch.empty((self._cap, 4), dtype=torch.float64).pin_memory(),
-                         torch.empty(self._cap, dtype=torch.int32).pin_memory(),
-                         torch.empty(self._cap, dtype=torch.int32).pin_memory())
-            self._dev = tuple(torch.empty_like(p, device=self.device) for p in self._pin)
-        if getattr(self, "_ev", None) is not None:
-            self._ev.synchronize()            # the previous upload must have left the pinned buffers
-        ps, pl, pv = self._pin
-        ps[:K].copy_(torch.from_numpy(strokes))
-        pl[:K].copy_(torch.from_numpy(np.ascontiguousarray(layer_of, dtype=np.int32)))
-        pv[:K].copy_(torch.from_numpy(vals.view(np.int32)))
-        for p, d in zip(self._pin, self._dev):
-            d[:K].copy_(p[:K], non_blocking=True)
+        self._h_value[:K] = v.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[dt.itemsize])
+        if fill:
+            self._h_strokes[K:] = np.nan
+            self._h_layer[K:] = 0
+            self._h_value[K:] = 0
+        self.packed.copy_(self._pin, non_blocking=True)
         self._ev = torch.cuda.Event()
         self._ev.record()
-        self.d_strokes, self.d_layer_of, self.d_values = (d[:K] for d in self._dev)
-        self.upload_bytes = K * (32 + 4 + 4)
-        return self
+        self.upload_bytes = (self._cap if fill else K) * self.RECORD_BYTES
+        return self.use(self._cap if fill else K)
 
 
 def select_sphere_batch(pos, batch, *, tiles=None):

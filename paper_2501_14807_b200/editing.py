@@ -166,16 +166,19 @@ def _stroke_checks(ctx, layer):
         raise LayerMeshMismatch("no uv coverage at layer resolution")
 
 
-def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False, cull=True):
+def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False, cull=True, counts=None):
     """SPEC.md:277-285 TEA.  Uses the per-texel kernel over the cached triangle-id map when the uv
     layout has no overlaps (bit-identical), else the direct per-triangle kernel.
     ``cull`` (default) restricts the per-texel kernel to the stroke's footprint tiles, so a stroke
-    costs O(triangles + footprint) instead of O(atlas); results are identical."""
+    costs O(triangles + footprint) instead of O(atlas); results are identical.  ``counts``: a
+    ZEROED int64 device tensor of 2 elements to accumulate (edited, fragments) into (callers that queue many
+    strokes keep one counter block per step instead of one allocation + fill per stroke)."""
     torch = _native._torch()
     _stroke_checks(ctx, layer)
     s = ctx.surface
     sfx, sfy, bx, by = compute_tool_projection(ctx.camera, tool).kernel_factors
-    counts = torch.zeros(2, dtype=torch.int64, device=ctx.device)
+    if counts is None:
+        counts = torch.zeros(2, dtype=torch.int64, device=ctx.device)
     shape = tool.shape if _native._is_cuda_tensor(tool.shape) else _native._as_dev_bytes(tool.shape, ctx.device)
     args = (float(ctx.camera.width), float(ctx.camera.height), ctx.depth.plane, eps, sfx, sfy, bx, by,
             shape, layer.data, layer.mask, ctx.edited, tool.value)
@@ -330,7 +333,7 @@ def stroke_gesture(ctx, tools, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):
 # --------------------------------------------------------------------------------------------
 # north-star selection brushes
 
-def select_sphere(surface, layer, center, radius, value, edited=None, *, cull=True):
+def select_sphere(surface, layer, center, radius, value, edited=None, *, cull=True, counts=None):
     """Sphere brush: every covered texel whose surface point lies within ``radius`` of ``center``
     gets data = value, mask = true (definition: oracle ext_select_sphere).  ``cull`` (default) reads
     only the position-map tiles the sphere can reach (identical result, O(footprint) traffic);
@@ -340,7 +343,8 @@ def select_sphere(surface, layer, center, radius, value, edited=None, *, cull=Tr
         raise TargetMismatch("layer does not match the surface map")
     if edited is None:
         edited = torch.zeros(layer.shape, dtype=torch.uint8, device=surface.pos.device)
-    counts = torch.zeros(1, dtype=torch.int64, device=surface.pos.device)
+    if counts is None:
+        counts = torch.zeros(1, dtype=torch.int64, device=surface.pos.device)
     _native.select_sphere(surface.pos, center, radius, layer.data, layer.mask, edited, value, counts=counts,
                           tiles=surface.tiles if cull else None)
     return EditResult(edited_mask=edited, _counts=counts, transfer_bytes=40)
@@ -353,7 +357,7 @@ def select_sphere_batch(surface, batch, *, cull=True):
     return batch.counts
 
 
-def select_threshold(attr, valid, lo, hi, layer, value, edited=None, *, tiles=None):
+def select_threshold(attr, valid, lo, hi, layer, value, edited=None, *, tiles=None, counts=None):
     """Attribute-threshold selection into ``layer`` (definition: oracle ext_select_threshold).
     ``tiles`` = ``_native.attr_tiles(attr)`` of a float32 attribute plane that does not change between
     selections (e.g. the surface map's height plane): only tiles whose value range meets [lo, hi]
@@ -363,7 +367,8 @@ def select_threshold(attr, valid, lo, hi, layer, value, edited=None, *, tiles=No
         raise TargetMismatch("attribute plane does not match the layer")
     if edited is None:
         edited = torch.zeros(layer.shape, dtype=torch.uint8, device=attr.device)
-    counts = torch.zeros(1, dtype=torch.int64, device=attr.device)
+    if counts is None:
+        counts = torch.zeros(1, dtype=torch.int64, device=attr.device)
     _native.select_threshold(attr, valid, lo, hi, layer.data, layer.mask, edited, value, counts=counts, tiles=tiles)
     return EditResult(edited_mask=edited, _counts=counts, transfer_bytes=24)
 

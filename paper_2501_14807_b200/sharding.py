@@ -43,35 +43,86 @@ def all_slabs(height, world_size):
     return [shard_rows(height, world_size, r) for r in range(world_size)]
 
 
-def broadcast_strokes(strokes, layer_of, values, device, src=0):
-    """Rank ``src`` supplies numpy arrays (strokes (K,4) f64, layer_of (K,) i32, values (K,) u32
-    bit patterns); every rank returns the same three numpy arrays.  One broadcast of a packed
-    (K,6) float64 tensor; K is broadcast first so receivers can size the buffer."""
+def broadcast_strokes(strokes, layer_of, values, device, src=0, capacity=256):
+    """Host-facing form: rank ``src`` supplies numpy arrays (strokes (K,4) f64, layer_of (K,) i32, values
+    (K,) u32 bit patterns); every rank returns the same three numpy arrays.  ONE broadcast of a fixed
+    (capacity+1, 6) float64 buffer whose first row carries K (batches larger than ``capacity`` go in several
+    rounds).  Returning numpy means a read-back on the receivers; the per-step device path is
+    ``broadcast_batch``, which has none."""
     import torch
     dist = _dist()
     rank, ws = world()
     if ws == 1:
         return strokes, layer_of, values
-    k = torch.zeros(1, dtype=torch.int64, device=device)
-    if rank == src:
-        k[0] = len(strokes)
-    dist.broadcast(k, src=src)
-    K = int(k.item())
-    buf = torch.zeros((K, 6), dtype=torch.float64, device=device)
-    if rank == src:
-        packed = np.zeros((K, 6), dtype=np.float64)
-        packed[:, :4] = strokes
-        packed[:, 4] = layer_of
-        packed[:, 5] = values            # uint32 bit patterns are exact in float64
-        buf.copy_(torch.from_numpy(packed))
-    dist.broadcast(buf, src=src)
-    out = buf.cpu().numpy()
+    outs, start = [], 0
+    while True:
+        buf = torch.zeros((capacity + 1, 6), dtype=torch.float64, device=device)
+        if rank == src:
+            k = min(capacity, len(strokes) - start)
+            packed = np.zeros((capacity + 1, 6), dtype=np.float64)
+            packed[0, 0], packed[0, 1] = k, len(strokes) - start - k       # this round, still to come
+            packed[1:k + 1, :4] = strokes[start:start + k]
+            packed[1:k + 1, 4] = layer_of[start:start + k]
+            packed[1:k + 1, 5] = values[start:start + k]                   # uint32 bit patterns are exact in float64
+            buf.copy_(torch.from_numpy(packed))
+            start += k
+        dist.broadcast(buf, src=src)
+        out = buf.cpu().numpy()
+        k, more = int(out[0, 0]), int(out[0, 1])
+        outs.append(out[1:k + 1])
+        if more <= 0:
+            break
+    out = np.concatenate(outs, axis=0)
     return (np.ascontiguousarray(out[:, :4]), out[:, 4].astype(np.int32), out[:, 5].astype(np.uint32))
+
+
+def broadcast_batch(batch, src=0):
+    """Device-to-device broadcast of a ``_native.StrokeBatch``'s packed record buffer (rank ``src`` has called
+    ``batch.upload(..., fill=True)``; every rank's batch was created with the same ``capacity``).  One
+    collective on the compute stream, no host read-back: receivers use the whole buffer (unused slots hold
+    NaN strokes, which hit nothing), so the stroke path never waits for the host."""
+    dist = _dist()
+    _, ws = world()
+    if ws > 1:
+        dist.broadcast(batch.packed, src=src)
+    return batch.use(batch._cap)
+
+
+class AreaReducer:
+    """Cross-rank sum of the per-layer areas (float64) and texel counts (int64) with ONE collective and no
+    conversion kernels: every rank's 2L raw 8-byte slots are all-gathered (a few hundred bytes) and summed
+    locally in rank order, so all ranks get bit-identical areas whatever algorithm the backend picks for an
+    all-reduce.  ``slots``: int64 tensor of 2L elements, [0, L) holding the float64 bit patterns of the
+    partial sums (the area kernel writes them through a float64 view), [L, 2L) the counts."""
+
+    def __init__(self, layers, device):
+        import torch
+        self.L = int(layers)
+        _, self.ws = world()
+        self.gathered = torch.empty((self.ws, 2 * self.L), dtype=torch.int64, device=device) if self.ws > 1 else None
+
+    def __call__(self, slots):
+        if self.ws == 1:
+            return slots
+        import torch
+        dist = _dist()
+        if slots.is_cuda and dist.get_backend() != "nccl":
+            # gloo (CPU tests, single-GPU rehearsal of the multi-rank path) gathers host tensors only
+            host = [torch.empty(2 * self.L, dtype=torch.int64) for _ in range(self.ws)]
+            dist.all_gather(host, slots.cpu())
+            self.gathered.copy_(torch.stack(host))
+        else:
+            dist.all_gather_into_tensor(self.gathered.view(-1), slots.contiguous())
+        L = self.L
+        slots[:L].view(torch.float64).copy_(self.gathered[:, :L].view(torch.float64).sum(dim=0))
+        slots[L:].copy_(self.gathered[:, L:].sum(dim=0))
+        return slots
 
 
 def allreduce_areas(sums, counts=None):
     """Sum per-layer partial areas (float64 tensor) and counts (int64 tensor) over all ranks, in
-    place.  One collective: counts ride along as exact float64 (< 2^53 texels)."""
+    place.  One collective: counts ride along as exact float64 (< 2^53 texels).  (Convenience form;
+    the per-step path uses ``AreaReducer``, which needs no packing kernels.)"""
     import torch
     dist = _dist()
     _, ws = world()

@@ -67,7 +67,18 @@ def test_gpu_arm_json_contract(extra):
     assert d["gpu_launches"] == per_step * 3
     assert set(d["config"]["stage_results"]) == {"tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area"}
     assert d["config"]["footprint_culling"] == (not extra)
-    assert ("stream_kernels" in d["config"]) and (bool(d["config"]["stream_kernels"]) == (not extra))
+    assert set(d["config"]["stream_kernels"]) == set(d["config"]["stage_results"])
+    assert set(d["config"]["stage_results_streamed"]) == set(d["config"]["stage_results"])
+    assert d["value_streamed"] > 0 and d["ms_per_step_streamed"] > 0
+    assert ro["streamed"]["bound"] == "hbm" and ro["streamed"]["kernel"] in d["config"]["stage_results"]
+    # in-run parity of the two arms: GPU planes of the sampled rows == the CPU restatement's, both GPU paths
+    pa = d["parity"]
+    assert pa["checked"] is True and pa["ok"] is True, pa
+    assert set(pa["paths"]) == {"default", "streamed"} and all(not v["mismatches"] for v in pa["paths"].values())
+    assert pa["paths"]["default"]["planes_compared"] == 3 * 4 + 4
+    # the reference's call shape with host planes
+    hp = d["e2e_host_planes"]
+    assert hp["ms_per_call"] > 0 and hp["equal_to_resident_stroke"] is True and hp["edited"] > 0
 
 
 @pytest.mark.gpu
@@ -90,5 +101,51 @@ def test_gpu_arm_two_rank_rehearsal_over_gloo():
     assert len(lines) == 1                                            # rank 0 alone prints
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["parallelism"] == "row-sharded x2" and d["config"]["atlas"] == [1024, 512]
-    assert d["cpu_baseline"] is None                                  # N = 1 only
+    assert d["config"]["parallelism"] == "row-sharded x2 (weak scaling)" and d["config"]["atlas"] == [1024, 512]
+    assert d["cpu_baseline"] is None and d["parity"] is None          # N = 1 only
+
+
+@pytest.mark.gpu
+def test_gpu_arm_config5_strong_scaling_rehearsal():
+    """--config c5 (BASELINE config 5: 64 batched strokes + per-layer areas, strong scaling) at a tiny atlas, on one
+    rank and on two gloo ranks sharing cuda:0: the rows are SPLIT over the ranks, the whole-job texel count stays."""
+    import socket
+    base = ["--config", "c5", "--steps", "3", "--warmup", "3", "--atlas", "512", "--cpu-rows", "64", "--quads", "48", "--layers", "4"]
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + base, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d1 = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d1["scaling"] == "strong" and d1["config"]["stages"] == ["batch", "area"] and d1["config"]["batch_strokes"] == 64
+    assert d1["parity"]["ok"] is True and d1["config"]["atlas"] == [512, 512]
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, ML_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py")] + base + ["--gpus", "2"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d2 = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d2["n_gpus"] == 2 and d2["scaling"] == "strong" and d2["config"]["atlas"] == [512, 512]
+
+
+
+@pytest.mark.gpu
+def test_nccl_two_ranks_when_two_gpus_are_visible():
+    """The real thing: two ranks, one GPU each, NCCL over NVLink (stroke-table broadcast, cross-rank area gather,
+    halo rows point-to-point).  Runs whenever the box shows >= 2 GPUs, skips otherwise (the round's boxes have one)."""
+    import socket
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    for cfg in ([], ["--config", "c5"]):
+        args = cfg + ["--gpus", "2", "--steps", "5", "--warmup", "3", "--atlas", "1024", "--cpu-rows", "64", "--quads", "96",
+                      "--window", "256", "--layers", "4"]
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py")] + args,
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+        assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0

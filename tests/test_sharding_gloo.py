@@ -52,8 +52,21 @@ def _worker(rank, world_size, port, out_dir):
             counts[L] += kn.select_sphere(surf["pos"], s[k, :3], s[k, 3], data[L], mask[L], edited[L], int(v[k]))
         sums = torch.tensor([kn.layer_area(surf["area"], m)[0] for m in mask], dtype=torch.float64)
         texels = torch.tensor([kn.layer_area(surf["area"], m)[1] for m in mask], dtype=torch.int64)
+        # the per-step form: raw 8-byte slots, one all-gather, summed in rank order on every rank
+        slots = torch.cat([sums.view(torch.int64), texels])
+        sharding.AreaReducer(2, "cpu")(slots)
         sharding.allreduce_areas(sums, texels)
         sharding.allreduce_counts(counts)
+        assert torch.equal(slots[2:], texels)
+        assert torch.allclose(slots[:2].view(torch.float64), sums, rtol=1e-15, atol=0.0)
+        # a batch larger than the broadcast buffer travels in several rounds
+        if rank == 0:
+            big = np.arange(44, dtype=np.float64).reshape(11, 4)
+            got = sharding.broadcast_strokes(big, np.arange(11, dtype=np.int32), np.arange(11, dtype=np.uint32) + 7, "cpu", capacity=4)
+        else:
+            got = sharding.broadcast_strokes(np.zeros((0, 4)), np.zeros(0, np.int32), np.zeros(0, np.uint32), "cpu", capacity=4)
+        assert np.array_equal(got[0], np.arange(44, dtype=np.float64).reshape(11, 4))
+        assert got[1].tolist() == list(range(11)) and got[2].tolist() == [k + 7 for k in range(11)]
 
         # ---- halo exchange of a byte plane for a radius-2 stencil
         cov = torch.from_numpy((surf["tri_id"] >= 0).astype(np.uint8))
