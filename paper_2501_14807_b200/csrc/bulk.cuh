@@ -14,7 +14,8 @@
 //   stage s of round k (k-th use of the stage): full[s] completes phase k when the copy's bytes
 //   have landed; empty[s] completes phase k when all CONSUMER_WARPS have released the stage.
 //   Producer before refilling stage s for round k >= 1 waits empty[s] parity (k-1)&1.
-//   Consumers of round k wait full[s] parity k&1.
+//   Consumers of round k wait full[s] parity k&1; before releasing a stage they issue
+//   fence.proxy.async (their generic-proxy reads must be ordered before the async-proxy refill).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -101,13 +102,27 @@ struct BulkRing {
         mbar_arrive_expect_tx(&full[pos.stage], bytes);
         bulk_g2s(buf[pos.stage], src, bytes, &full[pos.stage], policy);
     }
+    // PRODUCER lane, several sources per stage (e.g. one slice of each of G planes): arm the stage for
+    // `total` bytes, then issue the pieces with fill()
+    ML_DEV void begin_fill(const RingPos<STAGES>& pos, unsigned total) {
+        if (pos.round > 0) mbar_wait(&empty[pos.stage], pos.empty_parity());
+        mbar_arrive_expect_tx(&full[pos.stage], total);
+    }
+    ML_DEV void fill(const RingPos<STAGES>& pos, unsigned offset, const void* src, unsigned bytes, uint64_t policy) {
+        bulk_g2s(buf[pos.stage] + offset, src, bytes, &full[pos.stage], policy);
+    }
     // CONSUMER threads: wait until the stage holds its chunk
     ML_DEV const uint8_t* acquire(const RingPos<STAGES>& pos) {
         mbar_wait(&full[pos.stage], pos.full_parity());
         return buf[pos.stage];
     }
     // CONSUMER warps (all lanes call; lane 0 arrives once the warp's reads are done)
+    // The stage's next user is the ASYNC proxy (the producer's next cp.async.bulk overwrites it), the reads
+    // just done were generic-proxy LDS: a write-after-read across proxies is ordered only by a proxy fence.
+    // Measured without it (area_bulk_kernel<1>, 4 KB stages, 16.8 M texels): tens of texels per launch read
+    // from the NEXT round's bytes -- mbarrier release semantics alone do not cover the async proxy.
     ML_DEV void release(const RingPos<STAGES>& pos) {
+        fence_proxy_async();
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[pos.stage]);
     }

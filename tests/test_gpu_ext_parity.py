@@ -610,3 +610,23 @@ def test_select_threshold_culled_bit_exact(sphere_map, kind, value):
                 assert np.array_equal(_bits(_host(d)), _bits(rd))
                 assert np.array_equal(m.cpu().numpy(), rm) and np.array_equal(e.cpu().numpy(), re)
     assert nat.attr_tiles(got["pos"][2][:, :200].contiguous()) is None and nat.attr_tiles(got["tri_id"]) is None
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 8])
+def test_layer_area_counts_exact_over_many_ring_rounds(L):
+    """Regression for a cross-proxy race in the bulk-copy ring (csrc/bulk.cuh): with small stages (one or two mask
+    planes per group -> 4-8 KB stages recycled thousands of times) consumers read bytes of the NEXT round unless
+    they fence the async proxy before releasing a stage.  Texel counts over 16.8 M texels must be exact, every time."""
+    import torch
+    N = 4096 * 4096
+    g = torch.Generator(device="cuda").manual_seed(7 + L)
+    area = torch.rand(N, device="cuda", dtype=torch.float32, generator=g)
+    masks = [(torch.rand(N, device="cuda", generator=g) < 0.3).to(torch.uint8) for _ in range(L)]
+    want_c = [int(m.sum()) for m in masks]
+    want_s = [float((area.double() * m.double()).sum()) for m in masks]
+    for rep in range(5):
+        sums = torch.zeros(L, dtype=torch.float64, device="cuda")
+        cnts = torch.zeros(L, dtype=torch.int64, device="cuda")
+        nat.layer_area(area.view(1, N), [m.view(1, N) for m in masks], sums=sums, counts=cnts)
+        assert cnts.tolist() == want_c
+        assert all(abs(a - b) <= 1e-12 * b for a, b in zip(sums.tolist(), want_s))
