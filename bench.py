@@ -753,8 +753,10 @@ def run_ours(args):
                 key = "chain" if cull else "chain_stream"
             tb = traffic.get(key)
             if tb is not None:
-                # traffic.json holds bytes per launch of the stage's dominant kernel at 16384^2 x 8 layers
-                per_step = tb * (launches[st] if st == "area" else 1)
+                # traffic.json: DRAM bytes of one launch of each of the stage's kernels in the default workload
+                # (16384^2 texels, 8 layers); other atlas sizes scale with the texel count, more layers with the
+                # number of 8-layer area launches
+                per_step = tb * (launches[st] if st == "area" else 1) * n / float(traffic.get("_texels", 16384 * 16384))
                 row["dram_bytes"] = per_step
                 row["dram_frac_of_peak"] = round(per_step / ms / 1e6 / peak, 4)
             if st in BRUSH:

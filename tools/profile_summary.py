@@ -13,11 +13,19 @@ import json
 import subprocess
 import sys
 
-STAGE_OF = (("chain_lazy_kernel", "chain"), ("chain_kernel", "chain_stream"), ("binary_kernel", "mask_op"), ("sphere_batch_tiles_kernel", "batch"),
-            ("sphere_batch_kernel", "batch_stream"), ("sphere_tiles_kernel", "sphere"), ("sphere_kernel", "sphere_stream"),
-            ("threshold_tiles_kernel", "threshold"), ("threshold_kernel", "threshold_stream"), ("area_kernel", "area"),
-            ("tea_eval_kernel", "tea"),
-            ("padding_tile_kernel", "tpa"), ("padding_stream_kernel", "tpa_stream"), ("tea_stream_kernel", "tea_stream"))
+# kernel-name substring -> the bench stages it belongs to ("<stage>" = default path, "<stage>_stream" = whole-atlas
+# form).  traffic.json sums ONE launch of every kernel of a stage (classification + main + evaluation kernels).
+STAGE_OF = (("chain_lazy_kernel", ("chain",)), ("chain_kernel", ("chain_stream",)), ("binary_kernel", ("mask_op",)),
+            ("sphere_batch_tiles_kernel", ("batch",)), ("sphere_batch_kernel", ("batch_stream",)),
+            ("sphere_tiles_kernel", ("sphere",)), ("sphere_kernel", ("sphere_stream",)),
+            ("tile_classify_kernel", ("sphere", "batch")),
+            ("threshold_tiles_kernel", ("threshold",)), ("range_classify_kernel", ("threshold",)),
+            ("threshold_bulk_kernel", ("threshold_stream",)), ("threshold_vec_kernel", ("threshold_stream",)),
+            ("threshold_kernel", ("threshold_stream",)),
+            ("area_bulk_kernel", ("area",)), ("area_kernel", ("area",)),
+            ("tea_eval_kernel", ("tea", "tea_stream")), ("tea_classify", ("tea", "tea_stream")),
+            ("tea_tile_kernel", ("tea",)), ("tea_stream_bulk_kernel", ("tea_stream",)), ("tea_stream_kernel", ("tea_stream",)),
+            ("padding_tile_kernel", ("tpa",)), ("padding_bulk_kernel", ("tpa_stream",)), ("padding_stream_kernel", ("tpa_stream",)))
 
 METRICS = [
     ("gpu__time_duration.sum", "time"),
@@ -102,12 +110,16 @@ def full(srcs, dst, traffic_dst=None):
                         f.write("| %s | %s %s |\n" % (label, r[i], units[i]))
                 top = sorted(((float(r[i]), h) for i, h in stall if r[i]), reverse=True)[:4]
                 f.write("| top stalls (warps per issue) | %s |\n\n" % ", ".join("%s %.2f" % (h, v) for v, h in top))
-                for key, stage in STAGE_OF:
-                    if key in name and stage not in traffic and "dram__bytes_read.sum" in hdr:
-                        traffic[stage] = tobytes(r, "dram__bytes_read.sum") + tobytes(r, "dram__bytes_write.sum")
+                for key, stages in STAGE_OF:
+                    if key in name and "dram__bytes_read.sum" in hdr:
+                        for stage in stages:
+                            traffic[stage] = traffic.get(stage, 0.0) + tobytes(r, "dram__bytes_read.sum") + tobytes(r, "dram__bytes_write.sum")
                         break
     print("wrote", dst)
     if traffic_dst:
+        # the capture is the default bench workload: 16384^2 texels, 8 layers (bench.py scales by texels for other sizes)
+        traffic["_texels"] = 16384 * 16384
+        traffic["_layers"] = 8
         json.dump(traffic, open(traffic_dst, "w"), indent=1, sort_keys=True)
         print("wrote", traffic_dst, traffic)
 
