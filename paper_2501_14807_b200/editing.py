@@ -72,14 +72,30 @@ def project_fragment(s, t, w):
 
 @dataclass
 class EditResult:
-    """SPEC.md:245-247.  Counts stay on the device until read (no sync on the stroke path)."""
+    """SPEC.md:245-247.  Counts stay on the device until read (no sync on the stroke path).
+
+    ``edited_mask`` is the stroke context's EditedAreaMask plane: ONE plane per context, reset
+    and rewritten by the next stroke -- it describes this stroke only until then (clone it, or bit-pack it with
+    ``_native.pack_mask``, to keep it).  Results of ``stroke_gesture`` other than the last carry ``None``: all
+    strokes of a gesture are queued by one host call and only the last stroke's marks survive it.
+    ``duration_ms``: device time of the stroke when it was run with ``timed=True`` (two CUDA events around the
+    engine call, read lazily), else ``None`` -- the stroke path does not pay for events nobody reads."""
     edited_mask: object
     _counts: object = None
     padded: int = 0
-    duration_ms: float = 0.0
     transfer_bytes: int = TRANSFER_BYTES_PER_STROKE
     _cache: dict = field(default_factory=dict)
     _padded: object = None
+    _events: object = None
+
+    @property
+    def duration_ms(self):
+        if self._events is None:
+            return None
+        if "ms" not in self._cache:
+            self._events[1].synchronize()
+            self._cache["ms"] = float(self._events[0].elapsed_time(self._events[1]))
+        return self._cache["ms"]
 
     @property
     def padded_count(self):
@@ -204,7 +220,28 @@ def apply_stroke(ctx, tool, layer, *, eps=DEFAULT_DEPTH_BIAS, force_direct=False
     return EditResult(edited_mask=ctx.edited, _counts=counts)
 
 
-def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, halo=None):
+def _timed(fn, timed):
+    """Run fn() between two CUDA events when ``timed``; returns (result, events or None)."""
+    if not timed:
+        return fn(), None
+    torch = _native._torch()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = fn()
+    e1.record()
+    return res, (e0, e1)
+
+
+def stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, halo=None, timed=False):
+    """The service's ``stroke`` (the edit the paper times): TEA followed by TPA with
+    the tool's padding radius (details: ``_stroke``).  ``timed=True`` brackets the edit with two CUDA events;
+    ``EditResult.duration_ms`` then reports its device time."""
+    res, ev = _timed(lambda: _stroke(ctx, tool, layer, outline, eps=eps, cull=cull, halo=halo), timed)
+    res._events = ev
+    return res
+
+
+def _stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, halo=None):
     """The service's ``stroke`` (the edit the paper times): TEA
     (``apply_stroke``) followed by TPA (``apply_padding``) with the tool's padding radius.
     ``outline`` is the layer-resolution outline mask (``build_outline_mask``).  The padded count
@@ -313,7 +350,10 @@ def stroke_gesture(ctx, tools, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):
                 and all(t.padding_radius == radius for t in tools)
                 and all(t.data_ptr() % 16 == 0 for t in (layer.data, layer.mask, as_u8)))
     if not one_call:
-        return [stroke(ctx, t, layer, outline, eps=eps) for t in tools]
+        res = [stroke(ctx, t, layer, outline, eps=eps) for t in tools]
+        for r in res[:-1]:
+            r.edited_mask = None              # the shared EditedAreaMask plane now holds the last stroke's marks
+        return res
     _stroke_checks(ctx, layer)
     ctx.begin_culled_stroke()
     if ctx._cstruct is None or ctx._cstruct[0] != as_u8.data_ptr():
@@ -327,7 +367,9 @@ def stroke_gesture(ctx, tools, layer, outline, *, eps=DEFAULT_DEPTH_BIAS):
                                  [t.value for t in tools], radius, counts)
     for _ in tools:
         ctx.end_culled_stroke()
-    return [EditResult(edited_mask=ctx.edited, _counts=counts[k, :2], _padded=counts[k, 2:]) for k in range(len(tools))]
+    last = len(tools) - 1
+    return [EditResult(edited_mask=ctx.edited if k == last else None, _counts=counts[k, :2], _padded=counts[k, 2:])
+            for k in range(len(tools))]
 
 
 # --------------------------------------------------------------------------------------------

@@ -141,13 +141,54 @@ def mesh_surface_area(mesh):
     return float(np.sqrt((cr * cr).sum(axis=1)).sum() * 0.5)
 
 
+def _clip_eye_plane(clip, eps_w):
+    """Triangles (T,3,4) in clip space with vertices on both sides of the plane w = eps_w, clipped to
+    w >= eps_w (Sutherland-Hodgman against one plane): one triangle when one vertex is inside, two when two
+    are.  Vertex order (winding) is preserved."""
+    inside = clip[..., 3] > eps_w                                        # (T,3)
+    nin = inside.sum(axis=1)
+    out = []
+    idx = np.arange(3)
+
+    def cut(p_in, p_out):                                               # intersection of edge in -> out with the plane
+        t = (p_in[:, 3] - eps_w) / (p_in[:, 3] - p_out[:, 3])
+        return p_in + t[:, None] * (p_out - p_in)
+
+    one = np.flatnonzero(nin == 1)
+    if one.size:
+        k = inside[one].argmax(axis=1)                                  # the inside vertex, rotated to the front
+        a = clip[one, k]
+        b = clip[one, (k + 1) % 3]
+        c = clip[one, (k + 2) % 3]
+        out.append(np.stack([a, cut(a, b), cut(a, c)], axis=1))
+    two = np.flatnonzero(nin == 2)
+    if two.size:
+        k = (~inside[two]).argmax(axis=1)                               # the outside vertex c; a, b follow it cyclically
+        c = clip[two, k]
+        a = clip[two, (k + 1) % 3]
+        b = clip[two, (k + 2) % 3]
+        bc, ca = cut(b, c), cut(a, c)
+        out.append(np.stack([a, b, bc], axis=1))
+        out.append(np.stack([a, bc, ca], axis=1))
+    del idx
+    return np.concatenate(out, axis=0) if out else np.zeros((0, 3, 4))
+
+
 def window_triangles(mesh, camera):
-    """Per-triangle window-space xy (T,3,2) and NDC z (T,3) for the depth pass.  Triangles with a
-    vertex at w <= 0 are dropped (KN:106 expects pre-clipped input; near-plane clipping proper is
-    a mesh-preparation concern outside the hot path)."""
+    """Per-triangle window-space xy (T',3,2) and NDC z (T',3) for the depth pass (KN:106 expects input with
+    w > 0).  Triangles entirely behind the eye plane are dropped; triangles CROSSING it are clipped to
+    w >= eps_w (1 or 2 triangles, appended after the untouched ones), so geometry that straddles the camera
+    still occludes what lies behind its visible part (SPEC 'occlusion safety'; round-1 dropped such triangles
+    whole).  Triangles with all three w > 0 pass through unchanged, in order."""
     clip = camera.clip_coords(mesh.vertices)[mesh.triangles]            # (T,3,4)
-    keep = (clip[..., 3] > 0.0).all(axis=1)
-    clip = clip[keep]
+    w = clip[..., 3]
+    keep = (w > 0.0).all(axis=1)
+    crossing = (~keep) & (w > 0.0).any(axis=1)
+    parts = [clip[keep]]
+    if crossing.any():
+        eps_w = 1e-9 * float(np.abs(w).max())
+        parts.append(_clip_eye_plane(clip[crossing], eps_w))
+    clip = np.concatenate(parts, axis=0) if len(parts) > 1 else parts[0]
     ndc = clip[..., :3] / clip[..., 3:4]
     xy = np.empty(clip.shape[:2] + (2,), dtype=np.float64)
     xy[..., 0] = (ndc[..., 0] + 1.0) * 0.5 * camera.width

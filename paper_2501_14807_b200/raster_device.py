@@ -121,15 +121,28 @@ def rasterize(tri_xy, targets, values, keep=None):
         raise TargetMismatch("targets disagree in dimensions")
     import numpy as np
     T = int(tri_xy.shape[0])
-    tri_id, _, _ = _native.raster_tri_id(tri_xy, shape[1], shape[0], device=planes[0].device)
     if T == 0:
         return 0
     dev = planes[0].device
-    keep_dev = None if keep is None else _native._as_dev_bytes(np.asarray(keep).astype(np.uint8), dev)
+    # Fragments are offered to the rule triangle by triangle and the LAST KEPT write wins: a texel
+    # covered by a kept triangle and by a later discarded one holds the kept triangle's value.  So the discarded
+    # triangles are dropped BEFORE the owner pass (an owner map over all triangles followed by a keep test would
+    # leave such texels unwritten); values are gathered with the same selection, which keeps submission order.
+    sel = None
+    if keep is not None:
+        sel = np.flatnonzero(np.asarray(keep).astype(bool).reshape(T))
+        if sel.size == 0:
+            return 0
+        if torch.is_tensor(tri_xy):
+            tri_xy = tri_xy[torch.from_numpy(sel).to(tri_xy.device)]
+        else:
+            tri_xy = np.ascontiguousarray(np.asarray(tri_xy)[sel])
+    tri_id, _, _ = _native.raster_tri_id(tri_xy, shape[1], shape[0], device=dev)
     written = 0
     for plane, vals in zip(planes, values):
         dt = _native._np_dtype_of(plane)
-        v = np.broadcast_to(np.asarray(vals).astype(dt), (T,)).copy()
+        v = np.broadcast_to(np.asarray(vals).astype(dt), (T,))
+        v = np.ascontiguousarray(v if sel is None else v[sel])
         vt = torch.from_numpy(v.view({1: np.uint8, 2: np.int16, 4: np.int32}[dt.itemsize])).to(dev)
-        written = _native.owner_values(tri_id, vt, plane, keep_dev)
+        written = _native.owner_values(tri_id, vt, plane, None)
     return written

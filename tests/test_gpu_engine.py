@@ -530,6 +530,40 @@ def test_layer_algebra_and_area_api():
         ml.layer_union(a, ml.create_layer("small", "uint8", 64, 64, pool=pool))
 
 
+def test_edit_result_duration_and_gesture_masks():
+    mesh, cam, surf, depth, ctx = _scene()
+    A = 128
+    outline = ml.build_outline_mask(surf.coverage, thickness=1)
+    layer = ml.create_layer("L", "uint8", A, A, pool=ml.TexturePool())
+    tool = ml.EditingTool(px=48.0, py=48.0, shape=synth.circle_shape(10), value=4)
+    assert ml.stroke(ctx, tool, layer, outline).duration_ms is None           # nobody asked: no events on the stroke path
+    r = ml.stroke(ctx, tool, layer, outline, timed=True)
+    assert r.duration_ms is not None and 0.0 < r.duration_ms < 1000.0
+    tools = [ml.EditingTool(px=30.0 + 9 * k, py=50.0, shape=synth.circle_shape(6), value=5 + k) for k in range(4)]
+    res = ml.stroke_gesture(ctx, tools, layer, outline)
+    assert [x.edited_mask is None for x in res] == [True, True, True, False]   # one EditedAreaMask per context
+    assert int(res[-1].edited_mask.sum().item()) == res[-1].edited_count > 0
+
+
+def test_rasterize_discarded_triangle_does_not_hide_a_kept_one():
+    """A texel covered by a kept triangle and by a LATER discarded triangle holds the kept triangle's value,
+    and the written count includes it."""
+    pool = ml.TexturePool()
+    big = np.array([[[0.0, 0.0], [8.0, 0.0], [0.0, 8.0]]])                     # covers the lower-left half
+    later = np.array([[[0.0, 0.0], [4.0, 0.0], [0.0, 4.0]]])                   # inside it, submitted later
+    tri = np.concatenate([big, later])
+    a = pool.acquire(8, 8, "uint8")
+    n_all = ml.rasterize(tri, [a], [np.array([3, 9])])
+    got_all = a.tensor.cpu().numpy().copy()
+    assert (got_all == 9).sum() > 0 and (got_all == 3).sum() > 0               # last submission wins on the overlap
+    b = pool.acquire(8, 8, "uint8")
+    n_kept = ml.rasterize(tri, [b], [np.array([3, 9])], keep=[True, False])
+    c = pool.acquire(8, 8, "uint8")
+    n_big = ml.rasterize(big, [c], [3])
+    assert n_kept == n_big == n_all
+    assert np.array_equal(b.tensor.cpu().numpy(), c.tensor.cpu().numpy())     # the discarded triangle left no hole
+
+
 def test_rasterize_known_answers():
     """rule "always keep, write 7" fills exactly the covered centres; "always
     discard" writes nothing; two overlapping triangles writing 1 then 2 leave 2 on the overlap; targets

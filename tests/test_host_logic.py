@@ -154,6 +154,33 @@ def test_camera_generation_follows_every_change():                              
     assert cam.generation == g0 + 3 and cam.state_key() != k1                         # different key
 
 
+def test_triangles_crossing_the_eye_plane_still_occlude():                       # SPEC occlusion safety
+    """A triangle with a vertex BEHIND the camera is clipped to w >= eps_w for the depth pass instead of being
+    dropped: its visible part must hide the wall behind it.  (Oracle depth pass; host preparation only.)"""
+    from oracle import kn
+    from paper_2501_14807_b200.mesh_core import TriangleMesh, window_triangles, _clip_eye_plane
+    cam = synth.default_camera(64, 64, eye=(0.0, 0.0, 0.0), target=(0.0, 0.0, -1.0), fovy=60.0, near=0.1, far=10.0)
+    wall = np.array([[-4, -4, -3], [4, -4, -3], [4, 4, -3], [-4, 4, -3]], float)
+    blade = np.array([[-3, -3, -2], [3, -3, -2], [0, 4, 1]], float)               # third vertex behind the eye
+    verts = np.concatenate([wall, blade])
+    tris = np.array([[0, 1, 2], [0, 2, 3], [4, 5, 6]])
+    mesh = TriangleMesh(vertices=verts, normals=None, uvs=np.zeros((7, 2)), triangles=tris)
+    xy, zn = window_triangles(mesh, cam)
+    assert xy.shape[0] == 2 + 2 and np.isfinite(xy).all() and np.isfinite(zn).all()   # blade: two inside vertices -> 2 triangles
+    depth = np.ones((64, 64), np.float32)
+    kn.raster_depth(xy, zn, depth)
+    only_wall = np.ones((64, 64), np.float32)
+    kn.raster_depth(xy[:2], zn[:2], only_wall)
+    assert depth[20, 32] < only_wall[20, 32] < 1.0                                   # the blade is nearer than the wall there
+    assert (depth <= only_wall).all()
+    # clipping keeps the winding and stays on the visible side
+    clip = cam.clip_coords(mesh.vertices)[mesh.triangles][2:3]
+    parts = _clip_eye_plane(clip, 1e-9)
+    assert (parts[..., 3] >= 0.999e-9).all()
+    sign = lambda t: np.sign(np.linalg.det(np.stack([t[:, 0] / t[:, 3], t[:, 1] / t[:, 3], np.ones(3)], axis=1)))
+    assert all(sign(t) == sign(parts[0]) for t in parts)
+
+
 def test_mesh_surface_area_known_answers():                                     # SPEC.md:78-80
     tri = ml.TriangleMesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0.0]]), None, np.zeros((3, 2)), np.array([[0, 1, 2]]))
     assert ml.mesh_surface_area(tri) == 0.5
