@@ -12,6 +12,14 @@ int ml_fail_cuda(cudaError_t e, const char* what);
         if (_e != cudaSuccess) return ml_fail_cuda(_e, #call);   \
     } while (0)
 
+// Row-slab triangle list (raster.cu): list[0 .. *count) = indices of the triangles whose conservative raster row
+// range meets [row0, row0 + rows), any order.  list: ntri ints, count: one zeroed u64 (both device).  For row-sharded
+// atlases: every later per-triangle pass of a rank walks the list instead of all triangles.
+int ml_slab_triangle_list(const void* tri_xy, int tri_dtype, long long ntri, long long row0, long long rows,
+                          int* list, unsigned long long* count, cudaStream_t st);
+// slabs of at most this fraction of the atlas height use the list
+inline bool ml_slab_uses_list(long long rows, long long height, long long ntri) { return rows * 2 <= height && ntri >= 4096; }
+
 #ifdef __CUDACC__
 #include "common.cuh"
 inline TeaParams ml_make_tea_params(const ml_tea_params* tp) {

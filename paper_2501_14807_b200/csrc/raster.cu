@@ -196,11 +196,15 @@ template <typename T, typename F, bool SPANS>
 __global__ void __launch_bounds__(BLOCK)
 raster_warp_kernel(const T* __restrict__ tri_xy, long long ntri, long long width, long long height,
                    long long row0, long long rows, F f, LargeList ll,
-                   unsigned long long* counters) {
+                   unsigned long long* counters, const int* __restrict__ slab_list,
+                   const unsigned long long* __restrict__ slab_count) {
     const int lane = threadIdx.x & 31;
     const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
     long long c0 = 0, c1 = 0;
-    for (long long t = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); t < ntri; t += nwarps) {
+    // row slabs: walk the slab's triangle list (ml_slab_triangle_list) instead of every triangle of the mesh
+    const long long nwork = slab_list ? (long long)*slab_count : ntri;
+    for (long long k = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5); k < nwork; k += nwarps) {
+        const long long t = slab_list ? (long long)slab_list[k] : k;
         TriSetup s;
         if (!tri_load_ccw(tri_xy + 6 * t, s)) continue;
         if (!tri_bbox(s, width, height, row0, rows)) continue;
@@ -349,6 +353,46 @@ owner_values_kernel(const int* __restrict__ tri_id, long long n, const E* __rest
     block_count_add(cnt, written);
 }
 
+// Row-slab triangle list: one thread per triangle, the reference's own conservative row range
+// floor(ymin - 0.5) .. ceil(ymax) (KN:54-57; tri_bbox never looks outside it), ballot-compacted.
+template <typename T>
+__global__ void __launch_bounds__(BLOCK)
+slab_list_kernel(const T* __restrict__ tri_xy, long long ntri, long long row0, long long rows,
+                 int* __restrict__ list, unsigned long long* count) {
+    const int lane = threadIdx.x & 31;
+    for (long long t0 = (long long)blockIdx.x * BLOCK; t0 < ntri; t0 += (long long)gridDim.x * BLOCK) {
+        const long long t = t0 + threadIdx.x;
+        bool keep = false;
+        if (t < ntri) {
+            const double y0 = (double)tri_xy[6 * t + 1], y1 = (double)tri_xy[6 * t + 3], y2 = (double)tri_xy[6 * t + 5];
+            const double lo = floor(fmin(fmin(y0, y1), y2) - 0.5), hi = ceil(fmax(fmax(y0, y1), y2));
+            keep = hi >= (double)row0 && lo <= (double)(row0 + rows - 1);      // false for NaN rows: such triangles are skipped anyway
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (!bal) continue;
+        unsigned long long slot = 0;
+        if (lane == 0) slot = atomicAdd(count, (unsigned long long)__popc(bal));
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (keep) list[slot + __popc(bal & ((1u << lane) - 1u))] = (int)t;
+    }
+}
+
+}  // namespace
+
+int ml_slab_triangle_list(const void* tri_xy, int tri_dtype, long long ntri, long long row0, long long rows,
+                          int* list, unsigned long long* count, cudaStream_t st) {
+    if (ntri <= 0) return ML_OK;
+    long long blocks = (ntri + BLOCK - 1) / BLOCK;
+    const long long cap = (long long)ml_sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    if (tri_dtype == ML_F32) slab_list_kernel<float><<<(unsigned)blocks, BLOCK, 0, st>>>((const float*)tri_xy, ntri, row0, rows, list, count);
+    else slab_list_kernel<double><<<(unsigned)blocks, BLOCK, 0, st>>>((const double*)tri_xy, ntri, row0, rows, list, count);
+    ML_CUDA(cudaGetLastError());
+    return ML_OK;
+}
+
+namespace {
+
 template <typename T, typename F>
 int raster_launch(const T* tri_xy, long long ntri, long long width, long long height,
                   long long row0, long long rows, const F& f, void* workspace, size_t ws_bytes,
@@ -356,22 +400,30 @@ int raster_launch(const T* tri_xy, long long ntri, long long width, long long he
     if (ntri <= 0 || rows <= 0 || width <= 0) return ML_OK;
     if (ntri > 0x7fffffffLL) return ml_fail(ML_ERR_ARG, "more than 2^31-1 triangles");
     if (ws_bytes < ml_raster_workspace_bytes(ntri)) return ml_fail(ML_ERR_ARG, "raster workspace too small");
-    // workspace layout: [count, total, c0, c1] u64 | off[ntri+1] u64 | tri[ntri] i32
+    // workspace layout: [count, total, c0, c1, slab count, -] u64 | off[ntri+1] u64 | tri[ntri] i32 | TEA flags | slab list[ntri] i32
     unsigned long long* head = (unsigned long long*)workspace;
     LargeList ll;
     ll.count = head; ll.total = head + 1;
-    ll.off = head + 4;
+    ll.off = head + 6;
     ll.tri = (int*)(ll.off + ntri + 1);
     unsigned long long* ctr = counters ? counters : head + 2;
-    ML_CUDA(cudaMemsetAsync(head, 0, 4 * sizeof(unsigned long long), st));
+    ML_CUDA(cudaMemsetAsync(head, 0, 6 * sizeof(unsigned long long), st));
+    const int* slab_list = nullptr;
+    const unsigned long long* slab_count = nullptr;
+    if (ml_slab_uses_list(rows, height, ntri)) {
+        int* list = (int*)((char*)workspace + ml_raster_workspace_bytes(ntri) - (size_t)ntri * sizeof(int) - 16);
+        const int rc = ml_slab_triangle_list(tri_xy, sizeof(T) == 4 ? ML_F32 : ML_F64, ntri, row0, rows, list, head + 4, st);
+        if (rc != ML_OK) return rc;
+        slab_list = list; slab_count = head + 4;
+    }
     const long long warps_per_block = BLOCK / 32;
     long long blocks = (ntri + warps_per_block - 1) / warps_per_block;
     const long long cap = (long long)ml_sm_count() * 64;
     if (blocks > cap) blocks = cap;
     if ((double)width * (double)rows >= 40.0 * (double)ntri)          // >= ~40 texels per triangle: row spans pay off
-        raster_warp_kernel<T, F, true><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr);
+        raster_warp_kernel<T, F, true><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr, slab_list, slab_count);
     else
-        raster_warp_kernel<T, F, false><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr);
+        raster_warp_kernel<T, F, false><<<(unsigned)blocks, BLOCK, 0, st>>>(tri_xy, ntri, width, height, row0, rows, f, ll, ctr, slab_list, slab_count);
     scan_kernel<<<1, 1024, 0, st>>>(ll);
     raster_chunk_kernel<T, F><<<(unsigned)(ml_sm_count() * 8), BLOCK, 0, st>>>(tri_xy, width, height, row0, rows, f, ll, ctr);
     ML_CUDA(cudaGetLastError());
@@ -384,8 +436,10 @@ extern "C" {
 
 size_t ml_raster_workspace_bytes(int64_t ntri) {
     if (ntri < 0) ntri = 0;
-    return 4 * sizeof(unsigned long long) + (size_t)(ntri + 1) * sizeof(unsigned long long) +
-           (size_t)ntri * sizeof(int) + (size_t)((ntri + 31) / 32) * sizeof(uint32_t) + 64;   // + TEA triangle flags
+    size_t b = 6 * sizeof(unsigned long long) + (size_t)(ntri + 1) * sizeof(unsigned long long) +
+               (size_t)ntri * sizeof(int) + (size_t)((ntri + 31) / 32) * sizeof(uint32_t) + 64;   // + TEA triangle flags
+    b = (b + 15) & ~(size_t)15;
+    return b + (size_t)ntri * sizeof(int) + 16;                                                  // + row-slab triangle list (last)
 }
 
 int ml_coverage_fill(const void* tri_xy, int tri_dtype, int64_t ntri, int64_t width, int64_t height,
@@ -461,7 +515,7 @@ int ml_raster_tea(const void* tri_xy, const void* tri_clip, int tri_dtype, int64
     // rasterised and counted, so planes and both counts are unchanged
     uint32_t* flags = nullptr;
     if (ntri > 0 && workspace && workspace_bytes >= ml_raster_workspace_bytes(ntri) && (tri_dtype == ML_F32 || tri_dtype == ML_F64)) {
-        flags = (uint32_t*)((char*)workspace + 4 * sizeof(unsigned long long) + (size_t)(ntri + 1) * sizeof(unsigned long long) +
+        flags = (uint32_t*)((char*)workspace + 6 * sizeof(unsigned long long) + (size_t)(ntri + 1) * sizeof(unsigned long long) +
                             (size_t)ntri * sizeof(int));
         const int rc = ml_tea_classify(tri_clip, tri_dtype, ntri, tp, flags, nullptr, width, height, row0, rows, nullptr, stream);
         if (rc != ML_OK) return rc;

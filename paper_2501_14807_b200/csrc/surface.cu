@@ -46,9 +46,12 @@ static_assert(sizeof(TriRec) == 208, "TriRec is thirteen 16-byte words");
 template <typename T>
 __global__ void __launch_bounds__(BLOCK)
 tri_prepare_kernel(const T* __restrict__ tri_xy, const T* __restrict__ tri_pos, const T* __restrict__ tri_nrm,
-                   long long ntri, TriRec* __restrict__ recs) {
-    const long long t = (long long)blockIdx.x * BLOCK + threadIdx.x;
-    if (t >= ntri) return;
+                   long long ntri, TriRec* __restrict__ recs, const int* __restrict__ slab_list,
+                   const unsigned long long* __restrict__ slab_count) {
+    // row slabs: only the triangles of the slab's list can own a texel of the slab, only their records are needed
+    const long long k = (long long)blockIdx.x * BLOCK + threadIdx.x;
+    if (k >= (slab_list ? (long long)*slab_count : ntri)) return;
+    const long long t = slab_list ? (long long)slab_list[k] : k;
     TriSetup s;
     TriRec& r = recs[t];
     if (!tri_load_ccw(tri_xy + 6 * t, s)) {       // degenerate / non-finite: never owns a texel
@@ -898,7 +901,9 @@ int launch_tea_texels(const T* tri_xy, const T* tri_clip, const TeaRec* recs, lo
 
 extern "C" {
 
-size_t ml_surface_workspace_bytes(int64_t ntri) { return (size_t)(ntri > 0 ? ntri : 0) * sizeof(TriRec) + 64; }
+size_t ml_surface_workspace_bytes(int64_t ntri) {          // records | slab count | slab list
+    return (size_t)(ntri > 0 ? ntri : 0) * (sizeof(TriRec) + sizeof(int)) + 64;
+}
 
 int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_nrm, int tri_dtype,
                        int64_t ntri, int64_t width, int64_t row0, int64_t rows,
@@ -915,10 +920,23 @@ int ml_surface_resolve(const void* tri_xy, const void* tri_pos, const void* tri_
     const bool small = n <= 0xffffffffLL && width <= 0xffffffffLL;
     const unsigned pgrid = (unsigned)((ntri + BLOCK - 1) / BLOCK);
     if (ntri > 0) {
+        const int* slab_list = nullptr;
+        const unsigned long long* slab_count = nullptr;
+        // the caller's slab geometry is (row0, rows) only; a slab is recognised by the list paying off: rows of the
+        // slab against the rows the triangles span is unknown here, so the list is built whenever the mesh is large
+        // (0.1 ms per 10 M triangles) and the records of the listed triangles alone are written
+        if (ntri >= 4096) {
+            unsigned long long* cnt = (unsigned long long*)((char*)workspace + (size_t)ntri * sizeof(TriRec));
+            int* list = (int*)(cnt + 2);
+            ML_CUDA(cudaMemsetAsync(cnt, 0, 16, st));
+            const int rc = ml_slab_triangle_list(tri_xy, tri_dtype, ntri, row0, rows, list, cnt, st);
+            if (rc != ML_OK) return rc;
+            slab_list = list; slab_count = cnt;
+        }
         if (tri_dtype == ML_F32)
-            tri_prepare_kernel<float><<<pgrid, BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_pos, (const float*)tri_nrm, ntri, recs);
+            tri_prepare_kernel<float><<<pgrid, BLOCK, 0, st>>>((const float*)tri_xy, (const float*)tri_pos, (const float*)tri_nrm, ntri, recs, slab_list, slab_count);
         else
-            tri_prepare_kernel<double><<<pgrid, BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_pos, (const double*)tri_nrm, ntri, recs);
+            tri_prepare_kernel<double><<<pgrid, BLOCK, 0, st>>>((const double*)tri_xy, (const double*)tri_pos, (const double*)tri_nrm, ntri, recs, slab_list, slab_count);
     }
     if (small) resolve_kernel<true><<<grid_for(n), BLOCK, 0, st>>>(recs, width, row0, n, tri_id, pos, nrm, area, ctr);
     else resolve_kernel<false><<<grid_for(n), BLOCK, 0, st>>>(recs, width, row0, n, tri_id, pos, nrm, area, ctr);
