@@ -712,6 +712,18 @@ def run_ours(args):
             stream_kernels[st] = {"ms": round(ms, 4), "gb_s": round(b / ms / 1e6, 1), "frac_of_peak": round(b / ms / 1e6 / peak, 4),
                                   "timed": "cuda graph of 10 calls" if graphed else "eager back-to-back calls"}
 
+        if "tea" in stages:
+            # the id stream of the whole-atlas TEA stage alone: a tool far outside the window flags no triangle, so the
+            # stage is classification + id stream with the edited reset + an empty evaluation launch (5 B/texel); the
+            # difference to "tea" above is the float64 evaluation of the 70 px tool's footprint
+            off_tool = ml.EditingTool(px=-1.0e6, py=-1.0e6, shape=arm.tool_shape_dev, value=7)
+            ms, graphed = time_graph(lambda: arm.stage("tea", inp, off_tool, scratch_row, False), inner=10, reps=5)
+            b = wl.algorithmic_bytes(n, "tea", T, 0)
+            stream_kernels["tea_id_stream_only"] = {"ms": round(ms, 4), "gb_s": round(b / ms / 1e6, 1),
+                                                    "frac_of_peak": round(b / ms / 1e6 / peak, 4),
+                                                    "timed": "cuda graph of 10 calls" if graphed else "eager back-to-back calls",
+                                                    "note": "tool outside the window: no triangle flagged, nothing to evaluate"}
+
     # ---- parity (untimed) + cpu_baseline
     parity, cpu = None, None
     if rank == 0 and world_size == 1 and not args.no_cpu:

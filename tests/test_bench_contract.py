@@ -67,7 +67,7 @@ def test_gpu_arm_json_contract(extra):
     assert d["gpu_launches"] == per_step * 3
     assert set(d["config"]["stage_results"]) == {"tea", "tpa", "sphere", "batch", "chain", "mask_op", "threshold", "area"}
     assert d["config"]["footprint_culling"] == (not extra)
-    assert set(d["config"]["stream_kernels"]) == set(d["config"]["stage_results"])
+    assert set(d["config"]["stream_kernels"]) == set(d["config"]["stage_results"]) | {"tea_id_stream_only"}
     assert set(d["config"]["stage_results_streamed"]) == set(d["config"]["stage_results"])
     assert d["value_streamed"] > 0 and d["ms_per_step_streamed"] > 0
     assert ro["streamed"]["bound"] == "hbm" and ro["streamed"]["kernel"] in d["config"]["stage_results"]
