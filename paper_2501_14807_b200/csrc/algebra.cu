@@ -186,7 +186,10 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
 #pragma unroll
             for (int k = 0; k < GL; ++k) if (k < a.nlayers) mn[k] = ld_stream_rw((const uint4*)a.mask[k] + v + nthreads);
         }
-        // dry run of the mask fold: which layers' data can reach the result of this vector?
+        // Pass 1 -- the mask fold alone (the masks are normalised to 0x00 / 0xff byte flags in place, so pass 2
+        // does not repeat that): final mask `sim`, and which layers' data can reach the result of this vector
+        // (the first operand where its mask is set, a union operand where it fills texels the accumulator does
+        // not hold; intersection / difference / masking operands never).
         unsigned need = 0;
         uint32_t sim[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -197,6 +200,7 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
                     const uint32_t bff = nz_bytes(((const uint32_t*)&m[k])[g]);
+                    ((uint32_t*)&m[k])[g] = bff;
                     if (k == 0) { nd |= bff != 0u; sim[g] = bff; }
                     else if (op == ML_OP_UNION) { nd |= (bff & ~sim[g]) != 0u; sim[g] |= bff; }
                     else if (op == ML_OP_DIFFERENCE) sim[g] &= ~bff;
@@ -213,32 +217,58 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
             for (int k = 0; k < GL; ++k)
                 d1[k] = ((need >> k) & 1u) ? ld_stream_rw((const uint4*)a.data[k] + v) : make_uint4(0u, 0u, 0u, 0u);
         }
+        // Pass 2 -- the data fold, restricted to the layers of `need`.  A layer outside `need` changes the
+        // accumulator's data only by clearing texels it removes from the mask; that clearing is deferred: a
+        // needed union masks the accumulator with the mask it has at that point (combine(): keep_a = acc.ff)
+        // before it fills, and the result is masked with the FINAL mask once at the end -- the same bytes as
+        // folding every layer, for a cost proportional to the layers that matter (usually one).
         Group<ESIZE> acc[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            acc[g].ff = 0u;
+#pragma unroll
+            for (int j = 0; j < ESIZE; ++j) acc[g].d[j] = 0u;
+        }
 #pragma unroll
         for (int k = 0; k < GL; ++k) {
             if (k < a.nlayers) {
                 const int op = a.ops[k];
+                const bool needed = (need >> k) & 1u;
                 uint4 dk[ESIZE];
-                if (ESIZE == 1) dk[0] = d1[k];
-                else {
+                if (needed) {
+                    if (ESIZE == 1) dk[0] = d1[k];
+                    else {
 #pragma unroll
-                    for (int j = 0; j < ESIZE; ++j)
-                        dk[j] = ((need >> k) & 1u) ? ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j) : make_uint4(0u, 0u, 0u, 0u);
+                        for (int j = 0; j < ESIZE; ++j) dk[j] = ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j);
+                    }
                 }
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    Group<ESIZE> b;
-                    b.ff = nz_bytes(((const uint32_t*)&m[k])[g]);
-#pragma unroll
-                    for (int j = 0; j < ESIZE; ++j) b.d[j] = ((const uint32_t*)&dk[0])[g * ESIZE + j];
+                    const uint32_t bff = ((const uint32_t*)&m[k])[g];
                     if (k == 0) {
-                        acc[g].ff = b.ff;
+                        acc[g].ff = bff;
+                        if (needed) {
 #pragma unroll
-                        for (int j = 0; j < ESIZE; ++j) acc[g].d[j] = b.d[j] & expand<ESIZE>(b.ff, j);
-                    } else combine<ESIZE>(op, acc[g], b);
+                            for (int j = 0; j < ESIZE; ++j) acc[g].d[j] = ((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(bff, j);
+                        }
+                    } else if (op == ML_OP_UNION) {
+                        if (needed) {
+                            const uint32_t keep_a = acc[g].ff, take_b = bff & ~acc[g].ff;
+#pragma unroll
+                            for (int j = 0; j < ESIZE; ++j)
+                                acc[g].d[j] = (acc[g].d[j] & expand<ESIZE>(keep_a, j)) |
+                                              (((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(take_b, j));
+                        }
+                        acc[g].ff |= bff;
+                    } else if (op == ML_OP_DIFFERENCE) acc[g].ff &= ~bff;
+                    else acc[g].ff &= bff;
                 }
             }
         }
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+            for (int j = 0; j < ESIZE; ++j) acc[g].d[j] &= expand<ESIZE>(acc[g].ff, j);
         st_stream((uint4*)mc + v, make_uint4(acc[0].ff & 0x01010101u, acc[1].ff & 0x01010101u, acc[2].ff & 0x01010101u,
                                               acc[3].ff & 0x01010101u));
         uint4 od[ESIZE];
