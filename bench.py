@@ -455,7 +455,7 @@ class GpuArm:
             tiles = self.ctx.stroke_tiles if cull else None
             if self.ws > 1:
                 ml.editing.pad_slab(self.outline, self.ctx.edited, 1, layers[0].data, layers[0].mask, tool.value, row[a:b],
-                                    row0=self.row0, height=wl.height, tiles=tiles)
+                                    row0=self.row0, height=wl.height, tiles=tiles, ext=self.ctx.edited_ext)
             else:
                 nat.apply_padding(self.outline, self.ctx.edited, 1, layers[0].data, layers[0].mask, tool.value,
                                   counts=row[a:b], tiles=tiles)

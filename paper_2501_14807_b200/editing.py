@@ -125,12 +125,22 @@ class StrokeContext:
     (grid units), clip coordinates MVP*vertex per triangle, the depth map, the surface map and a
     per-stroke ``edited`` plane (SPEC.md:253-255 EditedAreaMask, reset before each stroke)."""
 
+    HALO_ROWS = 4                       # spare rows of a slab's edited plane = the largest padding radius of the culled path
+
     def __init__(self, mesh, camera, depth, surface, device="cuda"):
         torch = _native.require_cuda()
         self.mesh, self.camera, self.depth, self.surface = mesh, camera, depth, surface
         self.device = device
         self.tri_xy = surface.tri_xy
-        self.edited = torch.zeros((surface.rows, surface.width), dtype=torch.uint8, device=device)
+        # EditedAreaMask plane.  On a row slab of a taller atlas it carries HALO_ROWS spare rows above and below:
+        # the neighbours' border rows of a stroke are received straight into them (sharding.exchange_halo_into)
+        self.edited_ext = None
+        if surface.rows != surface.height:
+            self.edited_ext = (torch.zeros((surface.rows + 2 * self.HALO_ROWS, surface.width), dtype=torch.uint8, device=device),
+                               self.HALO_ROWS)
+            self.edited = self.edited_ext[0][self.HALO_ROWS:self.HALO_ROWS + surface.rows]
+        else:
+            self.edited = torch.zeros((surface.rows, surface.width), dtype=torch.uint8, device=device)
         self.scratch = _native.tea_scratch(mesh.num_triangles, surface.rows * surface.width, device)
         self._cstruct = None              # (outline data_ptr, ml_stroke_ctx) of the one-call stroke path
         self.refresh_camera()
@@ -281,12 +291,12 @@ def _stroke(ctx, tool, layer, outline, *, eps=DEFAULT_DEPTH_BIAS, cull=True, hal
                                   tiles=ctx.stroke_tiles if cull else None)
         else:
             pad_slab(as_u8, ctx.edited, radius, layer.data, layer.mask, tool.value, pc, row0=s.row0, height=s.height,
-                     tiles=ctx.stroke_tiles if cull else None, halo=halo)
+                     tiles=ctx.stroke_tiles if cull else None, halo=halo, ext=ctx.edited_ext)
         res._padded = pc
     return res
 
 
-def pad_slab(outline, edited, radius, data, mask, value, counts, *, row0, height, tiles=None, halo=None):
+def pad_slab(outline, edited, radius, data, mask, value, counts, *, row0, height, tiles=None, halo=None, ext=None):
     """TPA on one row slab of a taller atlas.  The ``radius`` rows next to a slab border need the
     neighbour's ``edited`` rows: they are exchanged point-to-point (``sharding.exchange_halo``, 16 KB per
     neighbour at 16384 texels; ``halo`` replaces the exchange in single-process tests and returns either
@@ -296,6 +306,30 @@ def pad_slab(outline, edited, radius, data, mask, value, counts, *, row0, height
     the passes, so planes and count equal the whole-plane result."""
     torch = _native._torch()
     rows, w = edited.shape
+    if halo is None and ext is not None and radius <= ext[1]:
+        # ``ext = (buf, margin)``: `edited` is buf[margin:margin + rows]; the halo rows land in buf's spare rows and
+        # every window below is a VIEW of buf -- no concatenation, no allocation on the stroke path
+        from . import sharding
+        buf, margin = ext
+        up_n, dn_n = sharding.exchange_halo_into(buf, margin, rows, row0, height, radius)
+        top = min(radius, rows) if up_n else 0
+        bot = min(radius, rows - top) if dn_n else 0
+        culled = (tiles is not None and w % 128 == 0 and 0 < radius <= 4 and rows >= 2 * radius
+                  and all(t.data_ptr() % 16 == 0 for t in (outline, edited, data, mask)))
+        if not culled:
+            _native.apply_padding(outline, buf[margin - up_n:margin + rows + dn_n], radius, data, mask, value, counts=counts,
+                                  in_row0=row0 - up_n, out_row0=row0)
+            return
+        _native.apply_padding(outline, edited, radius, data, mask, value, counts=counts, tiles=tiles,
+                              row_range=(top, rows - bot))
+        if top:      # output rows [0, top): stencil rows [-radius, top + radius)
+            _native.apply_padding(outline[:top], buf[margin - up_n:margin + min(rows, top + radius)], radius, data[:top],
+                                  mask[:top], value, counts=counts, in_row0=row0 - up_n, out_row0=row0)
+        if bot:      # output rows [rows - bot, rows)
+            lo = max(0, rows - bot - radius)
+            _native.apply_padding(outline[rows - bot:], buf[margin + lo:margin + rows + dn_n], radius, data[rows - bot:],
+                                  mask[rows - bot:], value, counts=counts, in_row0=row0 + lo, out_row0=row0 + rows - bot)
+        return
     if halo is None:
         from . import sharding
         up, dn = sharding.exchange_halo(edited, row0, height, radius, parts=True)

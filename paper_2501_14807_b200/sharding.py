@@ -191,3 +191,42 @@ def exchange_halo(plane, row0, height, radius, parts=False):
         return up, dn
     pieces = [p for p in (up, plane, dn) if p is not None]
     return torch.cat(pieces, dim=0), row0 - (up.shape[0] if up is not None else 0)
+
+
+def exchange_halo_into(buf, margin, rows, row0, height, radius):
+    """Per-stroke form of ``exchange_halo``: ``buf`` is a rank's byte plane allocated with ``margin`` spare rows above
+    and below its ``rows`` slab rows (the slab is ``buf[margin:margin + rows]``); the neighbours' ``radius`` border rows
+    are received STRAIGHT INTO those spare rows (no concatenation, no allocation: round 1 built two ``torch.cat``
+    windows per stroke).  Returns ``(up_n, dn_n)``, the rows now valid above / below the slab."""
+    import torch
+    dist = _dist()
+    rank, ws = world()
+    if ws == 1 or radius <= 0:
+        return 0, 0
+    if radius > margin:
+        raise ValueError("halo radius exceeds the plane's spare rows")
+    up_n = min(radius, row0)
+    dn_n = min(radius, height - (row0 + rows))
+    slab = buf[margin:margin + rows]
+    direct = dist.get_backend() == "nccl" or not buf.is_cuda
+    ops, stage_up, stage_dn = [], None, None
+    if rank > 0:
+        dst = buf[margin - up_n:margin]
+        stage_up = dst if direct else torch.empty(dst.shape, dtype=dst.dtype)
+        ops.append(dist.P2POp(dist.irecv, stage_up, rank - 1))
+        src = slab[:min(radius, rows)]
+        ops.append(dist.P2POp(dist.isend, src if direct else src.cpu(), rank - 1))
+    if rank < ws - 1:
+        dst = buf[margin + rows:margin + rows + dn_n]
+        stage_dn = dst if direct else torch.empty(dst.shape, dtype=dst.dtype)
+        ops.append(dist.P2POp(dist.irecv, stage_dn, rank + 1))
+        src = slab[max(0, rows - radius):]
+        ops.append(dist.P2POp(dist.isend, src if direct else src.cpu(), rank + 1))
+    for r in dist.batch_isend_irecv(ops):
+        r.wait()
+    if not direct:                      # gloo with device planes (single-GPU rehearsal): staged through the host
+        if stage_up is not None:
+            buf[margin - up_n:margin].copy_(stage_up)
+        if stage_dn is not None:
+            buf[margin + rows:margin + rows + dn_n].copy_(stage_dn)
+    return (up_n if rank > 0 else 0), (dn_n if rank < ws - 1 else 0)

@@ -81,6 +81,14 @@ def _worker(rank, world_size, port, out_dir):
             assert torch.equal(up, ext[:k])
         if dn is not None:
             assert torch.equal(dn, ext[k + rows:])
+        # the stroke-path form: the halo rows land in the spare rows of the rank's own plane (no concatenation)
+        margin = 4
+        buf = torch.zeros((rows + 2 * margin, A), dtype=torch.uint8)
+        buf[margin:margin + rows] = cov
+        up_n, dn_n = sharding.exchange_halo_into(buf, margin, rows, r0, A, 2)
+        assert (up_n, dn_n) == (0 if up is None else up.shape[0], 0 if dn is None else dn.shape[0])
+        assert torch.equal(buf[margin - up_n:margin + rows + dn_n], ext)
+        assert not bool(buf[:margin - up_n].any()) and not bool(buf[margin + rows + dn_n:].any())
         np.savez(os.path.join(out_dir, "rank%d.npz" % rank), data0=data[0], data1=data[1], mask0=mask[0], mask1=mask[1],
                  sums=sums.numpy(), texels=texels.numpy(), counts=counts.numpy(), ext=ext.numpy(), ext_row0=ext_row0,
                  r0=r0, rows=rows)
@@ -175,6 +183,18 @@ def _pad_worker(rank, world_size, port, out_dir):
                          radius, data, mask, 7, counts, row0=r0, height=H, tiles=torch.zeros(1, dtype=torch.int32))
         # the decomposition under test really ran: one interior pass + one border pass per neighbour
         assert _CALLS.count("interior") == 1 and _CALLS.count("border") == (rank > 0) + (rank < world_size - 1), _CALLS
+        # same stroke through the allocation-free form: the edited plane carries spare rows, the halo lands in them
+        margin = 4
+        buf = torch.zeros((rows + 2 * margin, W), dtype=torch.uint8)
+        buf[margin:margin + rows] = torch.from_numpy(edited[r0:r0 + rows].copy())
+        data2 = torch.zeros((rows, W), dtype=torch.uint8)
+        mask2 = torch.zeros((rows, W), dtype=torch.uint8)
+        counts2 = torch.zeros(1, dtype=torch.int64)
+        del _CALLS[:]
+        editing.pad_slab(torch.from_numpy(outline[r0:r0 + rows].copy()), buf[margin:margin + rows], radius, data2, mask2, 7,
+                         counts2, row0=r0, height=H, tiles=torch.zeros(1, dtype=torch.int32), ext=(buf, margin))
+        assert _CALLS.count("interior") == 1 and _CALLS.count("border") == (rank > 0) + (rank < world_size - 1), _CALLS
+        assert torch.equal(data2, data) and torch.equal(mask2, mask) and int(counts2) == int(counts)
         sharding.allreduce_counts(counts)
         np.savez(os.path.join(out_dir, "pad%d.npz" % rank), data=data.numpy(), mask=mask.numpy(), count=counts.numpy(),
                  outline=outline, edited=edited)
