@@ -46,8 +46,9 @@ Inputs are far larger than the 126 MB L2 (every plane is >= 268 MB), so no expli
 needed between iterations.
 
 Multi-GPU (torchrun, one rank per GPU): weak scaling -- the atlas grows to 16384 x (16384*N) and
-each rank owns one 16384-row slab; the only collectives are the stroke-table broadcast and the
-cross-rank area sum (one all-gather of 16 L bytes).  ``--config c5`` is BASELINE config 5: a
+each rank owns one 16384-row slab; the only exchanges are the stroke-table broadcast, the TPA halo rows and
+the cross-rank area sum, which is fused into the reduction kernel (system-scope atomics into every rank's
+result row over IPC-mapped peer memory; ``ML_AREA_REDUCE=gather`` = one all-gather of 16 L bytes instead).  ``--config c5`` is BASELINE config 5: a
 32768^2 atlas with the 9,999,392-triangle heightfield, STRONG scaling (the rows are split over the
 ranks), stages batch (64 strokes) + area.
 
@@ -403,7 +404,27 @@ class GpuArm:
         self.attr = self.surf.pos[2]
         self.attr_tiles = nat.attr_tiles(self.attr)     # per-tile height ranges for the culled threshold selection
         self.tool_shape_dev = nat._as_dev_bytes(wl.tool_shape, dev)
+        # cross-rank area sum: fused into the reduction kernel over peer memory (sharding.PeerAreaReducer: system-scope
+        # atomics into every rank's row, no collective call); ML_AREA_REDUCE=gather, or a node without CUDA IPC, uses
+        # the one-all-gather form (sharding.AreaReducer)
         self.area_reduce = sharding.AreaReducer(L, dev)
+        self.peer_areas, self.area_step = None, 0
+        self.area_reduce_kind = "none (1 rank)" if world_size == 1 else "all-gather"
+        if world_size > 1 and os.environ.get("ML_AREA_REDUCE", "peer") == "peer":
+            ok = torch.zeros(1, dtype=torch.int64)
+            try:
+                self.peer_areas = sharding.PeerAreaReducer(L, dev)
+                ok[0] = 1
+            except Exception as exc:                         # e.g. IPC not permitted in this container
+                sys.stderr.write("peer area reduction unavailable (%s); using the all-gather form\n" % exc)
+            import torch.distributed as dist
+            if dist.get_backend() == "nccl":
+                ok = ok.to(dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)         # all ranks or none
+            if int(ok.item()) == 1:
+                self.area_reduce_kind = "fused: system-scope atomics into every rank's row over peer memory"
+            else:
+                self.peer_areas = None
         self.T = wl.mesh.num_triangles
         self.seed()
         torch.cuda.synchronize()
@@ -479,9 +500,13 @@ class GpuArm:
             ml.select_threshold(self.attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L],
                                 tiles=self.attr_tiles if cull else None, counts=row[a:b])
         elif st == "area":
-            nat.layer_area(self.surf.area, [l.mask for l in layers], sums=row[a:a + L].view(self.torch.float64),
-                           counts=row[a + L:b])
-            self.area_reduce(row[a:b])
+            if self.peer_areas is not None:
+                self.peer_areas.reduce(self.area_step, self.surf.area, [l.mask for l in layers], row[a:b])
+                self.area_step += 1
+            else:
+                nat.layer_area(self.surf.area, [l.mask for l in layers], sums=row[a:a + L].view(self.torch.float64),
+                               counts=row[a + L:b])
+                self.area_reduce(row[a:b])
 
     def hits_of(self, st, row_host):
         a, b = self.slot[st]
@@ -802,6 +827,7 @@ def run_ours(args):
         cfg["setup_s"] = round(arm.setup_s, 2)
         cfg["surface_map"] = {"covered": arm.surf.covered, "overlap": arm.surf.overlap}
         cfg["footprint_culling"] = bool(arm.culled(primary_cull))
+        cfg["area_reduce"] = arm.area_reduce_kind
         roofline = roof(tab, stage_ms, "slowest stage of the default step: SURVEY 8(d) algorithmic bytes / CUDA-event time "
                                        "(frac); dram_frac = ncu-measured DRAM bytes of the stage's kernels / the same time. "
                                        "A stage that skips bytes by design (culled brushes, lazy chain, sparse-mask area) shows "
@@ -824,8 +850,13 @@ def run_ours(args):
             "clocks": clocks_summary(samples, windows),
         }
         print(json.dumps(out))
+    if arm.peer_areas is not None:
+        arm.peer_areas.check()
     if world_size > 1:
         import torch.distributed as dist
+        dist.barrier()
+        if arm.peer_areas is not None:
+            arm.peer_areas.close()
         dist.destroy_process_group()
     if parity is not None and not parity["ok"]:
         sys.exit(3)

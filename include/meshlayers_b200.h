@@ -256,6 +256,27 @@ int ml_layer_chain(int64_t nlayers, const void* const* data, const uint8_t* cons
  * HOST array of L device pointers (L <= 64): one pass reads area once and the L masks. */
 int ml_layer_area(const float* area, const uint8_t* const* masks, int64_t L, int64_t n,
                   double* sums, uint64_t* counts, void* stream);
+
+/* ---- fused cross-rank area reduction over peer memory (row-sharded atlases) --------
+ * The reduction kernel of every rank adds its per-block partial sums / counts with SYSTEM-scope atomics into the
+ * same slots of EVERY rank's result row (NVLink peer memory mapped through CUDA IPC; own row included), so the
+ * all-reduce of the per-layer areas happens inside the compute kernel: no collective launch, no packing kernels.
+ * Row layout (8-byte slots): [L float64 sums | L uint64 counts | uint64 arrivals | uint64 spare], zeroed before use.
+ * peer_rows: HOST array of npeers device pointers (valid in THIS process) to the row of every rank for this step,
+ * own row at index `self`.  arrive_table: DEVICE array of npeers pointers to the arrival slots (row + 2L) of the
+ * same rows.  After the reduction kernels ONE thread signals every rank's arrival slot and waits until all npeers
+ * ranks have signalled this rank's row (bounded: ~10 s without progress sets *status = 1 instead of hanging);
+ * operations queued behind the call see the complete global sums in the own row.  recycle_row (may be NULL): an
+ * own row to zero afterwards for a later step.  ml_peer_*: cudaMalloc'ed, zeroed regions and their 64-byte IPC
+ * handles (torch's caching allocator cannot export allocation bases). */
+int ml_layer_area_peers(const float* area, const uint8_t* const* masks, int64_t L, int64_t n,
+                        void* const* peer_rows, int npeers, int self, void* arrive_table, uint32_t* status,
+                        void* recycle_row, void* stream);
+int ml_peer_alloc(void** ptr, size_t bytes);
+int ml_peer_free(void* ptr);
+int ml_peer_export(const void* ptr, void* handle64);
+int ml_peer_open(const void* handle64, void** ptr);
+int ml_peer_close(void* ptr);
 /* uint8 label plane: sums[v] += area over texels with mask != 0 and data == v (v < 256). */
 int ml_label_area(const float* area, const uint8_t* data, const uint8_t* mask, int64_t n,
                   double* sums /* [256] */, uint64_t* counts /* [256] */, void* stream);

@@ -119,6 +119,12 @@ def lib():
         "ml_layer_op": (i32, [i32, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
         "ml_layer_chain": (i32, [i64, vp, vp, vp, vp, vp, i32, i64, vp]),
         "ml_layer_area": (i32, [vp, vp, i64, i64, vp, vp, vp]),
+        "ml_layer_area_peers": (i32, [vp, vp, i64, i64, vp, i32, i32, vp, vp, vp, vp]),
+        "ml_peer_alloc": (i32, [C.POINTER(vp), sz]),
+        "ml_peer_free": (i32, [vp]),
+        "ml_peer_export": (i32, [vp, vp]),
+        "ml_peer_open": (i32, [vp, C.POINTER(vp)]),
+        "ml_peer_close": (i32, [vp]),
         "ml_label_area": (i32, [vp, vp, vp, i64, vp, vp, vp]),
         "ml_layer_stats": (i32, [vp, i32, vp, i64, vp, vp]),
         "ml_outline_mask": (i32, [vp, i64, i64, i64, i64, i64, i64, vp, vp]),
@@ -158,7 +164,8 @@ EXPORTED_SYMBOLS = (
     "ml_tea_classify", "ml_tea_tile_words", "ml_select_sphere", "ml_select_sphere_batch", "ml_tile_count",
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
     "ml_select_threshold", "ml_plane_tile_range", "ml_select_threshold_tiles", "ml_layer_op",
-    "ml_layer_chain", "ml_layer_area", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
+    "ml_layer_chain", "ml_layer_area", "ml_layer_area_peers", "ml_peer_alloc", "ml_peer_free", "ml_peer_export",
+    "ml_peer_open", "ml_peer_close", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_apply_padding_tiles", "ml_apply_padding_tiles_rows", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
     "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host", "ml_host_release",
     "ml_expand_pairs_workspace_bytes", "ml_expand_pairs_count", "ml_expand_pairs_emit", "ml_raycast",
@@ -1154,6 +1161,69 @@ def layer_area(area, masks, *, sums=None, counts=None):
     if own:
         return sums.cpu().numpy(), counts.cpu().numpy()
     return None
+
+
+class PeerRegion:
+    """A zeroed cudaMalloc region that other processes of the node can map (CUDA IPC): ``handle`` is the 64-byte
+    blob to send them, ``PeerRegion.open(handle)`` maps a peer's region into this process.  ``tensor(dtype)`` views
+    the bytes as a torch tensor without copying."""
+
+    def __init__(self, nbytes=None, *, _ptr_value=None, _opened=False):
+        require_cuda()
+        self.nbytes, self.opened = nbytes, _opened
+        if _ptr_value is None:
+            p = C.c_void_p()
+            _check(lib().ml_peer_alloc(C.byref(p), nbytes))
+            self.ptr = p.value
+        else:
+            self.ptr = _ptr_value
+
+    @property
+    def handle(self):
+        buf = C.create_string_buffer(64)
+        _check(lib().ml_peer_export(self.ptr, buf))
+        return buf.raw
+
+    @classmethod
+    def open(cls, handle, nbytes):
+        p = C.c_void_p()
+        _check(lib().ml_peer_open(C.c_char_p(handle), C.byref(p)))
+        return cls(nbytes, _ptr_value=p.value, _opened=True)
+
+    def tensor(self, dtype, device):
+        torch = _torch()
+        item = torch.empty(0, dtype=dtype).element_size()
+        typestr = {torch.int64: "<i8", torch.float64: "<f8", torch.uint8: "|u1"}[dtype]
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (self.nbytes // item,), "typestr": typestr, "data": (self.ptr, False), "version": 2}
+        return torch.as_tensor(_View(), device=device)
+
+    def close(self):
+        if self.ptr:
+            (lib().ml_peer_close if self.opened else lib().ml_peer_free)(self.ptr)
+            self.ptr = None
+
+
+def layer_area_peers(area, masks, peer_rows, self_index, arrive_table, status, recycle_row=None):
+    """Per-layer areas of this rank's slab added straight into EVERY rank's result row over peer memory, followed
+    by the signal / wait of the fused reduction (ml_layer_area_peers).  ``peer_rows``: device addresses (ints) of
+    the step's row in every rank's region, ``arrive_table``: device int64 tensor holding the addresses of their
+    arrival slots, ``status``: device int32[1] raised when the wait times out."""
+    torch = require_cuda()
+    masks = list(masks)
+    n = area.numel()
+    if area.dtype != torch.float32 or not area.is_contiguous():
+        raise TargetMismatch("area must be a contiguous float32 plane")
+    for m in masks:
+        _byte_plane(m, "mask")
+        if m.numel() != n:
+            raise TargetMismatch("mask plane does not match the area plane")
+    mptr = (C.c_void_p * len(masks))(*[m.data_ptr() for m in masks])
+    rows = (C.c_void_p * len(peer_rows))(*[int(p) for p in peer_rows])
+    _check(lib().ml_layer_area_peers(_ptr(area), mptr, len(masks), n, rows, len(peer_rows), int(self_index),
+                                     _ptr(arrive_table), _ptr(status), None if recycle_row is None else C.c_void_p(int(recycle_row)),
+                                     _stream()))
 
 
 def label_area(area, data, mask):

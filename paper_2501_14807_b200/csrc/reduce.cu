@@ -6,6 +6,7 @@
 // group (4 + G B/texel), accumulates in float64 registers, reduces with warp shuffles and issues
 // ONE float64 atomic per block per layer.
 #include <stdlib.h>
+#include <string.h>
 #include "common.cuh"
 #include "bulk.cuh"
 #include "meshlayers_b200.h"
@@ -16,11 +17,56 @@ namespace {
 constexpr int BLOCK = 256;
 constexpr int MAX_G = 8;
 
+constexpr int MAX_PEERS = 16;
+
 struct AreaArgs {
     const uint8_t* mask[MAX_G];
     double* sums;              // [G] slice of the caller's array
     unsigned long long* counts;
+    // Fused cross-rank reduction (row-sharded atlases): npeers > 0 -> every block adds its partial sums with
+    // SYSTEM-scope atomics into the same slots of EVERY rank's result row (peer memory over NVLink, IPC-mapped;
+    // own row included), so the all-reduce of the areas happens inside the reduction kernel.
+    int npeers;
+    double* peer_sums[MAX_PEERS];
+    unsigned long long* peer_counts[MAX_PEERS];
 };
+
+// one value per block and layer: to the local accumulator, or to the row of every rank
+ML_DEV void area_emit(const AreaArgs& a, int g, double t, unsigned long long c, bool lane0) {
+    if (!lane0) return;
+    if (a.npeers == 0) {
+        if (t != 0.0) atomicAdd(a.sums + g, t);
+        if (a.counts && c) atomicAdd(a.counts + g, c);
+        return;
+    }
+    for (int p = 0; p < a.npeers; ++p) {
+        if (t != 0.0) atomicAdd_system(a.peer_sums[p] + g, t);
+        if (c) atomicAdd_system(a.peer_counts[p] + g, c);
+    }
+}
+
+// block reduction of (acc, cnt) per layer over NW warps + area_emit by one thread
+template <int G, int NW>
+ML_DEV void area_commit(const AreaArgs& a, const double (&acc)[G], const unsigned (&cnt)[G]) {
+    __shared__ double s_sum[NW];
+    __shared__ unsigned long long s_cnt[NW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const double v = warp_sum(acc[g]);
+        const long long c = warp_sum((long long)cnt[g]);
+        if (lane == 0) { s_sum[wid] = v; s_cnt[wid] = (unsigned long long)c; }
+        __syncthreads();
+        if (wid == 0) {
+            double t = lane < NW ? s_sum[lane] : 0.0;
+            long long tc = lane < NW ? (long long)s_cnt[lane] : 0;
+            t = warp_sum(t);
+            tc = warp_sum(tc);
+            area_emit(a, g, t, (unsigned long long)tc, lane == 0);
+        }
+        __syncthreads();
+    }
+}
 
 ML_DEV void block_sum_atomic(double v, double* out) {
     __shared__ double s_part[BLOCK / 32];
@@ -100,11 +146,7 @@ area_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
         for (int g = 0; g < G; ++g)
             if (a.mask[g][i] != 0) { acc[g] = xadd(acc[g], d); ++cnt[g]; }
     }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        block_sum_atomic(acc[g], a.sums + g);
-        if (a.counts) block_count_add((long long)cnt[g], a.counts + g);
-    }
+    area_commit<G, BLOCK / 32>(a, acc, cnt);
 }
 
 // Bulk-copy form (default for aligned planes): the G mask planes -- G of the 4 + G B/texel -- travel
@@ -195,21 +237,7 @@ area_bulk_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
         }
     }
     // block reduction over all AB_THREADS threads (the producer warp contributes zeros)
-    __shared__ double s_part[AB_CW + 1];
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-        const double v = warp_sum(acc[g]);
-        if (lane == 0) s_part[warp] = v;
-        __syncthreads();
-        if (warp == 0) {
-            double t = lane <= AB_CW ? s_part[lane] : 0.0;
-            t = warp_sum(t);
-            if (lane == 0 && t != 0.0) atomicAdd(a.sums + g, t);
-        }
-        __syncthreads();
-        if (a.counts) block_count_add((long long)cnt[g], a.counts + g);
-    }
+    area_commit<G, AB_CW + 1>(a, acc, cnt);
 }
 
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
@@ -409,18 +437,20 @@ int launch_stats(const void* attr, const uint8_t* mask, long long n, double* out
 
 extern "C" {
 
-int ml_layer_area(const float* area, const uint8_t* const* masks, int64_t L, int64_t n,
-                  double* sums, uint64_t* counts, void* stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    if (L < 0 || L > 64) return ml_fail(ML_ERR_ARG, "layer count must be 0..64");
-    if (n <= 0) return ML_OK;
+static int layer_area_groups(const float* area, const uint8_t* const* masks, int64_t L, int64_t n, double* sums,
+                             uint64_t* counts, void* const* peer_rows, int npeers, cudaStream_t st) {
     for (int64_t l0 = 0; l0 < L; ) {
         const int64_t left = L - l0;
         const int g = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
         AreaArgs a;
         for (int k = 0; k < MAX_G; ++k) a.mask[k] = k < g ? masks[l0 + k] : nullptr;
-        a.sums = sums + l0;
+        a.sums = sums ? sums + l0 : nullptr;
         a.counts = counts ? (unsigned long long*)counts + l0 : nullptr;
+        a.npeers = npeers;
+        for (int p = 0; p < MAX_PEERS; ++p) {
+            a.peer_sums[p] = p < npeers ? (double*)peer_rows[p] + l0 : nullptr;
+            a.peer_counts[p] = p < npeers ? (unsigned long long*)peer_rows[p] + L + l0 : nullptr;
+        }
         int rc;
         switch (g) {
         case 8: rc = launch_area<8>(area, a, n, st); break;
@@ -433,6 +463,73 @@ int ml_layer_area(const float* area, const uint8_t* const* masks, int64_t L, int
     }
     return ML_OK;
 }
+
+int ml_layer_area(const float* area, const uint8_t* const* masks, int64_t L, int64_t n,
+                  double* sums, uint64_t* counts, void* stream) {
+    if (L < 0 || L > 64) return ml_fail(ML_ERR_ARG, "layer count must be 0..64");
+    if (n <= 0) return ML_OK;
+    return layer_area_groups(area, masks, L, n, sums, counts, nullptr, 0, (cudaStream_t)stream);
+}
+
+// Signal + wait of the fused cross-rank reduction: ONE thread tells every rank (system-scope atomic on its row's
+// arrival slot) that this rank's contributions are complete, then waits until all `target` ranks have told THIS rank.
+// Bounded: after ~10 s without progress it raises *status instead of hanging the GPU.
+__global__ void peer_arrive_wait_kernel(unsigned long long* const* arrive, int npeers, const volatile unsigned long long* own,
+                                        unsigned long long target, unsigned int* status) {
+    __threadfence_system();
+    for (int p = 0; p < npeers; ++p) atomicAdd_system(arrive[p], 1ull);
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (*own < target) {
+        __nanosleep(200);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 10000000000ull) { if (status) atomicExch(status, 1u); break; }
+    }
+    __threadfence_system();
+}
+
+int ml_layer_area_peers(const float* area, const uint8_t* const* masks, int64_t L, int64_t n,
+                        void* const* peer_rows, int npeers, int self, void* arrive_table, uint32_t* status,
+                        void* recycle_row, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (L < 0 || L > 64) return ml_fail(ML_ERR_ARG, "layer count must be 0..64");
+    if (npeers < 1 || npeers > MAX_PEERS || self < 0 || self >= npeers || peer_rows == nullptr || arrive_table == nullptr)
+        return ml_fail(ML_ERR_ARG, "ml_layer_area_peers: 1..16 peers, self among them, row pointers and the arrival table");
+    if (n > 0) {
+        const int rc = layer_area_groups(area, masks, L, n, nullptr, nullptr, peer_rows, npeers, st);
+        if (rc != ML_OK) return rc;
+    }
+    // arrive_table: device array of npeers pointers = the arrival slot (u64 at index 2L) of every rank's row
+    const volatile unsigned long long* own = (const volatile unsigned long long*)peer_rows[self] + 2 * L;
+    peer_arrive_wait_kernel<<<1, 1, 0, st>>>((unsigned long long* const*)arrive_table, npeers, own, (unsigned long long)npeers, status);
+    ML_CUDA(cudaGetLastError());
+    if (recycle_row) ML_CUDA(cudaMemsetAsync(recycle_row, 0, (size_t)(2 * L + 2) * sizeof(unsigned long long), st));
+    return ML_OK;
+}
+
+// Peer memory for the fused reduction: plain cudaMalloc regions (IPC handles need allocation bases, which torch's
+// caching allocator does not hand out), exported / opened as 64-byte cudaIpcMemHandle_t blobs.
+int ml_peer_alloc(void** ptr, size_t bytes) {
+    if (!ptr) return ml_fail(ML_ERR_ARG, "ml_peer_alloc: null");
+    ML_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+    ML_CUDA(cudaMemset(*ptr, 0, bytes ? bytes : 1));
+    return ML_OK;
+}
+int ml_peer_free(void* ptr) { if (ptr) ML_CUDA(cudaFree(ptr)); return ML_OK; }
+int ml_peer_export(const void* ptr, void* handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handles are 64 bytes");
+    cudaIpcMemHandle_t h;
+    ML_CUDA(cudaIpcGetMemHandle(&h, (void*)ptr));
+    memcpy(handle64, &h, 64);
+    return ML_OK;
+}
+int ml_peer_open(const void* handle64, void** ptr) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    ML_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return ML_OK;
+}
+int ml_peer_close(void* ptr) { if (ptr) ML_CUDA(cudaIpcCloseMemHandle(ptr)); return ML_OK; }
 
 int ml_label_area(const float* area, const uint8_t* data, const uint8_t* mask, int64_t n,
                   double* sums, uint64_t* counts, void* stream) {

@@ -119,6 +119,61 @@ class AreaReducer:
         return slots
 
 
+class PeerAreaReducer:
+    """Fused compute + collective for the per-layer areas: no collective call at all.  Every rank owns a ring of
+    result rows in an IPC-exported region; the area reduction kernel of every rank adds its per-block partials with
+    system-scope atomics into the step's row of EVERY rank (NVLink peer memory), one thread then signals / awaits the
+    arrival slots (``_native.layer_area_peers``).  ``reduce(step, area, masks, out)`` leaves the global sums and counts
+    of all L layers in ``out`` (int64[2L], sums as float64 bit patterns) on every rank.
+
+    Set-up (once): regions are allocated with cudaMalloc, the 64-byte IPC handles travel through the default process
+    group (host side), every rank maps every other rank's region.  Rows are recycled NSLOTS steps later; a row is
+    zeroed by its owner half a ring ahead, right after the wait of the current step -- at that point every rank has
+    finished the current step (that is what the wait established) and none is further than one step ahead."""
+
+    NSLOTS = 16
+
+    def __init__(self, layers, device):
+        import torch
+        from . import _native
+        dist = _dist()
+        self.L = int(layers)
+        self.rank, self.ws = world()
+        self.device = device
+        self.row_bytes = (2 * self.L + 2) * 8
+        self.region = _native.PeerRegion(self.NSLOTS * self.row_bytes)
+        handles = [None] * self.ws
+        dist.all_gather_object(handles, self.region.handle)
+        self.peers = [self.region if r == self.rank else _native.PeerRegion.open(handles[r], self.region.nbytes)
+                      for r in range(self.ws)]
+        self.own = self.region.tensor(torch.int64, device).view(self.NSLOTS, 2 * self.L + 2)
+        # per slot: the addresses of every rank's arrival slot, as a device table
+        self.arrive = torch.tensor([[p.ptr + s * self.row_bytes + 2 * self.L * 8 for p in self.peers] for s in range(self.NSLOTS)],
+                                   dtype=torch.int64, device=device)
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        dist.barrier()                      # every region is mapped everywhere before anybody adds into one
+
+    def reduce(self, step, area, masks, out):
+        from . import _native
+        s = step % self.NSLOTS
+        ahead = (step + self.NSLOTS // 2) % self.NSLOTS
+        rows = [p.ptr + s * self.row_bytes for p in self.peers]
+        _native.layer_area_peers(area, masks, rows, self.rank, self.arrive[s], self.status,
+                                 recycle_row=self.region.ptr + ahead * self.row_bytes)
+        out.copy_(self.own[s, :2 * self.L])
+        return out
+
+    def check(self):
+        if int(self.status.item()):
+            raise RuntimeError("peer area reduction timed out waiting for another rank")
+
+    def close(self):
+        for p in self.peers:
+            if p is not self.region:
+                p.close()
+        self.region.close()
+
+
 def allreduce_areas(sums, counts=None):
     """Sum per-layer partial areas (float64 tensor) and counts (int64 tensor) over all ranks, in
     place.  One collective: counts ride along as exact float64 (< 2^53 texels).  (Convenience form;
