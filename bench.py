@@ -700,6 +700,27 @@ def run_ours(args):
                        "d2h_bytes_per_call": "O(hit texels / 8): the written SET as a bitmap or word list",
                        "plane_round_trip_bytes_avoided": int(naive), "edited": int(last[0]), "fragments": int(last[1]),
                        "equal_to_resident_stroke": bool(same)}
+        # the other two reference call shapes, same conditions: coverage_fill (KN:84) into a zeroed 16384^2 host
+        # plane and raster_depth (KN:103) into a host depth plane pre-filled with 1.0
+        from paper_2501_14807_b200.mesh_core import window_triangles
+        cov = planes[0]
+        t_cov = []
+        for r in range(3):
+            cov[:] = 0
+            t0 = time.perf_counter()
+            written = nat.coverage_fill(tri_xy, W, rows, cov)
+            t_cov.append((time.perf_counter() - t0) * 1e3)
+        wxy, wzn = window_triangles(wl.mesh, wl.cam)
+        t_dep = []
+        for r in range(3):
+            dplane = np.ones((wl.cam.height, wl.cam.width), np.float32)
+            t0 = time.perf_counter()
+            nat.raster_depth(wxy, wzn, dplane)
+            t_dep.append((time.perf_counter() - t0) * 1e3)
+        host_planes["coverage_fill_ms_per_call"] = round(float(np.median(t_cov[1:])), 3)
+        host_planes["coverage_fill_equals_surface_map"] = bool(int(written) == arm.surf.covered)
+        host_planes["raster_depth_ms_per_call"] = round(float(np.median(t_dep[1:])), 3)
+        host_planes["raster_depth_equals_resident"] = bool(np.array_equal(dplane.view(np.uint32), depth_np.view(np.uint32)))
         del planes, tri_xy, clip
     stop.set()
     th.join()

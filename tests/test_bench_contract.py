@@ -79,6 +79,8 @@ def test_gpu_arm_json_contract(extra):
     # the reference's call shape with host planes
     hp = d["e2e_host_planes"]
     assert hp["ms_per_call"] > 0 and hp["equal_to_resident_stroke"] is True and hp["edited"] > 0
+    assert hp["coverage_fill_ms_per_call"] > 0 and hp["coverage_fill_equals_surface_map"] is True
+    assert hp["raster_depth_ms_per_call"] > 0 and hp["raster_depth_equals_resident"] is True
 
 
 @pytest.mark.gpu
