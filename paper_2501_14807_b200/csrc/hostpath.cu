@@ -26,6 +26,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 #include <algorithm>
 #include <condition_variable>
 #include <functional>
@@ -226,6 +227,23 @@ struct Arena {
 };
 
 Arena g_arena;
+
+// ML_HOST_TRACE=1: phase times of the host-buffer calls on stderr (each phase ends with a stream sync, so the
+// traced call is slower than the untraced one; for finding out where a call spends its time)
+struct Trace {
+    bool on;
+    double t0;
+    static double now() { timespec ts; clock_gettime(CLOCK_MONOTONIC, &ts); return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6; }
+    Trace() : on(getenv("ML_HOST_TRACE") != nullptr), t0(now()) {}
+    void mark(const char* what, cudaStream_t a = nullptr, cudaStream_t b = nullptr) {
+        if (!on) return;
+        if (a) cudaStreamSynchronize(a);
+        if (b) cudaStreamSynchronize(b);
+        const double t = now();
+        fprintf(stderr, "[ml host] %-28s %7.3f ms\n", what, t - t0);
+        t0 = t;
+    }
+};
 
 // ------------------------------------------------------------------------------------------------
 // device side of the sparse write-back: byte plane (0 / non-zero) -> 1 bit per texel, 64 texels per word,
@@ -485,8 +503,10 @@ int ml_raster_tea_host(const void* tri_xy, const void* tri_clip, int tri_dtype, 
     const size_t es = tri_elem(tri_dtype), ws = ml_raster_workspace_bytes(ntri);
     const size_t b_tri = (size_t)ntri * 6 * es, b_clip = (size_t)ntri * 12 * es;
     const size_t b_depth = (size_t)depth_w * depth_h * sizeof(float), b_shape = (size_t)shape_w * shape_h;
+    Trace tr;
     ML_TRY(A.begin(Arena::padded(b_tri) + Arena::padded(b_clip) + Arena::padded(b_depth) + Arena::padded(b_shape) +
                    Arena::padded((size_t)nwords * 64) + 2 * Arena::padded((size_t)nwords * 8) + Arena::padded(ws) + 1024));
+    tr.mark("arena");
     void* d_tri = A.take<void>(b_tri);
     void* d_clip = A.take<void>(b_clip);
     float* d_depth = A.take<float>(b_depth);
@@ -502,6 +522,7 @@ int ml_raster_tea_host(const void* tri_xy, const void* tri_clip, int tri_dtype, 
     ML_TRY(A.upload(d_shape, shape, b_shape, A.s_up));
     ML_TRY(A.upload(d_clip, tri_clip, b_clip, A.s_up));
     ML_TRY(A.upload(d_tri, tri_xy, b_tri, A.s_up));
+    tr.mark("uploads (staged, pipelined)", A.s_up, A.s_run);
     ML_CUDA(cudaEventRecord(A.ev, A.s_up));
     ML_CUDA(cudaStreamWaitEvent(A.s_run, A.ev, 0));
     ml_tea_params tp;
@@ -513,9 +534,11 @@ int ml_raster_tea_host(const void* tri_xy, const void* tri_clip, int tri_dtype, 
     // data = mask = NULL: the kernel records the stroke's texels in the zeroed scratch plane only
     ML_TRY(ml_raster_tea(d_tri, d_clip, tri_dtype, ntri, width, height, 0, height, &tp, nullptr, esize, value_bits,
                          nullptr, d_hit, (uint64_t*)d_ctr, d_ws, ws, A.s_run));
+    tr.mark("classify + direct TEA kernel", A.s_run);
     long long newly = 0;
     unsigned long long c[4];                               // [1] = fragments offered (KN:158-161, 203)
     ML_TRY(write_back(A, d_hit, n, d_bits, d_list, d_ctr, c, edited, mask, data, esize, value_bits, &newly));
+    tr.mark("pack + download + apply");
     if (edited_count) *edited_count = newly;
     if (fragments) *fragments = (int64_t)c[1];
     return ML_OK;
