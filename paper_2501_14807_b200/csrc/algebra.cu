@@ -167,8 +167,11 @@ chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
 // are never read (8 masks + 2 output bytes per texel instead of 18).  The mask -> data dependency is
 // hidden by software pipelining: the masks of the thread's NEXT vector are requested before the data
 // of the current one, so as many bytes are in flight as in the eager kernel.
+#ifndef ML_CHAIN_LAZY_MINB
+#define ML_CHAIN_LAZY_MINB 2
+#endif
 template <int ESIZE>
-__global__ void __launch_bounds__(BLOCK, 2)
+__global__ void __launch_bounds__(BLOCK, ML_CHAIN_LAZY_MINB)
 chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
     constexpr int GL = 8;
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
@@ -186,96 +189,122 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
 #pragma unroll
             for (int k = 0; k < GL; ++k) if (k < a.nlayers) mn[k] = ld_stream_rw((const uint4*)a.mask[k] + v + nthreads);
         }
-        // Pass 1 -- the mask fold alone (the masks are normalised to 0x00 / 0xff byte flags in place, so pass 2
-        // does not repeat that): final mask `sim`, and which layers' data can reach the result of this vector
-        // (the first operand where its mask is set, a union operand where it fills texels the accumulator does
-        // not hold; intersection / difference / masking operands never).
+        // The fold works on mask bytes that are exactly 0 / 1 (what every writer of this library stores); a vector
+        // holding any other non-zero byte value is normalised first (rare: caller-made planes).
+        uint32_t odd = 0u;
+#pragma unroll
+        for (int k = 0; k < GL; ++k)
+            if (k < a.nlayers) odd |= (m[k].x | m[k].y | m[k].z | m[k].w) & 0xfefefefeu;
+        if (odd) {
+#pragma unroll
+            for (int k = 0; k < GL; ++k) {
+                if (k < a.nlayers) {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) ((uint32_t*)&m[k])[g] = nz_bytes(((const uint32_t*)&m[k])[g]) & 0x01010101u;
+                }
+            }
+        }
+        // Pass 1 -- the mask fold alone, in the 0 / 1 byte domain (one or two LOP3 per word and layer): final mask
+        // `sim`, and which layers' data can reach the result of this vector (the first operand where its mask is set,
+        // a union operand where it fills texels the accumulator does not hold; intersection / difference / masking
+        // operands never).
         unsigned need = 0;
         uint32_t sim[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int k = 0; k < GL; ++k) {
             if (k < a.nlayers) {
                 const int op = a.ops[k];
-                bool nd = false;
+                uint32_t fills = 0u;
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    const uint32_t bff = nz_bytes(((const uint32_t*)&m[k])[g]);
-                    ((uint32_t*)&m[k])[g] = bff;
-                    if (k == 0) { nd |= bff != 0u; sim[g] = bff; }
-                    else if (op == ML_OP_UNION) { nd |= (bff & ~sim[g]) != 0u; sim[g] |= bff; }
-                    else if (op == ML_OP_DIFFERENCE) sim[g] &= ~bff;
-                    else sim[g] &= bff;
+                    const uint32_t bm = ((const uint32_t*)&m[k])[g];
+                    if (k == 0) { fills |= bm; sim[g] = bm; }
+                    else if (op == ML_OP_UNION) { fills |= bm & ~sim[g]; sim[g] |= bm; }
+                    else if (op == ML_OP_DIFFERENCE) sim[g] &= ~bm;
+                    else sim[g] &= bm;
                 }
-                if (nd) need |= 1u << k;
+                if (fills) need |= 1u << k;
             }
         }
-        // one-byte layers: all needed vectors are requested together; wider layers (64 bytes per
-        // layer and vector) are fetched one layer at a time inside the fold to bound the registers
-        uint4 d1[ESIZE == 1 ? GL : 1];
-        if (ESIZE == 1) {
+        const uint4 om = make_uint4(sim[0], sim[1], sim[2], sim[3]);
+        uint4 od[ESIZE];
+        if (need <= 1u) {
+            // no union operand fills anything: the result's data is the first operand's under the final mask
+            // (need == 1), or nothing at all (need == 0: the first operand is empty here and so is the result)
 #pragma unroll
-            for (int k = 0; k < GL; ++k)
-                d1[k] = ((need >> k) & 1u) ? ld_stream_rw((const uint4*)a.data[k] + v) : make_uint4(0u, 0u, 0u, 0u);
-        }
-        // Pass 2 -- the data fold, restricted to the layers of `need`.  A layer outside `need` changes the
-        // accumulator's data only by clearing texels it removes from the mask; that clearing is deferred: a
-        // needed union masks the accumulator with the mask it has at that point (combine(): keep_a = acc.ff)
-        // before it fills, and the result is masked with the FINAL mask once at the end -- the same bytes as
-        // folding every layer, for a cost proportional to the layers that matter (usually one).
-        Group<ESIZE> acc[4];
+            for (int j = 0; j < ESIZE; ++j) od[j] = make_uint4(0u, 0u, 0u, 0u);
+            if (need) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            acc[g].ff = 0u;
+                for (int j = 0; j < ESIZE; ++j) {
+                    const uint4 d0 = ld_stream_rw((const uint4*)a.data[0] + v * ESIZE + j);
+                    od[j] = d0;
+                }
 #pragma unroll
-            for (int j = 0; j < ESIZE; ++j) acc[g].d[j] = 0u;
-        }
+                for (int g = 0; g < 4; ++g)
 #pragma unroll
-        for (int k = 0; k < GL; ++k) {
-            if (k < a.nlayers) {
-                const int op = a.ops[k];
-                const bool needed = (need >> k) & 1u;
-                uint4 dk[ESIZE];
-                if (needed) {
-                    if (ESIZE == 1) dk[0] = d1[k];
-                    else {
+                    for (int j = 0; j < ESIZE; ++j)
+                        ((uint32_t*)&od[0])[g * ESIZE + j] &= expand<ESIZE>(sim[g] * 0xffu, j);
+            }
+        } else {
+            // one-byte layers: all needed vectors are requested together; wider layers (64 bytes per
+            // layer and vector) are fetched one layer at a time inside the fold to bound the registers
+            uint4 d1[ESIZE == 1 ? GL : 1];
+            if (ESIZE == 1) {
 #pragma unroll
-                        for (int j = 0; j < ESIZE; ++j) dk[j] = ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j);
+                for (int k = 0; k < GL; ++k)
+                    d1[k] = ((need >> k) & 1u) ? ld_stream_rw((const uint4*)a.data[k] + v) : make_uint4(0u, 0u, 0u, 0u);
+            }
+            // Pass 2 -- the data fold, restricted to the layers of `need`.  A layer outside `need` changes the
+            // accumulator's data only by clearing texels it removes from the mask; that clearing is deferred: a needed
+            // union masks the accumulator with the mask it has at that point before it fills, and the result is masked
+            // with the FINAL mask once at the end -- the same bytes as folding every layer.
+            uint32_t cur[4] = {0u, 0u, 0u, 0u};             // the accumulator's mask (0 / 1 bytes) while folding
+            uint32_t accd[4 * ESIZE];
+#pragma unroll
+            for (int i = 0; i < 4 * ESIZE; ++i) accd[i] = 0u;
+#pragma unroll
+            for (int k = 0; k < GL; ++k) {
+                if (k < a.nlayers) {
+                    const int op = a.ops[k];
+                    const bool needed = (need >> k) & 1u;
+                    uint4 dk[ESIZE];
+                    if (needed) {
+                        if (ESIZE == 1) dk[0] = d1[k];
+                        else {
+#pragma unroll
+                            for (int j = 0; j < ESIZE; ++j) dk[j] = ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j);
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const uint32_t bm = ((const uint32_t*)&m[k])[g];
+                        if (k == 0) {
+                            cur[g] = bm;
+                            if (needed) {
+#pragma unroll
+                                for (int j = 0; j < ESIZE; ++j)
+                                    accd[g * ESIZE + j] = ((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(bm * 0xffu, j);
+                            }
+                        } else if (op == ML_OP_UNION) {
+                            if (needed) {
+                                const uint32_t keep_a = cur[g] * 0xffu, take_b = (bm & ~cur[g]) * 0xffu;
+#pragma unroll
+                                for (int j = 0; j < ESIZE; ++j)
+                                    accd[g * ESIZE + j] = (accd[g * ESIZE + j] & expand<ESIZE>(keep_a, j)) |
+                                                          (((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(take_b, j));
+                            }
+                            cur[g] |= bm;
+                        } else if (op == ML_OP_DIFFERENCE) cur[g] &= ~bm;
+                        else cur[g] &= bm;
                     }
                 }
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    const uint32_t bff = ((const uint32_t*)&m[k])[g];
-                    if (k == 0) {
-                        acc[g].ff = bff;
-                        if (needed) {
-#pragma unroll
-                            for (int j = 0; j < ESIZE; ++j) acc[g].d[j] = ((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(bff, j);
-                        }
-                    } else if (op == ML_OP_UNION) {
-                        if (needed) {
-                            const uint32_t keep_a = acc[g].ff, take_b = bff & ~acc[g].ff;
-#pragma unroll
-                            for (int j = 0; j < ESIZE; ++j)
-                                acc[g].d[j] = (acc[g].d[j] & expand<ESIZE>(keep_a, j)) |
-                                              (((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(take_b, j));
-                        }
-                        acc[g].ff |= bff;
-                    } else if (op == ML_OP_DIFFERENCE) acc[g].ff &= ~bff;
-                    else acc[g].ff &= bff;
-                }
             }
+#pragma unroll
+            for (int g = 0; g < 4; ++g)
+#pragma unroll
+                for (int j = 0; j < ESIZE; ++j) ((uint32_t*)&od[0])[g * ESIZE + j] = accd[g * ESIZE + j] & expand<ESIZE>(sim[g] * 0xffu, j);
         }
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-#pragma unroll
-            for (int j = 0; j < ESIZE; ++j) acc[g].d[j] &= expand<ESIZE>(acc[g].ff, j);
-        st_stream((uint4*)mc + v, make_uint4(acc[0].ff & 0x01010101u, acc[1].ff & 0x01010101u, acc[2].ff & 0x01010101u,
-                                              acc[3].ff & 0x01010101u));
-        uint4 od[ESIZE];
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-#pragma unroll
-            for (int j = 0; j < ESIZE; ++j) ((uint32_t*)&od[0])[g * ESIZE + j] = acc[g].d[j];
+        st_stream((uint4*)mc + v, om);
 #pragma unroll
         for (int j = 0; j < ESIZE; ++j) st_stream((uint4*)dc + v * ESIZE + j, od[j]);
     }
