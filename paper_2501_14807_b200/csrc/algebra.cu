@@ -228,7 +228,8 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
         }
         const uint4 om = make_uint4(sim[0], sim[1], sim[2], sim[3]);
         uint4 od[ESIZE];
-        if (need <= 1u) {
+        // warp-uniform choice: a warp that took both branches would pay for both (dense / mixed layers)
+        if (__all_sync(__activemask(), need <= 1u)) {
             // no union operand fills anything: the result's data is the first operand's under the final mask
             // (need == 1), or nothing at all (need == 0: the first operand is empty here and so is the result)
 #pragma unroll

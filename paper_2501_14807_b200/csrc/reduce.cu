@@ -157,16 +157,20 @@ area_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
 // blocks).  The register form above holds the next step's masks in registers (128 B per thread at 128
 // registers, two blocks per SM): ncu r1 24 % warps active, long_scoreboard on top, 0.78 of the DRAM peak.
 #ifndef ML_AREA_STAGES
-#define ML_AREA_STAGES 2
+#define ML_AREA_STAGES 3                               // for groups of 8 masks (28 KB stages); smaller groups get deeper rings
 #endif
-constexpr int AB_STAGES = ML_AREA_STAGES;
-constexpr int AB_CW = 8;                               // consumer warps
+#ifndef ML_AREA_CW
+#define ML_AREA_CW 7                                   // + the producer warp = 8 warps: 128 registers per thread at two blocks per SM
+#endif
+template <int G> struct AreaStages { static constexpr int N = G >= 8 ? ML_AREA_STAGES : (G >= 4 ? 4 : 6); };
+constexpr int AB_CW = ML_AREA_CW;                      // consumer warps
 constexpr int AB_THREADS = 32 * (AB_CW + 1);
 constexpr int AB_TEXELS = 16 * 32 * AB_CW;             // texels (= bytes per mask plane) per chunk
 
 template <int G>
 __global__ void __launch_bounds__(AB_THREADS, 2)
 area_bulk_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
+    constexpr int AB_STAGES = AreaStages<G>::N;
     typedef BulkRing<AB_STAGES, G * AB_TEXELS> Ring;
     extern __shared__ __align__(128) uint8_t ab_smem[];
     Ring& ring = *reinterpret_cast<Ring*>(ab_smem);
@@ -193,25 +197,23 @@ area_bulk_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
             }
         }
     } else {
-        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
-            const long long base = c * AB_TEXELS;
-            const unsigned bytes = (unsigned)(vbytes - base < AB_TEXELS ? vbytes - base : AB_TEXELS);
-            const uint8_t* b = ring.acquire(pos);
-            const unsigned off = (unsigned)threadIdx.x << 4;
+        // Two-deep software pipeline per thread: the area loads of chunk c are in flight while the masks of chunk
+        // c + 1 are looked at and ITS area loads are issued; only then is chunk c accumulated -- from the masks still
+        // sitting in its ring stage, which is released afterwards (so a block holds two stages while a third fills:
+        // AB_STAGES >= 3).  One vector per thread and chunk with an immediate accumulate left a dependent DRAM round
+        // trip exposed per step (ncu r2: long_scoreboard 10.8 per issue at 24 % issue-active).
+        const unsigned off = (unsigned)threadIdx.x << 4;
+        float4 ap[4];                       // area vector of the previous chunk, in flight / waiting
+        RingPos<AB_STAGES> held;            // the previous chunk's stage
+        unsigned held_bytes = 0;
+        bool have = false, holding = false;
+        auto accumulate = [&](const uint8_t* b, unsigned bytes, const float4 (&ar)[4]) {
             uint4 m[G];
-            uint32_t anyset = 0;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 m[g] = make_uint4(0u, 0u, 0u, 0u);
                 if (off < bytes) m[g] = *(const uint4*)(b + g * AB_TEXELS + off);
-                anyset |= m[g].x | m[g].y | m[g].z | m[g].w;
             }
-            ring.release(pos);
-            if (anyset == 0) continue;
-            float4 ar[4];
-            const float4* ap = (const float4*)(area + base + off);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) ar[j] = ld_stream(ap + j);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const double d[4] = {(double)ar[j].x, (double)ar[j].y, (double)ar[j].z, (double)ar[j].w};
@@ -226,6 +228,39 @@ area_bulk_kernel(const float* __restrict__ area, AreaArgs a, long long n) {
                         if (w & (0xffu << (8 * e))) { acc[g] = xadd(acc[g], d[e]); ++cnt[g]; }
                 }
             }
+        };
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x, pos.next()) {
+            const long long base = c * AB_TEXELS;
+            const unsigned bytes = (unsigned)(vbytes - base < AB_TEXELS ? vbytes - base : AB_TEXELS);
+            const uint8_t* b = ring.acquire(pos);
+            uint32_t anyset = 0;
+            if (off < bytes) {
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint4 m = *(const uint4*)(b + g * AB_TEXELS + off);
+                    anyset |= m.x | m.y | m.z | m.w;
+                }
+            }
+            float4 ar[4];
+            if (anyset) {
+                const float4* ap4 = (const float4*)(area + base + off);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) ar[j] = ld_stream(ap4 + j);
+            }
+            if (holding) {
+                if (have) accumulate(ring.buf[held.stage], held_bytes, ap);
+                ring.release(held);
+            }
+            held = pos; held_bytes = bytes; holding = true;
+            have = anyset != 0;
+            if (have) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) ap[j] = ar[j];
+            }
+        }
+        if (holding) {
+            if (have) accumulate(ring.buf[held.stage], held_bytes, ap);
+            ring.release(held);
         }
         if (blockIdx.x == 0) {
             for (long long i = vbytes + threadIdx.x; i < n; i += 32 * AB_CW) {     // < 16 texels of tail
@@ -244,7 +279,7 @@ inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 template <int G>
 int launch_area_bulk(const float* area, const AreaArgs& a, long long n, cudaStream_t st) {
-    typedef BulkRing<AB_STAGES, G * AB_TEXELS> Ring;
+    typedef BulkRing<AreaStages<G>::N, G * AB_TEXELS> Ring;
     static int per_sm = 0;
     const void* fn = (const void*)area_bulk_kernel<G>;
     if (!per_sm) {
