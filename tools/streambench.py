@@ -8,8 +8,8 @@ ctypes per call, a third of a 75 us kernel.)
     python tools/streambench.py [--atlas 16384] [--inner 10] [--reps 7] [--json out.json] [names...]
 
 Prints name, ms per call, algorithmic GB/s (SURVEY.md 8(d) bytes), fraction of the measured HBM
-peak (MEASURED_PEAKS.json).  Not the judged benchmark (bench.py is); bench.py imports
-`time_graph` from here for its `stream_kernels` block."""
+peak (MEASURED_PEAKS.json).  Not the judged benchmark (bench.py is); the timing routine is bench.py's
+`time_graph`, the one behind its `stream_kernels` block."""
 import argparse
 import json
 import os
@@ -22,34 +22,9 @@ sys.path.insert(0, ROOT)
 
 
 def time_graph(fn, inner=10, reps=7, warm=2):
-    """Median ms per call of `fn` over `reps` replays of a CUDA graph of `inner` calls.  Falls back to
-    eager back-to-back calls between two events if the call cannot be captured."""
-    import torch
-    for _ in range(warm):
-        fn()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    graph = None
-    try:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for _ in range(inner):
-                fn()
-        graph = g
-    except Exception:            # not capturable (host sync inside): eager back-to-back launches
-        torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps + 1):
-        a.record()
-        if graph is not None:
-            graph.replay()
-        else:
-            for _ in range(inner):
-                fn()
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) / inner)
-    return float(np.median(ts[1:])), graph is not None
+    """bench.time_graph: median ms per call over replays of a CUDA graph holding `inner` back-to-back calls."""
+    import bench
+    return bench.time_graph(fn, inner=inner, reps=reps, warm=warm)
 
 
 def main():
