@@ -414,7 +414,7 @@ class GpuArm:
             ok = torch.zeros(1, dtype=torch.int64)
             try:
                 self.peer_areas = sharding.PeerAreaReducer(L, dev)
-                ok[0] = 1
+                ok[0] = 1 if self.peer_areas.self_test() else 0
             except Exception as exc:                         # e.g. IPC not permitted in this container
                 sys.stderr.write("peer area reduction unavailable (%s); using the all-gather form\n" % exc)
             import torch.distributed as dist

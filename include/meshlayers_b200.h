@@ -277,6 +277,8 @@ int ml_peer_free(void* ptr);
 int ml_peer_export(const void* ptr, void* handle64);
 int ml_peer_open(const void* handle64, void** ptr);
 int ml_peer_close(void* ptr);
+/* 1 iff the current device can run native atomics on memory of device `peer_device` (NVLink peers; same device: 1) */
+int ml_peer_atomics_supported(int peer_device);
 /* uint8 label plane: sums[v] += area over texels with mask != 0 and data == v (v < 256). */
 int ml_label_area(const float* area, const uint8_t* data, const uint8_t* mask, int64_t n,
                   double* sums /* [256] */, uint64_t* counts /* [256] */, void* stream);

@@ -125,6 +125,7 @@ def lib():
         "ml_peer_export": (i32, [vp, vp]),
         "ml_peer_open": (i32, [vp, C.POINTER(vp)]),
         "ml_peer_close": (i32, [vp]),
+        "ml_peer_atomics_supported": (i32, [i32]),
         "ml_label_area": (i32, [vp, vp, vp, i64, vp, vp, vp]),
         "ml_layer_stats": (i32, [vp, i32, vp, i64, vp, vp]),
         "ml_outline_mask": (i32, [vp, i64, i64, i64, i64, i64, i64, vp, vp]),
@@ -165,7 +166,7 @@ EXPORTED_SYMBOLS = (
     "ml_tile_workspace_bytes", "ml_surface_tile_boxes", "ml_select_sphere_tiles", "ml_select_sphere_batch_tiles",
     "ml_select_threshold", "ml_plane_tile_range", "ml_select_threshold_tiles", "ml_layer_op",
     "ml_layer_chain", "ml_layer_area", "ml_layer_area_peers", "ml_peer_alloc", "ml_peer_free", "ml_peer_export",
-    "ml_peer_open", "ml_peer_close", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
+    "ml_peer_open", "ml_peer_close", "ml_peer_atomics_supported", "ml_label_area", "ml_layer_stats", "ml_outline_mask",
     "ml_apply_padding", "ml_apply_padding_tiles", "ml_apply_padding_tiles_rows", "ml_resolve_display", "ml_pack_mask", "ml_unpack_mask",
     "ml_coverage_fill_host", "ml_raster_depth_host", "ml_raster_tea_host", "ml_host_release",
     "ml_expand_pairs_workspace_bytes", "ml_expand_pairs_count", "ml_expand_pairs_emit", "ml_raycast",

@@ -565,6 +565,16 @@ int ml_peer_open(const void* handle64, void** ptr) {
     return ML_OK;
 }
 int ml_peer_close(void* ptr) { if (ptr) ML_CUDA(cudaIpcCloseMemHandle(ptr)); return ML_OK; }
+// 1 iff the current device can run native atomics on memory of `peer_device` (same device: always)
+int ml_peer_atomics_supported(int peer_device) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (dev == peer_device) return 1;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, peer_device) != cudaSuccess || !can) return 0;
+    if (cudaDeviceGetP2PAttribute(&v, cudaDevP2PAttrNativeAtomicSupported, dev, peer_device) != cudaSuccess) return 0;
+    return v ? 1 : 0;
+}
 
 int ml_label_area(const float* area, const uint8_t* data, const uint8_t* mask, int64_t n,
                   double* sums, uint64_t* counts, void* stream) {

@@ -143,8 +143,11 @@ class PeerAreaReducer:
         self.row_bytes = (2 * self.L + 2) * 8
         self.region = _native.PeerRegion(self.NSLOTS * self.row_bytes)
         handles = [None] * self.ws
-        dist.all_gather_object(handles, self.region.handle)
-        self.peers = [self.region if r == self.rank else _native.PeerRegion.open(handles[r], self.region.nbytes)
+        dist.all_gather_object(handles, (self.region.handle, int(torch.cuda.current_device())))
+        for _, peer_dev in handles:
+            if not _native.lib().ml_peer_atomics_supported(int(peer_dev)):
+                raise RuntimeError("no native peer atomics between cuda:%d and cuda:%d" % (torch.cuda.current_device(), peer_dev))
+        self.peers = [self.region if r == self.rank else _native.PeerRegion.open(handles[r][0], self.region.nbytes)
                       for r in range(self.ws)]
         self.own = self.region.tensor(torch.int64, device).view(self.NSLOTS, 2 * self.L + 2)
         # per slot: the addresses of every rank's arrival slot, as a device table
@@ -152,6 +155,27 @@ class PeerAreaReducer:
                                    dtype=torch.int64, device=device)
         self.status = torch.zeros(1, dtype=torch.int32, device=device)
         dist.barrier()                      # every region is mapped everywhere before anybody adds into one
+
+    def self_test(self):
+        """One trial reduction with known contributions (rank r adds r + 1 for each of 4096 texels into every layer):
+        True iff this rank's row then holds the expected global sums and counts and the wait did not time out.  Uses
+        the last slot of the ring and leaves it zeroed (it is recycled again long before its first real use)."""
+        import torch
+        from . import _native
+        n = 4096
+        area = torch.full((1, n), float(self.rank + 1), dtype=torch.float32, device=self.device)
+        mask = torch.ones((1, n), dtype=torch.uint8, device=self.device)
+        s = self.NSLOTS - 1
+        rows = [p.ptr + s * self.row_bytes for p in self.peers]
+        _native.layer_area_peers(area, [mask] * self.L, rows, self.rank, self.arrive[s], self.status)
+        got = self.own[s, :2 * self.L].clone()
+        self.own[s].zero_()
+        got = got.cpu()
+        want_sum = float(n * sum(r + 1 for r in range(self.ws)))
+        ok = (not int(self.status.item())
+              and bool((got[:self.L].view(torch.float64) == want_sum).all())
+              and bool((got[self.L:] == n * self.ws).all()))
+        return ok
 
     def reduce(self, step, area, masks, out):
         from . import _native

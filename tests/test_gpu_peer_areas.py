@@ -35,6 +35,8 @@ def _worker(rank, ws, port, L, steps, out_dir):
         r0, rows = sharding.shard_rows(H, ws, rank)
         d_area = torch.from_numpy(area[r0:r0 + rows].copy()).to(dev)
         red = sharding.PeerAreaReducer(L, dev)
+        assert red.self_test()
+        dist.barrier()
         out = torch.zeros(2 * L, dtype=torch.int64, device=dev)
         worst = 0.0
         for step in range(steps):
