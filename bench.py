@@ -849,6 +849,9 @@ def run_ours(args):
         cfg["surface_map"] = {"covered": arm.surf.covered, "overlap": arm.surf.overlap}
         cfg["footprint_culling"] = bool(arm.culled(primary_cull))
         cfg["area_reduce"] = arm.area_reduce_kind
+        cfg["value_basis"] = ("value counts NOMINAL texel passes (stages x slab texels) of the default path, whose brush / selection stages "
+                              "and chain skip most of their bytes by design; value_streamed is the same step with every stage reading "
+                              "its whole atlas (byte-honest); both from CUDA events over the same %d steps" % args.steps)
         roofline = roof(tab, stage_ms, "slowest stage of the default step: SURVEY 8(d) algorithmic bytes / CUDA-event time "
                                        "(frac); dram_frac = ncu-measured DRAM bytes of the stage's kernels / the same time. "
                                        "A stage that skips bytes by design (culled brushes, lazy chain, sparse-mask area) shows "
