@@ -98,6 +98,9 @@ def parse():
     ap.add_argument("--parity-steps", type=int, default=2)
     ap.add_argument("--host-plane-reps", type=int, default=8)
     ap.add_argument("--stages", default=None)
+    ap.add_argument("--profile-loop", default=None, choices=["default", "streamed"],
+                    help="ncu target: set-up, then ONLY the resident loop of that path (W warm-up + K timed steps), a short "
+                         "JSON line with the stage times, exit -- so that a launch list holds the kernels of one path only")
     a = ap.parse_args()
     cfg = CONFIGS[a.config]
     for k in ("atlas", "layers", "quads", "stages"):
@@ -597,6 +600,15 @@ def run_ours(args):
                     for j, st in enumerate(stages)}
         return total_ms, stage_ms, slots[args.warmup:].cpu().numpy()
 
+    if args.profile_loop:
+        t_ms, s_ms, _ = resident_loop(args.profile_loop == "default")
+        stop.set()
+        th.join()
+        if rank == 0:
+            print(json.dumps({"profile_loop": args.profile_loop, "steps": args.steps, "warmup": args.warmup,
+                              "ms_per_step": t_ms / args.steps, "stage_ms": {k: round(v, 4) for k, v in s_ms.items()},
+                              "launches_per_step": sum(arm.launches(args.profile_loop == "default")[s] for s in stages)}))
+        return
     # ---- value: the default path;  value_streamed: every stage streams the whole atlas
     total_ms, stage_ms, _ = resident_loop(primary_cull)
     if primary_cull:
