@@ -956,6 +956,7 @@ class StrokeBatch:
         self.K = 0
         self._cap = 0
         self._ev = None
+        self.ready = None
         if capacity:
             self._reserve(int(capacity))
 
@@ -967,14 +968,56 @@ class StrokeBatch:
         self._cap = cap
         nbytes = cap * self.RECORD_BYTES
         self._pin = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
-        self.packed = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        # TWO device copies, written alternately: an upload may run on a side stream while the kernels of the previous
+        # batch (which hold raw pointers into the other copy) are still queued or running
+        self._bufs = [torch.empty(nbytes, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        self._cur = 0
         host = self._pin.numpy()
         self._h_strokes = host[:32 * cap].view(np.float64).reshape(cap, 4)
         self._h_layer = host[32 * cap:36 * cap].view(np.int32)
         self._h_value = host[36 * cap:40 * cap].view(np.uint32)
+        self._bind(0)
+
+    def _bind(self, k):
+        torch = _torch()
+        cap = self._cap
+        self._cur = k
+        self.packed = self._bufs[k]
         self._d_strokes = self.packed[:32 * cap].view(torch.float64).view(cap, 4)
         self._d_layer = self.packed[32 * cap:36 * cap].view(torch.int32)
         self._d_value = self.packed[36 * cap:40 * cap].view(torch.int32)
+
+    def pack_host(self, strokes, layer_of, values, out):
+        """Write one batch in the packed record layout into `out`, a uint8 numpy array of capacity * RECORD_BYTES
+        bytes (callers that stage many batches at once, e.g. one table per step of a resident loop)."""
+        cap = self._cap
+        strokes = np.ascontiguousarray(strokes, dtype=np.float64)
+        K = strokes.shape[0]
+        dt = _np_dtype_of(self.data[0])
+        hs = out[:32 * cap].view(np.float64).reshape(cap, 4)
+        hl = out[32 * cap:36 * cap].view(np.int32)
+        hv = out[36 * cap:40 * cap].view(np.uint32)
+        hs[:K] = strokes
+        hs[K:] = np.nan
+        hl[:K] = np.asarray(layer_of, dtype=np.int32)
+        hl[K:] = 0
+        v = np.asarray(values).astype(dt).reshape(K)
+        hv[:K] = v.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[dt.itemsize])
+        hv[K:] = 0
+        return K
+
+    def bind(self, packed, K):
+        """Point the batch at a packed record buffer that is already on the device (uint8, capacity * RECORD_BYTES
+        bytes, 16-byte aligned): no copy."""
+        torch = _torch()
+        cap = self._cap
+        if packed.numel() != cap * self.RECORD_BYTES or packed.data_ptr() % 8:
+            raise TargetMismatch("packed stroke table does not match the batch's capacity")
+        self.packed = packed
+        self._d_strokes = packed[:32 * cap].view(torch.float64).view(cap, 4)
+        self._d_layer = packed[32 * cap:36 * cap].view(torch.int32)
+        self._d_value = packed[36 * cap:40 * cap].view(torch.int32)
+        return self.use(K)
 
     def use(self, K):
         """Strokes [0, K) of the packed buffer are the batch (after an upload or a broadcast)."""
@@ -1005,9 +1048,12 @@ class StrokeBatch:
             self._h_strokes[K:] = np.nan
             self._h_layer[K:] = 0
             self._h_value[K:] = 0
+        self._bind(self._cur ^ 1)                 # the copy the queued kernels are NOT reading
         self.packed.copy_(self._pin, non_blocking=True)
         self._ev = torch.cuda.Event()
-        self._ev.record()
+        self._ev.record()                         # on the current stream: callers that upload on a side stream make the
+        #                                           compute stream wait for `ready` before the batch kernel
+        self.ready = self._ev
         self.upload_bytes = (self._cap if fill else K) * self.RECORD_BYTES
         return self.use(self._cap if fill else K)
 
