@@ -145,7 +145,9 @@ class Workload:
         tool_xy = rng.uniform(0.3 * w, 0.7 * w, size=2)
         strokes, labels = synth.sphere_strokes(self.mesh, self.K + 1, seed=synth.SEED + 1000 + i,
                                                rmin_frac=0.01, rmax_frac=0.05)
-        return dict(tool_xy=tool_xy, sphere=strokes[0], sphere_value=int(labels[0]),
+        # the threshold selection re-labels its window with a different value every step (an identical selection
+        # repeated would leave nothing to write from the second step on)
+        return dict(tool_xy=tool_xy, sphere=strokes[0], sphere_value=int(labels[0]), thr_value=9 + (i % 7),
                     batch=strokes[1:], batch_layers=(np.arange(self.K) % self.L).astype(np.int32), batch_values=labels[1:])
 
     def algorithmic_bytes(self, n, stage, T, hits=0):
@@ -317,7 +319,7 @@ class CpuArm:
                 kn.layer_op("union", None, self.mask[0], None, self.mask[1 % wl.L], None, self.tmp_m, threads=th)
             elif st == "threshold":
                 res["threshold"] = kn.select_threshold(self.surf["pos"][2], None, wl.thr[0], wl.thr[1], self.data[2 % wl.L],
-                                                       self.mask[2 % wl.L], self.edited[2 % wl.L], 9, threads=th)
+                                                       self.mask[2 % wl.L], self.edited[2 % wl.L], inp["thr_value"], threads=th)
             elif st == "area":
                 res["area"] = kn.layers_area(self.surf["area"], self.mask, threads=th)
             t[st] = time.perf_counter() - t0
@@ -495,7 +497,7 @@ class GpuArm:
         elif st == "mask_op":
             nat.layer_op("union", None, layers[0].mask, None, layers[1 % L].mask, None, self.tmp_mask)
         elif st == "threshold":
-            ml.select_threshold(self.attr, None, wl.thr[0], wl.thr[1], layers[2 % L], 9, edited=edited[2 % L],
+            ml.select_threshold(self.attr, None, wl.thr[0], wl.thr[1], layers[2 % L], inp["thr_value"], edited=edited[2 % L],
                                 tiles=self.attr_tiles if cull else None, counts=row[a:b])
         elif st == "area":
             if self.peer_areas is not None:
