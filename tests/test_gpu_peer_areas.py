@@ -1,7 +1,8 @@
 """The fused cross-rank area reduction (sharding.PeerAreaReducer / ml_layer_area_peers): every rank's reduction kernel
 adds its partials with system-scope atomics straight into every rank's result row over IPC-mapped peer memory, one
-thread signals / awaits the arrival slots -- no collective call.  Exercised here with TWO processes that share
-cuda:0 (CUDA IPC works between processes on one device; the round's boxes have one GPU): global sums and counts
+thread signals / awaits the arrival slots -- no collective call.  Exercised here with TWO processes: one GPU each
+when the box has two (NVLink peer atomics), else sharing cuda:0 (CUDA IPC works between processes on one device; the
+round's boxes have one GPU): global sums and counts
 on both ranks == the whole-plane values, over more steps than the row ring holds (recycling), layer counts that
 need one and several launch groups."""
 import os
@@ -24,10 +25,12 @@ def _worker(rank, ws, port, L, steps, out_dir):
     import torch.distributed as dist
     from paper_2501_14807_b200 import _native as nat, sharding
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
+    # one GPU per rank when the box has them (real NVLink peer atomics), else both ranks share cuda:0 (IPC on one device)
+    index = rank if torch.cuda.device_count() >= ws else 0
+    torch.cuda.set_device(index)
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     try:
-        dev = torch.device("cuda", 0)
+        dev = torch.device("cuda", index)
         H, W = 512, 640                                       # whole plane; rank r owns rows shard_rows(H, ws, r)
         rng = np.random.default_rng(99)
         area = rng.random((H, W)).astype(np.float32)
