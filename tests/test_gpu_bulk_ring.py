@@ -140,6 +140,31 @@ def test_tea_stream_bulk_with_folded_reset(dkind, value):
     assert np.array_equal(ctx.edited.cpu().numpy(), edited)
 
 
+def test_tea_stream_bulk_with_the_bitmap_in_global_memory():
+    """More triangles than the shared-memory bitmap holds beside the ring (> ~1.07 M): the id stream looks the
+    classification bits up in global memory (the SMEM = false instantiation).  1,155,200-triangle heightfield on a
+    2048^2 atlas, whole-atlas TEA == oracle."""
+    import torch
+    mesh = synth.heightfield_mesh(760, margin=0.01)
+    assert mesh.num_triangles > 1_100_000
+    A, W = 2048, 256
+    cam = synth.default_camera(W, W, eye=(0.5, 0.5, 1.6), target=(0.5, 0.5, 0.0), fovy=40.0, near=0.2, far=5.0)
+    surf = ml.build_surface_map(mesh, A, A)
+    depth = ml.render_depth(mesh, cam)
+    ctx = ml.StrokeContext(mesh, cam, depth, surf)
+    layer = ml.create_layer("L", "uint8", A, A, pool=ml.TexturePool())
+    tool = ml.EditingTool(px=120.0, py=131.0, shape=synth.circle_shape(30), value=5)
+    res = ml.apply_stroke(ctx, tool, layer, cull=False)
+    sfx, sfy, bx, by = ml.compute_tool_projection(cam, tool).kernel_factors
+    data = np.zeros((A, A), np.uint8); mask = np.zeros((A, A), bool); edited = np.zeros((A, A), np.uint8)
+    want = kn.raster_tea_slab(mesh.tri_uv_texels(A, A), cam.clip_coords(mesh.vertices)[mesh.triangles], float(W), float(W),
+                              depth.plane.cpu().numpy(), 1e-4, sfx, sfy, bx, by, tool.shape, data, mask, edited, 5, A, 0,
+                              kn.max_threads())
+    assert (res.edited_count, res.fragments) == want and want[0] > 0
+    assert np.array_equal(layer.data.cpu().numpy(), data) and np.array_equal(layer.mask.cpu().numpy(), mask)
+    assert np.array_equal(ctx.edited.cpu().numpy(), edited)
+
+
 REGISTER_FORMS = {"ML_THR_REGISTER_STREAM": "1", "ML_THR_QUAD_STREAM": "1", "ML_AREA_REGISTER_STREAM": "1",
                   "ML_PAD_REGISTER_STREAM": "1", "ML_TEA_REGISTER_STREAM": "1"}
 
