@@ -416,20 +416,23 @@ class GpuArm:
         self.peer_areas, self.area_step = None, 0
         self.area_reduce_kind = "none (1 rank)" if world_size == 1 else "all-gather"
         if world_size > 1 and os.environ.get("ML_AREA_REDUCE", "peer") == "peer":
-            ok = torch.zeros(1, dtype=torch.int64)
+            # every rank walks the same sequence of collectives whatever fails locally: the constructor votes after
+            # mapping the peers (raising on ALL ranks or none), the trial reduction is bounded by its 10 s wait
+            passed = False
             try:
                 self.peer_areas = sharding.PeerAreaReducer(L, dev)
-                ok[0] = 1 if self.peer_areas.self_test() else 0
             except Exception as exc:                         # e.g. IPC not permitted in this container
                 sys.stderr.write("peer area reduction unavailable (%s); using the all-gather form\n" % exc)
-            import torch.distributed as dist
-            if dist.get_backend() == "nccl":
-                ok = ok.to(dev)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)         # all ranks or none
-            if int(ok.item()) == 1:
-                self.area_reduce_kind = "fused: system-scope atomics into every rank's row over peer memory"
-            else:
-                self.peer_areas = None
+            if self.peer_areas is not None:
+                try:
+                    passed = self.peer_areas.self_test()
+                except Exception as exc:
+                    sys.stderr.write("peer area self-test failed (%s); using the all-gather form\n" % exc)
+                if sharding.agree(passed, dev):               # all ranks or none
+                    self.area_reduce_kind = "fused: system-scope atomics into every rank's row over peer memory"
+                else:
+                    self.peer_areas.close()
+                    self.peer_areas = None
         self.T = wl.mesh.num_triangles
         self.seed()
         torch.cuda.synchronize()

@@ -119,6 +119,20 @@ class AreaReducer:
         return slots
 
 
+def agree(flag, device=None):
+    """True iff ``flag`` is true on EVERY rank (one all-reduce; ranks reach it whatever happened locally)."""
+    import torch
+    dist = _dist()
+    _, ws = world()
+    if ws == 1:
+        return bool(flag)
+    t = torch.tensor([1 if flag else 0], dtype=torch.int64)
+    if dist.get_backend() == "nccl":
+        t = t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return int(t.item()) == 1
+
+
 class PeerAreaReducer:
     """Fused compute + collective for the per-layer areas: no collective call at all.  Every rank owns a ring of
     result rows in an IPC-exported region; the area reduction kernel of every rank adds its per-block partials with
@@ -144,17 +158,27 @@ class PeerAreaReducer:
         self.region = _native.PeerRegion(self.NSLOTS * self.row_bytes)
         handles = [None] * self.ws
         dist.all_gather_object(handles, (self.region.handle, int(torch.cuda.current_device())))
-        for _, peer_dev in handles:
-            if not _native.lib().ml_peer_atomics_supported(int(peer_dev)):
-                raise RuntimeError("no native peer atomics between cuda:%d and cuda:%d" % (torch.cuda.current_device(), peer_dev))
-        self.peers = [self.region if r == self.rank else _native.PeerRegion.open(handles[r][0], self.region.nbytes)
-                      for r in range(self.ws)]
-        self.own = self.region.tensor(torch.int64, device).view(self.NSLOTS, 2 * self.L + 2)
-        # per slot: the addresses of every rank's arrival slot, as a device table
-        self.arrive = torch.tensor([[p.ptr + s * self.row_bytes + 2 * self.L * 8 for p in self.peers] for s in range(self.NSLOTS)],
-                                   dtype=torch.int64, device=device)
-        self.status = torch.zeros(1, dtype=torch.int32, device=device)
-        dist.barrier()                      # every region is mapped everywhere before anybody adds into one
+        # Mapping the peers can fail on ONE rank only (no peer atomics on some link, IPC not permitted); the ranks must
+        # leave this constructor together, so the local failure is kept until all of them have voted.
+        failure = None
+        self.peers = [self.region]
+        try:
+            for _, peer_dev in handles:
+                if not _native.lib().ml_peer_atomics_supported(int(peer_dev)):
+                    raise RuntimeError("no native peer atomics between cuda:%d and cuda:%d" % (torch.cuda.current_device(), peer_dev))
+            self.peers = [self.region if r == self.rank else _native.PeerRegion.open(handles[r][0], self.region.nbytes)
+                          for r in range(self.ws)]
+            self.own = self.region.tensor(torch.int64, device).view(self.NSLOTS, 2 * self.L + 2)
+            # per slot: the addresses of every rank's arrival slot, as a device table
+            self.arrive = torch.tensor([[p.ptr + s * self.row_bytes + 2 * self.L * 8 for p in self.peers] for s in range(self.NSLOTS)],
+                                       dtype=torch.int64, device=device)
+            self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        except Exception as exc:
+            failure = exc
+        # the vote is also the barrier: every region is mapped everywhere before anybody adds into one
+        if not agree(failure is None, device):
+            self.close()
+            raise RuntimeError("peer regions could not be mapped on every rank (%s)" % (failure or "another rank failed"))
 
     def self_test(self):
         """One trial reduction with known contributions (rank r adds r + 1 for each of 4096 texels into every layer):
@@ -195,6 +219,7 @@ class PeerAreaReducer:
         for p in self.peers:
             if p is not self.region:
                 p.close()
+        self.peers = [self.region]
         self.region.close()
 
 
