@@ -257,8 +257,8 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
             }
             // Pass 2 -- the data fold, restricted to the layers of `need`.  A layer outside `need` changes the
             // accumulator's data only by clearing texels it removes from the mask; that clearing is deferred: a needed
-            // union masks the accumulator with the mask it has at that point before it fills, and the result is masked
-            // with the FINAL mask once at the end -- the same bytes as folding every layer.
+            // union overwrites exactly the texels it fills (set in the operand, not held at that point), and the result
+            // is masked with the FINAL mask once at the end -- the same bytes as folding every layer.
             uint32_t cur[4] = {0u, 0u, 0u, 0u};             // the accumulator's mask (0 / 1 bytes) while folding
             uint32_t accd[4 * ESIZE];
 #pragma unroll
@@ -288,11 +288,15 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
                             }
                         } else if (op == ML_OP_UNION) {
                             if (needed) {
-                                const uint32_t keep_a = cur[g] * 0xffu, take_b = (bm & ~cur[g]) * 0xffu;
+                                // bit select: b's value where b fills (set in b, not held), the accumulator's elsewhere.
+                                // A texel the accumulator does not hold may keep a stale value here: it can only come
+                                // back through a later fill, which replaces it, or not at all (final mask clears it).
+                                const uint32_t take_b = (bm & ~cur[g]) * 0xffu;
 #pragma unroll
-                                for (int j = 0; j < ESIZE; ++j)
-                                    accd[g * ESIZE + j] = (accd[g * ESIZE + j] & expand<ESIZE>(keep_a, j)) |
-                                                          (((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(take_b, j));
+                                for (int j = 0; j < ESIZE; ++j) {
+                                    const uint32_t t = expand<ESIZE>(take_b, j);
+                                    accd[g * ESIZE + j] = (accd[g * ESIZE + j] & ~t) | (((const uint32_t*)&dk[0])[g * ESIZE + j] & t);
+                                }
                             }
                             cur[g] |= bm;
                         } else if (op == ML_OP_DIFFERENCE) cur[g] &= ~bm;
