@@ -259,6 +259,9 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
             // accumulator's data only by clearing texels it removes from the mask; that clearing is deferred: a needed
             // union overwrites exactly the texels it fills (set in the operand, not held at that point), and the result
             // is masked with the FINAL mask once at the end -- the same bytes as folding every layer.
+            // layers no lane of the warp needs are skipped by a warp-uniform branch (a per-lane predicate would still
+            // issue their instructions)
+            const unsigned wneed = __reduce_or_sync(__activemask(), need);
             uint32_t cur[4] = {0u, 0u, 0u, 0u};             // the accumulator's mask (0 / 1 bytes) while folding
             uint32_t accd[4 * ESIZE];
 #pragma unroll
@@ -268,6 +271,7 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
                 if (k < a.nlayers) {
                     const int op = a.ops[k];
                     const bool needed = (need >> k) & 1u;
+                    const bool wneeded = (wneed >> k) & 1u;
                     uint4 dk[ESIZE];
                     if (needed) {
                         if (ESIZE == 1) dk[0] = d1[k];
@@ -287,7 +291,7 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
                                     accd[g * ESIZE + j] = ((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(bm * 0xffu, j);
                             }
                         } else if (op == ML_OP_UNION) {
-                            if (needed) {
+                            if (wneeded && needed) {
                                 // bit select: b's value where b fills (set in b, not held), the accumulator's elsewhere.
                                 // A texel the accumulator does not hold may keep a stale value here: it can only come
                                 // back through a later fill, which replaces it, or not at all (final mask clears it).
