@@ -535,6 +535,82 @@ threshold_tiles_kernel(const float* __restrict__ attr, const uint8_t* __restrict
     block_count_add(cnt, counter);
 }
 
+// 16-texel form of the tile walk (default; the quad form above serves a valid plane that is only 4-byte aligned).
+// The attribute loads stay as they are -- row u of the tile, lane l = quad l: one coalesced 512-byte access per row --
+// but the byte planes are written by OWNER lanes: lane L owns the 16 texels [16 (L & 7), +16) of row L >> 3, so
+// edited / mask / data move as one 128-bit access per plane and lane (vec16_load / vec16_commit) instead of four
+// 32-bit ones.  The 4 x 4 hit bits of a lane travel to the owners with 4 shuffles.
+#ifndef ML_TTV_U
+#define ML_TTV_U 1          // tiles per warp step; measured at 16k^2 (C3 window): U = 1 at 4 blocks/SM 0.112 ms, U = 2 at 3 / 4 / 2 blocks 0.122 / 0.128 / 0.131
+#endif
+#ifndef ML_TTV_MINB
+#define ML_TTV_MINB 4
+#endif
+template <int ES, bool HV>
+__global__ void __launch_bounds__(BLOCK, ML_TTV_MINB)
+threshold_tiles_vec_kernel(const float* __restrict__ attr, const uint8_t* __restrict__ valid, TileGrid g, TileList list,
+                           Thr thr, void* __restrict__ data, uint32_t value, uint8_t* __restrict__ mask,
+                           uint8_t* __restrict__ edited, unsigned long long* counter) {
+    constexpr int U = ML_TTV_U;
+    long long cnt = 0;
+    const int lane = threadIdx.x & 31;
+    const int orow = lane >> 3, oseg = lane & 7;
+    const long long count = (long long)*list.count;
+    const long long nwarps = (long long)gridDim.x * (BLOCK / 32);
+    long long j = (long long)blockIdx.x * (BLOCK / 32) + (threadIdx.x >> 5);
+    long long tile[U];
+#pragma unroll
+    for (int t = 0; t < U; ++t) tile[t] = j + t * nwarps < count ? (long long)list.tiles[j + t * nwarps] : -1;
+    for (; j < count; j += U * nwarps) {
+        long long row_base[U], col[U];
+        float4 a[U][4];
+        uint4 vv[U];
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+            const long long ty = tile[t] / g.segs, tx = tile[t] - ty * g.segs;
+            row_base[t] = tile[t] >= 0 ? ty << ST_H_SHIFT : g.rows;          // no tile: every row is "below the slab"
+            col[t] = tx << ST_W_SHIFT;
+            const long long jn = j + (U + t) * nwarps;
+            tile[t] = jn < count ? (long long)list.tiles[jn] : -1;           // next step's tile: off the dependent-load chain
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (row_base[t] + u < g.rows)
+                    a[t][u] = ld_stream((const float4*)attr + ((((row_base[t] + u) * g.width + col[t]) >> 2) + lane));
+            vv[t] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+            if (HV && row_base[t] + orow < g.rows)
+                vv[t] = ld_stream((const uint4*)(valid + (row_base[t] + orow) * g.width + col[t] + 16 * oseg));
+        }
+        unsigned hit16[U];
+        uint4 ew[U], mw[U], dw[U];
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+            unsigned packed = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (row_base[t] + u >= g.rows) continue;
+                const float v[4] = {a[t][u].x, a[t][u].y, a[t][u].z, a[t][u].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (AttrT<ML_FLOAT32>::hit(v[e], thr)) packed |= 1u << (4 * u + e);
+            }
+            hit16[t] = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const unsigned v = __shfl_sync(0xffffffffu, packed, 4 * oseg + k);
+                hit16[t] |= ((v >> (4 * orow)) & 0xfu) << (4 * k);
+            }
+            if (HV) hit16[t] &= nz_bits4(vv[t].x) | (nz_bits4(vv[t].y) << 4) | (nz_bits4(vv[t].z) << 8) | (nz_bits4(vv[t].w) << 12);
+            if (row_base[t] + orow >= g.rows) hit16[t] = 0;
+            vec16_load<ES>(data, mask, edited, (row_base[t] + orow) * g.width + col[t] + 16 * oseg, hit16[t], ew[t], mw[t], dw[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < U; ++t)
+            vec16_commit<ES>(data, value, mask, edited, (row_base[t] + orow) * g.width + col[t] + 16 * oseg, hit16[t],
+                             ew[t], mw[t], dw[t], cnt);
+    }
+    block_count_add(cnt, counter);
+}
+
 // 16-texel form (default when attribute, valid and layer planes are 16-byte aligned).  A warp owns
 // 512 consecutive texels per step.  The ATTRIBUTE bytes are fetched lane-interleaved -- load k of
 // lane l is the 16-byte chunk k*32 + l of the warp's 512*S attribute bytes, so every load
@@ -1032,7 +1108,17 @@ int ml_select_threshold_tiles(const float* attr, const uint8_t* valid, int64_t w
                                                                                        thr.lo_f, thr.hi_f, list);
     const unsigned grid = (unsigned)(ml_sm_count() * 16);
     unsigned long long* c = (unsigned long long*)count;
-    if (esize == 1) threshold_tiles_kernel<1><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c);
+    static const bool quad_form = getenv("ML_THR_QUAD_STREAM") != nullptr;              // the round-1 tile walk, kept for comparison
+    if (!quad_form && (!valid || aligned(valid, 16))) {
+#define ML_LAUNCH_TTV(ES) do { \
+        if (valid) threshold_tiles_vec_kernel<ES, true><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c); \
+        else threshold_tiles_vec_kernel<ES, false><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c); } while (0)
+        if (esize == 1) ML_LAUNCH_TTV(1);
+        else if (esize == 2) ML_LAUNCH_TTV(2);
+        else ML_LAUNCH_TTV(4);
+#undef ML_LAUNCH_TTV
+    }
+    else if (esize == 1) threshold_tiles_kernel<1><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c);
     else if (esize == 2) threshold_tiles_kernel<2><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c);
     else threshold_tiles_kernel<4><<<grid, BLOCK, 0, st>>>(attr, valid, g, list, thr, data, value_bits, mask, edited, c);
     ML_CUDA(cudaGetLastError());
