@@ -68,6 +68,11 @@ def _worker(rank, world_size, port, out_dir):
         assert np.array_equal(got[0], np.arange(44, dtype=np.float64).reshape(11, 4))
         assert got[1].tolist() == list(range(11)) and got[2].tolist() == [k + 7 for k in range(11)]
 
+        # ---- the set-up vote: true only if every rank says so (a local failure takes all ranks to the fallback)
+        assert sharding.agree(True) is True
+        assert sharding.agree(rank != 1) is False
+        assert sharding.agree(False) is False
+
         # ---- halo exchange of a byte plane for a radius-2 stencil
         cov = torch.from_numpy((surf["tri_id"] >= 0).astype(np.uint8))
         ext, ext_row0 = sharding.exchange_halo(cov, r0, A, 2)

@@ -19,7 +19,7 @@ STAGE_OF = (("chain_lazy_kernel", ("chain",)), ("chain_kernel", ("chain_stream",
             ("sphere_batch_tiles_kernel", ("batch",)), ("sphere_batch_kernel", ("batch_stream",)),
             ("sphere_tiles_kernel", ("sphere",)), ("sphere_kernel", ("sphere_stream",)),
             ("tile_classify_kernel", ("sphere", "batch")),
-            ("threshold_tiles_kernel", ("threshold",)), ("range_classify_kernel", ("threshold",)),
+            ("threshold_tiles_kernel", ("threshold",)), ("threshold_tiles_vec_kernel", ("threshold",)), ("range_classify_kernel", ("threshold",)),
             ("threshold_bulk_kernel", ("threshold_stream",)), ("threshold_vec_kernel", ("threshold_stream",)),
             ("threshold_kernel", ("threshold_stream",)),
             ("area_bulk_kernel", ("area",)), ("area_kernel", ("area",)),
