@@ -170,21 +170,20 @@ chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
 #ifndef ML_CHAIN_LAZY_MINB
 #define ML_CHAIN_LAZY_MINB 2
 #endif
+
 template <int ESIZE>
 __global__ void __launch_bounds__(BLOCK, ML_CHAIN_LAZY_MINB)
 chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
     constexpr int GL = 8;
     const long long tid = (long long)blockIdx.x * BLOCK + threadIdx.x;
     const long long nthreads = (long long)gridDim.x * BLOCK;
-    uint4 mn[GL];
+    // ma: the vector being folded; mb: the next vector's masks, requested before the current vector's data
+    uint4 ma[GL], mb[GL];
     if (tid < nv) {
 #pragma unroll
-        for (int k = 0; k < GL; ++k) if (k < a.nlayers) mn[k] = ld_stream_rw((const uint4*)a.mask[k] + tid);
+        for (int k = 0; k < GL; ++k) if (k < a.nlayers) ma[k] = ld_stream_rw((const uint4*)a.mask[k] + tid);
     }
-    for (long long v = tid; v < nv; v += nthreads) {
-        uint4 m[GL];
-#pragma unroll
-        for (int k = 0; k < GL; ++k) m[k] = mn[k];
+    auto step = [&](const long long v, uint4 (&m)[GL], uint4 (&mn)[GL]) {
         if (v + nthreads < nv) {
 #pragma unroll
             for (int k = 0; k < GL; ++k) if (k < a.nlayers) mn[k] = ld_stream_rw((const uint4*)a.mask[k] + v + nthreads);
@@ -249,11 +248,13 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
         } else {
             // one-byte layers: all needed vectors are requested together; wider layers (64 bytes per
             // layer and vector) are fetched one layer at a time inside the fold to bound the registers
-            uint4 d1[ESIZE == 1 ? GL : 1];
+            uint4 d1[ESIZE == 1 ? GL : 1];                  // d1[k] is defined (and read) only where bit k of `need` is set
             if (ESIZE == 1) {
+                long long off = v << 4;                     // one byte offset for all planes (opaque: no per-plane re-derivation)
+                asm volatile("" : "+l"(off));
 #pragma unroll
                 for (int k = 0; k < GL; ++k)
-                    d1[k] = ((need >> k) & 1u) ? ld_stream_rw((const uint4*)a.data[k] + v) : make_uint4(0u, 0u, 0u, 0u);
+                    if ((need >> k) & 1u) d1[k] = ld_stream_rw((const uint4*)((const uint8_t*)a.data[k] + off));
             }
             // Pass 2 -- the data fold, restricted to the layers of `need`.  A layer outside `need` changes the
             // accumulator's data only by clearing texels it removes from the mask; that clearing is deferred: a needed
@@ -273,12 +274,10 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
                     const bool needed = (need >> k) & 1u;
                     const bool wneeded = (wneed >> k) & 1u;
                     uint4 dk[ESIZE];
-                    if (needed) {
-                        if (ESIZE == 1) dk[0] = d1[k];
-                        else {
+                    if (ESIZE == 1) dk[0] = d1[k];         // plain alias: read only under `needed`, where it is defined
+                    else if (needed) {
 #pragma unroll
-                            for (int j = 0; j < ESIZE; ++j) dk[j] = ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j);
-                        }
+                        for (int j = 0; j < ESIZE; ++j) dk[j] = ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j);
                     }
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
@@ -316,6 +315,11 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
         st_stream((uint4*)mc + v, om);
 #pragma unroll
         for (int j = 0; j < ESIZE; ++j) st_stream((uint4*)dc + v * ESIZE + j, od[j]);
+    };
+    for (long long v = tid; v < nv; v += nthreads) {
+        step(v, ma, mb);
+#pragma unroll
+        for (int k = 0; k < GL; ++k) ma[k] = mb[k];     // (unrolling by two with the buffers swapped spills: 0.54 -> 0.72 ms)
     }
 }
 
