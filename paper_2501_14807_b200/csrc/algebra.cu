@@ -256,54 +256,53 @@ chain_lazy_kernel(ChainArgs a, void* dc, uint8_t* mc, long long nv) {
                 for (int k = 0; k < GL; ++k)
                     if ((need >> k) & 1u) d1[k] = ld_stream_rw((const uint4*)((const uint8_t*)a.data[k] + off));
             }
-            // Pass 2 -- the data fold, restricted to the layers of `need`.  A layer outside `need` changes the
-            // accumulator's data only by clearing texels it removes from the mask; that clearing is deferred: a needed
-            // union overwrites exactly the texels it fills (set in the operand, not held at that point), and the result
-            // is masked with the FINAL mask once at the end -- the same bytes as folding every layer.
-            // layers no lane of the warp needs are skipped by a warp-uniform branch (a per-lane predicate would still
-            // issue their instructions)
-            const unsigned wneed = __reduce_or_sync(__activemask(), need);
+            // Pass 2a -- masks only, so it runs while the data vectors requested above are in flight: a one-hot SOURCE
+            // byte per texel, bit k set where union operand k (or the first operand, bit 0) supplied a value, i.e. filled
+            // a texel the accumulator did not hold at that point.  Bits are only ever added: a texel that is removed and
+            // filled again later carries two bits and the gather below lets the later layer win; a removed texel that
+            // never comes back is cleared by the final mask.
             uint32_t cur[4] = {0u, 0u, 0u, 0u};             // the accumulator's mask (0 / 1 bytes) while folding
+            uint32_t src[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int k = 0; k < GL; ++k) {
+                if (k < a.nlayers) {
+                    const int op = a.ops[k];
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const uint32_t bm = ((const uint32_t*)&m[k])[g];
+                        if (k == 0) { cur[g] = bm; src[g] = bm; }
+                        else if (op == ML_OP_UNION) { src[g] += (bm & ~cur[g]) << k; cur[g] |= bm; }    // bit k is new: + is |
+                        else if (op == ML_OP_DIFFERENCE) cur[g] &= ~bm;
+                        else cur[g] &= bm;
+                    }
+                }
+            }
+            // Pass 2b -- the gather, in layer order (a later source overwrites an earlier one), restricted to the layers
+            // some lane of the warp needs (warp-uniform branch: a per-lane predicate would still issue the instructions)
+            const unsigned wneed = __reduce_or_sync(__activemask(), need);
             uint32_t accd[4 * ESIZE];
 #pragma unroll
             for (int i = 0; i < 4 * ESIZE; ++i) accd[i] = 0u;
 #pragma unroll
             for (int k = 0; k < GL; ++k) {
-                if (k < a.nlayers) {
-                    const int op = a.ops[k];
+                if (k < a.nlayers && ((wneed >> k) & 1u)) {
                     const bool needed = (need >> k) & 1u;
-                    const bool wneeded = (wneed >> k) & 1u;
                     uint4 dk[ESIZE];
                     if (ESIZE == 1) dk[0] = d1[k];         // plain alias: read only under `needed`, where it is defined
                     else if (needed) {
 #pragma unroll
                         for (int j = 0; j < ESIZE; ++j) dk[j] = ld_stream_rw((const uint4*)a.data[k] + v * ESIZE + j);
                     }
+                    if (needed) {
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        const uint32_t bm = ((const uint32_t*)&m[k])[g];
-                        if (k == 0) {
-                            cur[g] = bm;
-                            if (needed) {
+                        for (int g = 0; g < 4; ++g) {
+                            const uint32_t take = ((src[g] >> k) & 0x01010101u) * 0xffu;
 #pragma unroll
-                                for (int j = 0; j < ESIZE; ++j)
-                                    accd[g * ESIZE + j] = ((const uint32_t*)&dk[0])[g * ESIZE + j] & expand<ESIZE>(bm * 0xffu, j);
+                            for (int j = 0; j < ESIZE; ++j) {
+                                const uint32_t t = expand<ESIZE>(take, j);
+                                accd[g * ESIZE + j] = (accd[g * ESIZE + j] & ~t) | (((const uint32_t*)&dk[0])[g * ESIZE + j] & t);
                             }
-                        } else if (op == ML_OP_UNION) {
-                            if (wneeded && needed) {
-                                // bit select: b's value where b fills (set in b, not held), the accumulator's elsewhere.
-                                // A texel the accumulator does not hold may keep a stale value here: it can only come
-                                // back through a later fill, which replaces it, or not at all (final mask clears it).
-                                const uint32_t take_b = (bm & ~cur[g]) * 0xffu;
-#pragma unroll
-                                for (int j = 0; j < ESIZE; ++j) {
-                                    const uint32_t t = expand<ESIZE>(take_b, j);
-                                    accd[g * ESIZE + j] = (accd[g * ESIZE + j] & ~t) | (((const uint32_t*)&dk[0])[g * ESIZE + j] & t);
-                                }
-                            }
-                            cur[g] |= bm;
-                        } else if (op == ML_OP_DIFFERENCE) cur[g] &= ~bm;
-                        else cur[g] &= bm;
+                        }
                     }
                 }
             }
