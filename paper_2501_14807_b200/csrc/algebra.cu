@@ -166,7 +166,10 @@ chain_kernel(ChainArgs a, void* dc, uint8_t* mc, long long n) {
 // them and only their data vectors are fetched -- thematic layers are sparse, so most data vectors
 // are never read (8 masks + 2 output bytes per texel instead of 18).  The mask -> data dependency is
 // hidden by software pipelining: the masks of the thread's NEXT vector are requested before the data
-// of the current one, so as many bytes are in flight as in the eager kernel.
+// of the current one, so as many bytes are in flight as in the eager kernel.  Per vector: (1) dry run of the mask
+// fold -> final mask + the set of layers that matter; (2) their data vectors are requested; (3) while they are in
+// flight a second masks-only pass records, per texel, WHICH operand supplied its value (one-hot source byte);
+// (4) the data vectors are gathered by source; (5) the final mask clears what was removed.
 #ifndef ML_CHAIN_LAZY_MINB
 #define ML_CHAIN_LAZY_MINB 2
 #endif
